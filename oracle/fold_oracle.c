@@ -1,0 +1,450 @@
+/*
+ * oracle/fold_oracle.c — fp64 CPU ORACLE for dynamic batching (arXiv 1702.02181).
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library. The product path
+ * (paper_1702_02181_b200/, include/fold.h, libfold.so) never links, includes or
+ * calls anything here, and this file includes nothing from the product.
+ *
+ * What it computes, each function citing the passage it follows:
+ *   oracle_schedule      — the dynamic-batching schedule by its definition
+ *                          (§2 bullets 1-5), executor form
+ *                          (global append-only pool, no pass-throughs; the
+ *                          paper form with pass-throughs is oracle/paper_form.py).
+ *   oracle_forward       — every node evaluated individually, one at a time, in a
+ *                          topological order (batching reaches the
+ *                          unbatched result; L86 "no measurable penalty ...").
+ *   oracle_forward_levels— the same values computed level by level from this
+ *                          oracle's own schedule (PAPER.md L47 loop model); used
+ *                          only to pin "batched == unbatched" bitwise.
+ *   oracle_backward      — hand-derived reverse mode ("gradients ...
+ *                          do not require any additional code" in TF; here written
+ *                          out), pinned by finite differences in tests/.
+ * All floating point is fp64; parameters arrive as fp64 copies of the fp32 masters.
+ *
+ * Cell equations (Tai et al. eqs 9-14 with x = 0, N = 2, cited
+ * at PAPER.md L301-304; TreeRNN form read from Fig. 1 "RNN Cell"):
+ *   TreeRNN  (gates=1): z = W [h_L; h_R] + b,   h = tanh(z),  c = 0
+ *   TreeLSTM (gates=5, row blocks i, fL, fR, o, u of U[5S][2S]):
+ *     z = U [h_L; h_R] + b
+ *     i = s(z_i), fL = s(z_fL), fR = s(z_fR), o = s(z_o), u = tanh(z_u)
+ *     c = i*u + fL*c_L + fR*c_R,   h = o*tanh(c)
+ *   EMBED: h = E[token], c = 0        (leaf; its token is the depth-0 constant)
+ *   s(x) = 1 / (1 + exp(-x))
+ *
+ * Status codes are this file's own (the product's fold.h defines its own; tests
+ * compare by name).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum { OR_OK = 0, OR_E_INVALID = 1, OR_E_CHILD_RANGE = 2, OR_E_ARITY = 3,
+       OR_E_TOKEN_RANGE = 4, OR_E_ROOT_RANGE = 5, OR_E_CYCLE = 6, OR_E_OP_RANGE = 10 };
+enum { OR_EMBED = 0, OR_CELL = 1, OR_N_OPS = 2 };
+enum { OR_TREERNN = 0, OR_TREELSTM = 1 };
+
+/* ---------------------------------------------------------------- validation */
+/* Error classes checked in this order; the smallest offending node id (graph id
+ * for ROOT_RANGE) of the first failing class is reported. */
+static int validate(int N, int G, int V, const int32_t *op, const int32_t *child,
+                    const int32_t *token, const int32_t *root, int32_t *err)
+{
+    for (int n = 0; n < N; n++)
+        for (int k = 0; k < 2; k++)
+            if (child[2 * n + k] < -1 || child[2 * n + k] >= N) { *err = n; return OR_E_CHILD_RANGE; }
+    for (int n = 0; n < N; n++)
+        if (op[n] != OR_EMBED && op[n] != OR_CELL) { *err = n; return OR_E_OP_RANGE; }
+    for (int n = 0; n < N; n++) {
+        int nch = (child[2 * n] >= 0) + (child[2 * n + 1] >= 0);
+        int ok = (op[n] == OR_EMBED) ? (child[2 * n] == -1 && child[2 * n + 1] == -1)
+                                     : (nch == 2);
+        if (!ok) { *err = n; return OR_E_ARITY; }
+    }
+    for (int n = 0; n < N; n++)
+        if (op[n] == OR_EMBED && (token[n] < 0 || token[n] >= V)) { *err = n; return OR_E_TOKEN_RANGE; }
+    for (int g = 0; g < G; g++)
+        if (root[g] < 0 || root[g] >= N) { *err = g; return OR_E_ROOT_RANGE; }
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------- depth
+ * "Nodes with no dependencies (constants) are assigned depth zero. Nodes with only
+ * dependencies of depth zero are assigned depth one, nodes whose dependencies have
+ * a maximum depth of one get assigned depth two, etc."
+ * EMBED's only dependency is its token constant (depth 0) => depth 1.
+ * CELL => 1 + max(depth(L), depth(R)).
+ * Memoised DFS with an explicit stack and white/grey/black colouring. A node that
+ * reaches a cycle (grey child) or a bad child is "bad"; the cycle error reports the
+ * smallest bad id. Also emits a post-order (children before parents) in `topo`. */
+static int assign_depths(int N, const int32_t *op, const int32_t *child,
+                         int32_t *depth, int32_t *topo, int32_t *err)
+{
+    enum { WHITE = 0, GREY = 1, OK = 2, BAD = 3 };
+    unsigned char *col = (unsigned char *)calloc((size_t)N + 1, 1);
+    int32_t *stk = (int32_t *)malloc(sizeof(int32_t) * ((size_t)N + 1));
+    int32_t *nxt = (int32_t *)malloc(sizeof(int32_t) * ((size_t)N + 1)); /* next child slot */
+    int ntopo = 0, any_bad = 0;
+    for (int s = 0; s < N; s++) {
+        if (col[s] != WHITE) continue;
+        int sp = 0;
+        stk[sp++] = s; col[s] = GREY; nxt[s] = 0;
+        while (sp > 0) {
+            int n = stk[sp - 1];
+            int nc = (op[n] == OR_CELL) ? 2 : 0;
+            if (nxt[n] < nc) {
+                int c = child[2 * n + nxt[n]];
+                nxt[n]++;
+                if (col[c] == WHITE) { col[c] = GREY; nxt[c] = 0; stk[sp++] = c; }
+                /* grey child = back edge (cycle); handled when n finishes */
+                continue;
+            }
+            /* all children visited: finish n */
+            int bad = 0, dmax = 0;
+            for (int k = 0; k < nc; k++) {
+                int c = child[2 * n + k];
+                if (col[c] == GREY || col[c] == BAD) bad = 1;
+                else if (depth[c] > dmax) dmax = depth[c];
+            }
+            if (bad) { col[n] = BAD; depth[n] = -1; any_bad = 1; }
+            else { col[n] = OK; depth[n] = (op[n] == OR_EMBED) ? 1 : 1 + dmax; topo[ntopo++] = n; }
+            sp--;
+        }
+    }
+    int st = OR_OK;
+    if (any_bad) {
+        for (int n = 0; n < N; n++) if (col[n] == BAD) { *err = n; break; }
+        st = OR_E_CYCLE;
+    }
+    free(col); free(stk); free(nxt);
+    return st;
+}
+
+/* ---------------------------------------------------------------- schedule
+ * Executor form:
+ *  perm: for d = 1..D, for op in enumeration order (EMBED=0, CELL=1; PAPER.md L43
+ *        "The order of concatenation corresponds to the order in which the dynamic
+ *        batching operations were enumerated"), for n ascending with (depth, op) =
+ *        (d, op): append n  ("Batch together all nodes invoking the same
+ *        operation at the same depth"). Filled with bucket lists in one id-ordered pass.
+ *  rank = perm^-1 (the pool row of each node).
+ *  level_off[d] = #rows with depth < d, d = 0..D+1.
+ *  group_off[k] = #rows with key < k, key = 2*depth + op, k = 0..2(D+1).
+ *  gather[r][k] = rank[child[perm[r]][k]] for CELL rows, -1 otherwise (PAPER.md L44:
+ *        the label i of an edge; here the global pool row; the paper's per-depth
+ *        index is gather - level_off[depth(child)]).
+ *  cons_off/cons_edge: for every child row (ascending), its consumer edges e = 2c + k
+ *        in ascending e, where c = r - n_leaves is the cell index of consumer row r
+ *        (all EMBED rows precede all CELL rows: EMBED depth = 1 < CELL depth).
+ *  leaf_perm: EMBED rows sorted by (token, row); tok_seg: segment starts + end.
+ *  root_row[g] = rank[root[g]]; root_perm: graph ids sorted by (root_row, g).
+ * info[0..4] = n_levels (D), n_leaves, n_cells, n_tok_segs, err_node.
+ */
+int oracle_schedule(int N, int G, int V, const int32_t *op, const int32_t *child,
+                    const int32_t *token, const int32_t *root,
+                    int32_t *depth, int32_t *perm, int32_t *rank, int32_t *gather,
+                    int32_t *level_off, int32_t *group_off, int32_t *cons_off,
+                    int32_t *cons_edge, int32_t *leaf_perm, int32_t *tok_seg,
+                    int32_t *root_row, int32_t *root_perm, int32_t *info)
+{
+    int32_t err = -1;
+    info[0] = info[1] = info[2] = info[3] = 0; info[4] = -1;
+    if (N < 0 || G < 0 || V < 0) return OR_E_INVALID;
+    int st = validate(N, G, V, op, child, token, root, &err);
+    if (st != OR_OK) { info[4] = err; return st; }
+    int32_t *topo = (int32_t *)malloc(sizeof(int32_t) * ((size_t)N + 1));
+    st = assign_depths(N, op, child, depth, topo, &err);
+    free(topo);
+    if (st != OR_OK) { info[4] = err; return st; }
+
+    int D = 0;
+    for (int n = 0; n < N; n++) if (depth[n] > D) D = depth[n];
+    int nkeys = 2 * (D + 1);
+    /* bucket lists: count, then append in ascending id */
+    int32_t *cnt = (int32_t *)calloc((size_t)nkeys + 1, sizeof(int32_t));
+    for (int n = 0; n < N; n++) cnt[2 * depth[n] + op[n]]++;
+    group_off[0] = 0;
+    for (int k = 0; k < nkeys; k++) group_off[k + 1] = group_off[k] + cnt[k];
+    int32_t *fill = (int32_t *)malloc(sizeof(int32_t) * ((size_t)nkeys + 1));
+    for (int k = 0; k <= nkeys; k++) fill[k] = group_off[k];
+    for (int n = 0; n < N; n++) perm[fill[2 * depth[n] + op[n]]++] = n;
+    for (int r = 0; r < N; r++) rank[perm[r]] = r;
+    for (int d = 0; d <= D + 1; d++) level_off[d] = group_off[2 * d];
+    int n_leaves = 0;
+    for (int n = 0; n < N; n++) n_leaves += (op[n] == OR_EMBED);
+    int n_cells = N - n_leaves;
+
+    for (int r = 0; r < N; r++) {
+        int n = perm[r];
+        for (int k = 0; k < 2; k++)
+            gather[2 * r + k] = (op[n] == OR_CELL) ? rank[child[2 * n + k]] : -1;
+    }
+    /* consumer CSR */
+    for (int r = 0; r <= N; r++) cons_off[r] = 0;
+    for (int c = 0; c < n_cells; c++)
+        for (int k = 0; k < 2; k++) cons_off[gather[2 * (n_leaves + c) + k] + 1]++;
+    for (int r = 0; r < N; r++) cons_off[r + 1] += cons_off[r];
+    int32_t *pos = (int32_t *)malloc(sizeof(int32_t) * ((size_t)N + 1));
+    for (int r = 0; r < N; r++) pos[r] = cons_off[r];
+    for (int e = 0; e < 2 * n_cells; e++) {   /* ascending e => ascending within a row */
+        int r = gather[2 * n_leaves + e];
+        cons_edge[pos[r]++] = e;
+    }
+    free(pos);
+    /* leaves by (token, row): insertion into token buckets in ascending row order */
+    int32_t *tcnt = (int32_t *)calloc((size_t)V + 1, sizeof(int32_t));
+    for (int r = 0; r < n_leaves; r++) tcnt[token[perm[r]] + 1]++;
+    for (int t = 0; t < V; t++) tcnt[t + 1] += tcnt[t];
+    int nseg = 0;
+    for (int t = 0; t < V; t++) if (tcnt[t + 1] > tcnt[t]) tok_seg[nseg++] = tcnt[t];
+    tok_seg[nseg] = n_leaves;
+    for (int r = 0; r < n_leaves; r++) leaf_perm[tcnt[token[perm[r]]]++] = r;
+    free(tcnt);
+    for (int g = 0; g < G; g++) root_row[g] = rank[root[g]];
+    /* roots by (root_row, g): stable insertion sort (G is small in tests) */
+    for (int g = 0; g < G; g++) {
+        int j = g;
+        while (j > 0 && root_row[root_perm[j - 1]] > root_row[g]) { root_perm[j] = root_perm[j - 1]; j--; }
+        root_perm[j] = g;
+    }
+    free(cnt); free(fill);
+    info[0] = D; info[1] = n_leaves; info[2] = n_cells; info[3] = nseg; info[4] = -1;
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------- cell math */
+static double sigm(double x) { return 1.0 / (1.0 + exp(-x)); }
+
+/* z[j] = b[j] + sum_{k<S} U[j][k] hL[k] + sum_{k<S} U[j][S+k] hR[k], k ascending */
+static void cell_z(int rows, int S, const double *U, const double *b,
+                   const double *hL, const double *hR, double *z)
+{
+    for (int j = 0; j < rows; j++) {
+        const double *u = U + (size_t)j * 2 * S;
+        double acc = b[j];
+        for (int k = 0; k < S; k++) acc += u[k] * hL[k];
+        for (int k = 0; k < S; k++) acc += u[S + k] * hR[k];
+        z[j] = acc;
+    }
+}
+
+/* one node, given its children's (h, c); writes h, c and (optionally) the gate
+ * activations act[gates*S] = (i, fL, fR, o, u) or (h) for TreeRNN */
+static void cell_forward(int cell, int S, const double *U, const double *b,
+                         const double *hL, const double *cL, const double *hR, const double *cR,
+                         double *h, double *c, double *z, double *act)
+{
+    int gates = (cell == OR_TREELSTM) ? 5 : 1;
+    cell_z(gates * S, S, U, b, hL, hR, z);
+    if (cell == OR_TREERNN) {
+        for (int j = 0; j < S; j++) { h[j] = tanh(z[j]); c[j] = 0.0; if (act) act[j] = h[j]; }
+        return;
+    }
+    for (int j = 0; j < S; j++) {
+        double i = sigm(z[j]), fl = sigm(z[S + j]), fr = sigm(z[2 * S + j]);
+        double o = sigm(z[3 * S + j]), u = tanh(z[4 * S + j]);
+        double cc = i * u + fl * cL[j] + fr * cR[j];
+        c[j] = cc;
+        h[j] = o * tanh(cc);
+        if (act) { act[j] = i; act[S + j] = fl; act[2 * S + j] = fr; act[3 * S + j] = o; act[4 * S + j] = u; }
+    }
+}
+
+/* post-order of all nodes (children first), assuming a validated acyclic input */
+static int topo_order(int N, const int32_t *op, const int32_t *child, int32_t *topo)
+{
+    int32_t *depth = (int32_t *)malloc(sizeof(int32_t) * ((size_t)N + 1));
+    int32_t err;
+    int st = assign_depths(N, op, child, depth, topo, &err);
+    free(depth);
+    return st;
+}
+
+/* ---------------------------------------------------------------- forward
+ * Evaluates every node individually in a topological order (each node exactly once,
+ * a DAG node shared by several consumers is evaluated once). Outputs root h/c
+ * [G][S]; optionally all node states H_all/C_all [N][S] (node-id order).
+ */
+int oracle_forward(int cell, int S, int N, int G, int V,
+                   const int32_t *op, const int32_t *child, const int32_t *token, const int32_t *root,
+                   const double *U, const double *b, const double *E,
+                   double *h_root, double *c_root, double *H_all, double *C_all)
+{
+    if (S <= 0 || (cell != OR_TREERNN && cell != OR_TREELSTM)) return OR_E_INVALID;
+    int32_t err;
+    int st = validate(N, G, V, op, child, token, root, &err);
+    if (st) return st;
+    int gates = (cell == OR_TREELSTM) ? 5 : 1;
+    double *H = H_all ? H_all : (double *)malloc(sizeof(double) * (size_t)N * S + 8);
+    double *C = C_all ? C_all : (double *)malloc(sizeof(double) * (size_t)N * S + 8);
+    double *z = (double *)malloc(sizeof(double) * (size_t)gates * S);
+    int32_t *topo = (int32_t *)malloc(sizeof(int32_t) * ((size_t)N + 1));
+    st = topo_order(N, op, child, topo);
+    if (st == OR_OK) {
+        for (int t = 0; t < N; t++) {
+            int n = topo[t];
+            double *h = H + (size_t)n * S, *c = C + (size_t)n * S;
+            if (op[n] == OR_EMBED) {
+                for (int j = 0; j < S; j++) { h[j] = E[(size_t)token[n] * S + j]; c[j] = 0.0; }
+            } else {
+                int L = child[2 * n], R = child[2 * n + 1];
+                cell_forward(cell, S, U, b, H + (size_t)L * S, C + (size_t)L * S,
+                             H + (size_t)R * S, C + (size_t)R * S, h, c, z, NULL);
+            }
+        }
+        for (int g = 0; g < G; g++)
+            for (int j = 0; j < S; j++) {
+                if (h_root) h_root[(size_t)g * S + j] = H[(size_t)root[g] * S + j];
+                if (c_root) c_root[(size_t)g * S + j] = C[(size_t)root[g] * S + j];
+            }
+    }
+    free(z); free(topo);
+    if (!H_all) free(H);
+    if (!C_all) free(C);
+    return st;
+}
+
+/* Level-ordered evaluation driven by this oracle's own schedule (each
+ * loop iteration evaluates all operations at one depth, gathering from earlier
+ * results). Row r of the pool holds node perm[r]. Outputs in node-id order. */
+int oracle_forward_levels(int cell, int S, int N, int G, int V,
+                          const int32_t *op, const int32_t *child, const int32_t *token,
+                          const int32_t *root, const double *U, const double *b, const double *E,
+                          double *H_out, double *C_out)
+{
+    int32_t *depth = malloc(sizeof(int32_t) * (N + 1)), *perm = malloc(sizeof(int32_t) * (N + 1));
+    int32_t *rank = malloc(sizeof(int32_t) * (N + 1)), *gat = malloc(sizeof(int32_t) * (2 * N + 2));
+    int32_t *lo = malloc(sizeof(int32_t) * (N + 3)), *go = malloc(sizeof(int32_t) * (2 * N + 5));
+    int32_t *co = malloc(sizeof(int32_t) * (N + 2)), *ce = malloc(sizeof(int32_t) * (2 * N + 2));
+    int32_t *lp = malloc(sizeof(int32_t) * (N + 1)), *ts = malloc(sizeof(int32_t) * (N + 2));
+    int32_t *rr = malloc(sizeof(int32_t) * (G + 1)), *rp = malloc(sizeof(int32_t) * (G + 1));
+    int32_t info[5];
+    int gates = (cell == OR_TREELSTM) ? 5 : 1;
+    int st = oracle_schedule(N, G, V, op, child, token, root, depth, perm, rank, gat, lo, go,
+                             co, ce, lp, ts, rr, rp, info);
+    if (st == OR_OK) {
+        int D = info[0];
+        double *Hp = malloc(sizeof(double) * (size_t)N * S + 8), *Cp = malloc(sizeof(double) * (size_t)N * S + 8);
+        double *z = malloc(sizeof(double) * (size_t)gates * S);
+        for (int d = 1; d <= D; d++) {
+            for (int r = lo[d]; r < lo[d + 1]; r++) {
+                int n = perm[r];
+                double *h = Hp + (size_t)r * S, *c = Cp + (size_t)r * S;
+                if (op[n] == OR_EMBED) {
+                    for (int j = 0; j < S; j++) { h[j] = E[(size_t)token[n] * S + j]; c[j] = 0.0; }
+                } else {
+                    int gl = gat[2 * r], gr = gat[2 * r + 1];
+                    cell_forward(cell, S, U, b, Hp + (size_t)gl * S, Cp + (size_t)gl * S,
+                                 Hp + (size_t)gr * S, Cp + (size_t)gr * S, h, c, z, NULL);
+                }
+            }
+        }
+        for (int n = 0; n < N; n++)
+            for (int j = 0; j < S; j++) {
+                H_out[(size_t)n * S + j] = Hp[(size_t)rank[n] * S + j];
+                C_out[(size_t)n * S + j] = Cp[(size_t)rank[n] * S + j];
+            }
+        free(Hp); free(Cp); free(z);
+    }
+    free(depth); free(perm); free(rank); free(gat); free(lo); free(go); free(co); free(ce);
+    free(lp); free(ts); free(rr); free(rp);
+    return st;
+}
+
+/* ---------------------------------------------------------------- backward
+ * Loss L = sum_g <dh_root[g], h_root(g)> + <dc_root[g], c_root(g)> (dc_root nullable;
+ * SURVEY §8(c.8) #10). Reverse-mode over the reverse of the topological order, so
+ * every consumer is processed before its children; a node's (dh, dc) is the sum over
+ * its consumers and root seeds (DAG: several terms). Per CELL node:
+ *   TreeLSTM: tc = tanh(c); do = dh*tc; dc += dh*o*(1-tc^2)
+ *             dz_i = dc*u*i(1-i); dz_fL = dc*c_L*fL(1-fL); dz_fR = dc*c_R*fR(1-fR)
+ *             dz_o = do*o(1-o);   dz_u  = dc*i*(1-u^2)
+ *             dc_L += dc*fL; dc_R += dc*fR
+ *   TreeRNN:  dz = dh*(1-h^2)
+ *   both:     dU += dz (x) [h_L; h_R]; db += dz; dh_L += U_L^T dz; dh_R += U_R^T dz
+ *   EMBED:    dE[token] += dh   (its c is the constant 0; dc is dropped)
+ * Outputs dU [gates*S][2S], db [gates*S], dE [V][S] are overwritten (not accumulated).
+ */
+int oracle_backward(int cell, int S, int N, int G, int V,
+                    const int32_t *op, const int32_t *child, const int32_t *token, const int32_t *root,
+                    const double *U, const double *b, const double *E,
+                    const double *dh_root, const double *dc_root,
+                    double *dU, double *db, double *dE)
+{
+    if (S <= 0 || (cell != OR_TREERNN && cell != OR_TREELSTM)) return OR_E_INVALID;
+    int32_t err;
+    int st = validate(N, G, V, op, child, token, root, &err);
+    if (st) return st;
+    int gates = (cell == OR_TREELSTM) ? 5 : 1;
+    size_t NS = (size_t)N * S;
+    double *H = malloc(sizeof(double) * NS + 8), *C = malloc(sizeof(double) * NS + 8);
+    double *A = malloc(sizeof(double) * (size_t)N * gates * S + 8);   /* gate activations */
+    double *dH = calloc(NS + 1, sizeof(double)), *dC = calloc(NS + 1, sizeof(double));
+    double *z = malloc(sizeof(double) * (size_t)gates * S), *dz = malloc(sizeof(double) * (size_t)gates * S);
+    int32_t *topo = malloc(sizeof(int32_t) * ((size_t)N + 1));
+    st = topo_order(N, op, child, topo);
+    if (st != OR_OK) goto done;
+    /* forward, saving activations */
+    for (int t = 0; t < N; t++) {
+        int n = topo[t];
+        double *h = H + (size_t)n * S, *c = C + (size_t)n * S;
+        if (op[n] == OR_EMBED) {
+            for (int j = 0; j < S; j++) { h[j] = E[(size_t)token[n] * S + j]; c[j] = 0.0; }
+        } else {
+            int L = child[2 * n], R = child[2 * n + 1];
+            cell_forward(cell, S, U, b, H + (size_t)L * S, C + (size_t)L * S,
+                         H + (size_t)R * S, C + (size_t)R * S, h, c, z, A + (size_t)n * gates * S);
+        }
+    }
+    memset(dU, 0, sizeof(double) * (size_t)gates * S * 2 * S);
+    memset(db, 0, sizeof(double) * (size_t)gates * S);
+    memset(dE, 0, sizeof(double) * (size_t)V * S);
+    for (int g = 0; g < G; g++)
+        for (int j = 0; j < S; j++) {
+            dH[(size_t)root[g] * S + j] += dh_root[(size_t)g * S + j];
+            if (dc_root) dC[(size_t)root[g] * S + j] += dc_root[(size_t)g * S + j];
+        }
+    for (int t = N - 1; t >= 0; t--) {
+        int n = topo[t];
+        double *dh = dH + (size_t)n * S, *dc = dC + (size_t)n * S;
+        if (op[n] == OR_EMBED) {
+            for (int j = 0; j < S; j++) dE[(size_t)token[n] * S + j] += dh[j];
+            continue;
+        }
+        int L = child[2 * n], R = child[2 * n + 1];
+        const double *a = A + (size_t)n * gates * S, *c = C + (size_t)n * S;
+        const double *hL = H + (size_t)L * S, *hR = H + (size_t)R * S;
+        const double *cL = C + (size_t)L * S, *cR = C + (size_t)R * S;
+        if (cell == OR_TREERNN) {
+            for (int j = 0; j < S; j++) dz[j] = dh[j] * (1.0 - a[j] * a[j]);
+        } else {
+            for (int j = 0; j < S; j++) {
+                double i = a[j], fl = a[S + j], fr = a[2 * S + j], o = a[3 * S + j], u = a[4 * S + j];
+                double tc = tanh(c[j]);
+                double dO = dh[j] * tc;
+                double dcc = dc[j] + dh[j] * o * (1.0 - tc * tc);
+                dz[j] = dcc * u * i * (1.0 - i);
+                dz[S + j] = dcc * cL[j] * fl * (1.0 - fl);
+                dz[2 * S + j] = dcc * cR[j] * fr * (1.0 - fr);
+                dz[3 * S + j] = dO * o * (1.0 - o);
+                dz[4 * S + j] = dcc * i * (1.0 - u * u);
+                dC[(size_t)L * S + j] += dcc * fl;
+                dC[(size_t)R * S + j] += dcc * fr;
+            }
+        }
+        for (int r = 0; r < gates * S; r++) {
+            double *du = dU + (size_t)r * 2 * S;
+            for (int k = 0; k < S; k++) { du[k] += dz[r] * hL[k]; du[S + k] += dz[r] * hR[k]; }
+            db[r] += dz[r];
+        }
+        double *dhL = dH + (size_t)L * S, *dhR = dH + (size_t)R * S;
+        for (int r = 0; r < gates * S; r++) {
+            const double *u = U + (size_t)r * 2 * S;
+            for (int k = 0; k < S; k++) { dhL[k] += u[k] * dz[r]; dhR[k] += u[S + k] * dz[r]; }
+        }
+    }
+done:
+    free(H); free(C); free(A); free(dH); free(dC); free(z); free(dz); free(topo);
+    return st;
+}
