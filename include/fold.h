@@ -1,0 +1,205 @@
+/*
+ * fold.h — C ABI of the B200-native dynamic-batching hot path (arXiv 1702.02181,
+ * "Deep Learning with Dynamic Computation Graphs", TensorFlow Fold, §2).
+ *
+ * Three calls carry the method:
+ *   fold_schedule  — PAPER.md L40-44 (§2 bullets): depth per node, batching of all
+ *                    nodes with the same (depth, operation), concatenation order, and
+ *                    the gather indices ("the indices to gather encode the topology",
+ *                    L30). Executor form: one append-only pool, so no pass-through
+ *                    rows are materialised.
+ *   fold_forward   — PAPER.md L47 (§2 loop model): per depth, gather child states,
+ *                    run the batched operation once (embedding lookup at depth 1,
+ *                    TreeRNN/TreeLSTM cell above), append the outputs to the pool.
+ *   fold_backward  — PAPER.md L49: the gradient of gather/concat/loop, written out as
+ *                    a reverse-level sweep with deterministic pull-reductions plus one
+ *                    weight-gradient GEMM over all cells.
+ * plus fold_sgd_update (the training step's optimizer).
+ *
+ * Conventions (all calls):
+ *  - Every pointer named d_* / documented "device" is CUDA device memory, owned by the
+ *    caller (the library never allocates or frees on these paths). Host pointers are
+ *    documented "host".
+ *  - `stream` is a cudaStream_t (CUstream) passed as void*. All work is stream-ordered.
+ *    fold_schedule performs exactly one blocking device->host copy (status, depth count,
+ *    level offsets) because launch shapes depend on it; forward/backward/sgd never sync.
+ *  - No exceptions cross the ABI; every call returns fold_status. Data-dependent errors
+ *    of fold_schedule report the smallest offending node id through
+ *    fold_last_error_detail (graph id for FOLD_E_ROOT_RANGE).
+ *  - Thread safety: calls on different streams with disjoint buffers may run concurrently;
+ *    fold_last_error_detail is thread-local.
+ *  - Int arrays are int32, row-major. Floats are IEEE fp32 unless stated.
+ */
+#ifndef FOLD_H
+#define FOLD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FOLD_ABI_VERSION 1
+
+typedef enum {
+  FOLD_OK = 0,
+  FOLD_E_INVALID = 1,       /* bad host-visible argument: null pointer, negative size,
+                               unsupported S / cell / precision, schedule/model mismatch */
+  FOLD_E_CHILD_RANGE = 2,   /* some child[n][k] not in [-1, n_nodes) */
+  FOLD_E_ARITY = 3,         /* EMBED with a child, or CELL without two children */
+  FOLD_E_TOKEN_RANGE = 4,   /* EMBED token not in [0, vocab) */
+  FOLD_E_ROOT_RANGE = 5,    /* root[g] not in [0, n_nodes) (detail = g) */
+  FOLD_E_CYCLE = 6,         /* the graph is not acyclic (PAPER.md L37 requires a DAG);
+                               detail = smallest node that depends on a cycle */
+  FOLD_E_WORKSPACE = 7,     /* workspace smaller than the *_workspace() query */
+  FOLD_E_CUDA = 8,          /* a CUDA launch/copy failed */
+  FOLD_E_MISMATCH = 9,      /* schedule and acts/model disagree (e.g. n_nodes) */
+  FOLD_E_OP_RANGE = 10,     /* op[n] not in {FOLD_OP_EMBED, FOLD_OP_CELL} */
+  FOLD_E_UNSUPPORTED = 11,  /* valid request this build does not implement
+                               (e.g. not an sm_100 device) */
+} fold_status;
+
+/* Operation ids = the enumeration order of PAPER.md L32/L43 ("all operations ... be
+ * specified in advance, and it enumerates them"): a binary TreeRNN/TreeLSTM has two. */
+enum { FOLD_OP_EMBED = 0, FOLD_OP_CELL = 1, FOLD_N_OPS = 2 };
+/* Cell equations: DESIGN.md "Cell" (TreeRNN: Fig. 1 'RNN Cell', L67; TreeLSTM: Tai et
+ * al. eqs 9-14 with x = 0, N = 2, cited at L301-304). */
+enum { FOLD_CELL_TREERNN = 0, FOLD_CELL_TREELSTM = 1 };
+/* FP32: every product and sum in fp32 (SIMT kernels).
+ * BF16: states h, saved gates and GEMM operands in bf16, fp32 accumulation in TMEM
+ *       (tcgen05), c / gradients / reductions in fp32.                            */
+enum { FOLD_PREC_FP32 = 0, FOLD_PREC_BF16 = 2 };
+
+/* ----------------------------------------------------------------- input graphs
+ * A batch of graphs = one disconnected DAG. Node n:
+ *   op[n]            FOLD_OP_EMBED (leaf; consumes its depth-0 constant token[n]) or
+ *                    FOLD_OP_CELL (consumes nodes child[2n], child[2n+1] = left, right).
+ *   child[2n + k]    int32 node ids, -1 for "none" (EMBED: both -1).
+ *   token[n]         int32 in [0, vocab) for EMBED; ignored for CELL.
+ *   root[g]          int32 node whose state is graph g's result.
+ * Any node order is accepted (children need not precede parents); DAG sharing and
+ * child[2n] == child[2n+1] are allowed. All pointers are device. */
+typedef struct {
+  int32_t n_nodes, n_graphs, vocab;
+  const int32_t *op, *child, *token, *root;
+} fold_graphs;
+
+/* ----------------------------------------------------------------- schedule
+ * Executor-form schedule; all arrays device, caller-allocated with the sizes below
+ * (N = n_nodes, G = n_graphs). Definitions (bit-exact with oracle/fold_oracle.c):
+ *   depth[N]       PAPER.md L40: EMBED = 1 (its token constant is depth 0);
+ *                  CELL = 1 + max(depth of children).
+ *   perm[N]        pool row -> node: rows ordered by (depth, op, node id) (L42-43).
+ *   rank[N]        node -> pool row (= perm^-1).
+ *   gather[2N]     gather[2r + k] = rank[child[perm[r]][k]] for CELL rows, else -1 —
+ *                  the edge label of L44 as a global pool row (the paper's per-depth
+ *                  index i = gather - level_off[depth of child]).
+ *   level_off[N+2] level_off[d] = #rows with depth < d, d = 0..n_levels+1.
+ *   group_off[2N+3] group_off[k] = #rows with key < k, key = 2*depth + op, k = 0..2(D+1).
+ *   cons_off[N+1], cons_edge[2N]
+ *                  consumer CSR: for each pool row (ascending), the cell edges
+ *                  e = 2c + k that read it, ascending; c = row - n_leaves is the cell
+ *                  index (all EMBED rows precede all CELL rows).
+ *   leaf_perm[N]   EMBED rows ordered by (token, row) (first n_leaves entries).
+ *   tok_seg[N+1]   start of each distinct-token run of leaf_perm, + end sentinel
+ *                  (first n_tok_segs + 1 entries).
+ *   root_row[G]    rank[root[g]].
+ *   root_perm[G]   graph ids ordered by (root_row, g) (deterministic seeding).
+ *   leaf_token[N]  token of each EMBED row (first n_leaves entries): the depth-0
+ *                  constants of PAPER.md L40/L47 ("int [] state", Fig. 1) in pool order.
+ *   level_off_host host array [N+2]; receives level_off[0..n_levels+1].
+ * Scalars n_levels (= max depth D), n_leaves, n_cells, n_tok_segs are outputs. */
+typedef struct {
+  int32_t *depth, *perm, *rank, *gather, *level_off, *group_off, *cons_off, *cons_edge,
+          *leaf_perm, *tok_seg, *root_row, *root_perm, *leaf_token;
+  int32_t *level_off_host;
+  int32_t n_nodes, n_graphs, n_levels, n_leaves, n_cells, n_tok_segs;
+} fold_schedule_t;
+
+/* Workspace bytes fold_schedule needs for n_nodes / n_graphs (device scratch). */
+size_t fold_schedule_workspace(int32_t n_nodes, int32_t n_graphs);
+
+/* Validate + schedule. Errors in this order (smallest offending id): CHILD_RANGE,
+ * OP_RANGE, ARITY, TOKEN_RANGE, ROOT_RANGE, CYCLE. On error the schedule arrays are
+ * unspecified. Exactly one blocking D2H copy (two if n_levels + 2 > 4096). */
+fold_status fold_schedule(const fold_graphs *graphs, fold_schedule_t *sched,
+                          void *d_workspace, size_t workspace_bytes, void *stream);
+
+/* ----------------------------------------------------------------- model
+ * Parameters are the caller's fp32 masters (device):
+ *   U[gates*S][2S]  row-major, torch nn.Linear.weight order; gate row blocks
+ *                   (i, f_L, f_R, o, u) for TreeLSTM, one block for TreeRNN; columns
+ *                   [0,S) multiply h_L, [S,2S) multiply h_R.
+ *   b[gates*S]      bias.
+ *   E[vocab][S]     embedding table (leaf h = E[token], leaf c = 0).
+ * BF16 mode converts U to bf16 inside fold_forward / fold_backward (workspace). */
+typedef struct {
+  int32_t cell, prec, S, vocab;
+  const float *U, *b, *E;
+} fold_model;
+
+/* ----------------------------------------------------------------- activations
+ * One caller-owned device buffer holding everything the forward saves for the
+ * backward (the pool of PAPER.md L47's loop state for every depth):
+ *   H [N][ld] bf16 (BF16) or fp32 (FP32)  hidden state h per pool row
+ *   C [N][ld] fp32                        cell state c per pool row (0 for TreeRNN)
+ *   G [n_cells][gates*S] bf16 / fp32      saved gate activations (i, fL, fR, o, u)
+ *                                         or h (TreeRNN) per cell
+ * Offsets/strides come from fold_acts_layout; the buffer is otherwise opaque. */
+typedef struct {
+  size_t bytes;          /* total size of the buffer */
+  size_t h_off, c_off, g_off;   /* byte offsets of H, C, G */
+  int32_t ld;            /* row stride of H and C, in elements (>= S, multiple of 8) */
+  int32_t h_elem_bytes;  /* 2 (bf16) or 4 (fp32) */
+} fold_acts_layout_t;
+
+fold_status fold_acts_layout(const fold_schedule_t *sched, const fold_model *model,
+                             fold_acts_layout_t *layout);
+
+size_t fold_forward_workspace(const fold_schedule_t *sched, const fold_model *model);
+
+/* Forward over all levels. d_acts: buffer of fold_acts_layout().bytes.
+ * d_h_root / d_c_root: [G][S] fp32 outputs (root h and c; either may be NULL). */
+fold_status fold_forward(const fold_schedule_t *sched, const fold_model *model,
+                         void *d_acts, float *d_h_root, float *d_c_root,
+                         void *d_workspace, size_t workspace_bytes, void *stream);
+
+/* ----------------------------------------------------------------- backward
+ * Loss L = sum_g <dh_root[g], h_root(g)> + <dc_root[g], c_root(g)> (dc_root may be
+ * NULL = 0). Outputs dU/db/dE with the layouts of U/b/E (device fp32). With
+ * accumulate = 0 they are overwritten (dE rows of untouched tokens become 0);
+ * with accumulate = 1 the gradients are added. Deterministic: bitwise-identical
+ * results for identical inputs (no floating-point atomics). */
+typedef struct {
+  float *dU, *db, *dE;
+  int32_t accumulate;
+} fold_grads;
+
+size_t fold_backward_workspace(const fold_schedule_t *sched, const fold_model *model);
+
+fold_status fold_backward(const fold_schedule_t *sched, const fold_model *model,
+                          const void *d_acts, const float *d_dh_root, const float *d_dc_root,
+                          fold_grads *grads, void *d_workspace, size_t workspace_bytes,
+                          void *stream);
+
+/* param[i] -= lr * grad[i], i < n (device fp32). SPEC S:L511 sgd_step. */
+fold_status fold_sgd_update(float *d_param, const float *d_grad, int64_t n, float lr,
+                            void *stream);
+
+/* ----------------------------------------------------------------- misc */
+const char *fold_status_string(fold_status s);
+/* Detail of the last data-dependent error on this thread: the offending node (or
+ * graph) id, -1 if none. */
+int32_t fold_last_error_detail(void);
+int32_t fold_abi_version(void);
+/* FOLD_OK if the current CUDA device is sm_100 (B200) and the kernels are loadable. */
+fold_status fold_device_check(void);
+/* Number of kernels this library launched on the calling thread since the last reset
+ * (instrumentation for the bench's gpu_launches count). */
+int64_t fold_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FOLD_H */

@@ -1,0 +1,268 @@
+// abi.cu — the extern "C" entry points declared in include/fold.h: argument checks,
+// workspace carving and launch sequencing of the level loop (one
+// iteration per depth) forward and in reverse for the backward (L49).
+#include <cstring>
+
+#include "exec.cuh"
+
+namespace fold {
+
+fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws, size_t ws_bytes, cudaStream_t st);
+size_t schedule_workspace(int64_t N, int64_t G);
+extern thread_local int32_t g_last_detail;
+
+namespace {
+
+inline size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
+
+fold_status check_model(const fold_model *m) {
+  if (!m || !m->U || !m->b || !m->E) return FOLD_E_INVALID;
+  if (m->cell != FOLD_CELL_TREERNN && m->cell != FOLD_CELL_TREELSTM) return FOLD_E_INVALID;
+  if (m->prec != FOLD_PREC_FP32 && m->prec != FOLD_PREC_BF16) return FOLD_E_INVALID;
+  if (m->S <= 0 || m->S > 8192 || m->vocab <= 0) return FOLD_E_INVALID;
+  return FOLD_OK;
+}
+
+fold_status check_sched(const fold_schedule_t *s) {
+  if (!s || s->n_nodes < 0 || s->n_levels < 0 || !s->level_off_host) return FOLD_E_INVALID;
+  if (s->n_nodes > 0 && (!s->perm || !s->gather || !s->cons_off || !s->cons_edge)) return FOLD_E_INVALID;
+  return FOLD_OK;
+}
+
+// backward workspace carve
+struct BwdWs {
+  float *dA, *dCe, *partial;
+  void *dZ;
+  TcWeights w;
+  int ld_z, nsplit;
+  size_t bytes;
+};
+
+BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
+  BwdWs b{};
+  const int64_t nc = s->n_cells, S = m->S;
+  const int gates = gates_of(m->cell);
+  const bool bf16 = m->prec == FOLD_PREC_BF16;
+  b.ld_z = (int)round_up((int64_t)gates * S, 8);
+  b.nsplit = (int)(nc / 256 < 1 ? 1 : (nc / 256 > 128 ? 128 : nc / 256));
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = a256(off + bytes); return o; };
+  size_t o_dA = take((size_t)(2 * nc + 1) * S * 4);
+  size_t o_dCe = take(gates == 5 ? (size_t)(2 * nc + 1) * S * 4 : 256);
+  size_t o_dZ = take((size_t)(nc + 1) * b.ld_z * (bf16 ? 2 : 4));
+  size_t o_part = take((size_t)b.nsplit * gates * S * 4);
+  size_t o_w = take(bf16 ? tc_workspace_bytes(gates, (int)S) : 0);
+  b.bytes = off;
+  if (base) {
+    char *p = (char *)base;
+    b.dA = (float *)(p + o_dA);
+    b.dCe = (float *)(p + o_dCe);
+    b.dZ = p + o_dZ;
+    b.partial = (float *)(p + o_part);
+    if (bf16) {
+      b.w.ld_u = (int)round_up(2 * S, 8);
+      b.w.ld_ut = (int)round_up((int64_t)gates * S, 8);
+      b.w.U = (__nv_bfloat16 *)(p + o_w);
+      b.w.Ut = (__nv_bfloat16 *)(p + o_w + a256((size_t)gates * S * b.w.ld_u * 2));
+    }
+  }
+  return b;
+}
+
+size_t fwd_ws_bytes(const fold_model *m) {
+  if (m->prec != FOLD_PREC_BF16) return 256;
+  return tc_workspace_bytes(gates_of(m->cell), m->S);
+}
+
+}  // namespace
+
+ActsLayout acts_layout(const fold_schedule_t *s, const fold_model *m) {
+  ActsLayout L{};
+  const int64_t N = s->n_nodes, nc = s->n_cells, S = m->S;
+  const int gates = gates_of(m->cell);
+  L.helem = m->prec == FOLD_PREC_BF16 ? 2 : 4;
+  L.ld = ld_of((int)S);
+  L.ld_g = (int)round_up((int64_t)gates * S, 8);
+  size_t off = 0;
+  L.h_off = off; off = a256(off + (size_t)(N + 1) * L.ld * L.helem);
+  L.c_off = off; off = a256(off + (size_t)(N + 1) * L.ld * 4);
+  L.g_off = off; off = a256(off + (size_t)(nc + 1) * L.ld_g * L.helem);
+  L.bytes = off;
+  return L;
+}
+
+}  // namespace fold
+
+using namespace fold;
+
+extern "C" {
+
+size_t fold_schedule_workspace(int32_t n_nodes, int32_t n_graphs) {
+  return schedule_workspace(n_nodes < 0 ? 0 : n_nodes, n_graphs < 0 ? 0 : n_graphs);
+}
+
+fold_status fold_schedule(const fold_graphs *graphs, fold_schedule_t *sched, void *ws, size_t ws_bytes,
+                          void *stream) {
+  return run_schedule(graphs, sched, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+fold_status fold_acts_layout(const fold_schedule_t *s, const fold_model *m, fold_acts_layout_t *out) {
+  FOLD_TRY(check_sched(s));
+  FOLD_TRY(check_model(m));
+  if (!out) return FOLD_E_INVALID;
+  ActsLayout L = acts_layout(s, m);
+  out->bytes = L.bytes; out->h_off = L.h_off; out->c_off = L.c_off; out->g_off = L.g_off;
+  out->ld = L.ld; out->h_elem_bytes = L.helem;
+  return FOLD_OK;
+}
+
+size_t fold_forward_workspace(const fold_schedule_t *s, const fold_model *m) {
+  if (check_sched(s) != FOLD_OK || check_model(m) != FOLD_OK) return 0;
+  return fwd_ws_bytes(m);
+}
+
+// Forward level loop: depth 1 = embedding lookup, depth d >= 2 = one
+// batched cell invocation over the level's contiguous pool rows [lo[d], lo[d+1]).
+fold_status fold_forward(const fold_schedule_t *s, const fold_model *m, void *acts, float *h_root, float *c_root,
+                         void *ws, size_t ws_bytes, void *stream) {
+  FOLD_TRY(check_sched(s));
+  FOLD_TRY(check_model(m));
+  if (!acts && s->n_nodes > 0) return FOLD_E_INVALID;
+  if (ws_bytes < fwd_ws_bytes(m) || (!ws && m->prec == FOLD_PREC_BF16)) return FOLD_E_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int N = s->n_nodes, S = m->S, D = s->n_levels, nl = s->n_leaves, G = s->n_graphs;
+  if (N == 0) return FOLD_OK;
+  if (!s->leaf_token || !s->root_row) return FOLD_E_INVALID;
+  const bool bf16 = m->prec == FOLD_PREC_BF16;
+  const int gates = gates_of(m->cell);
+  ActsLayout L = acts_layout(s, m);
+  char *a = (char *)acts;
+  void *H = a + L.h_off;
+  float *C = (float *)(a + L.c_off);
+  void *Gact = a + L.g_off;
+  const int32_t *lo = s->level_off_host;
+  FOLD_TRY(launch_embed_fwd(bf16, lo[1], lo[2], s->leaf_token, m->E, S, L.ld, H, C, st));
+  if (bf16) {
+    TcWeights w{};
+    w.ld_u = (int)round_up(2 * (int64_t)S, 8);
+    w.ld_ut = (int)round_up((int64_t)gates * S, 8);
+    w.U = (__nv_bfloat16 *)ws;
+    w.Ut = nullptr;
+    if (D >= 2) FOLD_TRY(tc_prepare_U(gates, S, m->U, w, false, st));
+    for (int d = 2; d <= D; d++)
+      FOLD_TRY(tc_cell_fwd(m->cell, lo[d], lo[d + 1], nl, s->gather, S, L.ld, w, m->b, (__nv_bfloat16 *)H, N, C,
+                           (__nv_bfloat16 *)Gact, L.ld_g, st));
+  } else {
+    for (int d = 2; d <= D; d++)
+      FOLD_TRY(launch_cell_fwd_simt(m->cell, lo[d], lo[d + 1], s->gather, S, L.ld, m->U, m->b, (float *)H, C,
+                                    (float *)Gact, L.ld_g, nl, st));
+  }
+  FOLD_TRY(launch_root_out(bf16, G, S, L.ld, s->root_row, H, C, h_root, c_root, st));
+  return FOLD_OK;
+}
+
+size_t fold_backward_workspace(const fold_schedule_t *s, const fold_model *m) {
+  if (check_sched(s) != FOLD_OK || check_model(m) != FOLD_OK) return 0;
+  return bwd_layout(nullptr, s, m).bytes;
+}
+
+// Reverse level sweep: for d = D..2 pull-reduce the consumers' edge
+// gradients, form dz, and produce this level's edge gradients dA = dz U; then the
+// embedding gradient at depth 1 and one weight-gradient GEMM over all cells.
+fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const void *acts, const float *dh_root,
+                          const float *dc_root, fold_grads *grads, void *ws, size_t ws_bytes, void *stream) {
+  FOLD_TRY(check_sched(s));
+  FOLD_TRY(check_model(m));
+  if (!grads || !grads->dU || !grads->db || !grads->dE) return FOLD_E_INVALID;
+  if (s->n_graphs > 0 && !dh_root) return FOLD_E_INVALID;
+  BwdWs b = bwd_layout(ws, s, m);
+  if (!ws || ws_bytes < b.bytes) return FOLD_E_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int N = s->n_nodes, S = m->S, D = s->n_levels, nl = s->n_leaves, G = s->n_graphs, nc = s->n_cells;
+  const int gates = gates_of(m->cell);
+  const bool bf16 = m->prec == FOLD_PREC_BF16;
+  const int acc = grads->accumulate ? 1 : 0;
+  if (!acc) FOLD_TRY(launch_zero(grads->dE, (size_t)m->vocab * S * 4, st));
+  if (N == 0 || nc == 0) {
+    if (!acc) {
+      FOLD_TRY(launch_zero(grads->dU, (size_t)gates * S * 2 * S * 4, st));
+      FOLD_TRY(launch_zero(grads->db, (size_t)gates * S * 4, st));
+    }
+    if (N > 0)
+      FOLD_TRY(launch_embed_bwd(S, nl, s->n_tok_segs, s->tok_seg, s->leaf_perm, s->leaf_token, s->cons_off,
+                                s->cons_edge, s->root_row, s->root_perm, G, dh_root, b.dA, grads->dE, st));
+    return FOLD_OK;
+  }
+  if (!acts) return FOLD_E_INVALID;
+  ActsLayout L = acts_layout(s, m);
+  const char *a = (const char *)acts;
+  const void *H = a + L.h_off;
+  const float *C = (const float *)(a + L.c_off);
+  const void *Gact = a + L.g_off;
+  const int32_t *lo = s->level_off_host;
+  if (bf16) FOLD_TRY(tc_prepare_U(gates, S, m->U, b.w, true, st));
+  for (int d = D; d >= 2; d--) {
+    const int r0 = lo[d], r1 = lo[d + 1], M = r1 - r0, c0 = r0 - nl;
+    if (M <= 0) continue;
+    FOLD_TRY(launch_cell_bwd_pw(bf16, m->cell, r0, r1, nl, S, L.ld, L.ld_g, s->cons_off, s->cons_edge, s->root_row,
+                                s->root_perm, G, dh_root, dc_root, s->gather, Gact, C, b.dA, b.dCe, b.dZ, b.ld_z, st));
+    float *dA_lvl = b.dA + (size_t)2 * c0 * S;
+    if (bf16)
+      FOLD_TRY(tc_gemm_dA(c0, M, nc, S, gates, (const __nv_bfloat16 *)b.dZ, b.ld_z, b.w, b.dA, st));
+    else
+      FOLD_TRY(launch_gemm_dA_simt(M, S, gates, (const float *)b.dZ + (size_t)c0 * b.ld_z, b.ld_z, m->U, dA_lvl, st));
+  }
+  FOLD_TRY(launch_embed_bwd(S, nl, s->n_tok_segs, s->tok_seg, s->leaf_perm, s->leaf_token, s->cons_off, s->cons_edge,
+                            s->root_row, s->root_perm, G, dh_root, b.dA, grads->dE, st));
+  if (bf16)
+    FOLD_TRY(tc_gemm_dU(nc, nl, S, gates, (const __nv_bfloat16 *)b.dZ, b.ld_z, s->gather, (const __nv_bfloat16 *)H,
+                        L.ld, N, grads->dU, acc, st));
+  else
+    FOLD_TRY(launch_gemm_dU_simt(nc, nl, S, gates, (const float *)b.dZ, b.ld_z, s->gather, (const float *)H, L.ld,
+                                 grads->dU, acc, st));
+  FOLD_TRY(launch_colsum(bf16, nc, gates * S, b.dZ, b.ld_z, b.partial, b.nsplit, grads->db, acc, st));
+  return FOLD_OK;
+}
+
+fold_status fold_sgd_update(float *p, const float *g, int64_t n, float lr, void *stream) {
+  if (n < 0 || (n > 0 && (!p || !g))) return FOLD_E_INVALID;
+  return launch_sgd(p, g, n, lr, (cudaStream_t)stream);
+}
+
+const char *fold_status_string(fold_status s) {
+  switch (s) {
+    case FOLD_OK: return "FOLD_OK";
+    case FOLD_E_INVALID: return "FOLD_E_INVALID";
+    case FOLD_E_CHILD_RANGE: return "FOLD_E_CHILD_RANGE";
+    case FOLD_E_ARITY: return "FOLD_E_ARITY";
+    case FOLD_E_TOKEN_RANGE: return "FOLD_E_TOKEN_RANGE";
+    case FOLD_E_ROOT_RANGE: return "FOLD_E_ROOT_RANGE";
+    case FOLD_E_CYCLE: return "FOLD_E_CYCLE";
+    case FOLD_E_WORKSPACE: return "FOLD_E_WORKSPACE";
+    case FOLD_E_CUDA: return "FOLD_E_CUDA";
+    case FOLD_E_MISMATCH: return "FOLD_E_MISMATCH";
+    case FOLD_E_OP_RANGE: return "FOLD_E_OP_RANGE";
+    case FOLD_E_UNSUPPORTED: return "FOLD_E_UNSUPPORTED";
+  }
+  return "FOLD_E_UNKNOWN";
+}
+
+int32_t fold_last_error_detail(void) { return g_last_detail; }
+int32_t fold_abi_version(void) { return FOLD_ABI_VERSION; }
+
+fold_status fold_device_check(void) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return FOLD_E_CUDA;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return FOLD_E_CUDA;
+  if (cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) return FOLD_E_CUDA;
+  return (major == 10 && minor == 0) ? FOLD_OK : FOLD_E_UNSUPPORTED;
+}
+
+int64_t fold_launch_count(int32_t reset) {
+  int64_t v = g_launches;
+  if (reset) g_launches = 0;
+  return v;
+}
+
+}  // extern "C"
+

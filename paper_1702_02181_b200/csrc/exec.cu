@@ -1,0 +1,521 @@
+// exec.cu — level executor kernels other than the tcgen05 GEMMs:
+//   embedding level (Fig. 1 "embed lookup", L67), the fp32 SIMT cell kernel
+//   (FOLD_PREC_FP32 mode), root read-out, the backward pointwise pull-reduce kernel,
+//   fp32 SIMT GEMMs for the backward, deterministic column sums (db), the segmented
+//   embedding gradient, and SGD.
+// Cell equations: DESIGN.md "Cell" (TreeLSTM = Tai et al. eqs 9-14 with x=0, N=2,
+// cited at PAPER.md L301-304; TreeRNN = tanh(W[h_L;h_R]+b), Fig. 1 "RNN Cell").
+#include "exec.cuh"
+
+namespace fold {
+
+namespace {
+
+inline unsigned grid_cap(int64_t blocks) {
+  if (blocks < 1) blocks = 1;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  return (unsigned)blocks;
+}
+
+// ---------------------------------------------------------------- embedding forward
+// H[r] = E[token[perm[r]]], C[r] = 0 for the level-1 rows [r0, r1). One warp per row.
+template <typename T>
+__global__ void k_embed_fwd(int r0, int r1, const int32_t *__restrict__ leaf_token,
+                            const float *__restrict__ E, int S, int ld, T *__restrict__ H, float *__restrict__ C) {
+  int lane = threadIdx.x & 31;
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = r0 + w; r < r1; r += nw) {
+    int tok = leaf_token[r];
+    const float *e = E + (int64_t)tok * S;
+    T *h = H + r * ld;
+    float *c = C + r * ld;
+    if ((S & 3) == 0) {
+      for (int j = lane * 4; j < S; j += 128) {
+        float4 v = *reinterpret_cast<const float4 *>(e + j);
+        if constexpr (sizeof(T) == 2) {
+          __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b2 = __floats2bfloat162_rn(v.z, v.w);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t *>(&a);
+          pk.y = *reinterpret_cast<uint32_t *>(&b2);
+          *reinterpret_cast<uint2 *>(h + j) = pk;
+        } else {
+          *reinterpret_cast<float4 *>(h + j) = v;
+        }
+        *reinterpret_cast<float4 *>(c + j) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    } else {
+      for (int j = lane; j < S; j += 32) { h[j] = from_f<T>(e[j]); c[j] = 0.f; }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- fp32 SIMT cell forward
+// Block tile: 32 rows x 32 state columns x all GATES gate blocks; K = 2S in chunks of 32.
+// A row m = [H[gL] | H[gR]] gathered on the fly (gather -> op -> concat,
+// the concat being the append into rows [r0, r1) of the pool).
+template <int GATES>
+__global__ void __launch_bounds__(256) k_cell_fwd_simt(int r0, int r1, const int32_t *__restrict__ gather,
+                                                       int S, int ld, const float *__restrict__ U,
+                                                       const float *__restrict__ bias, float *__restrict__ H,
+                                                       float *__restrict__ C, float *__restrict__ Gact, int ld_g,
+                                                       int nl) {
+  constexpr int BM = 32, BW = 32, BK = 32;
+  __shared__ float As[BK][BM + 1];
+  __shared__ float Bs[GATES][BK][BW + 1];
+  __shared__ int gl[BM], gr[BM];
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;  // ty: 0..7
+  const int m0 = r0 + blockIdx.x * BM, j0 = blockIdx.y * BW;
+  const int M = r1 - r0;
+  if (tid < BM) {
+    int r = m0 + tid;
+    bool ok = r < r1;
+    gl[tid] = ok ? gather[2 * (int64_t)r] : 0;
+    gr[tid] = ok ? gather[2 * (int64_t)r + 1] : 0;
+  }
+  __syncthreads();
+  float acc[4][GATES];
+#pragma unroll
+  for (int i = 0; i < 4; i++)
+#pragma unroll
+    for (int g = 0; g < GATES; g++) acc[i][g] = 0.f;
+  const int K = 2 * S;
+  for (int k0 = 0; k0 < K; k0 += BK) {
+#pragma unroll
+    for (int it = 0; it < (BM * BK) / 256; it++) {
+      int idx = tid + it * 256, kk = idx & 31, mm = idx >> 5;
+      int k = k0 + kk;
+      float v = 0.f;
+      if (k < K && (m0 - r0) + mm < M) {
+        int row = k < S ? gl[mm] : gr[mm];
+        v = H[(int64_t)row * ld + (k < S ? k : k - S)];
+      }
+      As[kk][mm] = v;
+    }
+#pragma unroll
+    for (int g = 0; g < GATES; g++)
+#pragma unroll
+      for (int it = 0; it < (BW * BK) / 256; it++) {
+        int idx = tid + it * 256, kk = idx & 31, jj = idx >> 5;
+        int k = k0 + kk, j = j0 + jj;
+        Bs[g][kk][jj] = (k < K && j < S) ? U[((int64_t)g * S + j) * K + k] : 0.f;
+      }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < BK; kk++) {
+      float a[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int g = 0; g < GATES; g++) {
+        float bv = Bs[g][kk][tx];
+#pragma unroll
+        for (int i = 0; i < 4; i++) acc[i][g] = fmaf(a[i], bv, acc[i][g]);
+      }
+    }
+    __syncthreads();
+  }
+  const int j = j0 + tx;
+  if (j >= S) return;
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    int mm = ty * 4 + i;
+    int64_t r = m0 + mm;
+    if (r >= r1) continue;
+    int64_t c = r - nl;
+    if constexpr (GATES == 1) {
+      float h = tanhf(acc[i][0] + bias[j]);
+      H[r * ld + j] = h;
+      C[r * ld + j] = 0.f;
+      Gact[c * ld_g + j] = h;
+    } else {
+      float zi = acc[i][0] + bias[j], zfl = acc[i][1] + bias[S + j], zfr = acc[i][2] + bias[2 * S + j];
+      float zo = acc[i][3] + bias[3 * S + j], zu = acc[i][4] + bias[4 * S + j];
+      float ig = 1.f / (1.f + expf(-zi)), fl = 1.f / (1.f + expf(-zfl)), fr = 1.f / (1.f + expf(-zfr));
+      float og = 1.f / (1.f + expf(-zo)), ug = tanhf(zu);
+      float cl = C[(int64_t)gl[mm] * ld + j], cr = C[(int64_t)gr[mm] * ld + j];
+      float cc = ig * ug + fl * cl + fr * cr;
+      H[r * ld + j] = og * tanhf(cc);
+      C[r * ld + j] = cc;
+      float *ga = Gact + c * ld_g;
+      ga[j] = ig; ga[S + j] = fl; ga[2 * S + j] = fr; ga[3 * S + j] = og; ga[4 * S + j] = ug;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- roots out
+template <typename T>
+__global__ void k_root_out(int G, int S, int ld, const int32_t *__restrict__ root_row, const T *__restrict__ H,
+                           const float *__restrict__ C, float *__restrict__ h_root, float *__restrict__ c_root) {
+  int64_t total = (int64_t)G * S;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    int64_t g = i / S, j = i - g * S;
+    int64_t r = root_row[g];
+    if (h_root) h_root[i] = to_f(H[r * ld + j]);
+    if (c_root) c_root[i] = C[r * ld + j];
+  }
+}
+
+// ---------------------------------------------------------------- backward pointwise
+// Per cell row r of one level (one warp per row):
+//   dh = sum_{roots g at r, ascending g} dh_root[g] + sum_{e in cons(r), ascending} dA[e]
+//   dc = sum_{roots} dc_root[g] + sum_{e} dCe[e]                 (pull, no atomics)
+//   TreeLSTM: tc = tanh(c); do = dh*tc; dc += dh*o*(1-tc^2)
+//             dz = [dc*u*i(1-i), dc*cL*fL(1-fL), dc*cR*fR(1-fR), do*o(1-o), dc*i*(1-u^2)]
+//             dCe[2c] = dc*fL, dCe[2c+1] = dc*fR
+//   TreeRNN:  dz = dh*(1-h^2)
+template <typename T, int GATES>
+__global__ void k_cell_bwd_pw(int r0, int r1, int nl, int S, int ld, int ld_g, const int32_t *__restrict__ cons_off,
+                              const int32_t *__restrict__ cons_edge, const int32_t *__restrict__ root_row,
+                              const int32_t *__restrict__ root_perm, int G, const float *__restrict__ dh_root,
+                              const float *__restrict__ dc_root, const int32_t *__restrict__ gather,
+                              const T *__restrict__ Gact, const float *__restrict__ C, const float *__restrict__ dA,
+                              float *__restrict__ dCe, T *__restrict__ dZ, int ld_z) {
+  int lane = threadIdx.x & 31;
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = r0 + w; r < r1; r += nw) {
+    int64_t c = r - nl;
+    int e0 = cons_off[r], e1 = cons_off[r + 1];
+    // roots seeded at this row: root_perm orders graphs by (root_row, g)
+    int lo = 0, hi = G;
+    while (lo < hi) { int mid = (lo + hi) >> 1; if (root_row[root_perm[mid]] < r) lo = mid + 1; else hi = mid; }
+    int rs0 = lo;
+    int rs1 = rs0;
+    while (rs1 < G && root_row[root_perm[rs1]] == r) rs1++;
+    const T *ga = Gact + c * ld_g;
+    T *dz = dZ + c * ld_z;
+    int64_t gL = gather[2 * r], gR = gather[2 * r + 1];
+    for (int j = lane; j < S; j += 32) {
+      float dh = 0.f, dc = 0.f;
+      for (int q = rs0; q < rs1; q++) {
+        int g = root_perm[q];
+        dh += dh_root[(int64_t)g * S + j];
+        if (dc_root) dc += dc_root[(int64_t)g * S + j];
+      }
+      for (int e = e0; e < e1; e++) {
+        int64_t ed = cons_edge[e];
+        dh += dA[ed * S + j];
+        if (GATES == 5) dc += dCe[ed * S + j];
+      }
+      if constexpr (GATES == 1) {
+        float h = to_f(ga[j]);
+        dz[j] = from_f<T>(dh * (1.f - h * h));
+      } else {
+        float ig = to_f(ga[j]), fl = to_f(ga[S + j]), fr = to_f(ga[2 * S + j]);
+        float og = to_f(ga[3 * S + j]), ug = to_f(ga[4 * S + j]);
+        float cc = C[r * ld + j];
+        float tc = tanhf(cc);
+        float dO = dh * tc;
+        float dcc = dc + dh * og * (1.f - tc * tc);
+        float cl = C[gL * ld + j], cr = C[gR * ld + j];
+        dz[j] = from_f<T>(dcc * ug * ig * (1.f - ig));
+        dz[S + j] = from_f<T>(dcc * cl * fl * (1.f - fl));
+        dz[2 * S + j] = from_f<T>(dcc * cr * fr * (1.f - fr));
+        dz[3 * S + j] = from_f<T>(dO * og * (1.f - og));
+        dz[4 * S + j] = from_f<T>(dcc * ig * (1.f - ug * ug));
+        dCe[(2 * c) * S + j] = dcc * fl;
+        dCe[(2 * c + 1) * S + j] = dcc * fr;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- fp32 SIMT GEMMs
+// dA[m][n] = sum_k dZ[m][k] U[k][n];  M rows, N = 2S, K = gates*S. 64x64 tiles, BK 16.
+__global__ void __launch_bounds__(256) k_gemm_dA_simt(int M, int N, int K, const float *__restrict__ A, int lda,
+                                                      const float *__restrict__ B, int ldb, float *__restrict__ Cm,
+                                                      int ldc) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+#pragma unroll
+    for (int it = 0; it < 4; it++) {
+      int idx = tid + it * 256, kk = idx & 15, mm = idx >> 4;
+      int m = m0 + mm, k = k0 + kk;
+      As[kk][mm] = (m < M && k < K) ? A[(int64_t)m * lda + k] : 0.f;
+      int nn = idx & 63, kb = idx >> 6;
+      int n = n0 + nn, k2 = k0 + kb;
+      Bs[kb][nn] = (n < N && k2 < K) ? B[(int64_t)k2 * ldb + n] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; kk++) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) { a[i] = As[kk][ty * 4 + i]; b[i] = Bs[kk][tx * 4 + i]; }
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[i][q] = fmaf(a[i], b[q], acc[i][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    int m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      int n = n0 + tx * 4 + q;
+      if (n < N) Cm[(int64_t)m * ldc + n] = acc[i][q];
+    }
+  }
+}
+
+// dU[i][j] = sum_c dZ[c][i] * Acat(c, j), Acat(c, j) = H[gather[2(nl+c) + (j >= S)]][j mod S].
+// M = gates*S (i), N = 2S (j), K = n_cells (c, fixed ascending order per output).
+__global__ void __launch_bounds__(256) k_gemm_dU_simt(int n_cells, int nl, int S, int Mg, const float *__restrict__ dZ,
+                                                      int ld_z, const int32_t *__restrict__ gather,
+                                                      const float *__restrict__ H, int ld, float *__restrict__ dU,
+                                                      int accumulate) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const int N = 2 * S;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < n_cells; k0 += 16) {
+#pragma unroll
+    for (int it = 0; it < 4; it++) {
+      int idx = tid + it * 256, mm = idx & 63, kk = idx >> 6;
+      int c = k0 + kk;
+      int m = m0 + mm;
+      As[kk][mm] = (c < n_cells && m < Mg) ? dZ[(int64_t)c * ld_z + m] : 0.f;
+      int n = n0 + mm;
+      float v = 0.f;
+      if (c < n_cells && n < N) {
+        int half = n >= S;
+        int64_t row = gather[2 * ((int64_t)nl + c) + half];
+        v = H[row * ld + (n - half * S)];
+      }
+      Bs[kk][mm] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; kk++) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) { a[i] = As[kk][ty * 4 + i]; b[i] = Bs[kk][tx * 4 + i]; }
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[i][q] = fmaf(a[i], b[q], acc[i][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    int m = m0 + ty * 4 + i;
+    if (m >= Mg) continue;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      int n = n0 + tx * 4 + q;
+      if (n >= N) continue;
+      float *p = dU + (int64_t)m * N + n;
+      *p = accumulate ? *p + acc[i][q] : acc[i][q];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- column sums (db)
+// partial[s][j] = sum over rows of split s (ascending) ; then db[j] = sum_s partial[s][j].
+template <typename T>
+__global__ void k_colsum_partial(int n_rows, int ncols, const T *__restrict__ X, int ldx, int nsplit,
+                                 float *__restrict__ partial) {
+  int s = blockIdx.y;
+  int64_t rows_per = cdiv(n_rows, nsplit);
+  int64_t a = s * rows_per, b = a + rows_per < n_rows ? a + rows_per : n_rows;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ncols; j += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int64_t r = a; r < b; r++) acc += to_f(X[r * ldx + j]);
+    partial[(int64_t)s * ncols + j] = acc;
+  }
+}
+
+__global__ void k_colsum_final(int ncols, int nsplit, const float *__restrict__ partial, float *__restrict__ out,
+                               int accumulate) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ncols; j += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < nsplit; s++) acc += partial[(int64_t)s * ncols + j];
+    out[j] = accumulate ? out[j] + acc : acc;
+  }
+}
+
+// ---------------------------------------------------------------- embedding backward
+// For each distinct-token segment of leaf_perm (rows ascending): dE[tok] = sum over its
+// rows of dh(row), dh(row) = roots seeded at row + sum_{e in cons(row)} dA[e].
+// One warp per segment; deterministic order. dE must be pre-zeroed or hold the
+// accumulation base (rows of absent tokens are untouched).
+__global__ void k_embed_bwd(int S, int n_tok_segs, const int32_t *__restrict__ tok_seg,
+                            const int32_t *__restrict__ leaf_perm, const int32_t *__restrict__ leaf_token,
+                            const int32_t *__restrict__ cons_off,
+                            const int32_t *__restrict__ cons_edge, const int32_t *__restrict__ root_row,
+                            const int32_t *__restrict__ root_perm, int G, const float *__restrict__ dh_root,
+                            const float *__restrict__ dA, float *__restrict__ dE) {
+  int lane = threadIdx.x & 31;
+  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = w; s < n_tok_segs; s += nw) {
+    int a = tok_seg[s], b = tok_seg[s + 1];
+    int tok = leaf_token[leaf_perm[a]];
+    float *de = dE + (int64_t)tok * S;
+    for (int j0 = 0; j0 < S; j0 += 32 * 4) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int q = a; q < b; q++) {
+        int r = leaf_perm[q];
+        int lo = 0, hi = G;
+        while (lo < hi) { int mid = (lo + hi) >> 1; if (root_row[root_perm[mid]] < r) lo = mid + 1; else hi = mid; }
+        int e0 = cons_off[r], e1 = cons_off[r + 1];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          int j = j0 + u * 32 + lane;
+          if (j >= S) continue;
+          float dh = 0.f;
+          for (int k = lo; k < G && root_row[root_perm[k]] == r; k++) dh += dh_root[(int64_t)root_perm[k] * S + j];
+          for (int e = e0; e < e1; e++) dh += dA[(int64_t)cons_edge[e] * S + j];
+          acc[u] += dh;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        int j = j0 + u * 32 + lane;
+        if (j < S) de[j] += acc[u];
+      }
+    }
+  }
+}
+
+__global__ void k_sgd(float *p, const float *g, int64_t n, float lr) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) p[i] -= lr * g[i];
+}
+
+__global__ void k_zero(uint32_t *p, int64_t n) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) p[i] = 0u;
+}
+
+}  // namespace
+
+// ================================================================= launchers
+fold_status launch_embed_fwd(bool bf16, int r0, int r1, const int32_t *leaf_token, const float *E, int S, int ld,
+                             void *H, float *C, cudaStream_t st) {
+  if (r1 <= r0) return FOLD_OK;
+  unsigned g = grid_cap(cdiv((int64_t)(r1 - r0) * 32, 256));
+  if (bf16) k_embed_fwd<__nv_bfloat16><<<g, 256, 0, st>>>(r0, r1, leaf_token, E, S, ld, (__nv_bfloat16 *)H, C);
+  else k_embed_fwd<float><<<g, 256, 0, st>>>(r0, r1, leaf_token, E, S, ld, (float *)H, C);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+fold_status launch_cell_fwd_simt(int cell, int r0, int r1, const int32_t *gather, int S, int ld, const float *U,
+                                 const float *b, float *H, float *C, float *Gact, int ld_g, int nl, cudaStream_t st) {
+  if (r1 <= r0) return FOLD_OK;
+  dim3 grid((unsigned)cdiv(r1 - r0, 32), (unsigned)cdiv(S, 32));
+  if (cell == FOLD_CELL_TREELSTM)
+    k_cell_fwd_simt<5><<<grid, 256, 0, st>>>(r0, r1, gather, S, ld, U, b, H, C, Gact, ld_g, nl);
+  else
+    k_cell_fwd_simt<1><<<grid, 256, 0, st>>>(r0, r1, gather, S, ld, U, b, H, C, Gact, ld_g, nl);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+fold_status launch_root_out(bool bf16, int G, int S, int ld, const int32_t *root_row, const void *H, const float *C,
+                            float *h_root, float *c_root, cudaStream_t st) {
+  if (G <= 0 || (!h_root && !c_root)) return FOLD_OK;
+  unsigned g = grid_cap(cdiv((int64_t)G * S, 256));
+  if (bf16) k_root_out<__nv_bfloat16><<<g, 256, 0, st>>>(G, S, ld, root_row, (const __nv_bfloat16 *)H, C, h_root, c_root);
+  else k_root_out<float><<<g, 256, 0, st>>>(G, S, ld, root_row, (const float *)H, C, h_root, c_root);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+fold_status launch_cell_bwd_pw(bool bf16, int cell, int r0, int r1, int nl, int S, int ld, int ld_g,
+                               const int32_t *cons_off, const int32_t *cons_edge, const int32_t *root_row,
+                               const int32_t *root_perm, int G, const float *dh_root, const float *dc_root,
+                               const int32_t *gather, const void *Gact, const float *C, const float *dA, float *dCe,
+                               void *dZ, int ld_z, cudaStream_t st) {
+  if (r1 <= r0) return FOLD_OK;
+  unsigned g = grid_cap(cdiv((int64_t)(r1 - r0) * 32, 256));
+#define PW_ARGS r0, r1, nl, S, ld, ld_g, cons_off, cons_edge, root_row, root_perm, G, dh_root, dc_root, gather
+  if (bf16) {
+    if (cell == FOLD_CELL_TREELSTM)
+      k_cell_bwd_pw<__nv_bfloat16, 5><<<g, 256, 0, st>>>(PW_ARGS, (const __nv_bfloat16 *)Gact, C, dA, dCe,
+                                                         (__nv_bfloat16 *)dZ, ld_z);
+    else
+      k_cell_bwd_pw<__nv_bfloat16, 1><<<g, 256, 0, st>>>(PW_ARGS, (const __nv_bfloat16 *)Gact, C, dA, dCe,
+                                                         (__nv_bfloat16 *)dZ, ld_z);
+  } else {
+    if (cell == FOLD_CELL_TREELSTM)
+      k_cell_bwd_pw<float, 5><<<g, 256, 0, st>>>(PW_ARGS, (const float *)Gact, C, dA, dCe, (float *)dZ, ld_z);
+    else
+      k_cell_bwd_pw<float, 1><<<g, 256, 0, st>>>(PW_ARGS, (const float *)Gact, C, dA, dCe, (float *)dZ, ld_z);
+  }
+#undef PW_ARGS
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+fold_status launch_gemm_dA_simt(int M, int S, int gates, const float *dZ, int ld_z, const float *U, float *dA,
+                                cudaStream_t st) {
+  if (M <= 0) return FOLD_OK;
+  dim3 grid((unsigned)cdiv(2 * S, 64), (unsigned)cdiv(M, 64));
+  k_gemm_dA_simt<<<grid, 256, 0, st>>>(M, 2 * S, gates * S, dZ, ld_z, U, 2 * S, dA, 2 * S);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+fold_status launch_gemm_dU_simt(int n_cells, int nl, int S, int gates, const float *dZ, int ld_z,
+                                const int32_t *gather, const float *H, int ld, float *dU, int accumulate,
+                                cudaStream_t st) {
+  dim3 grid((unsigned)cdiv(2 * S, 64), (unsigned)cdiv(gates * S, 64));
+  k_gemm_dU_simt<<<grid, 256, 0, st>>>(n_cells, nl, S, gates * S, dZ, ld_z, gather, H, ld, dU, accumulate);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+fold_status launch_colsum(bool bf16, int n_rows, int ncols, const void *dZ, int ld_z, float *partial, int nsplit,
+                          float *db, int accumulate, cudaStream_t st) {
+  dim3 grid((unsigned)cdiv(ncols, 256), (unsigned)nsplit);
+  if (bf16) k_colsum_partial<__nv_bfloat16><<<grid, 256, 0, st>>>(n_rows, ncols, (const __nv_bfloat16 *)dZ, ld_z, nsplit, partial);
+  else k_colsum_partial<float><<<grid, 256, 0, st>>>(n_rows, ncols, (const float *)dZ, ld_z, nsplit, partial);
+  FOLD_LAUNCH_CHECK();
+  k_colsum_final<<<(unsigned)cdiv(ncols, 256), 256, 0, st>>>(ncols, nsplit, partial, db, accumulate);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+fold_status launch_embed_bwd(int S, int nl, int n_tok_segs, const int32_t *tok_seg, const int32_t *leaf_perm,
+                             const int32_t *leaf_token, const int32_t *cons_off,
+                             const int32_t *cons_edge, const int32_t *root_row, const int32_t *root_perm, int G,
+                             const float *dh_root, const float *dA, float *dE, cudaStream_t st) {
+  (void)nl;
+  if (n_tok_segs <= 0) return FOLD_OK;
+  unsigned g = grid_cap(cdiv((int64_t)n_tok_segs * 32, 256));
+  k_embed_bwd<<<g, 256, 0, st>>>(S, n_tok_segs, tok_seg, leaf_perm, leaf_token, cons_off, cons_edge, root_row,
+                                 root_perm, G, dh_root, dA, dE);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+fold_status launch_sgd(float *p, const float *g, int64_t n, float lr, cudaStream_t st) {
+  if (n <= 0) return FOLD_OK;
+  k_sgd<<<grid_cap(cdiv(n, 256)), 256, 0, st>>>(p, g, n, lr);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+fold_status launch_zero(void *p, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return FOLD_OK;
+  int64_t n = (int64_t)(bytes / 4);
+  k_zero<<<grid_cap(cdiv(n, 256)), 256, 0, st>>>((uint32_t *)p, n);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+}  // namespace fold

@@ -1,0 +1,65 @@
+// exec.cuh — declarations shared by the executor translation units.
+#pragma once
+#include "common.cuh"
+
+namespace fold {
+
+// Activation / workspace layouts (pure functions of the schedule and model).
+struct ActsLayout {
+  size_t bytes, h_off, c_off, g_off;
+  int ld;       // H, C row stride (elements)
+  int ld_g;     // G row stride (elements) = round_up(gates*S, 8)
+  int helem;    // bytes per H / G element
+};
+ActsLayout acts_layout(const fold_schedule_t *s, const fold_model *m);
+
+inline int gates_of(int cell) { return cell == FOLD_CELL_TREELSTM ? 5 : 1; }
+
+// --- SIMT / shared kernels (exec.cu)
+fold_status launch_embed_fwd(bool bf16, int r0, int r1, const int32_t *leaf_token, const float *E, int S, int ld,
+                             void *H, float *C, cudaStream_t st);
+fold_status launch_cell_fwd_simt(int cell, int r0, int r1, const int32_t *gather, int S, int ld,
+                                 const float *U, const float *b, float *H, float *C, float *Gact, int ld_g,
+                                 int nl, cudaStream_t st);
+fold_status launch_root_out(bool bf16, int G, int S, int ld, const int32_t *root_row, const void *H,
+                            const float *C, float *h_root, float *c_root, cudaStream_t st);
+fold_status launch_cell_bwd_pw(bool bf16, int cell, int r0, int r1, int nl, int S, int ld, int ld_g,
+                               const int32_t *cons_off, const int32_t *cons_edge, const int32_t *root_row,
+                               const int32_t *root_perm, int G, const float *dh_root, const float *dc_root,
+                               const int32_t *gather, const void *Gact, const float *C, const float *dA,
+                               float *dCe, void *dZ, int ld_z, cudaStream_t st);
+// dA[rows][2S] (edge-indexed, fp32) = dZ[rows][gates*S] * U[gates*S][2S]
+fold_status launch_gemm_dA_simt(int M, int S, int gates, const float *dZ, int ld_z, const float *U,
+                                float *dA, cudaStream_t st);
+// dU[gates*S][2S] (+)= sum_c dZ[c] (x) [H[gL(c)]; H[gR(c)]]
+fold_status launch_gemm_dU_simt(int n_cells, int nl, int S, int gates, const float *dZ, int ld_z,
+                                const int32_t *gather, const float *H, int ld, float *dU, int accumulate,
+                                cudaStream_t st);
+// db[j] (+)= sum_c dZ[c][j], fixed-order partials then fixed-order total
+fold_status launch_colsum(bool bf16, int n_rows, int ncols, const void *dZ, int ld_z, float *partial,
+                          int nsplit, float *db, int accumulate, cudaStream_t st);
+fold_status launch_embed_bwd(int S, int nl, int n_tok_segs, const int32_t *tok_seg, const int32_t *leaf_perm,
+                             const int32_t *leaf_token, const int32_t *cons_off,
+                             const int32_t *cons_edge, const int32_t *root_row, const int32_t *root_perm, int G,
+                             const float *dh_root, const float *dA, float *dE, cudaStream_t st);
+fold_status launch_sgd(float *p, const float *g, int64_t n, float lr, cudaStream_t st);
+fold_status launch_zero(void *p, size_t bytes, cudaStream_t st);
+
+// --- tcgen05 path (exec_tc.cu)
+struct TcWeights {  // bf16 copies made per call
+  __nv_bfloat16 *U;   // [gates*S][ld_u]  (ld_u = round_up(2S, 8)), canonical row order
+  __nv_bfloat16 *Ut;  // [2S][ld_ut]      (ld_ut = round_up(gates*S, 8)) = U^T
+  int ld_u, ld_ut;
+};
+fold_status tc_prepare_U(int gates, int S, const float *U, TcWeights &w, bool transpose, cudaStream_t st);
+fold_status tc_cell_fwd(int cell, int r0, int r1, int nl, const int32_t *gather, int S, int ld,
+                        const TcWeights &w, const float *b, __nv_bfloat16 *H, int n_rows_total, float *C,
+                        __nv_bfloat16 *Gact, int ld_g, cudaStream_t st);
+fold_status tc_gemm_dA(int c0, int M, int n_cells, int S, int gates, const __nv_bfloat16 *dZ, int ld_z,
+                       const TcWeights &w, float *dA, cudaStream_t st);
+fold_status tc_gemm_dU(int n_cells, int nl, int S, int gates, const __nv_bfloat16 *dZ, int ld_z,
+                       const int32_t *gather, const __nv_bfloat16 *H, int ld, int n_rows_total, float *dU,
+                       int accumulate, cudaStream_t st);
+size_t tc_workspace_bytes(int gates, int S);
+
+}  // namespace fold

@@ -1,0 +1,554 @@
+// exec_tc.cu — tcgen05 (5th-gen tensor core) kernels for the BF16 path.
+//
+//  k_cell_fwd_tc   one level of the forward (gather -> operation -> concat)
+//                  fused in one kernel: TMA tile::gather4 pulls the child rows
+//                  [H[gL] | H[gR]] of 128 pool rows straight into 128B-swizzled smem
+//                  (the gather), tcgen05.mma multiplies them with a gate-interleaved
+//                  slab of U into a TMEM accumulator (the batched cell), and the epilogue
+//                  warps apply the gates and write the level's contiguous pool rows
+//                  (the concat becomes an append).
+//  k_gemm_dA_tc    backward edge gradients of one level: dA = dZ_level * U  (K-major).
+//  k_gemm_dU_tc    weight gradient over all cells at once: dU = dZ^T * [H[gL] | H[gR]],
+//                  both operands MN-major, the H operand row-gathered by TMA.
+// Warp roles (256 threads): warp 0 TMA producer, warp 1 MMA issuer (one lane),
+// warp 2 TMEM allocator, warps 4-7 epilogue (warp w reads TMEM lanes 32(w%4)..+31).
+#include <cudaTypedefs.h>
+
+#include "exec.cuh"
+#include "ptx.cuh"
+
+namespace fold {
+
+namespace {
+
+constexpr int BM = 128;     // rows per tile (UMMA M)
+constexpr int BK = 64;      // K elements per stage (128 B of bf16 = one swizzle row)
+constexpr int ST = 4;       // pipeline stages
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
+  return (uint8_t *)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
+}
+
+constexpr int tmem_cols_for(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t *>(&v);
+}
+
+// =================================================================== forward cell level
+template <int GATES, int W>
+struct FwdCfg {
+  static constexpr int N = GATES * W;
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int B_BYTES = N * 128;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = tmem_cols_for(N);
+  static constexpr int SMEM = ST * STAGE + 1024;
+  static_assert(N % 16 == 0 && N <= 256, "UMMA N for M=128");
+  static_assert(W % 8 == 0, "gate slab rows must fill 8-row swizzle atoms");
+};
+
+template <int GATES, int W>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_cell_fwd_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmU, int r0, int r1,
+                  int nl, int S, int ld, int KBh, const int32_t *__restrict__ gather, const float *__restrict__ bias,
+                  __nv_bfloat16 *__restrict__ H, float *__restrict__ C, __nv_bfloat16 *__restrict__ Gact, int ld_g) {
+  using Cfg = FwdCfg<GATES, W>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = align1024(smem_raw);
+  __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ int gidx[2][BM];
+  __shared__ float sbias[GATES * W];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m0 = r0 + blockIdx.x * BM, j0 = blockIdx.y * W;
+
+  if (tid < BM) {
+    int r = m0 + tid;
+    int rr = r < r1 ? r : r0;
+    gidx[0][tid] = gather[2 * (int64_t)rr];
+    gidx[1][tid] = gather[2 * (int64_t)rr + 1];
+  }
+  for (int i = tid; i < GATES * W; i += kThreads) {
+    int g = i / W, j = j0 + (i - g * W);
+    sbias[i] = j < S ? bias[g * S + j] : 0.f;
+  }
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < ST; s++) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    ptx::mbar_init(&tfull, 1);
+    ptx::fence_mbar_init();
+    ptx::prefetch_tmap(&tmH);
+    ptx::prefetch_tmap(&tmU);
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc(&tmem_base_sh, Cfg::TMEM_COLS);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = tmem_base_sh;
+  const int KB = 2 * KBh;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < KB; kb++) {
+        int s = kb % ST;
+        uint32_t ph = (kb / ST) & 1;
+        ptx::mbar_wait(&empty[s], ph ^ 1);
+        ptx::mbar_arrive_expect_tx(&full[s], Cfg::STAGE);
+        int half = kb >= KBh;
+        int kc = (kb - half * KBh) * BK;
+        uint8_t *A = smem + s * Cfg::STAGE;
+        uint8_t *B = A + Cfg::A_BYTES;
+        const int *gi = gidx[half];
+#pragma unroll 4
+        for (int q = 0; q < BM / 4; q++)
+          ptx::tma_gather4(&tmH, &full[s], A + q * 512, kc, gi[4 * q], gi[4 * q + 1], gi[4 * q + 2], gi[4 * q + 3]);
+#pragma unroll
+        for (int g = 0; g < GATES; g++) ptx::tma_load_2d(&tmU, &full[s], B + g * W * 128, half * S + kc, g * S + j0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16(BM, Cfg::N, 0, 0);
+      for (int kb = 0; kb < KB; kb++) {
+        int s = kb % ST;
+        uint32_t ph = (kb / ST) & 1;
+        ptx::mbar_wait(&full[s], ph);
+        ptx::tc_fence_after();
+        uint32_t a0 = ptx::smem_u32(smem + s * Cfg::STAGE), b0 = a0 + Cfg::A_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / 16; k++)
+          ptx::umma_bf16(tbase, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024), ptx::sdesc_sw128(b0 + 32 * k, 16, 1024),
+                         idesc, (kb | k) != 0);
+        ptx::umma_commit(&empty[s]);
+      }
+      ptx::umma_commit(&tfull);
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    ptx::mbar_wait(&tfull, 0);
+    ptx::tc_fence_after();
+    const int row = q * 32 + lane;
+    const int64_t r = m0 + row;
+    const bool valid = r < r1;
+    const int64_t gl = gidx[0][row], gr = gidx[1][row];
+    const int64_t c = r - nl;
+    const uint32_t tl = tbase + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+    for (int jc = 0; jc < W / 8; jc++) {
+      float z[GATES][8];
+#pragma unroll
+      for (int g = 0; g < GATES; g++) ptx::tmem_ld8(tl + g * W + jc * 8, z[g]);
+      ptx::tmem_ld_wait();
+      if (!valid) continue;
+      const int jb = j0 + jc * 8;
+      if (jb >= S) continue;
+      const bool fullc = (jb + 8 <= S) && ((S & 7) == 0);
+      if constexpr (GATES == 1) {
+        float h[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) h[u] = tanhf(z[0][u] + sbias[jc * 8 + u]);
+        if (fullc) {
+          uint4 pk = make_uint4(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]), pack_bf16x2(h[4], h[5]),
+                                pack_bf16x2(h[6], h[7]));
+          *reinterpret_cast<uint4 *>(H + r * ld + jb) = pk;
+          *reinterpret_cast<uint4 *>(Gact + c * ld_g + jb) = pk;
+          *reinterpret_cast<float4 *>(C + r * ld + jb) = make_float4(0.f, 0.f, 0.f, 0.f);
+          *reinterpret_cast<float4 *>(C + r * ld + jb + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+          for (int u = 0; u < 8 && jb + u < S; u++) {
+            H[r * ld + jb + u] = __float2bfloat16_rn(h[u]);
+            Gact[c * ld_g + jb + u] = __float2bfloat16_rn(h[u]);
+            C[r * ld + jb + u] = 0.f;
+          }
+        }
+      } else {
+        float cl[8], cr[8];
+        if (fullc) {
+          float4 a = *reinterpret_cast<const float4 *>(C + gl * ld + jb);
+          float4 b = *reinterpret_cast<const float4 *>(C + gl * ld + jb + 4);
+          cl[0] = a.x; cl[1] = a.y; cl[2] = a.z; cl[3] = a.w; cl[4] = b.x; cl[5] = b.y; cl[6] = b.z; cl[7] = b.w;
+          a = *reinterpret_cast<const float4 *>(C + gr * ld + jb);
+          b = *reinterpret_cast<const float4 *>(C + gr * ld + jb + 4);
+          cr[0] = a.x; cr[1] = a.y; cr[2] = a.z; cr[3] = a.w; cr[4] = b.x; cr[5] = b.y; cr[6] = b.z; cr[7] = b.w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            bool ok = jb + u < S;
+            cl[u] = ok ? C[gl * ld + jb + u] : 0.f;
+            cr[u] = ok ? C[gr * ld + jb + u] : 0.f;
+          }
+        }
+        float gi[8], gfl[8], gfr[8], go[8], gu[8], hh[8], cc[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+          const int jj = jc * 8 + u;
+          gi[u] = sigmoidf_(z[0][u] + sbias[jj]);
+          gfl[u] = sigmoidf_(z[1][u] + sbias[W + jj]);
+          gfr[u] = sigmoidf_(z[2][u] + sbias[2 * W + jj]);
+          go[u] = sigmoidf_(z[3][u] + sbias[3 * W + jj]);
+          gu[u] = tanhf(z[4][u] + sbias[4 * W + jj]);
+          cc[u] = gi[u] * gu[u] + gfl[u] * cl[u] + gfr[u] * cr[u];
+          hh[u] = go[u] * tanhf(cc[u]);
+        }
+        __nv_bfloat16 *ga = Gact + c * ld_g;
+        if (fullc) {
+          *reinterpret_cast<uint4 *>(H + r * ld + jb) = make_uint4(
+              pack_bf16x2(hh[0], hh[1]), pack_bf16x2(hh[2], hh[3]), pack_bf16x2(hh[4], hh[5]), pack_bf16x2(hh[6], hh[7]));
+          *reinterpret_cast<float4 *>(C + r * ld + jb) = make_float4(cc[0], cc[1], cc[2], cc[3]);
+          *reinterpret_cast<float4 *>(C + r * ld + jb + 4) = make_float4(cc[4], cc[5], cc[6], cc[7]);
+          float *gs[5] = {gi, gfl, gfr, go, gu};
+#pragma unroll
+          for (int g = 0; g < 5; g++)
+            *reinterpret_cast<uint4 *>(ga + g * S + jb) =
+                make_uint4(pack_bf16x2(gs[g][0], gs[g][1]), pack_bf16x2(gs[g][2], gs[g][3]),
+                           pack_bf16x2(gs[g][4], gs[g][5]), pack_bf16x2(gs[g][6], gs[g][7]));
+        } else {
+          for (int u = 0; u < 8 && jb + u < S; u++) {
+            int j = jb + u;
+            H[r * ld + j] = __float2bfloat16_rn(hh[u]);
+            C[r * ld + j] = cc[u];
+            ga[j] = __float2bfloat16_rn(gi[u]);
+            ga[S + j] = __float2bfloat16_rn(gfl[u]);
+            ga[2 * S + j] = __float2bfloat16_rn(gfr[u]);
+            ga[3 * S + j] = __float2bfloat16_rn(go[u]);
+            ga[4 * S + j] = __float2bfloat16_rn(gu[u]);
+          }
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tbase, Cfg::TMEM_COLS);
+  }
+}
+
+// =================================================================== dA = dZ * U (one level)
+constexpr int DA_N = 256;
+constexpr int DA_A_BYTES = BM * 128, DA_B_BYTES = DA_N * 128, DA_STAGE = DA_A_BYTES + DA_B_BYTES;
+constexpr int DA_SMEM = ST * DA_STAGE + 1024;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_dA_tc(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmUt, int c0, int M,
+                 int KB, int S, float *__restrict__ dA) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = align1024(smem_raw);
+  __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull;
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int mt = c0 + blockIdx.y * BM, n0 = blockIdx.x * DA_N;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < ST; s++) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    ptx::mbar_init(&tfull, 1);
+    ptx::fence_mbar_init();
+    ptx::prefetch_tmap(&tmZ);
+    ptx::prefetch_tmap(&tmUt);
+  }
+  if (warp == 2) { ptx::tmem_alloc(&tmem_base_sh, 256); ptx::tmem_relinquish(); }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = tmem_base_sh;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < KB; kb++) {
+        int s = kb % ST;
+        uint32_t ph = (kb / ST) & 1;
+        ptx::mbar_wait(&empty[s], ph ^ 1);
+        ptx::mbar_arrive_expect_tx(&full[s], DA_STAGE);
+        uint8_t *A = smem + s * DA_STAGE;
+        ptx::tma_load_2d(&tmZ, &full[s], A, kb * BK, mt);
+        ptx::tma_load_2d(&tmUt, &full[s], A + DA_A_BYTES, kb * BK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16(BM, DA_N, 0, 0);
+      for (int kb = 0; kb < KB; kb++) {
+        int s = kb % ST;
+        uint32_t ph = (kb / ST) & 1;
+        ptx::mbar_wait(&full[s], ph);
+        ptx::tc_fence_after();
+        uint32_t a0 = ptx::smem_u32(smem + s * DA_STAGE), b0 = a0 + DA_A_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / 16; k++)
+          ptx::umma_bf16(tbase, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024), ptx::sdesc_sw128(b0 + 32 * k, 16, 1024),
+                         idesc, (kb | k) != 0);
+        ptx::umma_commit(&empty[s]);
+      }
+      ptx::umma_commit(&tfull);
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    ptx::mbar_wait(&tfull, 0);
+    ptx::tc_fence_after();
+    const int row = q * 32 + lane;
+    const int64_t c = mt + row;
+    const bool valid = (c - c0) < M;
+    const int N2 = 2 * S;
+    const uint32_t tl = tbase + ((uint32_t)(q * 32) << 16);
+    float *out = dA + c * N2;
+#pragma unroll 1
+    for (int nc = 0; nc < DA_N / 8; nc++) {
+      float v[8];
+      ptx::tmem_ld8(tl + nc * 8, v);
+      ptx::tmem_ld_wait();
+      int n = n0 + nc * 8;
+      if (!valid || n >= N2) continue;
+      if (n + 8 <= N2 && (N2 & 3) == 0) {
+        *reinterpret_cast<float4 *>(out + n) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4 *>(out + n + 4) = make_float4(v[4], v[5], v[6], v[7]);
+      } else {
+        for (int u = 0; u < 8 && n + u < N2; u++) out[n + u] = v[u];
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc(tbase, 256); }
+}
+
+// =================================================================== dU = dZ^T * Acat (all cells)
+constexpr int DU_N = 256;
+constexpr int DU_A_BYTES = BM * 128;     // 2 MN chunks x 64 K-rows x 128 B
+constexpr int DU_B_BYTES = DU_N * 128;   // 4 MN chunks x 64 K-rows x 128 B
+constexpr int DU_STAGE = DU_A_BYTES + DU_B_BYTES;
+constexpr int DU_SMEM = ST * DU_STAGE + 1024;
+constexpr int MN_CHUNK = 64 * 128;       // bytes per 64-element MN chunk of 64 K rows
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_dU_tc(const __grid_constant__ CUtensorMap tmZ2, const __grid_constant__ CUtensorMap tmH, int n_cells,
+                 int nl, int S, int Mg, int NT, const int32_t *__restrict__ gather, float *__restrict__ dU,
+                 int accumulate) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = align1024(smem_raw);
+  __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull;
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int half = blockIdx.x / NT, jt = blockIdx.x - half * NT;
+  const int i0 = blockIdx.y * BM, jn0 = jt * DU_N;
+  const int KB = (int)cdiv(n_cells, BK);
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < ST; s++) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    ptx::mbar_init(&tfull, 1);
+    ptx::fence_mbar_init();
+    ptx::prefetch_tmap(&tmZ2);
+    ptx::prefetch_tmap(&tmH);
+  }
+  if (warp == 2) { ptx::tmem_alloc(&tmem_base_sh, 256); ptx::tmem_relinquish(); }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = tmem_base_sh;
+  if (warp == 0) {
+    // whole warp: lanes 0..15 each gather 4 cells (rows) for the 4 MN chunks of B
+    int nxt_rows[4];
+    auto load_rows = [&](int kb, int (&rows)[4]) {
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        int cidx = kb * BK + 4 * (lane & 15) + u;
+        rows[u] = cidx < n_cells ? gather[2 * ((int64_t)nl + cidx) + half] : 0;
+      }
+    };
+    load_rows(0, nxt_rows);
+    for (int kb = 0; kb < KB; kb++) {
+      int rows[4] = {nxt_rows[0], nxt_rows[1], nxt_rows[2], nxt_rows[3]};
+      if (kb + 1 < KB) load_rows(kb + 1, nxt_rows);
+      int s = kb % ST;
+      uint32_t ph = (kb / ST) & 1;
+      if (lane == 0) {
+        ptx::mbar_wait(&empty[s], ph ^ 1);
+        ptx::mbar_arrive_expect_tx(&full[s], DU_STAGE);
+      }
+      __syncwarp();
+      uint8_t *A = smem + s * DU_STAGE;
+      uint8_t *B = A + DU_A_BYTES;
+      if (lane == 0) {
+        ptx::tma_load_2d(&tmZ2, &full[s], A, i0, kb * BK);
+        ptx::tma_load_2d(&tmZ2, &full[s], A + MN_CHUNK, i0 + 64, kb * BK);
+      }
+      if (lane < 16) {
+#pragma unroll
+        for (int ch = 0; ch < 4; ch++)
+          ptx::tma_gather4(&tmH, &full[s], B + ch * MN_CHUNK + lane * 512, jn0 + ch * 64, rows[0], rows[1], rows[2],
+                           rows[3]);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16(BM, DU_N, 1, 1);
+      for (int kb = 0; kb < KB; kb++) {
+        int s = kb % ST;
+        uint32_t ph = (kb / ST) & 1;
+        ptx::mbar_wait(&full[s], ph);
+        ptx::tc_fence_after();
+        uint32_t a0 = ptx::smem_u32(smem + s * DU_STAGE), b0 = a0 + DU_A_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / 16; k++)
+          ptx::umma_bf16(tbase, ptx::sdesc_sw128(a0 + 2048 * k, MN_CHUNK, 1024),
+                         ptx::sdesc_sw128(b0 + 2048 * k, MN_CHUNK, 1024), idesc, (kb | k) != 0);
+        ptx::umma_commit(&empty[s]);
+      }
+      ptx::umma_commit(&tfull);
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    ptx::mbar_wait(&tfull, 0);
+    ptx::tc_fence_after();
+    const int i = i0 + q * 32 + lane;
+    const bool valid = i < Mg && KB > 0;
+    const uint32_t tl = tbase + ((uint32_t)(q * 32) << 16);
+    float *out = dU + (int64_t)i * 2 * S + half * S;
+#pragma unroll 1
+    for (int nc = 0; nc < DU_N / 8; nc++) {
+      float v[8];
+      ptx::tmem_ld8(tl + nc * 8, v);
+      ptx::tmem_ld_wait();
+      int j = jn0 + nc * 8;
+      if (i >= Mg || j >= S) continue;
+      for (int u = 0; u < 8 && j + u < S; u++) {
+        float x = valid ? v[u] : 0.f;
+        out[j + u] = accumulate ? out[j + u] + x : x;
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc(tbase, 256); }
+}
+
+// =================================================================== weight prep
+// Ubf[r][k] = bf16(U[r][k]) (ld_u); Ut[k][r] = bf16(U[r][k]) (ld_ut). 32x32 smem tiles.
+__global__ void k_prep_U(int R, int K, const float *__restrict__ U, __nv_bfloat16 *__restrict__ Ubf, int ld_u,
+                         __nv_bfloat16 *__restrict__ Ut, int ld_ut) {
+  __shared__ float t[32][33];
+  int r0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
+  int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: ty 0..7
+  for (int i = ty; i < 32; i += 8) {
+    int r = r0 + i, k = k0 + tx;
+    float v = (r < R && k < K) ? U[(int64_t)r * K + k] : 0.f;
+    t[i][tx] = v;
+    if (r < R && k < K) Ubf[(int64_t)r * ld_u + k] = __float2bfloat16_rn(v);
+  }
+  if (!Ut) return;
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    int k = k0 + i, r = r0 + tx;
+    if (r < R && k < K) Ut[(int64_t)k * ld_ut + r] = __float2bfloat16_rn(t[tx][i]);
+  }
+}
+
+// =================================================================== host helpers
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+// 2D bf16 tensor map: `cols` contiguous elements per row, `rows` rows, `row_bytes` stride.
+fold_status make_map(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t rows, uint64_t row_bytes,
+                     uint32_t box_cols, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return FOLD_E_CUDA;
+  if (rows < 1) rows = 1;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? FOLD_OK : FOLD_E_CUDA;
+}
+
+template <typename K>
+fold_status set_smem(K kernel, int bytes) {
+  FOLD_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  return FOLD_OK;
+}
+
+template <int GATES, int W>
+fold_status launch_fwd(int r0, int r1, int nl, const int32_t *gather, int S, int ld, const TcWeights &w,
+                       const float *b, __nv_bfloat16 *H, int n_rows_total, float *C, __nv_bfloat16 *Gact, int ld_g,
+                       cudaStream_t st) {
+  using Cfg = FwdCfg<GATES, W>;
+  CUtensorMap tmH, tmU;
+  FOLD_TRY(make_map(&tmH, H, (uint64_t)S, (uint64_t)n_rows_total, (uint64_t)ld * 2, BK, 1));
+  FOLD_TRY(make_map(&tmU, w.U, (uint64_t)2 * S, (uint64_t)GATES * S, (uint64_t)w.ld_u * 2, BK, W));
+  auto kern = k_cell_fwd_tc<GATES, W>;
+  FOLD_TRY(set_smem(kern, Cfg::SMEM));
+  dim3 grid((unsigned)cdiv(r1 - r0, BM), (unsigned)cdiv(S, W));
+  int KBh = (int)cdiv(S, BK);
+  kern<<<grid, kThreads, Cfg::SMEM, st>>>(tmH, tmU, r0, r1, nl, S, ld, KBh, gather, b, H, C, Gact, ld_g);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+}  // namespace
+
+size_t tc_workspace_bytes(int gates, int S) {
+  size_t ld_u = round_up(2 * S, 8), ld_ut = round_up((int64_t)gates * S, 8);
+  return round_up((int64_t)gates * S * ld_u * 2, 256) + round_up((int64_t)2 * S * ld_ut * 2, 256);
+}
+
+fold_status tc_prepare_U(int gates, int S, const float *U, TcWeights &w, bool transpose, cudaStream_t st) {
+  int R = gates * S, K = 2 * S;
+  dim3 grid((unsigned)cdiv(K, 32), (unsigned)cdiv(R, 32));
+  k_prep_U<<<grid, 256, 0, st>>>(R, K, U, w.U, w.ld_u, transpose ? w.Ut : nullptr, w.ld_ut);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+fold_status tc_cell_fwd(int cell, int r0, int r1, int nl, const int32_t *gather, int S, int ld, const TcWeights &w,
+                        const float *b, __nv_bfloat16 *H, int n_rows_total, float *C, __nv_bfloat16 *Gact, int ld_g,
+                        cudaStream_t st) {
+  if (r1 <= r0) return FOLD_OK;
+  if (cell == FOLD_CELL_TREELSTM)
+    return launch_fwd<5, 32>(r0, r1, nl, gather, S, ld, w, b, H, n_rows_total, C, Gact, ld_g, st);
+  return launch_fwd<1, 128>(r0, r1, nl, gather, S, ld, w, b, H, n_rows_total, C, Gact, ld_g, st);
+}
+
+fold_status tc_gemm_dA(int c0, int M, int n_cells, int S, int gates, const __nv_bfloat16 *dZ, int ld_z,
+                       const TcWeights &w, float *dA, cudaStream_t st) {
+  if (M <= 0) return FOLD_OK;
+  CUtensorMap tmZ, tmUt;
+  FOLD_TRY(make_map(&tmZ, dZ, (uint64_t)gates * S, (uint64_t)n_cells, (uint64_t)ld_z * 2, BK, BM));
+  FOLD_TRY(make_map(&tmUt, w.Ut, (uint64_t)gates * S, (uint64_t)2 * S, (uint64_t)w.ld_ut * 2, BK, DA_N));
+  FOLD_TRY(set_smem(k_gemm_dA_tc, DA_SMEM));
+  dim3 grid((unsigned)cdiv(2 * S, DA_N), (unsigned)cdiv(M, BM));
+  int KB = (int)cdiv(gates * S, BK);
+  k_gemm_dA_tc<<<grid, kThreads, DA_SMEM, st>>>(tmZ, tmUt, c0, M, KB, S, dA);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+fold_status tc_gemm_dU(int n_cells, int nl, int S, int gates, const __nv_bfloat16 *dZ, int ld_z, const int32_t *gather,
+                       const __nv_bfloat16 *H, int ld, int n_rows_total, float *dU, int accumulate, cudaStream_t st) {
+  CUtensorMap tmZ2, tmH;
+  FOLD_TRY(make_map(&tmZ2, dZ, (uint64_t)gates * S, (uint64_t)(n_cells > 0 ? n_cells : 1), (uint64_t)ld_z * 2, 64, BK));
+  FOLD_TRY(make_map(&tmH, H, (uint64_t)S, (uint64_t)n_rows_total, (uint64_t)ld * 2, 64, 1));
+  FOLD_TRY(set_smem(k_gemm_dU_tc, DU_SMEM));
+  int NT = (int)cdiv(S, DU_N);
+  dim3 grid((unsigned)(2 * NT), (unsigned)cdiv(gates * S, BM));
+  k_gemm_dU_tc<<<grid, kThreads, DU_SMEM, st>>>(tmZ2, tmH, n_cells, nl, S, gates * S, NT, gather, dU, accumulate);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+}  // namespace fold

@@ -1,0 +1,303 @@
+"""Thin Python binding over libfold.so (include/fold.h) — argument marshalling only.
+
+Every step of the hot path (schedule, forward, backward, SGD) runs in the library's
+CUDA kernels; PyTorch supplies device memory (torch.empty on cuda) and the stream.
+There is no CPU fallback: if libfold.so is missing or the device is not sm_100,
+the calls raise.
+
+    sched = schedule(op, child, token, root, vocab)            # fold_schedule
+    h_root, c_root, acts = forward(sched, model)               # fold_forward
+    dU, db, dE = backward(sched, model, acts, dh_root)         # fold_backward
+    sgd_update(param, grad, lr)                                # fold_sgd_update
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+
+import numpy as np
+import torch
+
+from . import build as _build
+
+OK = 0
+STATUS = {0: "OK", 1: "INVALID", 2: "CHILD_RANGE", 3: "ARITY", 4: "TOKEN_RANGE", 5: "ROOT_RANGE",
+          6: "CYCLE", 7: "WORKSPACE", 8: "CUDA", 9: "MISMATCH", 10: "OP_RANGE", 11: "UNSUPPORTED"}
+CELLS = {"treernn": 0, "treelstm": 1}
+PRECS = {"fp32": 0, "bf16": 2}
+
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_f32p = ctypes.POINTER(ctypes.c_float)
+
+
+class _Graphs(ctypes.Structure):
+    _fields_ = [("n_nodes", ctypes.c_int32), ("n_graphs", ctypes.c_int32), ("vocab", ctypes.c_int32),
+                ("op", ctypes.c_void_p), ("child", ctypes.c_void_p), ("token", ctypes.c_void_p),
+                ("root", ctypes.c_void_p)]
+
+
+_SCHED_ARRAYS = ("depth", "perm", "rank", "gather", "level_off", "group_off", "cons_off", "cons_edge",
+                 "leaf_perm", "tok_seg", "root_row", "root_perm", "leaf_token")
+
+
+class _Sched(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_void_p) for k in _SCHED_ARRAYS] + [
+        ("level_off_host", ctypes.c_void_p),
+        ("n_nodes", ctypes.c_int32), ("n_graphs", ctypes.c_int32), ("n_levels", ctypes.c_int32),
+        ("n_leaves", ctypes.c_int32), ("n_cells", ctypes.c_int32), ("n_tok_segs", ctypes.c_int32)]
+
+
+class _Model(ctypes.Structure):
+    _fields_ = [("cell", ctypes.c_int32), ("prec", ctypes.c_int32), ("S", ctypes.c_int32),
+                ("vocab", ctypes.c_int32), ("U", ctypes.c_void_p), ("b", ctypes.c_void_p),
+                ("E", ctypes.c_void_p)]
+
+
+class _ActsLayout(ctypes.Structure):
+    _fields_ = [("bytes", ctypes.c_size_t), ("h_off", ctypes.c_size_t), ("c_off", ctypes.c_size_t),
+                ("g_off", ctypes.c_size_t), ("ld", ctypes.c_int32), ("h_elem_bytes", ctypes.c_int32)]
+
+
+class _Grads(ctypes.Structure):
+    _fields_ = [("dU", ctypes.c_void_p), ("db", ctypes.c_void_p), ("dE", ctypes.c_void_p),
+                ("accumulate", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _build.LIB_PATH
+
+
+def load() -> ctypes.CDLL:
+    """Load libfold.so (built by __graft_entry__.build() / `python -m paper_1702_02181_b200.build`)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_build.LIB_PATH):
+        raise ImportError(f"libfold.so not built at {_build.LIB_PATH}; run `python -m paper_1702_02181_b200.build`")
+    L = ctypes.CDLL(_build.LIB_PATH)
+    vp, sz, i32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int32
+    L.fold_schedule_workspace.restype = sz
+    L.fold_schedule_workspace.argtypes = [i32, i32]
+    L.fold_schedule.restype = i32
+    L.fold_schedule.argtypes = [ctypes.POINTER(_Graphs), ctypes.POINTER(_Sched), vp, sz, vp]
+    L.fold_acts_layout.restype = i32
+    L.fold_acts_layout.argtypes = [ctypes.POINTER(_Sched), ctypes.POINTER(_Model), ctypes.POINTER(_ActsLayout)]
+    L.fold_forward_workspace.restype = sz
+    L.fold_forward_workspace.argtypes = [ctypes.POINTER(_Sched), ctypes.POINTER(_Model)]
+    L.fold_forward.restype = i32
+    L.fold_forward.argtypes = [ctypes.POINTER(_Sched), ctypes.POINTER(_Model), vp, vp, vp, vp, sz, vp]
+    L.fold_backward_workspace.restype = sz
+    L.fold_backward_workspace.argtypes = [ctypes.POINTER(_Sched), ctypes.POINTER(_Model)]
+    L.fold_backward.restype = i32
+    L.fold_backward.argtypes = [ctypes.POINTER(_Sched), ctypes.POINTER(_Model), vp, vp, vp,
+                                ctypes.POINTER(_Grads), vp, sz, vp]
+    L.fold_sgd_update.restype = i32
+    L.fold_sgd_update.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_float, vp]
+    L.fold_status_string.restype = ctypes.c_char_p
+    L.fold_status_string.argtypes = [i32]
+    L.fold_last_error_detail.restype = i32
+    L.fold_abi_version.restype = i32
+    L.fold_device_check.restype = i32
+    L.fold_launch_count.restype = ctypes.c_int64
+    L.fold_launch_count.argtypes = [i32]
+    _lib = L
+    return L
+
+
+EXPORTED = ("fold_schedule_workspace", "fold_schedule", "fold_acts_layout", "fold_forward_workspace",
+            "fold_forward", "fold_backward_workspace", "fold_backward", "fold_sgd_update",
+            "fold_status_string", "fold_last_error_detail", "fold_abi_version", "fold_device_check",
+            "fold_launch_count")
+
+
+class FoldError(RuntimeError):
+    def __init__(self, status: int, what: str, detail: int = -1):
+        super().__init__(f"{what}: FOLD_E_{STATUS.get(status, status)} (detail {detail})")
+        self.status = STATUS.get(status, status)
+        self.detail = detail
+
+
+def _check(st: int, what: str):
+    if st != OK:
+        raise FoldError(st, what, load().fold_last_error_detail())
+
+
+def _ptr(t: torch.Tensor | None):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def device_check():
+    _check(load().fold_device_check(), "fold_device_check")
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(load().fold_launch_count(1 if reset else 0))
+
+
+# ----------------------------------------------------------------------------- schedule
+
+@dataclasses.dataclass
+class Schedule:
+    """Device arrays of the executor-form schedule (fold.h) + host scalars."""
+    arrays: dict
+    level_off_host: np.ndarray
+    n_nodes: int
+    n_graphs: int
+    n_levels: int
+    n_leaves: int
+    n_cells: int
+    n_tok_segs: int
+    _struct: _Sched = None
+    _host_buf: np.ndarray = None
+
+    def struct(self) -> _Sched:
+        return self._struct
+
+    def to_numpy(self) -> dict:
+        """Logical-length host copies (for tests): same keys/lengths as oracle.schedule."""
+        a = {k: v.cpu().numpy() for k, v in self.arrays.items()}
+        N, D = self.n_nodes, self.n_levels
+        out = {"depth": a["depth"][:N], "perm": a["perm"][:N], "rank": a["rank"][:N],
+               "gather": a["gather"][:2 * N].reshape(N, 2), "level_off": a["level_off"][:D + 2],
+               "group_off": a["group_off"][:2 * (D + 1) + 1], "cons_off": a["cons_off"][:N + 1],
+               "cons_edge": a["cons_edge"][:2 * self.n_cells], "leaf_perm": a["leaf_perm"][:self.n_leaves],
+               "tok_seg": a["tok_seg"][:self.n_tok_segs + 1], "root_row": a["root_row"][:self.n_graphs],
+               "root_perm": a["root_perm"][:self.n_graphs], "leaf_token": a["leaf_token"][:self.n_leaves],
+               "n_levels": D, "n_leaves": self.n_leaves, "n_cells": self.n_cells,
+               "n_tok_segs": self.n_tok_segs}
+        return out
+
+
+def schedule(op: torch.Tensor, child: torch.Tensor, token: torch.Tensor, root: torch.Tensor, vocab: int,
+             stream=None, workspace: torch.Tensor | None = None) -> Schedule:
+    """fold_schedule over int32 device tensors op[N], child[N,2], token[N], root[G]."""
+    L = load()
+    dev = op.device
+    N, G = int(op.shape[0]), int(root.shape[0])
+    for t in (op, child, token, root):
+        assert t.dtype == torch.int32 and t.is_cuda and t.is_contiguous()
+    sizes = {"depth": N, "perm": N, "rank": N, "gather": 2 * N, "level_off": N + 2, "group_off": 2 * N + 3,
+             "cons_off": N + 1, "cons_edge": 2 * N, "leaf_perm": N, "tok_seg": N + 1, "root_row": G,
+             "root_perm": G, "leaf_token": N}
+    arrays = {k: torch.empty(max(n, 1), dtype=torch.int32, device=dev) for k, n in sizes.items()}
+    host = np.zeros(N + 2, np.int32)
+    ws_bytes = int(L.fold_schedule_workspace(N, G))
+    if workspace is None or workspace.numel() < ws_bytes:
+        workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    g = _Graphs(N, G, int(vocab), op.data_ptr(), child.data_ptr(), token.data_ptr(), root.data_ptr())
+    s = _Sched(*[arrays[k].data_ptr() for k in _SCHED_ARRAYS], host.ctypes.data, 0, 0, 0, 0, 0, 0)
+    _check(L.fold_schedule(ctypes.byref(g), ctypes.byref(s), ctypes.c_void_p(workspace.data_ptr()),
+                           ws_bytes, _stream(stream)), "fold_schedule")
+    return Schedule(arrays, host, s.n_nodes, s.n_graphs, s.n_levels, s.n_leaves, s.n_cells, s.n_tok_segs,
+                    _struct=s, _host_buf=host)
+
+
+# ----------------------------------------------------------------------------- model / acts
+
+@dataclasses.dataclass
+class Model:
+    U: torch.Tensor   # [gates*S, 2S] fp32
+    b: torch.Tensor   # [gates*S] fp32
+    E: torch.Tensor   # [V, S] fp32
+    cell: str = "treelstm"
+    prec: str = "bf16"
+
+    @property
+    def S(self) -> int:
+        return int(self.E.shape[1])
+
+    def struct(self) -> _Model:
+        for t in (self.U, self.b, self.E):
+            assert t.dtype == torch.float32 and t.is_cuda and t.is_contiguous()
+        return _Model(CELLS[self.cell], PRECS[self.prec], self.S, int(self.E.shape[0]),
+                      self.U.data_ptr(), self.b.data_ptr(), self.E.data_ptr())
+
+
+@dataclasses.dataclass
+class Acts:
+    buf: torch.Tensor
+    layout: _ActsLayout
+
+    def views(self, sched: Schedule, model: Model):
+        """(H [N, ld], C [N, ld]) views into the activation buffer (pool-row order)."""
+        N = sched.n_nodes
+        lay = self.layout
+        hdt = torch.bfloat16 if lay.h_elem_bytes == 2 else torch.float32
+        H = self.buf[lay.h_off: lay.h_off + N * lay.ld * lay.h_elem_bytes].view(hdt).view(N, lay.ld)
+        C = self.buf[lay.c_off: lay.c_off + N * lay.ld * 4].view(torch.float32).view(N, lay.ld)
+        return H, C
+
+
+class Workspace:
+    """Reusable device scratch (grown on demand) so repeated steps do not re-allocate."""
+
+    def __init__(self, device):
+        self.device = device
+        self.bufs = {}
+
+    def get(self, name: str, nbytes: int) -> torch.Tensor:
+        t = self.bufs.get(name)
+        if t is None or t.numel() < nbytes:
+            t = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=self.device)
+            self.bufs[name] = t
+        return t
+
+
+def forward(sched: Schedule, model: Model, stream=None, ws: Workspace | None = None,
+            want_c: bool = True):
+    L = load()
+    dev = model.E.device
+    ms = model.struct()
+    lay = _ActsLayout()
+    _check(L.fold_acts_layout(ctypes.byref(sched.struct()), ctypes.byref(ms), ctypes.byref(lay)), "fold_acts_layout")
+    ws = ws or Workspace(dev)
+    acts_buf = ws.get("acts", lay.bytes)
+    fws = int(L.fold_forward_workspace(ctypes.byref(sched.struct()), ctypes.byref(ms)))
+    fbuf = ws.get("fwd", fws)
+    S, G = model.S, sched.n_graphs
+    h_root = torch.empty((G, S), dtype=torch.float32, device=dev)
+    c_root = torch.empty((G, S), dtype=torch.float32, device=dev) if want_c else None
+    _check(L.fold_forward(ctypes.byref(sched.struct()), ctypes.byref(ms), ctypes.c_void_p(acts_buf.data_ptr()),
+                          _ptr(h_root), _ptr(c_root), ctypes.c_void_p(fbuf.data_ptr()), fws, _stream(stream)),
+           "fold_forward")
+    return h_root, c_root, Acts(acts_buf, lay)
+
+
+def backward(sched: Schedule, model: Model, acts: Acts, dh_root: torch.Tensor, dc_root: torch.Tensor | None = None,
+             grads=None, accumulate: bool = False, stream=None, ws: Workspace | None = None):
+    L = load()
+    dev = model.E.device
+    ms = model.struct()
+    if grads is None:
+        grads = (torch.empty_like(model.U), torch.empty_like(model.b), torch.empty_like(model.E))
+    dU, db, dE = grads
+    gs = _Grads(dU.data_ptr(), db.data_ptr(), dE.data_ptr(), 1 if accumulate else 0)
+    ws = ws or Workspace(dev)
+    bws = int(L.fold_backward_workspace(ctypes.byref(sched.struct()), ctypes.byref(ms)))
+    bbuf = ws.get("bwd", bws)
+    assert dh_root.dtype == torch.float32 and dh_root.is_contiguous()
+    _check(L.fold_backward(ctypes.byref(sched.struct()), ctypes.byref(ms), ctypes.c_void_p(acts.buf.data_ptr()),
+                           _ptr(dh_root), _ptr(dc_root), ctypes.byref(gs), ctypes.c_void_p(bbuf.data_ptr()), bws,
+                           _stream(stream)), "fold_backward")
+    return dU, db, dE
+
+
+def sgd_update(param: torch.Tensor, grad: torch.Tensor, lr: float, stream=None):
+    assert param.dtype == torch.float32 and grad.dtype == torch.float32
+    _check(load().fold_sgd_update(_ptr(param), _ptr(grad), param.numel(), ctypes.c_float(lr), _stream(stream)),
+           "fold_sgd_update")
+
+
+def graphs_to_device(gr, device="cuda", non_blocking=False):
+    """int32 device tensors (op, child, token, root) from a foldgen.Graphs-like object."""
+    conv = lambda a: torch.as_tensor(np.ascontiguousarray(a, dtype=np.int32)).to(device, non_blocking=non_blocking)
+    return conv(gr.op), conv(gr.child.reshape(-1, 2)), conv(gr.token), conv(gr.root)

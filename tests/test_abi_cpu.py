@@ -1,0 +1,56 @@
+"""CPU-only checks of the boundary: libfold.so builds for sm_100a, loads, and exports
+every function include/fold.h declares (no compute calls without a GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_1702_02181_b200 import build as fbuild
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "fold.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(fold_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = _declared()
+    for n in ("fold_schedule", "fold_forward", "fold_backward", "fold_sgd_update",
+              "fold_schedule_workspace", "fold_forward_workspace", "fold_backward_workspace"):
+        assert n in names
+
+
+def test_library_builds_and_exports_all_symbols():
+    path = fbuild.build()
+    lib = ctypes.CDLL(path)
+    for n in _declared():
+        assert hasattr(lib, n), n
+    from paper_1702_02181_b200 import fold
+    assert set(fold.EXPORTED) == set(_declared())
+
+
+def test_library_host_only_calls():
+    """Calls that touch no device memory: version, status strings, workspace sizes."""
+    fbuild.build()
+    from paper_1702_02181_b200 import fold
+    L = fold.load()
+    assert L.fold_abi_version() == 1
+    assert L.fold_status_string(6) == b"FOLD_E_CYCLE"
+    assert L.fold_schedule_workspace(1000, 10) > 0
+    assert L.fold_schedule_workspace(2_000_000, 8192) > L.fold_schedule_workspace(1000, 10)
+
+
+def test_sass_is_blackwell_native():
+    """The shipped kernels use tcgen05 MMA, TMEM loads and TMA (gather4) — SASS check."""
+    import shutil
+    import subprocess
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    path = fbuild.build()
+    sass = subprocess.run(["cuobjdump", "-sass", path], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass and "LDTM" in sass and "UTMALDG.2D.GATHER4" in sass
+    assert "HMMA" not in sass.replace("UTCHMMA", "")
