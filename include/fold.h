@@ -199,6 +199,17 @@ fold_status fold_device_check(void);
  * (instrumentation for the bench's gpu_launches count). */
 int64_t fold_launch_count(int32_t reset);
 
+/* Instrumentation: with profiling on, every kernel class below is bracketed by a pair of
+ * CUDA events recorded on the launch stream (calling thread only). fold_profile_enable
+ * resets the records. fold_profile_read synchronizes on the recorded events and returns,
+ * per class, the summed elapsed milliseconds and the number of bracketed launches.
+ * Classes: 0 schedule (whole call), 1 embedding forward, 2 cell forward (one per level),
+ * 3 backward pointwise, 4 dA GEMM, 5 dU GEMM, 6 embedding backward, 7 db column sum,
+ * 8 SGD, 9 weight conversion, 10 root read-out. */
+#define FOLD_PROF_NCLASS 11
+void fold_profile_enable(int32_t on);
+fold_status fold_profile_read(int32_t n_classes, double *ms, int64_t *launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -103,6 +103,7 @@ size_t fold_schedule_workspace(int32_t n_nodes, int32_t n_graphs) {
 
 fold_status fold_schedule(const fold_graphs *graphs, fold_schedule_t *sched, void *ws, size_t ws_bytes,
                           void *stream) {
+  ProfScope ps(K_SCHED, (cudaStream_t)stream);
   return run_schedule(graphs, sched, ws, ws_bytes, (cudaStream_t)stream);
 }
 
@@ -141,22 +142,33 @@ fold_status fold_forward(const fold_schedule_t *s, const fold_model *m, void *ac
   float *C = (float *)(a + L.c_off);
   void *Gact = a + L.g_off;
   const int32_t *lo = s->level_off_host;
-  FOLD_TRY(launch_embed_fwd(bf16, lo[1], lo[2], s->leaf_token, m->E, S, L.ld, H, C, st));
+  {
+    ProfScope ps(K_EMBED_FWD, st);
+    FOLD_TRY(launch_embed_fwd(bf16, lo[1], lo[2], s->leaf_token, m->E, S, L.ld, H, C, st));
+  }
   if (bf16) {
     TcWeights w{};
     w.ld_u = (int)round_up(2 * (int64_t)S, 8);
     w.ld_ut = (int)round_up((int64_t)gates * S, 8);
     w.U = (__nv_bfloat16 *)ws;
     w.Ut = nullptr;
-    if (D >= 2) FOLD_TRY(tc_prepare_U(gates, S, m->U, w, false, st));
-    for (int d = 2; d <= D; d++)
+    if (D >= 2) {
+      ProfScope ps(K_PREP, st);
+      FOLD_TRY(tc_prepare_U(gates, S, m->U, w, false, st));
+    }
+    for (int d = 2; d <= D; d++) {
+      ProfScope ps(K_CELL_FWD, st);
       FOLD_TRY(tc_cell_fwd(m->cell, lo[d], lo[d + 1], nl, s->gather, S, L.ld, w, m->b, (__nv_bfloat16 *)H, N, C,
                            (__nv_bfloat16 *)Gact, L.ld_g, st));
+    }
   } else {
-    for (int d = 2; d <= D; d++)
+    for (int d = 2; d <= D; d++) {
+      ProfScope ps(K_CELL_FWD, st);
       FOLD_TRY(launch_cell_fwd_simt(m->cell, lo[d], lo[d + 1], s->gather, S, L.ld, m->U, m->b, (float *)H, C,
                                     (float *)Gact, L.ld_g, nl, st));
+    }
   }
+  ProfScope ps(K_ROOT, st);
   FOLD_TRY(launch_root_out(bf16, G, S, L.ld, s->root_row, H, C, h_root, c_root, st));
   return FOLD_OK;
 }
@@ -200,32 +212,47 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
   const float *C = (const float *)(a + L.c_off);
   const void *Gact = a + L.g_off;
   const int32_t *lo = s->level_off_host;
-  if (bf16) FOLD_TRY(tc_prepare_U(gates, S, m->U, b.w, true, st));
+  if (bf16) {
+    ProfScope ps(K_PREP, st);
+    FOLD_TRY(tc_prepare_U(gates, S, m->U, b.w, true, st));
+  }
   for (int d = D; d >= 2; d--) {
     const int r0 = lo[d], r1 = lo[d + 1], M = r1 - r0, c0 = r0 - nl;
     if (M <= 0) continue;
+    {
+    ProfScope ps(K_BWD_PW, st);
     FOLD_TRY(launch_cell_bwd_pw(bf16, m->cell, r0, r1, nl, S, L.ld, L.ld_g, s->cons_off, s->cons_edge, s->root_row,
                                 s->root_perm, G, dh_root, dc_root, s->gather, Gact, C, b.dA, b.dCe, b.dZ, b.ld_z, st));
+    }
+    ProfScope ps(K_GEMM_DA, st);
     float *dA_lvl = b.dA + (size_t)2 * c0 * S;
     if (bf16)
       FOLD_TRY(tc_gemm_dA(c0, M, nc, S, gates, (const __nv_bfloat16 *)b.dZ, b.ld_z, b.w, b.dA, st));
     else
       FOLD_TRY(launch_gemm_dA_simt(M, S, gates, (const float *)b.dZ + (size_t)c0 * b.ld_z, b.ld_z, m->U, dA_lvl, st));
   }
-  FOLD_TRY(launch_embed_bwd(S, nl, s->n_tok_segs, s->tok_seg, s->leaf_perm, s->leaf_token, s->cons_off, s->cons_edge,
-                            s->root_row, s->root_perm, G, dh_root, b.dA, grads->dE, st));
+  {
+    ProfScope ps(K_EMBED_BWD, st);
+    FOLD_TRY(launch_embed_bwd(S, nl, s->n_tok_segs, s->tok_seg, s->leaf_perm, s->leaf_token, s->cons_off,
+                              s->cons_edge, s->root_row, s->root_perm, G, dh_root, b.dA, grads->dE, st));
+  }
+  {
+  ProfScope ps(K_GEMM_DU, st);
   if (bf16)
     FOLD_TRY(tc_gemm_dU(nc, nl, S, gates, (const __nv_bfloat16 *)b.dZ, b.ld_z, s->gather, (const __nv_bfloat16 *)H,
                         L.ld, N, grads->dU, acc, st));
   else
     FOLD_TRY(launch_gemm_dU_simt(nc, nl, S, gates, (const float *)b.dZ, b.ld_z, s->gather, (const float *)H, L.ld,
                                  grads->dU, acc, st));
+  }
+  ProfScope ps(K_COLSUM, st);
   FOLD_TRY(launch_colsum(bf16, nc, gates * S, b.dZ, b.ld_z, b.partial, b.nsplit, grads->db, acc, st));
   return FOLD_OK;
 }
 
 fold_status fold_sgd_update(float *p, const float *g, int64_t n, float lr, void *stream) {
   if (n < 0 || (n > 0 && (!p || !g))) return FOLD_E_INVALID;
+  ProfScope ps(K_SGD, (cudaStream_t)stream);
   return launch_sgd(p, g, n, lr, (cudaStream_t)stream);
 }
 

@@ -14,6 +14,20 @@ constexpr int kNumSMsB200 = 148;
 // Per-thread launch counter (instrumentation for bench.py's gpu_launches).
 extern thread_local int64_t g_launches;
 
+// Optional per-kernel-class CUDA-event timing (fold_profile_enable / fold_profile_read):
+// when enabled, the launchers bracket their kernels with events on the launch stream.
+enum KClass {
+  K_SCHED = 0, K_EMBED_FWD, K_CELL_FWD, K_BWD_PW, K_GEMM_DA, K_GEMM_DU, K_EMBED_BWD, K_COLSUM,
+  K_SGD, K_PREP, K_ROOT, K_NCLASS
+};
+void prof_mark(int cls, cudaStream_t st, bool begin);
+struct ProfScope {
+  int cls;
+  cudaStream_t st;
+  ProfScope(int c, cudaStream_t s) : cls(c), st(s) { prof_mark(cls, st, true); }
+  ~ProfScope() { prof_mark(cls, st, false); }
+};
+
 #define FOLD_LAUNCH_CHECK()                                   \
   do {                                                        \
     ::fold::g_launches++;                                     \

@@ -104,6 +104,10 @@ def load() -> ctypes.CDLL:
     L.fold_device_check.restype = i32
     L.fold_launch_count.restype = ctypes.c_int64
     L.fold_launch_count.argtypes = [i32]
+    L.fold_profile_enable.restype = None
+    L.fold_profile_enable.argtypes = [i32]
+    L.fold_profile_read.restype = i32
+    L.fold_profile_read.argtypes = [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
     _lib = L
     return L
 
@@ -111,7 +115,23 @@ def load() -> ctypes.CDLL:
 EXPORTED = ("fold_schedule_workspace", "fold_schedule", "fold_acts_layout", "fold_forward_workspace",
             "fold_forward", "fold_backward_workspace", "fold_backward", "fold_sgd_update",
             "fold_status_string", "fold_last_error_detail", "fold_abi_version", "fold_device_check",
-            "fold_launch_count")
+            "fold_launch_count", "fold_profile_enable", "fold_profile_read")
+
+PROF_CLASSES = ("schedule", "embed_fwd", "cell_fwd", "bwd_pointwise", "gemm_dA", "gemm_dU", "embed_bwd",
+                "db_colsum", "sgd", "weight_prep", "root_out")
+
+
+def profile_enable(on: bool = True):
+    load().fold_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """{class: (total_ms, launches)} for the launches bracketed since profile_enable()."""
+    n = len(PROF_CLASSES)
+    ms = (ctypes.c_double * n)()
+    cnt = (ctypes.c_int64 * n)()
+    _check(load().fold_profile_read(n, ms, cnt), "fold_profile_read")
+    return {PROF_CLASSES[i]: (float(ms[i]), int(cnt[i])) for i in range(n)}
 
 
 class FoldError(RuntimeError):
