@@ -60,7 +60,7 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
     b.dZ = p + o_dZ;
     b.partial = (float *)(p + o_part);
     if (bf16) {
-      b.w.ld_u = (int)round_up(2 * S, 8);
+      b.w.ld_u = (int)(2 * round_up(S, 64));
       b.w.ld_ut = (int)round_up((int64_t)gates * S, 8);
       b.w.U = (__nv_bfloat16 *)(p + o_w);
       b.w.Ut = (__nv_bfloat16 *)(p + o_w + a256((size_t)gates * S * b.w.ld_u * 2));
@@ -148,7 +148,7 @@ fold_status fold_forward(const fold_schedule_t *s, const fold_model *m, void *ac
   }
   if (bf16) {
     TcWeights w{};
-    w.ld_u = (int)round_up(2 * (int64_t)S, 8);
+    w.ld_u = (int)(2 * round_up(S, 64));
     w.ld_ut = (int)round_up((int64_t)gates * S, 8);
     w.U = (__nv_bfloat16 *)ws;
     w.Ut = nullptr;

@@ -28,11 +28,13 @@ struct ProfScope {
   ~ProfScope() { prof_mark(cls, st, false); }
 };
 
-#define FOLD_LAUNCH_CHECK()                                   \
-  do {                                                        \
-    ::fold::g_launches++;                                     \
-    cudaError_t _e = cudaGetLastError();                      \
-    if (_e != cudaSuccess) return FOLD_E_CUDA;                \
+// After every launch: count it, surface launch errors; with FOLD_DEBUG_SYNC=1 in the
+// environment also synchronize and name the failing launch site on stderr.
+fold_status launch_check(const char *file, int line);
+#define FOLD_LAUNCH_CHECK()                                          \
+  do {                                                               \
+    fold_status _s = ::fold::launch_check(__FILE__, __LINE__);       \
+    if (_s != FOLD_OK) return _s;                                    \
   } while (0)
 
 #define FOLD_CUDA_TRY(x)                                      \

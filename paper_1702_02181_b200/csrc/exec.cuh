@@ -47,7 +47,7 @@ fold_status launch_zero(void *p, size_t bytes, cudaStream_t st);
 
 // --- tcgen05 path (exec_tc.cu)
 struct TcWeights {  // bf16 copies made per call
-  __nv_bfloat16 *U;   // [gates*S][ld_u]  (ld_u = round_up(2S, 8)), canonical row order
+  __nv_bfloat16 *U;   // [gates*S][ld_u]  (ld_u = 2*round_up(S, 64): K halves padded), canonical rows
   __nv_bfloat16 *Ut;  // [2S][ld_ut]      (ld_ut = round_up(gates*S, 8)) = U^T
   int ld_u, ld_ut;
 };

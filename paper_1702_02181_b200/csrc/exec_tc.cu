@@ -53,7 +53,7 @@ struct FwdCfg {
 template <int GATES, int W>
 __global__ void __launch_bounds__(kThreads, 1)
     k_cell_fwd_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmU, int r0, int r1,
-                  int nl, int S, int ld, int KBh, const int32_t *__restrict__ gather, const float *__restrict__ bias,
+                  int nl, int S, int Sp, int ld, int KBh, const int32_t *__restrict__ gather, const float *__restrict__ bias,
                   __nv_bfloat16 *__restrict__ H, float *__restrict__ C, __nv_bfloat16 *__restrict__ Gact, int ld_g) {
   using Cfg = FwdCfg<GATES, W>;
   extern __shared__ uint8_t smem_raw[];
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int q = 0; q < BM / 4; q++)
           ptx::tma_gather4(&tmH, &full[s], A + q * 512, kc, gi[4 * q], gi[4 * q + 1], gi[4 * q + 2], gi[4 * q + 3]);
 #pragma unroll
-        for (int g = 0; g < GATES; g++) ptx::tma_load_2d(&tmU, &full[s], B + g * W * 128, half * S + kc, g * S + j0);
+        for (int g = 0; g < GATES; g++) ptx::tma_load_2d(&tmU, &full[s], B + g * W * 128, half * Sp + kc, g * S + j0);
       }
     }
   } else if (warp == 1) {
@@ -427,23 +427,27 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // =================================================================== weight prep
-// Ubf[r][k] = bf16(U[r][k]) (ld_u); Ut[k][r] = bf16(U[r][k]) (ld_ut). 32x32 smem tiles.
-__global__ void k_prep_U(int R, int K, const float *__restrict__ U, __nv_bfloat16 *__restrict__ Ubf, int ld_u,
-                         __nv_bfloat16 *__restrict__ Ut, int ld_ut) {
+// Ubf[r][half*Sp + k] = bf16(U[r][half*S + k]) for k < S, 0 for S <= k < Sp (each K half
+// padded to Sp = round_up(S, 64) so every TMA box starts 128-byte aligned);
+// Ut[half*S + k][r] = bf16(U[r][half*S + k]) (ld_ut). 32x32 smem tiles over padded columns.
+__global__ void k_prep_U(int R, int S, int Sp, const float *__restrict__ U, __nv_bfloat16 *__restrict__ Ubf,
+                         int ld_u, __nv_bfloat16 *__restrict__ Ut, int ld_ut) {
   __shared__ float t[32][33];
-  int r0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
-  int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: ty 0..7
+  const int r0 = blockIdx.y * 32, kp0 = blockIdx.x * 32;
+  const int half = kp0 >= Sp, kk0 = kp0 - half * Sp;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: ty 0..7
   for (int i = ty; i < 32; i += 8) {
-    int r = r0 + i, k = k0 + tx;
-    float v = (r < R && k < K) ? U[(int64_t)r * K + k] : 0.f;
+    int r = r0 + i, kk = kk0 + tx;
+    bool ok = r < R && kk < S;
+    float v = ok ? U[(int64_t)r * 2 * S + half * S + kk] : 0.f;
     t[i][tx] = v;
-    if (r < R && k < K) Ubf[(int64_t)r * ld_u + k] = __float2bfloat16_rn(v);
+    if (r < R) Ubf[(int64_t)r * ld_u + kp0 + tx] = __float2bfloat16_rn(v);
   }
   if (!Ut) return;
   __syncthreads();
   for (int i = ty; i < 32; i += 8) {
-    int k = k0 + i, r = r0 + tx;
-    if (r < R && k < K) Ut[(int64_t)k * ld_ut + r] = __float2bfloat16_rn(t[tx][i]);
+    int kk = kk0 + i, r = r0 + tx;
+    if (r < R && kk < S) Ut[(int64_t)(half * S + kk) * ld_ut + r] = __float2bfloat16_rn(t[tx][i]);
   }
 }
 
@@ -490,12 +494,12 @@ fold_status launch_fwd(int r0, int r1, int nl, const int32_t *gather, int S, int
   using Cfg = FwdCfg<GATES, W>;
   CUtensorMap tmH, tmU;
   FOLD_TRY(make_map(&tmH, H, (uint64_t)S, (uint64_t)n_rows_total, (uint64_t)ld * 2, BK, 1));
-  FOLD_TRY(make_map(&tmU, w.U, (uint64_t)2 * S, (uint64_t)GATES * S, (uint64_t)w.ld_u * 2, BK, W));
+  FOLD_TRY(make_map(&tmU, w.U, (uint64_t)w.ld_u, (uint64_t)GATES * S, (uint64_t)w.ld_u * 2, BK, W));
   auto kern = k_cell_fwd_tc<GATES, W>;
   FOLD_TRY(set_smem(kern, Cfg::SMEM));
   dim3 grid((unsigned)cdiv(r1 - r0, BM), (unsigned)cdiv(S, W));
   int KBh = (int)cdiv(S, BK);
-  kern<<<grid, kThreads, Cfg::SMEM, st>>>(tmH, tmU, r0, r1, nl, S, ld, KBh, gather, b, H, C, Gact, ld_g);
+  kern<<<grid, kThreads, Cfg::SMEM, st>>>(tmH, tmU, r0, r1, nl, S, w.ld_u / 2, ld, KBh, gather, b, H, C, Gact, ld_g);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
@@ -503,14 +507,14 @@ fold_status launch_fwd(int r0, int r1, int nl, const int32_t *gather, int S, int
 }  // namespace
 
 size_t tc_workspace_bytes(int gates, int S) {
-  size_t ld_u = round_up(2 * S, 8), ld_ut = round_up((int64_t)gates * S, 8);
+  size_t ld_u = 2 * round_up(S, 64), ld_ut = round_up((int64_t)gates * S, 8);
   return round_up((int64_t)gates * S * ld_u * 2, 256) + round_up((int64_t)2 * S * ld_ut * 2, 256);
 }
 
 fold_status tc_prepare_U(int gates, int S, const float *U, TcWeights &w, bool transpose, cudaStream_t st) {
-  int R = gates * S, K = 2 * S;
-  dim3 grid((unsigned)cdiv(K, 32), (unsigned)cdiv(R, 32));
-  k_prep_U<<<grid, 256, 0, st>>>(R, K, U, w.U, w.ld_u, transpose ? w.Ut : nullptr, w.ld_ut);
+  int R = gates * S, Sp = (int)round_up(S, 64);
+  dim3 grid((unsigned)(2 * Sp / 32), (unsigned)cdiv(R, 32));
+  k_prep_U<<<grid, 256, 0, st>>>(R, S, Sp, U, w.U, w.ld_u, transpose ? w.Ut : nullptr, w.ld_ut);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }

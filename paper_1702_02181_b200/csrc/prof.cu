@@ -1,5 +1,7 @@
 // prof.cu — optional CUDA-event timing per kernel class (bench.py's roofline figures are
 // measured live inside the timed region with these events on the launch stream).
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -27,6 +29,21 @@ cudaEvent_t get_event() {
   return e;
 }
 }  // namespace
+
+fold_status launch_check(const char *file, int line) {
+  static const bool dbg = [] {
+    const char *e = getenv("FOLD_DEBUG_SYNC");
+    return e && e[0] == '1';
+  }();
+  g_launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && dbg) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    if (dbg) fprintf(stderr, "[fold] CUDA error after launch at %s:%d: %s\n", file, line, cudaGetErrorString(e));
+    return FOLD_E_CUDA;
+  }
+  return FOLD_OK;
+}
 
 void prof_mark(int cls, cudaStream_t st, bool begin) {
   if (!g_on) return;
