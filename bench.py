@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""bench.py — TreeLSTM tree nodes/s, forward + backward (BASELINE.json metric), B200.
+
+One step = the whole hot path of SURVEY.md §8(a) over one batch of synthetic trees:
+fold_schedule (validate, depths, (depth, op) grouping, gather vectors, consumer CSR) ->
+fold_forward (embedding level + one fused tcgen05 cell kernel per depth) ->
+fold_backward (reverse level sweep + weight-gradient GEMM) -> NCCL all_reduce of the
+flat [dU | db | dE] gradient (N > 1) -> fold_sgd_update.
+
+Default workload (N = 1): BASELINE configs[1] — complete 128-leaf binary trees
+("tree size is 128"), B = 1024 trees, state S = 1024, vocab 16384,
+TreeLSTM, BF16 operands / fp32 accumulation. With N > 1 (torchrun) every rank runs
+its own B-tree batch (weak scaling) and the gradients are all-reduced.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import foldgen  # noqa: E402
+
+METRIC = "TreeLSTM tree nodes/sec fwd+bwd"
+UNIT = "nodes/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["fold", "reference"], default="fold")
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--batch", type=int, default=None, help="trees per GPU (default: config's full size)")
+    ap.add_argument("--prec", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--cell", default=None, choices=["treelstm", "treernn"])
+    ap.add_argument("--lr", type=float, default=1e-4)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-batch1", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--ref-trees", type=int, default=1, help="trees per oracle step (--impl reference)")
+    return ap.parse_args()
+
+
+DEFAULT_B = {"c1": None, "c2": 1024, "c3": 1024, "c4": 1024, "c5": 8192}
+
+
+def workload(args, rank=0):
+    cfg = args.config
+    B = args.batch or DEFAULT_B[cfg]
+    cell = args.cell or ("treernn" if cfg == "c1" else "treelstm")
+    S = foldgen.CONFIG_STATE[cfg]
+    gr = foldgen.make_config(cfg, B, seed=foldgen.GRAPH_SEED + rank)
+    desc = {
+        "c1": "C1 TreeRNN, 8 random-split trees (<=16 leaves), S=16, V=32",
+        "c2": f"C2 complete-128-leaf binary trees, B={gr.n_graphs}/GPU, TreeLSTM S=1024, V=16384",
+        "c3": f"C3 parse-shaped trees (1-60 leaves), B={gr.n_graphs}/GPU, TreeLSTM S=300, V=16384 Zipf",
+        "c4": f"C4 chain-256 (depth 256), B={gr.n_graphs}/GPU, TreeLSTM S=1024",
+        "c5": f"C5 random-split 128-leaf trees, B={gr.n_graphs}/GPU, TreeLSTM S=1024",
+    }[cfg]
+    return gr, cell, S, desc
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=1)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 8:
+                for k, v in zip(names, r[4:8]):
+                    if v.lower().startswith("active"):
+                        reasons.add(k)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ============================================================================ fold arm
+
+def run_fold(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1702_02181_b200 import fold
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    fold.device_check()
+
+    gr, cell, S, desc = workload(args, rank)
+    V = gr.vocab
+    gates = foldgen.gates_of(cell)
+    N_nodes = gr.n_nodes
+    n_cells = int((gr.op == 1).sum())
+    p = foldgen.make_params(cell, S, V)
+    # flat parameter / gradient buffers: one all_reduce and one SGD launch per step
+    nU, nb, nE = p.U.size, p.b.size, p.E.size
+    flat_p = torch.empty(nU + nb + nE, dtype=torch.float32, device=dev)
+    flat_g = torch.zeros_like(flat_p)
+    U = flat_p[:nU].view(p.U.shape); b = flat_p[nU:nU + nb]; E = flat_p[nU + nb:].view(p.E.shape)
+    U.copy_(torch.from_numpy(p.U)); b.copy_(torch.from_numpy(p.b)); E.copy_(torch.from_numpy(p.E))
+    dU = flat_g[:nU].view(p.U.shape); db = flat_g[nU:nU + nb]; dE = flat_g[nU + nb:].view(p.E.shape)
+    model = fold.Model(U, b, E, cell=cell, prec=args.prec)
+    g_host = foldgen.make_upstream(gr.n_graphs, S)
+    g_dev = torch.from_numpy(g_host).to(dev)
+    op, child, token, root = fold.graphs_to_device(gr, dev)
+    ws = fold.Workspace(dev)
+    sched_ws = torch.empty(1, dtype=torch.uint8, device=dev)
+
+    def step(op, child, token, root, g):
+        nonlocal sched_ws
+        s = fold.schedule(op, child, token, root, V, workspace=sched_ws)
+        h, c, acts = fold.forward(s, model, ws=ws, want_c=False)
+        fold.backward(s, model, acts, g, grads=(dU, db, dE), ws=ws)
+        if world > 1:
+            dist.all_reduce(flat_g)
+        fold.sgd_update(flat_p, flat_g, args.lr)
+        return h
+
+    # size the schedule workspace once (fold_schedule_workspace)
+    sched_ws = torch.empty(int(fold.load().fold_schedule_workspace(N_nodes, gr.n_graphs)), dtype=torch.uint8,
+                           device=dev)
+    for _ in range(max(args.warmup, 3 if args.warmup >= 3 else args.warmup)):
+        step(op, child, token, root, g_dev)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local) if not args.no_clocks else None
+    # ---------------- timed region (device-resident inputs)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.start()
+    fold.launch_count(reset=True)
+    fold.profile_enable(True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step(op, child, token, root, g_dev)
+    e1.record()
+    torch.cuda.synchronize()
+    launches = fold.launch_count()
+    prof = fold.profile_read()
+    fold.profile_enable(False)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop() if clocks else None
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_per_step = ms_max / args.steps
+    value = world * N_nodes / (ms_per_step / 1e3)
+
+    # ---------------- e2e: host buffers, H2D + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        h_op, h_child, h_tok, h_root = pin(gr.op.astype(np.int32)), pin(gr.child.astype(np.int32)), \
+            pin(gr.token.astype(np.int32)), pin(gr.root.astype(np.int32))
+        h_g = pin(g_host)
+        h_out = torch.empty((gr.n_graphs, S), dtype=torch.float32).pin_memory()
+        d_op, d_child, d_tok, d_root = (torch.empty_like(x, device=dev) for x in (h_op, h_child, h_tok, h_root))
+        d_g = torch.empty_like(h_g, device=dev)
+        h2d = sum(x.numel() * x.element_size() for x in (h_op, h_child, h_tok, h_root, h_g))
+        d2h = h_out.numel() * 4
+
+        def e2e_step():
+            for d, h in ((d_op, h_op), (d_child, h_child), (d_tok, h_tok), (d_root, h_root), (d_g, h_g)):
+                d.copy_(h, non_blocking=True)
+            hr = step(d_op, d_child, d_tok, d_root, d_g)
+            h_out.copy_(hr, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(args.steps):
+            e2e_step()
+        a1.record()
+        torch.cuda.synchronize()
+        t2 = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        e_ms = float(t2.item()) / args.steps
+        e2e = {"value": world * N_nodes / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    # ---------------- batch-1 (within-tree batching only) for the speedup-vs-batch-size context
+    batch1 = None
+    if not args.no_batch1 and rank == 0 and args.config in ("c2", "c3", "c4", "c5"):
+        one = foldgen.sub_batch(gr, 0, 1)
+        o1 = fold.graphs_to_device(one, dev)
+        g1 = g_dev[:1].contiguous()
+        for _ in range(3):
+            step(*o1, g1)
+        torch.cuda.synchronize()
+        b0 = torch.cuda.Event(enable_timing=True)
+        b1 = torch.cuda.Event(enable_timing=True)
+        nrep = 20
+        b0.record()
+        for _ in range(nrep):
+            step(*o1, g1)
+        b1.record()
+        torch.cuda.synchronize()
+        ms1 = b0.elapsed_time(b1) / nrep
+        batch1 = {"nodes_per_s": one.n_nodes / (ms1 / 1e3), "ms_per_tree": ms1}
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---------------- roofline of the dominant kernel class (tensor-bound GEMM kernels)
+    pk, pk_src = peaks()
+    flops_per_cell = 2.0 * gates * S * 2 * S  # one GEMM pass (fwd Z, bwd dA, or dU) per cell
+    per_class = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
+                 for k, v in prof.items() if v[1] > 0}
+    tensor_classes = {"cell_fwd": "k_cell_fwd_tc", "gemm_dA": "k_gemm_dA_tc", "gemm_dU": "k_gemm_dU_tc"}
+    dom = max(tensor_classes, key=lambda k: prof[k][0])
+    dom_ms_total, dom_launches = prof[dom]
+    achieved = flops_per_cell * n_cells * args.steps / (dom_ms_total / 1e3) / 1e12
+    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(tensor_classes[dom], {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": tensor_classes[dom], "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": f"{pk_src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
+                "algorithmic": f"{flops_per_cell:.4g} FLOP/cell x {n_cells} cells per launch-set; "
+                               f"{dom_launches // max(args.steps, 1)} launches/step",
+                "share_of_step": (dom_ms_total / args.steps) / ms_per_step}
+
+    # ---------------- CPU baseline: the fp64 oracle as it stands, bounded sample, 1 thread
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = cpu_baseline(gr, cell, p, g_host, n_trees=2 if args.config in ("c2", "c4", "c5") else 64)
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.prec, "data": "synthetic",
+        "config": {"workload": desc, "trees_per_gpu": gr.n_graphs, "nodes_per_gpu": N_nodes,
+                   "cells_per_gpu": n_cells, "state": S, "cell": cell, "levels": None,
+                   "step": "schedule+fwd+bwd+allreduce+sgd" if world > 1 else "schedule+fwd+bwd+sgd",
+                   "l2": "working set > L2 (pool+saved gates+grads ~%.1f GB); no flush" % (
+                       (N_nodes * S * 6 + n_cells * gates * S * 4 + n_cells * S * 16) / 1e9),
+                   "parallelism": f"dp{world}"},
+        "gpu_launches": int(launches),
+        "kernels": per_class,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "clocks": clk,
+    }
+    if batch1:
+        out["batch1"] = batch1
+        out["speedup_vs_batch1"] = (value / world) / batch1["nodes_per_s"]
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(gr, cell, p, g_host, n_trees):
+    """Time the fp64 oracle (forward + backward, node at a time, 1 thread) on the first
+    n_trees trees of the same workload."""
+    import oracle
+    sub = foldgen.sub_batch(gr, 0, min(n_trees, gr.n_graphs))
+    g = g_host[:sub.n_graphs]
+    t0 = time.perf_counter()
+    oracle.forward(cell, sub.op, sub.child, sub.token, sub.root, p.U, p.b, p.E)
+    oracle.backward(cell, sub.op, sub.child, sub.token, sub.root, p.U, p.b, p.E, g)
+    dt = time.perf_counter() - t0
+    return {"value": sub.n_nodes / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {sub.n_graphs} trees ({sub.n_nodes} nodes) of the same batch, fp64 "
+                      f"forward + backward, single thread, {dt:.1f} s"}
+
+
+# ============================================================================ reference arm
+
+def run_reference(args):
+    """--impl reference: the fp64 oracle (the only reference this paper-only task has),
+    timed as it stands on host cores; each step = forward + backward over a bounded
+    sample (args.ref_trees trees) of the same workload. Rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    gr, cell, S, desc = workload(args, 0)
+    p = foldgen.make_params(cell, S, gr.vocab)
+    g_host = foldgen.make_upstream(gr.n_graphs, S)
+    sub = foldgen.sub_batch(gr, 0, min(args.ref_trees, gr.n_graphs))
+    g = g_host[:sub.n_graphs]
+
+    def step():
+        oracle.forward(cell, sub.op, sub.child, sub.token, sub.root, p.U, p.b, p.E)
+        oracle.backward(cell, sub.op, sub.child, sub.token, sub.root, p.U, p.b, p.E, g)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    value = sub.n_nodes / dt
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": desc, "trees_per_step": sub.n_graphs, "nodes_per_step": sub.n_nodes,
+                      "state": S, "cell": cell},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": f"{sub.n_graphs} tree(s) ({sub.n_nodes} nodes) per step, fp64 fwd+bwd, "
+                                      f"single thread"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_fold(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -31,7 +31,7 @@ fold_status check_sched(const fold_schedule_t *s) {
 
 // backward workspace carve
 struct BwdWs {
-  float *dA, *dCe, *partial;
+  float *dA, *dCe, *partial, *dU_split;
   void *dZ;
   TcWeights w;
   int ld_z, nsplit;
@@ -52,6 +52,8 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
   size_t o_dZ = take((size_t)(nc + 1) * b.ld_z * (bf16 ? 2 : 4));
   size_t o_part = take((size_t)b.nsplit * gates * S * 4);
   size_t o_w = take(bf16 ? tc_workspace_bytes(gates, (int)S) : 0);
+  const int splits = bf16 ? tc_dU_splits((int)nc, gates, (int)S) : 1;
+  size_t o_spl = take(splits > 1 ? (size_t)splits * gates * S * 2 * S * 4 : 0);
   b.bytes = off;
   if (base) {
     char *p = (char *)base;
@@ -59,6 +61,7 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
     b.dCe = (float *)(p + o_dCe);
     b.dZ = p + o_dZ;
     b.partial = (float *)(p + o_part);
+    b.dU_split = splits > 1 ? (float *)(p + o_spl) : nullptr;
     if (bf16) {
       b.w.ld_u = (int)(2 * round_up(S, 64));
       b.w.ld_ut = (int)round_up((int64_t)gates * S, 8);
@@ -240,7 +243,7 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
   ProfScope ps(K_GEMM_DU, st);
   if (bf16)
     FOLD_TRY(tc_gemm_dU(nc, nl, S, gates, (const __nv_bfloat16 *)b.dZ, b.ld_z, s->gather, (const __nv_bfloat16 *)H,
-                        L.ld, N, grads->dU, acc, st));
+                        L.ld, N, grads->dU, acc, b.dU_split, st));
   else
     FOLD_TRY(launch_gemm_dU_simt(nc, nl, S, gates, (const float *)b.dZ, b.ld_z, s->gather, (const float *)H, L.ld,
                                  grads->dU, acc, st));

@@ -165,13 +165,51 @@ __global__ void k_root_out(int G, int S, int ld, const int32_t *__restrict__ roo
 //             dz = [dc*u*i(1-i), dc*cL*fL(1-fL), dc*cR*fR(1-fR), do*o(1-o), dc*i*(1-u^2)]
 //             dCe[2c] = dc*fL, dCe[2c+1] = dc*fR
 //   TreeRNN:  dz = dh*(1-h^2)
-template <typename T, int GATES>
+template <typename T, int V> struct VecIO;
+template <> struct VecIO<float, 1> {
+  static __device__ __forceinline__ void ld(const float *p, float *v) { v[0] = *p; }
+  static __device__ __forceinline__ void st(float *p, const float *v) { *p = v[0]; }
+};
+template <> struct VecIO<float, 4> {
+  static __device__ __forceinline__ void ld(const float *p, float *v) {
+    float4 x = *reinterpret_cast<const float4 *>(p);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  }
+  static __device__ __forceinline__ void st(float *p, const float *v) {
+    *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+template <> struct VecIO<__nv_bfloat16, 1> {
+  static __device__ __forceinline__ void ld(const __nv_bfloat16 *p, float *v) { v[0] = __bfloat162float(*p); }
+  static __device__ __forceinline__ void st(__nv_bfloat16 *p, const float *v) { *p = __float2bfloat16_rn(v[0]); }
+};
+template <> struct VecIO<__nv_bfloat16, 4> {
+  static __device__ __forceinline__ void ld(const __nv_bfloat16 *p, float *v) {
+    uint2 x = *reinterpret_cast<const uint2 *>(p);
+    float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162 *>(&x.x));
+    float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162 *>(&x.y));
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+  static __device__ __forceinline__ void st(__nv_bfloat16 *p, const float *v) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]), b = __floats2bfloat162_rn(v[2], v[3]);
+    uint2 x;
+    x.x = *reinterpret_cast<uint32_t *>(&a);
+    x.y = *reinterpret_cast<uint32_t *>(&b);
+    *reinterpret_cast<uint2 *>(p) = x;
+  }
+};
+
+// VEC consecutive state columns per lane (VEC = 4 needs S % 4 == 0: 16-byte fp32 and
+// 8-byte bf16 accesses stay aligned since every row stride is a multiple of 8 elements).
+template <typename T, int GATES, int VEC>
 __global__ void k_cell_bwd_pw(int r0, int r1, int nl, int S, int ld, int ld_g, const int32_t *__restrict__ cons_off,
                               const int32_t *__restrict__ cons_edge, const int32_t *__restrict__ root_row,
                               const int32_t *__restrict__ root_perm, int G, const float *__restrict__ dh_root,
                               const float *__restrict__ dc_root, const int32_t *__restrict__ gather,
                               const T *__restrict__ Gact, const float *__restrict__ C, const float *__restrict__ dA,
                               float *__restrict__ dCe, T *__restrict__ dZ, int ld_z) {
+  using IT = VecIO<T, VEC>;
+  using IF = VecIO<float, VEC>;
   int lane = threadIdx.x & 31;
   int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -187,36 +225,61 @@ __global__ void k_cell_bwd_pw(int r0, int r1, int nl, int S, int ld, int ld_g, c
     const T *ga = Gact + c * ld_g;
     T *dz = dZ + c * ld_z;
     int64_t gL = gather[2 * r], gR = gather[2 * r + 1];
-    for (int j = lane; j < S; j += 32) {
-      float dh = 0.f, dc = 0.f;
+    for (int j = lane * VEC; j < S; j += 32 * VEC) {
+      float dh[VEC], dc[VEC], t[VEC];
+#pragma unroll
+      for (int u = 0; u < VEC; u++) { dh[u] = 0.f; dc[u] = 0.f; }
       for (int q = rs0; q < rs1; q++) {
         int g = root_perm[q];
-        dh += dh_root[(int64_t)g * S + j];
-        if (dc_root) dc += dc_root[(int64_t)g * S + j];
+        IF::ld(dh_root + (int64_t)g * S + j, t);
+#pragma unroll
+        for (int u = 0; u < VEC; u++) dh[u] += t[u];
+        if (dc_root) {
+          IF::ld(dc_root + (int64_t)g * S + j, t);
+#pragma unroll
+          for (int u = 0; u < VEC; u++) dc[u] += t[u];
+        }
       }
       for (int e = e0; e < e1; e++) {
         int64_t ed = cons_edge[e];
-        dh += dA[ed * S + j];
-        if (GATES == 5) dc += dCe[ed * S + j];
+        IF::ld(dA + ed * S + j, t);
+#pragma unroll
+        for (int u = 0; u < VEC; u++) dh[u] += t[u];
+        if (GATES == 5) {
+          IF::ld(dCe + ed * S + j, t);
+#pragma unroll
+          for (int u = 0; u < VEC; u++) dc[u] += t[u];
+        }
       }
       if constexpr (GATES == 1) {
-        float h = to_f(ga[j]);
-        dz[j] = from_f<T>(dh * (1.f - h * h));
+        float h[VEC], o[VEC];
+        IT::ld(ga + j, h);
+#pragma unroll
+        for (int u = 0; u < VEC; u++) o[u] = dh[u] * (1.f - h[u] * h[u]);
+        IT::st(dz + j, o);
       } else {
-        float ig = to_f(ga[j]), fl = to_f(ga[S + j]), fr = to_f(ga[2 * S + j]);
-        float og = to_f(ga[3 * S + j]), ug = to_f(ga[4 * S + j]);
-        float cc = C[r * ld + j];
-        float tc = tanhf(cc);
-        float dO = dh * tc;
-        float dcc = dc + dh * og * (1.f - tc * tc);
-        float cl = C[gL * ld + j], cr = C[gR * ld + j];
-        dz[j] = from_f<T>(dcc * ug * ig * (1.f - ig));
-        dz[S + j] = from_f<T>(dcc * cl * fl * (1.f - fl));
-        dz[2 * S + j] = from_f<T>(dcc * cr * fr * (1.f - fr));
-        dz[3 * S + j] = from_f<T>(dO * og * (1.f - og));
-        dz[4 * S + j] = from_f<T>(dcc * ig * (1.f - ug * ug));
-        dCe[(2 * c) * S + j] = dcc * fl;
-        dCe[(2 * c + 1) * S + j] = dcc * fr;
+        float ig[VEC], fl[VEC], fr[VEC], og[VEC], ug[VEC], cc[VEC], cl[VEC], cr[VEC];
+        IT::ld(ga + j, ig); IT::ld(ga + S + j, fl); IT::ld(ga + 2 * S + j, fr);
+        IT::ld(ga + 3 * S + j, og); IT::ld(ga + 4 * S + j, ug);
+        IF::ld(C + r * ld + j, cc); IF::ld(C + gL * ld + j, cl); IF::ld(C + gR * ld + j, cr);
+        float z0[VEC], z1[VEC], z2[VEC], z3[VEC], z4[VEC], eL[VEC], eR[VEC];
+#pragma unroll
+        for (int u = 0; u < VEC; u++) {
+          float tc = tanhf(cc[u]);
+          float dO = dh[u] * tc;
+          float dcc = dc[u] + dh[u] * og[u] * (1.f - tc * tc);
+          z0[u] = dcc * ug[u] * ig[u] * (1.f - ig[u]);
+          z1[u] = dcc * cl[u] * fl[u] * (1.f - fl[u]);
+          z2[u] = dcc * cr[u] * fr[u] * (1.f - fr[u]);
+          z3[u] = dO * og[u] * (1.f - og[u]);
+          z4[u] = dcc * ig[u] * (1.f - ug[u] * ug[u]);
+          eL[u] = dcc * fl[u];
+          eR[u] = dcc * fr[u];
+        }
+        IT::st(dz + j, z0); IT::st(dz + S + j, z1); IT::st(dz + 2 * S + j, z2);
+        IT::st(dz + 3 * S + j, z3); IT::st(dz + 4 * S + j, z4);
+        IF::st(dCe + (2 * c) * S + j, eL);
+        IF::st(dCe + (2 * c + 1) * S + j, eR);
       }
     }
   }
@@ -347,45 +410,45 @@ __global__ void k_colsum_final(int ncols, int nsplit, const float *__restrict__ 
 }
 
 // ---------------------------------------------------------------- embedding backward
-// For each distinct-token segment of leaf_perm (rows ascending): dE[tok] = sum over its
+// For each distinct-token segment of leaf_perm (rows ascending): dE[tok] += sum over its
 // rows of dh(row), dh(row) = roots seeded at row + sum_{e in cons(row)} dA[e].
-// One warp per segment; deterministic order. dE must be pre-zeroed or hold the
-// accumulation base (rows of absent tokens are untouched).
-__global__ void k_embed_bwd(int S, int n_tok_segs, const int32_t *__restrict__ tok_seg,
-                            const int32_t *__restrict__ leaf_perm, const int32_t *__restrict__ leaf_token,
-                            const int32_t *__restrict__ cons_off,
-                            const int32_t *__restrict__ cons_edge, const int32_t *__restrict__ root_row,
-                            const int32_t *__restrict__ root_perm, int G, const float *__restrict__ dh_root,
-                            const float *__restrict__ dA, float *__restrict__ dE) {
-  int lane = threadIdx.x & 31;
-  int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t s = w; s < n_tok_segs; s += nw) {
-    int a = tok_seg[s], b = tok_seg[s + 1];
-    int tok = leaf_token[leaf_perm[a]];
+// One 128-thread block per segment, VEC columns per thread; deterministic order.
+// dE must be pre-zeroed or hold the accumulation base (absent tokens are untouched).
+template <int VEC>
+__global__ void __launch_bounds__(128) k_embed_bwd(int S, int n_tok_segs, const int32_t *__restrict__ tok_seg,
+                                                   const int32_t *__restrict__ leaf_perm,
+                                                   const int32_t *__restrict__ leaf_token,
+                                                   const int32_t *__restrict__ cons_off,
+                                                   const int32_t *__restrict__ cons_edge,
+                                                   const int32_t *__restrict__ root_row,
+                                                   const int32_t *__restrict__ root_perm, int G,
+                                                   const float *__restrict__ dh_root, const float *__restrict__ dA,
+                                                   float *__restrict__ dE) {
+  using IF = VecIO<float, VEC>;
+  for (int64_t s = blockIdx.x; s < n_tok_segs; s += gridDim.x) {
+    const int a = tok_seg[s], b = tok_seg[s + 1];
+    const int tok = leaf_token[leaf_perm[a]];
     float *de = dE + (int64_t)tok * S;
-    for (int j0 = 0; j0 < S; j0 += 32 * 4) {
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int j = threadIdx.x * VEC; j < S; j += blockDim.x * VEC) {
+      float acc[VEC], t[VEC];
+      IF::ld(de + j, acc);
       for (int q = a; q < b; q++) {
-        int r = leaf_perm[q];
+        const int r = leaf_perm[q];
         int lo = 0, hi = G;
         while (lo < hi) { int mid = (lo + hi) >> 1; if (root_row[root_perm[mid]] < r) lo = mid + 1; else hi = mid; }
-        int e0 = cons_off[r], e1 = cons_off[r + 1];
+        for (int k = lo; k < G && root_row[root_perm[k]] == r; k++) {
+          IF::ld(dh_root + (int64_t)root_perm[k] * S + j, t);
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-          int j = j0 + u * 32 + lane;
-          if (j >= S) continue;
-          float dh = 0.f;
-          for (int k = lo; k < G && root_row[root_perm[k]] == r; k++) dh += dh_root[(int64_t)root_perm[k] * S + j];
-          for (int e = e0; e < e1; e++) dh += dA[(int64_t)cons_edge[e] * S + j];
-          acc[u] += dh;
+          for (int u = 0; u < VEC; u++) acc[u] += t[u];
+        }
+        const int e1 = cons_off[r + 1];
+        for (int e = cons_off[r]; e < e1; e++) {
+          IF::ld(dA + (int64_t)cons_edge[e] * S + j, t);
+#pragma unroll
+          for (int u = 0; u < VEC; u++) acc[u] += t[u];
         }
       }
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        int j = j0 + u * 32 + lane;
-        if (j < S) de[j] += acc[u];
-      }
+      IF::st(de + j, acc);
     }
   }
 }
@@ -443,19 +506,18 @@ fold_status launch_cell_bwd_pw(bool bf16, int cell, int r0, int r1, int nl, int 
   if (r1 <= r0) return FOLD_OK;
   unsigned g = grid_cap(cdiv((int64_t)(r1 - r0) * 32, 256));
 #define PW_ARGS r0, r1, nl, S, ld, ld_g, cons_off, cons_edge, root_row, root_perm, G, dh_root, dc_root, gather
+#define PW_LAUNCH(T, GT, VEC) \
+  k_cell_bwd_pw<T, GT, VEC><<<g, 256, 0, st>>>(PW_ARGS, (const T *)Gact, C, dA, dCe, (T *)dZ, ld_z)
+  const bool v4 = (S & 3) == 0;
+  const bool lstm = cell == FOLD_CELL_TREELSTM;
   if (bf16) {
-    if (cell == FOLD_CELL_TREELSTM)
-      k_cell_bwd_pw<__nv_bfloat16, 5><<<g, 256, 0, st>>>(PW_ARGS, (const __nv_bfloat16 *)Gact, C, dA, dCe,
-                                                         (__nv_bfloat16 *)dZ, ld_z);
-    else
-      k_cell_bwd_pw<__nv_bfloat16, 1><<<g, 256, 0, st>>>(PW_ARGS, (const __nv_bfloat16 *)Gact, C, dA, dCe,
-                                                         (__nv_bfloat16 *)dZ, ld_z);
+    if (lstm) { if (v4) PW_LAUNCH(__nv_bfloat16, 5, 4); else PW_LAUNCH(__nv_bfloat16, 5, 1); }
+    else { if (v4) PW_LAUNCH(__nv_bfloat16, 1, 4); else PW_LAUNCH(__nv_bfloat16, 1, 1); }
   } else {
-    if (cell == FOLD_CELL_TREELSTM)
-      k_cell_bwd_pw<float, 5><<<g, 256, 0, st>>>(PW_ARGS, (const float *)Gact, C, dA, dCe, (float *)dZ, ld_z);
-    else
-      k_cell_bwd_pw<float, 1><<<g, 256, 0, st>>>(PW_ARGS, (const float *)Gact, C, dA, dCe, (float *)dZ, ld_z);
+    if (lstm) { if (v4) PW_LAUNCH(float, 5, 4); else PW_LAUNCH(float, 5, 1); }
+    else { if (v4) PW_LAUNCH(float, 1, 4); else PW_LAUNCH(float, 1, 1); }
   }
+#undef PW_LAUNCH
 #undef PW_ARGS
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
@@ -496,9 +558,13 @@ fold_status launch_embed_bwd(int S, int nl, int n_tok_segs, const int32_t *tok_s
                              const float *dh_root, const float *dA, float *dE, cudaStream_t st) {
   (void)nl;
   if (n_tok_segs <= 0) return FOLD_OK;
-  unsigned g = grid_cap(cdiv((int64_t)n_tok_segs * 32, 256));
-  k_embed_bwd<<<g, 256, 0, st>>>(S, n_tok_segs, tok_seg, leaf_perm, leaf_token, cons_off, cons_edge, root_row,
-                                 root_perm, G, dh_root, dA, dE);
+  unsigned g = grid_cap(n_tok_segs);
+  if ((S & 3) == 0)
+    k_embed_bwd<4><<<g, 128, 0, st>>>(S, n_tok_segs, tok_seg, leaf_perm, leaf_token, cons_off, cons_edge, root_row,
+                                      root_perm, G, dh_root, dA, dE);
+  else
+    k_embed_bwd<1><<<g, 128, 0, st>>>(S, n_tok_segs, tok_seg, leaf_perm, leaf_token, cons_off, cons_edge, root_row,
+                                      root_perm, G, dh_root, dA, dE);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }

@@ -57,9 +57,11 @@ fold_status tc_cell_fwd(int cell, int r0, int r1, int nl, const int32_t *gather,
                         __nv_bfloat16 *Gact, int ld_g, cudaStream_t st);
 fold_status tc_gemm_dA(int c0, int M, int n_cells, int S, int gates, const __nv_bfloat16 *dZ, int ld_z,
                        const TcWeights &w, float *dA, cudaStream_t st);
+// split-K over cells into split_ws [splits][gates*S][2S] (fp32), then a fixed-order sum
+int tc_dU_splits(int n_cells, int gates, int S);
 fold_status tc_gemm_dU(int n_cells, int nl, int S, int gates, const __nv_bfloat16 *dZ, int ld_z,
                        const int32_t *gather, const __nv_bfloat16 *H, int ld, int n_rows_total, float *dU,
-                       int accumulate, cudaStream_t st);
+                       int accumulate, float *split_ws, cudaStream_t st);
 size_t tc_workspace_bytes(int gates, int S);
 
 }  // namespace fold

@@ -64,7 +64,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ float sbias[GATES * W];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int m0 = r0 + blockIdx.x * BM, j0 = blockIdx.y * W;
+  // grid.x = state-column tile (fast), grid.y = row tile: the CTAs of one wave share few
+  // gathered A tiles, which stay in L2 across the N tiles; U (21 MB bf16) is L2-resident.
+  const int m0 = r0 + blockIdx.y * BM, j0 = blockIdx.x * W;
 
   if (tid < BM) {
     int r = m0 + tid;
@@ -94,23 +96,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int KB = 2 * KBh;
 
   if (warp == 0) {
-    if (lane == 0) {
-      for (int kb = 0; kb < KB; kb++) {
-        int s = kb % ST;
-        uint32_t ph = (kb / ST) & 1;
+    // Producer warp: lane 0 arms the stage barrier, then all 32 lanes issue in parallel
+    // (lane q: gather4 of tile rows 4q..4q+3; lanes < GATES: one U gate slab each).
+    for (int kb = 0; kb < KB; kb++) {
+      int s = kb % ST;
+      uint32_t ph = (kb / ST) & 1;
+      if (lane == 0) {
         ptx::mbar_wait(&empty[s], ph ^ 1);
         ptx::mbar_arrive_expect_tx(&full[s], Cfg::STAGE);
-        int half = kb >= KBh;
-        int kc = (kb - half * KBh) * BK;
-        uint8_t *A = smem + s * Cfg::STAGE;
-        uint8_t *B = A + Cfg::A_BYTES;
-        const int *gi = gidx[half];
-#pragma unroll 4
-        for (int q = 0; q < BM / 4; q++)
-          ptx::tma_gather4(&tmH, &full[s], A + q * 512, kc, gi[4 * q], gi[4 * q + 1], gi[4 * q + 2], gi[4 * q + 3]);
-#pragma unroll
-        for (int g = 0; g < GATES; g++) ptx::tma_load_2d(&tmU, &full[s], B + g * W * 128, half * Sp + kc, g * S + j0);
       }
+      __syncwarp();
+      int half = kb >= KBh;
+      int kc = (kb - half * KBh) * BK;
+      uint8_t *A = smem + s * Cfg::STAGE;
+      uint8_t *B = A + Cfg::A_BYTES;
+      const int *gi = gidx[half] + 4 * lane;
+      ptx::tma_gather4(&tmH, &full[s], A + lane * 512, kc, gi[0], gi[1], gi[2], gi[3]);
+      if (lane < GATES) ptx::tma_load_2d(&tmU, &full[s], B + lane * W * 128, half * Sp + kc, lane * S + j0);
+      __syncwarp();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -326,8 +329,8 @@ constexpr int MN_CHUNK = 64 * 128;       // bytes per 64-element MN chunk of 64 
 
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_dU_tc(const __grid_constant__ CUtensorMap tmZ2, const __grid_constant__ CUtensorMap tmH, int n_cells,
-                 int nl, int S, int Mg, int NT, const int32_t *__restrict__ gather, float *__restrict__ dU,
-                 int accumulate) {
+                 int nl, int S, int Mg, int NT, int kb_per_split, const int32_t *__restrict__ gather,
+                 float *__restrict__ out_base, int64_t split_stride, int accumulate) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
   __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull;
@@ -335,7 +338,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int half = blockIdx.x / NT, jt = blockIdx.x - half * NT;
   const int i0 = blockIdx.y * BM, jn0 = jt * DU_N;
-  const int KB = (int)cdiv(n_cells, BK);
+  // split-K over cells: this CTA reduces k-blocks [kb0, kb1) into its own partial slab
+  const int KBall = (int)cdiv(n_cells, BK);
+  const int kb0 = blockIdx.z * kb_per_split;
+  const int kb1 = min(KBall, kb0 + kb_per_split);
+  const int KB = kb1 > kb0 ? kb1 - kb0 : 0;
+  float *dU = out_base + (int64_t)blockIdx.z * split_stride;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < ST; s++) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
     ptx::mbar_init(&tfull, 1);
@@ -349,21 +357,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tbase = tmem_base_sh;
   if (warp == 0) {
-    // whole warp: lanes 0..15 each gather 4 cells (rows) for the 4 MN chunks of B
+    // whole warp: lane l gathers the 4 cells 4(l&15)..+3 for MN chunks 2(l>>4), 2(l>>4)+1
+    const int grp = lane & 15, ch0 = 2 * (lane >> 4);
     int nxt_rows[4];
     auto load_rows = [&](int kb, int (&rows)[4]) {
 #pragma unroll
       for (int u = 0; u < 4; u++) {
-        int cidx = kb * BK + 4 * (lane & 15) + u;
+        int cidx = kb * BK + 4 * grp + u;
         rows[u] = cidx < n_cells ? gather[2 * ((int64_t)nl + cidx) + half] : 0;
       }
     };
-    load_rows(0, nxt_rows);
-    for (int kb = 0; kb < KB; kb++) {
+    if (KB > 0) load_rows(kb0, nxt_rows);
+    for (int it = 0; it < KB; it++) {
+      const int kb = kb0 + it;
       int rows[4] = {nxt_rows[0], nxt_rows[1], nxt_rows[2], nxt_rows[3]};
-      if (kb + 1 < KB) load_rows(kb + 1, nxt_rows);
-      int s = kb % ST;
-      uint32_t ph = (kb / ST) & 1;
+      if (it + 1 < KB) load_rows(kb + 1, nxt_rows);
+      int s = it % ST;
+      uint32_t ph = (it / ST) & 1;
       if (lane == 0) {
         ptx::mbar_wait(&empty[s], ph ^ 1);
         ptx::mbar_arrive_expect_tx(&full[s], DU_STAGE);
@@ -371,31 +381,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       uint8_t *A = smem + s * DU_STAGE;
       uint8_t *B = A + DU_A_BYTES;
-      if (lane == 0) {
-        ptx::tma_load_2d(&tmZ2, &full[s], A, i0, kb * BK);
-        ptx::tma_load_2d(&tmZ2, &full[s], A + MN_CHUNK, i0 + 64, kb * BK);
-      }
-      if (lane < 16) {
+      if (lane < 2) ptx::tma_load_2d(&tmZ2, &full[s], A + lane * MN_CHUNK, i0 + 64 * lane, kb * BK);
 #pragma unroll
-        for (int ch = 0; ch < 4; ch++)
-          ptx::tma_gather4(&tmH, &full[s], B + ch * MN_CHUNK + lane * 512, jn0 + ch * 64, rows[0], rows[1], rows[2],
-                           rows[3]);
+      for (int c2 = 0; c2 < 2; c2++) {
+        const int ch = ch0 + c2;
+        ptx::tma_gather4(&tmH, &full[s], B + ch * MN_CHUNK + grp * 512, jn0 + ch * 64, rows[0], rows[1], rows[2],
+                         rows[3]);
       }
       __syncwarp();
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_bf16(BM, DU_N, 1, 1);
-      for (int kb = 0; kb < KB; kb++) {
-        int s = kb % ST;
-        uint32_t ph = (kb / ST) & 1;
+      for (int it = 0; it < KB; it++) {
+        int s = it % ST;
+        uint32_t ph = (it / ST) & 1;
         ptx::mbar_wait(&full[s], ph);
         ptx::tc_fence_after();
         uint32_t a0 = ptx::smem_u32(smem + s * DU_STAGE), b0 = a0 + DU_A_BYTES;
 #pragma unroll
         for (int k = 0; k < BK / 16; k++)
           ptx::umma_bf16(tbase, ptx::sdesc_sw128(a0 + 2048 * k, MN_CHUNK, 1024),
-                         ptx::sdesc_sw128(b0 + 2048 * k, MN_CHUNK, 1024), idesc, (kb | k) != 0);
+                         ptx::sdesc_sw128(b0 + 2048 * k, MN_CHUNK, 1024), idesc, (it | k) != 0);
         ptx::umma_commit(&empty[s]);
       }
       ptx::umma_commit(&tfull);
@@ -405,7 +412,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::mbar_wait(&tfull, 0);
     ptx::tc_fence_after();
     const int i = i0 + q * 32 + lane;
-    const bool valid = i < Mg && KB > 0;
     const uint32_t tl = tbase + ((uint32_t)(q * 32) << 16);
     float *out = dU + (int64_t)i * 2 * S + half * S;
 #pragma unroll 1
@@ -415,15 +421,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tmem_ld_wait();
       int j = jn0 + nc * 8;
       if (i >= Mg || j >= S) continue;
-      for (int u = 0; u < 8 && j + u < S; u++) {
-        float x = valid ? v[u] : 0.f;
-        out[j + u] = accumulate ? out[j + u] + x : x;
+      if (KB == 0) {
+#pragma unroll
+        for (int u = 0; u < 8; u++) v[u] = 0.f;
+      }
+      if (j + 8 <= S && (S & 3) == 0 && !accumulate) {
+        *reinterpret_cast<float4 *>(out + j) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4 *>(out + j + 4) = make_float4(v[4], v[5], v[6], v[7]);
+      } else {
+        for (int u = 0; u < 8 && j + u < S; u++) out[j + u] = accumulate ? out[j + u] + v[u] : v[u];
       }
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc(tbase, 256); }
+}
+
+// out[i] = (accumulate ? out[i] : 0) + sum_{s < nsplit} part[s][i]   (fixed order)
+__global__ void k_reduce_splits(int64_t n, int nsplit, const float *__restrict__ part, float *__restrict__ out,
+                                int accumulate) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i4 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i4 < n; i4 += stride * 4) {
+    if (i4 + 4 <= n) {
+      float4 acc = accumulate ? *reinterpret_cast<const float4 *>(out + i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s = 0; s < nsplit; s++) {
+        float4 v = *reinterpret_cast<const float4 *>(part + (int64_t)s * n + i4);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+      *reinterpret_cast<float4 *>(out + i4) = acc;
+    } else {
+      for (int64_t i = i4; i < n; i++) {
+        float acc = accumulate ? out[i] : 0.f;
+        for (int s = 0; s < nsplit; s++) acc += part[(int64_t)s * n + i];
+        out[i] = acc;
+      }
+    }
+  }
 }
 
 // =================================================================== weight prep
@@ -497,7 +531,7 @@ fold_status launch_fwd(int r0, int r1, int nl, const int32_t *gather, int S, int
   FOLD_TRY(make_map(&tmU, w.U, (uint64_t)w.ld_u, (uint64_t)GATES * S, (uint64_t)w.ld_u * 2, BK, W));
   auto kern = k_cell_fwd_tc<GATES, W>;
   FOLD_TRY(set_smem(kern, Cfg::SMEM));
-  dim3 grid((unsigned)cdiv(r1 - r0, BM), (unsigned)cdiv(S, W));
+  dim3 grid((unsigned)cdiv(S, W), (unsigned)cdiv(r1 - r0, BM));
   int KBh = (int)cdiv(S, BK);
   kern<<<grid, kThreads, Cfg::SMEM, st>>>(tmH, tmU, r0, r1, nl, S, w.ld_u / 2, ld, KBh, gather, b, H, C, Gact, ld_g);
   FOLD_LAUNCH_CHECK();
@@ -542,15 +576,42 @@ fold_status tc_gemm_dA(int c0, int M, int n_cells, int S, int gates, const __nv_
   return FOLD_OK;
 }
 
+int tc_dU_splits(int n_cells, int gates, int S) {
+  int64_t tiles = 2 * cdiv(S, DU_N) * cdiv((int64_t)gates * S, BM);
+  int64_t kbs = cdiv(n_cells, BK);
+  int64_t want = cdiv(4 * 148, tiles);           // >= ~4 waves of CTAs in total
+  int64_t cap = kbs / 32;                         // keep >= 32 k-blocks (2048 cells) per split
+  int64_t sp = want < cap ? want : cap;
+  if (sp > 16) sp = 16;
+  return sp < 1 ? 1 : (int)sp;
+}
+
 fold_status tc_gemm_dU(int n_cells, int nl, int S, int gates, const __nv_bfloat16 *dZ, int ld_z, const int32_t *gather,
-                       const __nv_bfloat16 *H, int ld, int n_rows_total, float *dU, int accumulate, cudaStream_t st) {
+                       const __nv_bfloat16 *H, int ld, int n_rows_total, float *dU, int accumulate, float *split_ws,
+                       cudaStream_t st) {
   CUtensorMap tmZ2, tmH;
   FOLD_TRY(make_map(&tmZ2, dZ, (uint64_t)gates * S, (uint64_t)(n_cells > 0 ? n_cells : 1), (uint64_t)ld_z * 2, 64, BK));
   FOLD_TRY(make_map(&tmH, H, (uint64_t)S, (uint64_t)n_rows_total, (uint64_t)ld * 2, 64, 1));
   FOLD_TRY(set_smem(k_gemm_dU_tc, DU_SMEM));
-  int NT = (int)cdiv(S, DU_N);
-  dim3 grid((unsigned)(2 * NT), (unsigned)cdiv(gates * S, BM));
-  k_gemm_dU_tc<<<grid, kThreads, DU_SMEM, st>>>(tmZ2, tmH, n_cells, nl, S, gates * S, NT, gather, dU, accumulate);
+  const int NT = (int)cdiv(S, DU_N);
+  const int splits = tc_dU_splits(n_cells, gates, S);
+  const int KBall = (int)cdiv(n_cells, BK);
+  const int kbps = (int)cdiv(KBall, splits);
+  dim3 grid((unsigned)(2 * NT), (unsigned)cdiv(gates * S, BM), (unsigned)splits);
+  const int64_t n = (int64_t)gates * S * 2 * S;
+  if (splits == 1) {
+    k_gemm_dU_tc<<<grid, kThreads, DU_SMEM, st>>>(tmZ2, tmH, n_cells, nl, S, gates * S, NT, kbps, gather, dU, 0,
+                                                  accumulate);
+    FOLD_LAUNCH_CHECK();
+    return FOLD_OK;
+  }
+  if (!split_ws) return FOLD_E_WORKSPACE;
+  k_gemm_dU_tc<<<grid, kThreads, DU_SMEM, st>>>(tmZ2, tmH, n_cells, nl, S, gates * S, NT, kbps, gather, split_ws, n,
+                                                0);
+  FOLD_LAUNCH_CHECK();
+  int64_t blocks = cdiv(cdiv(n, 4), 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_reduce_splits<<<(unsigned)blocks, 256, 0, st>>>(n, splits, split_ws, dU, accumulate);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
