@@ -90,6 +90,9 @@ ActsLayout acts_layout(const fold_schedule_t *s, const fold_model *m) {
   L.h_off = off; off = a256(off + (size_t)(N + 1) * L.ld * L.helem);
   L.c_off = off; off = a256(off + (size_t)(N + 1) * L.ld * 4);
   L.g_off = off; off = a256(off + (size_t)(nc + 1) * L.ld_g * L.helem);
+  const bool planes = m->prec == FOLD_PREC_BF16;
+  L.al_off = off; off = a256(off + (planes ? (size_t)(nc + 1) * L.ld * 2 : 0));
+  L.ar_off = off; off = a256(off + (planes ? (size_t)(nc + 1) * L.ld * 2 : 0));
   L.bytes = off;
   return L;
 }
@@ -145,9 +148,10 @@ fold_status fold_forward(const fold_schedule_t *s, const fold_model *m, void *ac
   float *C = (float *)(a + L.c_off);
   void *Gact = a + L.g_off;
   const int32_t *lo = s->level_off_host;
+  ScatterA sc{s->cons_off, s->cons_edge, (__nv_bfloat16 *)(a + L.al_off), (__nv_bfloat16 *)(a + L.ar_off), L.ld};
   {
     ProfScope ps(K_EMBED_FWD, st);
-    FOLD_TRY(launch_embed_fwd(bf16, lo[1], lo[2], s->leaf_token, m->E, S, L.ld, H, C, st));
+    FOLD_TRY(launch_embed_fwd(bf16, lo[1], lo[2], s->leaf_token, m->E, S, L.ld, H, C, bf16 ? &sc : nullptr, st));
   }
   if (bf16) {
     TcWeights w{};
@@ -161,8 +165,8 @@ fold_status fold_forward(const fold_schedule_t *s, const fold_model *m, void *ac
     }
     for (int d = 2; d <= D; d++) {
       ProfScope ps(K_CELL_FWD, st);
-      FOLD_TRY(tc_cell_fwd(m->cell, lo[d], lo[d + 1], nl, s->gather, S, L.ld, w, m->b, (__nv_bfloat16 *)H, N, C,
-                           (__nv_bfloat16 *)Gact, L.ld_g, st));
+      FOLD_TRY(tc_cell_fwd(m->cell, lo[d], lo[d + 1], nl, s->n_cells, s->gather, S, L.ld, w, m->b,
+                           (__nv_bfloat16 *)H, C, (__nv_bfloat16 *)Gact, L.ld_g, sc, st));
     }
   } else {
     for (int d = 2; d <= D; d++) {
@@ -242,8 +246,10 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
   {
   ProfScope ps(K_GEMM_DU, st);
   if (bf16)
-    FOLD_TRY(tc_gemm_dU(nc, nl, S, gates, (const __nv_bfloat16 *)b.dZ, b.ld_z, s->gather, (const __nv_bfloat16 *)H,
-                        L.ld, N, grads->dU, acc, b.dU_split, st));
+    FOLD_TRY(tc_gemm_dU(nc, S, gates, (const __nv_bfloat16 *)b.dZ, b.ld_z,
+                        ScatterA{s->cons_off, s->cons_edge, (__nv_bfloat16 *)(a + L.al_off),
+                                 (__nv_bfloat16 *)(a + L.ar_off), L.ld},
+                        grads->dU, acc, b.dU_split, st));
   else
     FOLD_TRY(launch_gemm_dU_simt(nc, nl, S, gates, (const float *)b.dZ, b.ld_z, s->gather, (const float *)H, L.ld,
                                  grads->dU, acc, st));

@@ -18,10 +18,12 @@ inline unsigned grid_cap(int64_t blocks) {
 }
 
 // ---------------------------------------------------------------- embedding forward
-// H[r] = E[token[perm[r]]], C[r] = 0 for the level-1 rows [r0, r1). One warp per row.
+// H[r] = E[leaf_token[r]], C[r] = 0 for the level-1 rows [r0, r1). One warp per row.
+// BF16 path (sc != null): h is also pushed to the A-operand row of every consumer edge.
 template <typename T>
 __global__ void k_embed_fwd(int r0, int r1, const int32_t *__restrict__ leaf_token,
-                            const float *__restrict__ E, int S, int ld, T *__restrict__ H, float *__restrict__ C) {
+                            const float *__restrict__ E, int S, int ld, T *__restrict__ H, float *__restrict__ C,
+                            ScatterA sc, int has_sc) {
   int lane = threadIdx.x & 31;
   int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -30,6 +32,8 @@ __global__ void k_embed_fwd(int r0, int r1, const int32_t *__restrict__ leaf_tok
     const float *e = E + (int64_t)tok * S;
     T *h = H + r * ld;
     float *c = C + r * ld;
+    int e0 = 0, e1 = 0;
+    if (has_sc) { e0 = sc.cons_off[r]; e1 = sc.cons_off[r + 1]; }
     if ((S & 3) == 0) {
       for (int j = lane * 4; j < S; j += 128) {
         float4 v = *reinterpret_cast<const float4 *>(e + j);
@@ -39,13 +43,28 @@ __global__ void k_embed_fwd(int r0, int r1, const int32_t *__restrict__ leaf_tok
           pk.x = *reinterpret_cast<uint32_t *>(&a);
           pk.y = *reinterpret_cast<uint32_t *>(&b2);
           *reinterpret_cast<uint2 *>(h + j) = pk;
+          for (int q = e0; q < e1; q++) {
+            int ed = sc.cons_edge[q];
+            __nv_bfloat16 *dst = ((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld + j;
+            *reinterpret_cast<uint2 *>(dst) = pk;
+          }
         } else {
           *reinterpret_cast<float4 *>(h + j) = v;
         }
         *reinterpret_cast<float4 *>(c + j) = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     } else {
-      for (int j = lane; j < S; j += 32) { h[j] = from_f<T>(e[j]); c[j] = 0.f; }
+      for (int j = lane; j < S; j += 32) {
+        T hv = from_f<T>(e[j]);
+        h[j] = hv;
+        c[j] = 0.f;
+        if constexpr (sizeof(T) == 2) {
+          for (int q = e0; q < e1; q++) {
+            int ed = sc.cons_edge[q];
+            (((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld)[j] = hv;
+          }
+        }
+      }
     }
   }
 }
@@ -467,11 +486,14 @@ __global__ void k_zero(uint32_t *p, int64_t n) {
 
 // ================================================================= launchers
 fold_status launch_embed_fwd(bool bf16, int r0, int r1, const int32_t *leaf_token, const float *E, int S, int ld,
-                             void *H, float *C, cudaStream_t st) {
+                             void *H, float *C, const ScatterA *sc, cudaStream_t st) {
   if (r1 <= r0) return FOLD_OK;
   unsigned g = grid_cap(cdiv((int64_t)(r1 - r0) * 32, 256));
-  if (bf16) k_embed_fwd<__nv_bfloat16><<<g, 256, 0, st>>>(r0, r1, leaf_token, E, S, ld, (__nv_bfloat16 *)H, C);
-  else k_embed_fwd<float><<<g, 256, 0, st>>>(r0, r1, leaf_token, E, S, ld, (float *)H, C);
+  ScatterA s0{};
+  if (bf16)
+    k_embed_fwd<__nv_bfloat16><<<g, 256, 0, st>>>(r0, r1, leaf_token, E, S, ld, (__nv_bfloat16 *)H, C,
+                                                  sc ? *sc : s0, sc ? 1 : 0);
+  else k_embed_fwd<float><<<g, 256, 0, st>>>(r0, r1, leaf_token, E, S, ld, (float *)H, C, s0, 0);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }

@@ -4,9 +4,20 @@
 
 namespace fold {
 
+// Consumer-side operand planes (BF16 path): the forward "gather" is done at production
+// time — every produced row r is also written to the A operand row of each consumer edge
+// e = 2c + k in cons(r): A_k[c] = h(r). Level d's GEMM then reads its A rows
+// [c0, c0 + M_d) of A_L / A_R densely with TMA (no gather on the MMA critical path), and
+// the weight-gradient GEMM reads the same planes as its dense B operand.
+struct ScatterA {
+  const int32_t *cons_off, *cons_edge;
+  __nv_bfloat16 *AL, *AR;  // [n_cells][ld] each
+  int ld;
+};
+
 // Activation / workspace layouts (pure functions of the schedule and model).
 struct ActsLayout {
-  size_t bytes, h_off, c_off, g_off;
+  size_t bytes, h_off, c_off, g_off, al_off, ar_off;
   int ld;       // H, C row stride (elements)
   int ld_g;     // G row stride (elements) = round_up(gates*S, 8)
   int helem;    // bytes per H / G element
@@ -17,7 +28,7 @@ inline int gates_of(int cell) { return cell == FOLD_CELL_TREELSTM ? 5 : 1; }
 
 // --- SIMT / shared kernels (exec.cu)
 fold_status launch_embed_fwd(bool bf16, int r0, int r1, const int32_t *leaf_token, const float *E, int S, int ld,
-                             void *H, float *C, cudaStream_t st);
+                             void *H, float *C, const ScatterA *sc, cudaStream_t st);
 fold_status launch_cell_fwd_simt(int cell, int r0, int r1, const int32_t *gather, int S, int ld,
                                  const float *U, const float *b, float *H, float *C, float *Gact, int ld_g,
                                  int nl, cudaStream_t st);
@@ -52,16 +63,15 @@ struct TcWeights {  // bf16 copies made per call
   int ld_u, ld_ut;
 };
 fold_status tc_prepare_U(int gates, int S, const float *U, TcWeights &w, bool transpose, cudaStream_t st);
-fold_status tc_cell_fwd(int cell, int r0, int r1, int nl, const int32_t *gather, int S, int ld,
-                        const TcWeights &w, const float *b, __nv_bfloat16 *H, int n_rows_total, float *C,
-                        __nv_bfloat16 *Gact, int ld_g, cudaStream_t st);
+fold_status tc_cell_fwd(int cell, int r0, int r1, int nl, int n_cells, const int32_t *gather, int S, int ld,
+                        const TcWeights &w, const float *b, __nv_bfloat16 *H, float *C, __nv_bfloat16 *Gact,
+                        int ld_g, const ScatterA &sc, cudaStream_t st);
 fold_status tc_gemm_dA(int c0, int M, int n_cells, int S, int gates, const __nv_bfloat16 *dZ, int ld_z,
                        const TcWeights &w, float *dA, cudaStream_t st);
 // split-K over cells into split_ws [splits][gates*S][2S] (fp32), then a fixed-order sum
 int tc_dU_splits(int n_cells, int gates, int S);
-fold_status tc_gemm_dU(int n_cells, int nl, int S, int gates, const __nv_bfloat16 *dZ, int ld_z,
-                       const int32_t *gather, const __nv_bfloat16 *H, int ld, int n_rows_total, float *dU,
-                       int accumulate, float *split_ws, cudaStream_t st);
+fold_status tc_gemm_dU(int n_cells, int S, int gates, const __nv_bfloat16 *dZ, int ld_z, const ScatterA &sc,
+                       float *dU, int accumulate, float *split_ws, cudaStream_t st);
 size_t tc_workspace_bytes(int gates, int S);
 
 }  // namespace fold

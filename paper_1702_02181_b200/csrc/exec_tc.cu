@@ -1,15 +1,19 @@
 // exec_tc.cu — tcgen05 (5th-gen tensor core) kernels for the BF16 path.
 //
 //  k_cell_fwd_tc   one level of the forward (gather -> operation -> concat)
-//                  fused in one kernel: TMA tile::gather4 pulls the child rows
-//                  [H[gL] | H[gR]] of 128 pool rows straight into 128B-swizzled smem
-//                  (the gather), tcgen05.mma multiplies them with a gate-interleaved
-//                  slab of U into a TMEM accumulator (the batched cell), and the epilogue
-//                  warps apply the gates and write the level's contiguous pool rows
-//                  (the concat becomes an append).
+//                  in one kernel. The gather is moved to production time: whoever
+//                  produces a pool row (embedding kernel, or this kernel's epilogue for
+//                  the previous level) also writes it into the A-operand row of each
+//                  consumer edge (planes A_L / A_R, row = consumer cell). So the level's
+//                  A rows are contiguous and TMA streams them as dense 128B-swizzled boxes;
+//                  tcgen05.mma multiplies them with a gate-interleaved slab of U into a
+//                  TMEM accumulator; the epilogue warps apply the gates, append (h, c) to
+//                  the level's pool rows (the concat becomes an append) and push h to its
+//                  consumers' A rows.
 //  k_gemm_dA_tc    backward edge gradients of one level: dA = dZ_level * U  (K-major).
-//  k_gemm_dU_tc    weight gradient over all cells at once: dU = dZ^T * [H[gL] | H[gR]],
-//                  both operands MN-major, the H operand row-gathered by TMA.
+//  k_gemm_dU_tc    weight gradient over all cells at once: dU = dZ^T * [A_L | A_R], both
+//                  operands MN-major dense TMA boxes; split-K over cells with a
+//                  fixed-order reduction (deterministic).
 // Warp roles (256 threads): warp 0 TMA producer, warp 1 MMA issuer (one lane),
 // warp 2 TMEM allocator, warps 4-7 epilogue (warp w reads TMEM lanes 32(w%4)..+31).
 #include <cudaTypedefs.h>
@@ -52,9 +56,10 @@ struct FwdCfg {
 
 template <int GATES, int W>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_cell_fwd_tc(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmU, int r0, int r1,
-                  int nl, int S, int Sp, int ld, int KBh, const int32_t *__restrict__ gather, const float *__restrict__ bias,
-                  __nv_bfloat16 *__restrict__ H, float *__restrict__ C, __nv_bfloat16 *__restrict__ Gact, int ld_g) {
+    k_cell_fwd_tc(const __grid_constant__ CUtensorMap tmAL, const __grid_constant__ CUtensorMap tmAR,
+                  const __grid_constant__ CUtensorMap tmU, int r0, int r1, int nl, int S, int Sp, int ld, int KBh,
+                  const int32_t *__restrict__ gather, const float *__restrict__ bias, __nv_bfloat16 *__restrict__ H,
+                  float *__restrict__ C, __nv_bfloat16 *__restrict__ Gact, int ld_g, ScatterA sc) {
   using Cfg = FwdCfg<GATES, W>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
@@ -65,8 +70,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // grid.x = state-column tile (fast), grid.y = row tile: the CTAs of one wave share few
-  // gathered A tiles, which stay in L2 across the N tiles; U (21 MB bf16) is L2-resident.
+  // A tiles, which stay in L2 across the N tiles; U (21 MB bf16 at S=1024) is L2-resident.
   const int m0 = r0 + blockIdx.y * BM, j0 = blockIdx.x * W;
+  const int c0 = m0 - nl;  // first cell (A-plane row) of this tile
 
   if (tid < BM) {
     int r = m0 + tid;
@@ -82,7 +88,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < ST; s++) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
     ptx::mbar_init(&tfull, 1);
     ptx::fence_mbar_init();
-    ptx::prefetch_tmap(&tmH);
+    ptx::prefetch_tmap(&tmAL);
+    ptx::prefetch_tmap(&tmAR);
     ptx::prefetch_tmap(&tmU);
   }
   if (warp == 2) {
@@ -96,24 +103,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int KB = 2 * KBh;
 
   if (warp == 0) {
-    // Producer warp: lane 0 arms the stage barrier, then all 32 lanes issue in parallel
-    // (lane q: gather4 of tile rows 4q..4q+3; lanes < GATES: one U gate slab each).
-    for (int kb = 0; kb < KB; kb++) {
-      int s = kb % ST;
-      uint32_t ph = (kb / ST) & 1;
-      if (lane == 0) {
+    // TMA producer: per stage one dense box of 128 A rows (the level's contiguous cell rows
+    // of the left / right operand plane) + GATES boxes of W rows of U (gate-interleaved N).
+    if (lane == 0) {
+      for (int kb = 0; kb < KB; kb++) {
+        int s = kb % ST;
+        uint32_t ph = (kb / ST) & 1;
         ptx::mbar_wait(&empty[s], ph ^ 1);
         ptx::mbar_arrive_expect_tx(&full[s], Cfg::STAGE);
+        int half = kb >= KBh;
+        int kc = (kb - half * KBh) * BK;
+        uint8_t *A = smem + s * Cfg::STAGE;
+        uint8_t *B = A + Cfg::A_BYTES;
+        ptx::tma_load_2d(half ? &tmAR : &tmAL, &full[s], A, kc, c0);
+#pragma unroll
+        for (int g = 0; g < GATES; g++) ptx::tma_load_2d(&tmU, &full[s], B + g * W * 128, half * Sp + kc, g * S + j0);
       }
-      __syncwarp();
-      int half = kb >= KBh;
-      int kc = (kb - half * KBh) * BK;
-      uint8_t *A = smem + s * Cfg::STAGE;
-      uint8_t *B = A + Cfg::A_BYTES;
-      const int *gi = gidx[half] + 4 * lane;
-      ptx::tma_gather4(&tmH, &full[s], A + lane * 512, kc, gi[0], gi[1], gi[2], gi[3]);
-      if (lane < GATES) ptx::tma_load_2d(&tmU, &full[s], B + lane * W * 128, half * Sp + kc, lane * S + j0);
-      __syncwarp();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -133,14 +138,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::umma_commit(&tfull);
     }
   } else if (warp >= 4) {
+    // Epilogue: TMEM lane = tile row; gates -> (h, c); append to the level's pool rows and
+    // push h to the A-operand row of every consumer edge (the next levels' "gather").
     const int q = warp & 3;
-    ptx::mbar_wait(&tfull, 0);
-    ptx::tc_fence_after();
     const int row = q * 32 + lane;
     const int64_t r = m0 + row;
     const bool valid = r < r1;
     const int64_t gl = gidx[0][row], gr = gidx[1][row];
     const int64_t c = r - nl;
+    const int ce0 = valid ? sc.cons_off[r] : 0, ce1 = valid ? sc.cons_off[r + 1] : 0;
+    ptx::mbar_wait(&tfull, 0);
+    ptx::tc_fence_after();
     const uint32_t tl = tbase + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
     for (int jc = 0; jc < W / 8; jc++) {
@@ -152,21 +160,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int jb = j0 + jc * 8;
       if (jb >= S) continue;
       const bool fullc = (jb + 8 <= S) && ((S & 7) == 0);
+      float hh[8];
       if constexpr (GATES == 1) {
-        float h[8];
 #pragma unroll
-        for (int u = 0; u < 8; u++) h[u] = tanhf(z[0][u] + sbias[jc * 8 + u]);
+        for (int u = 0; u < 8; u++) hh[u] = tanhf(z[0][u] + sbias[jc * 8 + u]);
         if (fullc) {
-          uint4 pk = make_uint4(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]), pack_bf16x2(h[4], h[5]),
-                                pack_bf16x2(h[6], h[7]));
-          *reinterpret_cast<uint4 *>(H + r * ld + jb) = pk;
+          uint4 pk = make_uint4(pack_bf16x2(hh[0], hh[1]), pack_bf16x2(hh[2], hh[3]), pack_bf16x2(hh[4], hh[5]),
+                                pack_bf16x2(hh[6], hh[7]));
           *reinterpret_cast<uint4 *>(Gact + c * ld_g + jb) = pk;
           *reinterpret_cast<float4 *>(C + r * ld + jb) = make_float4(0.f, 0.f, 0.f, 0.f);
           *reinterpret_cast<float4 *>(C + r * ld + jb + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
         } else {
           for (int u = 0; u < 8 && jb + u < S; u++) {
-            H[r * ld + jb + u] = __float2bfloat16_rn(h[u]);
-            Gact[c * ld_g + jb + u] = __float2bfloat16_rn(h[u]);
+            Gact[c * ld_g + jb + u] = __float2bfloat16_rn(hh[u]);
             C[r * ld + jb + u] = 0.f;
           }
         }
@@ -187,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             cr[u] = ok ? C[gr * ld + jb + u] : 0.f;
           }
         }
-        float gi[8], gfl[8], gfr[8], go[8], gu[8], hh[8], cc[8];
+        float gi[8], gfl[8], gfr[8], go[8], gu[8], cc[8];
 #pragma unroll
         for (int u = 0; u < 8; u++) {
           const int jj = jc * 8 + u;
@@ -201,8 +207,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __nv_bfloat16 *ga = Gact + c * ld_g;
         if (fullc) {
-          *reinterpret_cast<uint4 *>(H + r * ld + jb) = make_uint4(
-              pack_bf16x2(hh[0], hh[1]), pack_bf16x2(hh[2], hh[3]), pack_bf16x2(hh[4], hh[5]), pack_bf16x2(hh[6], hh[7]));
           *reinterpret_cast<float4 *>(C + r * ld + jb) = make_float4(cc[0], cc[1], cc[2], cc[3]);
           *reinterpret_cast<float4 *>(C + r * ld + jb + 4) = make_float4(cc[4], cc[5], cc[6], cc[7]);
           float *gs[5] = {gi, gfl, gfr, go, gu};
@@ -214,13 +218,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           for (int u = 0; u < 8 && jb + u < S; u++) {
             int j = jb + u;
-            H[r * ld + j] = __float2bfloat16_rn(hh[u]);
             C[r * ld + j] = cc[u];
             ga[j] = __float2bfloat16_rn(gi[u]);
             ga[S + j] = __float2bfloat16_rn(gfl[u]);
             ga[2 * S + j] = __float2bfloat16_rn(gfr[u]);
             ga[3 * S + j] = __float2bfloat16_rn(go[u]);
             ga[4 * S + j] = __float2bfloat16_rn(gu[u]);
+          }
+        }
+      }
+      // h: pool row (append) + every consumer's A-operand row (push-gather)
+      if (fullc) {
+        uint4 pk = make_uint4(pack_bf16x2(hh[0], hh[1]), pack_bf16x2(hh[2], hh[3]), pack_bf16x2(hh[4], hh[5]),
+                              pack_bf16x2(hh[6], hh[7]));
+        *reinterpret_cast<uint4 *>(H + r * ld + jb) = pk;
+        for (int e = ce0; e < ce1; e++) {
+          int ed = sc.cons_edge[e];
+          *reinterpret_cast<uint4 *>(((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld + jb) = pk;
+        }
+      } else {
+        for (int u = 0; u < 8 && jb + u < S; u++) {
+          __nv_bfloat16 hv = __float2bfloat16_rn(hh[u]);
+          H[r * ld + jb + u] = hv;
+          for (int e = ce0; e < ce1; e++) {
+            int ed = sc.cons_edge[e];
+            (((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld)[jb + u] = hv;
           }
         }
       }
@@ -328,8 +350,8 @@ constexpr int DU_SMEM = ST * DU_STAGE + 1024;
 constexpr int MN_CHUNK = 64 * 128;       // bytes per 64-element MN chunk of 64 K rows
 
 __global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_dU_tc(const __grid_constant__ CUtensorMap tmZ2, const __grid_constant__ CUtensorMap tmH, int n_cells,
-                 int nl, int S, int Mg, int NT, int kb_per_split, const int32_t *__restrict__ gather,
+    k_gemm_dU_tc(const __grid_constant__ CUtensorMap tmZ2, const __grid_constant__ CUtensorMap tmAL,
+                 const __grid_constant__ CUtensorMap tmAR, int n_cells, int S, int Mg, int NT, int kb_per_split,
                  float *__restrict__ out_base, int64_t split_stride, int accumulate) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
@@ -349,47 +371,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::mbar_init(&tfull, 1);
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tmZ2);
-    ptx::prefetch_tmap(&tmH);
+    ptx::prefetch_tmap(&tmAL);
+    ptx::prefetch_tmap(&tmAR);
   }
   if (warp == 2) { ptx::tmem_alloc(&tmem_base_sh, 256); ptx::tmem_relinquish(); }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = tmem_base_sh;
-  if (warp == 0) {
-    // whole warp: lane l gathers the 4 cells 4(l&15)..+3 for MN chunks 2(l>>4), 2(l>>4)+1
-    const int grp = lane & 15, ch0 = 2 * (lane >> 4);
-    int nxt_rows[4];
-    auto load_rows = [&](int kb, int (&rows)[4]) {
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        int cidx = kb * BK + 4 * grp + u;
-        rows[u] = cidx < n_cells ? gather[2 * ((int64_t)nl + cidx) + half] : 0;
-      }
-    };
-    if (KB > 0) load_rows(kb0, nxt_rows);
+  if (warp == 0 && lane == 0) {
+    // A' = dZ^T chunk (2 boxes of 64 gate-rows x 64 cells), B' = the cells' [h_L | h_R]
+    // rows from the A operand planes written by the forward (4 boxes of 64 cols x 64 cells)
+    const CUtensorMap *tmB = half ? &tmAR : &tmAL;
     for (int it = 0; it < KB; it++) {
       const int kb = kb0 + it;
-      int rows[4] = {nxt_rows[0], nxt_rows[1], nxt_rows[2], nxt_rows[3]};
-      if (it + 1 < KB) load_rows(kb + 1, nxt_rows);
       int s = it % ST;
       uint32_t ph = (it / ST) & 1;
-      if (lane == 0) {
-        ptx::mbar_wait(&empty[s], ph ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[s], DU_STAGE);
-      }
-      __syncwarp();
+      ptx::mbar_wait(&empty[s], ph ^ 1);
+      ptx::mbar_arrive_expect_tx(&full[s], DU_STAGE);
       uint8_t *A = smem + s * DU_STAGE;
       uint8_t *B = A + DU_A_BYTES;
-      if (lane < 2) ptx::tma_load_2d(&tmZ2, &full[s], A + lane * MN_CHUNK, i0 + 64 * lane, kb * BK);
+      ptx::tma_load_2d(&tmZ2, &full[s], A, i0, kb * BK);
+      ptx::tma_load_2d(&tmZ2, &full[s], A + MN_CHUNK, i0 + 64, kb * BK);
 #pragma unroll
-      for (int c2 = 0; c2 < 2; c2++) {
-        const int ch = ch0 + c2;
-        ptx::tma_gather4(&tmH, &full[s], B + ch * MN_CHUNK + grp * 512, jn0 + ch * 64, rows[0], rows[1], rows[2],
-                         rows[3]);
-      }
-      __syncwarp();
+      for (int ch = 0; ch < 4; ch++) ptx::tma_load_2d(tmB, &full[s], B + ch * MN_CHUNK, jn0 + ch * 64, kb * BK);
     }
+  } else if (warp == 0) {
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_bf16(BM, DU_N, 1, 1);
@@ -522,18 +529,20 @@ fold_status set_smem(K kernel, int bytes) {
 }
 
 template <int GATES, int W>
-fold_status launch_fwd(int r0, int r1, int nl, const int32_t *gather, int S, int ld, const TcWeights &w,
-                       const float *b, __nv_bfloat16 *H, int n_rows_total, float *C, __nv_bfloat16 *Gact, int ld_g,
+fold_status launch_fwd(int r0, int r1, int nl, int n_cells, const int32_t *gather, int S, int ld, const TcWeights &w,
+                       const float *b, __nv_bfloat16 *H, float *C, __nv_bfloat16 *Gact, int ld_g, const ScatterA &sc,
                        cudaStream_t st) {
   using Cfg = FwdCfg<GATES, W>;
-  CUtensorMap tmH, tmU;
-  FOLD_TRY(make_map(&tmH, H, (uint64_t)S, (uint64_t)n_rows_total, (uint64_t)ld * 2, BK, 1));
+  CUtensorMap tmAL, tmAR, tmU;
+  FOLD_TRY(make_map(&tmAL, sc.AL, (uint64_t)S, (uint64_t)n_cells, (uint64_t)sc.ld * 2, BK, BM));
+  FOLD_TRY(make_map(&tmAR, sc.AR, (uint64_t)S, (uint64_t)n_cells, (uint64_t)sc.ld * 2, BK, BM));
   FOLD_TRY(make_map(&tmU, w.U, (uint64_t)w.ld_u, (uint64_t)GATES * S, (uint64_t)w.ld_u * 2, BK, W));
   auto kern = k_cell_fwd_tc<GATES, W>;
   FOLD_TRY(set_smem(kern, Cfg::SMEM));
   dim3 grid((unsigned)cdiv(S, W), (unsigned)cdiv(r1 - r0, BM));
   int KBh = (int)cdiv(S, BK);
-  kern<<<grid, kThreads, Cfg::SMEM, st>>>(tmH, tmU, r0, r1, nl, S, w.ld_u / 2, ld, KBh, gather, b, H, C, Gact, ld_g);
+  kern<<<grid, kThreads, Cfg::SMEM, st>>>(tmAL, tmAR, tmU, r0, r1, nl, S, w.ld_u / 2, ld, KBh, gather, b, H, C, Gact,
+                                          ld_g, sc);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
@@ -553,13 +562,13 @@ fold_status tc_prepare_U(int gates, int S, const float *U, TcWeights &w, bool tr
   return FOLD_OK;
 }
 
-fold_status tc_cell_fwd(int cell, int r0, int r1, int nl, const int32_t *gather, int S, int ld, const TcWeights &w,
-                        const float *b, __nv_bfloat16 *H, int n_rows_total, float *C, __nv_bfloat16 *Gact, int ld_g,
-                        cudaStream_t st) {
+fold_status tc_cell_fwd(int cell, int r0, int r1, int nl, int n_cells, const int32_t *gather, int S, int ld,
+                        const TcWeights &w, const float *b, __nv_bfloat16 *H, float *C, __nv_bfloat16 *Gact, int ld_g,
+                        const ScatterA &sc, cudaStream_t st) {
   if (r1 <= r0) return FOLD_OK;
   if (cell == FOLD_CELL_TREELSTM)
-    return launch_fwd<5, 32>(r0, r1, nl, gather, S, ld, w, b, H, n_rows_total, C, Gact, ld_g, st);
-  return launch_fwd<1, 128>(r0, r1, nl, gather, S, ld, w, b, H, n_rows_total, C, Gact, ld_g, st);
+    return launch_fwd<5, 32>(r0, r1, nl, n_cells, gather, S, ld, w, b, H, C, Gact, ld_g, sc, st);
+  return launch_fwd<1, 128>(r0, r1, nl, n_cells, gather, S, ld, w, b, H, C, Gact, ld_g, sc, st);
 }
 
 fold_status tc_gemm_dA(int c0, int M, int n_cells, int S, int gates, const __nv_bfloat16 *dZ, int ld_z,
@@ -586,12 +595,13 @@ int tc_dU_splits(int n_cells, int gates, int S) {
   return sp < 1 ? 1 : (int)sp;
 }
 
-fold_status tc_gemm_dU(int n_cells, int nl, int S, int gates, const __nv_bfloat16 *dZ, int ld_z, const int32_t *gather,
-                       const __nv_bfloat16 *H, int ld, int n_rows_total, float *dU, int accumulate, float *split_ws,
-                       cudaStream_t st) {
-  CUtensorMap tmZ2, tmH;
-  FOLD_TRY(make_map(&tmZ2, dZ, (uint64_t)gates * S, (uint64_t)(n_cells > 0 ? n_cells : 1), (uint64_t)ld_z * 2, 64, BK));
-  FOLD_TRY(make_map(&tmH, H, (uint64_t)S, (uint64_t)n_rows_total, (uint64_t)ld * 2, 64, 1));
+fold_status tc_gemm_dU(int n_cells, int S, int gates, const __nv_bfloat16 *dZ, int ld_z, const ScatterA &sc,
+                       float *dU, int accumulate, float *split_ws, cudaStream_t st) {
+  CUtensorMap tmZ2, tmAL, tmAR;
+  const uint64_t ncr = (uint64_t)(n_cells > 0 ? n_cells : 1);
+  FOLD_TRY(make_map(&tmZ2, dZ, (uint64_t)gates * S, ncr, (uint64_t)ld_z * 2, 64, BK));
+  FOLD_TRY(make_map(&tmAL, sc.AL, (uint64_t)S, ncr, (uint64_t)sc.ld * 2, 64, BK));
+  FOLD_TRY(make_map(&tmAR, sc.AR, (uint64_t)S, ncr, (uint64_t)sc.ld * 2, 64, BK));
   FOLD_TRY(set_smem(k_gemm_dU_tc, DU_SMEM));
   const int NT = (int)cdiv(S, DU_N);
   const int splits = tc_dU_splits(n_cells, gates, S);
@@ -600,14 +610,13 @@ fold_status tc_gemm_dU(int n_cells, int nl, int S, int gates, const __nv_bfloat1
   dim3 grid((unsigned)(2 * NT), (unsigned)cdiv(gates * S, BM), (unsigned)splits);
   const int64_t n = (int64_t)gates * S * 2 * S;
   if (splits == 1) {
-    k_gemm_dU_tc<<<grid, kThreads, DU_SMEM, st>>>(tmZ2, tmH, n_cells, nl, S, gates * S, NT, kbps, gather, dU, 0,
+    k_gemm_dU_tc<<<grid, kThreads, DU_SMEM, st>>>(tmZ2, tmAL, tmAR, n_cells, S, gates * S, NT, kbps, dU, 0,
                                                   accumulate);
     FOLD_LAUNCH_CHECK();
     return FOLD_OK;
   }
   if (!split_ws) return FOLD_E_WORKSPACE;
-  k_gemm_dU_tc<<<grid, kThreads, DU_SMEM, st>>>(tmZ2, tmH, n_cells, nl, S, gates * S, NT, kbps, gather, split_ws, n,
-                                                0);
+  k_gemm_dU_tc<<<grid, kThreads, DU_SMEM, st>>>(tmZ2, tmAL, tmAR, n_cells, S, gates * S, NT, kbps, split_ws, n, 0);
   FOLD_LAUNCH_CHECK();
   int64_t blocks = cdiv(cdiv(n, 4), 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
