@@ -133,7 +133,8 @@ fold_status fold_schedule(const fold_graphs *graphs, fold_schedule_t *sched,
  *                   [0,S) multiply h_L, [S,2S) multiply h_R.
  *   b[gates*S]      bias.
  *   E[vocab][S]     embedding table (leaf h = E[token], leaf c = 0).
- * BF16 mode converts U to bf16 inside fold_forward / fold_backward (workspace). */
+ * BF16 mode converts U to bf16 inside fold_forward / fold_backward (workspace).
+ * U, b and E must be 16-byte aligned (FOLD_E_INVALID otherwise). */
 typedef struct {
   int32_t cell, prec, S, vocab;
   const float *U, *b, *E;

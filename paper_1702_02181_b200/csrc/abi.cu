@@ -20,6 +20,8 @@ fold_status check_model(const fold_model *m) {
   if (m->cell != FOLD_CELL_TREERNN && m->cell != FOLD_CELL_TREELSTM) return FOLD_E_INVALID;
   if (m->prec != FOLD_PREC_FP32 && m->prec != FOLD_PREC_BF16) return FOLD_E_INVALID;
   if (m->S <= 0 || m->S > 8192 || m->vocab <= 0) return FOLD_E_INVALID;
+  // vectorised loads: parameter arrays must be 16-byte aligned
+  if (((uintptr_t)m->U | (uintptr_t)m->b | (uintptr_t)m->E) & 15) return FOLD_E_INVALID;
   return FOLD_OK;
 }
 

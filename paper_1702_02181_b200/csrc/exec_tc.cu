@@ -48,45 +48,34 @@ struct FwdCfg {
   static constexpr int A_BYTES = BM * 128;
   static constexpr int B_BYTES = N * 128;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int TMEM_COLS = tmem_cols_for(N);
+  static constexpr int ACC_STRIDE = 256;  // TMEM columns per accumulator buffer (2 buffers)
+  static constexpr int TMEM_COLS = 512;
   static constexpr int SMEM = ST * STAGE + 1024;
   static_assert(N % 16 == 0 && N <= 256, "UMMA N for M=128");
   static_assert(W % 8 == 0, "gate slab rows must fill 8-row swizzle atoms");
+  static_assert(SMEM <= 227 * 1024, "smem");
 };
 
+// Persistent: grid = min(#tiles, #SMs); tile t -> (state-column tile t % NT, row tile t / NT)
+// (N fast: the CTAs running concurrently share a few A tiles in L2; U is L2-resident).
+// Two TMEM accumulators: the epilogue of tile i overlaps the MMA main loop of tile i+1.
 template <int GATES, int W>
 __global__ void __launch_bounds__(kThreads, 1)
     k_cell_fwd_tc(const __grid_constant__ CUtensorMap tmAL, const __grid_constant__ CUtensorMap tmAR,
                   const __grid_constant__ CUtensorMap tmU, int r0, int r1, int nl, int S, int Sp, int ld, int KBh,
-                  const int32_t *__restrict__ gather, const float *__restrict__ bias, __nv_bfloat16 *__restrict__ H,
-                  float *__restrict__ C, __nv_bfloat16 *__restrict__ Gact, int ld_g, ScatterA sc) {
+                  int NT, int ntiles, const int32_t *__restrict__ gather, const float *__restrict__ bias,
+                  __nv_bfloat16 *__restrict__ H, float *__restrict__ C, __nv_bfloat16 *__restrict__ Gact, int ld_g,
+                  ScatterA sc) {
   using Cfg = FwdCfg<GATES, W>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
-  __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull;
+  __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ int gidx[2][BM];
-  __shared__ float sbias[GATES * W];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // grid.x = state-column tile (fast), grid.y = row tile: the CTAs of one wave share few
-  // A tiles, which stay in L2 across the N tiles; U (21 MB bf16 at S=1024) is L2-resident.
-  const int m0 = r0 + blockIdx.y * BM, j0 = blockIdx.x * W;
-  const int c0 = m0 - nl;  // first cell (A-plane row) of this tile
-
-  if (tid < BM) {
-    int r = m0 + tid;
-    int rr = r < r1 ? r : r0;
-    gidx[0][tid] = gather[2 * (int64_t)rr];
-    gidx[1][tid] = gather[2 * (int64_t)rr + 1];
-  }
-  for (int i = tid; i < GATES * W; i += kThreads) {
-    int g = i / W, j = j0 + (i - g * W);
-    sbias[i] = j < S ? bias[g * S + j] : 0.f;
-  }
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < ST; s++) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
-    ptx::mbar_init(&tfull, 1);
+    for (int a = 0; a < 2; a++) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 4); }
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tmAL);
     ptx::prefetch_tmap(&tmAR);
@@ -106,146 +95,180 @@ __global__ void __launch_bounds__(kThreads, 1)
     // TMA producer: per stage one dense box of 128 A rows (the level's contiguous cell rows
     // of the left / right operand plane) + GATES boxes of W rows of U (gate-interleaved N).
     if (lane == 0) {
-      for (int kb = 0; kb < KB; kb++) {
-        int s = kb % ST;
-        uint32_t ph = (kb / ST) & 1;
-        ptx::mbar_wait(&empty[s], ph ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[s], Cfg::STAGE);
-        int half = kb >= KBh;
-        int kc = (kb - half * KBh) * BK;
-        uint8_t *A = smem + s * Cfg::STAGE;
-        uint8_t *B = A + Cfg::A_BYTES;
-        ptx::tma_load_2d(half ? &tmAR : &tmAL, &full[s], A, kc, c0);
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int j0 = (t % NT) * W, c0 = (r0 - nl) + (t / NT) * BM;
+        for (int kb = 0; kb < KB; kb++, it++) {
+          int s = it % ST;
+          uint32_t ph = (it / ST) & 1;
+          ptx::mbar_wait(&empty[s], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[s], Cfg::STAGE);
+          int half = kb >= KBh;
+          int kc = (kb - half * KBh) * BK;
+          uint8_t *A = smem + s * Cfg::STAGE;
+          uint8_t *B = A + Cfg::A_BYTES;
+          ptx::tma_load_2d(half ? &tmAR : &tmAL, &full[s], A, kc, c0);
 #pragma unroll
-        for (int g = 0; g < GATES; g++) ptx::tma_load_2d(&tmU, &full[s], B + g * W * 128, half * Sp + kc, g * S + j0);
+          for (int g = 0; g < GATES; g++)
+            ptx::tma_load_2d(&tmU, &full[s], B + g * W * 128, half * Sp + kc, g * S + j0);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_bf16(BM, Cfg::N, 0, 0);
-      for (int kb = 0; kb < KB; kb++) {
-        int s = kb % ST;
-        uint32_t ph = (kb / ST) & 1;
-        ptx::mbar_wait(&full[s], ph);
+      int it = 0, tc = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, tc++) {
+        const int acc = tc & 1;
+        const uint32_t aph = (tc >> 1) & 1;
+        ptx::mbar_wait(&tempty[acc], aph ^ 1);
         ptx::tc_fence_after();
-        uint32_t a0 = ptx::smem_u32(smem + s * Cfg::STAGE), b0 = a0 + Cfg::A_BYTES;
+        const uint32_t dst = tbase + acc * Cfg::ACC_STRIDE;
+        for (int kb = 0; kb < KB; kb++, it++) {
+          int s = it % ST;
+          uint32_t ph = (it / ST) & 1;
+          ptx::mbar_wait(&full[s], ph);
+          ptx::tc_fence_after();
+          uint32_t a0 = ptx::smem_u32(smem + s * Cfg::STAGE), b0 = a0 + Cfg::A_BYTES;
 #pragma unroll
-        for (int k = 0; k < BK / 16; k++)
-          ptx::umma_bf16(tbase, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024), ptx::sdesc_sw128(b0 + 32 * k, 16, 1024),
-                         idesc, (kb | k) != 0);
-        ptx::umma_commit(&empty[s]);
+          for (int k = 0; k < BK / 16; k++)
+            ptx::umma_bf16(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024), ptx::sdesc_sw128(b0 + 32 * k, 16, 1024),
+                           idesc, (kb | k) != 0);
+          ptx::umma_commit(&empty[s]);
+        }
+        ptx::umma_commit(&tfull[acc]);
       }
-      ptx::umma_commit(&tfull);
     }
   } else if (warp >= 4) {
     // Epilogue: TMEM lane = tile row; gates -> (h, c); append to the level's pool rows and
     // push h to the A-operand row of every consumer edge (the next levels' "gather").
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int64_t r = m0 + row;
-    const bool valid = r < r1;
-    const int64_t gl = gidx[0][row], gr = gidx[1][row];
-    const int64_t c = r - nl;
-    const int ce0 = valid ? sc.cons_off[r] : 0, ce1 = valid ? sc.cons_off[r + 1] : 0;
-    ptx::mbar_wait(&tfull, 0);
-    ptx::tc_fence_after();
-    const uint32_t tl = tbase + ((uint32_t)(q * 32) << 16);
+    int tc = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, tc++) {
+      const int acc = tc & 1;
+      const uint32_t aph = (tc >> 1) & 1;
+      const int j0 = (t % NT) * W;
+      const int64_t r = r0 + (int64_t)(t / NT) * BM + row;
+      const bool valid = r < r1;
+      int64_t gl = 0, gr = 0;
+      int ce0 = 0, ce1 = 0;
+      if (valid) {
+        gl = gather[2 * r]; gr = gather[2 * r + 1];
+        ce0 = sc.cons_off[r]; ce1 = sc.cons_off[r + 1];
+      }
+      const int64_t c = r - nl;
+      ptx::mbar_wait(&tfull[acc], aph);
+      ptx::tc_fence_after();
+      const uint32_t tl = tbase + acc * Cfg::ACC_STRIDE + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-    for (int jc = 0; jc < W / 8; jc++) {
-      float z[GATES][8];
+      for (int jc = 0; jc < W / 8; jc++) {
+        float z[GATES][8];
 #pragma unroll
-      for (int g = 0; g < GATES; g++) ptx::tmem_ld8(tl + g * W + jc * 8, z[g]);
-      ptx::tmem_ld_wait();
-      if (!valid) continue;
-      const int jb = j0 + jc * 8;
-      if (jb >= S) continue;
-      const bool fullc = (jb + 8 <= S) && ((S & 7) == 0);
-      float hh[8];
-      if constexpr (GATES == 1) {
+        for (int g = 0; g < GATES; g++) ptx::tmem_ld8(tl + g * W + jc * 8, z[g]);
+        ptx::tmem_ld_wait();
+        const int jb = j0 + jc * 8;
+        if (!valid || jb >= S) continue;
+        const bool fullc = (jb + 8 <= S) && ((S & 7) == 0);
+        float hh[8];
+        if constexpr (GATES == 1) {
 #pragma unroll
-        for (int u = 0; u < 8; u++) hh[u] = tanhf(z[0][u] + sbias[jc * 8 + u]);
+          for (int u = 0; u < 8; u++) hh[u] = tanhf(z[0][u] + (jb + u < S ? __ldg(bias + jb + u) : 0.f));
+          if (fullc) {
+            uint4 pk = make_uint4(pack_bf16x2(hh[0], hh[1]), pack_bf16x2(hh[2], hh[3]), pack_bf16x2(hh[4], hh[5]),
+                                  pack_bf16x2(hh[6], hh[7]));
+            *reinterpret_cast<uint4 *>(Gact + c * ld_g + jb) = pk;
+            *reinterpret_cast<float4 *>(C + r * ld + jb) = make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4 *>(C + r * ld + jb + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {
+            for (int u = 0; u < 8 && jb + u < S; u++) {
+              Gact[c * ld_g + jb + u] = __float2bfloat16_rn(hh[u]);
+              C[r * ld + jb + u] = 0.f;
+            }
+          }
+        } else {
+          float cl[8], cr[8], bz[5][8];
+          if (fullc) {
+            float4 a = *reinterpret_cast<const float4 *>(C + gl * ld + jb);
+            float4 b = *reinterpret_cast<const float4 *>(C + gl * ld + jb + 4);
+            cl[0] = a.x; cl[1] = a.y; cl[2] = a.z; cl[3] = a.w; cl[4] = b.x; cl[5] = b.y; cl[6] = b.z; cl[7] = b.w;
+            a = *reinterpret_cast<const float4 *>(C + gr * ld + jb);
+            b = *reinterpret_cast<const float4 *>(C + gr * ld + jb + 4);
+            cr[0] = a.x; cr[1] = a.y; cr[2] = a.z; cr[3] = a.w; cr[4] = b.x; cr[5] = b.y; cr[6] = b.z; cr[7] = b.w;
+#pragma unroll
+            for (int g = 0; g < 5; g++) {
+              float4 x = __ldg(reinterpret_cast<const float4 *>(bias + g * S + jb));
+              float4 y = __ldg(reinterpret_cast<const float4 *>(bias + g * S + jb + 4));
+              bz[g][0] = x.x; bz[g][1] = x.y; bz[g][2] = x.z; bz[g][3] = x.w;
+              bz[g][4] = y.x; bz[g][5] = y.y; bz[g][6] = y.z; bz[g][7] = y.w;
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+              bool ok = jb + u < S;
+              cl[u] = ok ? C[gl * ld + jb + u] : 0.f;
+              cr[u] = ok ? C[gr * ld + jb + u] : 0.f;
+#pragma unroll
+              for (int g = 0; g < 5; g++) bz[g][u] = ok ? bias[g * S + jb + u] : 0.f;
+            }
+          }
+          float gi[8], gfl[8], gfr[8], go[8], gu[8], cc[8];
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            gi[u] = sigmoidf_(z[0][u] + bz[0][u]);
+            gfl[u] = sigmoidf_(z[1][u] + bz[1][u]);
+            gfr[u] = sigmoidf_(z[2][u] + bz[2][u]);
+            go[u] = sigmoidf_(z[3][u] + bz[3][u]);
+            gu[u] = tanhf(z[4][u] + bz[4][u]);
+            cc[u] = gi[u] * gu[u] + gfl[u] * cl[u] + gfr[u] * cr[u];
+            hh[u] = go[u] * tanhf(cc[u]);
+          }
+          __nv_bfloat16 *ga = Gact + c * ld_g;
+          if (fullc) {
+            *reinterpret_cast<float4 *>(C + r * ld + jb) = make_float4(cc[0], cc[1], cc[2], cc[3]);
+            *reinterpret_cast<float4 *>(C + r * ld + jb + 4) = make_float4(cc[4], cc[5], cc[6], cc[7]);
+            float *gs[5] = {gi, gfl, gfr, go, gu};
+#pragma unroll
+            for (int g = 0; g < 5; g++)
+              *reinterpret_cast<uint4 *>(ga + g * S + jb) =
+                  make_uint4(pack_bf16x2(gs[g][0], gs[g][1]), pack_bf16x2(gs[g][2], gs[g][3]),
+                             pack_bf16x2(gs[g][4], gs[g][5]), pack_bf16x2(gs[g][6], gs[g][7]));
+          } else {
+            for (int u = 0; u < 8 && jb + u < S; u++) {
+              int j = jb + u;
+              C[r * ld + j] = cc[u];
+              ga[j] = __float2bfloat16_rn(gi[u]);
+              ga[S + j] = __float2bfloat16_rn(gfl[u]);
+              ga[2 * S + j] = __float2bfloat16_rn(gfr[u]);
+              ga[3 * S + j] = __float2bfloat16_rn(go[u]);
+              ga[4 * S + j] = __float2bfloat16_rn(gu[u]);
+            }
+          }
+        }
+        // h: pool row (append) + every consumer's A-operand row (push-gather)
         if (fullc) {
           uint4 pk = make_uint4(pack_bf16x2(hh[0], hh[1]), pack_bf16x2(hh[2], hh[3]), pack_bf16x2(hh[4], hh[5]),
                                 pack_bf16x2(hh[6], hh[7]));
-          *reinterpret_cast<uint4 *>(Gact + c * ld_g + jb) = pk;
-          *reinterpret_cast<float4 *>(C + r * ld + jb) = make_float4(0.f, 0.f, 0.f, 0.f);
-          *reinterpret_cast<float4 *>(C + r * ld + jb + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
-        } else {
-          for (int u = 0; u < 8 && jb + u < S; u++) {
-            Gact[c * ld_g + jb + u] = __float2bfloat16_rn(hh[u]);
-            C[r * ld + jb + u] = 0.f;
-          }
-        }
-      } else {
-        float cl[8], cr[8];
-        if (fullc) {
-          float4 a = *reinterpret_cast<const float4 *>(C + gl * ld + jb);
-          float4 b = *reinterpret_cast<const float4 *>(C + gl * ld + jb + 4);
-          cl[0] = a.x; cl[1] = a.y; cl[2] = a.z; cl[3] = a.w; cl[4] = b.x; cl[5] = b.y; cl[6] = b.z; cl[7] = b.w;
-          a = *reinterpret_cast<const float4 *>(C + gr * ld + jb);
-          b = *reinterpret_cast<const float4 *>(C + gr * ld + jb + 4);
-          cr[0] = a.x; cr[1] = a.y; cr[2] = a.z; cr[3] = a.w; cr[4] = b.x; cr[5] = b.y; cr[6] = b.z; cr[7] = b.w;
-        } else {
-#pragma unroll
-          for (int u = 0; u < 8; u++) {
-            bool ok = jb + u < S;
-            cl[u] = ok ? C[gl * ld + jb + u] : 0.f;
-            cr[u] = ok ? C[gr * ld + jb + u] : 0.f;
-          }
-        }
-        float gi[8], gfl[8], gfr[8], go[8], gu[8], cc[8];
-#pragma unroll
-        for (int u = 0; u < 8; u++) {
-          const int jj = jc * 8 + u;
-          gi[u] = sigmoidf_(z[0][u] + sbias[jj]);
-          gfl[u] = sigmoidf_(z[1][u] + sbias[W + jj]);
-          gfr[u] = sigmoidf_(z[2][u] + sbias[2 * W + jj]);
-          go[u] = sigmoidf_(z[3][u] + sbias[3 * W + jj]);
-          gu[u] = tanhf(z[4][u] + sbias[4 * W + jj]);
-          cc[u] = gi[u] * gu[u] + gfl[u] * cl[u] + gfr[u] * cr[u];
-          hh[u] = go[u] * tanhf(cc[u]);
-        }
-        __nv_bfloat16 *ga = Gact + c * ld_g;
-        if (fullc) {
-          *reinterpret_cast<float4 *>(C + r * ld + jb) = make_float4(cc[0], cc[1], cc[2], cc[3]);
-          *reinterpret_cast<float4 *>(C + r * ld + jb + 4) = make_float4(cc[4], cc[5], cc[6], cc[7]);
-          float *gs[5] = {gi, gfl, gfr, go, gu};
-#pragma unroll
-          for (int g = 0; g < 5; g++)
-            *reinterpret_cast<uint4 *>(ga + g * S + jb) =
-                make_uint4(pack_bf16x2(gs[g][0], gs[g][1]), pack_bf16x2(gs[g][2], gs[g][3]),
-                           pack_bf16x2(gs[g][4], gs[g][5]), pack_bf16x2(gs[g][6], gs[g][7]));
-        } else {
-          for (int u = 0; u < 8 && jb + u < S; u++) {
-            int j = jb + u;
-            C[r * ld + j] = cc[u];
-            ga[j] = __float2bfloat16_rn(gi[u]);
-            ga[S + j] = __float2bfloat16_rn(gfl[u]);
-            ga[2 * S + j] = __float2bfloat16_rn(gfr[u]);
-            ga[3 * S + j] = __float2bfloat16_rn(go[u]);
-            ga[4 * S + j] = __float2bfloat16_rn(gu[u]);
-          }
-        }
-      }
-      // h: pool row (append) + every consumer's A-operand row (push-gather)
-      if (fullc) {
-        uint4 pk = make_uint4(pack_bf16x2(hh[0], hh[1]), pack_bf16x2(hh[2], hh[3]), pack_bf16x2(hh[4], hh[5]),
-                              pack_bf16x2(hh[6], hh[7]));
-        *reinterpret_cast<uint4 *>(H + r * ld + jb) = pk;
-        for (int e = ce0; e < ce1; e++) {
-          int ed = sc.cons_edge[e];
-          *reinterpret_cast<uint4 *>(((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld + jb) = pk;
-        }
-      } else {
-        for (int u = 0; u < 8 && jb + u < S; u++) {
-          __nv_bfloat16 hv = __float2bfloat16_rn(hh[u]);
-          H[r * ld + jb + u] = hv;
+          *reinterpret_cast<uint4 *>(H + r * ld + jb) = pk;
           for (int e = ce0; e < ce1; e++) {
             int ed = sc.cons_edge[e];
-            (((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld)[jb + u] = hv;
+            *reinterpret_cast<uint4 *>(((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld + jb) = pk;
+          }
+        } else {
+          for (int u = 0; u < 8 && jb + u < S; u++) {
+            __nv_bfloat16 hv = __float2bfloat16_rn(hh[u]);
+            H[r * ld + jb + u] = hv;
+            for (int e = ce0; e < ce1; e++) {
+              int ed = sc.cons_edge[e];
+              (((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld)[jb + u] = hv;
+            }
           }
         }
       }
+      // this accumulator buffer may be overwritten by the MMA of tile i+2
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
     }
   }
   ptx::tc_fence_before();
@@ -528,6 +551,17 @@ fold_status set_smem(K kernel, int bytes) {
   return FOLD_OK;
 }
 
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
 template <int GATES, int W>
 fold_status launch_fwd(int r0, int r1, int nl, int n_cells, const int32_t *gather, int S, int ld, const TcWeights &w,
                        const float *b, __nv_bfloat16 *H, float *C, __nv_bfloat16 *Gact, int ld_g, const ScatterA &sc,
@@ -539,10 +573,12 @@ fold_status launch_fwd(int r0, int r1, int nl, int n_cells, const int32_t *gathe
   FOLD_TRY(make_map(&tmU, w.U, (uint64_t)w.ld_u, (uint64_t)GATES * S, (uint64_t)w.ld_u * 2, BK, W));
   auto kern = k_cell_fwd_tc<GATES, W>;
   FOLD_TRY(set_smem(kern, Cfg::SMEM));
-  dim3 grid((unsigned)cdiv(S, W), (unsigned)cdiv(r1 - r0, BM));
+  const int NT = (int)cdiv(S, W);
+  const int ntiles = NT * (int)cdiv(r1 - r0, BM);
+  const int grid = ntiles < num_sms() ? ntiles : num_sms();
   int KBh = (int)cdiv(S, BK);
-  kern<<<grid, kThreads, Cfg::SMEM, st>>>(tmAL, tmAR, tmU, r0, r1, nl, S, w.ld_u / 2, ld, KBh, gather, b, H, C, Gact,
-                                          ld_g, sc);
+  kern<<<grid, kThreads, Cfg::SMEM, st>>>(tmAL, tmAR, tmU, r0, r1, nl, S, w.ld_u / 2, ld, KBh, NT, ntiles, gather, b,
+                                          H, C, Gact, ld_g, sc);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
@@ -567,7 +603,7 @@ fold_status tc_cell_fwd(int cell, int r0, int r1, int nl, int n_cells, const int
                         const ScatterA &sc, cudaStream_t st) {
   if (r1 <= r0) return FOLD_OK;
   if (cell == FOLD_CELL_TREELSTM)
-    return launch_fwd<5, 32>(r0, r1, nl, n_cells, gather, S, ld, w, b, H, C, Gact, ld_g, sc, st);
+    return launch_fwd<5, 48>(r0, r1, nl, n_cells, gather, S, ld, w, b, H, C, Gact, ld_g, sc, st);
   return launch_fwd<1, 128>(r0, r1, nl, n_cells, gather, S, ld, w, b, H, C, Gact, ld_g, sc, st);
 }
 
