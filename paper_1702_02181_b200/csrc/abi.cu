@@ -68,7 +68,7 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
       b.w.ld_u = (int)(2 * round_up(S, 64));
       b.w.ld_ut = (int)round_up((int64_t)gates * S, 8);
       b.w.U = (__nv_bfloat16 *)(p + o_w);
-      b.w.Ut = (__nv_bfloat16 *)(p + o_w + a256((size_t)gates * S * b.w.ld_u * 2));
+      b.w.Ut = (__nv_bfloat16 *)(p + o_w + tc_ut_offset(gates, (int)S));
     }
   }
   return b;

@@ -58,7 +58,7 @@ fold_status launch_zero(void *p, size_t bytes, cudaStream_t st);
 
 // --- tcgen05 path (exec_tc.cu)
 struct TcWeights {  // bf16 copies made per call
-  __nv_bfloat16 *U;   // [gates*S][ld_u]  (ld_u = 2*round_up(S, 64): K halves padded), canonical rows
+  __nv_bfloat16 *U;   // forward: gate-interleaved [cdiv(S,W)*gates*W][ld_u] (ld_u = 2*round_up(S, 64))
   __nv_bfloat16 *Ut;  // [2S][ld_ut]      (ld_ut = round_up(gates*S, 8)) = U^T
   int ld_u, ld_ut;
 };
@@ -73,5 +73,6 @@ int tc_dU_splits(int n_cells, int gates, int S);
 fold_status tc_gemm_dU(int n_cells, int S, int gates, const __nv_bfloat16 *dZ, int ld_z, const ScatterA &sc,
                        float *dU, int accumulate, float *split_ws, cudaStream_t st);
 size_t tc_workspace_bytes(int gates, int S);
+size_t tc_ut_offset(int gates, int S);  // byte offset of Ut inside the tc workspace
 
 }  // namespace fold

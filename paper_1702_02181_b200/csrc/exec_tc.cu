@@ -108,9 +108,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t *A = smem + s * Cfg::STAGE;
           uint8_t *B = A + Cfg::A_BYTES;
           ptx::tma_load_2d(half ? &tmAR : &tmAL, &full[s], A, kc, c0);
-#pragma unroll
-          for (int g = 0; g < GATES; g++)
-            ptx::tma_load_2d(&tmU, &full[s], B + g * W * 128, half * Sp + kc, g * S + j0);
+          // U is stored gate-interleaved per state-column tile (tc_prepare_U): one box of
+          // GATES*W rows holds (i, fL, fR, o, u) for the tile's W state columns
+          ptx::tma_load_2d(&tmU, &full[s], B, half * Sp + kc, (t % NT) * Cfg::N);
         }
       }
     }
@@ -491,27 +491,37 @@ __global__ void k_reduce_splits(int64_t n, int nsplit, const float *__restrict__
 }
 
 // =================================================================== weight prep
-// Ubf[r][half*Sp + k] = bf16(U[r][half*S + k]) for k < S, 0 for S <= k < Sp (each K half
-// padded to Sp = round_up(S, 64) so every TMA box starts 128-byte aligned);
-// Ut[half*S + k][r] = bf16(U[r][half*S + k]) (ld_ut). 32x32 smem tiles over padded columns.
-__global__ void k_prep_U(int R, int S, int Sp, const float *__restrict__ U, __nv_bfloat16 *__restrict__ Ubf,
-                         int ld_u, __nv_bfloat16 *__restrict__ Ut, int ld_ut) {
-  __shared__ float t[32][33];
-  const int r0 = blockIdx.y * 32, kp0 = blockIdx.x * 32;
-  const int half = kp0 >= Sp, kk0 = kp0 - half * Sp;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: ty 0..7
-  for (int i = ty; i < 32; i += 8) {
-    int r = r0 + i, kk = kk0 + tx;
-    bool ok = r < R && kk < S;
-    float v = ok ? U[(int64_t)r * 2 * S + half * S + kk] : 0.f;
-    t[i][tx] = v;
-    if (r < R) Ubf[(int64_t)r * ld_u + kp0 + tx] = __float2bfloat16_rn(v);
+// Forward operand: Uil[t*GW + g*W + jj][half*Sp + k] = bf16(U[g*S + t*W + jj][half*S + k])
+// (gate-interleaved per W-column tile; K halves padded to Sp = round_up(S, 64) so every TMA
+// box starts 128-byte aligned; rows / columns past S are zero).
+__global__ void k_prep_Uil(int gates, int W, int NT, int S, int Sp, const float *__restrict__ U,
+                           __nv_bfloat16 *__restrict__ Uil, int ld_u) {
+  const int GW = gates * W;
+  const int64_t total = (int64_t)NT * GW * (2 * Sp);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int64_t ri = i / (2 * Sp);
+    const int kp = (int)(i - ri * 2 * Sp);
+    const int t = (int)(ri / GW), rem = (int)(ri - (int64_t)t * GW), g = rem / W, j = t * W + (rem - g * W);
+    const int half = kp >= Sp, kk = kp - half * Sp;
+    float v = (j < S && kk < S) ? U[((int64_t)g * S + j) * 2 * S + half * S + kk] : 0.f;
+    Uil[ri * ld_u + kp] = __float2bfloat16_rn(v);
   }
-  if (!Ut) return;
+}
+
+// Backward operand: Ut[k][r] = bf16(U[r][k]) (ld_ut), 32x32 smem tiles.
+__global__ void k_prep_Ut(int R, int K, const float *__restrict__ U, __nv_bfloat16 *__restrict__ Ut, int ld_ut) {
+  __shared__ float t[32][33];
+  const int r0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int i = ty; i < 32; i += 8) {
+    int r = r0 + i, k = k0 + tx;
+    t[i][tx] = (r < R && k < K) ? U[(int64_t)r * K + k] : 0.f;
+  }
   __syncthreads();
   for (int i = ty; i < 32; i += 8) {
-    int kk = kk0 + i, r = r0 + tx;
-    if (r < R && kk < S) Ut[(int64_t)(half * S + kk) * ld_ut + r] = __float2bfloat16_rn(t[tx][i]);
+    int k = k0 + i, r = r0 + tx;
+    if (r < R && k < K) Ut[(int64_t)k * ld_ut + r] = __float2bfloat16_rn(t[tx][i]);
   }
 }
 
@@ -570,7 +580,8 @@ fold_status launch_fwd(int r0, int r1, int nl, int n_cells, const int32_t *gathe
   CUtensorMap tmAL, tmAR, tmU;
   FOLD_TRY(make_map(&tmAL, sc.AL, (uint64_t)S, (uint64_t)n_cells, (uint64_t)sc.ld * 2, BK, BM));
   FOLD_TRY(make_map(&tmAR, sc.AR, (uint64_t)S, (uint64_t)n_cells, (uint64_t)sc.ld * 2, BK, BM));
-  FOLD_TRY(make_map(&tmU, w.U, (uint64_t)w.ld_u, (uint64_t)GATES * S, (uint64_t)w.ld_u * 2, BK, W));
+  const int NTu = (int)cdiv(S, W);
+  FOLD_TRY(make_map(&tmU, w.U, (uint64_t)w.ld_u, (uint64_t)NTu * Cfg::N, (uint64_t)w.ld_u * 2, BK, Cfg::N));
   auto kern = k_cell_fwd_tc<GATES, W>;
   FOLD_TRY(set_smem(kern, Cfg::SMEM));
   const int NT = (int)cdiv(S, W);
@@ -585,15 +596,34 @@ fold_status launch_fwd(int r0, int r1, int nl, int n_cells, const int32_t *gathe
 
 }  // namespace
 
+int tc_fwd_W(int gates) { return gates == 5 ? 48 : 128; }
+
 size_t tc_workspace_bytes(int gates, int S) {
+  const int W = tc_fwd_W(gates);
   size_t ld_u = 2 * round_up(S, 64), ld_ut = round_up((int64_t)gates * S, 8);
-  return round_up((int64_t)gates * S * ld_u * 2, 256) + round_up((int64_t)2 * S * ld_ut * 2, 256);
+  size_t rows_il = (size_t)cdiv(S, W) * gates * W;
+  return round_up((int64_t)(rows_il * ld_u * 2), 256) + round_up((int64_t)2 * S * ld_ut * 2, 256);
+}
+
+size_t tc_ut_offset(int gates, int S) {
+  const int W = tc_fwd_W(gates);
+  size_t ld_u = 2 * round_up(S, 64);
+  size_t rows_il = (size_t)cdiv(S, W) * gates * W;
+  return round_up((int64_t)(rows_il * ld_u * 2), 256);
 }
 
 fold_status tc_prepare_U(int gates, int S, const float *U, TcWeights &w, bool transpose, cudaStream_t st) {
-  int R = gates * S, Sp = (int)round_up(S, 64);
-  dim3 grid((unsigned)(2 * Sp / 32), (unsigned)cdiv(R, 32));
-  k_prep_U<<<grid, 256, 0, st>>>(R, S, Sp, U, w.U, w.ld_u, transpose ? w.Ut : nullptr, w.ld_ut);
+  if (!transpose) {
+    const int W = tc_fwd_W(gates), NT = (int)cdiv(S, W), Sp = (int)round_up(S, 64);
+    int64_t total = (int64_t)NT * gates * W * 2 * Sp;
+    int64_t blocks = cdiv(total, 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_prep_Uil<<<(unsigned)blocks, 256, 0, st>>>(gates, W, NT, S, Sp, U, w.U, w.ld_u);
+  } else {
+    const int R = gates * S, K = 2 * S;
+    dim3 grid((unsigned)cdiv(K, 32), (unsigned)cdiv(R, 32));
+    k_prep_Ut<<<grid, 256, 0, st>>>(R, K, U, w.Ut, w.ld_ut);
+  }
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
