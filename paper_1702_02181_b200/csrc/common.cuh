@@ -58,6 +58,14 @@ __host__ __device__ inline int ld_of(int S) { return (int)round_up(S, 8); }
 
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.0f / (1.0f + __expf(-x)); }
 __device__ __forceinline__ float tanhf_(float x) { return tanhf(x); }
+// BF16-path epilogues: hardware tanh (MUFU.TANH, max rel. error ~2^-11, far below the
+// bf16 rounding of the stored states) and sigmoid(x) = 0.5 tanh(x/2) + 0.5.
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sigmoid_fast(float x) { return fmaf(0.5f, tanh_fast(0.5f * x), 0.5f); }
 
 __device__ __forceinline__ float to_f(float x) { return x; }
 __device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }

@@ -18,6 +18,8 @@
 // warp 2 TMEM allocator, warps 4-7 epilogue (warp w reads TMEM lanes 32(w%4)..+31).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "exec.cuh"
 #include "ptx.cuh"
 
@@ -51,6 +53,9 @@ struct FwdCfg {
   static constexpr int ACC_STRIDE = 256;  // TMEM columns per accumulator buffer (2 buffers)
   static constexpr int TMEM_COLS = 512;
   static constexpr int SMEM = ST * STAGE + 1024;
+  static constexpr int EPI_WARPS = 8;     // 2 per SM sub-partition: each owns half the columns
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
+  static constexpr int CHUNKS = W / 8;
   static_assert(N % 16 == 0 && N <= 256, "UMMA N for M=128");
   static_assert(W % 8 == 0, "gate slab rows must fill 8-row swizzle atoms");
   static_assert(SMEM <= 227 * 1024, "smem");
@@ -59,13 +64,15 @@ struct FwdCfg {
 // Persistent: grid = min(#tiles, #SMs); tile t -> (state-column tile t % NT, row tile t / NT)
 // (N fast: the CTAs running concurrently share a few A tiles in L2; U is L2-resident).
 // Two TMEM accumulators: the epilogue of tile i overlaps the MMA main loop of tile i+1.
+// Warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4..11 epilogue
+// (warp w reads TMEM lanes 32 (w % 4) .. +31, column chunks (w - 4) / 4, +2, +4, ...).
 template <int GATES, int W>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
     k_cell_fwd_tc(const __grid_constant__ CUtensorMap tmAL, const __grid_constant__ CUtensorMap tmAR,
                   const __grid_constant__ CUtensorMap tmU, int r0, int r1, int nl, int S, int Sp, int ld, int KBh,
                   int NT, int ntiles, const int32_t *__restrict__ gather, const float *__restrict__ bias,
                   __nv_bfloat16 *__restrict__ H, float *__restrict__ C, __nv_bfloat16 *__restrict__ Gact, int ld_g,
-                  ScatterA sc) {
+                  ScatterA sc, int dbg_epi) {
   using Cfg = FwdCfg<GATES, W>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
@@ -75,7 +82,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < ST; s++) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; a++) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 4); }
+    for (int a = 0; a < 2; a++) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], Cfg::EPI_WARPS); }
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tmAL);
     ptx::prefetch_tmap(&tmAR);
@@ -93,11 +100,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // TMA producer: per stage one dense box of 128 A rows (the level's contiguous cell rows
-    // of the left / right operand plane) + GATES boxes of W rows of U (gate-interleaved N).
+    // of the left / right operand plane) + one box of the gate-interleaved U slab.
     if (lane == 0) {
       int it = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int j0 = (t % NT) * W, c0 = (r0 - nl) + (t / NT) * BM;
+        const int c0 = (r0 - nl) + (t / NT) * BM;
         for (int kb = 0; kb < KB; kb++, it++) {
           int s = it % ST;
           uint32_t ph = (it / ST) & 1;
@@ -106,11 +113,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           int half = kb >= KBh;
           int kc = (kb - half * KBh) * BK;
           uint8_t *A = smem + s * Cfg::STAGE;
-          uint8_t *B = A + Cfg::A_BYTES;
           ptx::tma_load_2d(half ? &tmAR : &tmAL, &full[s], A, kc, c0);
           // U is stored gate-interleaved per state-column tile (tc_prepare_U): one box of
           // GATES*W rows holds (i, fL, fR, o, u) for the tile's W state columns
-          ptx::tma_load_2d(&tmU, &full[s], B, half * Sp + kc, (t % NT) * Cfg::N);
+          ptx::tma_load_2d(&tmU, &full[s], A + Cfg::A_BYTES, half * Sp + kc, (t % NT) * Cfg::N);
         }
       }
     }
@@ -142,7 +148,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // Epilogue: TMEM lane = tile row; gates -> (h, c); append to the level's pool rows and
     // push h to the A-operand row of every consumer edge (the next levels' "gather").
-    const int q = warp & 3;
+    const int q = warp & 3;            // TMEM lane quarter
+    const int grp = (warp - 4) >> 2;   // column-chunk group (0 or 1)
     const int row = q * 32 + lane;
     int tc = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, tc++) {
@@ -150,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t aph = (tc >> 1) & 1;
       const int j0 = (t % NT) * W;
       const int64_t r = r0 + (int64_t)(t / NT) * BM + row;
-      const bool valid = r < r1;
+      const bool valid = r < r1 && !dbg_epi;
       int64_t gl = 0, gr = 0;
       int ce0 = 0, ce1 = 0;
       if (valid) {
@@ -158,22 +165,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         ce0 = sc.cons_off[r]; ce1 = sc.cons_off[r + 1];
       }
       const int64_t c = r - nl;
+      // prefetch the first chunk's child cell states before waiting for the accumulator
+      float cl[8], cr[8];
+      auto load_c = [&](int jb) {
+        if (GATES != 5) return;
+        if (valid && jb + 8 <= S && (S & 7) == 0) {
+          float4 a = __ldg(reinterpret_cast<const float4 *>(C + gl * ld + jb));
+          float4 b = __ldg(reinterpret_cast<const float4 *>(C + gl * ld + jb + 4));
+          cl[0] = a.x; cl[1] = a.y; cl[2] = a.z; cl[3] = a.w; cl[4] = b.x; cl[5] = b.y; cl[6] = b.z; cl[7] = b.w;
+          a = __ldg(reinterpret_cast<const float4 *>(C + gr * ld + jb));
+          b = __ldg(reinterpret_cast<const float4 *>(C + gr * ld + jb + 4));
+          cr[0] = a.x; cr[1] = a.y; cr[2] = a.z; cr[3] = a.w; cr[4] = b.x; cr[5] = b.y; cr[6] = b.z; cr[7] = b.w;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            bool ok = valid && jb + u < S;
+            cl[u] = ok ? C[gl * ld + jb + u] : 0.f;
+            cr[u] = ok ? C[gr * ld + jb + u] : 0.f;
+          }
+        }
+      };
+      load_c(j0 + grp * 8);
       ptx::mbar_wait(&tfull[acc], aph);
       ptx::tc_fence_after();
       const uint32_t tl = tbase + acc * Cfg::ACC_STRIDE + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-      for (int jc = 0; jc < W / 8; jc++) {
+      for (int jc = grp; jc < Cfg::CHUNKS; jc += 2) {
         float z[GATES][8];
 #pragma unroll
         for (int g = 0; g < GATES; g++) ptx::tmem_ld8(tl + g * W + jc * 8, z[g]);
         ptx::tmem_ld_wait();
         const int jb = j0 + jc * 8;
+        float ccl[8], ccr[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) { ccl[u] = cl[u]; ccr[u] = cr[u]; }
+        if (jc + 2 < Cfg::CHUNKS) load_c(jb + 16);  // next chunk of this warp, in flight during math
         if (!valid || jb >= S) continue;
         const bool fullc = (jb + 8 <= S) && ((S & 7) == 0);
         float hh[8];
         if constexpr (GATES == 1) {
 #pragma unroll
-          for (int u = 0; u < 8; u++) hh[u] = tanhf(z[0][u] + (jb + u < S ? __ldg(bias + jb + u) : 0.f));
+          for (int u = 0; u < 8; u++) hh[u] = tanh_fast(z[0][u] + (jb + u < S ? __ldg(bias + jb + u) : 0.f));
           if (fullc) {
             uint4 pk = make_uint4(pack_bf16x2(hh[0], hh[1]), pack_bf16x2(hh[2], hh[3]), pack_bf16x2(hh[4], hh[5]),
                                   pack_bf16x2(hh[6], hh[7]));
@@ -187,47 +219,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         } else {
-          float cl[8], cr[8], bz[5][8];
-          if (fullc) {
-            float4 a = *reinterpret_cast<const float4 *>(C + gl * ld + jb);
-            float4 b = *reinterpret_cast<const float4 *>(C + gl * ld + jb + 4);
-            cl[0] = a.x; cl[1] = a.y; cl[2] = a.z; cl[3] = a.w; cl[4] = b.x; cl[5] = b.y; cl[6] = b.z; cl[7] = b.w;
-            a = *reinterpret_cast<const float4 *>(C + gr * ld + jb);
-            b = *reinterpret_cast<const float4 *>(C + gr * ld + jb + 4);
-            cr[0] = a.x; cr[1] = a.y; cr[2] = a.z; cr[3] = a.w; cr[4] = b.x; cr[5] = b.y; cr[6] = b.z; cr[7] = b.w;
+          float gs[5][8], cc[8];
 #pragma unroll
-            for (int g = 0; g < 5; g++) {
+          for (int g = 0; g < 5; g++) {
+            float bz[8];
+            if (fullc) {
               float4 x = __ldg(reinterpret_cast<const float4 *>(bias + g * S + jb));
               float4 y = __ldg(reinterpret_cast<const float4 *>(bias + g * S + jb + 4));
-              bz[g][0] = x.x; bz[g][1] = x.y; bz[g][2] = x.z; bz[g][3] = x.w;
-              bz[g][4] = y.x; bz[g][5] = y.y; bz[g][6] = y.z; bz[g][7] = y.w;
-            }
-          } else {
+              bz[0] = x.x; bz[1] = x.y; bz[2] = x.z; bz[3] = x.w; bz[4] = y.x; bz[5] = y.y; bz[6] = y.z; bz[7] = y.w;
+            } else {
 #pragma unroll
-            for (int u = 0; u < 8; u++) {
-              bool ok = jb + u < S;
-              cl[u] = ok ? C[gl * ld + jb + u] : 0.f;
-              cr[u] = ok ? C[gr * ld + jb + u] : 0.f;
-#pragma unroll
-              for (int g = 0; g < 5; g++) bz[g][u] = ok ? bias[g * S + jb + u] : 0.f;
+              for (int u = 0; u < 8; u++) bz[u] = jb + u < S ? bias[g * S + jb + u] : 0.f;
             }
+#pragma unroll
+            for (int u = 0; u < 8; u++) gs[g][u] = g == 4 ? tanh_fast(z[g][u] + bz[u]) : sigmoid_fast(z[g][u] + bz[u]);
           }
-          float gi[8], gfl[8], gfr[8], go[8], gu[8], cc[8];
 #pragma unroll
           for (int u = 0; u < 8; u++) {
-            gi[u] = sigmoidf_(z[0][u] + bz[0][u]);
-            gfl[u] = sigmoidf_(z[1][u] + bz[1][u]);
-            gfr[u] = sigmoidf_(z[2][u] + bz[2][u]);
-            go[u] = sigmoidf_(z[3][u] + bz[3][u]);
-            gu[u] = tanhf(z[4][u] + bz[4][u]);
-            cc[u] = gi[u] * gu[u] + gfl[u] * cl[u] + gfr[u] * cr[u];
-            hh[u] = go[u] * tanhf(cc[u]);
+            cc[u] = gs[0][u] * gs[4][u] + gs[1][u] * ccl[u] + gs[2][u] * ccr[u];
+            hh[u] = gs[3][u] * tanh_fast(cc[u]);
           }
           __nv_bfloat16 *ga = Gact + c * ld_g;
           if (fullc) {
             *reinterpret_cast<float4 *>(C + r * ld + jb) = make_float4(cc[0], cc[1], cc[2], cc[3]);
             *reinterpret_cast<float4 *>(C + r * ld + jb + 4) = make_float4(cc[4], cc[5], cc[6], cc[7]);
-            float *gs[5] = {gi, gfl, gfr, go, gu};
 #pragma unroll
             for (int g = 0; g < 5; g++)
               *reinterpret_cast<uint4 *>(ga + g * S + jb) =
@@ -237,11 +252,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int u = 0; u < 8 && jb + u < S; u++) {
               int j = jb + u;
               C[r * ld + j] = cc[u];
-              ga[j] = __float2bfloat16_rn(gi[u]);
-              ga[S + j] = __float2bfloat16_rn(gfl[u]);
-              ga[2 * S + j] = __float2bfloat16_rn(gfr[u]);
-              ga[3 * S + j] = __float2bfloat16_rn(go[u]);
-              ga[4 * S + j] = __float2bfloat16_rn(gu[u]);
+#pragma unroll
+              for (int g = 0; g < 5; g++) ga[g * S + j] = __float2bfloat16_rn(gs[g][u]);
             }
           }
         }
@@ -572,6 +584,11 @@ int num_sms() {
   return g_num_sms;
 }
 
+int dbg_fwd_epi() {
+  static int v = [] { const char *e = getenv("FOLD_DBG_FWD_EPI"); return e ? atoi(e) : 0; }();
+  return v;
+}
+
 template <int GATES, int W>
 fold_status launch_fwd(int r0, int r1, int nl, int n_cells, const int32_t *gather, int S, int ld, const TcWeights &w,
                        const float *b, __nv_bfloat16 *H, float *C, __nv_bfloat16 *Gact, int ld_g, const ScatterA &sc,
@@ -588,8 +605,8 @@ fold_status launch_fwd(int r0, int r1, int nl, int n_cells, const int32_t *gathe
   const int ntiles = NT * (int)cdiv(r1 - r0, BM);
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
   int KBh = (int)cdiv(S, BK);
-  kern<<<grid, kThreads, Cfg::SMEM, st>>>(tmAL, tmAR, tmU, r0, r1, nl, S, w.ld_u / 2, ld, KBh, NT, ntiles, gather, b,
-                                          H, C, Gact, ld_g, sc);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(tmAL, tmAR, tmU, r0, r1, nl, S, w.ld_u / 2, ld, KBh, NT, ntiles, gather, b,
+                                          H, C, Gact, ld_g, sc, dbg_fwd_epi());
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
