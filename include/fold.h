@@ -144,7 +144,13 @@ typedef struct {
  * One caller-owned device buffer holding everything the forward saves for the
  * backward (the pool of PAPER.md L47's loop state for every depth):
  *   H [N][ld] bf16 (BF16) or fp32 (FP32)  hidden state h per pool row
- *   C [N][ld] fp32                        cell state c per pool row (0 for TreeRNN)
+ *   C [N][ld] fp32                        cell state c per pool row (0 for TreeRNN; leaf
+ *                                         rows are c = 0 by definition and are not
+ *                                         materialised in BF16 mode)
+ *   A_L, A_R [n_cells][ld] bf16 (BF16)    consumer-side operand planes: row c holds the h
+ *                                         of cell c's left / right child (written by the
+ *                                         producer of that child; read by the level GEMM
+ *                                         and by the weight-gradient GEMM)
  *   G [n_cells][gates*S] bf16 / fp32      saved gate activations (i, fL, fR, o, u)
  *                                         or h (TreeRNN) per cell
  * Offsets/strides come from fold_acts_layout; the buffer is otherwise opaque. */

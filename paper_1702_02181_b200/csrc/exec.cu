@@ -51,13 +51,13 @@ __global__ void k_embed_fwd(int r0, int r1, const int32_t *__restrict__ leaf_tok
         } else {
           *reinterpret_cast<float4 *>(h + j) = v;
         }
-        *reinterpret_cast<float4 *>(c + j) = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!has_sc) *reinterpret_cast<float4 *>(c + j) = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     } else {
       for (int j = lane; j < S; j += 32) {
         T hv = from_f<T>(e[j]);
         h[j] = hv;
-        c[j] = 0.f;
+        if (!has_sc) c[j] = 0.f;
         if constexpr (sizeof(T) == 2) {
           for (int q = e0; q < e1; q++) {
             int ed = sc.cons_edge[q];
@@ -164,15 +164,16 @@ __global__ void __launch_bounds__(256) k_cell_fwd_simt(int r0, int r1, const int
 
 // ---------------------------------------------------------------- roots out
 template <typename T>
-__global__ void k_root_out(int G, int S, int ld, const int32_t *__restrict__ root_row, const T *__restrict__ H,
-                           const float *__restrict__ C, float *__restrict__ h_root, float *__restrict__ c_root) {
+__global__ void k_root_out(int G, int S, int ld, int nl, const int32_t *__restrict__ root_row,
+                           const T *__restrict__ H, const float *__restrict__ C, float *__restrict__ h_root,
+                           float *__restrict__ c_root) {
   int64_t total = (int64_t)G * S;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
     int64_t g = i / S, j = i - g * S;
     int64_t r = root_row[g];
     if (h_root) h_root[i] = to_f(H[r * ld + j]);
-    if (c_root) c_root[i] = C[r * ld + j];
+    if (c_root) c_root[i] = r >= nl ? C[r * ld + j] : 0.f;
   }
 }
 
@@ -280,7 +281,12 @@ __global__ void k_cell_bwd_pw(int r0, int r1, int nl, int S, int ld, int ld_g, c
         float ig[VEC], fl[VEC], fr[VEC], og[VEC], ug[VEC], cc[VEC], cl[VEC], cr[VEC];
         IT::ld(ga + j, ig); IT::ld(ga + S + j, fl); IT::ld(ga + 2 * S + j, fr);
         IT::ld(ga + 3 * S + j, og); IT::ld(ga + 4 * S + j, ug);
-        IF::ld(C + r * ld + j, cc); IF::ld(C + gL * ld + j, cl); IF::ld(C + gR * ld + j, cr);
+        IF::ld(C + r * ld + j, cc);
+        // leaf children: c = 0 (not materialised in BF16 mode)
+#pragma unroll
+        for (int u = 0; u < VEC; u++) { cl[u] = 0.f; cr[u] = 0.f; }
+        if (gL >= nl) IF::ld(C + gL * ld + j, cl);
+        if (gR >= nl) IF::ld(C + gR * ld + j, cr);
         float z0[VEC], z1[VEC], z2[VEC], z3[VEC], z4[VEC], eL[VEC], eR[VEC];
 #pragma unroll
         for (int u = 0; u < VEC; u++) {
@@ -510,12 +516,12 @@ fold_status launch_cell_fwd_simt(int cell, int r0, int r1, const int32_t *gather
   return FOLD_OK;
 }
 
-fold_status launch_root_out(bool bf16, int G, int S, int ld, const int32_t *root_row, const void *H, const float *C,
-                            float *h_root, float *c_root, cudaStream_t st) {
+fold_status launch_root_out(bool bf16, int G, int S, int ld, int nl, const int32_t *root_row, const void *H,
+                            const float *C, float *h_root, float *c_root, cudaStream_t st) {
   if (G <= 0 || (!h_root && !c_root)) return FOLD_OK;
   unsigned g = grid_cap(cdiv((int64_t)G * S, 256));
-  if (bf16) k_root_out<__nv_bfloat16><<<g, 256, 0, st>>>(G, S, ld, root_row, (const __nv_bfloat16 *)H, C, h_root, c_root);
-  else k_root_out<float><<<g, 256, 0, st>>>(G, S, ld, root_row, (const float *)H, C, h_root, c_root);
+  if (bf16) k_root_out<__nv_bfloat16><<<g, 256, 0, st>>>(G, S, ld, nl, root_row, (const __nv_bfloat16 *)H, C, h_root, c_root);
+  else k_root_out<float><<<g, 256, 0, st>>>(G, S, ld, nl, root_row, (const float *)H, C, h_root, c_root);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }

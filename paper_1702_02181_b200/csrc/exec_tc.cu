@@ -169,19 +169,26 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
       float cl[8], cr[8];
       auto load_c = [&](int jb) {
         if (GATES != 5) return;
-        if (valid && jb + 8 <= S && (S & 7) == 0) {
-          float4 a = __ldg(reinterpret_cast<const float4 *>(C + gl * ld + jb));
-          float4 b = __ldg(reinterpret_cast<const float4 *>(C + gl * ld + jb + 4));
-          cl[0] = a.x; cl[1] = a.y; cl[2] = a.z; cl[3] = a.w; cl[4] = b.x; cl[5] = b.y; cl[6] = b.z; cl[7] = b.w;
-          a = __ldg(reinterpret_cast<const float4 *>(C + gr * ld + jb));
-          b = __ldg(reinterpret_cast<const float4 *>(C + gr * ld + jb + 4));
-          cr[0] = a.x; cr[1] = a.y; cr[2] = a.z; cr[3] = a.w; cr[4] = b.x; cr[5] = b.y; cr[6] = b.z; cr[7] = b.w;
+        // leaf children have c = 0 (their C rows are not materialised in BF16 mode)
+        const bool lok = valid && gl >= nl, rok = valid && gr >= nl;
+        if (jb + 8 <= S && (S & 7) == 0) {
+#pragma unroll
+          for (int u = 0; u < 8; u++) { cl[u] = 0.f; cr[u] = 0.f; }
+          if (lok) {
+            float4 a = __ldg(reinterpret_cast<const float4 *>(C + gl * ld + jb));
+            float4 b = __ldg(reinterpret_cast<const float4 *>(C + gl * ld + jb + 4));
+            cl[0] = a.x; cl[1] = a.y; cl[2] = a.z; cl[3] = a.w; cl[4] = b.x; cl[5] = b.y; cl[6] = b.z; cl[7] = b.w;
+          }
+          if (rok) {
+            float4 a = __ldg(reinterpret_cast<const float4 *>(C + gr * ld + jb));
+            float4 b = __ldg(reinterpret_cast<const float4 *>(C + gr * ld + jb + 4));
+            cr[0] = a.x; cr[1] = a.y; cr[2] = a.z; cr[3] = a.w; cr[4] = b.x; cr[5] = b.y; cr[6] = b.z; cr[7] = b.w;
+          }
         } else {
 #pragma unroll
           for (int u = 0; u < 8; u++) {
-            bool ok = valid && jb + u < S;
-            cl[u] = ok ? C[gl * ld + jb + u] : 0.f;
-            cr[u] = ok ? C[gr * ld + jb + u] : 0.f;
+            cl[u] = (lok && jb + u < S) ? C[gl * ld + jb + u] : 0.f;
+            cr[u] = (rok && jb + u < S) ? C[gr * ld + jb + u] : 0.f;
           }
         }
       };
