@@ -178,7 +178,7 @@ fold_status fold_forward(const fold_schedule_t *s, const fold_model *m, void *ac
     }
   }
   ProfScope ps(K_ROOT, st);
-  FOLD_TRY(launch_root_out(bf16, G, S, L.ld, nl, s->root_row, H, C, h_root, c_root, st));
+  FOLD_TRY(launch_root_out(bf16, G, S, L.ld, nl, s->root_row, H, C, h_root, c_root, bf16 ? &sc : nullptr, st));
   return FOLD_OK;
 }
 

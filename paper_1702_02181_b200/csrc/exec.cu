@@ -163,16 +163,23 @@ __global__ void __launch_bounds__(256) k_cell_fwd_simt(int r0, int r1, const int
 }
 
 // ---------------------------------------------------------------- roots out
+// BF16 path: cell rows that have consumers keep h only in their consumers' A-operand
+// rows (the pool row is written for consumer-free rows), so a consumed root reads it there.
 template <typename T>
 __global__ void k_root_out(int G, int S, int ld, int nl, const int32_t *__restrict__ root_row,
                            const T *__restrict__ H, const float *__restrict__ C, float *__restrict__ h_root,
-                           float *__restrict__ c_root) {
+                           float *__restrict__ c_root, ScatterA sc, int has_sc) {
   int64_t total = (int64_t)G * S;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
     int64_t g = i / S, j = i - g * S;
     int64_t r = root_row[g];
-    if (h_root) h_root[i] = to_f(H[r * ld + j]);
+    const T *src = H + r * ld;
+    if (has_sc && r >= nl && sc.cons_off[r + 1] > sc.cons_off[r]) {
+      int ed = sc.cons_edge[sc.cons_off[r]];
+      src = reinterpret_cast<const T *>(((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld);
+    }
+    if (h_root) h_root[i] = to_f(src[j]);
     if (c_root) c_root[i] = r >= nl ? C[r * ld + j] : 0.f;
   }
 }
@@ -517,11 +524,13 @@ fold_status launch_cell_fwd_simt(int cell, int r0, int r1, const int32_t *gather
 }
 
 fold_status launch_root_out(bool bf16, int G, int S, int ld, int nl, const int32_t *root_row, const void *H,
-                            const float *C, float *h_root, float *c_root, cudaStream_t st) {
+                            const float *C, float *h_root, float *c_root, const ScatterA *sc, cudaStream_t st) {
+  ScatterA s0{};
   if (G <= 0 || (!h_root && !c_root)) return FOLD_OK;
   unsigned g = grid_cap(cdiv((int64_t)G * S, 256));
-  if (bf16) k_root_out<__nv_bfloat16><<<g, 256, 0, st>>>(G, S, ld, nl, root_row, (const __nv_bfloat16 *)H, C, h_root, c_root);
-  else k_root_out<float><<<g, 256, 0, st>>>(G, S, ld, nl, root_row, (const float *)H, C, h_root, c_root);
+  if (bf16) k_root_out<__nv_bfloat16><<<g, 256, 0, st>>>(G, S, ld, nl, root_row, (const __nv_bfloat16 *)H, C, h_root, c_root,
+                                                                sc ? *sc : s0, sc ? 1 : 0);
+  else k_root_out<float><<<g, 256, 0, st>>>(G, S, ld, nl, root_row, (const float *)H, C, h_root, c_root, s0, 0);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }

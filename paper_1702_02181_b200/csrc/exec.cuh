@@ -33,7 +33,7 @@ fold_status launch_cell_fwd_simt(int cell, int r0, int r1, const int32_t *gather
                                  const float *U, const float *b, float *H, float *C, float *Gact, int ld_g,
                                  int nl, cudaStream_t st);
 fold_status launch_root_out(bool bf16, int G, int S, int ld, int nl, const int32_t *root_row, const void *H,
-                            const float *C, float *h_root, float *c_root, cudaStream_t st);
+                            const float *C, float *h_root, float *c_root, const ScatterA *sc, cudaStream_t st);
 fold_status launch_cell_bwd_pw(bool bf16, int cell, int r0, int r1, int nl, int S, int ld, int ld_g,
                                const int32_t *cons_off, const int32_t *cons_edge, const int32_t *root_row,
                                const int32_t *root_perm, int G, const float *dh_root, const float *dc_root,

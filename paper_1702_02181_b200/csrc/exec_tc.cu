@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
                   const __grid_constant__ CUtensorMap tmU, int r0, int r1, int nl, int S, int Sp, int ld, int KBh,
                   int NT, int ntiles, const int32_t *__restrict__ gather, const float *__restrict__ bias,
                   __nv_bfloat16 *__restrict__ H, float *__restrict__ C, __nv_bfloat16 *__restrict__ Gact, int ld_g,
-                  ScatterA sc, int dbg_epi) {
+                  ScatterA sc, int dbg_epi, int bias_in_smem) {
   using Cfg = FwdCfg<GATES, W>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
@@ -92,6 +92,11 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
     ptx::tmem_alloc(&tmem_base_sh, Cfg::TMEM_COLS);
     ptx::tmem_relinquish();
   }
+  // the whole bias (GATES*S fp32) stays in shared memory when it fits next to the ring
+  float *sbias = reinterpret_cast<float *>(smem + ST * Cfg::STAGE);
+  if (bias_in_smem)
+    for (int i = tid; i < GATES * S; i += blockDim.x) sbias[i] = bias[i];
+  const float *bsrc = bias_in_smem ? sbias : bias;
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -151,6 +156,20 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
     const int q = warp & 3;            // TMEM lane quarter
     const int grp = (warp - 4) >> 2;   // column-chunk group (0 or 1)
     const int row = q * 32 + lane;
+    // per-row metadata (child rows, consumer edges) of the next tile is fetched while the
+    // current tile's epilogue runs
+    struct Meta { int gl, gr, ce0, ce1, e0; };
+    auto fetch_meta = [&](int t, Meta &m) {
+      const int64_t rr = r0 + (int64_t)(t / NT) * BM + row;
+      m.gl = m.gr = m.ce0 = m.ce1 = 0; m.e0 = 0;
+      if (t < ntiles && rr < r1) {
+        m.gl = gather[2 * rr]; m.gr = gather[2 * rr + 1];
+        m.ce0 = sc.cons_off[rr]; m.ce1 = sc.cons_off[rr + 1];
+        if (m.ce1 > m.ce0) m.e0 = sc.cons_edge[m.ce0];
+      }
+    };
+    Meta nxt;
+    fetch_meta(blockIdx.x, nxt);
     int tc = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, tc++) {
       const int acc = tc & 1;
@@ -158,12 +177,10 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
       const int j0 = (t % NT) * W;
       const int64_t r = r0 + (int64_t)(t / NT) * BM + row;
       const bool valid = r < r1 && !dbg_epi;
-      int64_t gl = 0, gr = 0;
-      int ce0 = 0, ce1 = 0;
-      if (valid) {
-        gl = gather[2 * r]; gr = gather[2 * r + 1];
-        ce0 = sc.cons_off[r]; ce1 = sc.cons_off[r + 1];
-      }
+      const Meta cur = nxt;
+      fetch_meta(t + gridDim.x, nxt);
+      const int64_t gl = cur.gl, gr = cur.gr;
+      const int ce0 = cur.ce0, ce1 = cur.ce1;
       const int64_t c = r - nl;
       // prefetch the first chunk's child cell states before waiting for the accumulator
       float cl[8], cr[8];
@@ -212,7 +229,7 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
         float hh[8];
         if constexpr (GATES == 1) {
 #pragma unroll
-          for (int u = 0; u < 8; u++) hh[u] = tanh_fast(z[0][u] + (jb + u < S ? __ldg(bias + jb + u) : 0.f));
+          for (int u = 0; u < 8; u++) hh[u] = tanh_fast(z[0][u] + (jb + u < S ? bsrc[jb + u] : 0.f));
           if (fullc) {
             uint4 pk = make_uint4(pack_bf16x2(hh[0], hh[1]), pack_bf16x2(hh[2], hh[3]), pack_bf16x2(hh[4], hh[5]),
                                   pack_bf16x2(hh[6], hh[7]));
@@ -231,12 +248,12 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
           for (int g = 0; g < 5; g++) {
             float bz[8];
             if (fullc) {
-              float4 x = __ldg(reinterpret_cast<const float4 *>(bias + g * S + jb));
-              float4 y = __ldg(reinterpret_cast<const float4 *>(bias + g * S + jb + 4));
+              float4 x = *reinterpret_cast<const float4 *>(bsrc + g * S + jb);
+              float4 y = *reinterpret_cast<const float4 *>(bsrc + g * S + jb + 4);
               bz[0] = x.x; bz[1] = x.y; bz[2] = x.z; bz[3] = x.w; bz[4] = y.x; bz[5] = y.y; bz[6] = y.z; bz[7] = y.w;
             } else {
 #pragma unroll
-              for (int u = 0; u < 8; u++) bz[u] = jb + u < S ? bias[g * S + jb + u] : 0.f;
+              for (int u = 0; u < 8; u++) bz[u] = jb + u < S ? bsrc[g * S + jb + u] : 0.f;
             }
 #pragma unroll
             for (int u = 0; u < 8; u++) gs[g][u] = g == 4 ? tanh_fast(z[g][u] + bz[u]) : sigmoid_fast(z[g][u] + bz[u]);
@@ -264,19 +281,20 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
             }
           }
         }
-        // h: pool row (append) + every consumer's A-operand row (push-gather)
+        // h: every consumer's A-operand row (push-gather); rows without consumers (roots,
+        // dead nodes) are appended to the H pool instead
         if (fullc) {
           uint4 pk = make_uint4(pack_bf16x2(hh[0], hh[1]), pack_bf16x2(hh[2], hh[3]), pack_bf16x2(hh[4], hh[5]),
                                 pack_bf16x2(hh[6], hh[7]));
-          *reinterpret_cast<uint4 *>(H + r * ld + jb) = pk;
+          if (ce1 == ce0) *reinterpret_cast<uint4 *>(H + r * ld + jb) = pk;
           for (int e = ce0; e < ce1; e++) {
-            int ed = sc.cons_edge[e];
+            int ed = e == ce0 ? cur.e0 : sc.cons_edge[e];
             *reinterpret_cast<uint4 *>(((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld + jb) = pk;
           }
         } else {
           for (int u = 0; u < 8 && jb + u < S; u++) {
             __nv_bfloat16 hv = __float2bfloat16_rn(hh[u]);
-            H[r * ld + jb + u] = hv;
+            if (ce1 == ce0) H[r * ld + jb + u] = hv;
             for (int e = ce0; e < ce1; e++) {
               int ed = sc.cons_edge[e];
               (((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld)[jb + u] = hv;
@@ -607,13 +625,16 @@ fold_status launch_fwd(int r0, int r1, int nl, int n_cells, const int32_t *gathe
   const int NTu = (int)cdiv(S, W);
   FOLD_TRY(make_map(&tmU, w.U, (uint64_t)w.ld_u, (uint64_t)NTu * Cfg::N, (uint64_t)w.ld_u * 2, BK, Cfg::N));
   auto kern = k_cell_fwd_tc<GATES, W>;
-  FOLD_TRY(set_smem(kern, Cfg::SMEM));
+  const int bias_bytes = GATES * S * 4;
+  const int bias_in_smem = Cfg::SMEM + bias_bytes <= 227 * 1024 ? 1 : 0;
+  const int smem_bytes = Cfg::SMEM + (bias_in_smem ? bias_bytes : 0);
+  FOLD_TRY(set_smem(kern, smem_bytes));
   const int NT = (int)cdiv(S, W);
   const int ntiles = NT * (int)cdiv(r1 - r0, BM);
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
   int KBh = (int)cdiv(S, BK);
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(tmAL, tmAR, tmU, r0, r1, nl, S, w.ld_u / 2, ld, KBh, NT, ntiles, gather, b,
-                                          H, C, Gact, ld_g, sc, dbg_fwd_epi());
+  kern<<<grid, Cfg::THREADS, smem_bytes, st>>>(tmAL, tmAR, tmU, r0, r1, nl, S, w.ld_u / 2, ld, KBh, NT, ntiles,
+                                               gather, b, H, C, Gact, ld_g, sc, dbg_fwd_epi(), bias_in_smem);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
