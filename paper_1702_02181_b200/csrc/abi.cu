@@ -34,6 +34,7 @@ fold_status check_sched(const fold_schedule_t *s) {
 // backward workspace carve
 struct BwdWs {
   float *dA, *dCe, *partial, *dU_split;
+  int32_t *root_off;
   void *dZ;
   TcWeights w;
   int ld_z, nsplit;
@@ -46,13 +47,14 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
   const int gates = gates_of(m->cell);
   const bool bf16 = m->prec == FOLD_PREC_BF16;
   b.ld_z = (int)round_up((int64_t)gates * S, 8);
-  b.nsplit = (int)(nc / 256 < 1 ? 1 : (nc / 256 > 128 ? 128 : nc / 256));
+  b.nsplit = (int)(nc / 128 < 1 ? 1 : (nc / 128 > 256 ? 256 : nc / 128));
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = a256(off + bytes); return o; };
   size_t o_dA = take((size_t)(2 * nc + 1) * S * 4);
   size_t o_dCe = take(gates == 5 ? (size_t)(2 * nc + 1) * S * 4 : 256);
   size_t o_dZ = take((size_t)(nc + 1) * b.ld_z * (bf16 ? 2 : 4));
   size_t o_part = take((size_t)b.nsplit * gates * S * 4);
+  size_t o_roff = take((size_t)(s->n_nodes + 2) * 4);
   size_t o_w = take(bf16 ? tc_workspace_bytes(gates, (int)S) : 0);
   const int splits = bf16 ? tc_dU_splits((int)nc, gates, (int)S) : 1;
   size_t o_spl = take(splits > 1 ? (size_t)splits * gates * S * 2 * S * 4 : 0);
@@ -63,6 +65,7 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
     b.dCe = (float *)(p + o_dCe);
     b.dZ = p + o_dZ;
     b.partial = (float *)(p + o_part);
+    b.root_off = (int32_t *)(p + o_roff);
     b.dU_split = splits > 1 ? (float *)(p + o_spl) : nullptr;
     if (bf16) {
       b.w.ld_u = (int)(2 * round_up(S, 64));
@@ -204,6 +207,7 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
   const bool bf16 = m->prec == FOLD_PREC_BF16;
   const int acc = grads->accumulate ? 1 : 0;
   if (!acc) FOLD_TRY(launch_zero(grads->dE, (size_t)m->vocab * S * 4, st));
+  if (N > 0) FOLD_TRY(launch_root_off(N, G, s->root_row, s->root_perm, b.root_off, st));
   if (N == 0 || nc == 0) {
     if (!acc) {
       FOLD_TRY(launch_zero(grads->dU, (size_t)gates * S * 2 * S * 4, st));
@@ -211,7 +215,7 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
     }
     if (N > 0)
       FOLD_TRY(launch_embed_bwd(S, nl, s->n_tok_segs, s->tok_seg, s->leaf_perm, s->leaf_token, s->cons_off,
-                                s->cons_edge, s->root_row, s->root_perm, G, dh_root, b.dA, grads->dE, st));
+                                s->cons_edge, b.root_off, s->root_perm, G, dh_root, b.dA, grads->dE, st));
     return FOLD_OK;
   }
   if (!acts) return FOLD_E_INVALID;
@@ -230,7 +234,7 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
     if (M <= 0) continue;
     {
     ProfScope ps(K_BWD_PW, st);
-    FOLD_TRY(launch_cell_bwd_pw(bf16, m->cell, r0, r1, nl, S, L.ld, L.ld_g, s->cons_off, s->cons_edge, s->root_row,
+    FOLD_TRY(launch_cell_bwd_pw(bf16, m->cell, r0, r1, nl, S, L.ld, L.ld_g, s->cons_off, s->cons_edge, b.root_off,
                                 s->root_perm, G, dh_root, dc_root, s->gather, Gact, C, b.dA, b.dCe, b.dZ, b.ld_z, st));
     }
     ProfScope ps(K_GEMM_DA, st);
@@ -243,7 +247,7 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
   {
     ProfScope ps(K_EMBED_BWD, st);
     FOLD_TRY(launch_embed_bwd(S, nl, s->n_tok_segs, s->tok_seg, s->leaf_perm, s->leaf_token, s->cons_off,
-                              s->cons_edge, s->root_row, s->root_perm, G, dh_root, b.dA, grads->dE, st));
+                              s->cons_edge, b.root_off, s->root_perm, G, dh_root, b.dA, grads->dE, st));
   }
   {
   ProfScope ps(K_GEMM_DU, st);

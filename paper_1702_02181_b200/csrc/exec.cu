@@ -230,7 +230,7 @@ template <> struct VecIO<__nv_bfloat16, 4> {
 // 8-byte bf16 accesses stay aligned since every row stride is a multiple of 8 elements).
 template <typename T, int GATES, int VEC>
 __global__ void k_cell_bwd_pw(int r0, int r1, int nl, int S, int ld, int ld_g, const int32_t *__restrict__ cons_off,
-                              const int32_t *__restrict__ cons_edge, const int32_t *__restrict__ root_row,
+                              const int32_t *__restrict__ cons_edge, const int32_t *__restrict__ root_off,
                               const int32_t *__restrict__ root_perm, int G, const float *__restrict__ dh_root,
                               const float *__restrict__ dc_root, const int32_t *__restrict__ gather,
                               const T *__restrict__ Gact, const float *__restrict__ C, const float *__restrict__ dA,
@@ -243,12 +243,8 @@ __global__ void k_cell_bwd_pw(int r0, int r1, int nl, int S, int ld, int ld_g, c
   for (int64_t r = r0 + w; r < r1; r += nw) {
     int64_t c = r - nl;
     int e0 = cons_off[r], e1 = cons_off[r + 1];
-    // roots seeded at this row: root_perm orders graphs by (root_row, g)
-    int lo = 0, hi = G;
-    while (lo < hi) { int mid = (lo + hi) >> 1; if (root_row[root_perm[mid]] < r) lo = mid + 1; else hi = mid; }
-    int rs0 = lo;
-    int rs1 = rs0;
-    while (rs1 < G && root_row[root_perm[rs1]] == r) rs1++;
+    // roots seeded at this row: root_perm[root_off[r] .. root_off[r+1]) (ascending g)
+    const int rs0 = root_off[r], rs1 = root_off[r + 1];
     const T *ga = Gact + c * ld_g;
     T *dz = dZ + c * ld_z;
     int64_t gL = gather[2 * r], gR = gather[2 * r + 1];
@@ -419,16 +415,32 @@ __global__ void __launch_bounds__(256) k_gemm_dU_simt(int n_cells, int nl, int S
 
 // ---------------------------------------------------------------- column sums (db)
 // partial[s][j] = sum over rows of split s (ascending) ; then db[j] = sum_s partial[s][j].
-template <typename T>
+// VEC consecutive columns per thread (16-byte bf16 / 32-byte fp32 loads per row).
+template <typename T, int VEC>
 __global__ void k_colsum_partial(int n_rows, int ncols, const T *__restrict__ X, int ldx, int nsplit,
                                  float *__restrict__ partial) {
+  using IT = VecIO<T, VEC == 8 ? 4 : 1>;
   int s = blockIdx.y;
   int64_t rows_per = cdiv(n_rows, nsplit);
   int64_t a = s * rows_per, b = a + rows_per < n_rows ? a + rows_per : n_rows;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ncols; j += gridDim.x * blockDim.x) {
-    float acc = 0.f;
-    for (int64_t r = a; r < b; r++) acc += to_f(X[r * ldx + j]);
-    partial[(int64_t)s * ncols + j] = acc;
+  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) * VEC; j < ncols; j += gridDim.x * blockDim.x * VEC) {
+    float acc[VEC];
+#pragma unroll
+    for (int u = 0; u < VEC; u++) acc[u] = 0.f;
+    for (int64_t r = a; r < b; r++) {
+      const T *x = X + r * ldx + j;
+      if constexpr (VEC == 8) {
+        float t0[4], t1[4];
+        IT::ld(x, t0);
+        IT::ld(x + 4, t1);
+#pragma unroll
+        for (int u = 0; u < 4; u++) { acc[u] += t0[u]; acc[4 + u] += t1[u]; }
+      } else {
+        acc[0] += to_f(x[0]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < VEC; u++) partial[(int64_t)s * ncols + j + u] = acc[u];
   }
 }
 
@@ -438,6 +450,18 @@ __global__ void k_colsum_final(int ncols, int nsplit, const float *__restrict__ 
     float acc = 0.f;
     for (int s = 0; s < nsplit; s++) acc += partial[(int64_t)s * ncols + j];
     out[j] = accumulate ? out[j] + acc : acc;
+  }
+}
+
+// root_off[r] = #graphs whose root row is < r (r = 0..N): the roots seeded at row r are
+// root_perm[root_off[r] .. root_off[r+1]).
+__global__ void k_root_off(int N, int G, const int32_t *__restrict__ root_row, const int32_t *__restrict__ root_perm,
+                           int32_t *__restrict__ root_off) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= N; r += stride) {
+    int lo = 0, hi = G;
+    while (lo < hi) { int mid = (lo + hi) >> 1; if (root_row[root_perm[mid]] < r) lo = mid + 1; else hi = mid; }
+    root_off[r] = lo;
   }
 }
 
@@ -452,7 +476,7 @@ __global__ void __launch_bounds__(128) k_embed_bwd(int S, int n_tok_segs, const 
                                                    const int32_t *__restrict__ leaf_token,
                                                    const int32_t *__restrict__ cons_off,
                                                    const int32_t *__restrict__ cons_edge,
-                                                   const int32_t *__restrict__ root_row,
+                                                   const int32_t *__restrict__ root_off,
                                                    const int32_t *__restrict__ root_perm, int G,
                                                    const float *__restrict__ dh_root, const float *__restrict__ dA,
                                                    float *__restrict__ dE) {
@@ -466,9 +490,8 @@ __global__ void __launch_bounds__(128) k_embed_bwd(int S, int n_tok_segs, const 
       IF::ld(de + j, acc);
       for (int q = a; q < b; q++) {
         const int r = leaf_perm[q];
-        int lo = 0, hi = G;
-        while (lo < hi) { int mid = (lo + hi) >> 1; if (root_row[root_perm[mid]] < r) lo = mid + 1; else hi = mid; }
-        for (int k = lo; k < G && root_row[root_perm[k]] == r; k++) {
+        const int k1 = root_off[r + 1];
+        for (int k = root_off[r]; k < k1; k++) {
           IF::ld(dh_root + (int64_t)root_perm[k] * S + j, t);
 #pragma unroll
           for (int u = 0; u < VEC; u++) acc[u] += t[u];
@@ -536,13 +559,13 @@ fold_status launch_root_out(bool bf16, int G, int S, int ld, int nl, const int32
 }
 
 fold_status launch_cell_bwd_pw(bool bf16, int cell, int r0, int r1, int nl, int S, int ld, int ld_g,
-                               const int32_t *cons_off, const int32_t *cons_edge, const int32_t *root_row,
+                               const int32_t *cons_off, const int32_t *cons_edge, const int32_t *root_off,
                                const int32_t *root_perm, int G, const float *dh_root, const float *dc_root,
                                const int32_t *gather, const void *Gact, const float *C, const float *dA, float *dCe,
                                void *dZ, int ld_z, cudaStream_t st) {
   if (r1 <= r0) return FOLD_OK;
   unsigned g = grid_cap(cdiv((int64_t)(r1 - r0) * 32, 256));
-#define PW_ARGS r0, r1, nl, S, ld, ld_g, cons_off, cons_edge, root_row, root_perm, G, dh_root, dc_root, gather
+#define PW_ARGS r0, r1, nl, S, ld, ld_g, cons_off, cons_edge, root_off, root_perm, G, dh_root, dc_root, gather
 #define PW_LAUNCH(T, GT, VEC) \
   k_cell_bwd_pw<T, GT, VEC><<<g, 256, 0, st>>>(PW_ARGS, (const T *)Gact, C, dA, dCe, (T *)dZ, ld_z)
   const bool v4 = (S & 3) == 0;
@@ -580,27 +603,41 @@ fold_status launch_gemm_dU_simt(int n_cells, int nl, int S, int gates, const flo
 
 fold_status launch_colsum(bool bf16, int n_rows, int ncols, const void *dZ, int ld_z, float *partial, int nsplit,
                           float *db, int accumulate, cudaStream_t st) {
-  dim3 grid((unsigned)cdiv(ncols, 256), (unsigned)nsplit);
-  if (bf16) k_colsum_partial<__nv_bfloat16><<<grid, 256, 0, st>>>(n_rows, ncols, (const __nv_bfloat16 *)dZ, ld_z, nsplit, partial);
-  else k_colsum_partial<float><<<grid, 256, 0, st>>>(n_rows, ncols, (const float *)dZ, ld_z, nsplit, partial);
+  const bool v8 = (ncols & 7) == 0 && (ld_z & 7) == 0;
+  const int vec = v8 ? 8 : 1;
+  dim3 grid((unsigned)cdiv(cdiv(ncols, vec), 256), (unsigned)nsplit);
+  if (bf16) {
+    if (v8) k_colsum_partial<__nv_bfloat16, 8><<<grid, 256, 0, st>>>(n_rows, ncols, (const __nv_bfloat16 *)dZ, ld_z, nsplit, partial);
+    else k_colsum_partial<__nv_bfloat16, 1><<<grid, 256, 0, st>>>(n_rows, ncols, (const __nv_bfloat16 *)dZ, ld_z, nsplit, partial);
+  } else {
+    if (v8) k_colsum_partial<float, 8><<<grid, 256, 0, st>>>(n_rows, ncols, (const float *)dZ, ld_z, nsplit, partial);
+    else k_colsum_partial<float, 1><<<grid, 256, 0, st>>>(n_rows, ncols, (const float *)dZ, ld_z, nsplit, partial);
+  }
   FOLD_LAUNCH_CHECK();
   k_colsum_final<<<(unsigned)cdiv(ncols, 256), 256, 0, st>>>(ncols, nsplit, partial, db, accumulate);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
 
+fold_status launch_root_off(int N, int G, const int32_t *root_row, const int32_t *root_perm, int32_t *root_off,
+                            cudaStream_t st) {
+  k_root_off<<<grid_cap(cdiv((int64_t)N + 1, 256)), 256, 0, st>>>(N, G, root_row, root_perm, root_off);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
 fold_status launch_embed_bwd(int S, int nl, int n_tok_segs, const int32_t *tok_seg, const int32_t *leaf_perm,
                              const int32_t *leaf_token, const int32_t *cons_off,
-                             const int32_t *cons_edge, const int32_t *root_row, const int32_t *root_perm, int G,
+                             const int32_t *cons_edge, const int32_t *root_off, const int32_t *root_perm, int G,
                              const float *dh_root, const float *dA, float *dE, cudaStream_t st) {
   (void)nl;
   if (n_tok_segs <= 0) return FOLD_OK;
   unsigned g = grid_cap(n_tok_segs);
   if ((S & 3) == 0)
-    k_embed_bwd<4><<<g, 128, 0, st>>>(S, n_tok_segs, tok_seg, leaf_perm, leaf_token, cons_off, cons_edge, root_row,
+    k_embed_bwd<4><<<g, 128, 0, st>>>(S, n_tok_segs, tok_seg, leaf_perm, leaf_token, cons_off, cons_edge, root_off,
                                       root_perm, G, dh_root, dA, dE);
   else
-    k_embed_bwd<1><<<g, 128, 0, st>>>(S, n_tok_segs, tok_seg, leaf_perm, leaf_token, cons_off, cons_edge, root_row,
+    k_embed_bwd<1><<<g, 128, 0, st>>>(S, n_tok_segs, tok_seg, leaf_perm, leaf_token, cons_off, cons_edge, root_off,
                                       root_perm, G, dh_root, dA, dE);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;

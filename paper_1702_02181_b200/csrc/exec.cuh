@@ -35,7 +35,7 @@ fold_status launch_cell_fwd_simt(int cell, int r0, int r1, const int32_t *gather
 fold_status launch_root_out(bool bf16, int G, int S, int ld, int nl, const int32_t *root_row, const void *H,
                             const float *C, float *h_root, float *c_root, const ScatterA *sc, cudaStream_t st);
 fold_status launch_cell_bwd_pw(bool bf16, int cell, int r0, int r1, int nl, int S, int ld, int ld_g,
-                               const int32_t *cons_off, const int32_t *cons_edge, const int32_t *root_row,
+                               const int32_t *cons_off, const int32_t *cons_edge, const int32_t *root_off,
                                const int32_t *root_perm, int G, const float *dh_root, const float *dc_root,
                                const int32_t *gather, const void *Gact, const float *C, const float *dA,
                                float *dCe, void *dZ, int ld_z, cudaStream_t st);
@@ -51,8 +51,10 @@ fold_status launch_colsum(bool bf16, int n_rows, int ncols, const void *dZ, int 
                           int nsplit, float *db, int accumulate, cudaStream_t st);
 fold_status launch_embed_bwd(int S, int nl, int n_tok_segs, const int32_t *tok_seg, const int32_t *leaf_perm,
                              const int32_t *leaf_token, const int32_t *cons_off,
-                             const int32_t *cons_edge, const int32_t *root_row, const int32_t *root_perm, int G,
+                             const int32_t *cons_edge, const int32_t *root_off, const int32_t *root_perm, int G,
                              const float *dh_root, const float *dA, float *dE, cudaStream_t st);
+fold_status launch_root_off(int N, int G, const int32_t *root_row, const int32_t *root_perm, int32_t *root_off,
+                            cudaStream_t st);
 fold_status launch_sgd(float *p, const float *g, int64_t n, float lr, cudaStream_t st);
 fold_status launch_zero(void *p, size_t bytes, cudaStream_t st);
 

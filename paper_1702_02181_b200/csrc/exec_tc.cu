@@ -317,88 +317,109 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
 }
 
 // =================================================================== dA = dZ * U (one level)
+// Persistent (grid = min(#tiles, #SMs)), tile t -> (N tile t % NTn, row tile t / NTn),
+// 128 x 256 tiles, two TMEM accumulators so the fp32 store epilogue of tile i overlaps the
+// main loop of tile i+1.
 constexpr int DA_N = 256;
 constexpr int DA_A_BYTES = BM * 128, DA_B_BYTES = DA_N * 128, DA_STAGE = DA_A_BYTES + DA_B_BYTES;
 constexpr int DA_SMEM = ST * DA_STAGE + 1024;
 
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_dA_tc(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmUt, int c0, int M,
-                 int KB, int S, float *__restrict__ dA) {
+                 int KB, int S, int NTn, int ntiles, float *__restrict__ dA) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
-  __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull;
+  __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int mt = c0 + blockIdx.y * BM, n0 = blockIdx.x * DA_N;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < ST; s++) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
-    ptx::mbar_init(&tfull, 1);
+    for (int a = 0; a < 2; a++) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 4); }
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tmZ);
     ptx::prefetch_tmap(&tmUt);
   }
-  if (warp == 2) { ptx::tmem_alloc(&tmem_base_sh, 256); ptx::tmem_relinquish(); }
+  if (warp == 2) { ptx::tmem_alloc(&tmem_base_sh, 512); ptx::tmem_relinquish(); }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = tmem_base_sh;
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < KB; kb++) {
-        int s = kb % ST;
-        uint32_t ph = (kb / ST) & 1;
-        ptx::mbar_wait(&empty[s], ph ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[s], DA_STAGE);
-        uint8_t *A = smem + s * DA_STAGE;
-        ptx::tma_load_2d(&tmZ, &full[s], A, kb * BK, mt);
-        ptx::tma_load_2d(&tmUt, &full[s], A + DA_A_BYTES, kb * BK, n0);
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int mt = c0 + (t / NTn) * BM, n0 = (t % NTn) * DA_N;
+        for (int kb = 0; kb < KB; kb++, it++) {
+          int s = it % ST;
+          uint32_t ph = (it / ST) & 1;
+          ptx::mbar_wait(&empty[s], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[s], DA_STAGE);
+          uint8_t *A = smem + s * DA_STAGE;
+          ptx::tma_load_2d(&tmZ, &full[s], A, kb * BK, mt);
+          ptx::tma_load_2d(&tmUt, &full[s], A + DA_A_BYTES, kb * BK, n0);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_bf16(BM, DA_N, 0, 0);
-      for (int kb = 0; kb < KB; kb++) {
-        int s = kb % ST;
-        uint32_t ph = (kb / ST) & 1;
-        ptx::mbar_wait(&full[s], ph);
+      int it = 0, tc = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, tc++) {
+        const int acc = tc & 1;
+        ptx::mbar_wait(&tempty[acc], ((tc >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
-        uint32_t a0 = ptx::smem_u32(smem + s * DA_STAGE), b0 = a0 + DA_A_BYTES;
+        const uint32_t dst = tbase + acc * 256;
+        for (int kb = 0; kb < KB; kb++, it++) {
+          int s = it % ST;
+          uint32_t ph = (it / ST) & 1;
+          ptx::mbar_wait(&full[s], ph);
+          ptx::tc_fence_after();
+          uint32_t a0 = ptx::smem_u32(smem + s * DA_STAGE), b0 = a0 + DA_A_BYTES;
 #pragma unroll
-        for (int k = 0; k < BK / 16; k++)
-          ptx::umma_bf16(tbase, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024), ptx::sdesc_sw128(b0 + 32 * k, 16, 1024),
-                         idesc, (kb | k) != 0);
-        ptx::umma_commit(&empty[s]);
+          for (int k = 0; k < BK / 16; k++)
+            ptx::umma_bf16(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024), ptx::sdesc_sw128(b0 + 32 * k, 16, 1024),
+                           idesc, (kb | k) != 0);
+          ptx::umma_commit(&empty[s]);
+        }
+        ptx::umma_commit(&tfull[acc]);
       }
-      ptx::umma_commit(&tfull);
     }
   } else if (warp >= 4) {
     const int q = warp & 3;
-    ptx::mbar_wait(&tfull, 0);
-    ptx::tc_fence_after();
-    const int row = q * 32 + lane;
-    const int64_t c = mt + row;
-    const bool valid = (c - c0) < M;
     const int N2 = 2 * S;
-    const uint32_t tl = tbase + ((uint32_t)(q * 32) << 16);
-    float *out = dA + c * N2;
+    int tc = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, tc++) {
+      const int acc = tc & 1;
+      const int mt = c0 + (t / NTn) * BM, n0 = (t % NTn) * DA_N;
+      const int row = q * 32 + lane;
+      const int64_t c = mt + row;
+      const bool valid = (c - c0) < M;
+      float *out = dA + c * N2;
+      ptx::mbar_wait(&tfull[acc], (tc >> 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t tl = tbase + acc * 256 + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-    for (int nc = 0; nc < DA_N / 8; nc++) {
-      float v[8];
-      ptx::tmem_ld8(tl + nc * 8, v);
-      ptx::tmem_ld_wait();
-      int n = n0 + nc * 8;
-      if (!valid || n >= N2) continue;
-      if (n + 8 <= N2 && (N2 & 3) == 0) {
-        *reinterpret_cast<float4 *>(out + n) = make_float4(v[0], v[1], v[2], v[3]);
-        *reinterpret_cast<float4 *>(out + n + 4) = make_float4(v[4], v[5], v[6], v[7]);
-      } else {
-        for (int u = 0; u < 8 && n + u < N2; u++) out[n + u] = v[u];
+      for (int nc = 0; nc < DA_N / 8; nc++) {
+        float v[8];
+        ptx::tmem_ld8(tl + nc * 8, v);
+        ptx::tmem_ld_wait();
+        int n = n0 + nc * 8;
+        if (!valid || n >= N2) continue;
+        if (n + 8 <= N2 && (N2 & 3) == 0) {
+          *reinterpret_cast<float4 *>(out + n) = make_float4(v[0], v[1], v[2], v[3]);
+          *reinterpret_cast<float4 *>(out + n + 4) = make_float4(v[4], v[5], v[6], v[7]);
+        } else {
+          for (int u = 0; u < 8 && n + u < N2; u++) out[n + u] = v[u];
+        }
       }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc(tbase, 256); }
+  if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc(tbase, 512); }
 }
 
 // =================================================================== dU = dZ^T * Acat (all cells)
@@ -689,9 +710,11 @@ fold_status tc_gemm_dA(int c0, int M, int n_cells, int S, int gates, const __nv_
   FOLD_TRY(make_map(&tmZ, dZ, (uint64_t)gates * S, (uint64_t)n_cells, (uint64_t)ld_z * 2, BK, BM));
   FOLD_TRY(make_map(&tmUt, w.Ut, (uint64_t)gates * S, (uint64_t)2 * S, (uint64_t)w.ld_ut * 2, BK, DA_N));
   FOLD_TRY(set_smem(k_gemm_dA_tc, DA_SMEM));
-  dim3 grid((unsigned)cdiv(2 * S, DA_N), (unsigned)cdiv(M, BM));
+  const int NTn = (int)cdiv(2 * S, DA_N);
+  const int ntiles = NTn * (int)cdiv(M, BM);
+  const int grid = ntiles < num_sms() ? ntiles : num_sms();
   int KB = (int)cdiv(gates * S, BK);
-  k_gemm_dA_tc<<<grid, kThreads, DA_SMEM, st>>>(tmZ, tmUt, c0, M, KB, S, dA);
+  k_gemm_dA_tc<<<grid, kThreads, DA_SMEM, st>>>(tmZ, tmUt, c0, M, KB, S, NTn, ntiles, dA);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
