@@ -77,6 +77,32 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
   return b;
 }
 
+// Library-owned auxiliary stream (one per host thread and device), used to overlap
+// independent memory-bound kernels with tensor-bound ones inside one ABI call; ordering
+// with the caller's stream is by events, so the call stays stream-ordered for the caller.
+struct AuxStream {
+  bool ok = false;
+  int dev = -1;
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+AuxStream &aux_stream() {
+  static thread_local AuxStream ax[16];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) {
+    static AuxStream none;
+    return none;
+  }
+  AuxStream &a = ax[dev];
+  if (!a.ok) {
+    a.ok = cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) == cudaSuccess;
+    a.dev = dev;
+  }
+  return a;
+}
+
 size_t fwd_ws_bytes(const fold_model *m) {
   if (m->prec != FOLD_PREC_BF16) return 256;
   return tc_workspace_bytes(gates_of(m->cell), m->S);
@@ -244,24 +270,39 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
     else
       FOLD_TRY(launch_gemm_dA_simt(M, S, gates, (const float *)b.dZ + (size_t)c0 * b.ld_z, b.ld_z, m->U, dA_lvl, st));
   }
+  // The embedding gradient and db only need dA / dZ, the weight-gradient GEMM only dZ and
+  // the A planes: run the two memory-bound reductions on an auxiliary stream beside the
+  // tensor-bound dU GEMM, then join.
+  AuxStream &ax = aux_stream();
+  cudaStream_t s2 = ax.ok ? ax.s : st;
+  if (ax.ok) {
+    FOLD_CUDA_TRY(cudaEventRecord(ax.fork, st));
+    FOLD_CUDA_TRY(cudaStreamWaitEvent(s2, ax.fork, 0));
+  }
   {
-    ProfScope ps(K_EMBED_BWD, st);
+    ProfScope ps(K_EMBED_BWD, s2);
     FOLD_TRY(launch_embed_bwd(S, nl, s->n_tok_segs, s->tok_seg, s->leaf_perm, s->leaf_token, s->cons_off,
-                              s->cons_edge, b.root_off, s->root_perm, G, dh_root, b.dA, grads->dE, st));
+                              s->cons_edge, b.root_off, s->root_perm, G, dh_root, b.dA, grads->dE, s2));
   }
   {
-  ProfScope ps(K_GEMM_DU, st);
-  if (bf16)
-    FOLD_TRY(tc_gemm_dU(nc, S, gates, (const __nv_bfloat16 *)b.dZ, b.ld_z,
-                        ScatterA{s->cons_off, s->cons_edge, (__nv_bfloat16 *)(a + L.al_off),
-                                 (__nv_bfloat16 *)(a + L.ar_off), L.ld},
-                        grads->dU, acc, b.dU_split, st));
-  else
-    FOLD_TRY(launch_gemm_dU_simt(nc, nl, S, gates, (const float *)b.dZ, b.ld_z, s->gather, (const float *)H, L.ld,
-                                 grads->dU, acc, st));
+    ProfScope ps(K_COLSUM, s2);
+    FOLD_TRY(launch_colsum(bf16, nc, gates * S, b.dZ, b.ld_z, b.partial, b.nsplit, grads->db, acc, s2));
   }
-  ProfScope ps(K_COLSUM, st);
-  FOLD_TRY(launch_colsum(bf16, nc, gates * S, b.dZ, b.ld_z, b.partial, b.nsplit, grads->db, acc, st));
+  {
+    ProfScope ps(K_GEMM_DU, st);
+    if (bf16)
+      FOLD_TRY(tc_gemm_dU(nc, S, gates, (const __nv_bfloat16 *)b.dZ, b.ld_z,
+                          ScatterA{s->cons_off, s->cons_edge, (__nv_bfloat16 *)(a + L.al_off),
+                                   (__nv_bfloat16 *)(a + L.ar_off), L.ld},
+                          grads->dU, acc, b.dU_split, st));
+    else
+      FOLD_TRY(launch_gemm_dU_simt(nc, nl, S, gates, (const float *)b.dZ, b.ld_z, s->gather, (const float *)H, L.ld,
+                                   grads->dU, acc, st));
+  }
+  if (ax.ok) {
+    FOLD_CUDA_TRY(cudaEventRecord(ax.join, s2));
+    FOLD_CUDA_TRY(cudaStreamWaitEvent(st, ax.join, 0));
+  }
   return FOLD_OK;
 }
 

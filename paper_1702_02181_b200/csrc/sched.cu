@@ -149,9 +149,29 @@ __global__ void k_scan_add(int32_t *out, int64_t n, const int32_t *sums) {
     if (base + i < n) out[base + i] += add;
 }
 
+// single-block exclusive scan for small arrays (one launch): 1024 threads x 16 items
+constexpr int kSmallScan = kScanThreads * 16;
+__global__ void k_scan_small(const int32_t *in, int32_t *out, int n, int32_t *total) {
+  __shared__ int sw[32];
+  int v[16], sum = 0;
+  const int base = threadIdx.x * 16;
+#pragma unroll
+  for (int i = 0; i < 16; i++) { v[i] = base + i < n ? in[base + i] : 0; sum += v[i]; }
+  int tot;
+  int ex = block_excl_scan(sum, sw, &tot);
+#pragma unroll
+  for (int i = 0; i < 16; i++) { if (base + i < n) out[base + i] = ex; ex += v[i]; }
+  if (threadIdx.x == 0 && total) *total = tot;
+}
+
 fold_status excl_scan(const int32_t *in, int32_t *out, int64_t n, int32_t *sums, int32_t *total,
                       cudaStream_t st) {
   if (n <= 0) return FOLD_OK;
+  if (n <= kSmallScan) {
+    k_scan_small<<<1, kScanThreads, 0, st>>>(in, out, (int)n, total);
+    FOLD_LAUNCH_CHECK();
+    return FOLD_OK;
+  }
   int64_t nt = cdiv(n, kScanTile);
   k_scan_tiles<<<(unsigned)nt, kScanThreads, 0, st>>>(in, out, n, sums);
   FOLD_LAUNCH_CHECK();
@@ -383,9 +403,11 @@ __global__ void k_gather(int N, const int32_t *op, const int32_t *child, const i
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += stride) {
     int n = perm[r];
+    int c0 = child[2 * n], c1 = child[2 * n + 1];
     bool cell = op[n] == FOLD_OP_CELL;
-    gather[2 * r] = cell ? rank[child[2 * n]] : -1;
-    gather[2 * r + 1] = cell ? rank[child[2 * n + 1]] : -1;
+    // out-of-range children are reported by k_validate; never index with them
+    gather[2 * r] = (cell && c0 >= 0 && c0 < N) ? rank[c0] : -1;
+    gather[2 * r + 1] = (cell && c1 >= 0 && c1 < N) ? rank[c1] : -1;
   }
 }
 
@@ -450,15 +472,51 @@ __global__ void k_seg_write(int N, const int32_t *seg_flag, const int32_t *seg_s
   if (blockIdx.x == 0 && threadIdx.x == 0) tok_seg[nseg] = cnt;
 }
 
-__global__ void k_root_keys(int G, const int32_t *root, const int32_t *rank, int32_t *root_row,
+__global__ void k_root_keys(int N, int G, const int32_t *root, const int32_t *rank, int32_t *root_row,
                             uint32_t *keys, int32_t *vals) {
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += stride) {
-    int rr = rank[root[g]];
+    int ro = root[g];
+    int rr = (ro >= 0 && ro < N) ? rank[ro] : 0;  // invalid roots are reported by k_validate
     root_row[g] = rr;
     keys[g] = (uint32_t)rr;
     vals[g] = (int)g;
   }
+}
+
+// Stable sort of graph ids by root row for G <= 4096 in one block: bitonic sort of the
+// unique composite keys (root_row << 32 | g), so ties keep ascending g.
+constexpr int kSmallRoots = 4096;
+__global__ void k_roots_small(int N, int G, const int32_t *root, const int32_t *rank, int32_t *root_row,
+                              int32_t *root_perm) {
+  __shared__ unsigned long long key[kSmallRoots];
+  int n2 = 1;
+  while (n2 < G) n2 <<= 1;
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    if (i < G) {
+      int ro = root[i];
+      int rr = (ro >= 0 && ro < N) ? rank[ro] : 0;  // invalid roots are reported by k_validate
+      root_row[i] = rr;
+      key[i] = ((unsigned long long)(unsigned)rr << 32) | (unsigned)i;
+    } else {
+      key[i] = ~0ull;
+    }
+  }
+  __syncthreads();
+  for (int k = 2; k <= n2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        int ixj = i ^ j;
+        if (ixj > i) {
+          unsigned long long a = key[i], b = key[ixj];
+          bool up = (i & k) == 0;
+          if ((a > b) == up) { key[i] = b; key[ixj] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < G; i += blockDim.x) root_perm[i] = (int32_t)(key[i] & 0xffffffffu);
 }
 
 __global__ void k_copy_i32(const int32_t *src, int32_t *dst, int64_t n) {
@@ -575,9 +633,12 @@ fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr
   FOLD_LAUNCH_CHECK();
 
   // ---- roots
-  if (G > 0) {
+  if (G > 0 && G <= kSmallRoots) {
+    k_roots_small<<<1, 1024, 0, st>>>(N, G, gr->root, s->rank, s->root_row, s->root_perm);
+    FOLD_LAUNCH_CHECK();
+  } else if (G > 0) {
     int32_t *d_G = w.flags + 23;  // flags[23] = G (k_init_flags)
-    k_root_keys<<<grid_for(G), 256, 0, st>>>(G, gr->root, s->rank, s->root_row, w.ka, w.va);
+    k_root_keys<<<grid_for(G), 256, 0, st>>>(N, G, gr->root, s->rank, s->root_row, w.ka, w.va);
     FOLD_LAUNCH_CHECK();
     FOLD_TRY(radix_sort(w, d_G, G, bits_for(N), &sk, &sv, st));
     k_copy_i32<<<grid_for(G), 256, 0, st>>>(sv, s->root_perm, G);
