@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-batch1", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--ref-trees", type=int, default=1, help="trees per oracle step (--impl reference)")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the nodes/s vs batch-size sweep")
     return ap.parse_args()
 
 
@@ -184,8 +185,9 @@ def run_fold(args):
     # size the schedule workspace once (fold_schedule_workspace)
     sched_ws = torch.empty(int(fold.load().fold_schedule_workspace(N_nodes, gr.n_graphs)), dtype=torch.uint8,
                            device=dev)
-    for _ in range(max(args.warmup, 3 if args.warmup >= 3 else args.warmup)):
+    for _ in range(args.warmup):
         step(op, child, token, root, g_dev)
+    n_levels = fold.schedule(op, child, token, root, V, workspace=sched_ws).n_levels
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local) if not args.no_clocks else None
@@ -276,6 +278,31 @@ def run_fold(args):
         ms1 = b0.elapsed_time(b1) / nrep
         batch1 = {"nodes_per_s": one.n_nodes / (ms1 / 1e3), "ms_per_tree": ms1}
 
+    # ---------------- nodes/s vs batch size (BASELINE metric "... vs batch size"), rank 0
+    sweep = None
+    if not args.no_sweep and rank == 0 and args.config in ("c2", "c3", "c4", "c5"):
+        sweep = {}
+        for Bs in (1, 4, 16, 64, 256):
+            if Bs >= gr.n_graphs:
+                break
+            sub = foldgen.sub_batch(gr, 0, Bs)
+            o = fold.graphs_to_device(sub, dev)
+            gs = g_dev[:Bs].contiguous()
+            for _ in range(3):
+                step(*o, gs)
+            torch.cuda.synchronize()
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            nrep = 10
+            s0.record()
+            for _ in range(nrep):
+                step(*o, gs)
+            s1.record()
+            torch.cuda.synchronize()
+            msb = s0.elapsed_time(s1) / nrep
+            sweep[str(Bs)] = {"nodes_per_s": sub.n_nodes / (msb / 1e3), "ms_per_step": msb}
+        sweep[str(gr.n_graphs)] = {"nodes_per_s": value / world, "ms_per_step": ms_per_step}
+
     if world > 1:
         dist.barrier()
     if rank != 0:
@@ -294,10 +321,13 @@ def run_fold(args):
     achieved = flops_per_cell * n_cells * args.steps / (dom_ms_total / 1e3) / 1e12
     peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
     traffic = None
+    traffic_note = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(tensor_classes[dom], {}).get("dram_bytes_per_launch")
+            tr = json.load(open(tpath)).get(tensor_classes[dom], {})
+            traffic = tr.get("dram_bytes_per_launch")
+            traffic_note = tr.get("launch")
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "kernel": tensor_classes[dom], "achieved": achieved, "peak": peak,
@@ -305,7 +335,9 @@ def run_fold(args):
                 "peak_source": f"{pk_src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
                 "algorithmic": f"{flops_per_cell:.4g} FLOP/cell x {n_cells} cells per launch-set; "
                                f"{dom_launches // max(args.steps, 1)} launches/step",
-                "share_of_step": (dom_ms_total / args.steps) / ms_per_step}
+                "share_of_step": (dom_ms_total / args.steps) / ms_per_step,
+                "traffic_source": ("ncu --set full, DRAM read+write bytes of one launch (%s); profiles/ncu_traffic.json"
+                                   % traffic_note) if traffic is not None else None}
 
     # ---------------- CPU baseline: the fp64 oracle as it stands, bounded sample, 1 thread
     cpu = None
@@ -317,7 +349,7 @@ def run_fold(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.prec, "data": "synthetic",
         "config": {"workload": desc, "trees_per_gpu": gr.n_graphs, "nodes_per_gpu": N_nodes,
-                   "cells_per_gpu": n_cells, "state": S, "cell": cell, "levels": None,
+                   "cells_per_gpu": n_cells, "state": S, "cell": cell, "levels": n_levels,
                    "step": "schedule+fwd+bwd+allreduce+sgd" if world > 1 else "schedule+fwd+bwd+sgd",
                    "l2": "working set > L2 (pool+saved gates+grads ~%.1f GB); no flush" % (
                        (N_nodes * S * 6 + n_cells * gates * S * 4 + n_cells * S * 16) / 1e9),
@@ -329,6 +361,8 @@ def run_fold(args):
         "e2e": e2e,
         "clocks": clk,
     }
+    if sweep:
+        out["sweep_nodes_per_s_vs_batch"] = sweep
     if batch1:
         out["batch1"] = batch1
         out["speedup_vs_batch1"] = (value / world) / batch1["nodes_per_s"]
