@@ -35,6 +35,7 @@ fold_status check_sched(const fold_schedule_t *s) {
 struct BwdWs {
   float *dA, *dCe, *partial, *dU_split;
   int32_t *root_off;
+  EmbedBwdWs emb;
   void *dZ;
   TcWeights w;
   int ld_z, nsplit;
@@ -55,6 +56,11 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
   size_t o_dZ = take((size_t)(nc + 1) * b.ld_z * (bf16 ? 2 : 4));
   size_t o_part = take((size_t)b.nsplit * gates * S * 4);
   size_t o_roff = take((size_t)(s->n_nodes + 2) * 4);
+  const int64_t nseg = s->n_tok_segs;
+  const int64_t max_pieces = s->n_leaves / kEmbedPiece + nseg + 1;
+  size_t o_pc = take((size_t)(nseg + 2) * 4), o_po = take((size_t)(nseg + 2) * 4);
+  size_t o_ss = take((size_t)scan_sums_count(nseg + 1) * 4);
+  size_t o_ep = take((size_t)max_pieces * S * 4);
   size_t o_w = take(bf16 ? tc_workspace_bytes(gates, (int)S) : 0);
   const int splits = bf16 ? tc_dU_splits((int)nc, gates, (int)S) : 1;
   size_t o_spl = take(splits > 1 ? (size_t)splits * gates * S * 2 * S * 4 : 0);
@@ -66,6 +72,10 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
     b.dZ = p + o_dZ;
     b.partial = (float *)(p + o_part);
     b.root_off = (int32_t *)(p + o_roff);
+    b.emb.piece_cnt = (int32_t *)(p + o_pc);
+    b.emb.piece_off = (int32_t *)(p + o_po);
+    b.emb.scan_sums = (int32_t *)(p + o_ss);
+    b.emb.partial = (float *)(p + o_ep);
     b.dU_split = splits > 1 ? (float *)(p + o_spl) : nullptr;
     if (bf16) {
       b.w.ld_u = (int)(2 * round_up(S, 64));
@@ -281,8 +291,8 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
   }
   {
     ProfScope ps(K_EMBED_BWD, s2);
-    FOLD_TRY(launch_embed_bwd(S, nl, s->n_tok_segs, s->tok_seg, s->leaf_perm, s->leaf_token, s->cons_off,
-                              s->cons_edge, b.root_off, s->root_perm, G, dh_root, b.dA, grads->dE, s2));
+    FOLD_TRY(launch_embed_bwd_pieces(S, nl, s->n_tok_segs, s->tok_seg, s->leaf_perm, s->leaf_token, s->cons_off,
+                                     s->cons_edge, b.root_off, s->root_perm, dh_root, b.dA, grads->dE, b.emb, s2));
   }
   {
     ProfScope ps(K_COLSUM, s2);

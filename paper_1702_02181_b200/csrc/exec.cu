@@ -240,7 +240,12 @@ __global__ void k_cell_bwd_pw(int r0, int r1, int nl, int S, int ld, int ld_g, c
   int lane = threadIdx.x & 31;
   int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = r0 + w; r < r1; r += nw) {
+  // warp task = (row, block of 32*VEC columns): narrow levels still spread over all SMs
+  const int nblk = (int)cdiv(S, 32 * VEC);
+  const int64_t ntask = (int64_t)(r1 - r0) * nblk;
+  for (int64_t task = w; task < ntask; task += nw) {
+    const int64_t r = r0 + task / nblk;
+    const int j = (int)(task % nblk) * 32 * VEC + lane * VEC;
     int64_t c = r - nl;
     int e0 = cons_off[r], e1 = cons_off[r + 1];
     // roots seeded at this row: root_perm[root_off[r] .. root_off[r+1]) (ascending g)
@@ -248,7 +253,7 @@ __global__ void k_cell_bwd_pw(int r0, int r1, int nl, int S, int ld, int ld_g, c
     const T *ga = Gact + c * ld_g;
     T *dz = dZ + c * ld_z;
     int64_t gL = gather[2 * r], gR = gather[2 * r + 1];
-    for (int j = lane * VEC; j < S; j += 32 * VEC) {
+    if (j < S) {
       float dh[VEC], dc[VEC], t[VEC];
 #pragma unroll
       for (int u = 0; u < VEC; u++) { dh[u] = 0.f; dc[u] = 0.f; }
@@ -508,6 +513,91 @@ __global__ void __launch_bounds__(128) k_embed_bwd(int S, int n_tok_segs, const 
   }
 }
 
+// ---- pieces: segment s has ceil(len/P) pieces; piece k covers sorted leaves
+// [a_s + kP, min(b_s, a_s + (k+1)P)). Single-piece segments add straight into dE; the
+// pieces of longer segments write partials that k_embed_pieces_final sums in order.
+__global__ void k_embed_piece_cnt(int n_tok_segs, const int32_t *__restrict__ tok_seg, int32_t *__restrict__ cnt) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n_tok_segs; s += stride)
+    cnt[s] = (int)cdiv(tok_seg[s + 1] - tok_seg[s], kEmbedPiece);
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(128) k_embed_pieces(int S, int n_tok_segs, int n_pieces,
+                                                      const int32_t *__restrict__ tok_seg,
+                                                      const int32_t *__restrict__ piece_off,
+                                                      const int32_t *__restrict__ leaf_perm,
+                                                      const int32_t *__restrict__ leaf_token,
+                                                      const int32_t *__restrict__ cons_off,
+                                                      const int32_t *__restrict__ cons_edge,
+                                                      const int32_t *__restrict__ root_off,
+                                                      const int32_t *__restrict__ root_perm,
+                                                      const float *__restrict__ dh_root, const float *__restrict__ dA,
+                                                      float *__restrict__ dE, float *__restrict__ partial) {
+  using IF = VecIO<float, VEC>;
+  const int total = piece_off[n_tok_segs];  // n_pieces is only a host-side upper bound
+  for (int64_t p = blockIdx.x; p < n_pieces && p < total; p += gridDim.x) {
+    int lo = 0, hi = n_tok_segs;  // segment s with piece_off[s] <= p < piece_off[s+1]
+    while (lo < hi) { int mid = (lo + hi + 1) >> 1; if (piece_off[mid] <= p) lo = mid; else hi = mid - 1; }
+    const int s = lo;
+    const int k = (int)(p - piece_off[s]);
+    const int np = piece_off[s + 1] - piece_off[s];
+    const int a = tok_seg[s] + k * kEmbedPiece, b = min(tok_seg[s + 1], a + kEmbedPiece);
+    const int tok = leaf_token[leaf_perm[tok_seg[s]]];
+    float *dst = np == 1 ? dE + (int64_t)tok * S : partial + p * (int64_t)S;
+    for (int j = threadIdx.x * VEC; j < S; j += blockDim.x * VEC) {
+      float acc[VEC], t[VEC];
+      if (np == 1) IF::ld(dst + j, acc);
+      else {
+#pragma unroll
+        for (int u = 0; u < VEC; u++) acc[u] = 0.f;
+      }
+      for (int q = a; q < b; q++) {
+        const int r = leaf_perm[q];
+        const int k1 = root_off[r + 1];
+        for (int kk = root_off[r]; kk < k1; kk++) {
+          IF::ld(dh_root + (int64_t)root_perm[kk] * S + j, t);
+#pragma unroll
+          for (int u = 0; u < VEC; u++) acc[u] += t[u];
+        }
+        const int e1 = cons_off[r + 1];
+        for (int e = cons_off[r]; e < e1; e++) {
+          IF::ld(dA + (int64_t)cons_edge[e] * S + j, t);
+#pragma unroll
+          for (int u = 0; u < VEC; u++) acc[u] += t[u];
+        }
+      }
+      IF::st(dst + j, acc);
+    }
+  }
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(128) k_embed_pieces_final(int S, int n_tok_segs, const int32_t *__restrict__ tok_seg,
+                                                            const int32_t *__restrict__ piece_off,
+                                                            const int32_t *__restrict__ leaf_perm,
+                                                            const int32_t *__restrict__ leaf_token,
+                                                            const float *__restrict__ partial,
+                                                            float *__restrict__ dE) {
+  using IF = VecIO<float, VEC>;
+  for (int64_t s = blockIdx.x; s < n_tok_segs; s += gridDim.x) {
+    const int p0 = piece_off[s], p1 = piece_off[s + 1];
+    if (p1 - p0 <= 1) continue;
+    const int tok = leaf_token[leaf_perm[tok_seg[s]]];
+    float *de = dE + (int64_t)tok * S;
+    for (int j = threadIdx.x * VEC; j < S; j += blockDim.x * VEC) {
+      float acc[VEC], t[VEC];
+      IF::ld(de + j, acc);
+      for (int p = p0; p < p1; p++) {
+        IF::ld(partial + (int64_t)p * S + j, t);
+#pragma unroll
+        for (int u = 0; u < VEC; u++) acc[u] += t[u];
+      }
+      IF::st(de + j, acc);
+    }
+  }
+}
+
 __global__ void k_sgd(float *p, const float *g, int64_t n, float lr) {
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) p[i] -= lr * g[i];
@@ -564,7 +654,8 @@ fold_status launch_cell_bwd_pw(bool bf16, int cell, int r0, int r1, int nl, int 
                                const int32_t *gather, const void *Gact, const float *C, const float *dA, float *dCe,
                                void *dZ, int ld_z, cudaStream_t st) {
   if (r1 <= r0) return FOLD_OK;
-  unsigned g = grid_cap(cdiv((int64_t)(r1 - r0) * 32, 256));
+  const int vec = (S & 3) == 0 ? 4 : 1;
+  unsigned g = grid_cap(cdiv((int64_t)(r1 - r0) * cdiv(S, 32 * vec) * 32, 256));
 #define PW_ARGS r0, r1, nl, S, ld, ld_g, cons_off, cons_edge, root_off, root_perm, G, dh_root, dc_root, gather
 #define PW_LAUNCH(T, GT, VEC) \
   k_cell_bwd_pw<T, GT, VEC><<<g, 256, 0, st>>>(PW_ARGS, (const T *)Gact, C, dA, dCe, (T *)dZ, ld_z)
@@ -639,6 +730,37 @@ fold_status launch_embed_bwd(int S, int nl, int n_tok_segs, const int32_t *tok_s
   else
     k_embed_bwd<1><<<g, 128, 0, st>>>(S, n_tok_segs, tok_seg, leaf_perm, leaf_token, cons_off, cons_edge, root_off,
                                       root_perm, G, dh_root, dA, dE);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+fold_status launch_embed_bwd_pieces(int S, int n_leaves, int n_tok_segs, const int32_t *tok_seg,
+                                    const int32_t *leaf_perm, const int32_t *leaf_token, const int32_t *cons_off,
+                                    const int32_t *cons_edge, const int32_t *root_off, const int32_t *root_perm,
+                                    const float *dh_root, const float *dA, float *dE, const EmbedBwdWs &w,
+                                    cudaStream_t st) {
+  (void)n_leaves;
+  if (n_tok_segs <= 0) return FOLD_OK;
+  k_embed_piece_cnt<<<grid_cap(cdiv(n_tok_segs, 256)), 256, 0, st>>>(n_tok_segs, tok_seg, w.piece_cnt);
+  FOLD_LAUNCH_CHECK();
+  // piece_off[0..n_tok_segs] (the total lands in piece_off[n_tok_segs] via a zero tail)
+  FOLD_CUDA_TRY(cudaMemsetAsync(w.piece_cnt + n_tok_segs, 0, sizeof(int32_t), st));
+  FOLD_TRY(scan_exclusive(w.piece_cnt, w.piece_off, (int64_t)n_tok_segs + 1, w.scan_sums, nullptr, st));
+  // upper bound on pieces (host-side, no sync): sum ceil(len/P) <= n_leaves/P + n_tok_segs
+  const int max_pieces = n_leaves / kEmbedPiece + n_tok_segs;
+  const unsigned g = grid_cap(max_pieces);
+  const bool v4 = (S & 3) == 0;
+#define EP_ARGS S, n_tok_segs, max_pieces, tok_seg, w.piece_off, leaf_perm, leaf_token, cons_off, cons_edge, \
+                root_off, root_perm, dh_root, dA, dE, w.partial
+  if (v4) k_embed_pieces<4><<<g, 128, 0, st>>>(EP_ARGS);
+  else k_embed_pieces<1><<<g, 128, 0, st>>>(EP_ARGS);
+#undef EP_ARGS
+  FOLD_LAUNCH_CHECK();
+  const unsigned g2 = grid_cap(n_tok_segs);
+  if (v4) k_embed_pieces_final<4><<<g2, 128, 0, st>>>(S, n_tok_segs, tok_seg, w.piece_off, leaf_perm, leaf_token,
+                                                     w.partial, dE);
+  else k_embed_pieces_final<1><<<g2, 128, 0, st>>>(S, n_tok_segs, tok_seg, w.piece_off, leaf_perm, leaf_token,
+                                                  w.partial, dE);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }

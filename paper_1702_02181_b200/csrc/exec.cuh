@@ -56,6 +56,21 @@ fold_status launch_embed_bwd(int S, int nl, int n_tok_segs, const int32_t *tok_s
 fold_status launch_root_off(int N, int G, const int32_t *root_row, const int32_t *root_perm, int32_t *root_off,
                             cudaStream_t st);
 fold_status launch_sgd(float *p, const float *g, int64_t n, float lr, cudaStream_t st);
+// exclusive int32 scan (sched.cu)
+fold_status scan_exclusive(const int32_t *in, int32_t *out, int64_t n, int32_t *sums, int32_t *total,
+                           cudaStream_t st);
+int64_t scan_sums_count(int64_t n);
+// embedding gradient, segmented by token, long segments split into fixed pieces
+constexpr int kEmbedPiece = 64;
+struct EmbedBwdWs {
+  int32_t *piece_cnt, *piece_off, *scan_sums;
+  float *partial;
+};
+fold_status launch_embed_bwd_pieces(int S, int n_leaves, int n_tok_segs, const int32_t *tok_seg,
+                                    const int32_t *leaf_perm, const int32_t *leaf_token, const int32_t *cons_off,
+                                    const int32_t *cons_edge, const int32_t *root_off, const int32_t *root_perm,
+                                    const float *dh_root, const float *dA, float *dE, const EmbedBwdWs &w,
+                                    cudaStream_t st);
 fold_status launch_zero(void *p, size_t bytes, cudaStream_t st);
 
 // --- tcgen05 path (exec_tc.cu)

@@ -539,6 +539,14 @@ inline unsigned grid_for(int64_t n, int threads = 256) {
 
 thread_local int32_t g_last_detail = -1;
 
+// device-wide exclusive int32 scan for other translation units; `sums` needs
+// scan_sums_count(n) entries
+fold_status scan_exclusive(const int32_t *in, int32_t *out, int64_t n, int32_t *sums, int32_t *total,
+                           cudaStream_t st) {
+  return excl_scan(in, out, n, sums, total, st);
+}
+int64_t scan_sums_count(int64_t n) { return cdiv(n < 1 ? 1 : n, kScanTile) + 2; }
+
 size_t schedule_workspace(int64_t N, int64_t G) { return sched_ws_layout(nullptr, N, G).bytes; }
 
 fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr, size_t ws_bytes,
