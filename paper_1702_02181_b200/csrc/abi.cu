@@ -37,7 +37,7 @@ struct BwdWs {
   int32_t *root_off;
   EmbedBwdWs emb;
   void *dZ;
-  TcWeights w;
+  __nv_bfloat16 *Ub;
   int ld_z, nsplit;
   size_t bytes;
 };
@@ -61,7 +61,7 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
   size_t o_pc = take((size_t)(nseg + 2) * 4), o_po = take((size_t)(nseg + 2) * 4);
   size_t o_ss = take((size_t)scan_sums_count(nseg + 1) * 4);
   size_t o_ep = take((size_t)max_pieces * S * 4);
-  size_t o_w = take(bf16 ? tc_workspace_bytes(gates, (int)S) : 0);
+  size_t o_w = take(bf16 ? tc_weights_bytes(gates, (int)S) : 0);
   const int splits = bf16 ? tc_dU_splits((int)nc, gates, (int)S) : 1;
   size_t o_spl = take(splits > 1 ? (size_t)splits * gates * S * 2 * S * 4 : 0);
   b.bytes = off;
@@ -77,12 +77,7 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
     b.emb.scan_sums = (int32_t *)(p + o_ss);
     b.emb.partial = (float *)(p + o_ep);
     b.dU_split = splits > 1 ? (float *)(p + o_spl) : nullptr;
-    if (bf16) {
-      b.w.ld_u = (int)(2 * round_up(S, 64));
-      b.w.ld_ut = (int)round_up((int64_t)gates * S, 8);
-      b.w.U = (__nv_bfloat16 *)(p + o_w);
-      b.w.Ut = (__nv_bfloat16 *)(p + o_w + tc_ut_offset(gates, (int)S));
-    }
+    b.Ub = bf16 ? (__nv_bfloat16 *)(p + o_w) : nullptr;
   }
   return b;
 }
@@ -113,9 +108,10 @@ AuxStream &aux_stream() {
   return a;
 }
 
-size_t fwd_ws_bytes(const fold_model *m) {
+// forward workspace (BF16 path): bf16 U, then the per-level completion counters
+size_t fwd_ws_bytes(const fold_schedule_t *s, const fold_model *m) {
   if (m->prec != FOLD_PREC_BF16) return 256;
-  return tc_workspace_bytes(gates_of(m->cell), m->S);
+  return tc_weights_bytes(gates_of(m->cell), m->S) + a256((size_t)(s->n_levels + 2) * sizeof(int));
 }
 
 }  // namespace
@@ -166,7 +162,7 @@ fold_status fold_acts_layout(const fold_schedule_t *s, const fold_model *m, fold
 
 size_t fold_forward_workspace(const fold_schedule_t *s, const fold_model *m) {
   if (check_sched(s) != FOLD_OK || check_model(m) != FOLD_OK) return 0;
-  return fwd_ws_bytes(m);
+  return fwd_ws_bytes(s, m);
 }
 
 // Forward level loop: depth 1 = embedding lookup, depth d >= 2 = one
@@ -176,7 +172,7 @@ fold_status fold_forward(const fold_schedule_t *s, const fold_model *m, void *ac
   FOLD_TRY(check_sched(s));
   FOLD_TRY(check_model(m));
   if (!acts && s->n_nodes > 0) return FOLD_E_INVALID;
-  if (ws_bytes < fwd_ws_bytes(m) || (!ws && m->prec == FOLD_PREC_BF16)) return FOLD_E_WORKSPACE;
+  if (ws_bytes < fwd_ws_bytes(s, m) || (!ws && m->prec == FOLD_PREC_BF16)) return FOLD_E_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   const int N = s->n_nodes, S = m->S, D = s->n_levels, nl = s->n_leaves, G = s->n_graphs;
   if (N == 0) return FOLD_OK;
@@ -195,19 +191,20 @@ fold_status fold_forward(const fold_schedule_t *s, const fold_model *m, void *ac
     FOLD_TRY(launch_embed_fwd(bf16, lo[1], lo[2], s->leaf_token, m->E, S, L.ld, H, C, bf16 ? &sc : nullptr, st));
   }
   if (bf16) {
-    TcWeights w{};
-    w.ld_u = (int)(2 * round_up(S, 64));
-    w.ld_ut = (int)round_up((int64_t)gates * S, 8);
-    w.U = (__nv_bfloat16 *)ws;
-    w.Ut = nullptr;
+    __nv_bfloat16 *Ub = (__nv_bfloat16 *)ws;
     if (D >= 2) {
-      ProfScope ps(K_PREP, st);
-      FOLD_TRY(tc_prepare_U(gates, S, m->U, w, false, st));
-    }
-    for (int d = 2; d <= D; d++) {
+      {
+        ProfScope ps(K_PREP, st);
+        FOLD_TRY(tc_prepare_Uil(gates, S, m->U, Ub, st));
+      }
+      TcFwdArgs fa{};
+      fa.level_off = s->level_off; fa.level_off_host = lo;
+      fa.D = D; fa.S = S; fa.nl = nl; fa.n_cells = s->n_cells; fa.ld = L.ld; fa.ld_g = L.ld_g; fa.ld_u = tc_ld_u(S);
+      fa.gather = s->gather; fa.Ub = Ub; fa.b = m->b;
+      fa.H = (__nv_bfloat16 *)H; fa.Gact = (__nv_bfloat16 *)Gact; fa.C = C; fa.sc = sc;
+      fa.done = (int *)((char *)ws + tc_weights_bytes(gates, S));
       ProfScope ps(K_CELL_FWD, st);
-      FOLD_TRY(tc_cell_fwd(m->cell, lo[d], lo[d + 1], nl, s->n_cells, s->gather, S, L.ld, w, m->b,
-                           (__nv_bfloat16 *)H, C, (__nv_bfloat16 *)Gact, L.ld_g, sc, st));
+      FOLD_TRY(tc_fwd_levels(m->cell, fa, st));
     }
   } else {
     for (int d = 2; d <= D; d++) {
@@ -263,7 +260,7 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
   const int32_t *lo = s->level_off_host;
   if (bf16) {
     ProfScope ps(K_PREP, st);
-    FOLD_TRY(tc_prepare_U(gates, S, m->U, b.w, true, st));
+    FOLD_TRY(tc_prepare_U(gates, S, m->U, b.Ub, st));
   }
   for (int d = D; d >= 2; d--) {
     const int r0 = lo[d], r1 = lo[d + 1], M = r1 - r0, c0 = r0 - nl;
@@ -276,7 +273,7 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
     ProfScope ps(K_GEMM_DA, st);
     float *dA_lvl = b.dA + (size_t)2 * c0 * S;
     if (bf16)
-      FOLD_TRY(tc_gemm_dA(c0, M, nc, S, gates, (const __nv_bfloat16 *)b.dZ, b.ld_z, b.w, b.dA, st));
+      FOLD_TRY(tc_gemm_dA(c0, M, nc, S, gates, (const __nv_bfloat16 *)b.dZ, b.ld_z, b.Ub, b.dA, st));
     else
       FOLD_TRY(launch_gemm_dA_simt(M, S, gates, (const float *)b.dZ + (size_t)c0 * b.ld_z, b.ld_z, m->U, dA_lvl, st));
   }

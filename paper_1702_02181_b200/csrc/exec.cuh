@@ -74,22 +74,33 @@ fold_status launch_embed_bwd_pieces(int S, int n_leaves, int n_tok_segs, const i
 fold_status launch_zero(void *p, size_t bytes, cudaStream_t st);
 
 // --- tcgen05 path (exec_tc.cu)
-struct TcWeights {  // bf16 copies made per call
-  __nv_bfloat16 *U;   // forward: gate-interleaved [cdiv(S,W)*gates*W][ld_u] (ld_u = 2*round_up(S, 64))
-  __nv_bfloat16 *Ut;  // [2S][ld_ut]      (ld_ut = round_up(gates*S, 8)) = U^T
-  int ld_u, ld_ut;
+// bf16 copies of U per call, [rows][ld_u] with K halves padded to Sp = round_up(S, 64)
+// (ld_u = 2 Sp): natural row order for the backward's dA GEMM (MN-major B operand),
+// gate-interleaved in 8-column blocks for the forward (K-major B operand, one TMA box).
+int tc_ld_u(int S);
+size_t tc_weights_bytes(int gates, int S);
+fold_status tc_prepare_U(int gates, int S, const float *U, __nv_bfloat16 *Ub, cudaStream_t st);
+// the forward's gate-interleaved copy (Uil8, same size)
+fold_status tc_prepare_Uil(int gates, int S, const float *U, __nv_bfloat16 *Uil, cudaStream_t st);
+// All cell levels d = 2..D of the forward in one persistent launch.
+struct TcFwdArgs {
+  const int32_t *level_off;       // device
+  const int32_t *level_off_host;  // host copy (tile count)
+  int D, S, nl, n_cells, ld, ld_g, ld_u;
+  const int32_t *gather;
+  const __nv_bfloat16 *Ub;
+  const float *b;
+  __nv_bfloat16 *H, *Gact;
+  float *C;
+  ScatterA sc;
+  int *done;                       // [D + 2] level completion counters (workspace)
 };
-fold_status tc_prepare_U(int gates, int S, const float *U, TcWeights &w, bool transpose, cudaStream_t st);
-fold_status tc_cell_fwd(int cell, int r0, int r1, int nl, int n_cells, const int32_t *gather, int S, int ld,
-                        const TcWeights &w, const float *b, __nv_bfloat16 *H, float *C, __nv_bfloat16 *Gact,
-                        int ld_g, const ScatterA &sc, cudaStream_t st);
+fold_status tc_fwd_levels(int cell, const TcFwdArgs &a, cudaStream_t st);
 fold_status tc_gemm_dA(int c0, int M, int n_cells, int S, int gates, const __nv_bfloat16 *dZ, int ld_z,
-                       const TcWeights &w, float *dA, cudaStream_t st);
+                       const __nv_bfloat16 *Ub, float *dA, cudaStream_t st);
 // split-K over cells into split_ws [splits][gates*S][2S] (fp32), then a fixed-order sum
 int tc_dU_splits(int n_cells, int gates, int S);
 fold_status tc_gemm_dU(int n_cells, int S, int gates, const __nv_bfloat16 *dZ, int ld_z, const ScatterA &sc,
                        float *dU, int accumulate, float *split_ws, cudaStream_t st);
-size_t tc_workspace_bytes(int gates, int S);
-size_t tc_ut_offset(int gates, int S);  // byte offset of Ut inside the tc workspace
 
 }  // namespace fold

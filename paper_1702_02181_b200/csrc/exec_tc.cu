@@ -1,24 +1,31 @@
 // exec_tc.cu — tcgen05 (5th-gen tensor core) kernels for the BF16 path.
 //
-//  k_cell_fwd_tc   one level of the forward (gather -> operation -> concat)
-//                  in one kernel. The gather is moved to production time: whoever
-//                  produces a pool row (embedding kernel, or this kernel's epilogue for
-//                  the previous level) also writes it into the A-operand row of each
-//                  consumer edge (planes A_L / A_R, row = consumer cell). So the level's
-//                  A rows are contiguous and TMA streams them as dense 128B-swizzled boxes;
-//                  tcgen05.mma multiplies them with a gate-interleaved slab of U into a
-//                  TMEM accumulator; the epilogue warps apply the gates, append (h, c) to
-//                  the level's pool rows (the concat becomes an append) and push h to its
-//                  consumers' A rows.
-//  k_gemm_dA_tc    backward edge gradients of one level: dA = dZ_level * U  (K-major).
+//  k_fwd_levels    every cell level of the forward (gather -> operation ->
+//                  concat, once per depth) in ONE persistent launch. The gather is moved
+//                  to production time: whoever produces a pool row (embedding kernel, or
+//                  this kernel's epilogue for an earlier level) also writes it into the
+//                  A-operand row of each consumer edge (planes A_L / A_R, row = consumer
+//                  cell). So a level's A rows are contiguous and TMA streams them as dense
+//                  128B-swizzled boxes; tcgen05.mma multiplies them with a gate-interleaved
+//                  slab of U into a TMEM accumulator; the epilogue warps apply the gates,
+//                  append (h, c) to the level's pool rows (the concat becomes an append)
+//                  and push h to its consumers' A rows. Depth order is kept by device-side
+//                  level counters instead of one launch per level.
+//  k_gemm_dA_tc    backward edge gradients of one level: dA = dZ_level * U.
 //  k_gemm_dU_tc    weight gradient over all cells at once: dU = dZ^T * [A_L | A_R], both
 //                  operands MN-major dense TMA boxes; split-K over cells with a
 //                  fixed-order reduction (deterministic).
-// Warp roles (256 threads): warp 0 TMA producer, warp 1 MMA issuer (one lane),
-// warp 2 TMEM allocator, warps 4-7 epilogue (warp w reads TMEM lanes 32(w%4)..+31).
+// All three run on CTA PAIRS (cluster of 2, tcgen05.mma.cta_group::2, M = 256): each CTA
+// stages its 128 A rows and half of the B tile, so the operand bytes each SM pulls from L2
+// per FLOP drop by a third against single-CTA 128-row tiles (measured: single-CTA tiles
+// were bound by L2->SM ingress at ~56 B/clk/SM, not by the tensor pipe).
+// Warp roles: warp 0 TMA producer (both CTAs), warp 1 MMA issuer (leader CTA, one lane),
+// warp 2 TMEM allocator, warp 3 idle, warps 4.. epilogue (warp w reads TMEM lanes
+// 32 (w % 4) .. +31 of its own CTA).
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <unordered_map>
 
 #include "exec.cuh"
 #include "ptx.cuh"
@@ -27,9 +34,10 @@ namespace fold {
 
 namespace {
 
-constexpr int BM = 128;     // rows per tile (UMMA M)
+constexpr int BM = 128;     // rows per CTA (the pair's MMA has M = 256)
+constexpr int PM = 2 * BM;  // rows per CTA pair
 constexpr int BK = 64;      // K elements per stage (128 B of bf16 = one swizzle row)
-constexpr int ST = 4;       // pipeline stages
+constexpr int ST = 6;       // pipeline stages
 constexpr int kThreads = 256;
 
 __device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
@@ -43,54 +51,93 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   return *reinterpret_cast<uint32_t *>(&v);
 }
 
-// =================================================================== forward cell level
-template <int GATES, int W>
+// =================================================================== forward: all cell levels
+// One persistent launch runs every cell level d = 2..D (the while-loop over
+// depths, each iteration gather -> cell -> concat). Tiles are enumerated level by level
+// (level d's tiles before level d+1's) and dealt round-robin to the CTAs; a tile of level
+// d waits on a device counter until all tiles of level d-1 are published, so the depth
+// ordering of the paper's loop is kept with no host round trip and no launch per level.
+// Narrow levels use narrower state-column tiles (W_narrow) so they still spread over the
+// SMs (the U slab each CTA streams shrinks with W).
+struct FwdLevels {
+  const int32_t *lo;     // schedule level_off (device)
+  int D, S, Ww, Wn;      // deepest level, state size, wide / narrow tile widths
+  int narrow_below;      // a level whose wide tiling has fewer tiles than this uses Wn
+};
+
+__host__ __device__ inline int fwd_level_W(const FwdLevels &L, int M) {
+  int mt = (int)cdiv(M, PM);
+  return (int64_t)mt * cdiv(L.S, L.Ww) < L.narrow_below ? L.Wn : L.Ww;
+}
+
+// Walks the level table in tile order (each warp role keeps its own copy).
+struct LevelCursor {
+  int d, t0, nt, prev_nt, r0, r1, W, NT;
+  __device__ void load(const FwdLevels &L) {
+    r0 = __ldg(L.lo + d); r1 = __ldg(L.lo + d + 1);
+    W = fwd_level_W(L, r1 - r0);
+    NT = (int)cdiv(L.S, W);
+    nt = (int)cdiv(r1 - r0, PM) * NT;  // pair tiles
+  }
+  __device__ void init(const FwdLevels &L) { d = 2; t0 = 0; prev_nt = 0; load(L); }
+  __device__ void seek(const FwdLevels &L, int T) {
+    while (T >= t0 + nt) { t0 += nt; prev_nt = nt; d++; load(L); }
+  }
+};
+
+template <int GATES>
 struct FwdCfg {
-  static constexpr int N = GATES * W;
+  static constexpr int WMAX = GATES == 5 ? 48 : 128;   // wide tile: N = GATES * W <= 256
+  static constexpr int WNAR = GATES == 5 ? 16 : 32;    // narrow tile (N/2 a multiple of 8 rows)
   static constexpr int A_BYTES = BM * 128;
-  static constexpr int B_BYTES = N * 128;
+  static constexpr int B_BYTES = GATES * WMAX * 64;    // this CTA's half of the B rows
   static constexpr int STAGE = A_BYTES + B_BYTES;
+  static_assert(STAGE % 1024 == 0, "stages stay 1024 B aligned (128B swizzle atoms)");
   static constexpr int ACC_STRIDE = 256;  // TMEM columns per accumulator buffer (2 buffers)
   static constexpr int TMEM_COLS = 512;
   static constexpr int SMEM = ST * STAGE + 1024;
   static constexpr int EPI_WARPS = 8;     // 2 per SM sub-partition: each owns half the columns
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
-  static constexpr int CHUNKS = W / 8;
-  static_assert(N % 16 == 0 && N <= 256, "UMMA N for M=128");
-  static_assert(W % 8 == 0, "gate slab rows must fill 8-row swizzle atoms");
+  static_assert(GATES * WMAX <= 256 && (GATES * WNAR) % 16 == 0 && (GATES * WNAR / 2) % 8 == 0, "UMMA N, M=256");
   static_assert(SMEM <= 227 * 1024, "smem");
 };
 
-// Persistent: grid = min(#tiles, #SMs); tile t -> (state-column tile t % NT, row tile t / NT)
-// (N fast: the CTAs running concurrently share a few A tiles in L2; U is L2-resident).
-// Two TMEM accumulators: the epilogue of tile i overlaps the MMA main loop of tile i+1.
 // Warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4..11 epilogue
 // (warp w reads TMEM lanes 32 (w % 4) .. +31, column chunks (w - 4) / 4, +2, +4, ...).
-template <int GATES, int W>
-__global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
-    k_cell_fwd_tc(const __grid_constant__ CUtensorMap tmAL, const __grid_constant__ CUtensorMap tmAR,
-                  const __grid_constant__ CUtensorMap tmU, int r0, int r1, int nl, int S, int Sp, int ld, int KBh,
-                  int NT, int ntiles, const int32_t *__restrict__ gather, const float *__restrict__ bias,
-                  __nv_bfloat16 *__restrict__ H, float *__restrict__ C, __nv_bfloat16 *__restrict__ Gact, int ld_g,
-                  ScatterA sc, int dbg_epi, int bias_in_smem) {
-  using Cfg = FwdCfg<GATES, W>;
+// B operand per stage: one box of GATES*W rows of the gate-interleaved bf16 U (Uil8: row
+// (j/8)*8*GATES + g*8 + j%8 holds U row g*S + j; K halves padded to Sp = round_up(S, 64) so
+// every box starts 128 B aligned): tile column jc*8*GATES + g*8 + u is gate g of state
+// column j0 + 8*jc + u, for any tile width W that is a multiple of 8.
+template <int GATES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREADS, 1)
+    k_fwd_levels(const __grid_constant__ CUtensorMap tmAL, const __grid_constant__ CUtensorMap tmAR,
+                 const __grid_constant__ CUtensorMap tmUw, const __grid_constant__ CUtensorMap tmUn, FwdLevels L,
+                 int total_tiles, int nl, int ld, const int32_t *__restrict__ gather, const float *__restrict__ bias,
+                 __nv_bfloat16 *__restrict__ H, float *C, __nv_bfloat16 *__restrict__ Gact, int ld_g, ScatterA sc,
+                 int *done, int bias_in_smem) {
+  using Cfg = FwdCfg<GATES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
   __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
+  const int S = L.S;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < ST; s++) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; a++) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], Cfg::EPI_WARPS); }
+    // tempty (leader's copy used): drained by the epilogue warps of both CTAs
+    for (int a = 0; a < 2; a++) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 2 * Cfg::EPI_WARPS); }
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tmAL);
     ptx::prefetch_tmap(&tmAR);
-    ptx::prefetch_tmap(&tmU);
+    ptx::prefetch_tmap(&tmUw);
+    ptx::prefetch_tmap(&tmUn);
   }
   if (warp == 2) {
-    ptx::tmem_alloc(&tmem_base_sh, Cfg::TMEM_COLS);
-    ptx::tmem_relinquish();
+    ptx::tmem_alloc2(&tmem_base_sh, Cfg::TMEM_COLS);
+    ptx::tmem_relinquish2();
   }
   // the whole bias (GATES*S fp32) stays in shared memory when it fits next to the ring
   float *sbias = reinterpret_cast<float *>(smem + ST * Cfg::STAGE);
@@ -98,38 +145,54 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
     for (int i = tid; i < GATES * S; i += blockDim.x) sbias[i] = bias[i];
   const float *bsrc = bias_in_smem ? sbias : bias;
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();  // barrier inits and the pair's TMEM allocation visible to both CTAs
   ptx::tc_fence_after();
   const uint32_t tbase = tmem_base_sh;
-  const int KB = 2 * KBh;
+  const int KBh = (int)cdiv(S, BK), KB = 2 * KBh, Sp = KBh * BK;
+  const int pub_per_cta = 2;  // both CTAs of a pair publish
 
   if (warp == 0) {
     // TMA producer: per stage one dense box of 128 A rows (the level's contiguous cell rows
-    // of the left / right operand plane) + one box of the gate-interleaved U slab.
+    // of the left / right operand plane) + GATES boxes of W rows of U.
     if (lane == 0) {
-      int it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int c0 = (r0 - nl) + (t / NT) * BM;
+      LevelCursor cur;
+      cur.init(L);
+      int it = 0, ready_d = 2;
+      for (int T = pair; T < total_tiles; T += npairs) {
+        cur.seek(L, T);
+        if (cur.d > ready_d) {
+          // all of level d-1 (hence every level < d) published: its h rows are in the planes
+          ptx::wait_counter(done + (cur.d - 1), pub_per_cta * min(cur.prev_nt, npairs));
+          ptx::fence_proxy_async_global();
+          ready_d = cur.d;
+        }
+        const int lt = T - cur.t0, W = cur.W;
+        const int c0 = (cur.r0 - nl) + (lt / cur.NT) * PM + (int)rank * BM, j0 = (lt % cur.NT) * W;
+        const CUtensorMap *tmU = W == Cfg::WMAX ? &tmUw : &tmUn;
+        // the leader's full barrier counts both CTAs' bytes: 2 x (A rows + half the B rows)
+        const uint32_t bytes = 2 * Cfg::A_BYTES + GATES * W * 128;
+        const int urow = GATES * j0 + (int)rank * (GATES * W / 2);
         for (int kb = 0; kb < KB; kb++, it++) {
           int s = it % ST;
           uint32_t ph = (it / ST) & 1;
           ptx::mbar_wait(&empty[s], ph ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[s], Cfg::STAGE);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], bytes);
           int half = kb >= KBh;
           int kc = (kb - half * KBh) * BK;
           uint8_t *A = smem + s * Cfg::STAGE;
-          ptx::tma_load_2d(half ? &tmAR : &tmAL, &full[s], A, kc, c0);
-          // U is stored gate-interleaved per state-column tile (tc_prepare_U): one box of
-          // GATES*W rows holds (i, fL, fR, o, u) for the tile's W state columns
-          ptx::tma_load_2d(&tmU, &full[s], A + Cfg::A_BYTES, half * Sp + kc, (t % NT) * Cfg::N);
+          ptx::tma_load_2d_pair(half ? &tmAR : &tmAL, &full[s], A, kc, c0);
+          ptx::tma_load_2d_pair(tmU, &full[s], A + Cfg::A_BYTES, half * Sp + kc, urow);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16(BM, Cfg::N, 0, 0);
+    if (lane == 0 && rank == 0) {
+      LevelCursor cur;
+      cur.init(L);
       int it = 0, tc = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, tc++) {
+      for (int T = pair; T < total_tiles; T += npairs, tc++) {
+        cur.seek(L, T);
+        const uint32_t idesc = ptx::idesc_bf16(PM, GATES * cur.W, 0, 0);
         const int acc = tc & 1;
         const uint32_t aph = (tc >> 1) & 1;
         ptx::mbar_wait(&tempty[acc], aph ^ 1);
@@ -143,11 +206,11 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
           uint32_t a0 = ptx::smem_u32(smem + s * Cfg::STAGE), b0 = a0 + Cfg::A_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 16; k++)
-            ptx::umma_bf16(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024), ptx::sdesc_sw128(b0 + 32 * k, 16, 1024),
-                           idesc, (kb | k) != 0);
-          ptx::umma_commit(&empty[s]);
+            ptx::umma_bf16_2cta(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024),
+                                ptx::sdesc_sw128(b0 + 32 * k, 16, 1024), idesc, (kb | k) != 0);
+          ptx::umma_commit_2cta(&empty[s]);
         }
-        ptx::umma_commit(&tfull[acc]);
+        ptx::umma_commit_2cta(&tfull[acc]);
       }
     }
   } else if (warp >= 4) {
@@ -159,28 +222,40 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
     // per-row metadata (child rows, consumer edges) of the next tile is fetched while the
     // current tile's epilogue runs
     struct Meta { int gl, gr, ce0, ce1, e0; };
-    auto fetch_meta = [&](int t, Meta &m) {
-      const int64_t rr = r0 + (int64_t)(t / NT) * BM + row;
+    auto fetch_meta = [&](const LevelCursor &cu, int T, Meta &m) {
       m.gl = m.gr = m.ce0 = m.ce1 = 0; m.e0 = 0;
-      if (t < ntiles && rr < r1) {
-        m.gl = gather[2 * rr]; m.gr = gather[2 * rr + 1];
-        m.ce0 = sc.cons_off[rr]; m.ce1 = sc.cons_off[rr + 1];
-        if (m.ce1 > m.ce0) m.e0 = sc.cons_edge[m.ce0];
+      if (T >= total_tiles) return;
+      const int64_t rr = cu.r0 + (int64_t)((T - cu.t0) / cu.NT) * PM + rank * BM + row;
+      if (rr < cu.r1) {
+        m.gl = __ldg(gather + 2 * rr); m.gr = __ldg(gather + 2 * rr + 1);
+        m.ce0 = __ldg(sc.cons_off + rr); m.ce1 = __ldg(sc.cons_off + rr + 1);
+        if (m.ce1 > m.ce0) m.e0 = __ldg(sc.cons_edge + m.ce0);
       }
     };
+    LevelCursor cur, nxc;
+    cur.init(L);
+    nxc.init(L);
     Meta nxt;
-    fetch_meta(blockIdx.x, nxt);
-    int tc = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, tc++) {
+    nxc.seek(L, pair);
+    fetch_meta(nxc, pair, nxt);
+    int tc = 0, ready_d = 2;
+    for (int T = pair; T < total_tiles; T += npairs, tc++) {
+      cur.seek(L, T);
+      if (cur.d > ready_d) {  // order this thread's C reads after level d-1's publication
+        ptx::wait_counter(done + (cur.d - 1), pub_per_cta * min(cur.prev_nt, npairs));
+        ready_d = cur.d;
+      }
       const int acc = tc & 1;
       const uint32_t aph = (tc >> 1) & 1;
-      const int j0 = (t % NT) * W;
-      const int64_t r = r0 + (int64_t)(t / NT) * BM + row;
-      const bool valid = r < r1 && dbg_epi != 1;
-      const Meta cur = nxt;
-      fetch_meta(t + gridDim.x, nxt);
-      const int64_t gl = cur.gl, gr = cur.gr;
-      const int ce0 = cur.ce0, ce1 = cur.ce1;
+      const int lt = T - cur.t0, W = cur.W, chunks = W / 8;
+      const int j0 = (lt % cur.NT) * W;
+      const int64_t r = cur.r0 + (int64_t)(lt / cur.NT) * PM + rank * BM + row;
+      const bool valid = r < cur.r1;
+      const Meta m = nxt;
+      if (T + npairs < total_tiles) nxc.seek(L, T + npairs);
+      fetch_meta(nxc, T + npairs, nxt);
+      const int64_t gl = m.gl, gr = m.gr;
+      const int ce0 = m.ce0, ce1 = m.ce1;
       const int64_t c = r - nl;
       // prefetch the first chunk's child cell states before waiting for the accumulator
       float cl[8], cr[8];
@@ -192,20 +267,20 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
 #pragma unroll
           for (int u = 0; u < 8; u++) { cl[u] = 0.f; cr[u] = 0.f; }
           if (lok) {
-            float4 a = __ldg(reinterpret_cast<const float4 *>(C + gl * ld + jb));
-            float4 b = __ldg(reinterpret_cast<const float4 *>(C + gl * ld + jb + 4));
+            float4 a = __ldcg(reinterpret_cast<const float4 *>(C + gl * ld + jb));
+            float4 b = __ldcg(reinterpret_cast<const float4 *>(C + gl * ld + jb + 4));
             cl[0] = a.x; cl[1] = a.y; cl[2] = a.z; cl[3] = a.w; cl[4] = b.x; cl[5] = b.y; cl[6] = b.z; cl[7] = b.w;
           }
           if (rok) {
-            float4 a = __ldg(reinterpret_cast<const float4 *>(C + gr * ld + jb));
-            float4 b = __ldg(reinterpret_cast<const float4 *>(C + gr * ld + jb + 4));
+            float4 a = __ldcg(reinterpret_cast<const float4 *>(C + gr * ld + jb));
+            float4 b = __ldcg(reinterpret_cast<const float4 *>(C + gr * ld + jb + 4));
             cr[0] = a.x; cr[1] = a.y; cr[2] = a.z; cr[3] = a.w; cr[4] = b.x; cr[5] = b.y; cr[6] = b.z; cr[7] = b.w;
           }
         } else {
 #pragma unroll
           for (int u = 0; u < 8; u++) {
-            cl[u] = (lok && jb + u < S) ? C[gl * ld + jb + u] : 0.f;
-            cr[u] = (rok && jb + u < S) ? C[gr * ld + jb + u] : 0.f;
+            cl[u] = (lok && jb + u < S) ? __ldcg(C + gl * ld + jb + u) : 0.f;
+            cr[u] = (rok && jb + u < S) ? __ldcg(C + gr * ld + jb + u) : 0.f;
           }
         }
       };
@@ -214,16 +289,16 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
       ptx::tc_fence_after();
       const uint32_t tl = tbase + acc * Cfg::ACC_STRIDE + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-      for (int jc = grp; jc < Cfg::CHUNKS; jc += 2) {
+      for (int jc = grp; jc < chunks; jc += 2) {
         float z[GATES][8];
 #pragma unroll
-        for (int g = 0; g < GATES; g++) ptx::tmem_ld8(tl + g * W + jc * 8, z[g]);
+        for (int g = 0; g < GATES; g++) ptx::tmem_ld8(tl + jc * 8 * GATES + g * 8, z[g]);
         ptx::tmem_ld_wait();
         const int jb = j0 + jc * 8;
         float ccl[8], ccr[8];
 #pragma unroll
         for (int u = 0; u < 8; u++) { ccl[u] = cl[u]; ccr[u] = cr[u]; }
-        if (jc + 2 < Cfg::CHUNKS) load_c(jb + 16);  // next chunk of this warp, in flight during math
+        if (jc + 2 < chunks) load_c(jb + 16);  // next chunk of this warp, in flight during math
         if (!valid || jb >= S) continue;
         const bool fullc = (jb + 8 <= S) && ((S & 7) == 0);
         float hh[8];
@@ -264,19 +339,11 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
             hh[u] = gs[3][u] * tanh_fast(cc[u]);
           }
           __nv_bfloat16 *ga = Gact + c * ld_g;
-          if (dbg_epi == 2) {  // probe: no stores at all (keep the math alive)
-            float acc = 0.f;
-#pragma unroll
-            for (int u = 0; u < 8; u++) acc += cc[u] + hh[u] + gs[0][u] + gs[1][u] + gs[2][u] + gs[3][u] + gs[4][u];
-            if (acc == 12345.f) C[r * ld + jb] = acc;
-            continue;
-          }
           if (fullc) {
             *reinterpret_cast<float4 *>(C + r * ld + jb) = make_float4(cc[0], cc[1], cc[2], cc[3]);
             *reinterpret_cast<float4 *>(C + r * ld + jb + 4) = make_float4(cc[4], cc[5], cc[6], cc[7]);
 #pragma unroll
             for (int g = 0; g < 5; g++)
-              if (dbg_epi != 3)
               *reinterpret_cast<uint4 *>(ga + g * S + jb) =
                   make_uint4(pack_bf16x2(gs[g][0], gs[g][1]), pack_bf16x2(gs[g][2], gs[g][3]),
                              pack_bf16x2(gs[g][4], gs[g][5]), pack_bf16x2(gs[g][6], gs[g][7]));
@@ -296,7 +363,7 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
                                 pack_bf16x2(hh[6], hh[7]));
           if (ce1 == ce0) *reinterpret_cast<uint4 *>(H + r * ld + jb) = pk;
           for (int e = ce0; e < ce1; e++) {
-            int ed = e == ce0 ? cur.e0 : sc.cons_edge[e];
+            int ed = e == ce0 ? m.e0 : __ldg(sc.cons_edge + e);
             *reinterpret_cast<uint4 *>(((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld + jb) = pk;
           }
         } else {
@@ -304,75 +371,95 @@ __global__ void __launch_bounds__(FwdCfg<GATES, W>::THREADS, 1)
             __nv_bfloat16 hv = __float2bfloat16_rn(hh[u]);
             if (ce1 == ce0) H[r * ld + jb + u] = hv;
             for (int e = ce0; e < ce1; e++) {
-              int ed = sc.cons_edge[e];
+              int ed = __ldg(sc.cons_edge + e);
               (((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld)[jb + u] = hv;
             }
           }
         }
       }
-      // this accumulator buffer may be overwritten by the MMA of tile i+2
+      // this accumulator buffer may be overwritten by the MMA of tile i+2 (the leader's
+      // barrier collects both CTAs' epilogue warps)
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      if (lane == 0) ptx::mbar_arrive_leader(&tempty[acc]);
+      // last tile of this level for this CTA: publish (all epilogue warps' stores, then one
+      // release increment; level d is complete at 2 min(#pair tiles(d), #pairs) increments)
+      const int Tn = T + npairs;
+      if (Tn >= total_tiles || Tn >= cur.t0 + cur.nt) {
+        ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
+        if (warp == 4 && lane == 0) {
+          ptx::fence_proxy_async_global();
+          __threadfence();
+          ptx::red_release_gpu_add(done + cur.d, 1);
+        }
+      }
     }
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();  // neither CTA leaves while the pair's MMAs / arrivals may touch it
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tbase, Cfg::TMEM_COLS);
+    ptx::tmem_dealloc2(tbase, Cfg::TMEM_COLS);
   }
 }
 
 // =================================================================== dA = dZ * U (one level)
-// Persistent (grid = min(#tiles, #SMs)), tile t -> (N tile t % NTn, row tile t / NTn),
-// 128 x 256 tiles, two TMEM accumulators so the fp32 store epilogue of tile i overlaps the
-// main loop of tile i+1.
+// B operand = the bf16 U in its natural row order [gates*S][2*Sp] read MN-major (N = the
+// padded input columns contiguous, K = the gates*S rows): no transposed copy is needed.
+// CTA pairs, persistent (grid = 2 * min(#pair tiles, #pairs)); pair tile t -> (N tile
+// t % NTn, 256-row tile t / NTn); each CTA stages its 128 dZ rows and 128 of the 256 B
+// columns; two TMEM accumulators so the fp32 store epilogue of tile i overlaps the main
+// loop of tile i+1.
 constexpr int DA_N = 256;
-constexpr int DA_A_BYTES = BM * 128, DA_B_BYTES = DA_N * 128, DA_STAGE = DA_A_BYTES + DA_B_BYTES;
+constexpr int MN_CHUNK = 64 * 128;       // bytes per 64-element MN chunk of 64 K rows
+constexpr int DA_A_BYTES = BM * 128, DA_B_BYTES = (DA_N / 2) * 128, DA_STAGE = DA_A_BYTES + DA_B_BYTES;
 constexpr int DA_SMEM = ST * DA_STAGE + 1024;
 
-__global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_dA_tc(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmUt, int c0, int M,
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_gemm_dA_tc(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmU, int c0, int M,
                  int KB, int S, int NTn, int ntiles, float *__restrict__ dA) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
   __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < ST; s++) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; a++) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 4); }
+    for (int a = 0; a < 2; a++) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 2 * 4); }
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tmZ);
-    ptx::prefetch_tmap(&tmUt);
+    ptx::prefetch_tmap(&tmU);
   }
-  if (warp == 2) { ptx::tmem_alloc(&tmem_base_sh, 512); ptx::tmem_relinquish(); }
+  if (warp == 2) { ptx::tmem_alloc2(&tmem_base_sh, 512); ptx::tmem_relinquish2(); }
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tbase = tmem_base_sh;
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int mt = c0 + (t / NTn) * BM, n0 = (t % NTn) * DA_N;
+      for (int t = pair; t < ntiles; t += npairs) {
+        const int mt = c0 + (t / NTn) * PM + (int)rank * BM, nb = (t % NTn) * DA_N + (int)rank * (DA_N / 2);
         for (int kb = 0; kb < KB; kb++, it++) {
           int s = it % ST;
           uint32_t ph = (it / ST) & 1;
           ptx::mbar_wait(&empty[s], ph ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[s], DA_STAGE);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], 2 * DA_STAGE);
           uint8_t *A = smem + s * DA_STAGE;
-          ptx::tma_load_2d(&tmZ, &full[s], A, kb * BK, mt);
-          ptx::tma_load_2d(&tmUt, &full[s], A + DA_A_BYTES, kb * BK, n0);
+          ptx::tma_load_2d_pair(&tmZ, &full[s], A, kb * BK, mt);
+#pragma unroll
+          for (int ch = 0; ch < DA_N / 128; ch++)
+            ptx::tma_load_2d_pair(&tmU, &full[s], A + DA_A_BYTES + ch * MN_CHUNK, nb + ch * 64, kb * BK);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16(BM, DA_N, 0, 0);
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16(PM, DA_N, 0, 1);
       int it = 0, tc = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, tc++) {
+      for (int t = pair; t < ntiles; t += npairs, tc++) {
         const int acc = tc & 1;
         ptx::mbar_wait(&tempty[acc], ((tc >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
@@ -385,20 +472,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t a0 = ptx::smem_u32(smem + s * DA_STAGE), b0 = a0 + DA_A_BYTES;
 #pragma unroll
           for (int k = 0; k < BK / 16; k++)
-            ptx::umma_bf16(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024), ptx::sdesc_sw128(b0 + 32 * k, 16, 1024),
-                           idesc, (kb | k) != 0);
-          ptx::umma_commit(&empty[s]);
+            ptx::umma_bf16_2cta(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024),
+                                ptx::sdesc_sw128(b0 + 2048 * k, MN_CHUNK, 1024), idesc, (kb | k) != 0);
+          ptx::umma_commit_2cta(&empty[s]);
         }
-        ptx::umma_commit(&tfull[acc]);
+        ptx::umma_commit_2cta(&tfull[acc]);
       }
     }
   } else if (warp >= 4) {
     const int q = warp & 3;
-    const int N2 = 2 * S;
+    const int N2 = 2 * S, Sp = (int)round_up(S, BK);
     int tc = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, tc++) {
+    for (int t = pair; t < ntiles; t += npairs, tc++) {
       const int acc = tc & 1;
-      const int mt = c0 + (t / NTn) * BM, n0 = (t % NTn) * DA_N;
+      const int mt = c0 + (t / NTn) * PM + (int)rank * BM, n0 = (t % NTn) * DA_N;
       const int row = q * 32 + lane;
       const int64_t c = mt + row;
       const bool valid = (c - c0) < M;
@@ -411,34 +498,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         float v[8];
         ptx::tmem_ld8(tl + nc * 8, v);
         ptx::tmem_ld_wait();
-        int n = n0 + nc * 8;
-        if (!valid || n >= N2) continue;
-        if (n + 8 <= N2 && (N2 & 3) == 0) {
+        // padded B column n' = half * Sp + col  ->  dA column half * S + col (col < S)
+        const int np = n0 + nc * 8, half = np >= Sp, col = np - half * Sp;
+        if (!valid || col >= S) continue;
+        const int n = half * S + col;
+        if (col + 8 <= S && (S & 3) == 0) {
           *reinterpret_cast<float4 *>(out + n) = make_float4(v[0], v[1], v[2], v[3]);
           *reinterpret_cast<float4 *>(out + n + 4) = make_float4(v[4], v[5], v[6], v[7]);
         } else {
-          for (int u = 0; u < 8 && n + u < N2; u++) out[n + u] = v[u];
+          for (int u = 0; u < 8 && col + u < S; u++) out[n + u] = v[u];
         }
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      if (lane == 0) ptx::mbar_arrive_leader(&tempty[acc]);
     }
   }
   ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc(tbase, 512); }
+  ptx::cluster_sync();
+  if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc2(tbase, 512); }
 }
 
 // =================================================================== dU = dZ^T * Acat (all cells)
+// CTA pairs: pair tile = 256 gate rows (i) x 256 state columns (j) of one half (L / R);
+// each CTA stages its 128 rows of dZ^T and 128 of the 256 columns of the A plane.
 constexpr int DU_N = 256;
-constexpr int DU_A_BYTES = BM * 128;     // 2 MN chunks x 64 K-rows x 128 B
-constexpr int DU_B_BYTES = DU_N * 128;   // 4 MN chunks x 64 K-rows x 128 B
+constexpr int DU_A_BYTES = BM * 128;         // 2 MN chunks x 64 K-rows x 128 B
+constexpr int DU_B_BYTES = (DU_N / 2) * 128; // 2 MN chunks x 64 K-rows x 128 B
 constexpr int DU_STAGE = DU_A_BYTES + DU_B_BYTES;
 constexpr int DU_SMEM = ST * DU_STAGE + 1024;
-constexpr int MN_CHUNK = 64 * 128;       // bytes per 64-element MN chunk of 64 K rows
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_dU_tc(const __grid_constant__ CUtensorMap tmZ2, const __grid_constant__ CUtensorMap tmAL,
                  const __grid_constant__ CUtensorMap tmAR, int n_cells, int S, int Mg, int NT, int kb_per_split,
                  float *__restrict__ out_base, int64_t split_stride, int accumulate) {
@@ -447,9 +537,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull;
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int half = blockIdx.x / NT, jt = blockIdx.x - half * NT;
-  const int i0 = blockIdx.y * BM, jn0 = jt * DU_N;
-  // split-K over cells: this CTA reduces k-blocks [kb0, kb1) into its own partial slab
+  const uint32_t rank = ptx::cluster_ctarank();
+  const int px = blockIdx.x >> 1;
+  const int half = px / NT, jt = px - half * NT;
+  const int i0 = blockIdx.y * PM + (int)rank * BM;   // this CTA's gate rows
+  const int jn0 = jt * DU_N;                          // the pair's state columns
+  // split-K over cells: this pair reduces k-blocks [kb0, kb1) into its own partial slab
   const int KBall = (int)cdiv(n_cells, BK);
   const int kb0 = blockIdx.z * kb_per_split;
   const int kb1 = min(KBall, kb0 + kb_per_split);
@@ -463,32 +556,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::prefetch_tmap(&tmAL);
     ptx::prefetch_tmap(&tmAR);
   }
-  if (warp == 2) { ptx::tmem_alloc(&tmem_base_sh, 256); ptx::tmem_relinquish(); }
+  if (warp == 2) { ptx::tmem_alloc2(&tmem_base_sh, 256); ptx::tmem_relinquish2(); }
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tbase = tmem_base_sh;
   if (warp == 0 && lane == 0) {
-    // A' = dZ^T chunk (2 boxes of 64 gate-rows x 64 cells), B' = the cells' [h_L | h_R]
-    // rows from the A operand planes written by the forward (4 boxes of 64 cols x 64 cells)
+    // A' = dZ^T chunk (2 boxes of 64 gate-rows x 64 cells), B' = this CTA's 128 columns of
+    // the cells' h_L / h_R rows in the A operand planes written by the forward
     const CUtensorMap *tmB = half ? &tmAR : &tmAL;
+    const int jb = jn0 + (int)rank * (DU_N / 2);
     for (int it = 0; it < KB; it++) {
       const int kb = kb0 + it;
       int s = it % ST;
       uint32_t ph = (it / ST) & 1;
       ptx::mbar_wait(&empty[s], ph ^ 1);
-      ptx::mbar_arrive_expect_tx(&full[s], DU_STAGE);
+      if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], 2 * DU_STAGE);
       uint8_t *A = smem + s * DU_STAGE;
       uint8_t *B = A + DU_A_BYTES;
-      ptx::tma_load_2d(&tmZ2, &full[s], A, i0, kb * BK);
-      ptx::tma_load_2d(&tmZ2, &full[s], A + MN_CHUNK, i0 + 64, kb * BK);
-#pragma unroll
-      for (int ch = 0; ch < 4; ch++) ptx::tma_load_2d(tmB, &full[s], B + ch * MN_CHUNK, jn0 + ch * 64, kb * BK);
+      ptx::tma_load_2d_pair(&tmZ2, &full[s], A, i0, kb * BK);
+      ptx::tma_load_2d_pair(&tmZ2, &full[s], A + MN_CHUNK, i0 + 64, kb * BK);
+      ptx::tma_load_2d_pair(tmB, &full[s], B, jb, kb * BK);
+      ptx::tma_load_2d_pair(tmB, &full[s], B + MN_CHUNK, jb + 64, kb * BK);
     }
-  } else if (warp == 0) {
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16(BM, DU_N, 1, 1);
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16(PM, DU_N, 1, 1);
       for (int it = 0; it < KB; it++) {
         int s = it % ST;
         uint32_t ph = (it / ST) & 1;
@@ -497,15 +590,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t a0 = ptx::smem_u32(smem + s * DU_STAGE), b0 = a0 + DU_A_BYTES;
 #pragma unroll
         for (int k = 0; k < BK / 16; k++)
-          ptx::umma_bf16(tbase, ptx::sdesc_sw128(a0 + 2048 * k, MN_CHUNK, 1024),
-                         ptx::sdesc_sw128(b0 + 2048 * k, MN_CHUNK, 1024), idesc, (it | k) != 0);
-        ptx::umma_commit(&empty[s]);
+          ptx::umma_bf16_2cta(tbase, ptx::sdesc_sw128(a0 + 2048 * k, MN_CHUNK, 1024),
+                              ptx::sdesc_sw128(b0 + 2048 * k, MN_CHUNK, 1024), idesc, (it | k) != 0);
+        ptx::umma_commit_2cta(&empty[s]);
       }
-      ptx::umma_commit(&tfull);
+      if (KB > 0) ptx::umma_commit_2cta(&tfull);
     }
   } else if (warp >= 4) {
     const int q = warp & 3;
-    ptx::mbar_wait(&tfull, 0);
+    if (KB > 0) ptx::mbar_wait(&tfull, 0);
     ptx::tc_fence_after();
     const int i = i0 + q * 32 + lane;
     const uint32_t tl = tbase + ((uint32_t)(q * 32) << 16);
@@ -530,8 +623,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc(tbase, 256); }
+  ptx::cluster_sync();
+  if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc2(tbase, 256); }
 }
 
 // out[i] = (accumulate ? out[i] : 0) + sum_{s < nsplit} part[s][i]   (fixed order)
@@ -557,37 +650,41 @@ __global__ void k_reduce_splits(int64_t n, int nsplit, const float *__restrict__
 }
 
 // =================================================================== weight prep
-// Forward operand: Uil[t*GW + g*W + jj][half*Sp + k] = bf16(U[g*S + t*W + jj][half*S + k])
-// (gate-interleaved per W-column tile; K halves padded to Sp = round_up(S, 64) so every TMA
-// box starts 128-byte aligned; rows / columns past S are zero).
-__global__ void k_prep_Uil(int gates, int W, int NT, int S, int Sp, const float *__restrict__ U,
-                           __nv_bfloat16 *__restrict__ Uil, int ld_u) {
-  const int GW = gates * W;
-  const int64_t total = (int64_t)NT * GW * (2 * Sp);
+// Ub[r][half*Sp + k] = bf16(U[r][half*S + k]) for k < S, 0 for k in [S, Sp) (Sp =
+// round_up(S, 64)): the one bf16 copy of U serves the forward (K-major B operand, each K
+// half starting 128 B aligned) and dA (MN-major B operand over the padded 2*Sp columns).
+// With il_gates > 0 the output rows are gate-interleaved in blocks of 8 state columns
+// (Uil8, the forward's B operand): out row (j/8)*8*G + g*8 + j%8 <- U row g*S + j (zero for
+// j >= S).
+__global__ void k_prep_U(int64_t rows, int S, int Sp, const float *__restrict__ U, __nv_bfloat16 *__restrict__ Ub,
+                         int il_gates) {
+  const int cpr = Sp / 4;  // 8-element chunks per row (2*Sp / 8)
+  const int64_t total = rows * cpr;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool vec = (S & 3) == 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-    const int64_t ri = i / (2 * Sp);
-    const int kp = (int)(i - ri * 2 * Sp);
-    const int t = (int)(ri / GW), rem = (int)(ri - (int64_t)t * GW), g = rem / W, j = t * W + (rem - g * W);
-    const int half = kp >= Sp, kk = kp - half * Sp;
-    float v = (j < S && kk < S) ? U[((int64_t)g * S + j) * 2 * S + half * S + kk] : 0.f;
-    Uil[ri * ld_u + kp] = __float2bfloat16_rn(v);
-  }
-}
-
-// Backward operand: Ut[k][r] = bf16(U[r][k]) (ld_ut), 32x32 smem tiles.
-__global__ void k_prep_Ut(int R, int K, const float *__restrict__ U, __nv_bfloat16 *__restrict__ Ut, int ld_ut) {
-  __shared__ float t[32][33];
-  const int r0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int i = ty; i < 32; i += 8) {
-    int r = r0 + i, k = k0 + tx;
-    t[i][tx] = (r < R && k < K) ? U[(int64_t)r * K + k] : 0.f;
-  }
-  __syncthreads();
-  for (int i = ty; i < 32; i += 8) {
-    int k = k0 + i, r = r0 + tx;
-    if (r < R && k < K) Ut[(int64_t)k * ld_ut + r] = __float2bfloat16_rn(t[tx][i]);
+    const int64_t r = i / cpr;
+    const int kp = (int)(i - r * cpr) * 8;
+    const int half = kp >= Sp, k = kp - half * Sp;
+    int K = S;
+    int64_t src_row = r;
+    if (il_gates) {
+      const int64_t blk = r / (8 * il_gates), rem = r - blk * 8 * il_gates;
+      const int64_t j = blk * 8 + (rem & 7), g = rem >> 3;
+      src_row = g * S + j;
+      if (j >= S) K = 0;  // padding rows of the last 8-column block
+    }
+    const float *src = U + src_row * 2 * S + half * S + k;
+    float v[8];
+    if (vec && k + 8 <= K) {
+      float4 a = __ldg(reinterpret_cast<const float4 *>(src)), b = __ldg(reinterpret_cast<const float4 *>(src + 4));
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; u++) v[u] = k + u < K ? __ldg(src + u) : 0.f;
+    }
+    *reinterpret_cast<uint4 *>(Ub + r * 2 * Sp + kp) =
+        make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
   }
 }
 
@@ -621,9 +718,18 @@ fold_status make_map(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t ro
   return r == CUDA_SUCCESS ? FOLD_OK : FOLD_E_CUDA;
 }
 
+// cudaFuncSetAttribute once per kernel and size (it is a host round trip worth avoiding
+// inside the level loop)
 template <typename K>
 fold_status set_smem(K kernel, int bytes) {
+  static thread_local std::unordered_map<const void *, int> set;  // per host thread (and device)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const void *key = (const char *)(const void *)kernel + dev;
+  auto it = set.find(key);
+  if (it != set.end() && it->second >= bytes) return FOLD_OK;
   FOLD_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  set[key] = bytes;
   return FOLD_OK;
 }
 
@@ -638,97 +744,111 @@ int num_sms() {
   return g_num_sms;
 }
 
-int dbg_fwd_epi() {
-  static int v = [] { const char *e = getenv("FOLD_DBG_FWD_EPI"); return e ? atoi(e) : 0; }();
-  return v;
+// Max co-resident CTA pairs of a kernel (the persistent kernels' spin waits need every CTA
+// of the grid resident: the grid never exceeds this).
+template <typename K>
+int max_pairs(K kernel, int threads, int smem) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * (num_sms() / 2));
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, (const void *)kernel, &cfg) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = num_sms() / 2;
+  }
+  return n < num_sms() / 2 ? n : num_sms() / 2;
 }
 
-template <int GATES, int W>
-fold_status launch_fwd(int r0, int r1, int nl, int n_cells, const int32_t *gather, int S, int ld, const TcWeights &w,
-                       const float *b, __nv_bfloat16 *H, float *C, __nv_bfloat16 *Gact, int ld_g, const ScatterA &sc,
-                       cudaStream_t st) {
-  using Cfg = FwdCfg<GATES, W>;
-  CUtensorMap tmAL, tmAR, tmU;
-  FOLD_TRY(make_map(&tmAL, sc.AL, (uint64_t)S, (uint64_t)n_cells, (uint64_t)sc.ld * 2, BK, BM));
-  FOLD_TRY(make_map(&tmAR, sc.AR, (uint64_t)S, (uint64_t)n_cells, (uint64_t)sc.ld * 2, BK, BM));
-  const int NTu = (int)cdiv(S, W);
-  FOLD_TRY(make_map(&tmU, w.U, (uint64_t)w.ld_u, (uint64_t)NTu * Cfg::N, (uint64_t)w.ld_u * 2, BK, Cfg::N));
-  auto kern = k_cell_fwd_tc<GATES, W>;
+template <int GATES>
+fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
+  using Cfg = FwdCfg<GATES>;
+  const int S = a.S, nc = a.n_cells;
+  CUtensorMap tmAL, tmAR, tmUw, tmUn;
+  FOLD_TRY(make_map(&tmAL, a.sc.AL, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, BM));
+  FOLD_TRY(make_map(&tmAR, a.sc.AR, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, BM));
+  const uint64_t il_rows = (uint64_t)cdiv(S, 8) * 8 * GATES;
+  FOLD_TRY(make_map(&tmUw, a.Ub, (uint64_t)a.ld_u, il_rows, (uint64_t)a.ld_u * 2, BK, GATES * Cfg::WMAX / 2));
+  FOLD_TRY(make_map(&tmUn, a.Ub, (uint64_t)a.ld_u, il_rows, (uint64_t)a.ld_u * 2, BK, GATES * Cfg::WNAR / 2));
+  auto kern = k_fwd_levels<GATES>;
   const int bias_bytes = GATES * S * 4;
   const int bias_in_smem = Cfg::SMEM + bias_bytes <= 227 * 1024 ? 1 : 0;
   const int smem_bytes = Cfg::SMEM + (bias_in_smem ? bias_bytes : 0);
   FOLD_TRY(set_smem(kern, smem_bytes));
-  const int NT = (int)cdiv(S, W);
-  const int ntiles = NT * (int)cdiv(r1 - r0, BM);
-  const int grid = ntiles < num_sms() ? ntiles : num_sms();
-  int KBh = (int)cdiv(S, BK);
-  kern<<<grid, Cfg::THREADS, smem_bytes, st>>>(tmAL, tmAR, tmU, r0, r1, nl, S, w.ld_u / 2, ld, KBh, NT, ntiles,
-                                               gather, b, H, C, Gact, ld_g, sc, dbg_fwd_epi(), bias_in_smem);
+  static thread_local int npairs_max = 0;
+  if (!npairs_max) npairs_max = max_pairs(kern, Cfg::THREADS, smem_bytes);
+  FwdLevels L{a.level_off, a.D, S, Cfg::WMAX, Cfg::WNAR, npairs_max / 2};
+  int64_t total = 0;
+  for (int d = 2; d <= a.D; d++) {
+    const int M = a.level_off_host[d + 1] - a.level_off_host[d];
+    total += cdiv(M, PM) * cdiv(S, fwd_level_W(L, M));
+  }
+  if (total <= 0) return FOLD_OK;
+  if (total > INT32_MAX) return FOLD_E_INVALID;
+  FOLD_CUDA_TRY(cudaMemsetAsync(a.done, 0, (size_t)(a.D + 2) * sizeof(int), st));
+  const int npairs = total < npairs_max ? (int)total : npairs_max;
+  kern<<<2 * npairs, Cfg::THREADS, smem_bytes, st>>>(tmAL, tmAR, tmUw, tmUn, L, (int)total, a.nl, a.ld, a.gather,
+                                                      a.b, a.H, a.C, a.Gact, a.ld_g, a.sc, a.done, bias_in_smem);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
 
 }  // namespace
 
-int tc_fwd_W(int gates) { return gates == 5 ? 48 : 128; }
+int tc_ld_u(int S) { return 2 * (int)round_up(S, BK); }
 
-size_t tc_workspace_bytes(int gates, int S) {
-  const int W = tc_fwd_W(gates);
-  size_t ld_u = 2 * round_up(S, 64), ld_ut = round_up((int64_t)gates * S, 8);
-  size_t rows_il = (size_t)cdiv(S, W) * gates * W;
-  return round_up((int64_t)(rows_il * ld_u * 2), 256) + round_up((int64_t)2 * S * ld_ut * 2, 256);
-}
+size_t tc_weights_bytes(int gates, int S) { return round_up(cdiv(S, 8) * 8 * gates * tc_ld_u(S) * 2, 256); }
 
-size_t tc_ut_offset(int gates, int S) {
-  const int W = tc_fwd_W(gates);
-  size_t ld_u = 2 * round_up(S, 64);
-  size_t rows_il = (size_t)cdiv(S, W) * gates * W;
-  return round_up((int64_t)(rows_il * ld_u * 2), 256);
-}
-
-fold_status tc_prepare_U(int gates, int S, const float *U, TcWeights &w, bool transpose, cudaStream_t st) {
-  if (!transpose) {
-    const int W = tc_fwd_W(gates), NT = (int)cdiv(S, W), Sp = (int)round_up(S, 64);
-    int64_t total = (int64_t)NT * gates * W * 2 * Sp;
-    int64_t blocks = cdiv(total, 256);
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    k_prep_Uil<<<(unsigned)blocks, 256, 0, st>>>(gates, W, NT, S, Sp, U, w.U, w.ld_u);
-  } else {
-    const int R = gates * S, K = 2 * S;
-    dim3 grid((unsigned)cdiv(K, 32), (unsigned)cdiv(R, 32));
-    k_prep_Ut<<<grid, 256, 0, st>>>(R, K, U, w.Ut, w.ld_ut);
-  }
+fold_status tc_prepare_Uil(int gates, int S, const float *U, __nv_bfloat16 *Uil, cudaStream_t st) {
+  const int Sp = tc_ld_u(S) / 2;
+  const int64_t rows = cdiv(S, 8) * 8 * gates;
+  int64_t blocks = cdiv(rows * (Sp / 4), 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_prep_U<<<(unsigned)blocks, 256, 0, st>>>(rows, S, Sp, U, Uil, gates);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
 
-fold_status tc_cell_fwd(int cell, int r0, int r1, int nl, int n_cells, const int32_t *gather, int S, int ld,
-                        const TcWeights &w, const float *b, __nv_bfloat16 *H, float *C, __nv_bfloat16 *Gact, int ld_g,
-                        const ScatterA &sc, cudaStream_t st) {
-  if (r1 <= r0) return FOLD_OK;
-  if (cell == FOLD_CELL_TREELSTM)
-    return launch_fwd<5, 48>(r0, r1, nl, n_cells, gather, S, ld, w, b, H, C, Gact, ld_g, sc, st);
-  return launch_fwd<1, 128>(r0, r1, nl, n_cells, gather, S, ld, w, b, H, C, Gact, ld_g, sc, st);
+fold_status tc_prepare_U(int gates, int S, const float *U, __nv_bfloat16 *Ub, cudaStream_t st) {
+  const int64_t rows = (int64_t)gates * S;
+  const int Sp = tc_ld_u(S) / 2;
+  int64_t blocks = cdiv(rows * (Sp / 4), 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_prep_U<<<(unsigned)blocks, 256, 0, st>>>(rows, S, Sp, U, Ub, 0);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+fold_status tc_fwd_levels(int cell, const TcFwdArgs &a, cudaStream_t st) {
+  if (a.D < 2) return FOLD_OK;
+  if (cell == FOLD_CELL_TREELSTM) return launch_fwd_levels<5>(a, st);
+  return launch_fwd_levels<1>(a, st);
 }
 
 fold_status tc_gemm_dA(int c0, int M, int n_cells, int S, int gates, const __nv_bfloat16 *dZ, int ld_z,
-                       const TcWeights &w, float *dA, cudaStream_t st) {
+                       const __nv_bfloat16 *Ub, float *dA, cudaStream_t st) {
   if (M <= 0) return FOLD_OK;
-  CUtensorMap tmZ, tmUt;
+  CUtensorMap tmZ, tmU;
   FOLD_TRY(make_map(&tmZ, dZ, (uint64_t)gates * S, (uint64_t)n_cells, (uint64_t)ld_z * 2, BK, BM));
-  FOLD_TRY(make_map(&tmUt, w.Ut, (uint64_t)gates * S, (uint64_t)2 * S, (uint64_t)w.ld_ut * 2, BK, DA_N));
+  const int ld_u = tc_ld_u(S);
+  FOLD_TRY(make_map(&tmU, Ub, (uint64_t)ld_u, (uint64_t)gates * S, (uint64_t)ld_u * 2, 64, BK));
   FOLD_TRY(set_smem(k_gemm_dA_tc, DA_SMEM));
-  const int NTn = (int)cdiv(2 * S, DA_N);
-  const int ntiles = NTn * (int)cdiv(M, BM);
-  const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  const int NTn = (int)cdiv(ld_u, DA_N);
+  const int ntiles = NTn * (int)cdiv(M, PM);
+  const int np = ntiles < num_sms() / 2 ? ntiles : num_sms() / 2;
   int KB = (int)cdiv(gates * S, BK);
-  k_gemm_dA_tc<<<grid, kThreads, DA_SMEM, st>>>(tmZ, tmUt, c0, M, KB, S, NTn, ntiles, dA);
+  k_gemm_dA_tc<<<2 * np, kThreads, DA_SMEM, st>>>(tmZ, tmU, c0, M, KB, S, NTn, ntiles, dA);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
 
 int tc_dU_splits(int n_cells, int gates, int S) {
-  int64_t tiles = 2 * cdiv(S, DU_N) * cdiv((int64_t)gates * S, BM);
+  int64_t tiles = 2 * 2 * cdiv(S, DU_N) * cdiv((int64_t)gates * S, PM);  // CTAs per split
   int64_t kbs = cdiv(n_cells, BK);
   int64_t want = cdiv(4 * 148, tiles);           // >= ~4 waves of CTAs in total
   int64_t cap = kbs / 32;                         // keep >= 32 k-blocks (2048 cells) per split
@@ -749,7 +869,7 @@ fold_status tc_gemm_dU(int n_cells, int S, int gates, const __nv_bfloat16 *dZ, i
   const int splits = tc_dU_splits(n_cells, gates, S);
   const int KBall = (int)cdiv(n_cells, BK);
   const int kbps = (int)cdiv(KBall, splits);
-  dim3 grid((unsigned)(2 * NT), (unsigned)cdiv(gates * S, BM), (unsigned)splits);
+  dim3 grid((unsigned)(2 * 2 * NT), (unsigned)cdiv(gates * S, PM), (unsigned)splits);
   const int64_t n = (int64_t)gates * S * 2 * S;
   if (splits == 1) {
     k_gemm_dU_tc<<<grid, kThreads, DU_SMEM, st>>>(tmZ2, tmAL, tmAR, n_cells, S, gates * S, NT, kbps, dU, 0,
