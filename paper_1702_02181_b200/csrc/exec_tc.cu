@@ -95,7 +95,12 @@ struct FwdCfg {
   static_assert(STAGE % 1024 == 0, "stages stay 1024 B aligned (128B swizzle atoms)");
   static constexpr int ACC_STRIDE = 256;  // TMEM columns per accumulator buffer (2 buffers)
   static constexpr int TMEM_COLS = 512;
-  static constexpr int SMEM = ST * STAGE + 1024;
+  static constexpr int NST = 4;           // pipeline stages (the rest of smem stages the outputs)
+  // epilogue staging: the tile's saved gates [GATES][128][W] bf16 and cell states [128][W]
+  // fp32 leave through TMA bulk stores (row-scattered per-thread stores were LSU-bound)
+  static constexpr int G_STAGE = GATES * BM * WMAX * 2;
+  static constexpr int C_STAGE = BM * WMAX * 4;
+  static constexpr int SMEM = NST * STAGE + G_STAGE + C_STAGE + 1024;
   static constexpr int EPI_WARPS = 8;     // 2 per SM sub-partition: each owns half the columns
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static_assert(GATES * WMAX <= 256 && (GATES * WNAR) % 16 == 0 && (GATES * WNAR / 2) % 8 == 0, "UMMA N, M=256");
@@ -111,13 +116,17 @@ struct FwdCfg {
 template <int GATES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREADS, 1)
     k_fwd_levels(const __grid_constant__ CUtensorMap tmAL, const __grid_constant__ CUtensorMap tmAR,
-                 const __grid_constant__ CUtensorMap tmUw, const __grid_constant__ CUtensorMap tmUn, FwdLevels L,
+                 const __grid_constant__ CUtensorMap tmUw, const __grid_constant__ CUtensorMap tmUn,
+                 const __grid_constant__ CUtensorMap tmGw, const __grid_constant__ CUtensorMap tmGn,
+                 const __grid_constant__ CUtensorMap tmCw, const __grid_constant__ CUtensorMap tmCn, FwdLevels L,
                  int total_tiles, int nl, int ld, const int32_t *__restrict__ gather, const float *__restrict__ bias,
                  __nv_bfloat16 *__restrict__ H, float *C, __nv_bfloat16 *__restrict__ Gact, int ld_g, ScatterA sc,
-                 int *done, int bias_in_smem) {
+                 int *done) {
   using Cfg = FwdCfg<GATES>;
+  constexpr int ST = Cfg::NST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
+  uint8_t *gsm = smem + ST * Cfg::STAGE, *csm = gsm + Cfg::G_STAGE;
   __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
   const int S = L.S;
@@ -134,16 +143,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
     ptx::prefetch_tmap(&tmAR);
     ptx::prefetch_tmap(&tmUw);
     ptx::prefetch_tmap(&tmUn);
+    ptx::prefetch_tmap(&tmGw);
+    ptx::prefetch_tmap(&tmCw);
   }
   if (warp == 2) {
     ptx::tmem_alloc2(&tmem_base_sh, Cfg::TMEM_COLS);
     ptx::tmem_relinquish2();
   }
-  // the whole bias (GATES*S fp32) stays in shared memory when it fits next to the ring
-  float *sbias = reinterpret_cast<float *>(smem + ST * Cfg::STAGE);
-  if (bias_in_smem)
-    for (int i = tid; i < GATES * S; i += blockDim.x) sbias[i] = bias[i];
-  const float *bsrc = bias_in_smem ? sbias : bias;
+  const float *bsrc = bias;  // 5 x 8 floats per chunk, warp-uniform (broadcast) loads
   ptx::tc_fence_before();
   ptx::cluster_sync();  // barrier inits and the pair's TMEM allocation visible to both CTAs
   ptx::tc_fence_after();
@@ -285,8 +292,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         }
       };
       load_c(j0 + grp * 8);
+      // full-width tiles stage G and C in shared memory and leave by TMA (partial tiles at
+      // the S edge store directly)
+      const bool staged = (S & 7) == 0 && j0 + W <= S;
+      const int64_t c_tile = (int64_t)(cur.r0 - nl) + (int64_t)(lt / cur.NT) * PM + rank * BM;
       ptx::mbar_wait(&tfull[acc], aph);
       ptx::tc_fence_after();
+      if (staged) {  // the previous tile's bulk stores have finished reading the staging
+        if (warp == 4 && lane == 0) ptx::bulk_wait_read0();
+        ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
+      }
       const uint32_t tl = tbase + acc * Cfg::ACC_STRIDE + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
       for (int jc = grp; jc < chunks; jc += 2) {
@@ -305,7 +320,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         if constexpr (GATES == 1) {
 #pragma unroll
           for (int u = 0; u < 8; u++) hh[u] = tanh_fast(z[0][u] + (jb + u < S ? bsrc[jb + u] : 0.f));
-          if (fullc) {
+          if (staged) {
+            uint4 pk = make_uint4(pack_bf16x2(hh[0], hh[1]), pack_bf16x2(hh[2], hh[3]), pack_bf16x2(hh[4], hh[5]),
+                                  pack_bf16x2(hh[6], hh[7]));
+            *reinterpret_cast<uint4 *>(gsm + row * W * 2 + jc * 16) = pk;
+            *reinterpret_cast<float4 *>(csm + row * W * 4 + jc * 32) = make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4 *>(csm + row * W * 4 + jc * 32 + 16) = make_float4(0.f, 0.f, 0.f, 0.f);
+          } else if (fullc) {
             uint4 pk = make_uint4(pack_bf16x2(hh[0], hh[1]), pack_bf16x2(hh[2], hh[3]), pack_bf16x2(hh[4], hh[5]),
                                   pack_bf16x2(hh[6], hh[7]));
             *reinterpret_cast<uint4 *>(Gact + c * ld_g + jb) = pk;
@@ -323,8 +344,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
           for (int g = 0; g < 5; g++) {
             float bz[8];
             if (fullc) {
-              float4 x = *reinterpret_cast<const float4 *>(bsrc + g * S + jb);
-              float4 y = *reinterpret_cast<const float4 *>(bsrc + g * S + jb + 4);
+              float4 x = __ldg(reinterpret_cast<const float4 *>(bsrc + g * S + jb));
+              float4 y = __ldg(reinterpret_cast<const float4 *>(bsrc + g * S + jb + 4));
               bz[0] = x.x; bz[1] = x.y; bz[2] = x.z; bz[3] = x.w; bz[4] = y.x; bz[5] = y.y; bz[6] = y.z; bz[7] = y.w;
             } else {
 #pragma unroll
@@ -339,7 +360,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
             hh[u] = gs[3][u] * tanh_fast(cc[u]);
           }
           __nv_bfloat16 *ga = Gact + c * ld_g;
-          if (fullc) {
+          if (staged) {
+            *reinterpret_cast<float4 *>(csm + row * W * 4 + jc * 32) = make_float4(cc[0], cc[1], cc[2], cc[3]);
+            *reinterpret_cast<float4 *>(csm + row * W * 4 + jc * 32 + 16) = make_float4(cc[4], cc[5], cc[6], cc[7]);
+#pragma unroll
+            for (int g = 0; g < 5; g++)
+              *reinterpret_cast<uint4 *>(gsm + (g * BM + row) * W * 2 + jc * 16) =
+                  make_uint4(pack_bf16x2(gs[g][0], gs[g][1]), pack_bf16x2(gs[g][2], gs[g][3]),
+                             pack_bf16x2(gs[g][4], gs[g][5]), pack_bf16x2(gs[g][6], gs[g][7]));
+          } else if (fullc) {
             *reinterpret_cast<float4 *>(C + r * ld + jb) = make_float4(cc[0], cc[1], cc[2], cc[3]);
             *reinterpret_cast<float4 *>(C + r * ld + jb + 4) = make_float4(cc[4], cc[5], cc[6], cc[7]);
 #pragma unroll
@@ -382,18 +411,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_leader(&tempty[acc]);
-      // last tile of this level for this CTA: publish (all epilogue warps' stores, then one
-      // release increment; level d is complete at 2 min(#pair tiles(d), #pairs) increments)
       const int Tn = T + npairs;
-      if (Tn >= total_tiles || Tn >= cur.t0 + cur.nt) {
+      const bool last_of_level = Tn >= total_tiles || Tn >= cur.t0 + cur.nt;
+      if (staged) {
+        // staging complete -> one thread issues the tile's bulk stores (rows past the level
+        // land in later levels' rows, which those levels overwrite after this level is
+        // published, or are clipped at the tensor end)
+        ptx::fence_proxy_async_smem();
         ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
         if (warp == 4 && lane == 0) {
+          const CUtensorMap *tG = W == Cfg::WMAX ? &tmGw : &tmGn;
+          const CUtensorMap *tC = W == Cfg::WMAX ? &tmCw : &tmCn;
+#pragma unroll
+          for (int g = 0; g < GATES; g++) ptx::tma_store_2d(tG, gsm + g * BM * W * 2, g * S + j0, (int)c_tile);
+          ptx::tma_store_2d(tC, csm, j0, (int)(c_tile + nl));
+          ptx::bulk_commit();
+        }
+      }
+      // last tile of this level for this CTA: publish (all epilogue warps' stores and the
+      // bulk stores complete, then one release increment; level d is complete at
+      // 2 min(#pair tiles(d), #pairs) increments)
+      if (last_of_level) {
+        ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
+        if (warp == 4 && lane == 0) {
+          ptx::bulk_wait0();
           ptx::fence_proxy_async_global();
           __threadfence();
           ptx::red_release_gpu_add(done + cur.d, 1);
         }
       }
     }
+    if (warp == 4 && lane == 0) ptx::bulk_wait0();
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();  // neither CTA leaves while the pair's MMAs / arrivals may touch it
@@ -702,9 +750,9 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2D bf16 tensor map: `cols` contiguous elements per row, `rows` rows, `row_bytes` stride.
-fold_status make_map(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t rows, uint64_t row_bytes,
-                     uint32_t box_cols, uint32_t box_rows) {
+// 2D tensor map: `cols` contiguous elements per row, `rows` rows, `row_bytes` stride.
+fold_status make_map_ex(CUtensorMap *m, const void *ptr, CUtensorMapDataType dt, uint64_t cols, uint64_t rows,
+                        uint64_t row_bytes, uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle sw) {
   auto fn = encode_fn();
   if (!fn) return FOLD_E_CUDA;
   if (rows < 1) rows = 1;
@@ -712,10 +760,15 @@ fold_status make_map(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t ro
   cuuint64_t strides[1] = {row_bytes};
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = fn(m, dt, 2, const_cast<void *>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? FOLD_OK : FOLD_E_CUDA;
+}
+// bf16 operand map with 128B swizzle (UMMA operand tiles)
+fold_status make_map(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t rows, uint64_t row_bytes,
+                     uint32_t box_cols, uint32_t box_rows) {
+  return make_map_ex(m, ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, cols, rows, row_bytes, box_cols, box_rows,
+                     CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 // cudaFuncSetAttribute once per kernel and size (it is a host round trip worth avoiding
@@ -769,16 +822,25 @@ template <int GATES>
 fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
   using Cfg = FwdCfg<GATES>;
   const int S = a.S, nc = a.n_cells;
-  CUtensorMap tmAL, tmAR, tmUw, tmUn;
+  CUtensorMap tmAL, tmAR, tmUw, tmUn, tmGw, tmGn, tmCw, tmCn;
   FOLD_TRY(make_map(&tmAL, a.sc.AL, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, BM));
   FOLD_TRY(make_map(&tmAR, a.sc.AR, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, BM));
   const uint64_t il_rows = (uint64_t)cdiv(S, 8) * 8 * GATES;
   FOLD_TRY(make_map(&tmUw, a.Ub, (uint64_t)a.ld_u, il_rows, (uint64_t)a.ld_u * 2, BK, GATES * Cfg::WMAX / 2));
   FOLD_TRY(make_map(&tmUn, a.Ub, (uint64_t)a.ld_u, il_rows, (uint64_t)a.ld_u * 2, BK, GATES * Cfg::WNAR / 2));
+  // epilogue bulk stores: G [n_cells][GATES*S] bf16 and the pool's C [N][S] fp32, plain
+  // (unswizzled) boxes of W columns x 128 rows
+  const uint64_t Nrows = (uint64_t)nc + a.nl;
+  FOLD_TRY(make_map_ex(&tmGw, a.Gact, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (uint64_t)GATES * S, (uint64_t)nc,
+                       (uint64_t)a.ld_g * 2, Cfg::WMAX, BM, CU_TENSOR_MAP_SWIZZLE_NONE));
+  FOLD_TRY(make_map_ex(&tmGn, a.Gact, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (uint64_t)GATES * S, (uint64_t)nc,
+                       (uint64_t)a.ld_g * 2, Cfg::WNAR, BM, CU_TENSOR_MAP_SWIZZLE_NONE));
+  FOLD_TRY(make_map_ex(&tmCw, a.C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (uint64_t)S, Nrows, (uint64_t)a.ld * 4,
+                       Cfg::WMAX, BM, CU_TENSOR_MAP_SWIZZLE_NONE));
+  FOLD_TRY(make_map_ex(&tmCn, a.C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (uint64_t)S, Nrows, (uint64_t)a.ld * 4,
+                       Cfg::WNAR, BM, CU_TENSOR_MAP_SWIZZLE_NONE));
   auto kern = k_fwd_levels<GATES>;
-  const int bias_bytes = GATES * S * 4;
-  const int bias_in_smem = Cfg::SMEM + bias_bytes <= 227 * 1024 ? 1 : 0;
-  const int smem_bytes = Cfg::SMEM + (bias_in_smem ? bias_bytes : 0);
+  const int smem_bytes = Cfg::SMEM;
   FOLD_TRY(set_smem(kern, smem_bytes));
   static thread_local int npairs_max = 0;
   if (!npairs_max) npairs_max = max_pairs(kern, Cfg::THREADS, smem_bytes);
@@ -792,8 +854,9 @@ fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
   if (total > INT32_MAX) return FOLD_E_INVALID;
   FOLD_CUDA_TRY(cudaMemsetAsync(a.done, 0, (size_t)(a.D + 2) * sizeof(int), st));
   const int npairs = total < npairs_max ? (int)total : npairs_max;
-  kern<<<2 * npairs, Cfg::THREADS, smem_bytes, st>>>(tmAL, tmAR, tmUw, tmUn, L, (int)total, a.nl, a.ld, a.gather,
-                                                      a.b, a.H, a.C, a.Gact, a.ld_g, a.sc, a.done, bias_in_smem);
+  kern<<<2 * npairs, Cfg::THREADS, smem_bytes, st>>>(tmAL, tmAR, tmUw, tmUn, tmGw, tmGn, tmCw, tmCn, L, (int)total,
+                                                      a.nl, a.ld, a.gather, a.b, a.H, a.C, a.Gact, a.ld_g, a.sc,
+                                                      a.done);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
