@@ -1,10 +1,15 @@
 // sched.cu — GPU scheduler for dynamic batching (§2, L40-44).
 //
-// fold_schedule = validate -> consumer lists -> level-synchronous depth frontier
-// (one cooperative kernel, grid barrier per depth) -> stable LSD radix sort on
-// key = 2*depth + op (ties by node id) -> offsets / rank / gather vectors ->
-// consumer CSR (stable sort of cell edges by child row) -> leaves by token ->
-// roots. One blocking D2H at the end. All kernels are integer work, HBM/latency bound.
+// fold_schedule is ONE cooperative persistent kernel (k_schedule) whose phases are
+// separated by grid barriers: validate -> consumer counts and lists -> level-synchronous
+// depth frontier (one barrier per depth) -> stable counting/radix sort on
+// key = 2*depth + op, ties by node id (L42-43) -> perm / rank / offsets / gather vectors
+// (L44) -> consumer CSR (stable sort of cell edges by child row) -> leaves by token ->
+// roots. Radix pass counts depend on the batch's depth, node count and vocabulary, which
+// only the device knows: it chooses them itself, so the host sees one launch and one
+// blocking D2H (the executor's launch shapes need level_off). Small batches run as a
+// single block, where a "grid barrier" is a __syncthreads. All phases are integer work,
+// HBM / latency bound.
 #include <climits>
 #include <cstdio>
 #include <cstring>
@@ -29,9 +34,6 @@ enum { E_CHILD = 0, E_OP = 1, E_ARITY = 2, E_TOKEN = 3, E_ROOT = 4, E_CYCLE = 5,
 const fold_status kErrStatus[E_NCLASS] = {FOLD_E_CHILD_RANGE, FOLD_E_OP_RANGE, FOLD_E_ARITY,
                                          FOLD_E_TOKEN_RANGE, FOLD_E_ROOT_RANGE, FOLD_E_CYCLE};
 
-constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 4096
 constexpr int kScanThreads = 1024;
 constexpr int kScanTile = kScanThreads * 4;
 constexpr int kPendingInvalid = 0x3fffffff;
@@ -43,12 +45,17 @@ inline int bits_for(int64_t maxval) {  // #bits to represent values in [0, maxva
 }
 
 // ---------------------------------------------------------------- workspace layout
+constexpr int kSchedThreads = 512;
+constexpr int kSchedWarps = kSchedThreads / 32;
+constexpr int kMaxBins = 1024;      // radix digit <= 10 bits
+constexpr int kMaxSchedBlocks = 512;
+constexpr int kSmallN = 16384;      // up to this many nodes: one block
+
 struct SchedWs {
-  int32_t *flags, *ncons, *pcons_off, *pcons, *pending, *q0, *q1;
+  int32_t *flags, *ncons, *fillc, *pcons_off, *pcons, *pending, *q0, *q1;
   uint32_t *ka, *kb;
   int32_t *va, *vb;
-  int32_t *hist, *scan_sums, *seg_flag, *seg_scan;
-  int nb;        // radix tiles for the largest sort (2N elements)
+  int32_t *hist, *tot, *bsums, *seg_flag, *seg_scan;
   size_t bytes;
 };
 
@@ -58,27 +65,25 @@ SchedWs sched_ws_layout(void *base, int64_t N, int64_t G) {
   SchedWs w{};
   int64_t M = 2 * N > G ? 2 * N : G;
   if (M < 1) M = 1;
-  w.nb = (int)cdiv(M, kSortTile);
-  int64_t scan_len_max = (int64_t)256 * w.nb;
-  if (scan_len_max < N + 1) scan_len_max = N + 1;
-  int64_t nsums = cdiv(scan_len_max, kScanTile) + 1;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return o; };
   size_t o_flags = take(F_NFLAGS * 4);
-  size_t o_ncons = take((N + 1) * 4), o_pco = take((N + 2) * 4), o_pc = take((2 * N + 1) * 4);
+  size_t o_ncons = take((N + 1) * 4), o_fill = take((N + 1) * 4), o_pco = take((N + 2) * 4);
+  size_t o_pc = take((2 * N + 1) * 4);
   size_t o_pend = take((N + 1) * 4), o_q0 = take((N + 1) * 4), o_q1 = take((N + 1) * 4);
   size_t o_ka = take((M + 1) * 4), o_kb = take((M + 1) * 4), o_va = take((M + 1) * 4), o_vb = take((M + 1) * 4);
-  size_t o_hist = take(scan_len_max * 4 + 4), o_sums = take(nsums * 4 * 2);
+  size_t o_hist = take((size_t)kMaxBins * kMaxSchedBlocks * 4), o_tot = take((kMaxBins + 1) * 4);
+  size_t o_bs = take((kMaxSchedBlocks + 1) * 4);
   size_t o_sf = take((N + 1) * 4), o_ss = take((N + 2) * 4);
   w.bytes = off;
   if (base) {
     char *b = (char *)base;
-    w.flags = (int32_t *)(b + o_flags); w.ncons = (int32_t *)(b + o_ncons);
+    w.flags = (int32_t *)(b + o_flags); w.ncons = (int32_t *)(b + o_ncons); w.fillc = (int32_t *)(b + o_fill);
     w.pcons_off = (int32_t *)(b + o_pco); w.pcons = (int32_t *)(b + o_pc);
     w.pending = (int32_t *)(b + o_pend); w.q0 = (int32_t *)(b + o_q0); w.q1 = (int32_t *)(b + o_q1);
     w.ka = (uint32_t *)(b + o_ka); w.kb = (uint32_t *)(b + o_kb);
     w.va = (int32_t *)(b + o_va); w.vb = (int32_t *)(b + o_vb);
-    w.hist = (int32_t *)(b + o_hist); w.scan_sums = (int32_t *)(b + o_sums);
+    w.hist = (int32_t *)(b + o_hist); w.tot = (int32_t *)(b + o_tot); w.bsums = (int32_t *)(b + o_bs);
     w.seg_flag = (int32_t *)(b + o_sf); w.seg_scan = (int32_t *)(b + o_ss);
   }
   return w;
@@ -182,357 +187,373 @@ fold_status excl_scan(const int32_t *in, int32_t *out, int64_t n, int32_t *sums,
   return FOLD_OK;
 }
 
-// ---------------------------------------------------------------- stable LSD radix sort
-// Sorts (key, val) pairs by key, stable, count read on device (*d_n <= n_max).
-__global__ void k_rs_hist(const uint32_t *keys, const int32_t *d_n, int shift, int32_t *hist, int nb) {
-  __shared__ int h[256];
-  int n = *d_n;
-  h[threadIdx.x] = 0;
-  __syncthreads();
-  int64_t base = (int64_t)blockIdx.x * kSortTile;
-  for (int i = threadIdx.x; i < kSortTile; i += kSortThreads) {
-    int64_t idx = base + i;
-    if (idx < n) atomicAdd(&h[(keys[idx] >> shift) & 255u], 1);
-  }
-  __syncthreads();
-  hist[(int64_t)threadIdx.x * nb + blockIdx.x] = h[threadIdx.x];
+// ---------------------------------------------------------------- the persistent kernel
+struct SchedArgs {
+  int N, G, V;
+  const int32_t *op, *child, *token, *root;
+  fold_schedule_t s;  // output arrays (device pointers)
+  SchedWs w;
+};
+
+__device__ __forceinline__ int ld_volatile(const int32_t *p) { return *(volatile const int32_t *)p; }
+__device__ __forceinline__ int ld_acq(const int32_t *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int dev_bits_for(int maxval) {  // #bits for values in [0, maxval], >= 1
+  int b = 32 - __clz(maxval > 0 ? maxval : 1);
+  return b < 1 ? 1 : b;
 }
 
-__global__ void k_rs_scatter(const uint32_t *kin, const int32_t *vin, const int32_t *d_n, int shift,
-                             const int32_t *hist_scan, int nb, uint32_t *kout, int32_t *vout) {
-  __shared__ int run[256];
-  __shared__ int wcnt[kSortThreads / 32][257];
-  __shared__ int base[256];
-  int n = *d_n;
-  int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  base[tid] = hist_scan[(int64_t)tid * nb + blockIdx.x];
-  run[tid] = 0;
-  for (int w = 0; w < kSortThreads / 32; w++) wcnt[w][tid] = 0;
+// Grid-wide barrier (all blocks co-resident: cooperative launch). Release: every thread's
+// prior writes are fenced before the block arrives; acquire: the waiting thread's
+// ld.acquire also invalidates this SM's L1, so later plain loads see other blocks' writes.
+__device__ void gsync(int32_t *flags) {
   __syncthreads();
-  int64_t tile0 = (int64_t)blockIdx.x * kSortTile;
-  if (tile0 >= n) return;
-  for (int round = 0; round < kSortItems; round++) {
-    int64_t idx = tile0 + (int64_t)round * kSortThreads + tid;
-    bool valid = idx < n;
-    uint32_t k = valid ? kin[idx] : 0u;
-    int v = valid ? vin[idx] : 0;
-    int d = valid ? (int)((k >> shift) & 255u) : 256;
-    unsigned peers = __match_any_sync(0xffffffffu, d);
-    int lrank = __popc(peers & lanemask_lt());
-    if (lrank == 0) wcnt[warp][d] = __popc(peers);
+  // one block: __syncthreads orders the block's global writes; data updated by atomics is
+  // never read through L1 before its phase's barrier (flags are read volatile)
+  if (gridDim.x == 1) return;
+  if (threadIdx.x == 0) {
+    int32_t *cnt = &flags[F_BAR], *gen = &flags[F_BAR + 1];
+    const int g = ld_acq(gen);
+    __threadfence();
+    if (atomicAdd(cnt, 1) == (int)gridDim.x - 1) {
+      atomicExch(cnt, 0);
+      __threadfence();
+      atomicAdd(gen, 1);
+    } else {
+      while (ld_acq(gen) == g) __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+
+// block-wide sum (any blockDim multiple of 32)
+__device__ int block_sum(int v, int *sw) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) sw[warp] = v;
+  __syncthreads();
+  int t = 0;
+  for (int i = 0; i < nw; i++) t += sw[i];
+  __syncthreads();
+  return t;
+}
+
+// Device-wide exclusive scan of in[0, n) into out (in place allowed), each block a
+// contiguous chunk; *total (nullable) receives the sum. Ends with a grid barrier.
+__device__ void grid_excl_scan(const int32_t *in, int32_t *out, int n, int32_t *total, SchedWs &w, int *sw) {
+  const int nb = gridDim.x, b = blockIdx.x, T = blockDim.x;
+  const int chunk = (int)round_up(cdiv(n, nb), (int64_t)T * 4);
+  const int lo = min(n, b * chunk), hi = min(n, lo + chunk);
+  int s = 0;
+  for (int i = lo + threadIdx.x; i < hi; i += T) s += in[i];
+  s = block_sum(s, sw);
+  if (threadIdx.x == 0) w.bsums[b] = s;
+  gsync(w.flags);
+  int p = 0;
+  for (int i = threadIdx.x; i < b; i += T) p += w.bsums[i];
+  int carry = block_sum(p, sw);
+  for (int t0 = lo; t0 < hi; t0 += T * 4) {
+    const int base = t0 + threadIdx.x * 4;
+    int v[4], sum = 0;
+#pragma unroll
+    for (int i = 0; i < 4; i++) { v[i] = base + i < hi ? in[base + i] : 0; sum += v[i]; }
+    int tot;
+    int ex = block_excl_scan(sum, sw, &tot) + carry;
+#pragma unroll
+    for (int i = 0; i < 4; i++) { if (base + i < hi) out[base + i] = ex; ex += v[i]; }
+    carry += tot;
+  }
+  if (b == nb - 1 && threadIdx.x == 0 && total) *total = carry;
+  gsync(w.flags);
+}
+
+// One stable counting pass: (kin, vin)[0, n) -> (kout, vout) ordered by the digit
+// (key >> shift) & (nbins - 1), ties in input order. nbins <= kMaxBins.
+// Shared memory: wcnt[kSchedWarps][nbins + 1], run[nbins], base[nbins].
+__device__ void sort_pass(const uint32_t *kin, const int32_t *vin, int n, int shift, int nbins, uint32_t *kout,
+                          int32_t *vout, SchedWs &w, int *dsm) {
+  const int nb = gridDim.x, b = blockIdx.x, T = blockDim.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  int *wcnt = dsm;                                   // [kSchedWarps][nbins + 1]
+  int *run = dsm + kSchedWarps * (nbins + 1);        // [nbins]
+  int *base = run + nbins;                           // [nbins]
+  const uint32_t mask = (uint32_t)nbins - 1u;
+  const int chunk = (int)round_up(cdiv(n, nb), T);
+  const int lo = min(n, b * chunk), hi = min(n, lo + chunk);
+  // 1. block histogram
+  for (int d = tid; d < nbins; d += T) run[d] = 0;
+  for (int i = tid; i < kSchedWarps * (nbins + 1); i += T) wcnt[i] = 0;
+  __syncthreads();
+  for (int i = lo + tid; i < hi; i += T) atomicAdd(&run[(kin[i] >> shift) & mask], 1);
+  __syncthreads();
+  for (int d = tid; d < nbins; d += T) w.hist[d * nb + b] = run[d];
+  gsync(w.flags);
+  // 2. per digit (one warp each): exclusive prefix over blocks, digit totals
+  for (int d = (b * T + tid) >> 5; d < nbins; d += (nb * T) >> 5) {
+    int carry = 0;
+    for (int b0 = 0; b0 < nb; b0 += 32) {
+      const int bb = b0 + lane;
+      const int t = bb < nb ? w.hist[d * nb + bb] : 0;
+      int x = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (bb < nb) w.hist[d * nb + bb] = carry + x - t;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) w.tot[d] = carry;
+  }
+  gsync(w.flags);
+  // 3. digit offsets (every block scans the totals), then the stable in-order scatter
+  {
+    int carry = 0;
+    for (int d0 = 0; d0 < nbins; d0 += T) {
+      const int d = d0 + tid;
+      const int v = d < nbins ? w.tot[d] : 0;
+      int tot;
+      const int ex = block_excl_scan(v, (int *)(base + nbins), &tot);  // scratch after base
+      if (d < nbins) base[d] = carry + ex + w.hist[d * nb + b];
+      carry += tot;
+    }
+    for (int d = tid; d < nbins; d += T) run[d] = 0;
+  }
+  __syncthreads();
+  for (int t0 = lo; t0 < hi; t0 += T) {
+    const int i = t0 + tid;
+    const bool valid = i < hi;
+    const uint32_t k = valid ? kin[i] : 0u;
+    const int v = valid ? vin[i] : 0;
+    const int d = valid ? (int)((k >> shift) & mask) : nbins;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const int lrank = __popc(peers & lanemask_lt());
+    const int cnt = __popc(peers);
+    if (lrank == 0) wcnt[warp * (nbins + 1) + d] = cnt;
     __syncthreads();
     if (valid) {
       int pre = 0;
-      for (int w = 0; w < warp; w++) pre += wcnt[w][d];
-      int pos = base[d] + run[d] + pre + lrank;
+      for (int ww = 0; ww < warp; ww++) pre += wcnt[ww * (nbins + 1) + d];
+      const int pos = base[d] + run[d] + pre + lrank;
       kout[pos] = k;
       vout[pos] = v;
     }
     __syncthreads();
-    {
-      int s = 0;
-#pragma unroll
-      for (int w = 0; w < kSortThreads / 32; w++) { s += wcnt[w][tid]; wcnt[w][tid] = 0; }
-      run[tid] += s;
-      if (tid == 0) for (int w = 0; w < kSortThreads / 32; w++) wcnt[w][256] = 0;
+    if (lrank == 0) {
+      if (valid) atomicAdd(&run[d], cnt);
+      wcnt[warp * (nbins + 1) + d] = 0;
     }
     __syncthreads();
-    if (tile0 + (int64_t)(round + 1) * kSortThreads >= n) break;
   }
+  gsync(w.flags);
 }
 
-// Sorts (ws.ka, ws.va) with *d_n valid entries by the low `nbits` bits of the keys.
-// Result pointers returned in *kres / *vres (either the a or b buffers).
-fold_status radix_sort(SchedWs &w, const int32_t *d_n, int64_t n_max, int nbits, uint32_t **kres,
-                       int32_t **vres, cudaStream_t st) {
+// Stable sort of (ka, va)[0, n) by the low nbits of the keys; result pointers in k / v.
+__device__ void sort_pairs(SchedWs &w, int n, int nbits, const uint32_t *&k, const int32_t *&v, int *dsm) {
   uint32_t *ki = w.ka, *ko = w.kb;
   int32_t *vi = w.va, *vo = w.vb;
-  int nb = (int)cdiv(n_max < 1 ? 1 : n_max, kSortTile);
-  for (int shift = 0; shift < nbits; shift += 8) {
-    k_rs_hist<<<nb, kSortThreads, 0, st>>>(ki, d_n, shift, w.hist, nb);
-    FOLD_LAUNCH_CHECK();
-    FOLD_TRY(excl_scan(w.hist, w.hist, (int64_t)256 * nb, w.scan_sums, nullptr, st));
-    k_rs_scatter<<<nb, kSortThreads, 0, st>>>(ki, vi, d_n, shift, w.hist, nb, ko, vo);
-    FOLD_LAUNCH_CHECK();
+  const int passes = (nbits + 9) / 10;
+  const int db = (nbits + passes - 1) / passes;
+  for (int p = 0; p < passes; p++) {
+    sort_pass(ki, vi, n, p * db, 1 << db, ko, vo, w, dsm);
     uint32_t *tk = ki; ki = ko; ko = tk;
     int32_t *tv = vi; vi = vo; vo = tv;
   }
-  *kres = ki;
-  *vres = vi;
-  return FOLD_OK;
+  k = ki;
+  v = vi;
 }
 
-// ---------------------------------------------------------------- validation / lists
-__global__ void k_validate(int N, int G, int V, const int32_t *op, const int32_t *child,
-                           const int32_t *token, const int32_t *root, int32_t *flags,
-                           int32_t *ncons, int32_t *pending) {
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
-    int n = (int)i;
-    int o = op[n], c0 = child[2 * n], c1 = child[2 * n + 1];
-    bool crange = (c0 < -1 || c0 >= N || c1 < -1 || c1 >= N);
+__device__ __forceinline__ bool any_input_error(const int32_t *flags) {
+  for (int e = 0; e < E_CYCLE; e++)
+    if (ld_volatile(&flags[F_ERR0 + e]) != INT_MAX) return true;
+  return false;
+}
+
+__global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
+  extern __shared__ int dsm[];
+  __shared__ int sw[32];
+  SchedWs &w = a.w;
+  fold_schedule_t &s = a.s;
+  int32_t *flags = w.flags;
+  const int N = a.N, G = a.G, V = a.V;
+  const int tid = threadIdx.x, T = blockDim.x;
+  const int64_t gtid = (int64_t)blockIdx.x * T + tid, gstride = (int64_t)gridDim.x * T;
+
+  // ---- P0: flags (barrier slots were zeroed by the host), counters
+  if (blockIdx.x == 0 && tid < F_NFLAGS && (tid < F_BAR || tid > F_BAR + 1))
+    flags[tid] = tid < E_NCLASS ? INT_MAX : 0;
+  for (int64_t i = gtid; i <= N; i += gstride) { w.ncons[i] = 0; w.fillc[i] = 0; }
+  gsync(flags);
+
+  // ---- P1: validate (classes in order CHILD_RANGE, OP_RANGE, ARITY, TOKEN_RANGE,
+  // ROOT_RANGE; smallest offending id), consumer counts, pending child counts
+  for (int64_t i = gtid; i < N; i += gstride) {
+    const int n = (int)i;
+    const int o = a.op[n], c0 = a.child[2 * n], c1 = a.child[2 * n + 1];
+    const bool crange = (c0 < -1 || c0 >= N || c1 < -1 || c1 >= N);
     if (crange) atomicMin(&flags[F_ERR0 + E_CHILD], n);
-    bool orange = (o != FOLD_OP_EMBED && o != FOLD_OP_CELL);
-    if (orange) atomicMin(&flags[F_ERR0 + E_OP], n);
-    bool ar_ok = (o == FOLD_OP_EMBED) ? (c0 == -1 && c1 == -1) : (c0 >= 0 && c1 >= 0);
+    if (o != FOLD_OP_EMBED && o != FOLD_OP_CELL) atomicMin(&flags[F_ERR0 + E_OP], n);
+    const bool ar_ok = (o == FOLD_OP_EMBED) ? (c0 == -1 && c1 == -1) : (c0 >= 0 && c1 >= 0);
     if (!ar_ok) atomicMin(&flags[F_ERR0 + E_ARITY], n);
-    if (o == FOLD_OP_EMBED && (token[n] < 0 || token[n] >= V)) atomicMin(&flags[F_ERR0 + E_TOKEN], n);
-    bool good_cell = (o == FOLD_OP_CELL) && !crange && c0 >= 0 && c1 >= 0;
-    if (good_cell) { atomicAdd(&ncons[c0], 1); atomicAdd(&ncons[c1], 1); }
-    pending[n] = (o == FOLD_OP_CELL) ? (good_cell ? 2 : kPendingInvalid) : 0;
+    if (o == FOLD_OP_EMBED && (a.token[n] < 0 || a.token[n] >= V)) atomicMin(&flags[F_ERR0 + E_TOKEN], n);
+    const bool good_cell = (o == FOLD_OP_CELL) && !crange && c0 >= 0 && c1 >= 0;
+    if (good_cell) { atomicAdd(&w.ncons[c0], 1); atomicAdd(&w.ncons[c1], 1); }
+    w.pending[n] = (o == FOLD_OP_CELL) ? (good_cell ? 2 : kPendingInvalid) : 0;
   }
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += stride)
-    if (root[g] < 0 || root[g] >= N) atomicMin(&flags[F_ERR0 + E_ROOT], (int)g);
-}
+  for (int64_t g = gtid; g < G; g += gstride)
+    if (a.root[g] < 0 || a.root[g] >= N) atomicMin(&flags[F_ERR0 + E_ROOT], (int)g);
+  gsync(flags);
+  if (any_input_error(flags)) return;  // uniform: every block reads the same flags
 
-// parents list (unordered within a node) + initial frontier (EMBED nodes, depth 1)
-__global__ void k_fill_parents(int N, const int32_t *op, const int32_t *child, const int32_t *pcons_off,
-                               int32_t *fillc, int32_t *pcons, int32_t *depth, int32_t *q0,
-                               int32_t *flags) {
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t nloop = cdiv(N, stride) * stride;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nloop; i += stride) {
-    bool in = i < N;
-    int n = (int)i;
-    bool leaf = false;
-    if (in) {
-      int o = op[n], c0 = child[2 * n], c1 = child[2 * n + 1];
-      bool good_cell = (o == FOLD_OP_CELL) && c0 >= 0 && c0 < N && c1 >= 0 && c1 < N;
-      if (good_cell) {
-        pcons[pcons_off[c0] + atomicAdd(&fillc[c0], 1)] = n;
-        pcons[pcons_off[c1] + atomicAdd(&fillc[c1], 1)] = n;
+  // ---- P2: parent-list offsets
+  grid_excl_scan(w.ncons, w.pcons_off, N + 1, nullptr, w, sw);
+
+  // ---- P3: parent lists (unordered within a node), initial frontier = EMBED nodes (depth 1)
+  {
+    const int64_t nloop = cdiv(N, gstride) * gstride;
+    for (int64_t i = gtid; i < nloop; i += gstride) {
+      const bool in = i < N;
+      const int n = (int)i;
+      bool leaf = false;
+      if (in) {
+        const int o = a.op[n], c0 = a.child[2 * n], c1 = a.child[2 * n + 1];
+        if (o == FOLD_OP_CELL) {
+          w.pcons[w.pcons_off[c0] + atomicAdd(&w.fillc[c0], 1)] = n;
+          w.pcons[w.pcons_off[c1] + atomicAdd(&w.fillc[c1], 1)] = n;
+        }
+        leaf = (o == FOLD_OP_EMBED);
+        s.depth[n] = leaf ? 1 : -1;
       }
-      leaf = (o == FOLD_OP_EMBED);
-      depth[n] = leaf ? 1 : -1;
+      const int slot = warp_push(&flags[F_QCNT + 1], leaf);
+      if (leaf) w.q0[slot] = n;
+      const int nl = __popc(__ballot_sync(0xffffffffu, leaf));
+      if ((tid & 31) == 0 && nl) atomicAdd(&flags[F_NLEAVES], nl);
     }
-    int slot = warp_push(&flags[F_QCNT + 1], leaf);
-    if (leaf) q0[slot] = n;
-    int nl = __popc(__ballot_sync(0xffffffffu, leaf));
-    if ((threadIdx.x & 31) == 0 && nl) atomicAdd(&flags[F_NLEAVES], nl);
   }
-}
+  gsync(flags);
 
-__device__ __forceinline__ int ld_volatile(const int32_t *p) { return *(volatile const int32_t *)p; }
-
-__device__ void grid_barrier(int32_t *flags) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile int32_t *gen = &flags[F_BAR + 1];
-    int g = *gen;
-    __threadfence();
-    if (atomicAdd(&flags[F_BAR], 1) == (int)gridDim.x - 1) {
-      atomicExch(&flags[F_BAR], 0);
-      __threadfence();
-      atomicAdd((int32_t *)gen, 1);
-    } else {
-      while (*gen == g) __nanosleep(40);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
-// Level-synchronous depth propagation. Frontier_1 = EMBED nodes; a
-// parent whose last pending child finishes at level L gets depth L+1. One grid
-// barrier per level; must be launched cooperatively (all blocks co-resident).
-__global__ void k_depth_frontier(const int32_t *pcons_off, const int32_t *pcons, int32_t *pending,
-                                 int32_t *depth, int32_t *q0, int32_t *q1, int32_t *flags) {
-  int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // ---- P4: level-synchronous depth propagation: a parent whose last
+  // pending child finishes at level L gets depth L + 1; one barrier per level
   int L = 1;
   for (;; L++) {
-    int ncur = ld_volatile(&flags[F_QCNT + (L % 3)]);
+    const int ncur = ld_volatile(&flags[F_QCNT + (L % 3)]);
     if (ncur == 0) break;
-    const int32_t *cur = (L & 1) ? q0 : q1;
-    int32_t *nxt = (L & 1) ? q1 : q0;
+    const int32_t *cur = (L & 1) ? w.q0 : w.q1;
+    int32_t *nxt = (L & 1) ? w.q1 : w.q0;
     if (gtid == 0) flags[F_QCNT + ((L + 2) % 3)] = 0;
-    int64_t nloop = cdiv(ncur, stride) * stride;
-    for (int64_t i = gtid; i < nloop; i += stride) {
-      bool in = i < ncur;
-      int x = in ? ld_volatile(&cur[i]) : 0;
-      int e0 = in ? pcons_off[x] : 0, e1 = in ? pcons_off[x + 1] : 0;
+    const int64_t nloop = cdiv(ncur, gstride) * gstride;
+    for (int64_t i = gtid; i < nloop; i += gstride) {
+      const bool in = i < ncur;
+      const int x = in ? cur[i] : 0;
+      const int e0 = in ? w.pcons_off[x] : 0, e1 = in ? w.pcons_off[x + 1] : 0;
       for (int j = 0; __any_sync(0xffffffffu, e0 + j < e1); j++) {
         bool act = false;
         int p = 0;
         if (e0 + j < e1) {
-          p = pcons[e0 + j];
-          act = (atomicSub(&pending[p], 1) == 1);
-          if (act) depth[p] = L + 1;
+          p = w.pcons[e0 + j];
+          act = (atomicSub(&w.pending[p], 1) == 1);
+          if (act) s.depth[p] = L + 1;
         }
-        int slot = warp_push(&flags[F_QCNT + ((L + 1) % 3)], act);
+        const int slot = warp_push(&flags[F_QCNT + ((L + 1) % 3)], act);
         if (act) nxt[slot] = p;
       }
     }
-    grid_barrier(flags);
+    gsync(flags);
   }
-  if (gtid == 0) flags[F_MAXDEPTH] = L - 1;
-}
+  const int D = L - 1;
+  if (gtid == 0) flags[F_MAXDEPTH] = D;
 
-__global__ void k_post_depth(int N, const int32_t *op, const int32_t *depth, int32_t *flags,
-                             uint32_t *keys, int32_t *vals) {
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
-    int n = (int)i, d = depth[n];
+  // ---- P5: sort keys (cycle: a node never reached keeps depth -1)
+  for (int64_t i = gtid; i < N; i += gstride) {
+    const int n = (int)i, d = s.depth[n];
     if (d < 0) atomicMin(&flags[F_ERR0 + E_CYCLE], n);
-    keys[n] = (uint32_t)(2 * (d < 0 ? 0 : d) + (op[n] & 1));
-    vals[n] = n;
+    w.ka[n] = (uint32_t)(2 * (d < 0 ? 0 : d) + (a.op[n] & 1));
+    w.va[n] = n;
   }
-}
+  gsync(flags);
+  if (ld_volatile(&flags[F_ERR0 + E_CYCLE]) != INT_MAX) return;
 
-// perm/rank + group_off/level_off by binary search over the sorted keys
-__global__ void k_perm_offsets(int N, const uint32_t *skeys, const int32_t *svals, const int32_t *flags,
-                               int32_t *perm, int32_t *rank, int32_t *group_off, int32_t *level_off) {
-  int D = flags[F_MAXDEPTH];
-  int nk = 2 * (D + 1);
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
-    int n = svals[i];
-    perm[i] = n;
-    rank[n] = (int)i;
+  // ---- P6: stable sort by key = 2 depth + op (L42-43); ties keep ascending node id
+  const int nk = 2 * (D + 1);
+  const uint32_t *sk;
+  const int32_t *sv;
+  sort_pairs(w, N, dev_bits_for(nk - 1), sk, sv, dsm);
+
+  // ---- P7: perm / rank, group and level offsets (binary search over the sorted keys)
+  for (int64_t i = gtid; i < N; i += gstride) {
+    const int n = sv[i];
+    s.perm[i] = n;
+    s.rank[n] = (int)i;
   }
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k <= nk; k += stride) {
+  for (int64_t k = gtid; k <= nk; k += gstride) {
     int lo = 0, hi = N;
-    while (lo < hi) { int mid = (lo + hi) >> 1; if ((int)skeys[mid] < (int)k) lo = mid + 1; else hi = mid; }
-    group_off[k] = lo;
-    if ((k & 1) == 0) level_off[k >> 1] = lo;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if ((int)sk[mid] < (int)k) lo = mid + 1; else hi = mid; }
+    s.group_off[k] = lo;
+    if ((k & 1) == 0) s.level_off[k >> 1] = lo;
   }
-}
+  gsync(flags);
 
-__global__ void k_gather(int N, const int32_t *op, const int32_t *child, const int32_t *perm,
-                         const int32_t *rank, int32_t *gather) {
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += stride) {
-    int n = perm[r];
-    int c0 = child[2 * n], c1 = child[2 * n + 1];
-    bool cell = op[n] == FOLD_OP_CELL;
-    // out-of-range children are reported by k_validate; never index with them
-    gather[2 * r] = (cell && c0 >= 0 && c0 < N) ? rank[c0] : -1;
-    gather[2 * r + 1] = (cell && c1 >= 0 && c1 < N) ? rank[c1] : -1;
+  // ---- P8: gather vectors (L44: the indices encode the topology)
+  for (int64_t r = gtid; r < N; r += gstride) {
+    const int n = s.perm[r];
+    const bool cell = a.op[n] == FOLD_OP_CELL;
+    s.gather[2 * r] = cell ? s.rank[a.child[2 * n]] : -1;
+    s.gather[2 * r + 1] = cell ? s.rank[a.child[2 * n + 1]] : -1;
   }
-}
+  gsync(flags);
 
-// cell edges e in [0, 2 n_cells): key = child row, val = e; count = 2 (N - n_leaves)
-__global__ void k_cons_keys(int N, const int32_t *gather, int32_t *flags, int32_t *d_count,
-                            uint32_t *keys, int32_t *vals) {
-  int nl = flags[F_NLEAVES];
-  int cnt = 2 * (N - nl);
-  if (blockIdx.x == 0 && threadIdx.x == 0) *d_count = cnt;
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += stride) {
-    keys[e] = (uint32_t)gather[2 * (int64_t)nl + e];
-    vals[e] = (int)e;
+  // ---- P9: consumer CSR: cell edges e in [0, 2 n_cells), key = child row, stable
+  const int nl = ld_volatile(&flags[F_NLEAVES]);
+  const int ne = 2 * (N - nl);
+  for (int64_t e = gtid; e < ne; e += gstride) {
+    w.ka[e] = (uint32_t)s.gather[2 * (int64_t)nl + e];
+    w.va[e] = (int)e;
   }
-}
-
-__global__ void k_cons_finish(int N, const uint32_t *skeys, const int32_t *svals, const int32_t *d_count,
-                              int32_t *cons_off, int32_t *cons_edge) {
-  int cnt = *d_count;
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += stride)
-    cons_edge[i] = svals[i];
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= N; r += stride) {
-    int lo = 0, hi = cnt;
-    while (lo < hi) { int mid = (lo + hi) >> 1; if ((int)skeys[mid] < (int)r) lo = mid + 1; else hi = mid; }
-    cons_off[r] = lo;
+  gsync(flags);
+  sort_pairs(w, ne, dev_bits_for(N - 1), sk, sv, dsm);
+  for (int64_t i = gtid; i < ne; i += gstride) s.cons_edge[i] = sv[i];
+  for (int64_t r = gtid; r <= N; r += gstride) {
+    int lo = 0, hi = ne;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if ((int)sk[mid] < (int)r) lo = mid + 1; else hi = mid; }
+    s.cons_off[r] = lo;
   }
-}
+  gsync(flags);
 
-// leaves (rows [0, n_leaves)) keyed by token
-__global__ void k_leaf_keys(const int32_t *token, const int32_t *perm, const int32_t *flags,
-                            int32_t *d_count, uint32_t *keys, int32_t *vals, int32_t *leaf_token) {
-  int nl = flags[F_NLEAVES];
-  if (blockIdx.x == 0 && threadIdx.x == 0) *d_count = nl;
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += stride) {
-    int t = token[perm[r]];
-    keys[r] = (uint32_t)t;
-    vals[r] = (int)r;
-    leaf_token[r] = t;
+  // ---- P10: leaves by (token, row) and token segments
+  for (int64_t r = gtid; r < nl; r += gstride) {
+    const int t = a.token[s.perm[r]];
+    w.ka[r] = (uint32_t)t;
+    w.va[r] = (int)r;
+    s.leaf_token[r] = t;
   }
-}
-
-__global__ void k_seg_flags(int N, const uint32_t *skeys, const int32_t *svals, const int32_t *d_count,
-                            int32_t *leaf_perm, int32_t *seg_flag) {
-  int cnt = *d_count;
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
-    bool in = i < cnt;
-    if (in) leaf_perm[i] = svals[i];
-    seg_flag[i] = (in && (i == 0 || skeys[i] != skeys[i - 1])) ? 1 : 0;
+  gsync(flags);
+  sort_pairs(w, nl, dev_bits_for(V - 1), sk, sv, dsm);
+  for (int64_t i = gtid; i < nl; i += gstride) {
+    s.leaf_perm[i] = sv[i];
+    w.seg_flag[i] = (i == 0 || sk[i] != sk[i - 1]) ? 1 : 0;
   }
-}
+  gsync(flags);
+  grid_excl_scan(w.seg_flag, w.seg_scan, nl, &flags[F_NSEG], w, sw);
+  for (int64_t i = gtid; i < nl; i += gstride)
+    if (w.seg_flag[i]) s.tok_seg[w.seg_scan[i]] = (int)i;
+  if (gtid == 0) s.tok_seg[ld_volatile(&flags[F_NSEG])] = nl;
 
-__global__ void k_seg_write(int N, const int32_t *seg_flag, const int32_t *seg_scan, const int32_t *d_count,
-                            const int32_t *flags, int32_t *tok_seg) {
-  int cnt = *d_count;
-  int nseg = flags[F_NSEG];
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += stride)
-    if (seg_flag[i]) tok_seg[seg_scan[i]] = (int)i;
-  if (blockIdx.x == 0 && threadIdx.x == 0) tok_seg[nseg] = cnt;
-}
-
-__global__ void k_root_keys(int N, int G, const int32_t *root, const int32_t *rank, int32_t *root_row,
-                            uint32_t *keys, int32_t *vals) {
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += stride) {
-    int ro = root[g];
-    int rr = (ro >= 0 && ro < N) ? rank[ro] : 0;  // invalid roots are reported by k_validate
-    root_row[g] = rr;
-    keys[g] = (uint32_t)rr;
-    vals[g] = (int)g;
-  }
-}
-
-// Stable sort of graph ids by root row for G <= 4096 in one block: bitonic sort of the
-// unique composite keys (root_row << 32 | g), so ties keep ascending g.
-constexpr int kSmallRoots = 4096;
-__global__ void k_roots_small(int N, int G, const int32_t *root, const int32_t *rank, int32_t *root_row,
-                              int32_t *root_perm) {
-  __shared__ unsigned long long key[kSmallRoots];
-  int n2 = 1;
-  while (n2 < G) n2 <<= 1;
-  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-    if (i < G) {
-      int ro = root[i];
-      int rr = (ro >= 0 && ro < N) ? rank[ro] : 0;  // invalid roots are reported by k_validate
-      root_row[i] = rr;
-      key[i] = ((unsigned long long)(unsigned)rr << 32) | (unsigned)i;
-    } else {
-      key[i] = ~0ull;
+  // ---- P11: roots, and graph ids ordered by (root row, g)
+  if (G > 0) {
+    for (int64_t g = gtid; g < G; g += gstride) {
+      const int rr = s.rank[a.root[g]];
+      s.root_row[g] = rr;
+      w.ka[g] = (uint32_t)rr;
+      w.va[g] = (int)g;
     }
+    gsync(flags);
+    sort_pairs(w, G, dev_bits_for(N - 1), sk, sv, dsm);
+    for (int64_t g = gtid; g < G; g += gstride) s.root_perm[g] = sv[g];
   }
-  __syncthreads();
-  for (int k = 2; k <= n2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-        int ixj = i ^ j;
-        if (ixj > i) {
-          unsigned long long a = key[i], b = key[ixj];
-          bool up = (i & k) == 0;
-          if ((a > b) == up) { key[i] = b; key[ixj] = a; }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (int i = threadIdx.x; i < G; i += blockDim.x) root_perm[i] = (int32_t)(key[i] & 0xffffffffu);
-}
-
-__global__ void k_copy_i32(const int32_t *src, int32_t *dst, int64_t n) {
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[i];
-}
-
-__global__ void k_init_flags(int32_t *flags, int N, int G) {
-  int t = threadIdx.x;
-  if (t < F_NFLAGS) flags[t] = (t < E_NCLASS) ? INT_MAX : (t == 20 ? N : (t == 23 ? G : 0));
-}
-
-inline unsigned grid_for(int64_t n, int threads = 256) {
-  int64_t b = cdiv(n < 1 ? 1 : n, threads);
-  if (b > 148 * 16) b = 148 * 16;
-  return (unsigned)b;
 }
 
 }  // namespace
@@ -574,84 +595,28 @@ fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr
   SchedWs w = sched_ws_layout(ws_ptr, N, G);
   if (!ws_ptr || ws_bytes < w.bytes) return FOLD_E_WORKSPACE;
 
-  // ---- validate, consumer counts, pending counts
-  k_init_flags<<<1, F_NFLAGS, 0, st>>>(w.flags, N, G);
-  FOLD_LAUNCH_CHECK();
-  FOLD_CUDA_TRY(cudaMemsetAsync(w.ncons, 0, (size_t)(N + 1) * 4, st));
-  k_validate<<<grid_for(N > G ? N : G), 256, 0, st>>>(N, G, V, gr->op, gr->child, gr->token, gr->root,
-                                                       w.flags, w.ncons, w.pending);
-  FOLD_LAUNCH_CHECK();
-  FOLD_TRY(excl_scan(w.ncons, w.pcons_off, N + 1, w.scan_sums, nullptr, st));
-  FOLD_CUDA_TRY(cudaMemsetAsync(w.ncons, 0, (size_t)(N + 1) * 4, st));  // reuse as fill counters
-  k_fill_parents<<<grid_for(N), 256, 0, st>>>(N, gr->op, gr->child, w.pcons_off, w.ncons, w.pcons,
-                                               s->depth, w.q0, w.flags);
-  FOLD_LAUNCH_CHECK();
-
-  // ---- depth frontier (cooperative: all blocks resident for the grid barrier)
-  {
-    static thread_local int occ = 0, nsm = 0;
-    if (!occ) {
-      int dev;
-      FOLD_CUDA_TRY(cudaGetDevice(&dev));
-      FOLD_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-      FOLD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_depth_frontier, 256, 0));
-      if (occ < 1) occ = 1;
-    }
-    int64_t want = cdiv(N, 256);
-    int64_t cap = (int64_t)nsm * (occ < 2 ? occ : 2);
-    int blocks = (int)(want < cap ? want : cap);
-    if (blocks < 1) blocks = 1;
-    const int32_t *a0 = w.pcons_off, *a1 = w.pcons;
-    int32_t *a2 = w.pending, *a3 = s->depth, *a4 = w.q0, *a5 = w.q1, *a6 = w.flags;
-    void *args[] = {(void *)&a0, (void *)&a1, (void *)&a2, (void *)&a3, (void *)&a4, (void *)&a5, (void *)&a6};
-    FOLD_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_depth_frontier, dim3(blocks), dim3(256), args, 0, st));
-    g_launches++;
+  // grid: one block for small batches, else enough blocks for ~2K nodes each, all
+  // co-resident (cooperative launch)
+  const size_t dsmem = (size_t)(kSchedWarps * (kMaxBins + 1) + 2 * kMaxBins + 64) * sizeof(int);
+  static thread_local int max_blocks = 0;
+  if (!max_blocks) {
+    int dev, nsm, occ = 0;
+    FOLD_CUDA_TRY(cudaGetDevice(&dev));
+    FOLD_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    FOLD_CUDA_TRY(cudaFuncSetAttribute(k_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
+    FOLD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_schedule, kSchedThreads, dsmem));
+    if (occ < 1) occ = 1;
+    max_blocks = nsm * (occ < 2 ? occ : 2);
+    if (max_blocks > kMaxSchedBlocks) max_blocks = kMaxSchedBlocks;
   }
-  k_post_depth<<<grid_for(N), 256, 0, st>>>(N, gr->op, s->depth, w.flags, w.ka, w.va);
+  int blocks = N <= kSmallN ? 1 : (int)cdiv(N, 2048);
+  if (blocks > max_blocks) blocks = max_blocks;
+  FOLD_CUDA_TRY(cudaMemsetAsync(w.flags + F_BAR, 0, 2 * sizeof(int32_t), st));
+  SchedArgs args{N, G, V, gr->op, gr->child, gr->token, gr->root, *s, w};
+  void *kargs[] = {(void *)&args};
+  FOLD_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_schedule, dim3(blocks), dim3(kSchedThreads), kargs,
+                                            dsmem, st));
   FOLD_LAUNCH_CHECK();
-
-  // ---- stable sort by key = 2*depth + op (ties by node id: input order is id order)
-  // count pointer: a constant N lives in the flags scratch slot 20
-  int32_t *d_N = w.flags + 20, *d_cnt = w.flags + 21;  // flags[20] = N (k_init_flags)
-  uint32_t *sk;
-  int32_t *sv;
-  FOLD_TRY(radix_sort(w, d_N, N, bits_for(2 * (int64_t)N + 1), &sk, &sv, st));
-  k_perm_offsets<<<grid_for(2 * (int64_t)N + 3), 256, 0, st>>>(N, sk, sv, w.flags, s->perm, s->rank,
-                                                                s->group_off, s->level_off);
-  FOLD_LAUNCH_CHECK();
-  k_gather<<<grid_for(N), 256, 0, st>>>(N, gr->op, gr->child, s->perm, s->rank, s->gather);
-  FOLD_LAUNCH_CHECK();
-
-  // ---- consumer CSR: cell edges sorted (stably) by child row
-  k_cons_keys<<<grid_for(2 * (int64_t)N), 256, 0, st>>>(N, s->gather, w.flags, d_cnt, w.ka, w.va);
-  FOLD_LAUNCH_CHECK();
-  FOLD_TRY(radix_sort(w, d_cnt, 2 * (int64_t)N, bits_for(N), &sk, &sv, st));
-  k_cons_finish<<<grid_for(2 * (int64_t)N + 1), 256, 0, st>>>(N, sk, sv, d_cnt, s->cons_off, s->cons_edge);
-  FOLD_LAUNCH_CHECK();
-
-  // ---- leaves by (token, row) and token segments
-  int32_t *d_cnt2 = w.flags + 22;
-  k_leaf_keys<<<grid_for(N), 256, 0, st>>>(gr->token, s->perm, w.flags, d_cnt2, w.ka, w.va, s->leaf_token);
-  FOLD_LAUNCH_CHECK();
-  FOLD_TRY(radix_sort(w, d_cnt2, N, bits_for(V > 0 ? V - 1 : 0), &sk, &sv, st));
-  k_seg_flags<<<grid_for(N), 256, 0, st>>>(N, sk, sv, d_cnt2, s->leaf_perm, w.seg_flag);
-  FOLD_LAUNCH_CHECK();
-  FOLD_TRY(excl_scan(w.seg_flag, w.seg_scan, N, w.scan_sums, w.flags + F_NSEG, st));
-  k_seg_write<<<grid_for(N), 256, 0, st>>>(N, w.seg_flag, w.seg_scan, d_cnt2, w.flags, s->tok_seg);
-  FOLD_LAUNCH_CHECK();
-
-  // ---- roots
-  if (G > 0 && G <= kSmallRoots) {
-    k_roots_small<<<1, 1024, 0, st>>>(N, G, gr->root, s->rank, s->root_row, s->root_perm);
-    FOLD_LAUNCH_CHECK();
-  } else if (G > 0) {
-    int32_t *d_G = w.flags + 23;  // flags[23] = G (k_init_flags)
-    k_root_keys<<<grid_for(G), 256, 0, st>>>(N, G, gr->root, s->rank, s->root_row, w.ka, w.va);
-    FOLD_LAUNCH_CHECK();
-    FOLD_TRY(radix_sort(w, d_G, G, bits_for(N), &sk, &sv, st));
-    k_copy_i32<<<grid_for(G), 256, 0, st>>>(sv, s->root_perm, G);
-    FOLD_LAUNCH_CHECK();
-  }
 
   // ---- the one host sync: flags + level_off prefix
   int32_t hflags[F_NFLAGS];
