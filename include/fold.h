@@ -115,6 +115,8 @@ typedef struct {
           *leaf_perm, *tok_seg, *root_row, *root_perm, *leaf_token;
   int32_t *level_off_host;
   int32_t n_nodes, n_graphs, n_levels, n_leaves, n_cells, n_tok_segs;
+  int32_t tree_like;  /* output: 1 if every pool row is read by at most one cell edge and the
+                         rows read by none are exactly the (unconsumed) roots */
 } fold_schedule_t;
 
 /* Workspace bytes fold_schedule needs for n_nodes / n_graphs (device scratch). */

@@ -234,17 +234,24 @@ __global__ void k_cell_bwd_pw(int r0, int r1, int nl, int S, int ld, int ld_g, c
                               const int32_t *__restrict__ root_perm, int G, const float *__restrict__ dh_root,
                               const float *__restrict__ dc_root, const int32_t *__restrict__ gather,
                               const T *__restrict__ Gact, const float *__restrict__ C, const float *__restrict__ dA,
-                              float *__restrict__ dCe, T *__restrict__ dZ, int ld_z) {
+                              float *__restrict__ dCe, T *__restrict__ dZ, int ld_z, const int32_t *__restrict__ root_row) {
   using IT = VecIO<T, VEC>;
   using IF = VecIO<float, VEC>;
   int lane = threadIdx.x & 31;
   int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  // warp task = (row, block of 32*VEC columns): narrow levels still spread over all SMs
+  // warp task = (row, block of 32*VEC columns): narrow levels still spread over all SMs.
+  // Root mode (root_row != null): the rows are the distinct cell root rows, visited in
+  // root_perm order (index i in [r0, r1) = [0, G)).
   const int nblk = (int)cdiv(S, 32 * VEC);
   const int64_t ntask = (int64_t)(r1 - r0) * nblk;
   for (int64_t task = w; task < ntask; task += nw) {
-    const int64_t r = r0 + task / nblk;
+    int64_t r = r0 + task / nblk;
+    if (root_row) {
+      const int q = (int)r;
+      r = root_row[root_perm[q]];
+      if (r < nl || (q > 0 && root_row[root_perm[q - 1]] == r)) continue;
+    }
     const int j = (int)(task % nblk) * 32 * VEC + lane * VEC;
     int64_t c = r - nl;
     int e0 = cons_off[r], e1 = cons_off[r + 1];
@@ -652,13 +659,13 @@ fold_status launch_cell_bwd_pw(bool bf16, int cell, int r0, int r1, int nl, int 
                                const int32_t *cons_off, const int32_t *cons_edge, const int32_t *root_off,
                                const int32_t *root_perm, int G, const float *dh_root, const float *dc_root,
                                const int32_t *gather, const void *Gact, const float *C, const float *dA, float *dCe,
-                               void *dZ, int ld_z, cudaStream_t st) {
+                               void *dZ, int ld_z, cudaStream_t st, const int32_t *root_row) {
   if (r1 <= r0) return FOLD_OK;
   const int vec = (S & 3) == 0 ? 4 : 1;
   unsigned g = grid_cap(cdiv((int64_t)(r1 - r0) * cdiv(S, 32 * vec) * 32, 256));
 #define PW_ARGS r0, r1, nl, S, ld, ld_g, cons_off, cons_edge, root_off, root_perm, G, dh_root, dc_root, gather
 #define PW_LAUNCH(T, GT, VEC) \
-  k_cell_bwd_pw<T, GT, VEC><<<g, 256, 0, st>>>(PW_ARGS, (const T *)Gact, C, dA, dCe, (T *)dZ, ld_z)
+  k_cell_bwd_pw<T, GT, VEC><<<g, 256, 0, st>>>(PW_ARGS, (const T *)Gact, C, dA, dCe, (T *)dZ, ld_z, root_row)
   const bool v4 = (S & 3) == 0;
   const bool lstm = cell == FOLD_CELL_TREELSTM;
   if (bf16) {

@@ -38,7 +38,8 @@ fold_status launch_cell_bwd_pw(bool bf16, int cell, int r0, int r1, int nl, int 
                                const int32_t *cons_off, const int32_t *cons_edge, const int32_t *root_off,
                                const int32_t *root_perm, int G, const float *dh_root, const float *dc_root,
                                const int32_t *gather, const void *Gact, const float *C, const float *dA,
-                               float *dCe, void *dZ, int ld_z, cudaStream_t st);
+                               float *dCe, void *dZ, int ld_z, cudaStream_t st,
+                               const int32_t *root_row = nullptr);  // root mode: rows = distinct root rows, [r0,r1)=[0,G)
 // dA[rows][2S] (edge-indexed, fp32) = dZ[rows][gates*S] * U[gates*S][2S]
 fold_status launch_gemm_dA_simt(int M, int S, int gates, const float *dZ, int ld_z, const float *U,
                                 float *dA, cudaStream_t st);
@@ -96,6 +97,19 @@ struct TcFwdArgs {
   int *done;                       // [D + 2] level completion counters (workspace)
 };
 fold_status tc_fwd_levels(int cell, const TcFwdArgs &a, cudaStream_t st);
+// Tree-like schedules: the dA GEMM of every level in one persistent launch, each tile's
+// epilogue running the children's backward pointwise step (dZ, dCe); dA kept for leaves.
+struct TcBwdArgs {
+  const int32_t *level_off, *level_off_host;
+  int D, S, nl, n_cells, ld, ld_g, ld_z;
+  const int32_t *gather;
+  const __nv_bfloat16 *Ub, *Gact;
+  const float *C;
+  float *dA, *dCe;
+  __nv_bfloat16 *dZ;
+  int *done;  // [D + 2]
+};
+fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st);
 fold_status tc_gemm_dA(int c0, int M, int n_cells, int S, int gates, const __nv_bfloat16 *dZ, int ld_z,
                        const __nv_bfloat16 *Ub, float *dA, cudaStream_t st);
 // split-K over cells into split_ws [splits][gates*S][2S] (fp32), then a fixed-order sum

@@ -567,6 +567,277 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc2(tbase, 512); }
 }
 
+// =================================================================== backward: all cell levels
+// Tree-like schedules (every row read by at most one edge, unread rows = roots): ONE
+// persistent launch runs the dA GEMM of every level d = D..2 (the reverse
+// sweep), and each tile's epilogue turns the edge gradients dA[e] straight into the child's
+// backward pointwise step -- for edge e = (cell c, slot k) with child x (its single
+// consumer is e): dh(x) = dA[e], dc(x) = dCe[e] (written by c's own pointwise step), then
+// dz(x) -> dZ row of x and dCe of x's two edges. The dA rows never reach memory except for
+// leaf children (the embedding gradient reads them). Level d's tiles wait on a device
+// counter for level d+1, whose epilogues completed every dZ row of level d. Roots' dZ come
+// from a seeded pointwise pass launched before.
+// Epilogue layout: each warp owns 32 accumulator rows; per 64-column slab it moves the
+// fp32 values TMEM -> registers -> a padded smem transpose, then walks the rows with the
+// 32 lanes across columns, so every global access of the pointwise step is a coalesced
+// row segment.
+struct BwdLevels {
+  const int32_t *lo;
+  int D, S, nl;
+};
+struct BwdCursor {  // walks levels D, D-1, ..., 2 in tile order
+  int d, t0, nt, prev_nt, r0, r1;
+  __device__ void load(const BwdLevels &L, int NTn) {
+    r0 = __ldg(L.lo + d); r1 = __ldg(L.lo + d + 1);
+    nt = (int)cdiv(r1 - r0, PM) * NTn;
+  }
+  __device__ void init(const BwdLevels &L, int NTn) { d = L.D; t0 = 0; prev_nt = 0; load(L, NTn); }
+  __device__ void seek(const BwdLevels &L, int NTn, int T) {
+    while (T >= t0 + nt) { t0 += nt; prev_nt = nt; d--; load(L, NTn); }
+  }
+};
+
+constexpr int BW_ST = 4;
+constexpr int BW_EPI = 8;                       // epilogue warps
+constexpr int BW_THREADS = 128 + 32 * BW_EPI;
+constexpr int BW_XS = 32 * 66;                  // floats per warp transpose buffer (32 x 64, padded)
+constexpr int BW_SMEM = BW_ST * DA_STAGE + BW_EPI * BW_XS * 4 + 1024;
+
+template <int GATES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
+    k_bwd_levels(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmU, BwdLevels L,
+                 int NTn, int KB, int total_tiles, const int32_t *__restrict__ gather,
+                 const __nv_bfloat16 *__restrict__ Gact, int ld_g, const float *__restrict__ C, int ld, float *dA,
+                 float *dCe, __nv_bfloat16 *dZ, int ld_z, int *done) {
+  constexpr int ST = BW_ST;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = align1024(smem_raw);
+  float *xs_all = reinterpret_cast<float *>(smem + ST * DA_STAGE);
+  __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int S = L.S, nl = L.nl;
+  const int Sp = (int)round_up(S, BK);
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < ST; s++) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; a++) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 2 * BW_EPI); }
+    ptx::fence_mbar_init();
+    ptx::prefetch_tmap(&tmZ);
+    ptx::prefetch_tmap(&tmU);
+  }
+  if (warp == 2) { ptx::tmem_alloc2(&tmem_base_sh, 512); ptx::tmem_relinquish2(); }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tbase = tmem_base_sh;
+  if (warp == 0) {
+    if (lane == 0) {
+      BwdCursor cur;
+      cur.init(L, NTn);
+      int it = 0, ready_d = L.D;
+      for (int T = pair; T < total_tiles; T += npairs) {
+        cur.seek(L, NTn, T);
+        if (cur.d < ready_d) {
+          // level d+1 done (hence every level above): all dZ rows of level d are written
+          ptx::wait_counter(done + (cur.d + 1), 2 * min(cur.prev_nt, npairs));
+          ptx::fence_proxy_async_global();
+          ready_d = cur.d;
+        }
+        const int lt = T - cur.t0;
+        const int mt = (cur.r0 - nl) + (lt / NTn) * PM + (int)rank * BM;
+        const int nb = (lt % NTn) * DA_N + (int)rank * (DA_N / 2);
+        for (int kb = 0; kb < KB; kb++, it++) {
+          int s = it % ST;
+          uint32_t ph = (it / ST) & 1;
+          ptx::mbar_wait(&empty[s], ph ^ 1);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], 2 * DA_STAGE);
+          uint8_t *A = smem + s * DA_STAGE;
+          ptx::tma_load_2d_pair(&tmZ, &full[s], A, kb * BK, mt);
+#pragma unroll
+          for (int ch = 0; ch < DA_N / 128; ch++)
+            ptx::tma_load_2d_pair(&tmU, &full[s], A + DA_A_BYTES + ch * MN_CHUNK, nb + ch * 64, kb * BK);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16(PM, DA_N, 0, 1);
+      int it = 0, tc = 0;
+      for (int T = pair; T < total_tiles; T += npairs, tc++) {
+        const int acc = tc & 1;
+        ptx::mbar_wait(&tempty[acc], ((tc >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t dst = tbase + acc * 256;
+        for (int kb = 0; kb < KB; kb++, it++) {
+          int s = it % ST;
+          uint32_t ph = (it / ST) & 1;
+          ptx::mbar_wait(&full[s], ph);
+          ptx::tc_fence_after();
+          uint32_t a0 = ptx::smem_u32(smem + s * DA_STAGE), b0 = a0 + DA_A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; k++)
+            ptx::umma_bf16_2cta(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024),
+                                ptx::sdesc_sw128(b0 + 2048 * k, MN_CHUNK, 1024), idesc, (kb | k) != 0);
+          ptx::umma_commit_2cta(&empty[s]);
+        }
+        ptx::umma_commit_2cta(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3, grp = (warp - 4) >> 2;
+    float *xs = xs_all + (warp - 4) * BW_XS;
+    BwdCursor cur;
+    cur.init(L, NTn);
+    int tc = 0, ready_d = L.D;
+    for (int T = pair; T < total_tiles; T += npairs, tc++) {
+      cur.seek(L, NTn, T);
+      if (cur.d < ready_d) {  // order this thread's dCe / C reads after level d+1's publication
+        ptx::wait_counter(done + (cur.d + 1), 2 * min(cur.prev_nt, npairs));
+        ready_d = cur.d;
+      }
+      const int acc = tc & 1;
+      const int lt = T - cur.t0;
+      const int c_row0 = (cur.r0 - nl) + (lt / NTn) * PM + (int)rank * BM + q * 32;  // cell of row 0
+      const int c_end = cur.r1 - nl;
+      const int n0 = (lt % NTn) * DA_N;
+      // per-row metadata for this warp's 32 rows: lane i <-> row i
+      const int my_c = c_row0 + lane;
+      const bool my_valid = my_c < c_end;
+      int my_x[2] = {-1, -1}, my_xl[2] = {-1, -1}, my_xr[2] = {-1, -1};
+      if (my_valid) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          my_x[h] = __ldg(gather + 2 * (int64_t)(my_c + nl) + h);
+          if (my_x[h] >= nl) {
+            my_xl[h] = __ldg(gather + 2 * (int64_t)my_x[h]);
+            my_xr[h] = __ldg(gather + 2 * (int64_t)my_x[h] + 1);
+          }
+        }
+      }
+      ptx::mbar_wait(&tfull[acc], (tc >> 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t tl = tbase + acc * 256 + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+      for (int slab = grp; slab < DA_N / 64; slab += 2) {
+        // TMEM (thread = row) -> smem transpose buffer
+        float v[64];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          float t8[8];
+          ptx::tmem_ld8(tl + slab * 64 + k * 8, t8);
+#pragma unroll
+          for (int u = 0; u < 8; u++) v[k * 8 + u] = t8[u];
+        }
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int k = 0; k < 64; k += 2) *reinterpret_cast<float2 *>(xs + lane * 66 + k) = make_float2(v[k], v[k + 1]);
+        __syncwarp();
+        const int np = n0 + slab * 64;  // padded column of the slab (the slab lies in one half)
+        const int half = np >= Sp;
+        const int col = np - half * Sp + 2 * lane;  // this lane's 2 state columns
+        const bool colok = col < S;                  // S even (checked by the host)
+        // rows in groups of R: all loads of the group first (memory-level parallelism),
+        // then the math and the stores
+        constexpr int R = 6;
+#pragma unroll 1
+        for (int i0 = 0; i0 < 32 && c_row0 + i0 < c_end; i0 += R) {
+          int xs_[R], xls[R], xrs[R];
+          bool ok[R];
+          float2 dh[R], cc[R], cl[R], cr[R], dc[R];
+          uint32_t graw[R][GATES];
+#pragma unroll
+          for (int j = 0; j < R; j++) {
+            const int i = i0 + j;
+            xs_[j] = __shfl_sync(0xffffffffu, half ? my_x[1] : my_x[0], i);
+            xls[j] = __shfl_sync(0xffffffffu, half ? my_xl[1] : my_xl[0], i);
+            xrs[j] = __shfl_sync(0xffffffffu, half ? my_xr[1] : my_xr[0], i);
+            ok[j] = colok && i < 32 && c_row0 + i < c_end;
+            dh[j] = *reinterpret_cast<const float2 *>(xs + (i & 31) * 66 + 2 * lane);
+            const int64_t e = 2 * (int64_t)(c_row0 + i) + half;
+            if (ok[j] && xs_[j] >= nl) {
+              const int64_t xc = xs_[j] - nl;
+              const __nv_bfloat16 *gx = Gact + xc * ld_g + col;
+#pragma unroll
+              for (int g = 0; g < GATES; g++) graw[j][g] = __ldg(reinterpret_cast<const uint32_t *>(gx + g * S));
+              if constexpr (GATES == 5) {
+                cc[j] = __ldcg(reinterpret_cast<const float2 *>(C + (int64_t)xs_[j] * ld + col));
+                cl[j] = xls[j] >= nl ? __ldcg(reinterpret_cast<const float2 *>(C + (int64_t)xls[j] * ld + col))
+                                     : make_float2(0.f, 0.f);
+                cr[j] = xrs[j] >= nl ? __ldcg(reinterpret_cast<const float2 *>(C + (int64_t)xrs[j] * ld + col))
+                                     : make_float2(0.f, 0.f);
+                dc[j] = __ldcg(reinterpret_cast<const float2 *>(dCe + e * S + col));
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < R; j++) {
+            if (!ok[j]) continue;
+            const int64_t e = 2 * (int64_t)(c_row0 + i0 + j) + half;
+            if (xs_[j] < nl) {  // leaf child: the embedding gradient reads dA
+              *reinterpret_cast<float2 *>(dA + e * S + col) = dh[j];
+              continue;
+            }
+            const int64_t xc = xs_[j] - nl;
+            __nv_bfloat16 *dz = dZ + xc * ld_z + col;
+            float2 gg[GATES];
+#pragma unroll
+            for (int g = 0; g < GATES; g++) gg[g] = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&graw[j][g]));
+            if constexpr (GATES == 1) {
+              const float2 h = gg[0];
+              *reinterpret_cast<__nv_bfloat162 *>(dz) =
+                  __floats2bfloat162_rn(dh[j].x * (1.f - h.x * h.x), dh[j].y * (1.f - h.y * h.y));
+            } else {
+              float zz[5][2], el[2], er[2];
+              const float dhv[2] = {dh[j].x, dh[j].y}, dcv[2] = {dc[j].x, dc[j].y}, ccv[2] = {cc[j].x, cc[j].y};
+              const float clv[2] = {cl[j].x, cl[j].y}, crv[2] = {cr[j].x, cr[j].y};
+#pragma unroll
+              for (int u = 0; u < 2; u++) {
+                const float ig = u ? gg[0].y : gg[0].x, fl = u ? gg[1].y : gg[1].x;
+                const float fr = u ? gg[2].y : gg[2].x, og = u ? gg[3].y : gg[3].x;
+                const float ug = u ? gg[4].y : gg[4].x;
+                const float tcv = tanhf(ccv[u]);
+                const float dO = dhv[u] * tcv;
+                const float dcc = dcv[u] + dhv[u] * og * (1.f - tcv * tcv);
+                zz[0][u] = dcc * ug * ig * (1.f - ig);
+                zz[1][u] = dcc * clv[u] * fl * (1.f - fl);
+                zz[2][u] = dcc * crv[u] * fr * (1.f - fr);
+                zz[3][u] = dO * og * (1.f - og);
+                zz[4][u] = dcc * ig * (1.f - ug * ug);
+                el[u] = dcc * fl;
+                er[u] = dcc * fr;
+              }
+#pragma unroll
+              for (int g = 0; g < 5; g++)
+                *reinterpret_cast<__nv_bfloat162 *>(dz + g * S) = __floats2bfloat162_rn(zz[g][0], zz[g][1]);
+              *reinterpret_cast<float2 *>(dCe + (2 * xc) * S + col) = make_float2(el[0], el[1]);
+              *reinterpret_cast<float2 *>(dCe + (2 * xc + 1) * S + col) = make_float2(er[0], er[1]);
+            }
+          }
+        }
+        __syncwarp();
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_leader(&tempty[acc]);
+      // last tile of this level for this CTA: publish
+      const int Tn = T + npairs;
+      if (Tn >= total_tiles || Tn >= cur.t0 + cur.nt) {
+        ptx::named_bar_sync(1, 32 * BW_EPI);
+        if (warp == 4 && lane == 0) {
+          ptx::fence_proxy_async_global();
+          __threadfence();
+          ptx::red_release_gpu_add(done + cur.d, 1);
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc2(tbase, 512); }
+}
+
 // =================================================================== dU = dZ^T * Acat (all cells)
 // CTA pairs: pair tile = 256 gate rows (i) x 256 state columns (j) of one half (L / R);
 // each CTA stages its 128 rows of dZ^T and 128 of the 256 columns of the A plane.
@@ -906,6 +1177,32 @@ fold_status tc_gemm_dA(int c0, int M, int n_cells, int S, int gates, const __nv_
   const int np = ntiles < num_sms() / 2 ? ntiles : num_sms() / 2;
   int KB = (int)cdiv(gates * S, BK);
   k_gemm_dA_tc<<<2 * np, kThreads, DA_SMEM, st>>>(tmZ, tmU, c0, M, KB, S, NTn, ntiles, dA);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
+  if (a.D < 2) return FOLD_OK;
+  const int S = a.S, gates = cell == FOLD_CELL_TREELSTM ? 5 : 1;
+  if (S & 1) return FOLD_E_UNSUPPORTED;
+  CUtensorMap tmZ, tmU;
+  FOLD_TRY(make_map(&tmZ, a.dZ, (uint64_t)gates * S, (uint64_t)a.n_cells, (uint64_t)a.ld_z * 2, BK, BM));
+  const int ld_u = tc_ld_u(S);
+  FOLD_TRY(make_map(&tmU, a.Ub, (uint64_t)ld_u, (uint64_t)gates * S, (uint64_t)ld_u * 2, 64, BK));
+  const int NTn = (int)cdiv(ld_u, DA_N);
+  int64_t total = 0;
+  for (int d = 2; d <= a.D; d++) total += cdiv(a.level_off_host[d + 1] - a.level_off_host[d], PM) * NTn;
+  if (total <= 0) return FOLD_OK;
+  if (total > INT32_MAX) return FOLD_E_INVALID;
+  auto kern = gates == 5 ? k_bwd_levels<5> : k_bwd_levels<1>;
+  FOLD_TRY(set_smem(kern, BW_SMEM));
+  static thread_local int npairs_max = 0;
+  if (!npairs_max) npairs_max = max_pairs(kern, BW_THREADS, BW_SMEM);
+  FOLD_CUDA_TRY(cudaMemsetAsync(a.done, 0, (size_t)(a.D + 2) * sizeof(int), st));
+  const int npairs = total < npairs_max ? (int)total : npairs_max;
+  BwdLevels L{a.level_off, a.D, S, a.nl};
+  kern<<<2 * npairs, BW_THREADS, BW_SMEM, st>>>(tmZ, tmU, L, NTn, (int)cdiv(gates * S, BK), (int)total, a.gather,
+                                               a.Gact, a.ld_g, a.C, a.ld, a.dA, a.dCe, a.dZ, a.ld_z, a.done);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }

@@ -27,6 +27,8 @@ enum {
   F_ERR0 = 0,  // F_ERR0 + k for the k-th error class (min offending id, INT_MAX = none)
   F_NLEAVES = 8, F_MAXDEPTH = 9, F_NSEG = 10,
   F_QCNT = 12,  // 3 rotating frontier counters 12..14
+  F_MULTI = 24,     // 1: some row has >= 2 consumer edges, or a root row is consumed
+  F_NDISTROOT = 25, // number of distinct root rows
   F_BAR = 16,   // grid barrier count, generation (16, 17)
   F_NFLAGS = 64
 };
@@ -515,7 +517,10 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
   }
   gsync(flags);
   sort_pairs(w, ne, dev_bits_for(N - 1), sk, sv, dsm);
-  for (int64_t i = gtid; i < ne; i += gstride) s.cons_edge[i] = sv[i];
+  for (int64_t i = gtid; i < ne; i += gstride) {
+    s.cons_edge[i] = sv[i];
+    if (i > 0 && sk[i] == sk[i - 1]) flags[F_MULTI] = 1;  // a row read by two edges
+  }
   for (int64_t r = gtid; r <= N; r += gstride) {
     int lo = 0, hi = ne;
     while (lo < hi) { const int mid = (lo + hi) >> 1; if ((int)sk[mid] < (int)r) lo = mid + 1; else hi = mid; }
@@ -552,7 +557,14 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
     }
     gsync(flags);
     sort_pairs(w, G, dev_bits_for(N - 1), sk, sv, dsm);
-    for (int64_t g = gtid; g < G; g += gstride) s.root_perm[g] = sv[g];
+    for (int64_t q = gtid; q < G; q += gstride) {
+      s.root_perm[q] = sv[q];
+      const int rr = (int)sk[q];
+      if (q == 0 || sk[q] != sk[q - 1]) {
+        atomicAdd(&flags[F_NDISTROOT], 1);
+        if (s.cons_off[rr + 1] > s.cons_off[rr]) flags[F_MULTI] = 1;  // a consumed root
+      }
+    }
   }
 }
 
@@ -578,6 +590,7 @@ fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr
   if (N < 0 || G < 0 || V < 0) return FOLD_E_INVALID;
   s->n_nodes = N; s->n_graphs = G;
   s->n_levels = s->n_leaves = s->n_cells = s->n_tok_segs = 0;
+  s->tree_like = 0;
   if (N == 0) {
     if (G > 0) { g_last_detail = 0; return FOLD_E_ROOT_RANGE; }
     if (s->level_off_host) { s->level_off_host[0] = 0; s->level_off_host[1] = 0; }
@@ -640,6 +653,10 @@ fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr
   s->n_leaves = hflags[F_NLEAVES];
   s->n_cells = N - s->n_leaves;
   s->n_tok_segs = hflags[F_NSEG];
+  // tree-like: every row is read by at most one edge and the rows nobody reads are exactly
+  // the (unconsumed) roots -- the backward can then form each child's gradient in the
+  // epilogue of its single consumer's dA tile
+  s->tree_like = (hflags[F_MULTI] == 0 && N - 2 * s->n_cells == hflags[F_NDISTROOT]) ? 1 : 0;
   return FOLD_OK;
 }
 

@@ -45,7 +45,8 @@ class _Sched(ctypes.Structure):
     _fields_ = [(k, ctypes.c_void_p) for k in _SCHED_ARRAYS] + [
         ("level_off_host", ctypes.c_void_p),
         ("n_nodes", ctypes.c_int32), ("n_graphs", ctypes.c_int32), ("n_levels", ctypes.c_int32),
-        ("n_leaves", ctypes.c_int32), ("n_cells", ctypes.c_int32), ("n_tok_segs", ctypes.c_int32)]
+        ("n_leaves", ctypes.c_int32), ("n_cells", ctypes.c_int32), ("n_tok_segs", ctypes.c_int32),
+        ("tree_like", ctypes.c_int32)]
 
 
 class _Model(ctypes.Structure):
@@ -176,6 +177,7 @@ class Schedule:
     n_leaves: int
     n_cells: int
     n_tok_segs: int
+    tree_like: bool = False
     _struct: _Sched = None
     _host_buf: np.ndarray = None
 
@@ -214,11 +216,11 @@ def schedule(op: torch.Tensor, child: torch.Tensor, token: torch.Tensor, root: t
     if workspace is None or workspace.numel() < ws_bytes:
         workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     g = _Graphs(N, G, int(vocab), op.data_ptr(), child.data_ptr(), token.data_ptr(), root.data_ptr())
-    s = _Sched(*[arrays[k].data_ptr() for k in _SCHED_ARRAYS], host.ctypes.data, 0, 0, 0, 0, 0, 0)
+    s = _Sched(*[arrays[k].data_ptr() for k in _SCHED_ARRAYS], host.ctypes.data, 0, 0, 0, 0, 0, 0, 0)
     _check(L.fold_schedule(ctypes.byref(g), ctypes.byref(s), ctypes.c_void_p(workspace.data_ptr()),
                            ws_bytes, _stream(stream)), "fold_schedule")
     return Schedule(arrays, host, s.n_nodes, s.n_graphs, s.n_levels, s.n_leaves, s.n_cells, s.n_tok_segs,
-                    _struct=s, _host_buf=host)
+                    bool(s.tree_like), _struct=s, _host_buf=host)
 
 
 # ----------------------------------------------------------------------------- model / acts
