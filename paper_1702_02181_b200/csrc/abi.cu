@@ -35,7 +35,8 @@ fold_status check_sched(const fold_schedule_t *s) {
 struct BwdWs {
   float *dA, *dCe, *partial, *dU_split;
   int32_t *root_off;
-  int *done;  // [n_levels + 2] level counters of the fused backward
+  int *rt_cnt;      // [n_cells] row-tile counters of the fused backward
+  int32_t *tstart;  // [n_cells]
   EmbedBwdWs emb;
   void *dZ;
   __nv_bfloat16 *Ub;
@@ -57,7 +58,7 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
   size_t o_dZ = take((size_t)(nc + 1) * b.ld_z * (bf16 ? 2 : 4));
   size_t o_part = take((size_t)b.nsplit * gates * S * 4);
   size_t o_roff = take((size_t)(s->n_nodes + 2) * 4);
-  size_t o_done = take((size_t)(s->n_levels + 2) * 4);
+  size_t o_rtc = take((size_t)(nc + 1) * 4), o_ts = take((size_t)(nc + 1) * 4);
   const int64_t nseg = s->n_tok_segs;
   const int64_t max_pieces = s->n_leaves / kEmbedPiece + nseg + 1;
   size_t o_pc = take((size_t)(nseg + 2) * 4), o_po = take((size_t)(nseg + 2) * 4);
@@ -74,7 +75,8 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
     b.dZ = p + o_dZ;
     b.partial = (float *)(p + o_part);
     b.root_off = (int32_t *)(p + o_roff);
-    b.done = (int *)(p + o_done);
+    b.rt_cnt = (int *)(p + o_rtc);
+    b.tstart = (int32_t *)(p + o_ts);
     b.emb.piece_cnt = (int32_t *)(p + o_pc);
     b.emb.piece_off = (int32_t *)(p + o_po);
     b.emb.scan_sums = (int32_t *)(p + o_ss);
@@ -268,17 +270,18 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
   if (bf16 && s->tree_like && (S & 1) == 0) {
     // tree-like: roots' seeded pointwise step, then every level's dA GEMM with the
     // children's pointwise step fused into its epilogue (one persistent launch)
+    TcBwdArgs ba{};
+    ba.level_off = s->level_off; ba.level_off_host = lo;
+    ba.D = D; ba.S = S; ba.nl = nl; ba.n_cells = nc; ba.ld = L.ld; ba.ld_g = L.ld_g; ba.ld_z = b.ld_z;
+    ba.gather = s->gather; ba.Ub = b.Ub; ba.Gact = (const __nv_bfloat16 *)Gact; ba.C = C;
+    ba.dA = b.dA; ba.dCe = b.dCe; ba.dZ = (__nv_bfloat16 *)b.dZ; ba.rt_cnt = b.rt_cnt; ba.tstart = b.tstart;
     {
       ProfScope ps(K_BWD_PW, st);
       FOLD_TRY(launch_cell_bwd_pw(bf16, m->cell, 0, G, nl, S, L.ld, L.ld_g, s->cons_off, s->cons_edge, b.root_off,
                                   s->root_perm, G, dh_root, dc_root, s->gather, Gact, C, b.dA, b.dCe, b.dZ, b.ld_z,
                                   st, s->root_row));
+      FOLD_TRY(tc_bwd_prelude(ba, s->cons_off, st));
     }
-    TcBwdArgs ba{};
-    ba.level_off = s->level_off; ba.level_off_host = lo;
-    ba.D = D; ba.S = S; ba.nl = nl; ba.n_cells = nc; ba.ld = L.ld; ba.ld_g = L.ld_g; ba.ld_z = b.ld_z;
-    ba.gather = s->gather; ba.Ub = b.Ub; ba.Gact = (const __nv_bfloat16 *)Gact; ba.C = C;
-    ba.dA = b.dA; ba.dCe = b.dCe; ba.dZ = (__nv_bfloat16 *)b.dZ; ba.done = b.done;
     ProfScope ps(K_GEMM_DA, st);
     FOLD_TRY(tc_bwd_levels(m->cell, ba, st));
   } else

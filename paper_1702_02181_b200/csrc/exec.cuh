@@ -107,8 +107,11 @@ struct TcBwdArgs {
   const float *C;
   float *dA, *dCe;
   __nv_bfloat16 *dZ;
-  int *done;  // [D + 2]
+  int *rt_cnt;       // [n_cells] per-row-tile completion counters (keyed by a tile's first cell)
+  int32_t *tstart;   // [n_cells] first cell of each cell's row tile
 };
+// tile bookkeeping (zero counters, tstart, roots' pre-credit); before the seeded pass
+fold_status tc_bwd_prelude(const TcBwdArgs &a, const int32_t *cons_off, cudaStream_t st);
 fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st);
 fold_status tc_gemm_dA(int c0, int M, int n_cells, int S, int gates, const __nv_bfloat16 *dZ, int ld_z,
                        const __nv_bfloat16 *Ub, float *dA, cudaStream_t st);

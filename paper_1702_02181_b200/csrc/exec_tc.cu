@@ -574,9 +574,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // backward pointwise step -- for edge e = (cell c, slot k) with child x (its single
 // consumer is e): dh(x) = dA[e], dc(x) = dCe[e] (written by c's own pointwise step), then
 // dz(x) -> dZ row of x and dCe of x's two edges. The dA rows never reach memory except for
-// leaf children (the embedding gradient reads them). Level d's tiles wait on a device
-// counter for level d+1, whose epilogues completed every dZ row of level d. Roots' dZ come
-// from a seeded pointwise pass launched before.
+// leaf children (the embedding gradient reads them). Dependencies are per 256-row tile, not
+// per level: every tile has a counter (keyed by its first cell) that the epilogues of its
+// rows' consumers raise by one per (row, 64-column slab) they complete; the tile's TMA
+// producer waits for rows x slabs, so a tile starts as soon as ITS rows are ready, and the
+// depth order of PAPER.md L49 holds without level-wide drains. Roots' dZ come from a seeded
+// pointwise pass launched before (their counts are pre-set by k_bwd_prelude).
 // Epilogue layout: each warp owns 32 accumulator rows; per 64-column slab it moves the
 // fp32 values TMEM -> registers -> a padded smem transpose, then walks the rows with the
 // 32 lanes across columns, so every global access of the pointwise step is a coalesced
@@ -608,7 +611,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
     k_bwd_levels(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmU, BwdLevels L,
                  int NTn, int KB, int total_tiles, const int32_t *__restrict__ gather,
                  const __nv_bfloat16 *__restrict__ Gact, int ld_g, const float *__restrict__ C, int ld, float *dA,
-                 float *dCe, __nv_bfloat16 *dZ, int ld_z, int *done) {
+                 float *dCe, __nv_bfloat16 *dZ, int ld_z, int *rt_cnt, const int32_t *__restrict__ tstart,
+                 int slabs) {
   constexpr int ST = BW_ST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
@@ -636,16 +640,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
     if (lane == 0) {
       BwdCursor cur;
       cur.init(L, NTn);
-      int it = 0, ready_d = L.D;
+      int it = 0;
       for (int T = pair; T < total_tiles; T += npairs) {
         cur.seek(L, NTn, T);
-        if (cur.d < ready_d) {
-          // level d+1 done (hence every level above): all dZ rows of level d are written
-          ptx::wait_counter(done + (cur.d + 1), 2 * min(cur.prev_nt, npairs));
-          ptx::fence_proxy_async_global();
-          ready_d = cur.d;
-        }
         const int lt = T - cur.t0;
+        {  // this pair tile's 256 dZ rows (and their dCe) complete
+          const int ct = (cur.r0 - nl) + (lt / NTn) * PM;
+          ptx::wait_counter(rt_cnt + ct, min(PM, cur.r1 - nl - ct) * slabs);
+          ptx::fence_proxy_async_global();
+        }
         const int mt = (cur.r0 - nl) + (lt / NTn) * PM + (int)rank * BM;
         const int nb = (lt % NTn) * DA_N + (int)rank * (DA_N / 2);
         for (int kb = 0; kb < KB; kb++, it++) {
@@ -690,22 +693,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
     float *xs = xs_all + (warp - 4) * BW_XS;
     BwdCursor cur;
     cur.init(L, NTn);
-    int tc = 0, ready_d = L.D;
+    int tc = 0;
     for (int T = pair; T < total_tiles; T += npairs, tc++) {
       cur.seek(L, NTn, T);
-      if (cur.d < ready_d) {  // order this thread's dCe / C reads after level d+1's publication
-        ptx::wait_counter(done + (cur.d + 1), 2 * min(cur.prev_nt, npairs));
-        ready_d = cur.d;
-      }
       const int acc = tc & 1;
       const int lt = T - cur.t0;
+      {  // order this warp's dCe reads after the tile's publication (already complete)
+        const int ct = (cur.r0 - nl) + (lt / NTn) * PM;
+        if (lane == 0) ptx::wait_counter(rt_cnt + ct, min(PM, cur.r1 - nl - ct) * slabs);
+        __syncwarp();
+      }
       const int c_row0 = (cur.r0 - nl) + (lt / NTn) * PM + (int)rank * BM + q * 32;  // cell of row 0
       const int c_end = cur.r1 - nl;
       const int n0 = (lt % NTn) * DA_N;
       // per-row metadata for this warp's 32 rows: lane i <-> row i
       const int my_c = c_row0 + lane;
       const bool my_valid = my_c < c_end;
-      int my_x[2] = {-1, -1}, my_xl[2] = {-1, -1}, my_xr[2] = {-1, -1};
+      int my_x[2] = {-1, -1}, my_xl[2] = {-1, -1}, my_xr[2] = {-1, -1}, my_ts[2] = {-1, -1};
       if (my_valid) {
 #pragma unroll
         for (int h = 0; h < 2; h++) {
@@ -713,9 +717,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
           if (my_x[h] >= nl) {
             my_xl[h] = __ldg(gather + 2 * (int64_t)my_x[h]);
             my_xr[h] = __ldg(gather + 2 * (int64_t)my_x[h] + 1);
+            my_ts[h] = __ldg(tstart + (my_x[h] - nl));
           }
         }
       }
+      int slab_cnt[2] = {0, 0};  // 64-column slabs this warp completes, per half
       ptx::mbar_wait(&tfull[acc], (tc >> 1) & 1);
       ptx::tc_fence_after();
       const uint32_t tl = tbase + acc * 256 + ((uint32_t)(q * 32) << 16);
@@ -738,6 +744,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         const int half = np >= Sp;
         const int col = np - half * Sp + 2 * lane;  // this lane's 2 state columns
         const bool colok = col < S;                  // S even (checked by the host)
+        if (np - half * Sp < S) slab_cnt[half]++;
         // rows in groups of R: all loads of the group first (memory-level parallelism),
         // then the math and the stores
         constexpr int R = 6;
@@ -821,21 +828,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_leader(&tempty[acc]);
-      // last tile of this level for this CTA: publish
-      const int Tn = T + npairs;
-      if (Tn >= total_tiles || Tn >= cur.t0 + cur.nt) {
-        ptx::named_bar_sync(1, 32 * BW_EPI);
-        if (warp == 4 && lane == 0) {
-          ptx::fence_proxy_async_global();
-          __threadfence();
-          ptx::red_release_gpu_add(done + cur.d, 1);
-        }
-      }
+      // publish: every lane fences its own dZ / dCe stores, then lane i credits the tiles of
+      // row i's children with the slabs this warp completed
+      ptx::fence_proxy_async_global();
+      __threadfence();
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+        if (my_valid && my_ts[h] >= 0 && slab_cnt[h] > 0) atomicAdd(rt_cnt + my_ts[h], slab_cnt[h]);
     }
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();
   if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc2(tbase, 512); }
+}
+
+// Row-tile bookkeeping for k_bwd_levels: tstart[c] = first cell of c's 256-row tile (tiles
+// start at each level's first row), and the counters of tiles holding roots start at the
+// roots' share (their dZ rows come from the seeded pass before the kernel). rt_cnt must be
+// zeroed before.
+__global__ void k_bwd_prelude(const int32_t *__restrict__ lo, int D, int nl, int n_cells,
+                              const int32_t *__restrict__ cons_off, int32_t *__restrict__ tstart, int *rt_cnt,
+                              int slabs) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n_cells; c += stride) {
+    const int r = (int)c + nl;
+    int a = 2, b = D;  // level d with lo[d] <= r < lo[d + 1]
+    while (a < b) { const int m = (a + b + 1) >> 1; if (__ldg(lo + m) <= r) a = m; else b = m - 1; }
+    const int r0 = __ldg(lo + a);
+    const int ts = (r0 - nl) + ((r - r0) / PM) * PM;
+    tstart[c] = ts;
+    if (__ldg(cons_off + r + 1) == __ldg(cons_off + r)) atomicAdd(rt_cnt + ts, slabs);
+  }
 }
 
 // =================================================================== dU = dZ^T * Acat (all cells)
@@ -1181,6 +1205,19 @@ fold_status tc_gemm_dA(int c0, int M, int n_cells, int S, int gates, const __nv_
   return FOLD_OK;
 }
 
+int tc_bwd_slabs(int S) { return (int)cdiv(S, 64); }
+
+fold_status tc_bwd_prelude(const TcBwdArgs &a, const int32_t *cons_off, cudaStream_t st) {
+  if (a.n_cells <= 0) return FOLD_OK;
+  FOLD_CUDA_TRY(cudaMemsetAsync(a.rt_cnt, 0, (size_t)a.n_cells * sizeof(int), st));
+  int64_t blocks = cdiv(a.n_cells, 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_bwd_prelude<<<(unsigned)blocks, 256, 0, st>>>(a.level_off, a.D, a.nl, a.n_cells, cons_off, a.tstart, a.rt_cnt,
+                                                  tc_bwd_slabs(a.S));
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
 fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
   if (a.D < 2) return FOLD_OK;
   const int S = a.S, gates = cell == FOLD_CELL_TREELSTM ? 5 : 1;
@@ -1198,11 +1235,11 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
   FOLD_TRY(set_smem(kern, BW_SMEM));
   static thread_local int npairs_max = 0;
   if (!npairs_max) npairs_max = max_pairs(kern, BW_THREADS, BW_SMEM);
-  FOLD_CUDA_TRY(cudaMemsetAsync(a.done, 0, (size_t)(a.D + 2) * sizeof(int), st));
   const int npairs = total < npairs_max ? (int)total : npairs_max;
   BwdLevels L{a.level_off, a.D, S, a.nl};
   kern<<<2 * npairs, BW_THREADS, BW_SMEM, st>>>(tmZ, tmU, L, NTn, (int)cdiv(gates * S, BK), (int)total, a.gather,
-                                               a.Gact, a.ld_g, a.C, a.ld, a.dA, a.dCe, a.dZ, a.ld_z, a.done);
+                                               a.Gact, a.ld_g, a.C, a.ld, a.dA, a.dCe, a.dZ, a.ld_z, a.rt_cnt,
+                                               a.tstart, tc_bwd_slabs(S));
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
