@@ -113,10 +113,10 @@ AuxStream &aux_stream() {
   return a;
 }
 
-// forward workspace (BF16 path): bf16 U, then the per-level completion counters
+// forward workspace (BF16 path): bf16 U, then the row-tile counters and tile starts
 size_t fwd_ws_bytes(const fold_schedule_t *s, const fold_model *m) {
   if (m->prec != FOLD_PREC_BF16) return 256;
-  return tc_weights_bytes(gates_of(m->cell), m->S) + a256((size_t)(s->n_levels + 2) * sizeof(int));
+  return tc_weights_bytes(gates_of(m->cell), m->S) + 2 * a256((size_t)(s->n_cells + 1) * sizeof(int));
 }
 
 }  // namespace
@@ -207,7 +207,8 @@ fold_status fold_forward(const fold_schedule_t *s, const fold_model *m, void *ac
       fa.D = D; fa.S = S; fa.nl = nl; fa.n_cells = s->n_cells; fa.ld = L.ld; fa.ld_g = L.ld_g; fa.ld_u = tc_ld_u(S);
       fa.gather = s->gather; fa.Ub = Ub; fa.b = m->b;
       fa.H = (__nv_bfloat16 *)H; fa.Gact = (__nv_bfloat16 *)Gact; fa.C = C; fa.sc = sc;
-      fa.done = (int *)((char *)ws + tc_weights_bytes(gates, S));
+      fa.rt_cnt = (int *)((char *)ws + tc_weights_bytes(gates, S));
+      fa.tstart = (int32_t *)((char *)fa.rt_cnt + a256((size_t)(s->n_cells + 1) * sizeof(int)));
       ProfScope ps(K_CELL_FWD, st);
       FOLD_TRY(tc_fwd_levels(m->cell, fa, st));
     }

@@ -94,7 +94,8 @@ struct TcFwdArgs {
   __nv_bfloat16 *H, *Gact;
   float *C;
   ScatterA sc;
-  int *done;                       // [D + 2] level completion counters (workspace)
+  int *rt_cnt;                     // [n_cells] per-row-tile counters (workspace)
+  int32_t *tstart;                 // [n_cells] first cell of each cell's row tile (workspace)
 };
 fold_status tc_fwd_levels(int cell, const TcFwdArgs &a, cudaStream_t st);
 // Tree-like schedules: the dA GEMM of every level in one persistent launch, each tile's

@@ -121,13 +121,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
                  const __grid_constant__ CUtensorMap tmCw, const __grid_constant__ CUtensorMap tmCn, FwdLevels L,
                  int total_tiles, int nl, int ld, const int32_t *__restrict__ gather, const float *__restrict__ bias,
                  __nv_bfloat16 *__restrict__ H, float *C, __nv_bfloat16 *__restrict__ Gact, int ld_g, ScatterA sc,
-                 int *done) {
+                 int *rt_cnt, const int32_t *__restrict__ tstart, int dbg) {
   using Cfg = FwdCfg<GATES>;
   constexpr int ST = Cfg::NST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
   uint8_t *gsm = smem + ST * Cfg::STAGE, *csm = gsm + Cfg::G_STAGE;
   __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull[2], tempty[2];
+  // epilogue -> store warp hand-off: epi_done (8 epilogue warps arrive per tile), stg_free
+  // (the store warp: the tile's bulk stores finished reading the staging)
+  __shared__ __align__(8) uint64_t epi_done, stg_free;
+  __shared__ int2 credit_list[2][8][32];  // per tile parity, per epilogue warp: (tile, credit)
+  __shared__ int credit_n[2][8];          // entries, or -1: overflow (the store warp walks the rows)
   __shared__ uint32_t tmem_base_sh;
   const int S = L.S;
   const uint32_t rank = ptx::cluster_ctarank();
@@ -138,6 +143,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
     for (int s = 0; s < ST; s++) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
     // tempty (leader's copy used): drained by the epilogue warps of both CTAs
     for (int a = 0; a < 2; a++) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 2 * Cfg::EPI_WARPS); }
+    ptx::mbar_init(&epi_done, Cfg::EPI_WARPS);
+    ptx::mbar_init(&stg_free, 1);
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tmAL);
     ptx::prefetch_tmap(&tmAR);
@@ -156,7 +163,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
   ptx::tc_fence_after();
   const uint32_t tbase = tmem_base_sh;
   const int KBh = (int)cdiv(S, BK), KB = 2 * KBh, Sp = KBh * BK;
-  const int pub_per_cta = 2;  // both CTAs of a pair publish
 
   if (warp == 0) {
     // TMA producer: per stage one dense box of 128 A rows (the level's contiguous cell rows
@@ -164,16 +170,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
     if (lane == 0) {
       LevelCursor cur;
       cur.init(L);
-      int it = 0, ready_d = 2;
+      int it = 0;
       for (int T = pair; T < total_tiles; T += npairs) {
         cur.seek(L, T);
-        if (cur.d > ready_d) {
-          // all of level d-1 (hence every level < d) published: its h rows are in the planes
-          ptx::wait_counter(done + (cur.d - 1), pub_per_cta * min(cur.prev_nt, npairs));
-          ptx::fence_proxy_async_global();
-          ready_d = cur.d;
-        }
         const int lt = T - cur.t0, W = cur.W;
+        {  // both children's h (all S columns) pushed into every A row of this pair tile
+          // (and their C rows written); the rows are read only by TMA and, after this
+          // tile's MMA, through L2 by the epilogue
+          const int ct = (cur.r0 - nl) + (lt / cur.NT) * PM;
+          ptx::wait_counter_relaxed(rt_cnt + ct, min(PM, cur.r1 - nl - ct) * 2 * S);
+          ptx::fence_proxy_async_global();
+        }
         const int c0 = (cur.r0 - nl) + (lt / cur.NT) * PM + (int)rank * BM, j0 = (lt % cur.NT) * W;
         const CUtensorMap *tmU = W == Cfg::WMAX ? &tmUw : &tmUn;
         // the leader's full barrier counts both CTAs' bytes: 2 x (A rows + half the B rows)
@@ -245,13 +252,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
     Meta nxt;
     nxc.seek(L, pair);
     fetch_meta(nxc, pair, nxt);
-    int tc = 0, ready_d = 2;
+
+    // Publication goes through the store warp (warp 3): per tile each epilogue warp fences
+    // its pushes / staging writes, sums its rows' credits (h columns pushed) per consumer
+    // tile into credit_list and arrives on epi_done; the store warp issues the bulk stores,
+    // waits for them, fences (cumulative over the mbarrier hand-off) and adds the credits.
+    auto warp_credits = [&](int par, int ce0, int ce1, int e0, int cols) {
+      const int ew = warp - 4;
+      int n = 0;
+      bool over = false;
+      for (int k = 0; !over; k++) {
+        const int e = ce0 + k;
+        const bool act = e < ce1 && cols > 0;
+        if (!__any_sync(0xffffffffu, act)) break;
+        const int ts = act ? __ldg(tstart + ((k == 0 ? e0 : __ldg(sc.cons_edge + e)) >> 1)) : -1;
+        unsigned todo = __ballot_sync(0xffffffffu, act);
+        while (todo) {
+          if (n == 32) { over = true; break; }
+          const int src = __ffs(todo) - 1;
+          const int key = __shfl_sync(0xffffffffu, ts, src);
+          const bool mine = act && ts == key;
+          const int sum = (int)__reduce_add_sync(0xffffffffu, mine ? (unsigned)cols : 0u);
+          todo &= ~__ballot_sync(0xffffffffu, mine);
+          if (lane == src) credit_list[par][ew][n] = make_int2(key, sum);
+          n++;
+        }
+      }
+      if (lane == 0) credit_n[par][ew] = over ? -1 : n;
+    };
+    int tc = 0;
     for (int T = pair; T < total_tiles; T += npairs, tc++) {
       cur.seek(L, T);
-      if (cur.d > ready_d) {  // order this thread's C reads after level d-1's publication
-        ptx::wait_counter(done + (cur.d - 1), pub_per_cta * min(cur.prev_nt, npairs));
-        ready_d = cur.d;
-      }
       const int acc = tc & 1;
       const uint32_t aph = (tc >> 1) & 1;
       const int lt = T - cur.t0, W = cur.W, chunks = W / 8;
@@ -264,7 +295,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
       const int64_t gl = m.gl, gr = m.gr;
       const int ce0 = m.ce0, ce1 = m.ce1;
       const int64_t c = r - nl;
-      // prefetch the first chunk's child cell states before waiting for the accumulator
+      // child cell states: loaded only after the accumulator is ready (this tile's MMA ran
+      // after its producer saw the children published), then one chunk ahead of the math
       float cl[8], cr[8];
       auto load_c = [&](int jb) {
         if (GATES != 5) return;
@@ -291,17 +323,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
           }
         }
       };
-      load_c(j0 + grp * 8);
       // full-width tiles stage G and C in shared memory and leave by TMA (partial tiles at
       // the S edge store directly)
-      const bool staged = (S & 7) == 0 && j0 + W <= S;
       const int64_t c_tile = (int64_t)(cur.r0 - nl) + (int64_t)(lt / cur.NT) * PM + rank * BM;
+      // (the bulk stores never write past the level's last row: a later level's tile may
+      // already own those rows)
+      const bool staged = (S & 7) == 0 && j0 + W <= S && c_tile + BM <= cur.r1 - nl;
       ptx::mbar_wait(&tfull[acc], aph);
       ptx::tc_fence_after();
-      if (staged) {  // the previous tile's bulk stores have finished reading the staging
-        if (warp == 4 && lane == 0) ptx::bulk_wait_read0();
-        ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
-      }
+      load_c(j0 + grp * 8);
+      if (tc > 0) ptx::mbar_wait(&stg_free, (tc - 1) & 1);  // previous tile's staging consumed
       const uint32_t tl = tbase + acc * Cfg::ACC_STRIDE + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
       for (int jc = grp; jc < chunks; jc += 2) {
@@ -411,37 +442,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_leader(&tempty[acc]);
-      const int Tn = T + npairs;
-      const bool last_of_level = Tn >= total_tiles || Tn >= cur.t0 + cur.nt;
-      if (staged) {
-        // staging complete -> one thread issues the tile's bulk stores (rows past the level
-        // land in later levels' rows, which those levels overwrite after this level is
-        // published, or are clipped at the tensor end)
-        ptx::fence_proxy_async_smem();
-        ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
-        if (warp == 4 && lane == 0) {
+      // hand the tile to the store warp
+      ptx::fence_proxy_async_smem();
+      ptx::fence_proxy_async_global();
+      int cols = 0;
+      if (valid)
+        for (int jc = grp; jc < chunks; jc += 2) cols += max(0, min(8, S - (j0 + jc * 8)));
+      warp_credits(tc & 1, ce0, ce1, m.e0, cols);
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&epi_done);
+    }
+  } else if (warp == 3) {
+    // Store warp: bulk stores of the staged G / C tiles, then the tile's publication.
+    if (lane == 0) {
+      LevelCursor cur;
+      cur.init(L);
+      int tc = 0;
+      for (int T = pair; T < total_tiles; T += npairs, tc++) {
+        cur.seek(L, T);
+        const int lt = T - cur.t0, W = cur.W, chunks = W / 8;
+        const int j0 = (lt % cur.NT) * W;
+        const int64_t c_tile = (int64_t)(cur.r0 - nl) + (int64_t)(lt / cur.NT) * PM + rank * BM;
+        const bool staged = (S & 7) == 0 && j0 + W <= S && c_tile + BM <= cur.r1 - nl;
+        ptx::mbar_wait(&epi_done, tc & 1);
+        if (staged) {
           const CUtensorMap *tG = W == Cfg::WMAX ? &tmGw : &tmGn;
           const CUtensorMap *tC = W == Cfg::WMAX ? &tmCw : &tmCn;
 #pragma unroll
           for (int g = 0; g < GATES; g++) ptx::tma_store_2d(tG, gsm + g * BM * W * 2, g * S + j0, (int)c_tile);
           ptx::tma_store_2d(tC, csm, j0, (int)(c_tile + nl));
           ptx::bulk_commit();
+          ptx::bulk_wait_read0();
         }
-      }
-      // last tile of this level for this CTA: publish (all epilogue warps' stores and the
-      // bulk stores complete, then one release increment; level d is complete at
-      // 2 min(#pair tiles(d), #pairs) increments)
-      if (last_of_level) {
-        ptx::named_bar_sync(1, 32 * Cfg::EPI_WARPS);
-        if (warp == 4 && lane == 0) {
-          ptx::bulk_wait0();
-          ptx::fence_proxy_async_global();
-          __threadfence();
-          ptx::red_release_gpu_add(done + cur.d, 1);
+        ptx::mbar_arrive(&stg_free);
+        if (staged) ptx::bulk_wait0();  // the tile's C rows are written
+        __threadfence();
+        const int par = tc & 1;
+        for (int w = 0; w < Cfg::EPI_WARPS; w++) {
+          const int n = credit_n[par][w];
+          if (n >= 0) {
+            for (int i = 0; i < n; i++) atomicAdd(rt_cnt + credit_list[par][w][i].x, credit_list[par][w][i].y);
+          } else {  // overflow (wide DAG fan-out): walk warp w's 32 rows edge by edge
+            const int grp = w >> 2;
+            int cols = 0;
+            for (int jc = grp; jc < chunks; jc += 2) cols += max(0, min(8, S - (j0 + jc * 8)));
+            for (int i = 0; i < 32 && cols > 0; i++) {
+              const int64_t r = cur.r0 + (int64_t)(lt / cur.NT) * PM + rank * BM + (w & 3) * 32 + i;
+              if (r >= cur.r1) break;
+              for (int e = __ldg(sc.cons_off + r); e < __ldg(sc.cons_off + r + 1); e++)
+                atomicAdd(rt_cnt + __ldg(tstart + (__ldg(sc.cons_edge + e) >> 1)), cols);
+            }
+          }
         }
       }
     }
-    if (warp == 4 && lane == 0) ptx::bulk_wait0();
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();  // neither CTA leaves while the pair's MMAs / arrivals may touch it
@@ -862,6 +916,24 @@ __global__ void k_bwd_prelude(const int32_t *__restrict__ lo, int D, int nl, int
   }
 }
 
+// Forward row-tile bookkeeping: tstart[c] as for the backward; a tile's counter counts the
+// h columns pushed into its A rows (2 S per cell when complete), leaf children are credited
+// here (the embedding kernel, launched before, pushed them).
+__global__ void k_fwd_prelude(const int32_t *__restrict__ lo, int D, int nl, int n_cells, int S,
+                              const int32_t *__restrict__ gather, int32_t *__restrict__ tstart, int *rt_cnt) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n_cells; c += stride) {
+    const int r = (int)c + nl;
+    int a = 2, b = D;
+    while (a < b) { const int m = (a + b + 1) >> 1; if (__ldg(lo + m) <= r) a = m; else b = m - 1; }
+    const int r0 = __ldg(lo + a);
+    const int ts = (r0 - nl) + ((r - r0) / PM) * PM;
+    tstart[c] = ts;
+    const int leaves = (__ldg(gather + 2 * (int64_t)r) < nl) + (__ldg(gather + 2 * (int64_t)r + 1) < nl);
+    if (leaves) atomicAdd(rt_cnt + ts, leaves * S);
+  }
+}
+
 // =================================================================== dU = dZ^T * Acat (all cells)
 // CTA pairs: pair tile = 256 gate rows (i) x 256 state columns (j) of one half (L / R);
 // each CTA stages its 128 rows of dZ^T and 128 of the 256 columns of the A plane.
@@ -1113,6 +1185,11 @@ int max_pairs(K kernel, int threads, int smem) {
   return n < num_sms() / 2 ? n : num_sms() / 2;
 }
 
+int dbg_fwd() {
+  static int v = [] { const char *e = getenv("FOLD_DBG_FWD"); return e ? atoi(e) : 0; }();
+  return v;
+}
+
 template <int GATES>
 fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
   using Cfg = FwdCfg<GATES>;
@@ -1147,11 +1224,17 @@ fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
   }
   if (total <= 0) return FOLD_OK;
   if (total > INT32_MAX) return FOLD_E_INVALID;
-  FOLD_CUDA_TRY(cudaMemsetAsync(a.done, 0, (size_t)(a.D + 2) * sizeof(int), st));
+  FOLD_CUDA_TRY(cudaMemsetAsync(a.rt_cnt, 0, (size_t)nc * sizeof(int), st));
+  {
+    int64_t blocks = cdiv(nc, 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    k_fwd_prelude<<<(unsigned)blocks, 256, 0, st>>>(a.level_off, a.D, a.nl, nc, S, a.gather, a.tstart, a.rt_cnt);
+    FOLD_LAUNCH_CHECK();
+  }
   const int npairs = total < npairs_max ? (int)total : npairs_max;
   kern<<<2 * npairs, Cfg::THREADS, smem_bytes, st>>>(tmAL, tmAR, tmUw, tmUn, tmGw, tmGn, tmCw, tmCn, L, (int)total,
                                                       a.nl, a.ld, a.gather, a.b, a.H, a.C, a.Gact, a.ld_g, a.sc,
-                                                      a.done);
+                                                      a.rt_cnt, a.tstart, dbg_fwd());
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }

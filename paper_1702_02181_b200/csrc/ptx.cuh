@@ -144,6 +144,16 @@ __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ int ld_relaxed_gpu(const int *p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// spin until *p >= target with relaxed loads (no L1 invalidation per poll; for consumers
+// that read the published data only through L2 / the async proxy after this returns)
+__device__ __forceinline__ void wait_counter_relaxed(const int *p, int target) {
+  while (ld_relaxed_gpu(p) < target) __nanosleep(64);
+}
 // spin (with back-off) until *p >= target, then acquire
 __device__ __forceinline__ void wait_counter(const int *p, int target) {
   while (ld_acquire_gpu(p) < target) __nanosleep(64);
