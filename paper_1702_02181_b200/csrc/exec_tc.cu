@@ -640,17 +640,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // row segment.
 struct BwdLevels {
   const int32_t *lo;
-  int D, S, nl;
+  int D, S, nl, ld_u;
+  int narrow_below;  // a level with fewer 256-column pair tiles than this uses 128 columns
 };
+__host__ __device__ inline int bwd_level_N(const BwdLevels &L, int M) {
+  return cdiv(M, PM) * cdiv(L.ld_u, 256) < L.narrow_below ? 128 : 256;
+}
 struct BwdCursor {  // walks levels D, D-1, ..., 2 in tile order
-  int d, t0, nt, prev_nt, r0, r1;
-  __device__ void load(const BwdLevels &L, int NTn) {
+  int d, t0, nt, r0, r1, N, NTn;
+  __device__ void load(const BwdLevels &L) {
     r0 = __ldg(L.lo + d); r1 = __ldg(L.lo + d + 1);
+    N = bwd_level_N(L, r1 - r0);
+    NTn = (int)cdiv(L.ld_u, N);
     nt = (int)cdiv(r1 - r0, PM) * NTn;
   }
-  __device__ void init(const BwdLevels &L, int NTn) { d = L.D; t0 = 0; prev_nt = 0; load(L, NTn); }
-  __device__ void seek(const BwdLevels &L, int NTn, int T) {
-    while (T >= t0 + nt) { t0 += nt; prev_nt = nt; d--; load(L, NTn); }
+  __device__ void init(const BwdLevels &L) { d = L.D; t0 = 0; load(L); }
+  __device__ void seek(const BwdLevels &L, int T) {
+    while (T >= t0 + nt) { t0 += nt; d--; load(L); }
   }
 };
 
@@ -663,7 +669,7 @@ constexpr int BW_SMEM = BW_ST * DA_STAGE + BW_EPI * BW_XS * 4 + 1024;
 template <int GATES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
     k_bwd_levels(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmU, BwdLevels L,
-                 int NTn, int KB, int total_tiles, const int32_t *__restrict__ gather,
+                 int KB, int total_tiles, const int32_t *__restrict__ gather,
                  const __nv_bfloat16 *__restrict__ Gact, int ld_g, const float *__restrict__ C, int ld, float *dA,
                  float *dCe, __nv_bfloat16 *dZ, int ld_z, int *rt_cnt, const int32_t *__restrict__ tstart,
                  int slabs) {
@@ -693,36 +699,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       BwdCursor cur;
-      cur.init(L, NTn);
+      cur.init(L);
       int it = 0;
       for (int T = pair; T < total_tiles; T += npairs) {
-        cur.seek(L, NTn, T);
-        const int lt = T - cur.t0;
+        cur.seek(L, T);
+        const int lt = T - cur.t0, NTn = cur.NTn, N = cur.N;
         {  // this pair tile's 256 dZ rows (and their dCe) complete
           const int ct = (cur.r0 - nl) + (lt / NTn) * PM;
           ptx::wait_counter(rt_cnt + ct, min(PM, cur.r1 - nl - ct) * slabs);
           ptx::fence_proxy_async_global();
         }
         const int mt = (cur.r0 - nl) + (lt / NTn) * PM + (int)rank * BM;
-        const int nb = (lt % NTn) * DA_N + (int)rank * (DA_N / 2);
+        const int nb = (lt % NTn) * N + (int)rank * (N / 2);
+        const uint32_t bytes = 2 * (DA_A_BYTES + (N / 2) * 128);
         for (int kb = 0; kb < KB; kb++, it++) {
           int s = it % ST;
           uint32_t ph = (it / ST) & 1;
           ptx::mbar_wait(&empty[s], ph ^ 1);
-          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], 2 * DA_STAGE);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], bytes);
           uint8_t *A = smem + s * DA_STAGE;
           ptx::tma_load_2d_pair(&tmZ, &full[s], A, kb * BK, mt);
-#pragma unroll
-          for (int ch = 0; ch < DA_N / 128; ch++)
+          for (int ch = 0; ch < N / 128; ch++)
             ptx::tma_load_2d_pair(&tmU, &full[s], A + DA_A_BYTES + ch * MN_CHUNK, nb + ch * 64, kb * BK);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16(PM, DA_N, 0, 1);
+      BwdCursor cur;
+      cur.init(L);
       int it = 0, tc = 0;
       for (int T = pair; T < total_tiles; T += npairs, tc++) {
+        cur.seek(L, T);
+        const uint32_t idesc = ptx::idesc_bf16(PM, cur.N, 0, 1);
         const int acc = tc & 1;
         ptx::mbar_wait(&tempty[acc], ((tc >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
@@ -746,10 +755,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
     const int q = warp & 3, grp = (warp - 4) >> 2;
     float *xs = xs_all + (warp - 4) * BW_XS;
     BwdCursor cur;
-    cur.init(L, NTn);
+    cur.init(L);
     int tc = 0;
     for (int T = pair; T < total_tiles; T += npairs, tc++) {
-      cur.seek(L, NTn, T);
+      cur.seek(L, T);
+      const int NTn = cur.NTn, N = cur.N;
       const int acc = tc & 1;
       const int lt = T - cur.t0;
       {  // order this warp's dCe reads after the tile's publication (already complete)
@@ -759,7 +769,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
       }
       const int c_row0 = (cur.r0 - nl) + (lt / NTn) * PM + (int)rank * BM + q * 32;  // cell of row 0
       const int c_end = cur.r1 - nl;
-      const int n0 = (lt % NTn) * DA_N;
+      const int n0 = (lt % NTn) * N;
       // per-row metadata for this warp's 32 rows: lane i <-> row i
       const int my_c = c_row0 + lane;
       const bool my_valid = my_c < c_end;
@@ -780,7 +790,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
       ptx::tc_fence_after();
       const uint32_t tl = tbase + acc * 256 + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-      for (int slab = grp; slab < DA_N / 64; slab += 2) {
+      for (int slab = grp; slab < N / 64; slab += 2) {
         // TMEM (thread = row) -> smem transpose buffer
         float v[64];
 #pragma unroll
@@ -1309,18 +1319,20 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
   FOLD_TRY(make_map(&tmZ, a.dZ, (uint64_t)gates * S, (uint64_t)a.n_cells, (uint64_t)a.ld_z * 2, BK, BM));
   const int ld_u = tc_ld_u(S);
   FOLD_TRY(make_map(&tmU, a.Ub, (uint64_t)ld_u, (uint64_t)gates * S, (uint64_t)ld_u * 2, 64, BK));
-  const int NTn = (int)cdiv(ld_u, DA_N);
-  int64_t total = 0;
-  for (int d = 2; d <= a.D; d++) total += cdiv(a.level_off_host[d + 1] - a.level_off_host[d], PM) * NTn;
-  if (total <= 0) return FOLD_OK;
-  if (total > INT32_MAX) return FOLD_E_INVALID;
   auto kern = gates == 5 ? k_bwd_levels<5> : k_bwd_levels<1>;
   FOLD_TRY(set_smem(kern, BW_SMEM));
   static thread_local int npairs_max = 0;
   if (!npairs_max) npairs_max = max_pairs(kern, BW_THREADS, BW_SMEM);
+  BwdLevels L{a.level_off, a.D, S, a.nl, ld_u, npairs_max};
+  int64_t total = 0;
+  for (int d = 2; d <= a.D; d++) {
+    const int M = a.level_off_host[d + 1] - a.level_off_host[d];
+    total += cdiv(M, PM) * cdiv(ld_u, bwd_level_N(L, M));
+  }
+  if (total <= 0) return FOLD_OK;
+  if (total > INT32_MAX) return FOLD_E_INVALID;
   const int npairs = total < npairs_max ? (int)total : npairs_max;
-  BwdLevels L{a.level_off, a.D, S, a.nl};
-  kern<<<2 * npairs, BW_THREADS, BW_SMEM, st>>>(tmZ, tmU, L, NTn, (int)cdiv(gates * S, BK), (int)total, a.gather,
+  kern<<<2 * npairs, BW_THREADS, BW_SMEM, st>>>(tmZ, tmU, L, (int)cdiv(gates * S, BK), (int)total, a.gather,
                                                a.Gact, a.ld_g, a.C, a.ld, a.dA, a.dCe, a.dZ, a.ld_z, a.rt_cnt,
                                                a.tstart, tc_bwd_slabs(S));
   FOLD_LAUNCH_CHECK();
