@@ -86,53 +86,58 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock, power and clock-event (throttle) reasons sampled DURING the timed region:
+    NVML polled every ~5 ms from a thread (the timed region is ~0.1 s, shorter than
+    nvidia-smi's sampling period); nvidia-smi -lms 200 as a fallback."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_slowdown"}
 
     def __init__(self, index: int):
         self.index = index
         self.rows = []
-        self.proc = None
+        self.stop_flag = False
+        self.t = None
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+
+    def _poll(self):
+        nv = self.nvml
+        while not self.stop_flag:
+            try:
+                self.rows.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                                  nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+        if self.nvml is None:
+            return
+        self.t = threading.Thread(target=self._poll, daemon=True)
+        self.t.start()
 
     def stop(self):
-        if self.proc is None:
+        if self.t is None:
             return None
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
+        self.stop_flag = True
         self.t.join(timeout=1)
-        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            if len(r) >= 8:
-                for k, v in zip(names, r[4:8]):
-                    if v.lower().startswith("active"):
-                        reasons.add(k)
-        if not sm:
+        if not self.rows:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        reasons = set()
+        for _, r in self.rows:
+            for bit, name in self.REASONS.items():
+                if r & bit:
+                    reasons.add(name)
+        sm = [c for c, _ in self.rows]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "sm_min_mhz": min(sm),
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvml, ~5 ms polling"}
 
 
 # ============================================================================ fold arm
@@ -315,7 +320,10 @@ def run_fold(args):
     flops_per_cell = 2.0 * gates * S * 2 * S  # one GEMM pass (fwd Z, bwd dA, or dU) per cell
     per_class = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
                  for k, v in prof.items() if v[1] > 0}
-    tensor_classes = {"cell_fwd": "k_cell_fwd_tc", "gemm_dA": "k_gemm_dA_tc", "gemm_dU": "k_gemm_dU_tc"}
+    # kernel per class: the persistent all-levels forward; the persistent all-levels backward
+    # (dA GEMM with the children's pointwise step fused into its epilogue; tree-like
+    # schedules, as every bench workload is); the all-cells weight-gradient GEMM
+    tensor_classes = {"cell_fwd": "k_fwd_levels", "gemm_dA": "k_bwd_levels", "gemm_dU": "k_gemm_dU_tc"}
     dom = max(tensor_classes, key=lambda k: prof[k][0])
     dom_ms_total, dom_launches = prof[dom]
     achieved = flops_per_cell * n_cells * args.steps / (dom_ms_total / 1e3) / 1e12

@@ -15,7 +15,7 @@ import collections
 
 KEYS = {
     "duration_ms": ("gpu__time_duration.sum", {"ms": 1, "us": 1e-3, "s": 1e3, "ns": 1e-6}),
-    "tensor_pipe_pct": ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", None),
+    "tensor_pipe_pct": ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", None),
     "dram_read_bytes": ("dram__bytes_read.sum", {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}),
     "dram_write_bytes": ("dram__bytes_write.sum", {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}),
     "l2_to_sm_bytes": ("l1tex__m_xbar2l1tex_read_bytes.sum", {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}),
@@ -83,9 +83,24 @@ if __name__ == "__main__":
         with open(os.path.join(out_dir, "launch_shares.txt"), "w") as f:
             f.write(launch_shares(args[i + 1]) + "\n")
         args = args[:i] + args[i + 2:]
+    traffic_out = None
+    if "--traffic" in args:
+        i = args.index("--traffic")
+        traffic_out = args[i + 1]
+        args = args[:i] + args[i + 2:]
     for rep in args:
         s = summarise_rep(rep)
         summ[os.path.basename(rep)] = s
+    if traffic_out:
+        # per-launch DRAM bytes keyed by the kernel's short name (bench.py's roofline traffic)
+        tr = {"_note": "dram__bytes_read.sum + dram__bytes_write.sum of one captured launch per kernel "
+                       "(ncu --set full --clock-control none), C2 B=1024 S=1024 bf16; see ncu_summary.json"}
+        for rep, v in summ.items():
+            short = v["kernel"].split("(")[0].replace("void ", "").split("::")[-1].split("<")[0]
+            tr[short] = {"dram_bytes_per_launch": v.get("dram_bytes"), "launch": "one launch per step (%s)" % rep,
+                         "duration_ms_under_ncu": v.get("duration_ms"), "tensor_pipe_pct": v.get("tensor_pipe_pct")}
+        with open(traffic_out, "w") as f:
+            json.dump(tr, f, indent=1)
     with open(os.path.join(out_dir, "ncu_summary.json"), "w") as f:
         json.dump(summ, f, indent=1)
     print(json.dumps(summ, indent=1)[:3000])
