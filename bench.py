@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--ref-trees", type=int, default=1, help="trees per oracle step (--impl reference)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the nodes/s vs batch-size sweep")
+    ap.add_argument("--no-table1", action="store_true",
+                    help="skip the unbatched baseline and the PAPER.md Table 1 reproduction")
     return ap.parse_args()
 
 
@@ -177,10 +179,12 @@ def run_fold(args):
     ws = fold.Workspace(dev)
     sched_ws = torch.empty(1, dtype=torch.uint8, device=dev)
 
-    def step(op, child, token, root, g):
+    def step(op, child, token, root, g, level=None, train=True):
         nonlocal sched_ws
-        s = fold.schedule(op, child, token, root, V, workspace=sched_ws)
+        s = fold.schedule(op, child, token, root, V, workspace=sched_ws, level=level)
         h, c, acts = fold.forward(s, model, ws=ws, want_c=False)
+        if not train:
+            return h
         fold.backward(s, model, acts, g, grads=(dU, db, dE), ws=ws)
         if world > 1:
             dist.all_reduce(flat_g)
@@ -308,6 +312,11 @@ def run_fold(args):
             sweep[str(Bs)] = {"nodes_per_s": sub.n_nodes / (msb / 1e3), "ms_per_step": msb}
         sweep[str(gr.n_graphs)] = {"nodes_per_s": value / world, "ms_per_step": ms_per_step}
 
+    # ---------------- unbatched baseline + PAPER.md Table 1 on B200 (rank 0)
+    t1 = None
+    if not args.no_table1 and rank == 0 and args.config in ("c2", "c5"):
+        t1 = table1(step, fold, gr, g_dev, V, S, dev)
+
     if world > 1:
         dist.barrier()
     if rank != 0:
@@ -374,9 +383,83 @@ def run_fold(args):
     if batch1:
         out["batch1"] = batch1
         out["speedup_vs_batch1"] = (value / world) / batch1["nodes_per_s"]
+    if t1:
+        ub = t1.pop("unbatched")
+        out["unbatched"] = ub
+        out["speedup_vs_unbatched"] = (value / world) / ub["nodes_per_s"]
+        out["table1"] = t1
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _time(fn, nrep, warm=2):
+    import torch
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(nrep):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / nrep
+
+
+def table1(step, fold, gr, g_dev, V, S, dev):
+    """PAPER.md L83-L127 / Table 1 with our kernels on B200, training (fwd+bwd+SGD, the
+    bench step) and inference (schedule + forward) per-tree times.
+      unbatched:   ONE tree of the headline workload, manual levels (one cell per level:
+                   the node-at-a-time, batch-size-1 evaluation), the speedup denominator
+                   of BASELINE.json's "speedup vs unbatched".
+      manual:      B copies of one random 128-leaf shape, every tree position its own op
+                   (foldgen.manual_levels), batched across trees only (L83).
+      dynamic:     the same batch under the dynamic-batching schedule (L40-44).
+      full_dynamic: B random 128-leaf shapes, dynamic batching (L86 "full dynamic").
+    cost_ratio = dynamic / manual per-tree time (L114 column); speedup_ratio = manual
+    B=1 per-tree time / full-dynamic per-tree time at B (L127 column)."""
+    import torch
+
+    def dev_graphs(g, manual):
+        t = fold.graphs_to_device(g, dev)
+        lv = torch.from_numpy(foldgen.manual_levels(g)).to(dev) if manual else None
+        return t, lv
+
+    def per_tree(g, manual, train, nrep):
+        t, lv = dev_graphs(g, manual)
+        gg = g_dev[:g.n_graphs].contiguous() if g.n_graphs <= g_dev.shape[0] else \
+            torch.ones((g.n_graphs, S), device=dev) * 0.01
+        ms = _time(lambda: step(*t, gg, level=lv, train=train), nrep)
+        return ms / g.n_graphs
+
+    one = foldgen.sub_batch(gr, 0, 1)
+    ms_ub = per_tree(one, True, True, 10)
+    out = {"unbatched": {"nodes_per_s": one.n_nodes / (ms_ub / 1e3), "ms_per_tree": ms_ub,
+                         "levels": 1 + int((one.op == 1).sum()),
+                         "how": "one tree of the headline workload, manual levels (one cell per level), "
+                                "schedule+fwd+bwd+sgd"}}
+    rows = {}
+    for B in (1, 32, 64, 128, 256, 512, 1024):
+        same = foldgen.table1_batch(B, True, vocab=V)
+        full = foldgen.table1_batch(B, False, vocab=V)
+        nrep = 10 if B >= 256 else 20
+        row = {}
+        for mode, train in (("train", True), ("infer", False)):
+            m = per_tree(same, True, train, nrep)
+            d = per_tree(same, False, train, nrep)
+            f = per_tree(full, False, train, nrep)
+            row[mode] = {"manual_ms_per_tree": m, "dynamic_ms_per_tree": d, "full_dynamic_ms_per_tree": f,
+                         "cost_ratio": d / m}
+        rows[str(B)] = row
+    for mode in ("train", "infer"):
+        m1 = rows["1"][mode]["manual_ms_per_tree"]
+        for B, row in rows.items():
+            row[mode]["speedup_ratio"] = m1 / row[mode]["full_dynamic_ms_per_tree"]
+    out["rows"] = rows
+    out["workload"] = "random-split 128-leaf trees (Table 1: 'tree size is 128'), TreeLSTM S=1024, bf16"
+    return out
 
 
 def cpu_baseline(gr, cell, p, g_host, n_trees):

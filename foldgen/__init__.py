@@ -203,6 +203,35 @@ def config_c5(B: int = 8192, seed: int = GRAPH_SEED, vocab: int = 16384) -> Grap
     return batch_from_shapes(shapes, uniform_tokens(rng, vocab), vocab)
 
 
+def table1_batch(B: int, same_shape: bool, seed: int = GRAPH_SEED, vocab: int = 16384,
+                 leaves: int = 128) -> Graphs:
+    """PAPER.md L83/L86 Table 1 inputs: random binary trees of 128 leaves. same_shape=True:
+    "a batch of random binary trees, all of which have the same shape" (the manual and
+    "dynamic" columns); False: each tree its own random shape ("full dynamic")."""
+    rng = np.random.default_rng(seed)
+    if same_shape:
+        return replicate_shape(random_split_shape(rng, leaves), B, uniform_tokens(rng, vocab), vocab)
+    shapes = [random_split_shape(rng, leaves) for _ in range(B)]
+    return batch_from_shapes(shapes, uniform_tokens(rng, vocab), vocab)
+
+
+def manual_levels(gr: Graphs) -> np.ndarray:
+    """Caller-fixed levels of the manual-batching baseline ("For the manual
+    batching tests, we construct a static data-flow graph of operations corresponding to
+    the shape of the tree"): every tree position is its own operation. Leaves (EMBED,
+    no dependencies) are level 1; the j-th cell of a tree in node (post-)order is level
+    2 + j, so trees of one shape batch position by position and a single tree runs one
+    node at a time (the unbatched, batch-size-1 evaluation). Input preparation only:
+    the levels are the static graph's op order, not a schedule computation."""
+    level = np.ones(gr.n_nodes, np.int32)
+    off = 0
+    for n in gr.tree_sizes.tolist():
+        cells = np.nonzero(gr.op[off:off + n] == CELL)[0]
+        level[off + cells] = 2 + np.arange(len(cells), dtype=np.int32)
+        off += n
+    return level
+
+
 CONFIG_STATE = {"c1": 16, "c2": 1024, "c3": 300, "c4": 1024, "c5": 1024}
 
 

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FOLD_ABI_VERSION 1
+#define FOLD_ABI_VERSION 2
 
 typedef enum {
   FOLD_OK = 0,
@@ -58,6 +58,9 @@ typedef enum {
   FOLD_E_OP_RANGE = 10,     /* op[n] not in {FOLD_OP_EMBED, FOLD_OP_CELL} */
   FOLD_E_UNSUPPORTED = 11,  /* valid request this build does not implement
                                (e.g. not an sm_100 device) */
+  FOLD_E_LEVEL = 12,        /* caller-fixed levels (fold_graphs.level) violate
+                               level[n] in [1, n_nodes], level[EMBED] == 1,
+                               level[CELL] > level[each child] */
 } fold_status;
 
 /* Operation ids = the enumeration order of PAPER.md L32/L43 ("all operations ... be
@@ -79,16 +82,28 @@ enum { FOLD_PREC_FP32 = 0, FOLD_PREC_BF16 = 2 };
  *   token[n]         int32 in [0, vocab) for EMBED; ignored for CELL.
  *   root[g]          int32 node whose state is graph g's result.
  * Any node order is accepted (children need not precede parents); DAG sharing and
- * child[2n] == child[2n+1] are allowed. All pointers are device. */
+ * child[2n] == child[2n+1] are allowed. All pointers are device.
+ *   level[n]         OPTIONAL (NULL = dynamic batching). Caller-fixed schedule levels
+ *                    that replace L40's depth: the "manual batching" baseline of
+ *                    PAPER.md L83 / Table 1 ("we construct a static data-flow graph of
+ *                    operations corresponding to the shape of the tree"), where every
+ *                    tree position is its own operation, batched only across trees of
+ *                    the same shape; with one tree it is the unbatched, node-at-a-time
+ *                    evaluation. Requires level[n] in [1, n_nodes], == 1 for EMBED, and
+ *                    level[n] > level[c] for each child c of a CELL (checked after
+ *                    ROOT_RANGE, error FOLD_E_LEVEL, smallest offending node); levels
+ *                    may skip values (empty levels are allowed). */
 typedef struct {
   int32_t n_nodes, n_graphs, vocab;
   const int32_t *op, *child, *token, *root;
+  const int32_t *level;
 } fold_graphs;
 
 /* ----------------------------------------------------------------- schedule
  * Executor-form schedule; all arrays device, caller-allocated with the sizes below
  * (N = n_nodes, G = n_graphs). Definitions (bit-exact with oracle/fold_oracle.c):
  *   depth[N]       PAPER.md L40: EMBED = 1 (its token constant is depth 0);
+ *                  (with caller levels: depth[n] = level[n])
  *                  CELL = 1 + max(depth of children).
  *   perm[N]        pool row -> node: rows ordered by (depth, op, node id) (L42-43).
  *   rank[N]        node -> pool row (= perm^-1).
@@ -123,7 +138,8 @@ typedef struct {
 size_t fold_schedule_workspace(int32_t n_nodes, int32_t n_graphs);
 
 /* Validate + schedule. Errors in this order (smallest offending id): CHILD_RANGE,
- * OP_RANGE, ARITY, TOKEN_RANGE, ROOT_RANGE, CYCLE. On error the schedule arrays are
+ * OP_RANGE, ARITY, TOKEN_RANGE, ROOT_RANGE, LEVEL (only with caller levels), CYCLE
+ * (only without: strictly increasing levels exclude cycles). On error the schedule arrays are
  * unspecified. Exactly one blocking D2H copy (two if n_levels + 2 > 4096). */
 fold_status fold_schedule(const fold_graphs *graphs, fold_schedule_t *sched,
                           void *d_workspace, size_t workspace_bytes, void *stream);

@@ -31,7 +31,7 @@ _lock = threading.Lock()
 _lib = None
 
 STATUS = {0: "OK", 1: "INVALID", 2: "CHILD_RANGE", 3: "ARITY", 4: "TOKEN_RANGE",
-          5: "ROOT_RANGE", 6: "CYCLE", 10: "OP_RANGE"}
+          5: "ROOT_RANGE", 6: "CYCLE", 10: "OP_RANGE", 12: "LEVEL"}
 CELLS = {"treernn": 0, "treelstm": 1}
 
 
@@ -75,12 +75,14 @@ class OracleError(RuntimeError):
         self.node = node
 
 
-def schedule(op, child, token, root, vocab):
-    """Executor-form schedule (see fold_oracle.c `oracle_schedule`). Returns a dict of
+def schedule(op, child, token, root, vocab, level=None):
+    """Executor-form schedule (see fold_oracle.c `oracle_schedule`); `level` = optional
+    caller-fixed levels (manual batching). Returns a dict of
     int32 arrays sized to their logical lengths, plus n_levels/n_leaves/n_cells/n_tok_segs.
     Raises OracleError with the status name and offending node on invalid input."""
     lib = _load()
     op, child, token, root = _i32(op), _i32(child).reshape(-1), _i32(token), _i32(root)
+    level = _i32(level) if level is not None else None
     N, G = len(op), len(root)
     out = {k: np.zeros(n, np.int32) for k, n in [
         ("depth", N), ("perm", N), ("rank", N), ("gather", 2 * N), ("level_off", N + 2),
@@ -88,7 +90,7 @@ def schedule(op, child, token, root, vocab):
         ("leaf_perm", N), ("tok_seg", N + 1), ("root_row", G), ("root_perm", G)]}
     info = np.zeros(5, np.int32)
     st = lib.oracle_schedule(ctypes.c_int(N), ctypes.c_int(G), ctypes.c_int(vocab),
-                             _p(op), _p(child), _p(token), _p(root),
+                             _p(op), _p(child), _p(token), _p(root), _p(level),
                              *[_p(out[k]) for k in ("depth", "perm", "rank", "gather", "level_off",
                                                     "group_off", "cons_off", "cons_edge", "leaf_perm",
                                                     "tok_seg", "root_row", "root_perm")], _p(info))
@@ -123,16 +125,18 @@ def forward(cell, op, child, token, root, U, b, E, all_nodes=False):
     return (hr, cr, H, C) if all_nodes else (hr, cr)
 
 
-def forward_levels(cell, op, child, token, root, U, b, E):
-    """Level-ordered fp64 forward over this oracle's own schedule; (H[N,S], C[N,S])."""
+def forward_levels(cell, op, child, token, root, U, b, E, level=None):
+    """Level-ordered fp64 forward over this oracle's own schedule (optionally with
+    caller-fixed levels); (H[N,S], C[N,S])."""
     lib = _load()
     op, child, token, root = _i32(op), _i32(child).reshape(-1), _i32(token), _i32(root)
+    level = _i32(level) if level is not None else None
     U, b, E = _f64(U), _f64(b), _f64(E)
     N, G = len(op), len(root)
     V, S = E.shape
     H = np.zeros((N, S)); C = np.zeros((N, S))
     st = lib.oracle_forward_levels(CELLS[cell], S, N, G, V, _p(op), _p(child), _p(token), _p(root),
-                                   _p(U), _p(b), _p(E), _p(H), _p(C))
+                                   _p(level), _p(U), _p(b), _p(E), _p(H), _p(C))
     if st != 0:
         raise OracleError(st)
     return H, C

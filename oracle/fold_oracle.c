@@ -17,6 +17,8 @@
  *   oracle_forward_levels— the same values computed level by level from this
  *                          oracle's own schedule (PAPER.md L47 loop model); used
  *                          only to pin "batched == unbatched" bitwise.
+ *   (both schedule functions take optional caller-fixed levels: the manual-batching
+ *    baseline of PAPER.md L83 / Table 1, where each tree position is its own op)
  *   oracle_backward      — hand-derived reverse mode ("gradients ...
  *                          do not require any additional code" in TF; here written
  *                          out), pinned by finite differences in tests/.
@@ -41,7 +43,8 @@
 #include <string.h>
 
 enum { OR_OK = 0, OR_E_INVALID = 1, OR_E_CHILD_RANGE = 2, OR_E_ARITY = 3,
-       OR_E_TOKEN_RANGE = 4, OR_E_ROOT_RANGE = 5, OR_E_CYCLE = 6, OR_E_OP_RANGE = 10 };
+       OR_E_TOKEN_RANGE = 4, OR_E_ROOT_RANGE = 5, OR_E_CYCLE = 6, OR_E_OP_RANGE = 10,
+       OR_E_LEVEL = 12 };
 enum { OR_EMBED = 0, OR_CELL = 1, OR_N_OPS = 2 };
 enum { OR_TREERNN = 0, OR_TREELSTM = 1 };
 
@@ -66,6 +69,23 @@ static int validate(int N, int G, int V, const int32_t *op, const int32_t *child
         if (op[n] == OR_EMBED && (token[n] < 0 || token[n] >= V)) { *err = n; return OR_E_TOKEN_RANGE; }
     for (int g = 0; g < G; g++)
         if (root[g] < 0 || root[g] >= N) { *err = g; return OR_E_ROOT_RANGE; }
+    return OR_OK;
+}
+
+/* Caller-fixed levels (manual batching: "For the manual batching tests, we
+ * construct a static data-flow graph of operations corresponding to the shape of the
+ * tree"): a level replaces the L40 depth. Valid when every EMBED has level 1, every
+ * level is in [1, N] and every CELL's level exceeds both children's levels (so the
+ * level order is a topological order). Smallest offending node id. */
+static int validate_levels(int N, const int32_t *op, const int32_t *child, const int32_t *level,
+                           int32_t *err)
+{
+    for (int n = 0; n < N; n++) {
+        int bad = level[n] < 1 || level[n] > N;
+        if (op[n] == OR_EMBED && level[n] != 1) bad = 1;
+        if (op[n] == OR_CELL && (level[n] <= level[child[2 * n]] || level[n] <= level[child[2 * n + 1]])) bad = 1;
+        if (bad) { *err = n; return OR_E_LEVEL; }
+    }
     return OR_OK;
 }
 
@@ -142,7 +162,7 @@ static int assign_depths(int N, const int32_t *op, const int32_t *child,
  * info[0..4] = n_levels (D), n_leaves, n_cells, n_tok_segs, err_node.
  */
 int oracle_schedule(int N, int G, int V, const int32_t *op, const int32_t *child,
-                    const int32_t *token, const int32_t *root,
+                    const int32_t *token, const int32_t *root, const int32_t *level,
                     int32_t *depth, int32_t *perm, int32_t *rank, int32_t *gather,
                     int32_t *level_off, int32_t *group_off, int32_t *cons_off,
                     int32_t *cons_edge, int32_t *leaf_perm, int32_t *tok_seg,
@@ -153,10 +173,16 @@ int oracle_schedule(int N, int G, int V, const int32_t *op, const int32_t *child
     if (N < 0 || G < 0 || V < 0) return OR_E_INVALID;
     int st = validate(N, G, V, op, child, token, root, &err);
     if (st != OR_OK) { info[4] = err; return st; }
-    int32_t *topo = (int32_t *)malloc(sizeof(int32_t) * ((size_t)N + 1));
-    st = assign_depths(N, op, child, depth, topo, &err);
-    free(topo);
-    if (st != OR_OK) { info[4] = err; return st; }
+    if (level) {   /* manual batching: the caller's levels are the depths */
+        st = validate_levels(N, op, child, level, &err);
+        if (st != OR_OK) { info[4] = err; return st; }
+        for (int n = 0; n < N; n++) depth[n] = level[n];
+    } else {
+        int32_t *topo = (int32_t *)malloc(sizeof(int32_t) * ((size_t)N + 1));
+        st = assign_depths(N, op, child, depth, topo, &err);
+        free(topo);
+        if (st != OR_OK) { info[4] = err; return st; }
+    }
 
     int D = 0;
     for (int n = 0; n < N; n++) if (depth[n] > D) D = depth[n];
@@ -310,7 +336,8 @@ int oracle_forward(int cell, int S, int N, int G, int V,
  * results). Row r of the pool holds node perm[r]. Outputs in node-id order. */
 int oracle_forward_levels(int cell, int S, int N, int G, int V,
                           const int32_t *op, const int32_t *child, const int32_t *token,
-                          const int32_t *root, const double *U, const double *b, const double *E,
+                          const int32_t *root, const int32_t *level,
+                          const double *U, const double *b, const double *E,
                           double *H_out, double *C_out)
 {
     int32_t *depth = malloc(sizeof(int32_t) * (N + 1)), *perm = malloc(sizeof(int32_t) * (N + 1));
@@ -321,7 +348,7 @@ int oracle_forward_levels(int cell, int S, int N, int G, int V,
     int32_t *rr = malloc(sizeof(int32_t) * (G + 1)), *rp = malloc(sizeof(int32_t) * (G + 1));
     int32_t info[5];
     int gates = (cell == OR_TREELSTM) ? 5 : 1;
-    int st = oracle_schedule(N, G, V, op, child, token, root, depth, perm, rank, gat, lo, go,
+    int st = oracle_schedule(N, G, V, op, child, token, root, level, depth, perm, rank, gat, lo, go,
                              co, ce, lp, ts, rr, rp, info);
     if (st == OR_OK) {
         int D = info[0];

@@ -357,6 +357,7 @@ const char *fold_status_string(fold_status s) {
     case FOLD_E_MISMATCH: return "FOLD_E_MISMATCH";
     case FOLD_E_OP_RANGE: return "FOLD_E_OP_RANGE";
     case FOLD_E_UNSUPPORTED: return "FOLD_E_UNSUPPORTED";
+    case FOLD_E_LEVEL: return "FOLD_E_LEVEL";
   }
   return "FOLD_E_UNKNOWN";
 }

@@ -32,9 +32,10 @@ enum {
   F_BAR = 16,   // grid barrier count, generation (16, 17)
   F_NFLAGS = 64
 };
-enum { E_CHILD = 0, E_OP = 1, E_ARITY = 2, E_TOKEN = 3, E_ROOT = 4, E_CYCLE = 5, E_NCLASS = 6 };
+enum { E_CHILD = 0, E_OP = 1, E_ARITY = 2, E_TOKEN = 3, E_ROOT = 4, E_LEVEL = 5, E_CYCLE = 6, E_NCLASS = 7 };
 const fold_status kErrStatus[E_NCLASS] = {FOLD_E_CHILD_RANGE, FOLD_E_OP_RANGE, FOLD_E_ARITY,
-                                         FOLD_E_TOKEN_RANGE, FOLD_E_ROOT_RANGE, FOLD_E_CYCLE};
+                                         FOLD_E_TOKEN_RANGE, FOLD_E_ROOT_RANGE, FOLD_E_LEVEL,
+                                         FOLD_E_CYCLE};
 
 constexpr int kScanThreads = 1024;
 constexpr int kScanTile = kScanThreads * 4;
@@ -193,6 +194,7 @@ fold_status excl_scan(const int32_t *in, int32_t *out, int64_t n, int32_t *sums,
 struct SchedArgs {
   int N, G, V;
   const int32_t *op, *child, *token, *root;
+  const int32_t *level;  // caller-fixed levels (manual batching) or nullptr
   fold_schedule_t s;  // output arrays (device pointers)
   SchedWs w;
 };
@@ -404,6 +406,14 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
     if (o == FOLD_OP_EMBED && (a.token[n] < 0 || a.token[n] >= V)) atomicMin(&flags[F_ERR0 + E_TOKEN], n);
     const bool good_cell = (o == FOLD_OP_CELL) && !crange && c0 >= 0 && c1 >= 0;
     if (good_cell) { atomicAdd(&w.ncons[c0], 1); atomicAdd(&w.ncons[c1], 1); }
+    if (a.level) {  // manual batching: level[EMBED] == 1, level[CELL] > level[children], <= N
+      const int lv = a.level[n];
+      bool bad = lv < 1 || lv > N;
+      if (o == FOLD_OP_EMBED) bad = bad || lv != 1;
+      if (good_cell) bad = bad || lv <= a.level[c0] || lv <= a.level[c1];
+      if (bad && (o == FOLD_OP_EMBED || good_cell)) atomicMin(&flags[F_ERR0 + E_LEVEL], n);
+      if (o == FOLD_OP_EMBED || good_cell) atomicMax(&flags[F_MAXDEPTH], lv < 1 ? 1 : lv);
+    }
     w.pending[n] = (o == FOLD_OP_CELL) ? (good_cell ? 2 : kPendingInvalid) : 0;
   }
   for (int64_t g = gtid; g < G; g += gstride)
@@ -428,7 +438,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
           w.pcons[w.pcons_off[c1] + atomicAdd(&w.fillc[c1], 1)] = n;
         }
         leaf = (o == FOLD_OP_EMBED);
-        s.depth[n] = leaf ? 1 : -1;
+        s.depth[n] = a.level ? a.level[n] : (leaf ? 1 : -1);
       }
       const int slot = warp_push(&flags[F_QCNT + 1], leaf);
       if (leaf) w.q0[slot] = n;
@@ -441,7 +451,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
   // ---- P4: level-synchronous depth propagation: a parent whose last
   // pending child finishes at level L gets depth L + 1; one barrier per level
   int L = 1;
-  for (;; L++) {
+  for (; !a.level; L++) {
     const int ncur = ld_volatile(&flags[F_QCNT + (L % 3)]);
     if (ncur == 0) break;
     const int32_t *cur = (L & 1) ? w.q0 : w.q1;
@@ -466,8 +476,8 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
     }
     gsync(flags);
   }
-  const int D = L - 1;
-  if (gtid == 0) flags[F_MAXDEPTH] = D;
+  const int D = a.level ? ld_volatile(&flags[F_MAXDEPTH]) : L - 1;
+  if (gtid == 0 && !a.level) flags[F_MAXDEPTH] = D;
 
   // ---- P5: sort keys (cycle: a node never reached keeps depth -1)
   for (int64_t i = gtid; i < N; i += gstride) {
@@ -625,7 +635,7 @@ fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr
   int blocks = N <= kSmallN ? 1 : (int)cdiv(N, 2048);
   if (blocks > max_blocks) blocks = max_blocks;
   FOLD_CUDA_TRY(cudaMemsetAsync(w.flags + F_BAR, 0, 2 * sizeof(int32_t), st));
-  SchedArgs args{N, G, V, gr->op, gr->child, gr->token, gr->root, *s, w};
+  SchedArgs args{N, G, V, gr->op, gr->child, gr->token, gr->root, gr->level, *s, w};
   void *kargs[] = {(void *)&args};
   FOLD_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_schedule, dim3(blocks), dim3(kSchedThreads), kargs,
                                             dsmem, st));

@@ -23,7 +23,8 @@ from . import build as _build
 
 OK = 0
 STATUS = {0: "OK", 1: "INVALID", 2: "CHILD_RANGE", 3: "ARITY", 4: "TOKEN_RANGE", 5: "ROOT_RANGE",
-          6: "CYCLE", 7: "WORKSPACE", 8: "CUDA", 9: "MISMATCH", 10: "OP_RANGE", 11: "UNSUPPORTED"}
+          6: "CYCLE", 7: "WORKSPACE", 8: "CUDA", 9: "MISMATCH", 10: "OP_RANGE", 11: "UNSUPPORTED",
+          12: "LEVEL"}
 CELLS = {"treernn": 0, "treelstm": 1}
 PRECS = {"fp32": 0, "bf16": 2}
 
@@ -34,7 +35,7 @@ _f32p = ctypes.POINTER(ctypes.c_float)
 class _Graphs(ctypes.Structure):
     _fields_ = [("n_nodes", ctypes.c_int32), ("n_graphs", ctypes.c_int32), ("vocab", ctypes.c_int32),
                 ("op", ctypes.c_void_p), ("child", ctypes.c_void_p), ("token", ctypes.c_void_p),
-                ("root", ctypes.c_void_p)]
+                ("root", ctypes.c_void_p), ("level", ctypes.c_void_p)]
 
 
 _SCHED_ARRAYS = ("depth", "perm", "rank", "gather", "level_off", "group_off", "cons_off", "cons_edge",
@@ -200,12 +201,13 @@ class Schedule:
 
 
 def schedule(op: torch.Tensor, child: torch.Tensor, token: torch.Tensor, root: torch.Tensor, vocab: int,
-             stream=None, workspace: torch.Tensor | None = None) -> Schedule:
-    """fold_schedule over int32 device tensors op[N], child[N,2], token[N], root[G]."""
+             stream=None, workspace: torch.Tensor | None = None, level: torch.Tensor | None = None) -> Schedule:
+    """fold_schedule over int32 device tensors op[N], child[N,2], token[N], root[G];
+    `level` = optional caller-fixed levels [N] (manual batching, fold.h fold_graphs.level)."""
     L = load()
     dev = op.device
     N, G = int(op.shape[0]), int(root.shape[0])
-    for t in (op, child, token, root):
+    for t in (op, child, token, root) + ((level,) if level is not None else ()):
         assert t.dtype == torch.int32 and t.is_cuda and t.is_contiguous()
     sizes = {"depth": N, "perm": N, "rank": N, "gather": 2 * N, "level_off": N + 2, "group_off": 2 * N + 3,
              "cons_off": N + 1, "cons_edge": 2 * N, "leaf_perm": N, "tok_seg": N + 1, "root_row": G,
@@ -215,7 +217,8 @@ def schedule(op: torch.Tensor, child: torch.Tensor, token: torch.Tensor, root: t
     ws_bytes = int(L.fold_schedule_workspace(N, G))
     if workspace is None or workspace.numel() < ws_bytes:
         workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
-    g = _Graphs(N, G, int(vocab), op.data_ptr(), child.data_ptr(), token.data_ptr(), root.data_ptr())
+    g = _Graphs(N, G, int(vocab), op.data_ptr(), child.data_ptr(), token.data_ptr(), root.data_ptr(),
+                level.data_ptr() if level is not None else None)
     s = _Sched(*[arrays[k].data_ptr() for k in _SCHED_ARRAYS], host.ctypes.data, 0, 0, 0, 0, 0, 0, 0)
     _check(L.fold_schedule(ctypes.byref(g), ctypes.byref(s), ctypes.c_void_p(workspace.data_ptr()),
                            ws_bytes, _stream(stream)), "fold_schedule")
