@@ -63,20 +63,29 @@ def parse():
 DEFAULT_B = {"c1": None, "c2": 1024, "c3": 1024, "c4": 1024, "c5": 8192}
 
 
-def workload(args, rank=0):
+def workload(args, rank=0, world=1):
+    """C2/C3/C4: every rank runs its own B-tree batch (weak scaling, seed + rank). C5: ONE
+    global batch of B trees sharded across the ranks by node count (strong scaling,
+    SURVEY §8(e)); returns (graphs of this rank, cell, S, description, global node count)."""
     cfg = args.config
     B = args.batch or DEFAULT_B[cfg]
     cell = args.cell or ("treernn" if cfg == "c1" else "treelstm")
     S = foldgen.CONFIG_STATE[cfg]
+    if cfg == "c5":
+        from paper_1702_02181_b200 import dp
+        full = foldgen.make_config(cfg, B)
+        gr = dp.shard(full, rank, world)
+        desc = (f"C5 random-split 128-leaf trees, global batch {full.n_graphs} sharded by node count over "
+                f"{world} GPU(s), TreeLSTM S=1024, V=16384")
+        return gr, cell, S, desc, full.n_nodes
     gr = foldgen.make_config(cfg, B, seed=foldgen.GRAPH_SEED + rank)
     desc = {
         "c1": "C1 TreeRNN, 8 random-split trees (<=16 leaves), S=16, V=32",
         "c2": f"C2 complete-128-leaf binary trees, B={gr.n_graphs}/GPU, TreeLSTM S=1024, V=16384",
         "c3": f"C3 parse-shaped trees (1-60 leaves), B={gr.n_graphs}/GPU, TreeLSTM S=300, V=16384 Zipf",
         "c4": f"C4 chain-256 (depth 256), B={gr.n_graphs}/GPU, TreeLSTM S=1024",
-        "c5": f"C5 random-split 128-leaf trees, B={gr.n_graphs}/GPU, TreeLSTM S=1024",
     }[cfg]
-    return gr, cell, S, desc
+    return gr, cell, S, desc, world * gr.n_nodes
 
 
 def peaks():
@@ -159,7 +168,8 @@ def run_fold(args):
     dev = torch.device("cuda", local)
     fold.device_check()
 
-    gr, cell, S, desc = workload(args, rank)
+    gr, cell, S, desc, global_nodes = workload(args, rank, world)
+    strong = args.config == "c5"
     V = gr.vocab
     gates = foldgen.gates_of(cell)
     N_nodes = gr.n_nodes
@@ -227,7 +237,7 @@ def run_fold(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     ms_per_step = ms_max / args.steps
-    value = world * N_nodes / (ms_per_step / 1e3)
+    value = global_nodes / (ms_per_step / 1e3)
 
     # ---------------- e2e: host buffers, H2D + D2H inside the timed region
     e2e = None
@@ -264,7 +274,7 @@ def run_fold(args):
         if world > 1:
             dist.all_reduce(t2, op=dist.ReduceOp.MAX)
         e_ms = float(t2.item()) / args.steps
-        e2e = {"value": world * N_nodes / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
+        e2e = {"value": global_nodes / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
     # ---------------- batch-1 (within-tree batching only) for the speedup-vs-batch-size context
@@ -363,7 +373,8 @@ def run_fold(args):
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": args.prec, "data": "synthetic",
         "config": {"workload": desc, "trees_per_gpu": gr.n_graphs, "nodes_per_gpu": N_nodes,
                    "cells_per_gpu": n_cells, "state": S, "cell": cell, "levels": n_levels,
@@ -472,9 +483,33 @@ def cpu_baseline(gr, cell, p, g_host, n_trees):
     oracle.forward(cell, sub.op, sub.child, sub.token, sub.root, p.U, p.b, p.E)
     oracle.backward(cell, sub.op, sub.child, sub.token, sub.root, p.U, p.b, p.E, g)
     dt = time.perf_counter() - t0
-    return {"value": sub.n_nodes / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"first {sub.n_graphs} trees ({sub.n_nodes} nodes) of the same batch, fp64 "
-                      f"forward + backward, single thread, {dt:.1f} s"}
+    out = {"value": sub.n_nodes / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+           "sample": f"first {sub.n_graphs} trees ({sub.n_nodes} nodes) of the same batch, fp64 "
+                     f"forward + backward, single thread, {dt:.1f} s"}
+    # all host cores: one tree per task on a thread pool (the oracle's C
+    # calls release the GIL), as many trees as cores, same workload
+    import concurrent.futures
+    cores = len(os.sched_getaffinity(0))
+    per = max(1, sub.n_graphs // 2)  # trees per task (same per-call overhead as the 1-thread run)
+    ntr = min(cores * per, gr.n_graphs)
+    tasks = [(i, min(i + per, ntr)) for i in range(0, ntr, per)]
+    trees = [foldgen.sub_batch(gr, a, b) for a, b in tasks]
+    U64, b64, E64 = (np.ascontiguousarray(x, dtype=np.float64) for x in (p.U, p.b, p.E))
+
+    def one(i):
+        t = trees[i]
+        a = tasks[i][0]
+        oracle.forward(cell, t.op, t.child, t.token, t.root, U64, b64, E64)
+        oracle.backward(cell, t.op, t.child, t.token, t.root, U64, b64, E64, g_host[a:a + t.n_graphs])
+    t0 = time.perf_counter()
+    with concurrent.futures.ThreadPoolExecutor(max_workers=cores) as ex:
+        list(ex.map(one, range(len(tasks))))
+    dta = time.perf_counter() - t0
+    nn = sum(t.n_nodes for t in trees)
+    out["all_cores"] = {"value": nn / dta, "unit": UNIT, "cores": cores,
+                        "sample": f"first {ntr} trees ({nn} nodes), {per} tree(s) per task on {cores} threads, "
+                                  f"{dta:.1f} s"}
+    return out
 
 
 # ============================================================================ reference arm
@@ -487,7 +522,7 @@ def run_reference(args):
     if rank != 0:
         return
     import oracle
-    gr, cell, S, desc = workload(args, 0)
+    gr, cell, S, desc, _ = workload(args, 0, 1)
     p = foldgen.make_params(cell, S, gr.vocab)
     g_host = foldgen.make_upstream(gr.n_graphs, S)
     sub = foldgen.sub_batch(gr, 0, min(args.ref_trees, gr.n_graphs))

@@ -171,8 +171,10 @@ typedef struct {
  *                                         of cell c's left / right child (written by the
  *                                         producer of that child; read by the level GEMM
  *                                         and by the weight-gradient GEMM)
- *   G [n_cells][gates*S] bf16 / fp32      saved gate activations (i, fL, fR, o, u)
- *                                         or h (TreeRNN) per cell
+ *   G [n_cells][gates][ld] bf16 / fp32    saved gate activations (i, fL, fR, o, u)
+ *                                         or h (TreeRNN) per cell; gate g of state
+ *                                         column j at g*ld + j (every gate block starts
+ *                                         16-byte aligned)
  * Offsets/strides come from fold_acts_layout; the buffer is otherwise opaque. */
 typedef struct {
   size_t bytes;          /* total size of the buffer */
@@ -236,6 +238,15 @@ int64_t fold_launch_count(int32_t reset);
 #define FOLD_PROF_NCLASS 11
 void fold_profile_enable(int32_t on);
 fold_status fold_profile_read(int32_t n_classes, double *ms, int64_t *launches);
+/* Instrumentation: with FOLD_DBG_FWD=1 in the environment the BF16 forward kernel stamps
+ * %globaltimer (ns) per pair tile at nine points: 0 producer starts the tile, 1 its
+ * inputs are published, 2 its last MMA is issued, 3 its accumulator is ready in the
+ * epilogue, 4 its outputs are published, 5 the epilogue may write its staging, 6 the
+ * epilogue math is done, 7 the bulk stores have read the staging, 8 the bulk stores are
+ * complete. Copies the first n_tiles stamps of each point into host[9][n_tiles] (tiles in
+ * the kernel's order: levels ascending, row tile, column tile); returns the count, or -1
+ * on a CUDA error. */
+int32_t fold_debug_fwd_trace(unsigned long long *host, int32_t n_tiles);
 
 #ifdef __cplusplus
 }

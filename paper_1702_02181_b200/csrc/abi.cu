@@ -127,7 +127,7 @@ ActsLayout acts_layout(const fold_schedule_t *s, const fold_model *m) {
   const int gates = gates_of(m->cell);
   L.helem = m->prec == FOLD_PREC_BF16 ? 2 : 4;
   L.ld = ld_of((int)S);
-  L.ld_g = (int)round_up((int64_t)gates * S, 8);
+  L.ld_g = gates * L.ld;  // G row = gates blocks of ld (16-byte aligned gate blocks)
   size_t off = 0;
   L.h_off = off; off = a256(off + (size_t)(N + 1) * L.ld * L.helem);
   L.c_off = off; off = a256(off + (size_t)(N + 1) * L.ld * 4);
@@ -364,6 +364,11 @@ const char *fold_status_string(fold_status s) {
 
 int32_t fold_last_error_detail(void) { return g_last_detail; }
 int32_t fold_abi_version(void) { return FOLD_ABI_VERSION; }
+
+/* instrumentation: per-tile forward timeline of the last FOLD_DBG_FWD=1 run */
+int32_t fold_debug_fwd_trace(unsigned long long *host, int32_t n_tiles) {
+  return fold::tc_debug_fwd_trace(host, n_tiles);
+}
 
 fold_status fold_device_check(void) {
   int dev = 0, major = 0, minor = 0;

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(256) k_cell_fwd_simt(int r0, int r1, const int
       H[r * ld + j] = og * tanhf(cc);
       C[r * ld + j] = cc;
       float *ga = Gact + c * ld_g;
-      ga[j] = ig; ga[S + j] = fl; ga[2 * S + j] = fr; ga[3 * S + j] = og; ga[4 * S + j] = ug;
+      ga[j] = ig; ga[ld + j] = fl; ga[2 * ld + j] = fr; ga[3 * ld + j] = og; ga[4 * ld + j] = ug;
     }
   }
 }
@@ -294,8 +294,8 @@ __global__ void k_cell_bwd_pw(int r0, int r1, int nl, int S, int ld, int ld_g, c
         IT::st(dz + j, o);
       } else {
         float ig[VEC], fl[VEC], fr[VEC], og[VEC], ug[VEC], cc[VEC], cl[VEC], cr[VEC];
-        IT::ld(ga + j, ig); IT::ld(ga + S + j, fl); IT::ld(ga + 2 * S + j, fr);
-        IT::ld(ga + 3 * S + j, og); IT::ld(ga + 4 * S + j, ug);
+        IT::ld(ga + j, ig); IT::ld(ga + ld + j, fl); IT::ld(ga + 2 * ld + j, fr);
+        IT::ld(ga + 3 * ld + j, og); IT::ld(ga + 4 * ld + j, ug);
         IF::ld(C + r * ld + j, cc);
         // leaf children: c = 0 (not materialised in BF16 mode)
 #pragma unroll

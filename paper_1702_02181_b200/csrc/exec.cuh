@@ -19,7 +19,7 @@ struct ScatterA {
 struct ActsLayout {
   size_t bytes, h_off, c_off, g_off, al_off, ar_off;
   int ld;       // H, C row stride (elements)
-  int ld_g;     // G row stride (elements) = round_up(gates*S, 8)
+  int ld_g;     // G row stride (elements) = gates * ld; gate g at g * ld
   int helem;    // bytes per H / G element
 };
 ActsLayout acts_layout(const fold_schedule_t *s, const fold_model *m);
@@ -79,6 +79,7 @@ fold_status launch_zero(void *p, size_t bytes, cudaStream_t st);
 // (ld_u = 2 Sp): natural row order for the backward's dA GEMM (MN-major B operand),
 // gate-interleaved in 8-column blocks for the forward (K-major B operand, one TMA box).
 int tc_ld_u(int S);
+int tc_debug_fwd_trace(unsigned long long *host, int n);
 size_t tc_weights_bytes(int gates, int S);
 fold_status tc_prepare_U(int gates, int S, const float *U, __nv_bfloat16 *Ub, cudaStream_t st);
 // the forward's gate-interleaved copy (Uil8, same size)

@@ -34,7 +34,25 @@ namespace fold {
 
 namespace {
 
+// Debug timeline (FOLD_DBG_FWD=1): per tile, globaltimer stamps at five points of the
+// forward pipeline (read back with fold_debug_fwd_trace; instrumentation only).
+constexpr int kTraceTiles = 65536;
+__device__ unsigned long long g_fwd_trace[9][kTraceTiles];
+__device__ __forceinline__ void trace(int dbg, int pt, int T) {
+  if (dbg && T < kTraceTiles) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_fwd_trace[pt][T] = t;
+  }
+}
+
 constexpr int BM = 128;     // rows per CTA (the pair's MMA has M = 256)
+// A-operand box rows for a CTA holding m rows of a tile (narrow tiles load only their rows)
+#ifdef FOLD_AB_NOKPS
+#define FOLD_BOX(m) ((m) <= 0 ? 0 : BM)
+#else
+#define FOLD_BOX(m) ((m) <= 0 ? 0 : (m) <= 16 ? 16 : (m) <= 64 ? 64 : BM)
+#endif
 constexpr int PM = 2 * BM;  // rows per CTA pair
 constexpr int BK = 64;      // K elements per stage (128 B of bf16 = one swizzle row)
 constexpr int ST = 6;       // pipeline stages
@@ -107,6 +125,20 @@ struct FwdCfg {
   static_assert(SMEM <= 227 * 1024, "smem");
 };
 
+// k-blocks per pipeline stage of a tile: wide tiles 1; narrow tiles pack as many
+// (A box of bx0 rows + U box of GATES * W / 2 rows) pairs as one stage holds, so a tile's
+// K loop needs fewer round trips through the ring (narrow levels are latency bound).
+template <int GATES>
+__host__ __device__ inline int fwd_kps(int W, int bx0) {
+  using Cfg = FwdCfg<GATES>;
+#ifdef FOLD_AB_NOKPS
+  return 1;
+#endif
+  if (W == Cfg::WMAX) return 1;
+  const int k = Cfg::STAGE / (bx0 * 128 + GATES * W * 64);
+  return k < 1 ? 1 : k > 8 ? 8 : k;
+}
+
 // Warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4..11 epilogue
 // (warp w reads TMEM lanes 32 (w % 4) .. +31, column chunks (w - 4) / 4, +2, +4, ...).
 // B operand per stage: one box of GATES*W rows of the gate-interleaved bf16 U (Uil8: row
@@ -116,6 +148,8 @@ struct FwdCfg {
 template <int GATES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREADS, 1)
     k_fwd_levels(const __grid_constant__ CUtensorMap tmAL, const __grid_constant__ CUtensorMap tmAR,
+                 const __grid_constant__ CUtensorMap tmAL16, const __grid_constant__ CUtensorMap tmAR16,
+                 const __grid_constant__ CUtensorMap tmAL64, const __grid_constant__ CUtensorMap tmAR64,
                  const __grid_constant__ CUtensorMap tmUw, const __grid_constant__ CUtensorMap tmUn,
                  const __grid_constant__ CUtensorMap tmGw, const __grid_constant__ CUtensorMap tmGn,
                  const __grid_constant__ CUtensorMap tmCw, const __grid_constant__ CUtensorMap tmCn, FwdLevels L,
@@ -148,6 +182,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tmAL);
     ptx::prefetch_tmap(&tmAR);
+    ptx::prefetch_tmap(&tmAL16);
+    ptx::prefetch_tmap(&tmAR16);
+    ptx::prefetch_tmap(&tmAL64);
+    ptx::prefetch_tmap(&tmAR64);
     ptx::prefetch_tmap(&tmUw);
     ptx::prefetch_tmap(&tmUn);
     ptx::prefetch_tmap(&tmGw);
@@ -165,8 +203,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
   const int KBh = (int)cdiv(S, BK), KB = 2 * KBh, Sp = KBh * BK;
 
   if (warp == 0) {
-    // TMA producer: per stage one dense box of 128 A rows (the level's contiguous cell rows
-    // of the left / right operand plane) + GATES boxes of W rows of U.
+    // TMA producer: per stage one dense box of A rows (the level's contiguous cell rows of
+    // the left / right operand plane) + one box of GATES * W / 2 rows of U. Narrow tiles
+    // load only the rows they hold (16- or 64-row boxes; the MMA's other rows see stale
+    // shared memory and their accumulator rows are never read). The first stages' U boxes
+    // do not depend on the previous levels, so they are issued before the dependency wait.
     if (lane == 0) {
       LevelCursor cur;
       cur.init(L);
@@ -174,29 +215,83 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
       for (int T = pair; T < total_tiles; T += npairs) {
         cur.seek(L, T);
         const int lt = T - cur.t0, W = cur.W;
-        {  // both children's h (all S columns) pushed into every A row of this pair tile
-          // (and their C rows written); the rows are read only by TMA and, after this
-          // tile's MMA, through L2 by the epilogue
-          const int ct = (cur.r0 - nl) + (lt / cur.NT) * PM;
-          ptx::wait_counter_relaxed(rt_cnt + ct, min(PM, cur.r1 - nl - ct) * 2 * S);
-          ptx::fence_proxy_async_global();
-        }
-        const int c0 = (cur.r0 - nl) + (lt / cur.NT) * PM + (int)rank * BM, j0 = (lt % cur.NT) * W;
+        const int ct = (cur.r0 - nl) + (lt / cur.NT) * PM;  // first cell of the pair tile
+        const int rows = min(PM, cur.r1 - nl - ct);
+        auto box_of = [](int m) { return FOLD_BOX(m); };
+        const int bx0 = box_of(min(rows, BM)), bx1 = box_of(rows - BM), bx = rank ? bx1 : bx0;
+        const CUtensorMap *mL = bx == 16 ? &tmAL16 : bx == 64 ? &tmAL64 : &tmAL;
+        const CUtensorMap *mR = bx == 16 ? &tmAR16 : bx == 64 ? &tmAR64 : &tmAR;
+        const int c0 = ct + (int)rank * BM, j0 = (lt % cur.NT) * W;
         const CUtensorMap *tmU = W == Cfg::WMAX ? &tmUw : &tmUn;
-        // the leader's full barrier counts both CTAs' bytes: 2 x (A rows + half the B rows)
-        const uint32_t bytes = 2 * Cfg::A_BYTES + GATES * W * 128;
+        if (rank == 0) trace(dbg, 0, T);
+        // the leader's full barrier counts both CTAs' bytes: A rows of both + the B rows
+        const uint32_t bytes = (uint32_t)(bx0 + bx1) * 128 + GATES * W * 128;
         const int urow = GATES * j0 + (int)rank * (GATES * W / 2);
-        for (int kb = 0; kb < KB; kb++, it++) {
-          int s = it % ST;
-          uint32_t ph = (it / ST) & 1;
-          ptx::mbar_wait(&empty[s], ph ^ 1);
-          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], bytes);
-          int half = kb >= KBh;
-          int kc = (kb - half * KBh) * BK;
-          uint8_t *A = smem + s * Cfg::STAGE;
-          ptx::tma_load_2d_pair(half ? &tmAR : &tmAL, &full[s], A, kc, c0);
-          ptx::tma_load_2d_pair(tmU, &full[s], A + Cfg::A_BYTES, half * Sp + kc, urow);
+        // narrow tiles pack kps k-blocks per stage (fewer pipeline round trips per tile)
+        const int kps = fwd_kps<GATES>(W, bx0), abox = bx0 * 128, ubox = GATES * W * 64;
+        const int nst = (KB + kps - 1) / kps;
+        // inputs already published (the common case on wide levels): A and U per stage in
+        // order; otherwise the first stages' U boxes go out before the wait
+#ifdef FOLD_AB_NOPREFETCH
+        ptx::wait_counter_relaxed(rt_cnt + ct, rows * 2 * S);
+        const bool ready = true;
+#else
+        const bool ready = ptx::ld_relaxed_gpu(rt_cnt + ct) >= rows * 2 * S;
+#endif
+        if (ready) ptx::fence_proxy_async_global();
+        const int pre = ready ? 0 : (nst < ST ? nst : ST);
+        if (ready && rank == 0) trace(dbg, 1, T);
+        if (ready && kps == 1) {  // wide tiles, inputs published: one (A, U) box pair per stage
+          for (int kb = 0; kb < KB; kb++, it++) {
+            const int s = it % ST;
+            const uint32_t ph = (it / ST) & 1;
+            ptx::mbar_wait(&empty[s], ph ^ 1);
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], bytes);
+            const int half = kb >= KBh, kc = (kb - half * KBh) * BK;
+            uint8_t *A = smem + s * Cfg::STAGE;
+            if (bx) ptx::tma_load_2d_pair(half ? mR : mL, &full[s], A, kc, c0);
+            ptx::tma_load_2d_pair(tmU, &full[s], A + Cfg::A_BYTES, half * Sp + kc, urow);
+          }
+          continue;
         }
+        const int uoff = kps == 1 ? Cfg::A_BYTES : kps * abox;
+        for (int q = 0; q < nst; q++) {
+          const int s = (it + q) % ST;
+          const uint32_t ph = ((it + q) / ST) & 1;
+          const int kb0 = q * kps, nk = min(kps, KB - kb0);
+          uint8_t *stg = smem + s * Cfg::STAGE;
+          ptx::mbar_wait(&empty[s], ph ^ 1);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)nk * bytes);
+          for (int j = 0; j < nk; j++) {
+            const int kb = kb0 + j, half = kb >= KBh, kc = (kb - half * KBh) * BK;
+            ptx::tma_load_2d_pair(tmU, &full[s], stg + uoff + j * ubox, half * Sp + kc, urow);
+          }
+          if (q < pre - 1) continue;
+          if (q == pre - 1) {
+            // both children's h (all S columns) pushed into every A row of this pair tile
+            // (and their C rows written); the rows are read only by TMA and, after this
+            // tile's MMA, through L2 by the epilogue
+            ptx::wait_counter_relaxed(rt_cnt + ct, rows * 2 * S);
+            ptx::fence_proxy_async_global();
+            if (rank == 0) trace(dbg, 1, T);
+            if (bx)
+              for (int q2 = 0; q2 < pre; q2++) {
+                const int s2 = (it + q2) % ST;
+                for (int j = 0; j < kps && q2 * kps + j < KB; j++) {
+                  const int kb = q2 * kps + j, h2 = kb >= KBh;
+                  ptx::tma_load_2d_pair(h2 ? mR : mL, &full[s2], smem + s2 * Cfg::STAGE + j * abox,
+                                        (kb - h2 * KBh) * BK, c0);
+                }
+              }
+            continue;
+          }
+          if (bx)
+            for (int j = 0; j < nk; j++) {
+              const int kb = kb0 + j, half = kb >= KBh, kc = (kb - half * KBh) * BK;
+              ptx::tma_load_2d_pair(half ? mR : mL, &full[s], stg + j * abox, kc, c0);
+            }
+        }
+        it += nst;
       }
     }
   } else if (warp == 1) {
@@ -212,19 +307,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         ptx::mbar_wait(&tempty[acc], aph ^ 1);
         ptx::tc_fence_after();
         const uint32_t dst = tbase + acc * Cfg::ACC_STRIDE;
-        for (int kb = 0; kb < KB; kb++, it++) {
+        const int ct = (cur.r0 - nl) + ((T - cur.t0) / cur.NT) * PM;
+        const int rows0 = min(BM, cur.r1 - nl - ct);
+        #ifdef FOLD_AB_NOKPS
+        const int bx0 = BM;
+#else
+        const int bx0 = rows0 <= 16 ? 16 : rows0 <= 64 ? 64 : BM;
+#endif
+        const int kps = fwd_kps<GATES>(cur.W, bx0), abox = bx0 * 128, ubox = GATES * cur.W * 64;
+        const int nst = (KB + kps - 1) / kps;
+        if (kps == 1) {  // one k-block per stage, U at the fixed offset A_BYTES
+          for (int kb = 0; kb < KB; kb++, it++) {
+            int s = it % ST;
+            uint32_t ph = (it / ST) & 1;
+            ptx::mbar_wait(&full[s], ph);
+            ptx::tc_fence_after();
+            uint32_t a0 = ptx::smem_u32(smem + s * Cfg::STAGE), b0 = a0 + Cfg::A_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / 16; k++)
+              ptx::umma_bf16_2cta(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024),
+                                  ptx::sdesc_sw128(b0 + 32 * k, 16, 1024), idesc, (kb | k) != 0);
+            ptx::umma_commit_2cta(&empty[s]);
+          }
+          ptx::umma_commit_2cta(&tfull[acc]);
+          trace(dbg, 2, T);
+          continue;
+        }
+        for (int q = 0; q < nst; q++, it++) {
           int s = it % ST;
           uint32_t ph = (it / ST) & 1;
           ptx::mbar_wait(&full[s], ph);
           ptx::tc_fence_after();
-          uint32_t a0 = ptx::smem_u32(smem + s * Cfg::STAGE), b0 = a0 + Cfg::A_BYTES;
+          const uint32_t st0 = ptx::smem_u32(smem + s * Cfg::STAGE);
+          for (int j = 0; j < kps && q * kps + j < KB; j++) {
+            const uint32_t a0 = st0 + j * abox, b0 = st0 + kps * abox + j * ubox;
 #pragma unroll
-          for (int k = 0; k < BK / 16; k++)
-            ptx::umma_bf16_2cta(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024),
-                                ptx::sdesc_sw128(b0 + 32 * k, 16, 1024), idesc, (kb | k) != 0);
+            for (int k = 0; k < BK / 16; k++)
+              ptx::umma_bf16_2cta(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024),
+                                  ptx::sdesc_sw128(b0 + 32 * k, 16, 1024), idesc, (q | j | k) != 0);
+          }
           ptx::umma_commit_2cta(&empty[s]);
         }
         ptx::umma_commit_2cta(&tfull[acc]);
+        trace(dbg, 2, T);
       }
     }
   } else if (warp >= 4) {
@@ -302,7 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         if (GATES != 5) return;
         // leaf children have c = 0 (their C rows are not materialised in BF16 mode)
         const bool lok = valid && gl >= nl, rok = valid && gr >= nl;
-        if (jb + 8 <= S && (S & 7) == 0) {
+        if (jb + 8 <= S) {  // C rows have stride ld (a multiple of 8): 16-byte aligned
 #pragma unroll
           for (int u = 0; u < 8; u++) { cl[u] = 0.f; cr[u] = 0.f; }
           if (lok) {
@@ -328,11 +453,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
       const int64_t c_tile = (int64_t)(cur.r0 - nl) + (int64_t)(lt / cur.NT) * PM + rank * BM;
       // (the bulk stores never write past the level's last row: a later level's tile may
       // already own those rows)
-      const bool staged = (S & 7) == 0 && j0 + W <= S && c_tile + BM <= cur.r1 - nl;
+      const bool staged = j0 + W <= S && c_tile + BM <= cur.r1 - nl;
       ptx::mbar_wait(&tfull[acc], aph);
       ptx::tc_fence_after();
+      if (warp == 4 && lane == 0 && rank == 0) trace(dbg, 3, T);
       load_c(j0 + grp * 8);
       if (tc > 0) ptx::mbar_wait(&stg_free, (tc - 1) & 1);  // previous tile's staging consumed
+      if (warp == 4 && lane == 0 && rank == 0) trace(dbg, 5, T);
       const uint32_t tl = tbase + acc * Cfg::ACC_STRIDE + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
       for (int jc = grp; jc < chunks; jc += 2) {
@@ -346,7 +473,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         for (int u = 0; u < 8; u++) { ccl[u] = cl[u]; ccr[u] = cr[u]; }
         if (jc + 2 < chunks) load_c(jb + 16);  // next chunk of this warp, in flight during math
         if (!valid || jb >= S) continue;
-        const bool fullc = (jb + 8 <= S) && ((S & 7) == 0);
+        // full 8-column chunk: H / C / A rows (stride ld) and G gate blocks (stride ld) are
+        // 16-byte aligned for any S; the bias gate blocks (stride S) only when S % 4 == 0
+        const bool fullc = jb + 8 <= S;
+        const bool bias_vec = fullc && (S & 3) == 0;
         float hh[8];
         if constexpr (GATES == 1) {
 #pragma unroll
@@ -374,7 +504,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
 #pragma unroll
           for (int g = 0; g < 5; g++) {
             float bz[8];
-            if (fullc) {
+            if (bias_vec) {
               float4 x = __ldg(reinterpret_cast<const float4 *>(bsrc + g * S + jb));
               float4 y = __ldg(reinterpret_cast<const float4 *>(bsrc + g * S + jb + 4));
               bz[0] = x.x; bz[1] = x.y; bz[2] = x.z; bz[3] = x.w; bz[4] = y.x; bz[5] = y.y; bz[6] = y.z; bz[7] = y.w;
@@ -404,7 +534,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
             *reinterpret_cast<float4 *>(C + r * ld + jb + 4) = make_float4(cc[4], cc[5], cc[6], cc[7]);
 #pragma unroll
             for (int g = 0; g < 5; g++)
-              *reinterpret_cast<uint4 *>(ga + g * S + jb) =
+              *reinterpret_cast<uint4 *>(ga + g * ld + jb) =
                   make_uint4(pack_bf16x2(gs[g][0], gs[g][1]), pack_bf16x2(gs[g][2], gs[g][3]),
                              pack_bf16x2(gs[g][4], gs[g][5]), pack_bf16x2(gs[g][6], gs[g][7]));
           } else {
@@ -412,7 +542,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
               int j = jb + u;
               C[r * ld + j] = cc[u];
 #pragma unroll
-              for (int g = 0; g < 5; g++) ga[g * S + j] = __float2bfloat16_rn(gs[g][u]);
+              for (int g = 0; g < 5; g++) ga[g * ld + j] = __float2bfloat16_rn(gs[g][u]);
             }
           }
         }
@@ -450,6 +580,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         for (int jc = grp; jc < chunks; jc += 2) cols += max(0, min(8, S - (j0 + jc * 8)));
       warp_credits(tc & 1, ce0, ce1, m.e0, cols);
       __syncwarp();
+      if (warp == 4 && lane == 0 && rank == 0) trace(dbg, 6, T);
       if (lane == 0) ptx::mbar_arrive(&epi_done);
     }
   } else if (warp == 3) {
@@ -463,19 +594,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         const int lt = T - cur.t0, W = cur.W, chunks = W / 8;
         const int j0 = (lt % cur.NT) * W;
         const int64_t c_tile = (int64_t)(cur.r0 - nl) + (int64_t)(lt / cur.NT) * PM + rank * BM;
-        const bool staged = (S & 7) == 0 && j0 + W <= S && c_tile + BM <= cur.r1 - nl;
+        const bool staged = j0 + W <= S && c_tile + BM <= cur.r1 - nl;
         ptx::mbar_wait(&epi_done, tc & 1);
         if (staged) {
           const CUtensorMap *tG = W == Cfg::WMAX ? &tmGw : &tmGn;
           const CUtensorMap *tC = W == Cfg::WMAX ? &tmCw : &tmCn;
 #pragma unroll
-          for (int g = 0; g < GATES; g++) ptx::tma_store_2d(tG, gsm + g * BM * W * 2, g * S + j0, (int)c_tile);
+          for (int g = 0; g < GATES; g++) ptx::tma_store_2d(tG, gsm + g * BM * W * 2, g * ld + j0, (int)c_tile);
           ptx::tma_store_2d(tC, csm, j0, (int)(c_tile + nl));
           ptx::bulk_commit();
           ptx::bulk_wait_read0();
         }
+        if (rank == 0) trace(dbg, 7, T);
         ptx::mbar_arrive(&stg_free);
         if (staged) ptx::bulk_wait0();  // the tile's C rows are written
+        if (rank == 0) trace(dbg, 8, T);
         __threadfence();
         const int par = tc & 1;
         for (int w = 0; w < Cfg::EPI_WARPS; w++) {
@@ -494,6 +627,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
             }
           }
         }
+        if (rank == 0) trace(dbg, 4, T);
       }
     }
   }
@@ -660,6 +794,15 @@ struct BwdCursor {  // walks levels D, D-1, ..., 2 in tile order
   }
 };
 
+// k-blocks per stage of a backward tile (see fwd_kps): dZ box of bx0 rows + N/2 U columns
+__host__ __device__ inline int bwd_kps(int N, int bx0) {
+#ifdef FOLD_AB_NOKPS
+  return 1;
+#endif
+  const int k = DA_STAGE / (bx0 * 128 + (N / 128) * MN_CHUNK);
+  return k < 1 ? 1 : k > 8 ? 8 : k;
+}
+
 constexpr int BW_ST = 4;
 constexpr int BW_EPI = 8;                       // epilogue warps
 constexpr int BW_THREADS = 128 + 32 * BW_EPI;
@@ -668,7 +811,8 @@ constexpr int BW_SMEM = BW_ST * DA_STAGE + BW_EPI * BW_XS * 4 + 1024;
 
 template <int GATES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
-    k_bwd_levels(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmU, BwdLevels L,
+    k_bwd_levels(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmZ16,
+                 const __grid_constant__ CUtensorMap tmZ64, const __grid_constant__ CUtensorMap tmU, BwdLevels L,
                  int KB, int total_tiles, const int32_t *__restrict__ gather,
                  const __nv_bfloat16 *__restrict__ Gact, int ld_g, const float *__restrict__ C, int ld, float *dA,
                  float *dCe, __nv_bfloat16 *dZ, int ld_z, int *rt_cnt, const int32_t *__restrict__ tstart,
@@ -689,6 +833,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
     for (int a = 0; a < 2; a++) { ptx::mbar_init(&tfull[a], 1); ptx::mbar_init(&tempty[a], 2 * BW_EPI); }
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tmZ);
+    ptx::prefetch_tmap(&tmZ16);
+    ptx::prefetch_tmap(&tmZ64);
     ptx::prefetch_tmap(&tmU);
   }
   if (warp == 2) { ptx::tmem_alloc2(&tmem_base_sh, 512); ptx::tmem_relinquish2(); }
@@ -704,24 +850,69 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
       for (int T = pair; T < total_tiles; T += npairs) {
         cur.seek(L, T);
         const int lt = T - cur.t0, NTn = cur.NTn, N = cur.N;
-        {  // this pair tile's 256 dZ rows (and their dCe) complete
-          const int ct = (cur.r0 - nl) + (lt / NTn) * PM;
-          ptx::wait_counter(rt_cnt + ct, min(PM, cur.r1 - nl - ct) * slabs);
-          ptx::fence_proxy_async_global();
-        }
-        const int mt = (cur.r0 - nl) + (lt / NTn) * PM + (int)rank * BM;
+        const int ct = (cur.r0 - nl) + (lt / NTn) * PM;  // first cell of the pair tile
+        const int rows = min(PM, cur.r1 - nl - ct);
+        // narrow tiles load only the dZ rows they hold (see k_fwd_levels)
+        auto box_of = [](int m) { return FOLD_BOX(m); };
+        const int bx0 = box_of(min(rows, BM)), bx1 = box_of(rows - BM), bx = rank ? bx1 : bx0;
+        const CUtensorMap *mZ = bx == 16 ? &tmZ16 : bx == 64 ? &tmZ64 : &tmZ;
+        const int mt = ct + (int)rank * BM;
         const int nb = (lt % NTn) * N + (int)rank * (N / 2);
-        const uint32_t bytes = 2 * (DA_A_BYTES + (N / 2) * 128);
-        for (int kb = 0; kb < KB; kb++, it++) {
-          int s = it % ST;
-          uint32_t ph = (it / ST) & 1;
-          ptx::mbar_wait(&empty[s], ph ^ 1);
-          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], bytes);
-          uint8_t *A = smem + s * DA_STAGE;
-          ptx::tma_load_2d_pair(&tmZ, &full[s], A, kb * BK, mt);
-          for (int ch = 0; ch < N / 128; ch++)
-            ptx::tma_load_2d_pair(&tmU, &full[s], A + DA_A_BYTES + ch * MN_CHUNK, nb + ch * 64, kb * BK);
+        const uint32_t bytes = (uint32_t)(bx0 + bx1) * 128 + N * 128;
+        // the first stages' U boxes are issued before the dependency wait; narrow tiles pack
+        // kps k-blocks per stage
+        const int kps = bwd_kps(N, bx0), abox = bx0 * 128, ubox = (N / 128) * MN_CHUNK;
+        const int nst = (KB + kps - 1) / kps;
+#ifdef FOLD_AB_NOPREFETCH
+        ptx::wait_counter(rt_cnt + ct, rows * slabs);
+        const bool ready = true;
+#else
+        const bool ready = ptx::ld_acquire_gpu(rt_cnt + ct) >= rows * slabs;
+#endif
+        if (ready) ptx::fence_proxy_async_global();
+        const int pre = ready ? 0 : (nst < ST ? nst : ST);
+        if (ready && kps == 1) {  // inputs published: one (A, U) box set per stage
+          for (int kb = 0; kb < KB; kb++, it++) {
+            const int s = it % ST;
+            const uint32_t ph = (it / ST) & 1;
+            ptx::mbar_wait(&empty[s], ph ^ 1);
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], bytes);
+            uint8_t *A = smem + s * DA_STAGE;
+            if (bx) ptx::tma_load_2d_pair(mZ, &full[s], A, kb * BK, mt);
+            for (int ch = 0; ch < N / 128; ch++)
+              ptx::tma_load_2d_pair(&tmU, &full[s], A + DA_A_BYTES + ch * MN_CHUNK, nb + ch * 64, kb * BK);
+          }
+          continue;
         }
+        const int uoff = kps == 1 ? DA_A_BYTES : kps * abox;
+        for (int q = 0; q < nst; q++) {
+          const int s = (it + q) % ST;
+          const uint32_t ph = ((it + q) / ST) & 1;
+          const int kb0 = q * kps, nk = min(kps, KB - kb0);
+          uint8_t *stg = smem + s * DA_STAGE;
+          ptx::mbar_wait(&empty[s], ph ^ 1);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)nk * bytes);
+          for (int j = 0; j < nk; j++)
+            for (int ch = 0; ch < N / 128; ch++)
+              ptx::tma_load_2d_pair(&tmU, &full[s], stg + uoff + j * ubox + ch * MN_CHUNK, nb + ch * 64,
+                                    (kb0 + j) * BK);
+          if (q < pre - 1) continue;
+          if (q == pre - 1) {
+            // this pair tile's dZ rows (and their dCe) complete
+            ptx::wait_counter(rt_cnt + ct, rows * slabs);
+            ptx::fence_proxy_async_global();
+            if (bx)
+              for (int q2 = 0; q2 < pre; q2++) {
+                const int s2 = (it + q2) % ST;
+                for (int j = 0; j < kps && q2 * kps + j < KB; j++)
+                  ptx::tma_load_2d_pair(mZ, &full[s2], smem + s2 * DA_STAGE + j * abox, (q2 * kps + j) * BK, mt);
+              }
+            continue;
+          }
+          if (bx)
+            for (int j = 0; j < nk; j++) ptx::tma_load_2d_pair(mZ, &full[s], stg + j * abox, (kb0 + j) * BK, mt);
+        }
+        it += nst;
       }
     }
   } else if (warp == 1) {
@@ -736,16 +927,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         ptx::mbar_wait(&tempty[acc], ((tc >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t dst = tbase + acc * 256;
-        for (int kb = 0; kb < KB; kb++, it++) {
+        const int ct = (cur.r0 - nl) + ((T - cur.t0) / cur.NTn) * PM;
+        const int rows0 = min(BM, cur.r1 - nl - ct);
+        #ifdef FOLD_AB_NOKPS
+        const int bx0 = BM;
+#else
+        const int bx0 = rows0 <= 16 ? 16 : rows0 <= 64 ? 64 : BM;
+#endif
+        const int kps = bwd_kps(cur.N, bx0), abox = bx0 * 128, ubox = (cur.N / 128) * MN_CHUNK;
+        const int nst = (KB + kps - 1) / kps;
+        if (kps == 1) {  // one k-block per stage, U at the fixed offset DA_A_BYTES
+          for (int kb = 0; kb < KB; kb++, it++) {
+            int s = it % ST;
+            uint32_t ph = (it / ST) & 1;
+            ptx::mbar_wait(&full[s], ph);
+            ptx::tc_fence_after();
+            uint32_t a0 = ptx::smem_u32(smem + s * DA_STAGE), b0 = a0 + DA_A_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / 16; k++)
+              ptx::umma_bf16_2cta(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024),
+                                  ptx::sdesc_sw128(b0 + 2048 * k, MN_CHUNK, 1024), idesc, (kb | k) != 0);
+            ptx::umma_commit_2cta(&empty[s]);
+          }
+          ptx::umma_commit_2cta(&tfull[acc]);
+          continue;
+        }
+        for (int q = 0; q < nst; q++, it++) {
           int s = it % ST;
           uint32_t ph = (it / ST) & 1;
           ptx::mbar_wait(&full[s], ph);
           ptx::tc_fence_after();
-          uint32_t a0 = ptx::smem_u32(smem + s * DA_STAGE), b0 = a0 + DA_A_BYTES;
+          const uint32_t st0 = ptx::smem_u32(smem + s * DA_STAGE);
+          for (int j = 0; j < kps && q * kps + j < KB; j++) {
+            const uint32_t a0 = st0 + j * abox, b0 = st0 + kps * abox + j * ubox;
 #pragma unroll
-          for (int k = 0; k < BK / 16; k++)
-            ptx::umma_bf16_2cta(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024),
-                                ptx::sdesc_sw128(b0 + 2048 * k, MN_CHUNK, 1024), idesc, (kb | k) != 0);
+            for (int k = 0; k < BK / 16; k++)
+              ptx::umma_bf16_2cta(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024),
+                                  ptx::sdesc_sw128(b0 + 2048 * k, MN_CHUNK, 1024), idesc, (q | j | k) != 0);
+          }
           ptx::umma_commit_2cta(&empty[s]);
         }
         ptx::umma_commit_2cta(&tfull[acc]);
@@ -831,7 +1050,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
               const int64_t xc = xs_[j] - nl;
               const __nv_bfloat16 *gx = Gact + xc * ld_g + col;
 #pragma unroll
-              for (int g = 0; g < GATES; g++) graw[j][g] = __ldg(reinterpret_cast<const uint32_t *>(gx + g * S));
+              for (int g = 0; g < GATES; g++) graw[j][g] = __ldg(reinterpret_cast<const uint32_t *>(gx + g * ld));
               if constexpr (GATES == 5) {
                 cc[j] = __ldcg(reinterpret_cast<const float2 *>(C + (int64_t)xs_[j] * ld + col));
                 cl[j] = xls[j] >= nl ? __ldcg(reinterpret_cast<const float2 *>(C + (int64_t)xls[j] * ld + col))
@@ -1207,15 +1426,20 @@ fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
   CUtensorMap tmAL, tmAR, tmUw, tmUn, tmGw, tmGn, tmCw, tmCn;
   FOLD_TRY(make_map(&tmAL, a.sc.AL, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, BM));
   FOLD_TRY(make_map(&tmAR, a.sc.AR, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, BM));
+  CUtensorMap tmAL16, tmAR16, tmAL64, tmAR64;  // narrow tiles: boxes of the rows they hold
+  FOLD_TRY(make_map(&tmAL16, a.sc.AL, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, 16));
+  FOLD_TRY(make_map(&tmAR16, a.sc.AR, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, 16));
+  FOLD_TRY(make_map(&tmAL64, a.sc.AL, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, 64));
+  FOLD_TRY(make_map(&tmAR64, a.sc.AR, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, 64));
   const uint64_t il_rows = (uint64_t)cdiv(S, 8) * 8 * GATES;
   FOLD_TRY(make_map(&tmUw, a.Ub, (uint64_t)a.ld_u, il_rows, (uint64_t)a.ld_u * 2, BK, GATES * Cfg::WMAX / 2));
   FOLD_TRY(make_map(&tmUn, a.Ub, (uint64_t)a.ld_u, il_rows, (uint64_t)a.ld_u * 2, BK, GATES * Cfg::WNAR / 2));
   // epilogue bulk stores: G [n_cells][GATES*S] bf16 and the pool's C [N][S] fp32, plain
   // (unswizzled) boxes of W columns x 128 rows
   const uint64_t Nrows = (uint64_t)nc + a.nl;
-  FOLD_TRY(make_map_ex(&tmGw, a.Gact, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (uint64_t)GATES * S, (uint64_t)nc,
+  FOLD_TRY(make_map_ex(&tmGw, a.Gact, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (uint64_t)a.ld_g, (uint64_t)nc,
                        (uint64_t)a.ld_g * 2, Cfg::WMAX, BM, CU_TENSOR_MAP_SWIZZLE_NONE));
-  FOLD_TRY(make_map_ex(&tmGn, a.Gact, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (uint64_t)GATES * S, (uint64_t)nc,
+  FOLD_TRY(make_map_ex(&tmGn, a.Gact, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (uint64_t)a.ld_g, (uint64_t)nc,
                        (uint64_t)a.ld_g * 2, Cfg::WNAR, BM, CU_TENSOR_MAP_SWIZZLE_NONE));
   FOLD_TRY(make_map_ex(&tmCw, a.C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (uint64_t)S, Nrows, (uint64_t)a.ld * 4,
                        Cfg::WMAX, BM, CU_TENSOR_MAP_SWIZZLE_NONE));
@@ -1242,7 +1466,7 @@ fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
     FOLD_LAUNCH_CHECK();
   }
   const int npairs = total < npairs_max ? (int)total : npairs_max;
-  kern<<<2 * npairs, Cfg::THREADS, smem_bytes, st>>>(tmAL, tmAR, tmUw, tmUn, tmGw, tmGn, tmCw, tmCn, L, (int)total,
+  kern<<<2 * npairs, Cfg::THREADS, smem_bytes, st>>>(tmAL, tmAR, tmAL16, tmAR16, tmAL64, tmAR64, tmUw, tmUn, tmGw, tmGn, tmCw, tmCn, L, (int)total,
                                                       a.nl, a.ld, a.gather, a.b, a.H, a.C, a.Gact, a.ld_g, a.sc,
                                                       a.rt_cnt, a.tstart, dbg_fwd());
   FOLD_LAUNCH_CHECK();
@@ -1252,6 +1476,15 @@ fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
 }  // namespace
 
 int tc_ld_u(int S) { return 2 * (int)round_up(S, BK); }
+
+int tc_debug_fwd_trace(unsigned long long *host, int n) {
+  if (n > kTraceTiles) n = kTraceTiles;
+  for (int p = 0; p < 9; p++)
+    if (cudaMemcpyFromSymbol(host + (size_t)p * n, g_fwd_trace, (size_t)n * 8, (size_t)p * kTraceTiles * 8) !=
+        cudaSuccess)
+      return -1;
+  return n;
+}
 
 size_t tc_weights_bytes(int gates, int S) { return round_up(cdiv(S, 8) * 8 * gates * tc_ld_u(S) * 2, 256); }
 
@@ -1315,8 +1548,10 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
   if (a.D < 2) return FOLD_OK;
   const int S = a.S, gates = cell == FOLD_CELL_TREELSTM ? 5 : 1;
   if (S & 1) return FOLD_E_UNSUPPORTED;
-  CUtensorMap tmZ, tmU;
+  CUtensorMap tmZ, tmZ16, tmZ64, tmU;
   FOLD_TRY(make_map(&tmZ, a.dZ, (uint64_t)gates * S, (uint64_t)a.n_cells, (uint64_t)a.ld_z * 2, BK, BM));
+  FOLD_TRY(make_map(&tmZ16, a.dZ, (uint64_t)gates * S, (uint64_t)a.n_cells, (uint64_t)a.ld_z * 2, BK, 16));
+  FOLD_TRY(make_map(&tmZ64, a.dZ, (uint64_t)gates * S, (uint64_t)a.n_cells, (uint64_t)a.ld_z * 2, BK, 64));
   const int ld_u = tc_ld_u(S);
   FOLD_TRY(make_map(&tmU, a.Ub, (uint64_t)ld_u, (uint64_t)gates * S, (uint64_t)ld_u * 2, 64, BK));
   auto kern = gates == 5 ? k_bwd_levels<5> : k_bwd_levels<1>;
@@ -1332,7 +1567,7 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
   if (total <= 0) return FOLD_OK;
   if (total > INT32_MAX) return FOLD_E_INVALID;
   const int npairs = total < npairs_max ? (int)total : npairs_max;
-  kern<<<2 * npairs, BW_THREADS, BW_SMEM, st>>>(tmZ, tmU, L, (int)cdiv(gates * S, BK), (int)total, a.gather,
+  kern<<<2 * npairs, BW_THREADS, BW_SMEM, st>>>(tmZ, tmZ16, tmZ64, tmU, L, (int)cdiv(gates * S, BK), (int)total, a.gather,
                                                a.Gact, a.ld_g, a.C, a.ld, a.dA, a.dCe, a.dZ, a.ld_z, a.rt_cnt,
                                                a.tstart, tc_bwd_slabs(S));
   FOLD_LAUNCH_CHECK();

@@ -110,6 +110,8 @@ def load() -> ctypes.CDLL:
     L.fold_profile_enable.argtypes = [i32]
     L.fold_profile_read.restype = i32
     L.fold_profile_read.argtypes = [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
+    L.fold_debug_fwd_trace.argtypes = [vp, i32]
+    L.fold_debug_fwd_trace.restype = i32
     _lib = L
     return L
 
@@ -117,7 +119,7 @@ def load() -> ctypes.CDLL:
 EXPORTED = ("fold_schedule_workspace", "fold_schedule", "fold_acts_layout", "fold_forward_workspace",
             "fold_forward", "fold_backward_workspace", "fold_backward", "fold_sgd_update",
             "fold_status_string", "fold_last_error_detail", "fold_abi_version", "fold_device_check",
-            "fold_launch_count", "fold_profile_enable", "fold_profile_read")
+            "fold_launch_count", "fold_profile_enable", "fold_profile_read", "fold_debug_fwd_trace")
 
 PROF_CLASSES = ("schedule", "embed_fwd", "cell_fwd", "bwd_pointwise", "gemm_dA", "gemm_dU", "embed_bwd",
                 "db_colsum", "sgd", "weight_prep", "root_out")
