@@ -113,11 +113,15 @@ struct FwdCfg {
   static_assert(STAGE % 1024 == 0, "stages stay 1024 B aligned (128B swizzle atoms)");
   static constexpr int ACC_STRIDE = 256;  // TMEM columns per accumulator buffer (2 buffers)
   static constexpr int TMEM_COLS = 512;
-  static constexpr int NST = 4;           // pipeline stages (the rest of smem stages the outputs)
-  // epilogue staging: the tile's saved gates [GATES][128][W] bf16 and cell states [128][W]
-  // fp32 leave through TMA bulk stores (row-scattered per-thread stores were LSU-bound)
+  // epilogue staging: the tile's saved gates [GATES][128][W] bf16 leave through TMA bulk
+  // stores (row-scattered per-thread stores of 5 gate blocks were LSU-bound); the cell
+  // states (one fp32 block) are stored directly, which leaves room for a 5th stage
   static constexpr int G_STAGE = GATES * BM * WMAX * 2;
-  static constexpr int C_STAGE = BM * WMAX * 4;
+  static constexpr int C_STAGE = 0;
+  // pipeline stages: as many as the rest of shared memory holds (at most 8)
+  // (220 KB of dynamic shared memory: the kernel's static arrays take ~4.3 KB of the 227)
+  static constexpr int NST_FIT = (220 * 1024 - G_STAGE - C_STAGE - 1024) / STAGE;
+  static constexpr int NST = NST_FIT > 8 ? 8 : NST_FIT;
   static constexpr int SMEM = NST * STAGE + G_STAGE + C_STAGE + 1024;
   static constexpr int EPI_WARPS = 8;     // 2 per SM sub-partition: each owns half the columns
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
@@ -160,7 +164,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
   constexpr int ST = Cfg::NST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
-  uint8_t *gsm = smem + ST * Cfg::STAGE, *csm = gsm + Cfg::G_STAGE;
+  uint8_t *gsm = smem + ST * Cfg::STAGE;
   __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull[2], tempty[2];
   // epilogue -> store warp hand-off: epi_done (8 epilogue warps arrive per tile), stg_free
   // (the store warp: the tile's bulk stores finished reading the staging)
@@ -485,8 +489,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
             uint4 pk = make_uint4(pack_bf16x2(hh[0], hh[1]), pack_bf16x2(hh[2], hh[3]), pack_bf16x2(hh[4], hh[5]),
                                   pack_bf16x2(hh[6], hh[7]));
             *reinterpret_cast<uint4 *>(gsm + row * W * 2 + jc * 16) = pk;
-            *reinterpret_cast<float4 *>(csm + row * W * 4 + jc * 32) = make_float4(0.f, 0.f, 0.f, 0.f);
-            *reinterpret_cast<float4 *>(csm + row * W * 4 + jc * 32 + 16) = make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4 *>(C + r * ld + jb) = make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4 *>(C + r * ld + jb + 4) = make_float4(0.f, 0.f, 0.f, 0.f);
           } else if (fullc) {
             uint4 pk = make_uint4(pack_bf16x2(hh[0], hh[1]), pack_bf16x2(hh[2], hh[3]), pack_bf16x2(hh[4], hh[5]),
                                   pack_bf16x2(hh[6], hh[7]));
@@ -522,8 +526,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
           }
           __nv_bfloat16 *ga = Gact + c * ld_g;
           if (staged) {
-            *reinterpret_cast<float4 *>(csm + row * W * 4 + jc * 32) = make_float4(cc[0], cc[1], cc[2], cc[3]);
-            *reinterpret_cast<float4 *>(csm + row * W * 4 + jc * 32 + 16) = make_float4(cc[4], cc[5], cc[6], cc[7]);
+            *reinterpret_cast<float4 *>(C + r * ld + jb) = make_float4(cc[0], cc[1], cc[2], cc[3]);
+            *reinterpret_cast<float4 *>(C + r * ld + jb + 4) = make_float4(cc[4], cc[5], cc[6], cc[7]);
 #pragma unroll
             for (int g = 0; g < 5; g++)
               *reinterpret_cast<uint4 *>(gsm + (g * BM + row) * W * 2 + jc * 16) =
@@ -598,16 +602,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         ptx::mbar_wait(&epi_done, tc & 1);
         if (staged) {
           const CUtensorMap *tG = W == Cfg::WMAX ? &tmGw : &tmGn;
-          const CUtensorMap *tC = W == Cfg::WMAX ? &tmCw : &tmCn;
 #pragma unroll
           for (int g = 0; g < GATES; g++) ptx::tma_store_2d(tG, gsm + g * BM * W * 2, g * ld + j0, (int)c_tile);
-          ptx::tma_store_2d(tC, csm, j0, (int)(c_tile + nl));
           ptx::bulk_commit();
           ptx::bulk_wait_read0();
         }
         if (rank == 0) trace(dbg, 7, T);
         ptx::mbar_arrive(&stg_free);
-        if (staged) ptx::bulk_wait0();  // the tile's C rows are written
+        // (the staged G rows are read only by the backward, after this kernel; the C rows
+        // the consumers read were stored by the epilogue threads, ordered by the fence below)
         if (rank == 0) trace(dbg, 8, T);
         __threadfence();
         const int par = tc & 1;
@@ -629,6 +632,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         }
         if (rank == 0) trace(dbg, 4, T);
       }
+      ptx::bulk_wait0();  // the last G bulk stores are complete before the CTA exits
     }
   }
   ptx::tc_fence_before();
@@ -637,6 +641,253 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
     ptx::tc_fence_after();
     ptx::tmem_dealloc2(tbase, Cfg::TMEM_COLS);
   }
+}
+
+// =================================================================== forward: narrow tail levels
+// Levels with at most a few rows (the tops of trees, chains, single trees) are latency
+// bound: in k_fwd_levels every such level still streams its U slab through shared memory
+// and runs M = 256 MMAs for a handful of rows. k_fwd_narrow keeps U STATIONARY instead and
+// swaps the operands: CTA x owns state columns [8x, 8x + 8) and holds their GATES * 8
+// gate-interleaved U rows (all 2S inputs) in shared memory for the whole kernel; per chunk
+// of <= 8 rows of a level it loads only the chunk's A rows (8 x 2S bf16) and computes
+// Z^T = U_x * A^T with one CTA (cta_group::1). An SS-mode MMA costs about its operand bytes
+// read from shared memory, dominated by the M = 128 U operand, so the two K halves (h_L and
+// h_R inputs) are stacked in M: slot q holds U_x[:, K-block q of h_L] in rows 0..UROWS-1 and
+// U_x[:, K-block q of h_R] in rows UROWS..2 UROWS-1 (rows past that alias the next slot and
+// are never read back), the B operand holds the chunk's h_L K-block q in rows 0..7 and its
+// h_R K-block q in rows 8..15 (SBO = the distance between the halves), so one M = 128,
+// N = 16 MMA per 16 K advances both halves: Z = D[0:UROWS, 0:8] + D[UROWS:2 UROWS, 8:16],
+// S/16 MMAs per chunk instead of 2S/16. The epilogue (three warps = TMEM lanes 0..95)
+// regroups the gates of each (state column, row) through shared memory, applies the cell,
+// appends c / G, pushes h to the consumers' A rows and publishes h-column credits exactly
+// like k_fwd_levels, so the two kernels share the dependency counters (this one runs after
+// it, on the remaining levels d0..D).
+constexpr int NW_ROWS = 8;          // rows per chunk
+constexpr int NW_THREADS = 224;     // warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4-6 epilogue
+constexpr int NW_MAX_S = 1024;      // U slice (GATES*8 rows x 2S) + A chunk fit in shared memory
+
+template <int GATES>
+struct NwCfg {
+  static constexpr int UROWS = GATES * 8;               // U rows per CTA (per K half)
+  static constexpr int USLOT = 2 * UROWS * 128;         // bytes per K-block slot (both halves)
+  static constexpr int SLACK = (16 - 2 * UROWS / 8) * 1024; // the M = 128 operand reads 16 8-row groups
+  static constexpr int BKB = NW_ROWS * 128;             // bytes per K-block of the A chunk
+  static int smem(int KBh) { return 2 * KBh * BKB + KBh * USLOT + SLACK + 1024; }
+  static_assert(2 * UROWS <= 96, "both halves' U rows are read by TMEM lane quarters 0..2");
+};
+
+template <int GATES>
+__global__ void __launch_bounds__(NW_THREADS, 1)
+    k_fwd_narrow(const __grid_constant__ CUtensorMap tmUs, const __grid_constant__ CUtensorMap tmAL8,
+                 const __grid_constant__ CUtensorMap tmAR8, const __grid_constant__ CUtensorMap tmA4, int use3d,
+                 const int32_t *__restrict__ lo, int d0, int D, int S,
+                 int nl, int ld, const int32_t *__restrict__ gather, const float *__restrict__ bias,
+                 __nv_bfloat16 *__restrict__ H, float *C, __nv_bfloat16 *__restrict__ Gact, int ld_g, ScatterA sc,
+                 int *rt_cnt, const int32_t *__restrict__ tstart, int dbg) {
+  using Cfg = NwCfg<GATES>;
+  dbg = dbg && blockIdx.x == 0;  // timeline of CTA 0 only
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = align1024(smem_raw);
+  const int KBh = (int)cdiv(S, BK), KB = 2 * KBh, Sp = KBh * BK;
+  uint8_t *Bsm = smem, *Usm = smem + KB * Cfg::BKB;  // B: [slot][half][8 rows]; U: [slot][half][UROWS]
+  __shared__ __align__(8) uint64_t u_full, b_full, b_empty, acc_full[2], acc_empty[2];
+  __shared__ float zs[2][GATES * 8][NW_ROWS + 1];
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int j0 = blockIdx.x * 8;
+  const int ncols = min(8, S - j0);
+  if (tid == 0) {
+    ptx::mbar_init(&u_full, 1);
+    ptx::mbar_init(&b_full, 1);
+    ptx::mbar_init(&b_empty, 1);
+    for (int a = 0; a < 2; a++) { ptx::mbar_init(&acc_full[a], 1); ptx::mbar_init(&acc_empty[a], 3); }
+    ptx::fence_mbar_init();
+    ptx::prefetch_tmap(&tmUs);
+    ptx::prefetch_tmap(&tmAL8);
+    ptx::prefetch_tmap(&tmAR8);
+    ptx::prefetch_tmap(&tmA4);
+  }
+  if (warp == 2) { ptx::tmem_alloc(&tmem_base_sh, 32); ptx::tmem_relinquish(); }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = tmem_base_sh;
+
+  // chunk walk (every role keeps its own cursor): level d, rows [r, r + rows)
+  struct Cur {
+    int d, r, r1;
+    __device__ void init(const int32_t *lo, int d0) { d = d0; r = __ldg(lo + d); r1 = __ldg(lo + d + 1); }
+    __device__ bool next(const int32_t *lo, int D) {  // advance to the next chunk
+      r += NW_ROWS;
+      while (r >= r1) {
+        if (++d > D) return false;
+        r = __ldg(lo + d); r1 = __ldg(lo + d + 1);
+      }
+      return true;
+    }
+    __device__ bool valid(const int32_t *lo, int D) {  // skip empty leading levels
+      while (r >= r1) {
+        if (++d > D) return false;
+        r = __ldg(lo + d); r1 = __ldg(lo + d + 1);
+      }
+      return true;
+    }
+  };
+  // a chunk's inputs are complete once its 256-row tile has all 2S h columns of its rows
+  auto tile_target = [&](const Cur &cu, int &key) {
+    const int c = cu.r - nl;
+    key = __ldg(tstart + c);
+    const int tend = min(key + PM, cu.r1 - nl);
+    return (tend - key) * 2 * S;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(&u_full, (uint32_t)(KBh * Cfg::USLOT));
+      for (int kb = 0; kb < KB; kb++) {
+        const int half = kb >= KBh, q = kb - half * KBh;
+        ptx::tma_load_2d(&tmUs, &u_full, Usm + q * Cfg::USLOT + half * (Cfg::USLOT / 2), half * Sp + q * BK,
+                         blockIdx.x * Cfg::UROWS);
+      }
+      Cur cu;
+      cu.init(lo, d0);
+      int i = 0;
+      for (bool ok = cu.valid(lo, D); ok; ok = cu.next(lo, D), i++) {
+        if (i > 0) ptx::mbar_wait(&b_empty, (i - 1) & 1);
+        trace(dbg, 0, i);
+        int key;
+        const int target = tile_target(cu, key);
+        ptx::wait_counter_relaxed(rt_cnt + key, target);
+        ptx::fence_proxy_async_global();
+        trace(dbg, 1, i);
+        ptx::mbar_arrive_expect_tx(&b_full, (uint32_t)(KB * Cfg::BKB));
+        const int c0 = cu.r - nl;
+        if (use3d) {  // one 4D box: the chunk's 8 rows x both halves x all K-blocks
+          ptx::tma_load_4d(&tmA4, &b_full, Bsm, 0, c0, 0, 0);
+        } else {
+          for (int kb = 0; kb < KB; kb++) {
+            const int half = kb >= KBh, q = kb - half * KBh;
+            ptx::tma_load_2d(half ? &tmAR8 : &tmAL8, &b_full, Bsm + (2 * q + half) * Cfg::BKB, q * BK, c0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16(128, 2 * NW_ROWS, 0, 0);
+      ptx::mbar_wait(&u_full, 0);
+      Cur cu;
+      cu.init(lo, d0);
+      int i = 0;
+      for (bool ok = cu.valid(lo, D); ok; ok = cu.next(lo, D), i++) {
+        const int acc = i & 1;
+        ptx::mbar_wait(&acc_empty[acc], ((i >> 1) & 1) ^ 1);
+        ptx::mbar_wait(&b_full, i & 1);
+        ptx::tc_fence_after();
+        trace(dbg, 7, i);
+        const uint32_t dst = tbase + acc * 2 * NW_ROWS;
+        const uint32_t u0 = ptx::smem_u32(Usm), b0 = ptx::smem_u32(Bsm);
+        for (int q = 0; q < KBh; q++) {  // B rows 0..7: h_L K-block q, rows 8..15: h_R K-block q
+#pragma unroll
+          for (int k = 0; k < BK / 16; k++)
+            ptx::umma_bf16(dst, ptx::sdesc_sw128(u0 + q * Cfg::USLOT + 32 * k, 16, 1024),
+                           ptx::sdesc_sw128(b0 + 2 * q * Cfg::BKB + 32 * k, 16, 1024), idesc, (q | k) != 0);
+        }
+        ptx::umma_commit(&b_empty);
+        ptx::umma_commit(&acc_full[acc]);
+        trace(dbg, 2, i);
+      }
+    }
+  } else if (warp >= 4) {
+    const int t = tid - 128;          // 0..95 (the math uses 0..63)
+    const int q = warp & 3;           // TMEM lane quarter 0 / 1 / 2
+    const int n = t >> 3, u = t & 7;  // this thread's (row in chunk, state column) in the math
+    const int j = j0 + u;
+    Cur cu;
+    cu.init(lo, d0);
+    int i = 0;
+    for (bool ok = cu.valid(lo, D); ok; ok = cu.next(lo, D), i++) {
+      const int acc = i & 1;
+      const int rows = min(NW_ROWS, cu.r1 - cu.r);
+      const int64_t r = cu.r + n;
+      const bool act = n < rows && u < ncols;
+      // children's c (published with their h): fetched while the MMA runs
+      int64_t gl = 0, gr = 0;
+      float cl = 0.f, cr = 0.f;
+      if (act) {
+        gl = __ldg(gather + 2 * r);
+        gr = __ldg(gather + 2 * r + 1);
+        if (GATES == 5 && (gl >= nl || gr >= nl)) {
+          int key;
+          const int target = tile_target(cu, key);
+          ptx::wait_counter(rt_cnt + key, target);
+          if (gl >= nl) cl = __ldcg(C + gl * ld + j);
+          if (gr >= nl) cr = __ldcg(C + gr * ld + j);
+        }
+      }
+      if (t == 0) trace(dbg, 5, i);
+      ptx::mbar_wait(&acc_full[acc], (i >> 1) & 1);
+      ptx::tc_fence_after();
+      if (t == 0) trace(dbg, 3, i);
+      float z0[8], z1[8];
+      const int m = q * 32 + lane;  // D row = stacked U row
+      const int hf = m >= Cfg::UROWS;   // which K half this row accumulated
+      // its half's 8 columns: rows < UROWS pair with B rows 0..7, the next UROWS with 8..15
+      // (tcgen05.ld addresses are warp-uniform: read both and select per lane)
+      const uint32_t ta = tbase + acc * 2 * NW_ROWS + ((uint32_t)(q * 32) << 16);
+      ptx::tmem_ld8(ta, z0);
+      ptx::tmem_ld8(ta + NW_ROWS, z1);
+      ptx::tmem_ld_wait();
+      if (m < 2 * Cfg::UROWS)
+#pragma unroll
+        for (int k = 0; k < NW_ROWS; k++) zs[hf][m - hf * Cfg::UROWS][k] = hf ? z1[k] : z0[k];
+      ptx::tc_fence_before();
+      ptx::named_bar_sync(1, 96);
+      if (lane == 0) ptx::mbar_arrive(&acc_empty[acc]);
+      if (act) {
+        const int64_t c = r - nl;
+        float hh;
+        if constexpr (GATES == 1) {
+          hh = tanh_fast(zs[0][u][n] + zs[1][u][n] + __ldg(bias + j));
+          C[r * ld + j] = 0.f;
+          Gact[c * ld_g + j] = __float2bfloat16_rn(hh);
+        } else {
+          float gs[5];
+#pragma unroll
+          for (int g = 0; g < 5; g++) {
+            const float x = zs[0][g * 8 + u][n] + zs[1][g * 8 + u][n] + __ldg(bias + g * S + j);
+            gs[g] = g == 4 ? tanh_fast(x) : sigmoid_fast(x);
+          }
+          const float cc = gs[0] * gs[4] + gs[1] * cl + gs[2] * cr;
+          hh = gs[3] * tanh_fast(cc);
+          C[r * ld + j] = cc;
+#pragma unroll
+          for (int g = 0; g < 5; g++) Gact[c * ld_g + g * ld + j] = __float2bfloat16_rn(gs[g]);
+        }
+        const __nv_bfloat16 hv = __float2bfloat16_rn(hh);
+        const int e0 = __ldg(sc.cons_off + r), e1 = __ldg(sc.cons_off + r + 1);
+        if (e0 == e1) H[r * ld + j] = hv;
+        for (int e = e0; e < e1; e++) {
+          const int ed = __ldg(sc.cons_edge + e);
+          (((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld)[j] = hv;
+        }
+      }
+      ptx::fence_proxy_async_global();
+      ptx::named_bar_sync(1, 96);
+      if (t == 0) trace(dbg, 6, i);
+      // publish: h columns [j0, j0 + ncols) of every row of the chunk, per consumer edge
+      if (t < rows) {
+        const int64_t rr = cu.r + t;
+        const int e0 = __ldg(sc.cons_off + rr), e1 = __ldg(sc.cons_off + rr + 1);
+        if (e1 > e0) __threadfence();
+        for (int e = e0; e < e1; e++) atomicAdd(rt_cnt + __ldg(tstart + (__ldg(sc.cons_edge + e) >> 1)), ncols);
+      }
+      if (t == 0) trace(dbg, 4, i);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc(tbase, 32); }
 }
 
 // =================================================================== dA = dZ * U (one level)
@@ -1419,6 +1670,20 @@ int dbg_fwd() {
   return v;
 }
 
+// First level of the forward's narrow tail: every level d0..D has at most narrow_max rows
+// (FOLD_FWD_NARROW_MAX, default 32; 0 disables k_fwd_narrow). D + 1 if there is none or S is
+// too large for the stationary U slice.
+int fwd_narrow_start(const int32_t *lo, int D, int S) {
+  static const int narrow_max = [] {
+    const char *e = getenv("FOLD_FWD_NARROW_MAX");
+    return e ? atoi(e) : 32;
+  }();
+  if (narrow_max <= 0 || S > NW_MAX_S || S < 1) return D + 1;
+  int d0 = D + 1;
+  while (d0 - 1 >= 2 && lo[d0] - lo[d0 - 1] <= narrow_max) d0--;
+  return d0;
+}
+
 template <int GATES>
 fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
   using Cfg = FwdCfg<GATES>;
@@ -1451,13 +1716,15 @@ fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
   static thread_local int npairs_max = 0;
   if (!npairs_max) npairs_max = max_pairs(kern, Cfg::THREADS, smem_bytes);
   FwdLevels L{a.level_off, a.D, S, Cfg::WMAX, Cfg::WNAR, npairs_max / 2};
+  // the narrow tail: levels d0..D all of at most narrow_max rows go to k_fwd_narrow
+  const int d0 = fwd_narrow_start(a.level_off_host, a.D, S);
   int64_t total = 0;
-  for (int d = 2; d <= a.D; d++) {
+  for (int d = 2; d < d0; d++) {
     const int M = a.level_off_host[d + 1] - a.level_off_host[d];
     total += cdiv(M, PM) * cdiv(S, fwd_level_W(L, M));
   }
-  if (total <= 0) return FOLD_OK;
   if (total > INT32_MAX) return FOLD_E_INVALID;
+  if (total <= 0 && d0 > a.D) return FOLD_OK;
   FOLD_CUDA_TRY(cudaMemsetAsync(a.rt_cnt, 0, (size_t)nc * sizeof(int), st));
   {
     int64_t blocks = cdiv(nc, 256);
@@ -1465,11 +1732,61 @@ fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
     k_fwd_prelude<<<(unsigned)blocks, 256, 0, st>>>(a.level_off, a.D, a.nl, nc, S, a.gather, a.tstart, a.rt_cnt);
     FOLD_LAUNCH_CHECK();
   }
-  const int npairs = total < npairs_max ? (int)total : npairs_max;
-  kern<<<2 * npairs, Cfg::THREADS, smem_bytes, st>>>(tmAL, tmAR, tmAL16, tmAR16, tmAL64, tmAR64, tmUw, tmUn, tmGw, tmGn, tmCw, tmCn, L, (int)total,
-                                                      a.nl, a.ld, a.gather, a.b, a.H, a.C, a.Gact, a.ld_g, a.sc,
-                                                      a.rt_cnt, a.tstart, dbg_fwd());
-  FOLD_LAUNCH_CHECK();
+  if (total > 0) {
+    const int npairs = total < npairs_max ? (int)total : npairs_max;
+    kern<<<2 * npairs, Cfg::THREADS, smem_bytes, st>>>(tmAL, tmAR, tmAL16, tmAR16, tmAL64, tmAR64, tmUw, tmUn, tmGw,
+                                                        tmGn, tmCw, tmCn, L, (int)total, a.nl, a.ld, a.gather, a.b,
+                                                        a.H, a.C, a.Gact, a.ld_g, a.sc, a.rt_cnt, a.tstart,
+                                                        dbg_fwd());
+    FOLD_LAUNCH_CHECK();
+  }
+  if (d0 <= a.D) {
+    using NC = NwCfg<GATES>;
+    CUtensorMap tmUs, tmAL8, tmAR8;
+    FOLD_TRY(make_map(&tmUs, a.Ub, (uint64_t)a.ld_u, il_rows, (uint64_t)a.ld_u * 2, BK, NC::UROWS));
+    FOLD_TRY(make_map(&tmAL8, a.sc.AL, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, NW_ROWS));
+    FOLD_TRY(make_map(&tmAR8, a.sc.AR, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, NW_ROWS));
+    // 4D view of the two planes as [K-block][half][row][64 columns] (S % 64 == 0 and A_R at a
+    // fixed offset from A_L): one box = the chunk's 8 rows of both halves and all K-blocks,
+    // landing slot-major with the halves interleaved (the B operand's 8-row groups)
+    CUtensorMap tmA4;
+    const int64_t half_off = (const char *)a.sc.AR - (const char *)a.sc.AL;
+    int use3d = (S % BK == 0) && (S / BK) <= 256 && half_off > 0 && half_off % 16 == 0;
+    if (use3d) {
+      auto enc = encode_fn();
+      if (!enc) return FOLD_E_CUDA;
+      cuuint64_t dims[4] = {(cuuint64_t)BK, (cuuint64_t)nc, 2, (cuuint64_t)(S / BK)};
+      cuuint64_t strides[3] = {(cuuint64_t)a.sc.ld * 2, (cuuint64_t)half_off, (cuuint64_t)BK * 2};
+      cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)NW_ROWS, 2, (cuuint32_t)(S / BK)};
+      cuuint32_t es[4] = {1, 1, 1, 1};
+      CUresult r = enc(&tmA4, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void *)a.sc.AL, dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) use3d = 0;
+    }
+    if (!use3d) tmA4 = tmAL8;
+    const int nsm = NC::smem((int)cdiv(S, BK));
+    auto nk = k_fwd_narrow<GATES>;
+    FOLD_TRY(set_smem(nk, nsm));
+    const int grid = (int)cdiv(S, 8);
+    const int32_t *lo = a.level_off;
+    int D = a.D, nl = a.nl, ld = a.ld, ld_g = a.ld_g;
+    const int32_t *gather = a.gather;
+    const float *bias = a.b;
+    __nv_bfloat16 *H = a.H, *G = a.Gact;
+    float *C = a.C;
+    ScatterA sc = a.sc;
+    int *rt = a.rt_cnt;
+    const int32_t *ts = a.tstart;
+    int d0v = d0, Sv = S, dbgv = dbg_fwd() == 2;
+    void *args[] = {(void *)&tmUs, (void *)&tmAL8, (void *)&tmAR8, (void *)&tmA4, (void *)&use3d,
+                    (void *)&lo, (void *)&d0v, (void *)&D,
+                    (void *)&Sv, (void *)&nl, (void *)&ld, (void *)&gather, (void *)&bias, (void *)&H, (void *)&C,
+                    (void *)&G, (void *)&ld_g, (void *)&sc, (void *)&rt, (void *)&ts, (void *)&dbgv};
+    // cooperative: every CTA must be resident (they wait on each other's published columns)
+    FOLD_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)nk, dim3(grid), dim3(NW_THREADS), args, (size_t)nsm, st));
+    FOLD_LAUNCH_CHECK();
+  }
   return FOLD_OK;
 }
 
