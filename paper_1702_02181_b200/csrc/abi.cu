@@ -39,7 +39,7 @@ struct BwdWs {
   int32_t *tstart;  // [n_cells]
   EmbedBwdWs emb;
   void *dZ;
-  __nv_bfloat16 *Ub;
+  __nv_bfloat16 *Ub, *Ut;
   int ld_z, nsplit;
   size_t bytes;
 };
@@ -65,6 +65,7 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
   size_t o_ss = take((size_t)scan_sums_count(nseg + 1) * 4);
   size_t o_ep = take((size_t)max_pieces * S * 4);
   size_t o_w = take(bf16 ? tc_weights_bytes(gates, (int)S) : 0);
+  size_t o_ut = take(bf16 ? tc_ut_bytes(gates, (int)S) : 0);
   const int splits = bf16 ? tc_dU_splits((int)nc, gates, (int)S) : 1;
   size_t o_spl = take(splits > 1 ? (size_t)splits * gates * S * 2 * S * 4 : 0);
   b.bytes = off;
@@ -83,6 +84,7 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
     b.emb.partial = (float *)(p + o_ep);
     b.dU_split = splits > 1 ? (float *)(p + o_spl) : nullptr;
     b.Ub = bf16 ? (__nv_bfloat16 *)(p + o_w) : nullptr;
+    b.Ut = bf16 ? (__nv_bfloat16 *)(p + o_ut) : nullptr;
   }
   return b;
 }
@@ -274,7 +276,7 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
     TcBwdArgs ba{};
     ba.level_off = s->level_off; ba.level_off_host = lo;
     ba.D = D; ba.S = S; ba.nl = nl; ba.n_cells = nc; ba.ld = L.ld; ba.ld_g = L.ld_g; ba.ld_z = b.ld_z;
-    ba.gather = s->gather; ba.Ub = b.Ub; ba.Gact = (const __nv_bfloat16 *)Gact; ba.C = C;
+    ba.gather = s->gather; ba.Ub = b.Ub; ba.U = m->U; ba.Ut = b.Ut; ba.Gact = (const __nv_bfloat16 *)Gact; ba.C = C;
     ba.dA = b.dA; ba.dCe = b.dCe; ba.dZ = (__nv_bfloat16 *)b.dZ; ba.rt_cnt = b.rt_cnt; ba.tstart = b.tstart;
     {
       ProfScope ps(K_BWD_PW, st);

@@ -80,6 +80,7 @@ fold_status launch_zero(void *p, size_t bytes, cudaStream_t st);
 // gate-interleaved in 8-column blocks for the forward (K-major B operand, one TMA box).
 int tc_ld_u(int S);
 int tc_debug_fwd_trace(unsigned long long *host, int n);
+size_t tc_ut_bytes(int gates, int S);
 size_t tc_weights_bytes(int gates, int S);
 fold_status tc_prepare_U(int gates, int S, const float *U, __nv_bfloat16 *Ub, cudaStream_t st);
 // the forward's gate-interleaved copy (Uil8, same size)
@@ -105,6 +106,8 @@ struct TcBwdArgs {
   const int32_t *level_off, *level_off_host;
   int D, S, nl, n_cells, ld, ld_g, ld_z;
   const int32_t *gather;
+  const float *U;        // fp32 master (the narrow backward's transposed copy is made from it)
+  __nv_bfloat16 *Ut;     // workspace [2 Sp][gates*S] for that copy
   const __nv_bfloat16 *Ub, *Gact;
   const float *C;
   float *dA, *dCe;

@@ -1015,8 +1015,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // dz(x) -> dZ row of x and dCe of x's two edges. The dA rows never reach memory except for
 // leaf children (the embedding gradient reads them). Dependencies are per 256-row tile, not
 // per level: every tile has a counter (keyed by its first cell) that the epilogues of its
-// rows' consumers raise by one per (row, 64-column slab) they complete; the tile's TMA
-// producer waits for rows x slabs, so a tile starts as soon as ITS rows are ready, and the
+// rows' consumers raise by the number of columns of each row they complete; the tile's TMA
+// producer waits for rows x S, so a tile starts as soon as ITS rows are ready, and the
 // depth order of PAPER.md L49 holds without level-wide drains. Roots' dZ come from a seeded
 // pointwise pass launched before (their counts are pre-set by k_bwd_prelude).
 // Epilogue layout: each warp owns 32 accumulator rows; per 64-column slab it moves the
@@ -1255,7 +1255,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
           }
         }
       }
-      int slab_cnt[2] = {0, 0};  // 64-column slabs this warp completes, per half
+      int slab_cnt[2] = {0, 0};  // columns this warp completes (its 64-column slabs), per half
       ptx::mbar_wait(&tfull[acc], (tc >> 1) & 1);
       ptx::tc_fence_after();
       const uint32_t tl = tbase + acc * 256 + ((uint32_t)(q * 32) << 16);
@@ -1278,7 +1278,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         const int half = np >= Sp;
         const int col = np - half * Sp + 2 * lane;  // this lane's 2 state columns
         const bool colok = col < S;                  // S even (checked by the host)
-        if (np - half * Sp < S) slab_cnt[half]++;
+        if (np - half * Sp < S) slab_cnt[half] += min(64, S - (np - half * Sp));
         // rows in groups of R: all loads of the group first (memory-level parallelism),
         // then the math and the stores
         constexpr int R = 6;
@@ -1363,7 +1363,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_leader(&tempty[acc]);
       // publish: every lane fences its own dZ / dCe stores, then lane i credits the tiles of
-      // row i's children with the slabs this warp completed
+      // row i's children with the columns this warp completed
       ptx::fence_proxy_async_global();
       __threadfence();
       __syncwarp();
@@ -1375,6 +1375,218 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
   ptx::tc_fence_before();
   ptx::cluster_sync();
   if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc2(tbase, 512); }
+}
+
+// =================================================================== backward: narrow top levels
+// The backward's first levels (the tree tops, chains, single trees) are latency bound like
+// the forward's last ones. k_bwd_narrow keeps U stationary and swaps the operands: CTA x
+// owns 16 dA columns [16x, 16x + 16) of the padded [h_L | h_R] layout and holds U[:, those
+// columns] (all GATES*S rows) in shared memory, read from the transposed bf16 copy Ut
+// [2 Sp][GATES*S] (K-major A operand). The K = GATES*S reduction is cut into 8 parts of Kp
+// rows stacked in M (M row 16 p + c = column c over part p; one 3D TMA box per K-block
+// fetches all 8 parts' 16 rows), and the chunk's <= 4 dZ rows are stacked
+// the same way in N (N row 4 p + n = row n's dZ over part p), so one M = 128, N = 32 MMA
+// advances all 8 parts: dA[n][c] = sum_p D[16 p + c][4 p + n], Kp/16 MMAs per chunk. The
+// epilogue sums the parts and runs the child's pointwise step for its 16 columns (the same
+// arithmetic as k_bwd_levels' epilogue), then credits the child's row tile with the columns
+// done, so the wide kernel (launched after it, on the remaining levels) sees the same
+// dependency counters.
+constexpr int NB_ROWS = 4;        // rows per chunk
+constexpr int NB_PARTS = 8;       // K parts stacked in M (16 columns each) and N (4 rows each)
+constexpr int NB_THREADS = 256;   // warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4-7 epilogue
+
+template <int GATES>
+__global__ void __launch_bounds__(NB_THREADS, 1)
+    k_bwd_narrow(const __grid_constant__ CUtensorMap tmU3, const __grid_constant__ CUtensorMap tmZ4,
+                 const int32_t *__restrict__ lo, int D, int d1, int S, int nl, int Kp,
+                 const int32_t *__restrict__ gather, const __nv_bfloat16 *__restrict__ Gact, int ld_g,
+                 const float *__restrict__ C, int ld, float *dA, float *dCe, __nv_bfloat16 *dZ, int ld_z, int *rt_cnt,
+                 const int32_t *__restrict__ tstart) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = align1024(smem_raw);
+  const int NSLOT = Kp / BK;              // K-blocks per part
+  constexpr int USLOT = NB_PARTS * 16 * 128;   // bytes per K-block slot of the U slice (128 rows)
+  uint8_t *Usm = smem, *Bsm = smem + NSLOT * USLOT;  // U: [slot][part][16 rows]; B: [slot][part][4 rows]
+  __shared__ __align__(8) uint64_t u_full, b_full, b_empty, acc_full[2], acc_empty[2];
+  __shared__ float red[NB_PARTS][16][NB_ROWS + 1];
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int Sp = (int)round_up(S, BK);
+  const int col0 = blockIdx.x * 16, half = col0 >= Sp, j0 = col0 - half * Sp;
+  const int ncols = min(16, S - j0);
+  if (ncols <= 0) return;  // padding columns only (uniform over the CTA)
+  if (tid == 0) {
+    ptx::mbar_init(&u_full, 1);
+    ptx::mbar_init(&b_full, 1);
+    ptx::mbar_init(&b_empty, 1);
+    for (int a = 0; a < 2; a++) { ptx::mbar_init(&acc_full[a], 1); ptx::mbar_init(&acc_empty[a], 4); }
+    ptx::fence_mbar_init();
+    ptx::prefetch_tmap(&tmU3);
+    ptx::prefetch_tmap(&tmZ4);
+  }
+  if (warp == 2) { ptx::tmem_alloc(&tmem_base_sh, 64); ptx::tmem_relinquish(); }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = tmem_base_sh;
+
+  struct Cur {  // chunks of levels D, D-1, ..., d1
+    int d, r, r1;
+    __device__ bool load(const int32_t *lo, int d1) {
+      for (;; d--) {
+        if (d < d1) return false;
+        r = __ldg(lo + d); r1 = __ldg(lo + d + 1);
+        if (r < r1) return true;
+      }
+    }
+    __device__ bool init(const int32_t *lo, int D, int d1) { d = D; return load(lo, d1); }
+    __device__ bool next(const int32_t *lo, int d1) {
+      r += NB_ROWS;
+      if (r < r1) return true;
+      d--;
+      return load(lo, d1);
+    }
+  };
+  auto tile_target = [&](const Cur &cu, int &key) {
+    const int c = cu.r - nl;
+    key = __ldg(tstart + c);
+    const int tend = min(key + PM, cu.r1 - nl);
+    return (tend - key) * S;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(&u_full, (uint32_t)(NSLOT * USLOT));
+      for (int q = 0; q < NSLOT; q++) ptx::tma_load_3d(&tmU3, &u_full, Usm + q * USLOT, q * BK, col0, 0);
+      Cur cu;
+      int i = 0;
+      for (bool ok = cu.init(lo, D, d1); ok; ok = cu.next(lo, d1), i++) {
+        if (i > 0) ptx::mbar_wait(&b_empty, (i - 1) & 1);
+        int key;
+        const int target = tile_target(cu, key);
+        ptx::wait_counter(rt_cnt + key, target);
+        ptx::fence_proxy_async_global();
+        ptx::mbar_arrive_expect_tx(&b_full, (uint32_t)(NSLOT * NB_PARTS * NB_ROWS * 128));
+        ptx::tma_load_4d(&tmZ4, &b_full, Bsm, 0, cu.r - nl, 0, 0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16(128, NB_PARTS * NB_ROWS, 0, 0);
+      ptx::mbar_wait(&u_full, 0);
+      Cur cu;
+      int i = 0;
+      for (bool ok = cu.init(lo, D, d1); ok; ok = cu.next(lo, d1), i++) {
+        const int acc = i & 1;
+        ptx::mbar_wait(&acc_empty[acc], ((i >> 1) & 1) ^ 1);
+        ptx::mbar_wait(&b_full, i & 1);
+        ptx::tc_fence_after();
+        const uint32_t dst = tbase + acc * NB_PARTS * NB_ROWS;
+        const uint32_t u0 = ptx::smem_u32(Usm), b0 = ptx::smem_u32(Bsm);
+        for (int q = 0; q < NSLOT; q++) {
+#pragma unroll
+          for (int k = 0; k < BK / 16; k++)
+            ptx::umma_bf16(dst, ptx::sdesc_sw128(u0 + q * USLOT + 32 * k, 16, 1024),
+                           ptx::sdesc_sw128(b0 + q * (NB_PARTS * NB_ROWS * 128) + 32 * k, 16, 1024), idesc,
+                           (q | k) != 0);
+        }
+        ptx::umma_commit(&b_empty);
+        ptx::umma_commit(&acc_full[acc]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int t = tid - 128;           // 0..127 (the pointwise uses 0..63)
+    const int qw = warp & 3;           // TMEM lane quarter = M rows 32 qw .. 32 qw + 31
+    const int n = t >> 4, c = t & 15;  // this thread's (row in chunk, column) in the pointwise
+    const int j = j0 + c;
+    Cur cu;
+    int i = 0;
+    for (bool ok = cu.init(lo, D, d1); ok; ok = cu.next(lo, d1), i++) {
+      const int acc = i & 1;
+      const int rows = min(NB_ROWS, cu.r1 - cu.r);
+      const int64_t r = cu.r + n;
+      const bool act = t < 64 && n < rows && c < ncols;
+      // operands of the child's pointwise step (G / C from the forward; dCe of the edge was
+      // written by this row's own pointwise step, published with its dZ)
+      int64_t x = -1, xl = -1, xr = -1;
+      float gg[GATES], cc = 0.f, cl = 0.f, cr = 0.f, dc = 0.f;
+      const int64_t e = 2 * (r - nl) + half;
+      if (act) {
+        x = __ldg(gather + 2 * r + half);
+        if (x >= nl) {
+          const int64_t xc = x - nl;
+          const __nv_bfloat16 *gx = Gact + xc * ld_g + j;
+#pragma unroll
+          for (int g = 0; g < GATES; g++) gg[g] = __bfloat162float(gx[g * ld]);
+          if constexpr (GATES == 5) {
+            xl = __ldg(gather + 2 * x);
+            xr = __ldg(gather + 2 * x + 1);
+            cc = __ldcg(C + x * ld + j);
+            if (xl >= nl) cl = __ldcg(C + xl * ld + j);
+            if (xr >= nl) cr = __ldcg(C + xr * ld + j);
+            int key;
+            const int target = tile_target(cu, key);
+            ptx::wait_counter(rt_cnt + key, target);
+            dc = __ldcg(dCe + e * S + j);
+          }
+        }
+      }
+      ptx::mbar_wait(&acc_full[acc], (i >> 1) & 1);
+      ptx::tc_fence_after();
+      float z[8];
+      ptx::tmem_ld8(tbase + acc * NB_PARTS * NB_ROWS + qw * 8 + ((uint32_t)(qw * 32) << 16), z);
+      ptx::tmem_ld_wait();
+      {  // M row 32 qw + lane = (part 2 qw + lane / 16, column lane % 16); its rows are
+         // D columns 4 part .. 4 part + 3 = this warp's columns 8 qw + 4 (lane / 16) ..
+        const int hi = lane >> 4, p = 2 * qw + hi;
+#pragma unroll
+        for (int k = 0; k < NB_ROWS; k++) red[p][lane & 15][k] = hi ? z[4 + k] : z[k];
+      }
+      ptx::tc_fence_before();
+      ptx::named_bar_sync(1, 128);
+      if (lane == 0) ptx::mbar_arrive(&acc_empty[acc]);
+      if (act) {
+        float dh = 0.f;
+#pragma unroll
+        for (int p = 0; p < NB_PARTS; p++) dh += red[p][c][n];
+        if (x < nl) {
+          dA[e * S + j] = dh;  // leaf child: the embedding gradient reads dA
+        } else {
+          const int64_t xc = x - nl;
+          __nv_bfloat16 *dz = dZ + xc * ld_z + j;
+          if constexpr (GATES == 1) {
+            dz[0] = __float2bfloat16_rn(dh * (1.f - gg[0] * gg[0]));
+          } else {
+            const float ig = gg[0], fl = gg[1], fr = gg[2], og = gg[3], ug = gg[4];
+            const float tcv = tanhf(cc);
+            const float dO = dh * tcv;
+            const float dcc = dc + dh * og * (1.f - tcv * tcv);
+            dz[0] = __float2bfloat16_rn(dcc * ug * ig * (1.f - ig));
+            dz[S] = __float2bfloat16_rn(dcc * cl * fl * (1.f - fl));
+            dz[2 * S] = __float2bfloat16_rn(dcc * cr * fr * (1.f - fr));
+            dz[3 * S] = __float2bfloat16_rn(dO * og * (1.f - og));
+            dz[4 * S] = __float2bfloat16_rn(dcc * ig * (1.f - ug * ug));
+            dCe[(2 * xc) * S + j] = dcc * fl;
+            dCe[(2 * xc + 1) * S + j] = dcc * fr;
+          }
+        }
+      }
+      ptx::fence_proxy_async_global();
+      ptx::named_bar_sync(1, 128);
+      // publish: each cell child of the chunk's rows gets this CTA's columns
+      if (t < rows) {
+        const int64_t rr = cu.r + t;
+        const int64_t xx = __ldg(gather + 2 * rr + half);
+        if (xx >= nl) {
+          __threadfence();
+          atomicAdd(rt_cnt + __ldg(tstart + (xx - nl)), ncols);
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc(tbase, 64); }
 }
 
 // Row-tile bookkeeping for k_bwd_levels: tstart[c] = first cell of c's 256-row tile (tiles
@@ -1825,6 +2037,40 @@ fold_status tc_prepare_U(int gates, int S, const float *U, __nv_bfloat16 *Ub, cu
   return FOLD_OK;
 }
 
+// Ut[r][k] = U[k][half * S + j] in bf16 for the padded column r = half * Sp + j (0 for
+// j >= S): the narrow backward's K-major copy of U's columns. 32 x 32 tiles through shared
+// memory (coalesced reads of U rows and writes of Ut rows).
+__global__ void k_prep_Ut(int K, int S, int Sp, const float *__restrict__ U, __nv_bfloat16 *__restrict__ Ut) {
+  __shared__ float tile[32][33];
+  const int R = 2 * Sp;
+  const int ntk = (K + 31) / 32, ntr = (R + 31) / 32;
+  for (int t = blockIdx.x; t < ntk * ntr; t += gridDim.x) {
+    const int k0 = (t / ntr) * 32, r0 = (t % ntr) * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {  // rows k0 + i of U, columns r0 + tx
+      const int k = k0 + i, r = r0 + threadIdx.x;
+      const int half = r >= Sp, j = r - half * Sp;
+      tile[i][threadIdx.x] = (k < K && r < R && j < S) ? __ldg(U + (int64_t)k * 2 * S + half * S + j) : 0.f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {  // rows r0 + i of Ut, columns k0 + tx
+      const int r = r0 + i, k = k0 + threadIdx.x;
+      if (r < R && k < K) Ut[(int64_t)r * K + k] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+    }
+    __syncthreads();
+  }
+}
+
+fold_status tc_prepare_Ut(int gates, int S, const float *U, __nv_bfloat16 *Ut, cudaStream_t st) {
+  if (!U || !Ut) return FOLD_E_INVALID;
+  const int Sp = (int)round_up(S, BK), K = gates * S;
+  int64_t tiles = cdiv(K, 32) * cdiv(2 * Sp, 32);
+  unsigned grid = (unsigned)(tiles < 148 * 16 ? tiles : 148 * 16);
+  k_prep_Ut<<<grid, dim3(32, 8), 0, st>>>(K, S, Sp, U, Ut);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+size_t tc_ut_bytes(int gates, int S) { return round_up((size_t)2 * round_up(S, BK) * gates * S * 2, 256); }
+
 fold_status tc_fwd_levels(int cell, const TcFwdArgs &a, cudaStream_t st) {
   if (a.D < 2) return FOLD_OK;
   if (cell == FOLD_CELL_TREELSTM) return launch_fwd_levels<5>(a, st);
@@ -1848,7 +2094,9 @@ fold_status tc_gemm_dA(int c0, int M, int n_cells, int S, int gates, const __nv_
   return FOLD_OK;
 }
 
-int tc_bwd_slabs(int S) { return (int)cdiv(S, 64); }
+// backward dependency credits: a child row is complete once all S columns of its pointwise
+// step are written (credits are columns, so tiles of any width can publish)
+int tc_bwd_slabs(int S) { return S; }
 
 fold_status tc_bwd_prelude(const TcBwdArgs &a, const int32_t *cons_off, cudaStream_t st) {
   if (a.n_cells <= 0) return FOLD_OK;
@@ -1859,6 +2107,20 @@ fold_status tc_bwd_prelude(const TcBwdArgs &a, const int32_t *cons_off, cudaStre
                                                   tc_bwd_slabs(a.S));
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
+}
+
+// First level (from the top) handled by the wide backward: levels d1..D all of at most
+// FOLD_BWD_NARROW_MAX rows (default 32; 0 disables) run in k_bwd_narrow, which needs
+// GATES*S/8 to be a multiple of 64 and S <= 1024 (the stationary U slice). D + 1 if none.
+int bwd_narrow_start(const int32_t *lo, int D, int S, int gates) {
+  static const int narrow_max = [] {
+    const char *e = getenv("FOLD_BWD_NARROW_MAX");
+    return e ? atoi(e) : 32;
+  }();
+  if (narrow_max <= 0 || S > 1024 || (gates * S) % (NB_PARTS * BK) != 0) return D + 1;
+  int d1 = D + 1;
+  while (d1 - 1 >= 2 && lo[d1] - lo[d1 - 1] <= narrow_max) d1--;
+  return d1;
 }
 
 fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
@@ -1875,9 +2137,57 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
   FOLD_TRY(set_smem(kern, BW_SMEM));
   static thread_local int npairs_max = 0;
   if (!npairs_max) npairs_max = max_pairs(kern, BW_THREADS, BW_SMEM);
-  BwdLevels L{a.level_off, a.D, S, a.nl, ld_u, npairs_max};
+  // the narrow top: levels D..d1 (all of at most FOLD_BWD_NARROW_MAX rows) run first in
+  // k_bwd_narrow, the wide kernel takes levels d1-1..2
+  const int d1 = bwd_narrow_start(a.level_off_host, a.D, S, gates);
+  if (d1 <= a.D) {
+    const int Kp = gates * S / NB_PARTS;
+    const int nsm = (Kp / BK) * (NB_PARTS * 16 * 128) + (Kp / BK) * NB_PARTS * NB_ROWS * 128 + 1024;
+    auto enc = encode_fn();
+    if (!enc) return FOLD_E_CUDA;
+    FOLD_TRY(tc_prepare_Ut(gates, S, a.U, a.Ut, st));
+    CUtensorMap tmU3, tmZ4;
+    {  // Ut [2 Sp][GATES*S] viewed as [part][row][K in part]: box 64 K x 16 rows x 8 parts
+      const int K = gates * S;
+      cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)ld_u, (cuuint64_t)NB_PARTS};
+      cuuint64_t strides[2] = {(cuuint64_t)K * 2, (cuuint64_t)Kp * 2};
+      cuuint32_t box[3] = {(cuuint32_t)BK, 16, (cuuint32_t)NB_PARTS};
+      cuuint32_t es[3] = {1, 1, 1};
+      if (enc(&tmU3, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void *)a.Ut, dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return FOLD_E_CUDA;
+    }
+    {  // dZ viewed as [K-block][part][row][64]: box = a chunk's rows x all parts x all K-blocks
+      cuuint64_t dims[4] = {(cuuint64_t)BK, (cuuint64_t)a.n_cells, (cuuint64_t)NB_PARTS, (cuuint64_t)(Kp / BK)};
+      cuuint64_t strides[3] = {(cuuint64_t)a.ld_z * 2, (cuuint64_t)Kp * 2, (cuuint64_t)BK * 2};
+      cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)NB_ROWS, (cuuint32_t)NB_PARTS, (cuuint32_t)(Kp / BK)};
+      cuuint32_t es[4] = {1, 1, 1, 1};
+      if (enc(&tmZ4, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void *)a.dZ, dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return FOLD_E_CUDA;
+    }
+    auto nk = gates == 5 ? k_bwd_narrow<5> : k_bwd_narrow<1>;
+    FOLD_TRY(set_smem(nk, nsm));
+    const int grid = ld_u / 16;
+    const int32_t *lo = a.level_off;
+    int D = a.D, d1v = d1, Sv = S, nl = a.nl, Kpv = Kp, ld_g = a.ld_g, ld = a.ld, ld_z = a.ld_z;
+    const int32_t *gather = a.gather, *ts = a.tstart;
+    const __nv_bfloat16 *G = a.Gact;
+    const float *C = a.C;
+    float *dA = a.dA, *dCe = a.dCe;
+    __nv_bfloat16 *dZ = a.dZ;
+    int *rt = a.rt_cnt;
+    void *args[] = {(void *)&tmU3, (void *)&tmZ4, (void *)&lo, (void *)&D, (void *)&d1v, (void *)&Sv, (void *)&nl,
+                    (void *)&Kpv, (void *)&gather, (void *)&G, (void *)&ld_g, (void *)&C, (void *)&ld, (void *)&dA,
+                    (void *)&dCe, (void *)&dZ, (void *)&ld_z, (void *)&rt, (void *)&ts};
+    FOLD_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)nk, dim3(grid), dim3(NB_THREADS), args, (size_t)nsm, st));
+    FOLD_LAUNCH_CHECK();
+  }
+  BwdLevels L{a.level_off, d1 - 1, S, a.nl, ld_u, npairs_max};
   int64_t total = 0;
-  for (int d = 2; d <= a.D; d++) {
+  for (int d = 2; d < d1; d++) {
     const int M = a.level_off_host[d + 1] - a.level_off_host[d];
     total += cdiv(M, PM) * cdiv(ld_u, bwd_level_N(L, M));
   }

@@ -126,3 +126,15 @@ def test_manual_unbatched_full_state():
     per level (127 dependent levels), forward + backward."""
     gr = foldgen.config_c2(1)
     _fwd_bwd(gr, foldgen.manual_levels(gr), "treelstm", "bf16", 1024)
+
+
+@pytest.mark.parametrize("B,same", [(3, False), (40, True)])
+def test_narrow_paths_s512(B, same):
+    """S = 512 (the stationary-U narrow kernels of both directions apply: GATES*S/8 is a
+    multiple of 64): ragged chunks, random shapes, dynamic and manual schedules."""
+    gr = foldgen.table1_batch(B, same, leaves=40, vocab=64)
+    import oracle as _o
+    d = _o.schedule(gr.op, gr.child, gr.token, gr.root, gr.vocab)["depth"]
+    _fwd_bwd(gr, d.astype(np.int32), "treelstm", "bf16", 512)   # levels = L40 depths
+    _fwd_bwd(gr, foldgen.manual_levels(gr), "treelstm", "bf16", 512)
+    _fwd_bwd(gr, foldgen.manual_levels(gr), "treernn", "bf16", 512)
