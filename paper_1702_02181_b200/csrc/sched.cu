@@ -449,9 +449,41 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
   gsync(flags);
 
   // ---- P4: level-synchronous depth propagation: a parent whose last
-  // pending child finishes at level L gets depth L + 1; one barrier per level
+  // pending child finishes at level L gets depth L + 1; one barrier per level.
+  // One block (small batches; deep chains are the latency-bound case): the pending counts
+  // and both frontiers live in shared memory (the sort's scratch, sized 3N for this
+  // launch), so a level is a __syncthreads plus shared-memory atomics.
   int L = 1;
-  for (; !a.level; L++) {
+  if (gridDim.x == 1 && !a.level) {
+    int *pend = dsm, *qa = dsm + N, *qb = dsm + 2 * N;
+    __shared__ int qn[2];
+    const int n0 = ld_volatile(&flags[F_QCNT + 1]);
+    for (int i = tid; i < N; i += T) pend[i] = w.pending[i];
+    for (int i = tid; i < n0; i += T) qa[i] = w.q0[i];
+    if (tid == 0) { qn[0] = n0; qn[1] = 0; }
+    __syncthreads();
+    for (;; L++) {
+      const int cb = (L & 1) ? 0 : 1;  // current queue: qa on odd levels
+      const int ncur = qn[cb];
+      if (ncur == 0) break;
+      const int *cur = cb ? qb : qa;
+      int *nxt = cb ? qa : qb;
+      for (int i = tid; i < ncur; i += T) {
+        const int x = cur[i];
+        for (int e = w.pcons_off[x]; e < w.pcons_off[x + 1]; e++) {
+          const int p = w.pcons[e];
+          if (atomicSub(&pend[p], 1) == 1) {
+            s.depth[p] = L + 1;
+            nxt[atomicAdd(&qn[cb ^ 1], 1)] = p;
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) qn[cb] = 0;  // becomes the next-next frontier
+      __syncthreads();
+    }
+  }
+  for (; !a.level && gridDim.x > 1; L++) {
     const int ncur = ld_volatile(&flags[F_QCNT + (L % 3)]);
     if (ncur == 0) break;
     const int32_t *cur = (L & 1) ? w.q0 : w.q1;
@@ -632,13 +664,34 @@ fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr
     max_blocks = nsm * (occ < 2 ? occ : 2);
     if (max_blocks > kMaxSchedBlocks) max_blocks = kMaxSchedBlocks;
   }
-  int blocks = N <= kSmallN ? 1 : (int)cdiv(N, 2048);
+  // one block up to small_n nodes, else ~per_block nodes per block (FOLD_SCHED_SMALLN /
+  // FOLD_SCHED_PER_BLOCK override the defaults for tuning experiments)
+  static const int small_n = [] {
+    const char *e = getenv("FOLD_SCHED_SMALLN");
+    const int v = e ? atoi(e) : kSmallN;
+    return v < 0 ? 0 : (v > kSmallN ? kSmallN : v);
+  }();
+  static const int per_block = [] {
+    const char *e = getenv("FOLD_SCHED_PER_BLOCK");
+    const int v = e ? atoi(e) : 2048;
+    return v < 256 ? 256 : v;
+  }();
+  int blocks = N <= small_n ? 1 : (int)cdiv(N, per_block);
   if (blocks > max_blocks) blocks = max_blocks;
+  // one block: its depth propagation keeps pending counts and both frontiers in shared
+  // memory (3N ints, at most 192 KB for kSmallN nodes)
+  size_t launch_smem = dsmem;
+  if (blocks == 1 && (size_t)3 * N * sizeof(int) > launch_smem) launch_smem = (size_t)3 * N * sizeof(int);
+  static thread_local size_t smem_set = 0;
+  if (launch_smem > smem_set) {
+    FOLD_CUDA_TRY(cudaFuncSetAttribute(k_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)launch_smem));
+    smem_set = launch_smem;
+  }
   FOLD_CUDA_TRY(cudaMemsetAsync(w.flags + F_BAR, 0, 2 * sizeof(int32_t), st));
   SchedArgs args{N, G, V, gr->op, gr->child, gr->token, gr->root, gr->level, *s, w};
   void *kargs[] = {(void *)&args};
   FOLD_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_schedule, dim3(blocks), dim3(kSchedThreads), kargs,
-                                            dsmem, st));
+                                            launch_smem, st));
   FOLD_LAUNCH_CHECK();
 
   // ---- the one host sync: flags + level_off prefix

@@ -1,6 +1,10 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_schedule.py -x -q > gpurun_out/pytest_sched.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_sched.log
-timeout 200 python tools/probe_clocks.py --steps 100 > gpurun_out/probe.json 2>&1
-timeout 200 python tools/probe_clocks.py --steps 100 --batch 1 > gpurun_out/probe_b1.json 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_sched.csv python tools/probe_clocks.py --steps 2 --batch 1024 > /dev/null 2>&1
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_sched1.csv python tools/probe_clocks.py --steps 2 --batch 1 > /dev/null 2>&1
+C="c4:1 c2:1 c2:4 c2:16 c2:64 c3:64 c3:256 c2:256 c2:1024"
+{
+python tools/sched_time.py $C
+FOLD_SCHED_SMALLN=4096 python tools/sched_time.py $C
+FOLD_SCHED_SMALLN=1024 python tools/sched_time.py $C
+FOLD_SCHED_SMALLN=1024 FOLD_SCHED_PER_BLOCK=1024 python tools/sched_time.py $C
+FOLD_SCHED_SMALLN=4096 FOLD_SCHED_PER_BLOCK=4096 python tools/sched_time.py $C
+} > gpurun_out/sched_times.txt 2>&1
+timeout 600 python -m pytest tests/test_gpu_schedule.py tests/test_gpu_manual.py -q > gpurun_out/pytest_sched.log 2>&1; echo "exit $?" >> gpurun_out/pytest_sched.log
