@@ -52,7 +52,9 @@ constexpr int kSchedThreads = 512;
 constexpr int kSchedWarps = kSchedThreads / 32;
 constexpr int kMaxBins = 1024;      // radix digit <= 10 bits
 constexpr int kMaxSchedBlocks = 512;
-constexpr int kSmallN = 16384;      // up to this many nodes: one block
+constexpr int kLoMirror = 4096;     // level_off entries mirrored after the flags (one D2H copy)
+constexpr int kSmallN = 16384;      // cap of the one-block path (shared-memory depth frontier)
+constexpr int kOneBlockN = 4096;    // default: up to this many nodes run as one block (measured)
 
 struct SchedWs {
   int32_t *flags, *ncons, *fillc, *pcons_off, *pcons, *pending, *q0, *q1;
@@ -70,7 +72,7 @@ SchedWs sched_ws_layout(void *base, int64_t N, int64_t G) {
   if (M < 1) M = 1;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return o; };
-  size_t o_flags = take(F_NFLAGS * 4);
+  size_t o_flags = take((F_NFLAGS + kLoMirror) * 4);  // flags, then a level_off prefix mirror
   size_t o_ncons = take((N + 1) * 4), o_fill = take((N + 1) * 4), o_pco = take((N + 2) * 4);
   size_t o_pc = take((2 * N + 1) * 4);
   size_t o_pend = take((N + 1) * 4), o_q0 = take((N + 1) * 4), o_q1 = take((N + 1) * 4);
@@ -537,7 +539,10 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
     int lo = 0, hi = N;
     while (lo < hi) { const int mid = (lo + hi) >> 1; if ((int)sk[mid] < (int)k) lo = mid + 1; else hi = mid; }
     s.group_off[k] = lo;
-    if ((k & 1) == 0) s.level_off[k >> 1] = lo;
+    if ((k & 1) == 0) {
+      s.level_off[k >> 1] = lo;
+      if ((k >> 1) < kLoMirror) flags[F_NFLAGS + (k >> 1)] = lo;  // fetched with the flags
+    }
   }
   gsync(flags);
 
@@ -668,7 +673,7 @@ fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr
   // FOLD_SCHED_PER_BLOCK override the defaults for tuning experiments)
   static const int small_n = [] {
     const char *e = getenv("FOLD_SCHED_SMALLN");
-    const int v = e ? atoi(e) : kSmallN;
+    const int v = e ? atoi(e) : kOneBlockN;
     return v < 0 ? 0 : (v > kSmallN ? kSmallN : v);
   }();
   static const int per_block = [] {
@@ -687,20 +692,26 @@ fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr
     FOLD_CUDA_TRY(cudaFuncSetAttribute(k_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)launch_smem));
     smem_set = launch_smem;
   }
-  FOLD_CUDA_TRY(cudaMemsetAsync(w.flags + F_BAR, 0, 2 * sizeof(int32_t), st));
   SchedArgs args{N, G, V, gr->op, gr->child, gr->token, gr->root, gr->level, *s, w};
-  void *kargs[] = {(void *)&args};
-  FOLD_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_schedule, dim3(blocks), dim3(kSchedThreads), kargs,
-                                            launch_smem, st));
+  if (blocks == 1) {  // no grid barrier: a plain launch (cheaper than a cooperative one)
+    k_schedule<<<1, kSchedThreads, launch_smem, st>>>(args);
+  } else {
+    FOLD_CUDA_TRY(cudaMemsetAsync(w.flags + F_BAR, 0, 2 * sizeof(int32_t), st));
+    void *kargs[] = {(void *)&args};
+    FOLD_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_schedule, dim3(blocks), dim3(kSchedThreads), kargs,
+                                              launch_smem, st));
+  }
   FOLD_LAUNCH_CHECK();
 
-  // ---- the one host sync: flags + level_off prefix
-  int32_t hflags[F_NFLAGS];
-  const int kPrefix = 4096;
-  int npre = (N + 2) < kPrefix ? (N + 2) : kPrefix;
-  FOLD_CUDA_TRY(cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
-  FOLD_CUDA_TRY(cudaMemcpyAsync(s->level_off_host, s->level_off, (size_t)npre * 4, cudaMemcpyDeviceToHost, st));
+  // ---- the one host sync: flags + the level_off prefix mirrored after them, one copy into
+  // a pinned staging buffer
+  static thread_local int32_t *hbuf = nullptr;
+  if (!hbuf) FOLD_CUDA_TRY(cudaMallocHost((void **)&hbuf, (F_NFLAGS + kLoMirror) * sizeof(int32_t)));
+  const int npre = (N + 2) < kLoMirror ? (N + 2) : kLoMirror;
+  FOLD_CUDA_TRY(cudaMemcpyAsync(hbuf, w.flags, (size_t)(F_NFLAGS + npre) * 4, cudaMemcpyDeviceToHost, st));
   FOLD_CUDA_TRY(cudaStreamSynchronize(st));
+  const int32_t *hflags = hbuf;
+  memcpy(s->level_off_host, hbuf + F_NFLAGS, (size_t)npre * 4);
   for (int e = 0; e < E_NCLASS; e++) {
     if (hflags[F_ERR0 + e] != INT_MAX) {
       g_last_detail = hflags[F_ERR0 + e];
