@@ -220,11 +220,16 @@ def run_fold(args):
     fold.profile_enable(True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    # per-step boundaries (median and p10/p90 of the steps)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0.record()
-    for _ in range(args.steps):
+    marks[0].record()
+    for i in range(args.steps):
         step(op, child, token, root, g_dev)
+        marks[i + 1].record()
     e1.record()
     torch.cuda.synchronize()
+    step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
     launches = fold.launch_count()
     prof = fold.profile_read()
     fold.profile_enable(False)
@@ -383,7 +388,13 @@ def run_fold(args):
                        (N_nodes * S * 6 + n_cells * gates * S * 4 + n_cells * S * 16) / 1e9),
                    "parallelism": f"dp{world}"},
         "gpu_launches": int(launches),
+        "step_ms": {"median": float(np.median(step_ms)), "p10": float(np.percentile(step_ms, 10)),
+                    "p90": float(np.percentile(step_ms, 90)), "rank0": [round(x, 4) for x in step_ms]},
         "kernels": per_class,
+        "us_per_level": {  # the latency-bound view (n_levels - 1 cell levels)
+            "fwd": 1e3 * sum(per_class.get(k, {}).get("ms_per_step", 0.0) for k in ("cell_fwd",)) / max(n_levels - 1, 1),
+            "bwd": 1e3 * sum(per_class.get(k, {}).get("ms_per_step", 0.0) for k in ("gemm_dA", "bwd_pointwise"))
+                   / max(n_levels - 1, 1)},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,

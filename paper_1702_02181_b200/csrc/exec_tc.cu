@@ -1398,6 +1398,7 @@ constexpr int NB_THREADS = 256;   // warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 
 template <int GATES>
 __global__ void __launch_bounds__(NB_THREADS, 1)
     k_bwd_narrow(const __grid_constant__ CUtensorMap tmU3, const __grid_constant__ CUtensorMap tmZ4,
+                 const __grid_constant__ CUtensorMap tmU2, const __grid_constant__ CUtensorMap tmZ2, int packed,
                  const int32_t *__restrict__ lo, int D, int d1, int S, int nl, int Kp,
                  const int32_t *__restrict__ gather, const __nv_bfloat16 *__restrict__ Gact, int ld_g,
                  const float *__restrict__ C, int ld, float *dA, float *dCe, __nv_bfloat16 *dZ, int ld_z, int *rt_cnt,
@@ -1457,7 +1458,16 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       ptx::mbar_arrive_expect_tx(&u_full, (uint32_t)(NSLOT * USLOT));
-      for (int q = 0; q < NSLOT; q++) ptx::tma_load_3d(&tmU3, &u_full, Usm + q * USLOT, q * BK, col0, 0);
+      // packed (GATES*S = 8 Kp): one 3D box per K-block slot; otherwise one 2D box per
+      // (part, K-block) whose K columns past GATES*S are zero-filled by the TMA bounds
+      for (int q = 0; q < NSLOT; q++) {
+        if (packed) {
+          ptx::tma_load_3d(&tmU3, &u_full, Usm + q * USLOT, q * BK, col0, 0);
+        } else {
+          for (int p = 0; p < NB_PARTS; p++)
+            ptx::tma_load_2d(&tmU2, &u_full, Usm + q * USLOT + p * 16 * 128, p * Kp + q * BK, col0);
+        }
+      }
       Cur cu;
       int i = 0;
       for (bool ok = cu.init(lo, D, d1); ok; ok = cu.next(lo, d1), i++) {
@@ -1467,7 +1477,13 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
         ptx::wait_counter(rt_cnt + key, target);
         ptx::fence_proxy_async_global();
         ptx::mbar_arrive_expect_tx(&b_full, (uint32_t)(NSLOT * NB_PARTS * NB_ROWS * 128));
-        ptx::tma_load_4d(&tmZ4, &b_full, Bsm, 0, cu.r - nl, 0, 0);
+        if (packed) {
+          ptx::tma_load_4d(&tmZ4, &b_full, Bsm, 0, cu.r - nl, 0, 0);
+        } else {
+          for (int q = 0; q < NSLOT; q++)
+            for (int p = 0; p < NB_PARTS; p++)
+              ptx::tma_load_2d(&tmZ2, &b_full, Bsm + (q * NB_PARTS + p) * NB_ROWS * 128, p * Kp + q * BK, cu.r - nl);
+        }
       }
     }
   } else if (warp == 1) {
@@ -2040,7 +2056,7 @@ fold_status tc_prepare_U(int gates, int S, const float *U, __nv_bfloat16 *Ub, cu
 // Ut[r][k] = U[k][half * S + j] in bf16 for the padded column r = half * Sp + j (0 for
 // j >= S): the narrow backward's K-major copy of U's columns. 32 x 32 tiles through shared
 // memory (coalesced reads of U rows and writes of Ut rows).
-__global__ void k_prep_Ut(int K, int S, int Sp, const float *__restrict__ U, __nv_bfloat16 *__restrict__ Ut) {
+__global__ void k_prep_Ut(int K, int Kt, int S, int Sp, const float *__restrict__ U, __nv_bfloat16 *__restrict__ Ut) {
   __shared__ float tile[32][33];
   const int R = 2 * Sp;
   const int ntk = (K + 31) / 32, ntr = (R + 31) / 32;
@@ -2054,7 +2070,7 @@ __global__ void k_prep_Ut(int K, int S, int Sp, const float *__restrict__ U, __n
     __syncthreads();
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {  // rows r0 + i of Ut, columns k0 + tx
       const int r = r0 + i, k = k0 + threadIdx.x;
-      if (r < R && k < K) Ut[(int64_t)r * K + k] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+      if (r < R && k < K) Ut[(int64_t)r * Kt + k] = __float2bfloat16_rn(tile[threadIdx.x][i]);
     }
     __syncthreads();
   }
@@ -2065,11 +2081,11 @@ fold_status tc_prepare_Ut(int gates, int S, const float *U, __nv_bfloat16 *Ut, c
   const int Sp = (int)round_up(S, BK), K = gates * S;
   int64_t tiles = cdiv(K, 32) * cdiv(2 * Sp, 32);
   unsigned grid = (unsigned)(tiles < 148 * 16 ? tiles : 148 * 16);
-  k_prep_Ut<<<grid, dim3(32, 8), 0, st>>>(K, S, Sp, U, Ut);
+  k_prep_Ut<<<grid, dim3(32, 8), 0, st>>>(K, (int)round_up(K, 8), S, Sp, U, Ut);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
-size_t tc_ut_bytes(int gates, int S) { return round_up((size_t)2 * round_up(S, BK) * gates * S * 2, 256); }
+size_t tc_ut_bytes(int gates, int S) { return round_up((size_t)2 * round_up(S, BK) * round_up(gates * S, 8) * 2, 256); }
 
 fold_status tc_fwd_levels(int cell, const TcFwdArgs &a, cudaStream_t st) {
   if (a.D < 2) return FOLD_OK;
@@ -2117,7 +2133,7 @@ int bwd_narrow_start(const int32_t *lo, int D, int S, int gates) {
     const char *e = getenv("FOLD_BWD_NARROW_MAX");
     return e ? atoi(e) : 32;
   }();
-  if (narrow_max <= 0 || S > 1024 || (gates * S) % (NB_PARTS * BK) != 0) return D + 1;
+  if (narrow_max <= 0 || S > 1024) return D + 1;
   int d1 = D + 1;
   while (d1 - 1 >= 2 && lo[d1] - lo[d1 - 1] <= narrow_max) d1--;
   return d1;
@@ -2141,12 +2157,22 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
   // k_bwd_narrow, the wide kernel takes levels d1-1..2
   const int d1 = bwd_narrow_start(a.level_off_host, a.D, S, gates);
   if (d1 <= a.D) {
-    const int Kp = gates * S / NB_PARTS;
+    const int Kp = (int)round_up(cdiv(gates * S, NB_PARTS), BK);
+    int packed = (gates * S) % (NB_PARTS * BK) == 0;
     const int nsm = (Kp / BK) * (NB_PARTS * 16 * 128) + (Kp / BK) * NB_PARTS * NB_ROWS * 128 + 1024;
     auto enc = encode_fn();
     if (!enc) return FOLD_E_CUDA;
     FOLD_TRY(tc_prepare_Ut(gates, S, a.U, a.Ut, st));
-    CUtensorMap tmU3, tmZ4;
+    CUtensorMap tmU3, tmZ4, tmU2, tmZ2;
+    // per-(part, K-block) 2D boxes for S where GATES*S is not 8 K-blocks' multiple (K past
+    // GATES*S out of bounds = zero)
+    const int Kt = (int)round_up(gates * S, 8);  // Ut row stride (16-byte aligned rows)
+    FOLD_TRY(make_map(&tmU2, a.Ut, (uint64_t)gates * S, (uint64_t)ld_u, (uint64_t)Kt * 2, BK, 16));
+    FOLD_TRY(make_map(&tmZ2, a.dZ, (uint64_t)gates * S, (uint64_t)a.n_cells, (uint64_t)a.ld_z * 2, BK, NB_ROWS));
+    if (!packed) {
+      tmU3 = tmU2;  // (unused)
+      tmZ4 = tmZ2;
+    } else {
     {  // Ut [2 Sp][GATES*S] viewed as [part][row][K in part]: box 64 K x 16 rows x 8 parts
       const int K = gates * S;
       cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)ld_u, (cuuint64_t)NB_PARTS};
@@ -2168,6 +2194,7 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return FOLD_E_CUDA;
     }
+    }
     auto nk = gates == 5 ? k_bwd_narrow<5> : k_bwd_narrow<1>;
     FOLD_TRY(set_smem(nk, nsm));
     const int grid = ld_u / 16;
@@ -2179,7 +2206,7 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
     float *dA = a.dA, *dCe = a.dCe;
     __nv_bfloat16 *dZ = a.dZ;
     int *rt = a.rt_cnt;
-    void *args[] = {(void *)&tmU3, (void *)&tmZ4, (void *)&lo, (void *)&D, (void *)&d1v, (void *)&Sv, (void *)&nl,
+    void *args[] = {(void *)&tmU3, (void *)&tmZ4, (void *)&tmU2, (void *)&tmZ2, (void *)&packed, (void *)&lo, (void *)&D, (void *)&d1v, (void *)&Sv, (void *)&nl,
                     (void *)&Kpv, (void *)&gather, (void *)&G, (void *)&ld_g, (void *)&C, (void *)&ld, (void *)&dA,
                     (void *)&dCe, (void *)&dZ, (void *)&ld_z, (void *)&rt, (void *)&ts};
     FOLD_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)nk, dim3(grid), dim3(NB_THREADS), args, (size_t)nsm, st));

@@ -38,3 +38,7 @@ gr = foldgen.table1_batch(3, False, leaves=40, vocab=64)
 print("S512 random B=3 dyn", run(gr, None, 512))
 gr = foldgen.config_c4(1)
 print("C4 B=1", run(gr, None, 1024))
+gr = foldgen.config_c3(64)
+print("C3 B=64 S=300", run(gr, None, 300))
+print("C3 B=64 S=300 manual", run(gr, foldgen.manual_levels(gr), 300))
+print("C3 B=64 S=300 rnn", run(gr, None, 300, cell="treernn"))
