@@ -386,6 +386,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
     // its pushes / staging writes, sums its rows' credits (h columns pushed) per consumer
     // tile into credit_list and arrives on epi_done; the store warp issues the bulk stores,
     // waits for them, fences (cumulative over the mbarrier hand-off) and adds the credits.
+    // Latency-bound levels (at most 2 tiles per CTA pair): each epilogue warp publishes its
+    // own rows right after its stores (fence + one atomic per distinct consumer tile), so
+    // the dependency does not wait for the store warp's G bulk store; consumers need only h
+    // (pushed) and c (stored directly). Wide levels keep the hand-off below (one fence per
+    // tile in the store warp, the epilogue warps never block on a fence).
+    auto publish = [&](int ce0, int ce1, int e0, int cols) {
+      __syncwarp();
+      __threadfence();
+      for (int k = 0;; k++) {
+        const int e = ce0 + k;
+        const bool act = e < ce1 && cols > 0;
+        if (!__any_sync(0xffffffffu, act)) break;
+        const int ts = act ? __ldg(tstart + ((k == 0 ? e0 : __ldg(sc.cons_edge + e)) >> 1)) : -1;
+        unsigned todo = __ballot_sync(0xffffffffu, act);
+        while (todo) {
+          const int src = __ffs(todo) - 1;
+          const int key = __shfl_sync(0xffffffffu, ts, src);
+          const bool mine = act && ts == key;
+          const int sum = (int)__reduce_add_sync(0xffffffffu, mine ? (unsigned)cols : 0u);
+          todo &= ~__ballot_sync(0xffffffffu, mine);
+          if (lane == src) atomicAdd(rt_cnt + key, sum);
+        }
+      }
+    };
     auto warp_credits = [&](int par, int ce0, int ce1, int e0, int cols) {
       const int ew = warp - 4;
       int n = 0;
@@ -582,10 +606,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
       int cols = 0;
       if (valid)
         for (int jc = grp; jc < chunks; jc += 2) cols += max(0, min(8, S - (j0 + jc * 8)));
-      warp_credits(tc & 1, ce0, ce1, m.e0, cols);
-      __syncwarp();
+      if (cur.nt <= 2 * npairs) {  // latency-bound level: publish here
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&epi_done);
+        publish(ce0, ce1, m.e0, cols);
+      } else {
+        warp_credits(tc & 1, ce0, ce1, m.e0, cols);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&epi_done);
+      }
       if (warp == 4 && lane == 0 && rank == 0) trace(dbg, 6, T);
-      if (lane == 0) ptx::mbar_arrive(&epi_done);
     }
   } else if (warp == 3) {
     // Store warp: bulk stores of the staged G / C tiles, then the tile's publication.
@@ -610,8 +640,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         if (rank == 0) trace(dbg, 7, T);
         ptx::mbar_arrive(&stg_free);
         // (the staged G rows are read only by the backward, after this kernel; the C rows
-        // the consumers read were stored by the epilogue threads, ordered by the fence below)
+        // the consumers read were stored by the epilogue threads, ordered by the fence below
+        // or by the epilogue warps' own fences on latency-bound levels)
         if (rank == 0) trace(dbg, 8, T);
+        if (cur.nt <= 2 * npairs) {  // the epilogue warps published this tile themselves
+          if (rank == 0) trace(dbg, 4, T);
+          continue;
+        }
         __threadfence();
         const int par = tc & 1;
         for (int w = 0; w < Cfg::EPI_WARPS; w++) {

@@ -12,6 +12,7 @@ ap.add_argument("--levels", type=int, default=16)
 a = ap.parse_args()
 assert os.environ.get("FOLD_DBG_FWD") == "1"
 gr = foldgen.make_config(a.config, a.batch)
+print("nodes", gr.n_nodes)
 S = foldgen.CONFIG_STATE[a.config]
 p = foldgen.make_params("treelstm", S, gr.vocab)
 dev = "cuda"
