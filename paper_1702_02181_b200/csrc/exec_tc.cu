@@ -1418,22 +1418,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
 // owns 16 dA columns [16x, 16x + 16) of the padded [h_L | h_R] layout and holds U[:, those
 // columns] (all GATES*S rows) in shared memory, read from the transposed bf16 copy Ut
 // [2 Sp][GATES*S] (K-major A operand). The K = GATES*S reduction is cut into 8 parts of Kp
-// rows stacked in M (M row 16 p + c = column c over part p; one 3D TMA box per K-block
-// fetches all 8 parts' 16 rows), and the chunk's <= 4 dZ rows are stacked
-// the same way in N (N row 4 p + n = row n's dZ over part p), so one M = 128, N = 32 MMA
-// advances all 8 parts: dA[n][c] = sum_p D[16 p + c][4 p + n], Kp/16 MMAs per chunk. The
+// rows stacked in M (M row 16 p + c = column c over part p), and a chunk's R dZ rows are
+// stacked the same way in N (N row R p + n = row n's dZ over part p; R = 4 for levels of at
+// most 4 rows, else 16), so one M = 128, N = 8R MMA advances all 8 parts:
+// dA[n][c] = sum_p D[16 p + c][R p + n], Kp/16 MMAs per chunk (an SS-mode MMA costs about
+// its operand bytes, so 16 rows cost ~1.6x 4 rows). The chunk's dZ streams through a ring
+// of 3 x 16 KB stages (one K-block of all parts per stage for R = 16, four for R = 4). The
 // epilogue sums the parts and runs the child's pointwise step for its 16 columns (the same
 // arithmetic as k_bwd_levels' epilogue), then credits the child's row tile with the columns
 // done, so the wide kernel (launched after it, on the remaining levels) sees the same
 // dependency counters.
-constexpr int NB_ROWS = 4;        // rows per chunk
-constexpr int NB_PARTS = 8;       // K parts stacked in M (16 columns each) and N (4 rows each)
+constexpr int NB_RMAX = 16;       // rows per chunk (levels of <= 4 rows use 4)
+constexpr int NB_PARTS = 8;       // K parts stacked in M (16 columns each) and N (R rows each)
 constexpr int NB_THREADS = 256;   // warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4-7 epilogue
+constexpr int NB_ST = 3;          // dZ ring stages
+constexpr int NB_STAGE = NB_PARTS * NB_RMAX * 128;  // 16 KB
 
 template <int GATES>
 __global__ void __launch_bounds__(NB_THREADS, 1)
-    k_bwd_narrow(const __grid_constant__ CUtensorMap tmU3, const __grid_constant__ CUtensorMap tmZ4,
-                 const __grid_constant__ CUtensorMap tmU2, const __grid_constant__ CUtensorMap tmZ2, int packed,
+    k_bwd_narrow(const __grid_constant__ CUtensorMap tmU3, const __grid_constant__ CUtensorMap tmZ4a,
+                 const __grid_constant__ CUtensorMap tmZ4b, const __grid_constant__ CUtensorMap tmU2,
+                 const __grid_constant__ CUtensorMap tmZ2a, const __grid_constant__ CUtensorMap tmZ2b, int packed,
                  const int32_t *__restrict__ lo, int D, int d1, int S, int nl, int Kp,
                  const int32_t *__restrict__ gather, const __nv_bfloat16 *__restrict__ Gact, int ld_g,
                  const float *__restrict__ C, int ld, float *dA, float *dCe, __nv_bfloat16 *dZ, int ld_z, int *rt_cnt,
@@ -1442,9 +1447,9 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
   uint8_t *smem = align1024(smem_raw);
   const int NSLOT = Kp / BK;              // K-blocks per part
   constexpr int USLOT = NB_PARTS * 16 * 128;   // bytes per K-block slot of the U slice (128 rows)
-  uint8_t *Usm = smem, *Bsm = smem + NSLOT * USLOT;  // U: [slot][part][16 rows]; B: [slot][part][4 rows]
-  __shared__ __align__(8) uint64_t u_full, b_full, b_empty, acc_full[2], acc_empty[2];
-  __shared__ float red[NB_PARTS][16][NB_ROWS + 1];
+  uint8_t *Usm = smem, *Bsm = smem + NSLOT * USLOT;  // U: [slot][part][16 rows]; B: ring of stages
+  __shared__ __align__(8) uint64_t u_full, full[NB_ST], empty[NB_ST], acc_full[2], acc_empty[2];
+  __shared__ float red[NB_PARTS][16][NB_RMAX + 1];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Sp = (int)round_up(S, BK);
@@ -1453,31 +1458,35 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
   if (ncols <= 0) return;  // padding columns only (uniform over the CTA)
   if (tid == 0) {
     ptx::mbar_init(&u_full, 1);
-    ptx::mbar_init(&b_full, 1);
-    ptx::mbar_init(&b_empty, 1);
+    for (int s2 = 0; s2 < NB_ST; s2++) { ptx::mbar_init(&full[s2], 1); ptx::mbar_init(&empty[s2], 1); }
     for (int a = 0; a < 2; a++) { ptx::mbar_init(&acc_full[a], 1); ptx::mbar_init(&acc_empty[a], 4); }
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tmU3);
-    ptx::prefetch_tmap(&tmZ4);
+    ptx::prefetch_tmap(&tmZ4a);
+    ptx::prefetch_tmap(&tmZ4b);
+    ptx::prefetch_tmap(&tmU2);
+    ptx::prefetch_tmap(&tmZ2a);
+    ptx::prefetch_tmap(&tmZ2b);
   }
-  if (warp == 2) { ptx::tmem_alloc(&tmem_base_sh, 64); ptx::tmem_relinquish(); }
+  if (warp == 2) { ptx::tmem_alloc(&tmem_base_sh, 256); ptx::tmem_relinquish(); }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = tmem_base_sh;
 
-  struct Cur {  // chunks of levels D, D-1, ..., d1
-    int d, r, r1;
+  struct Cur {  // chunks of levels D, D-1, ..., d1; R = rows per chunk of the level
+    int d, r, r1, R;
     __device__ bool load(const int32_t *lo, int d1) {
       for (;; d--) {
         if (d < d1) return false;
         r = __ldg(lo + d); r1 = __ldg(lo + d + 1);
+        R = r1 - r <= 4 ? 4 : NB_RMAX;
         if (r < r1) return true;
       }
     }
     __device__ bool init(const int32_t *lo, int D, int d1) { d = D; return load(lo, d1); }
     __device__ bool next(const int32_t *lo, int d1) {
-      r += NB_ROWS;
+      r += R;
       if (r < r1) return true;
       d--;
       return load(lo, d1);
@@ -1504,122 +1513,162 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
         }
       }
       Cur cu;
-      int i = 0;
-      for (bool ok = cu.init(lo, D, d1); ok; ok = cu.next(lo, d1), i++) {
-        if (i > 0) ptx::mbar_wait(&b_empty, (i - 1) & 1);
+      int it = 0;
+      for (bool ok = cu.init(lo, D, d1); ok; ok = cu.next(lo, d1)) {
         int key;
         const int target = tile_target(cu, key);
         ptx::wait_counter(rt_cnt + key, target);
         ptx::fence_proxy_async_global();
-        ptx::mbar_arrive_expect_tx(&b_full, (uint32_t)(NSLOT * NB_PARTS * NB_ROWS * 128));
-        if (packed) {
-          ptx::tma_load_4d(&tmZ4, &b_full, Bsm, 0, cu.r - nl, 0, 0);
-        } else {
-          for (int q = 0; q < NSLOT; q++)
-            for (int p = 0; p < NB_PARTS; p++)
-              ptx::tma_load_2d(&tmZ2, &b_full, Bsm + (q * NB_PARTS + p) * NB_ROWS * 128, p * Kp + q * BK, cu.r - nl);
+        const int slot_bytes = NB_PARTS * cu.R * 128, kps = NB_STAGE / slot_bytes;
+        const CUtensorMap *m4 = cu.R == 4 ? &tmZ4a : &tmZ4b, *m2 = cu.R == 4 ? &tmZ2a : &tmZ2b;
+        for (int q0 = 0; q0 < NSLOT; q0 += kps, it++) {
+          const int s2 = it % NB_ST;
+          ptx::mbar_wait(&empty[s2], ((it / NB_ST) & 1) ^ 1);
+          const int nk = min(kps, NSLOT - q0);
+          uint8_t *stg = Bsm + s2 * NB_STAGE;
+          if (packed) {  // one 4D box = kps K-blocks of all parts (K-blocks past the end zero-filled)
+            ptx::mbar_arrive_expect_tx(&full[s2], (uint32_t)(kps * slot_bytes));
+            ptx::tma_load_4d(m4, &full[s2], stg, 0, cu.r - nl, 0, q0);
+            continue;
+          }
+          ptx::mbar_arrive_expect_tx(&full[s2], (uint32_t)(nk * slot_bytes));
+          for (int j = 0; j < nk; j++) {
+            const int q = q0 + j;
+            {
+              for (int p = 0; p < NB_PARTS; p++)
+                ptx::tma_load_2d(m2, &full[s2], stg + j * slot_bytes + p * cu.R * 128, p * Kp + q * BK, cu.r - nl);
+            }
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = ptx::idesc_bf16(128, NB_PARTS * NB_ROWS, 0, 0);
       ptx::mbar_wait(&u_full, 0);
       Cur cu;
-      int i = 0;
+      int i = 0, it = 0;
       for (bool ok = cu.init(lo, D, d1); ok; ok = cu.next(lo, d1), i++) {
         const int acc = i & 1;
+        const uint32_t idesc = ptx::idesc_bf16(128, NB_PARTS * cu.R, 0, 0);
+        const int slot_bytes = NB_PARTS * cu.R * 128, kps = NB_STAGE / slot_bytes;
         ptx::mbar_wait(&acc_empty[acc], ((i >> 1) & 1) ^ 1);
-        ptx::mbar_wait(&b_full, i & 1);
         ptx::tc_fence_after();
-        const uint32_t dst = tbase + acc * NB_PARTS * NB_ROWS;
+        const uint32_t dst = tbase + acc * NB_PARTS * NB_RMAX;
         const uint32_t u0 = ptx::smem_u32(Usm), b0 = ptx::smem_u32(Bsm);
-        for (int q = 0; q < NSLOT; q++) {
+        for (int q0 = 0; q0 < NSLOT; q0 += kps, it++) {
+          const int s2 = it % NB_ST;
+          ptx::mbar_wait(&full[s2], (it / NB_ST) & 1);
+          ptx::tc_fence_after();
+          const int nk = min(kps, NSLOT - q0);
+          for (int j = 0; j < nk; j++) {
+            const int q = q0 + j;
 #pragma unroll
-          for (int k = 0; k < BK / 16; k++)
-            ptx::umma_bf16(dst, ptx::sdesc_sw128(u0 + q * USLOT + 32 * k, 16, 1024),
-                           ptx::sdesc_sw128(b0 + q * (NB_PARTS * NB_ROWS * 128) + 32 * k, 16, 1024), idesc,
-                           (q | k) != 0);
+            for (int k = 0; k < BK / 16; k++)
+              ptx::umma_bf16(dst, ptx::sdesc_sw128(u0 + q * USLOT + 32 * k, 16, 1024),
+                             ptx::sdesc_sw128(b0 + s2 * NB_STAGE + j * slot_bytes + 32 * k, 16, 1024), idesc,
+                             (q | k) != 0);
+          }
+          ptx::umma_commit(&empty[s2]);
         }
-        ptx::umma_commit(&b_empty);
         ptx::umma_commit(&acc_full[acc]);
       }
     }
   } else if (warp >= 4) {
-    const int t = tid - 128;           // 0..127 (the pointwise uses 0..63)
+    const int t = tid - 128;           // 0..127
     const int qw = warp & 3;           // TMEM lane quarter = M rows 32 qw .. 32 qw + 31
-    const int n = t >> 4, c = t & 15;  // this thread's (row in chunk, column) in the pointwise
+    const int c = t & 15, nb = t >> 4; // this thread's column; rows nb and nb + 8 of the chunk
     const int j = j0 + c;
     Cur cu;
     int i = 0;
     for (bool ok = cu.init(lo, D, d1); ok; ok = cu.next(lo, d1), i++) {
       const int acc = i & 1;
-      const int rows = min(NB_ROWS, cu.r1 - cu.r);
-      const int64_t r = cu.r + n;
-      const bool act = t < 64 && n < rows && c < ncols;
-      // operands of the child's pointwise step (G / C from the forward; dCe of the edge was
-      // written by this row's own pointwise step, published with its dZ)
-      int64_t x = -1, xl = -1, xr = -1;
-      float gg[GATES], cc = 0.f, cl = 0.f, cr = 0.f, dc = 0.f;
-      const int64_t e = 2 * (r - nl) + half;
-      if (act) {
-        x = __ldg(gather + 2 * r + half);
-        if (x >= nl) {
-          const int64_t xc = x - nl;
+      const int R = cu.R;
+      const int rows = min(R, cu.r1 - cu.r);
+      // operands of the children's pointwise steps (G / C from the forward; dCe of each edge
+      // was written by its row's own pointwise step, published with its dZ)
+      int64_t x[2] = {-1, -1};
+      float gg[2][GATES], cc[2] = {0.f, 0.f}, cl[2] = {0.f, 0.f}, cr[2] = {0.f, 0.f}, dc[2] = {0.f, 0.f};
+      bool waited = false;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int n = nb + 8 * h;
+        if (n >= rows || c >= ncols) continue;
+        const int64_t r = cu.r + n;
+        const int64_t xx = __ldg(gather + 2 * r + half);
+        x[h] = xx;
+        if (xx >= nl) {
+          const int64_t xc = xx - nl;
           const __nv_bfloat16 *gx = Gact + xc * ld_g + j;
 #pragma unroll
-          for (int g = 0; g < GATES; g++) gg[g] = __bfloat162float(gx[g * ld]);
+          for (int g = 0; g < GATES; g++) gg[h][g] = __bfloat162float(gx[g * ld]);
           if constexpr (GATES == 5) {
-            xl = __ldg(gather + 2 * x);
-            xr = __ldg(gather + 2 * x + 1);
-            cc = __ldcg(C + x * ld + j);
-            if (xl >= nl) cl = __ldcg(C + xl * ld + j);
-            if (xr >= nl) cr = __ldcg(C + xr * ld + j);
-            int key;
-            const int target = tile_target(cu, key);
-            ptx::wait_counter(rt_cnt + key, target);
-            dc = __ldcg(dCe + e * S + j);
+            const int64_t xl = __ldg(gather + 2 * xx), xr = __ldg(gather + 2 * xx + 1);
+            cc[h] = __ldcg(C + xx * ld + j);
+            if (xl >= nl) cl[h] = __ldcg(C + xl * ld + j);
+            if (xr >= nl) cr[h] = __ldcg(C + xr * ld + j);
+            if (!waited) {
+              int key;
+              const int target = tile_target(cu, key);
+              ptx::wait_counter(rt_cnt + key, target);
+              waited = true;
+            }
+            dc[h] = __ldcg(dCe + (2 * (r - nl) + half) * S + j);
           }
         }
       }
       ptx::mbar_wait(&acc_full[acc], (i >> 1) & 1);
       ptx::tc_fence_after();
-      float z[8];
-      ptx::tmem_ld8(tbase + acc * NB_PARTS * NB_ROWS + qw * 8 + ((uint32_t)(qw * 32) << 16), z);
-      ptx::tmem_ld_wait();
-      {  // M row 32 qw + lane = (part 2 qw + lane / 16, column lane % 16); its rows are
-         // D columns 4 part .. 4 part + 3 = this warp's columns 8 qw + 4 (lane / 16) ..
+      {  // M row 32 qw + lane = (part p = 2 qw + lane / 16, column lane % 16); its rows are the
+         // D columns R p .. R p + R - 1
         const int hi = lane >> 4, p = 2 * qw + hi;
+        const uint32_t ta = tbase + acc * NB_PARTS * NB_RMAX + ((uint32_t)(qw * 32) << 16);
+        if (R == 4) {
+          float z[8];
+          ptx::tmem_ld8(ta + qw * 8, z);
+          ptx::tmem_ld_wait();
 #pragma unroll
-        for (int k = 0; k < NB_ROWS; k++) red[p][lane & 15][k] = hi ? z[4 + k] : z[k];
+          for (int k = 0; k < 4; k++) red[p][lane & 15][k] = hi ? z[4 + k] : z[k];
+        } else {
+          float z[32];
+#pragma unroll
+          for (int b = 0; b < 4; b++) ptx::tmem_ld8(ta + qw * 32 + b * 8, *reinterpret_cast<float(*)[8]>(z + 8 * b));
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int k = 0; k < 16; k++) red[p][lane & 15][k] = hi ? z[16 + k] : z[k];
+        }
       }
       ptx::tc_fence_before();
       ptx::named_bar_sync(1, 128);
       if (lane == 0) ptx::mbar_arrive(&acc_empty[acc]);
-      if (act) {
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int n = nb + 8 * h;
+        if (n >= rows || c >= ncols) continue;
         float dh = 0.f;
 #pragma unroll
         for (int p = 0; p < NB_PARTS; p++) dh += red[p][c][n];
-        if (x < nl) {
+        const int64_t r = cu.r + n;
+        const int64_t e = 2 * (r - nl) + half;
+        if (x[h] < nl) {
           dA[e * S + j] = dh;  // leaf child: the embedding gradient reads dA
+          continue;
+        }
+        const int64_t xc = x[h] - nl;
+        __nv_bfloat16 *dz = dZ + xc * ld_z + j;
+        if constexpr (GATES == 1) {
+          dz[0] = __float2bfloat16_rn(dh * (1.f - gg[h][0] * gg[h][0]));
         } else {
-          const int64_t xc = x - nl;
-          __nv_bfloat16 *dz = dZ + xc * ld_z + j;
-          if constexpr (GATES == 1) {
-            dz[0] = __float2bfloat16_rn(dh * (1.f - gg[0] * gg[0]));
-          } else {
-            const float ig = gg[0], fl = gg[1], fr = gg[2], og = gg[3], ug = gg[4];
-            const float tcv = tanhf(cc);
-            const float dO = dh * tcv;
-            const float dcc = dc + dh * og * (1.f - tcv * tcv);
-            dz[0] = __float2bfloat16_rn(dcc * ug * ig * (1.f - ig));
-            dz[S] = __float2bfloat16_rn(dcc * cl * fl * (1.f - fl));
-            dz[2 * S] = __float2bfloat16_rn(dcc * cr * fr * (1.f - fr));
-            dz[3 * S] = __float2bfloat16_rn(dO * og * (1.f - og));
-            dz[4 * S] = __float2bfloat16_rn(dcc * ig * (1.f - ug * ug));
-            dCe[(2 * xc) * S + j] = dcc * fl;
-            dCe[(2 * xc + 1) * S + j] = dcc * fr;
-          }
+          const float ig = gg[h][0], fl = gg[h][1], fr = gg[h][2], og = gg[h][3], ug = gg[h][4];
+          const float tcv = tanhf(cc[h]);
+          const float dO = dh * tcv;
+          const float dcc = dc[h] + dh * og * (1.f - tcv * tcv);
+          dz[0] = __float2bfloat16_rn(dcc * ug * ig * (1.f - ig));
+          dz[S] = __float2bfloat16_rn(dcc * cl[h] * fl * (1.f - fl));
+          dz[2 * S] = __float2bfloat16_rn(dcc * cr[h] * fr * (1.f - fr));
+          dz[3 * S] = __float2bfloat16_rn(dO * og * (1.f - og));
+          dz[4 * S] = __float2bfloat16_rn(dcc * ig * (1.f - ug * ug));
+          dCe[(2 * xc) * S + j] = dcc * fl;
+          dCe[(2 * xc + 1) * S + j] = dcc * fr;
         }
       }
       ptx::fence_proxy_async_global();
@@ -1637,7 +1686,7 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc(tbase, 64); }
+  if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc(tbase, 256); }
 }
 
 // Row-tile bookkeeping for k_bwd_levels: tstart[c] = first cell of c's 256-row tile (tiles
@@ -2161,12 +2210,12 @@ fold_status tc_bwd_prelude(const TcBwdArgs &a, const int32_t *cons_off, cudaStre
 }
 
 // First level (from the top) handled by the wide backward: levels d1..D all of at most
-// FOLD_BWD_NARROW_MAX rows (default 32; 0 disables) run in k_bwd_narrow, which needs
-// GATES*S/8 to be a multiple of 64 and S <= 1024 (the stationary U slice). D + 1 if none.
+// FOLD_BWD_NARROW_MAX rows (default 128; 0 disables) run in k_bwd_narrow, which needs
+// S <= 1024 (the stationary U slice). D + 1 if none.
 int bwd_narrow_start(const int32_t *lo, int D, int S, int gates) {
   static const int narrow_max = [] {
     const char *e = getenv("FOLD_BWD_NARROW_MAX");
-    return e ? atoi(e) : 32;
+    return e ? atoi(e) : 128;  // measured: 128 rows (16-row chunks) beat the wide tiles below it
   }();
   if (narrow_max <= 0 || S > 1024) return D + 1;
   int d1 = D + 1;
@@ -2194,41 +2243,43 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
   if (d1 <= a.D) {
     const int Kp = (int)round_up(cdiv(gates * S, NB_PARTS), BK);
     int packed = (gates * S) % (NB_PARTS * BK) == 0;
-    const int nsm = (Kp / BK) * (NB_PARTS * 16 * 128) + (Kp / BK) * NB_PARTS * NB_ROWS * 128 + 1024;
+    const int nsm = (Kp / BK) * (NB_PARTS * 16 * 128) + NB_ST * NB_STAGE + 1024;
     auto enc = encode_fn();
     if (!enc) return FOLD_E_CUDA;
     FOLD_TRY(tc_prepare_Ut(gates, S, a.U, a.Ut, st));
-    CUtensorMap tmU3, tmZ4, tmU2, tmZ2;
+    CUtensorMap tmU3, tmZ4a, tmZ4b, tmU2, tmZ2a, tmZ2b;
     // per-(part, K-block) 2D boxes for S where GATES*S is not 8 K-blocks' multiple (K past
     // GATES*S out of bounds = zero)
     const int Kt = (int)round_up(gates * S, 8);  // Ut row stride (16-byte aligned rows)
     FOLD_TRY(make_map(&tmU2, a.Ut, (uint64_t)gates * S, (uint64_t)ld_u, (uint64_t)Kt * 2, BK, 16));
-    FOLD_TRY(make_map(&tmZ2, a.dZ, (uint64_t)gates * S, (uint64_t)a.n_cells, (uint64_t)a.ld_z * 2, BK, NB_ROWS));
-    if (!packed) {
-      tmU3 = tmU2;  // (unused)
-      tmZ4 = tmZ2;
-    } else {
-    {  // Ut [2 Sp][GATES*S] viewed as [part][row][K in part]: box 64 K x 16 rows x 8 parts
-      const int K = gates * S;
-      cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)ld_u, (cuuint64_t)NB_PARTS};
-      cuuint64_t strides[2] = {(cuuint64_t)K * 2, (cuuint64_t)Kp * 2};
-      cuuint32_t box[3] = {(cuuint32_t)BK, 16, (cuuint32_t)NB_PARTS};
-      cuuint32_t es[3] = {1, 1, 1};
-      if (enc(&tmU3, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void *)a.Ut, dims, strides, box, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return FOLD_E_CUDA;
-    }
-    {  // dZ viewed as [K-block][part][row][64]: box = a chunk's rows x all parts x all K-blocks
-      cuuint64_t dims[4] = {(cuuint64_t)BK, (cuuint64_t)a.n_cells, (cuuint64_t)NB_PARTS, (cuuint64_t)(Kp / BK)};
-      cuuint64_t strides[3] = {(cuuint64_t)a.ld_z * 2, (cuuint64_t)Kp * 2, (cuuint64_t)BK * 2};
-      cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)NB_ROWS, (cuuint32_t)NB_PARTS, (cuuint32_t)(Kp / BK)};
-      cuuint32_t es[4] = {1, 1, 1, 1};
-      if (enc(&tmZ4, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void *)a.dZ, dims, strides, box, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return FOLD_E_CUDA;
-    }
+    FOLD_TRY(make_map(&tmZ2a, a.dZ, (uint64_t)gates * S, (uint64_t)a.n_cells, (uint64_t)a.ld_z * 2, BK, 4));
+    FOLD_TRY(make_map(&tmZ2b, a.dZ, (uint64_t)gates * S, (uint64_t)a.n_cells, (uint64_t)a.ld_z * 2, BK, NB_RMAX));
+    tmU3 = tmU2;  // (replaced below when packed)
+    tmZ4a = tmZ2a;
+    tmZ4b = tmZ2b;
+    if (packed) {
+      {  // Ut [2 Sp][GATES*S] viewed as [part][row][K in part]: box 64 K x 16 rows x 8 parts
+        const int K = gates * S;
+        cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)ld_u, (cuuint64_t)NB_PARTS};
+        cuuint64_t strides[2] = {(cuuint64_t)Kt * 2, (cuuint64_t)Kp * 2};
+        cuuint32_t box[3] = {(cuuint32_t)BK, 16, (cuuint32_t)NB_PARTS};
+        cuuint32_t es[3] = {1, 1, 1};
+        if (enc(&tmU3, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void *)a.Ut, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+          return FOLD_E_CUDA;
+      }
+      for (int v = 0; v < 2; v++) {  // dZ viewed as [K-block][part][row][64]: box = R rows x 8 parts x 1 K-block
+        const int R = v ? NB_RMAX : 4;
+        cuuint64_t dims[4] = {(cuuint64_t)BK, (cuuint64_t)a.n_cells, (cuuint64_t)NB_PARTS, (cuuint64_t)(Kp / BK)};
+        cuuint64_t strides[3] = {(cuuint64_t)a.ld_z * 2, (cuuint64_t)Kp * 2, (cuuint64_t)BK * 2};
+        cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)R, (cuuint32_t)NB_PARTS, (cuuint32_t)(NB_STAGE / (NB_PARTS * R * 128))};
+        cuuint32_t es[4] = {1, 1, 1, 1};
+        if (enc(v ? &tmZ4b : &tmZ4a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void *)a.dZ, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+          return FOLD_E_CUDA;
+      }
     }
     auto nk = gates == 5 ? k_bwd_narrow<5> : k_bwd_narrow<1>;
     FOLD_TRY(set_smem(nk, nsm));
@@ -2241,7 +2292,8 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
     float *dA = a.dA, *dCe = a.dCe;
     __nv_bfloat16 *dZ = a.dZ;
     int *rt = a.rt_cnt;
-    void *args[] = {(void *)&tmU3, (void *)&tmZ4, (void *)&tmU2, (void *)&tmZ2, (void *)&packed, (void *)&lo, (void *)&D, (void *)&d1v, (void *)&Sv, (void *)&nl,
+    void *args[] = {(void *)&tmU3, (void *)&tmZ4a, (void *)&tmZ4b, (void *)&tmU2, (void *)&tmZ2a, (void *)&tmZ2b,
+                    (void *)&packed, (void *)&lo, (void *)&D, (void *)&d1v, (void *)&Sv, (void *)&nl,
                     (void *)&Kpv, (void *)&gather, (void *)&G, (void *)&ld_g, (void *)&C, (void *)&ld, (void *)&dA,
                     (void *)&dCe, (void *)&dZ, (void *)&ld_z, (void *)&rt, (void *)&ts};
     FOLD_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)nk, dim3(grid), dim3(NB_THREADS), args, (size_t)nsm, st));
