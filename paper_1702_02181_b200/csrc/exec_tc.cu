@@ -1437,7 +1437,8 @@ constexpr int NB_STAGE = NB_PARTS * NB_RMAX * 128;  // 16 KB
 template <int GATES>
 __global__ void __launch_bounds__(NB_THREADS, 1)
     k_bwd_narrow(const __grid_constant__ CUtensorMap tmU3, const __grid_constant__ CUtensorMap tmZ4a,
-                 const __grid_constant__ CUtensorMap tmZ4b, const __grid_constant__ CUtensorMap tmU2,
+                 const __grid_constant__ CUtensorMap tmZ4b, const __grid_constant__ CUtensorMap tmZ4c,
+                 const __grid_constant__ CUtensorMap tmU2,
                  const __grid_constant__ CUtensorMap tmZ2a, const __grid_constant__ CUtensorMap tmZ2b, int packed,
                  const int32_t *__restrict__ lo, int D, int d1, int S, int nl, int Kp,
                  const int32_t *__restrict__ gather, const __nv_bfloat16 *__restrict__ Gact, int ld_g,
@@ -1464,6 +1465,7 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
     ptx::prefetch_tmap(&tmU3);
     ptx::prefetch_tmap(&tmZ4a);
     ptx::prefetch_tmap(&tmZ4b);
+    ptx::prefetch_tmap(&tmZ4c);
     ptx::prefetch_tmap(&tmU2);
     ptx::prefetch_tmap(&tmZ2a);
     ptx::prefetch_tmap(&tmZ2b);
@@ -1521,6 +1523,17 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
         ptx::fence_proxy_async_global();
         const int slot_bytes = NB_PARTS * cu.R * 128, kps = NB_STAGE / slot_bytes;
         const CUtensorMap *m4 = cu.R == 4 ? &tmZ4a : &tmZ4b, *m2 = cu.R == 4 ? &tmZ2a : &tmZ2b;
+        if (packed && cu.R == 4 && NSLOT * slot_bytes <= NB_ST * NB_STAGE) {
+          // few rows: the whole ring takes all K-blocks in ONE box (one round trip per chunk);
+          // every stage is used once so the per-stage phases stay uniform
+          for (int k = 0; k < NB_ST; k++) ptx::mbar_wait(&empty[(it + k) % NB_ST], (((it + k) / NB_ST) & 1) ^ 1);
+          const int s0 = it % NB_ST;
+          ptx::mbar_arrive_expect_tx(&full[s0], (uint32_t)(NSLOT * slot_bytes));
+          ptx::tma_load_4d(&tmZ4c, &full[s0], Bsm, 0, cu.r - nl, 0, 0);
+          for (int k = 1; k < NB_ST; k++) ptx::mbar_arrive(&full[(it + k) % NB_ST]);
+          it += NB_ST;
+          continue;
+        }
         for (int q0 = 0; q0 < NSLOT; q0 += kps, it++) {
           const int s2 = it % NB_ST;
           ptx::mbar_wait(&empty[s2], ((it / NB_ST) & 1) ^ 1);
@@ -1555,6 +1568,20 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
         ptx::tc_fence_after();
         const uint32_t dst = tbase + acc * NB_PARTS * NB_RMAX;
         const uint32_t u0 = ptx::smem_u32(Usm), b0 = ptx::smem_u32(Bsm);
+        if (packed && cu.R == 4 && NSLOT * slot_bytes <= NB_ST * NB_STAGE) {  // one box in the whole ring
+          for (int k = 0; k < NB_ST; k++) ptx::mbar_wait(&full[(it + k) % NB_ST], ((it + k) / NB_ST) & 1);
+          ptx::tc_fence_after();
+          for (int q = 0; q < NSLOT; q++) {
+#pragma unroll
+            for (int k = 0; k < BK / 16; k++)
+              ptx::umma_bf16(dst, ptx::sdesc_sw128(u0 + q * USLOT + 32 * k, 16, 1024),
+                             ptx::sdesc_sw128(b0 + q * slot_bytes + 32 * k, 16, 1024), idesc, (q | k) != 0);
+          }
+          for (int k = 0; k < NB_ST; k++) ptx::umma_commit(&empty[(it + k) % NB_ST]);
+          it += NB_ST;
+          ptx::umma_commit(&acc_full[acc]);
+          continue;
+        }
         for (int q0 = 0; q0 < NSLOT; q0 += kps, it++) {
           const int s2 = it % NB_ST;
           ptx::mbar_wait(&full[s2], (it / NB_ST) & 1);
@@ -2247,7 +2274,7 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
     auto enc = encode_fn();
     if (!enc) return FOLD_E_CUDA;
     FOLD_TRY(tc_prepare_Ut(gates, S, a.U, a.Ut, st));
-    CUtensorMap tmU3, tmZ4a, tmZ4b, tmU2, tmZ2a, tmZ2b;
+    CUtensorMap tmU3, tmZ4a, tmZ4b, tmZ4c, tmU2, tmZ2a, tmZ2b;
     // per-(part, K-block) 2D boxes for S where GATES*S is not 8 K-blocks' multiple (K past
     // GATES*S out of bounds = zero)
     const int Kt = (int)round_up(gates * S, 8);  // Ut row stride (16-byte aligned rows)
@@ -2257,6 +2284,7 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
     tmU3 = tmU2;  // (replaced below when packed)
     tmZ4a = tmZ2a;
     tmZ4b = tmZ2b;
+    tmZ4c = tmZ2a;
     if (packed) {
       {  // Ut [2 Sp][GATES*S] viewed as [part][row][K in part]: box 64 K x 16 rows x 8 parts
         const int K = gates * S;
@@ -2269,13 +2297,15 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
           return FOLD_E_CUDA;
       }
-      for (int v = 0; v < 2; v++) {  // dZ viewed as [K-block][part][row][64]: box = R rows x 8 parts x 1 K-block
-        const int R = v ? NB_RMAX : 4;
+      for (int v = 0; v < 3; v++) {  // dZ viewed as [K-block][part][row][64]: box = R rows x 8 parts x K-blocks
+        const int R = v == 1 ? NB_RMAX : 4;
+        const int nslot_box = v == 2 ? Kp / BK : NB_STAGE / (NB_PARTS * R * 128);
+        if (v == 2 && (nslot_box > 256 || nslot_box * NB_PARTS * 4 * 128 > NB_ST * NB_STAGE)) { tmZ4c = tmZ4a; continue; }
         cuuint64_t dims[4] = {(cuuint64_t)BK, (cuuint64_t)a.n_cells, (cuuint64_t)NB_PARTS, (cuuint64_t)(Kp / BK)};
         cuuint64_t strides[3] = {(cuuint64_t)a.ld_z * 2, (cuuint64_t)Kp * 2, (cuuint64_t)BK * 2};
-        cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)R, (cuuint32_t)NB_PARTS, (cuuint32_t)(NB_STAGE / (NB_PARTS * R * 128))};
+        cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)R, (cuuint32_t)NB_PARTS, (cuuint32_t)nslot_box};
         cuuint32_t es[4] = {1, 1, 1, 1};
-        if (enc(v ? &tmZ4b : &tmZ4a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void *)a.dZ, dims, strides, box, es,
+        if (enc(v == 2 ? &tmZ4c : v ? &tmZ4b : &tmZ4a, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void *)a.dZ, dims, strides, box, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
           return FOLD_E_CUDA;
@@ -2292,7 +2322,7 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
     float *dA = a.dA, *dCe = a.dCe;
     __nv_bfloat16 *dZ = a.dZ;
     int *rt = a.rt_cnt;
-    void *args[] = {(void *)&tmU3, (void *)&tmZ4a, (void *)&tmZ4b, (void *)&tmU2, (void *)&tmZ2a, (void *)&tmZ2b,
+    void *args[] = {(void *)&tmU3, (void *)&tmZ4a, (void *)&tmZ4b, (void *)&tmZ4c, (void *)&tmU2, (void *)&tmZ2a, (void *)&tmZ2b,
                     (void *)&packed, (void *)&lo, (void *)&D, (void *)&d1v, (void *)&Sv, (void *)&nl,
                     (void *)&Kpv, (void *)&gather, (void *)&G, (void *)&ld_g, (void *)&C, (void *)&ld, (void *)&dA,
                     (void *)&dCe, (void *)&dZ, (void *)&ld_z, (void *)&rt, (void *)&ts};
