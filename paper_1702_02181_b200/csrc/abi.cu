@@ -306,22 +306,17 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
   // The embedding gradient and db only need dA / dZ, the weight-gradient GEMM only dZ and
   // the A planes: run the two memory-bound reductions on an auxiliary stream beside the
   // tensor-bound dU GEMM, then join.
-  AuxStream &ax = aux_stream();
+  // FOLD_AUX_ORDER (experiments): 0 = reductions on the aux stream launched before the
+  // GEMM (default), 1 = after it, 2 = everything serial on the caller's stream
+  static const int aux_order = [] { const char *e = getenv("FOLD_AUX_ORDER"); return e ? atoi(e) : 0; }();
+  static AuxStream serial;  // ok == false: everything on the caller's stream
+  AuxStream &ax = aux_order == 2 ? serial : aux_stream();
   cudaStream_t s2 = ax.ok ? ax.s : st;
   if (ax.ok) {
     FOLD_CUDA_TRY(cudaEventRecord(ax.fork, st));
     FOLD_CUDA_TRY(cudaStreamWaitEvent(s2, ax.fork, 0));
   }
-  {
-    ProfScope ps(K_EMBED_BWD, s2);
-    FOLD_TRY(launch_embed_bwd_pieces(S, nl, s->n_tok_segs, s->tok_seg, s->leaf_perm, s->leaf_token, s->cons_off,
-                                     s->cons_edge, b.root_off, s->root_perm, dh_root, b.dA, grads->dE, b.emb, s2));
-  }
-  {
-    ProfScope ps(K_COLSUM, s2);
-    FOLD_TRY(launch_colsum(bf16, nc, gates * S, b.dZ, b.ld_z, b.partial, b.nsplit, grads->db, acc, s2));
-  }
-  {
+  auto run_du = [&]() -> fold_status {
     ProfScope ps(K_GEMM_DU, st);
     if (bf16)
       FOLD_TRY(tc_gemm_dU(nc, S, gates, (const __nv_bfloat16 *)b.dZ, b.ld_z,
@@ -331,7 +326,19 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
     else
       FOLD_TRY(launch_gemm_dU_simt(nc, nl, S, gates, (const float *)b.dZ, b.ld_z, s->gather, (const float *)H, L.ld,
                                    grads->dU, acc, st));
+    return FOLD_OK;
+  };
+  if (aux_order == 1) FOLD_TRY(run_du());
+  {
+    ProfScope ps(K_EMBED_BWD, s2);
+    FOLD_TRY(launch_embed_bwd_pieces(S, nl, s->n_tok_segs, s->tok_seg, s->leaf_perm, s->leaf_token, s->cons_off,
+                                     s->cons_edge, b.root_off, s->root_perm, dh_root, b.dA, grads->dE, b.emb, s2));
   }
+  {
+    ProfScope ps(K_COLSUM, s2);
+    FOLD_TRY(launch_colsum(bf16, nc, gates * S, b.dZ, b.ld_z, b.partial, b.nsplit, grads->db, acc, s2));
+  }
+  if (aux_order != 1) FOLD_TRY(run_du());
   if (ax.ok) {
     FOLD_CUDA_TRY(cudaEventRecord(ax.join, s2));
     FOLD_CUDA_TRY(cudaStreamWaitEvent(st, ax.join, 0));
