@@ -296,6 +296,21 @@ __device__ void sort_pass(const uint32_t *kin, const int32_t *vin, int n, int sh
   __syncthreads();
   for (int i = lo + tid; i < hi; i += T) atomicAdd(&run[(kin[i] >> shift) & mask], 1);
   __syncthreads();
+  if (nb == 1) {
+    // one block: the digit offsets are the exclusive scan of its own histogram (no
+    // cross-block prefix through global memory)
+    int carry = 0;
+    for (int d0 = 0; d0 < nbins; d0 += T) {
+      const int d = d0 + tid;
+      const int v = d < nbins ? run[d] : 0;
+      int tot;
+      const int ex = block_excl_scan(v, (int *)(base + nbins), &tot);
+      if (d < nbins) base[d] = carry + ex;
+      carry += tot;
+    }
+    __syncthreads();
+    for (int d = tid; d < nbins; d += T) run[d] = 0;
+  } else {
   for (int d = tid; d < nbins; d += T) w.hist[d * nb + b] = run[d];
   gsync(w.flags);
   // 2. per digit (one warp each): exclusive prefix over blocks, digit totals
@@ -328,6 +343,7 @@ __device__ void sort_pass(const uint32_t *kin, const int32_t *vin, int n, int sh
       carry += tot;
     }
     for (int d = tid; d < nbins; d += T) run[d] = 0;
+  }
   }
   __syncthreads();
   for (int t0 = lo; t0 < hi; t0 += T) {
