@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--ref-trees", type=int, default=1, help="trees per oracle step (--impl reference)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the nodes/s vs batch-size sweep")
+    ap.add_argument("--pipeline", default="auto", choices=["auto", "on", "off"],
+                    help="run the next batch's fold_schedule on a side stream while the current batch executes "
+                         "(auto: for batches of at most %d nodes and 64 levels, where it measured faster)" % 131072)
     ap.add_argument("--no-table1", action="store_true",
                     help="skip the unbatched baseline and the PAPER.md Table 1 reproduction")
     return ap.parse_args()
@@ -201,12 +204,88 @@ def run_fold(args):
         fold.sgd_update(flat_p, flat_g, args.lr)
         return h
 
+    # Pipelined steps ("overlap fold_schedule(k+1) with execution of
+    # batch k"): the next batch's schedule is computed on a side stream right after batch k's
+    # forward / backward / SGD are enqueued, so its kernel fills the gaps of batch k's tail
+    # and its one host sync no longer idles the GPU; batch k+1's forward waits on its event.
+    # Every step still schedules its own batch (K schedules in K timed steps).
+    side_stream = torch.cuda.Stream(device=dev) if args.pipeline != "off" else None
+    pipe_max_nodes = {"auto": 131072, "on": 1 << 62, "off": -1}[args.pipeline]
+    side = None  # set per timed workload by use_pipeline()
+
+    def use_pipeline(n_nodes, n_levels):
+        # measured crossover: with a few hundred thousand nodes, or hundreds of
+        # levels (one grid barrier each), the scheduler's cooperative kernel running beside
+        # the previous batch's GEMMs costs more than it hides
+        nonlocal side
+        ok = n_nodes <= pipe_max_nodes and (n_levels <= 64 or args.pipeline == "on")
+        side = side_stream if ok else None
+        return side is not None
+
+    def schedule_async(op, child, token, root, copies=(), level=None):
+        if side is None:
+            for d, h in copies:
+                d.copy_(h, non_blocking=True)
+            return fold.schedule(op, child, token, root, V, workspace=sched_ws, level=level), None
+        main = torch.cuda.current_stream()
+        with torch.cuda.stream(side):
+            for d, h in copies:
+                d.copy_(h, non_blocking=True)
+            sc = fold.schedule(op, child, token, root, V, workspace=sched_ws, stream=side, level=level)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        for t in sc.arrays.values():
+            t.record_stream(main)
+        return sc, ev
+
+    def run_step(sc, ev, g, train=True):
+        if ev is not None:
+            torch.cuda.current_stream().wait_event(ev)
+        h, c, acts = fold.forward(sc, model, ws=ws, want_c=False)
+        if not train:
+            return h
+        fold.backward(sc, model, acts, g, grads=(dU, db, dE), ws=ws)
+        if world > 1:
+            dist.all_reduce(flat_g)
+        fold.sgd_update(flat_p, flat_g, args.lr)
+        return h
+
+    def time_steps(o, g, nrep, level=None, train=True, warm=3):
+        """ms per step of nrep steps over the device graphs o (same step and pipelining
+        policy as the headline: schedule + forward [+ backward + SGD])."""
+        nlev = fold.schedule(*o, V, workspace=sched_ws, level=level).n_levels
+        use_pipeline(int(o[0].shape[0]), nlev)
+        sp = schedule_async(*o, level=level)
+        for _ in range(warm):
+            run_step(*sp, g, train)
+            sp = schedule_async(*o, level=level)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(nrep):
+            run_step(*sp, g, train)
+            sp = schedule_async(*o, level=level)
+        if sp[1] is not None:
+            torch.cuda.current_stream().wait_event(sp[1])
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / nrep
+
     # size the schedule workspace once (fold_schedule_workspace)
     sched_ws = torch.empty(int(fold.load().fold_schedule_workspace(N_nodes, gr.n_graphs)), dtype=torch.uint8,
                            device=dev)
     for _ in range(args.warmup):
         step(op, child, token, root, g_dev)
     n_levels = fold.schedule(op, child, token, root, V, workspace=sched_ws).n_levels
+    torch.cuda.synchronize()
+    # pipelined warm-up (the allocator reaches its steady rotation of schedule arrays), then
+    # batch 1's schedule, both before the timed region
+    pipelined = use_pipeline(N_nodes, n_levels)
+    sp = schedule_async(op, child, token, root)
+    for _ in range(max(args.warmup, 3)):
+        run_step(*sp, g_dev)
+        sp = schedule_async(op, child, token, root)
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local) if not args.no_clocks else None
@@ -225,8 +304,11 @@ def run_fold(args):
     e0.record()
     marks[0].record()
     for i in range(args.steps):
-        step(op, child, token, root, g_dev)
+        run_step(*sp, g_dev)
+        sp = schedule_async(op, child, token, root)  # the next batch's schedule (side stream)
         marks[i + 1].record()
+    if sp[1] is not None:
+        torch.cuda.current_stream().wait_event(sp[1])  # the K-th schedule inside the region
     e1.record()
     torch.cuda.synchronize()
     step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
@@ -257,14 +339,21 @@ def run_fold(args):
         h2d = sum(x.numel() * x.element_size() for x in (h_op, h_child, h_tok, h_root, h_g))
         d2h = h_out.numel() * 4
 
-        def e2e_step():
-            for d, h in ((d_op, h_op), (d_child, h_child), (d_tok, h_tok), (d_root, h_root), (d_g, h_g)):
-                d.copy_(h, non_blocking=True)
-            hr = step(d_op, d_child, d_tok, d_root, d_g)
-            h_out.copy_(hr, non_blocking=True)
+        graph_copies = ((d_op, h_op), (d_child, h_child), (d_tok, h_tok), (d_root, h_root))
 
-        for _ in range(2):
-            e2e_step()
+        def e2e_step(sp):
+            # this batch's upstream gradient H2D and result D2H on the compute stream; the
+            # next batch's graph arrays H2D + schedule on the side stream (pipelined)
+            d_g.copy_(h_g, non_blocking=True)
+            hr = run_step(*sp, d_g)
+            nxt = schedule_async(d_op, d_child, d_tok, d_root, copies=graph_copies)
+            h_out.copy_(hr, non_blocking=True)
+            return nxt
+
+        use_pipeline(N_nodes, n_levels)
+        sp = schedule_async(d_op, d_child, d_tok, d_root, copies=graph_copies)
+        for _ in range(max(args.warmup, 3)):
+            sp = e2e_step(sp)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -272,7 +361,9 @@ def run_fold(args):
         a1 = torch.cuda.Event(enable_timing=True)
         a0.record()
         for _ in range(args.steps):
-            e2e_step()
+            sp = e2e_step(sp)
+        if sp[1] is not None:
+            torch.cuda.current_stream().wait_event(sp[1])
         a1.record()
         torch.cuda.synchronize()
         t2 = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)
@@ -288,18 +379,7 @@ def run_fold(args):
         one = foldgen.sub_batch(gr, 0, 1)
         o1 = fold.graphs_to_device(one, dev)
         g1 = g_dev[:1].contiguous()
-        for _ in range(3):
-            step(*o1, g1)
-        torch.cuda.synchronize()
-        b0 = torch.cuda.Event(enable_timing=True)
-        b1 = torch.cuda.Event(enable_timing=True)
-        nrep = 20
-        b0.record()
-        for _ in range(nrep):
-            step(*o1, g1)
-        b1.record()
-        torch.cuda.synchronize()
-        ms1 = b0.elapsed_time(b1) / nrep
+        ms1 = time_steps(o1, g1, 20)
         batch1 = {"nodes_per_s": one.n_nodes / (ms1 / 1e3), "ms_per_tree": ms1}
 
     # ---------------- nodes/s vs batch size (BASELINE metric "... vs batch size"), rank 0
@@ -312,25 +392,14 @@ def run_fold(args):
             sub = foldgen.sub_batch(gr, 0, Bs)
             o = fold.graphs_to_device(sub, dev)
             gs = g_dev[:Bs].contiguous()
-            for _ in range(3):
-                step(*o, gs)
-            torch.cuda.synchronize()
-            s0 = torch.cuda.Event(enable_timing=True)
-            s1 = torch.cuda.Event(enable_timing=True)
-            nrep = 10
-            s0.record()
-            for _ in range(nrep):
-                step(*o, gs)
-            s1.record()
-            torch.cuda.synchronize()
-            msb = s0.elapsed_time(s1) / nrep
+            msb = time_steps(o, gs, 10)
             sweep[str(Bs)] = {"nodes_per_s": sub.n_nodes / (msb / 1e3), "ms_per_step": msb}
         sweep[str(gr.n_graphs)] = {"nodes_per_s": value / world, "ms_per_step": ms_per_step}
 
     # ---------------- unbatched baseline + PAPER.md Table 1 on B200 (rank 0)
     t1 = None
     if not args.no_table1 and rank == 0 and args.config in ("c2", "c5"):
-        t1 = table1(step, fold, gr, g_dev, V, S, dev)
+        t1 = table1(time_steps, fold, gr, g_dev, V, S, dev)
 
     if world > 1:
         dist.barrier()
@@ -386,7 +455,9 @@ def run_fold(args):
                    "step": "schedule+fwd+bwd+allreduce+sgd" if world > 1 else "schedule+fwd+bwd+sgd",
                    "l2": "working set > L2 (pool+saved gates+grads ~%.1f GB); no flush" % (
                        (N_nodes * S * 6 + n_cells * gates * S * 4 + n_cells * S * 16) / 1e9),
-                   "parallelism": f"dp{world}"},
+                   "parallelism": f"dp{world}",
+                   "pipeline": "next batch's fold_schedule on a side stream during this batch's step"
+                   if pipelined else "off (policy %s)" % args.pipeline},
         "gpu_launches": int(launches),
         "step_ms": {"median": float(np.median(step_ms)), "p10": float(np.percentile(step_ms, 10)),
                     "p90": float(np.percentile(step_ms, 90)), "rank0": [round(x, 4) for x in step_ms]},
@@ -430,7 +501,7 @@ def _time(fn, nrep, warm=2):
     return a.elapsed_time(b) / nrep
 
 
-def table1(step, fold, gr, g_dev, V, S, dev):
+def table1(time_steps, fold, gr, g_dev, V, S, dev):
     """PAPER.md L83-L127 / Table 1 with our kernels on B200, training (fwd+bwd+SGD, the
     bench step) and inference (schedule + forward) per-tree times.
       unbatched:   ONE tree of the headline workload, manual levels (one cell per level:
@@ -453,7 +524,7 @@ def table1(step, fold, gr, g_dev, V, S, dev):
         t, lv = dev_graphs(g, manual)
         gg = g_dev[:g.n_graphs].contiguous() if g.n_graphs <= g_dev.shape[0] else \
             torch.ones((g.n_graphs, S), device=dev) * 0.01
-        ms = _time(lambda: step(*t, gg, level=lv, train=train), nrep)
+        ms = time_steps(t, gg, nrep, level=lv, train=train, warm=2)
         return ms / g.n_graphs
 
     one = foldgen.sub_batch(gr, 0, 1)
