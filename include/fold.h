@@ -29,6 +29,18 @@
  *  - Thread safety: calls on different streams with disjoint buffers may run concurrently;
  *    fold_last_error_detail is thread-local.
  *  - Int arrays are int32, row-major. Floats are IEEE fp32 unless stated.
+ *
+ * Environment (read once per process; tuning and test hooks, defaults are the measured
+ * best):
+ *   FOLD_FWD_NARROW_MAX   forward levels of at most this many rows after the last wider
+ *                         level run in the weight-stationary narrow kernel (default 32; 0 off)
+ *   FOLD_BWD_NARROW_MAX   same for the backward's first levels (default 128; 0 off)
+ *   FOLD_SCHED_SMALLN     fold_schedule runs as one block up to this many nodes (4096)
+ *   FOLD_SCHED_PER_BLOCK  nodes per block of the cooperative scheduler above it (2048)
+ *   FOLD_AUX_ORDER        0: embedding / db reductions on an auxiliary stream beside the
+ *                         weight-gradient GEMM (default), 1: launched after it, 2: serial
+ *   FOLD_DBG_FWD          1/2: per-tile forward timelines (fold_debug_fwd_trace)
+ *   FOLD_DEBUG_SYNC       1: synchronize and check after every launch
  */
 #ifndef FOLD_H
 #define FOLD_H
