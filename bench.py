@@ -279,6 +279,11 @@ def run_fold(args):
         step(op, child, token, root, g_dev)
     n_levels = fold.schedule(op, child, token, root, V, workspace=sched_ws).n_levels
     torch.cuda.synchronize()
+    # the host enqueues every kernel of a step: keep the Python cyclic GC out of the timed
+    # regions (a collection pause idles the GPU for tens of ms; nothing here builds cycles)
+    import gc
+    gc.collect()
+    gc.disable()
     # pipelined warm-up (the allocator reaches its steady rotation of schedule arrays), then
     # batch 1's schedule, both before the timed region
     pipelined = use_pipeline(N_nodes, n_levels)
