@@ -697,32 +697,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
 // appends c / G, pushes h to the consumers' A rows and publishes h-column credits exactly
 // like k_fwd_levels, so the two kernels share the dependency counters (this one runs after
 // it, on the remaining levels d0..D).
-constexpr int NW_RMAX = 32;         // rows per chunk: 8 on levels of <= 8 rows, 16 up to 16, else 32
+constexpr int NW_ROWS = 8;          // rows per chunk
 constexpr int NW_THREADS = 224;     // warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4-6 epilogue
 constexpr int NW_MAX_S = 1024;      // U slice (GATES*8 rows x 2S) + A chunk fit in shared memory
-constexpr int NW_ST = 4;            // A-chunk ring stages
-constexpr int NW_STAGE = 2 * NW_RMAX * 128;  // 8 KB: one K-block of both halves of 32 rows
 
 template <int GATES>
 struct NwCfg {
   static constexpr int UROWS = GATES * 8;               // U rows per CTA (per K half)
   static constexpr int USLOT = 2 * UROWS * 128;         // bytes per K-block slot (both halves)
   static constexpr int SLACK = (16 - 2 * UROWS / 8) * 1024; // the M = 128 operand reads 16 8-row groups
-  static int smem(int KBh) { return NW_ST * NW_STAGE + KBh * USLOT + SLACK + 1024; }
+  static constexpr int BKB = NW_ROWS * 128;             // bytes per K-block of the A chunk
+  static int smem(int KBh) { return 2 * KBh * BKB + KBh * USLOT + SLACK + 1024; }
   static_assert(2 * UROWS <= 96, "both halves' U rows are read by TMEM lane quarters 0..2");
 };
 
-__device__ __forceinline__ int nw_rows_per_chunk(int level_rows) {
-  return level_rows <= 8 ? 8 : level_rows <= 16 ? 16 : NW_RMAX;
-}
-
 template <int GATES>
 __global__ void __launch_bounds__(NW_THREADS, 1)
-    k_fwd_narrow(const __grid_constant__ CUtensorMap tmUs, const __grid_constant__ CUtensorMap tmA8,
-                 const __grid_constant__ CUtensorMap tmA16, const __grid_constant__ CUtensorMap tmA32,
-                 const __grid_constant__ CUtensorMap tmL8, const __grid_constant__ CUtensorMap tmR8,
-                 const __grid_constant__ CUtensorMap tmL16, const __grid_constant__ CUtensorMap tmR16,
-                 const __grid_constant__ CUtensorMap tmL32, const __grid_constant__ CUtensorMap tmR32, int use4d,
+    k_fwd_narrow(const __grid_constant__ CUtensorMap tmUs, const __grid_constant__ CUtensorMap tmAL8,
+                 const __grid_constant__ CUtensorMap tmAR8, const __grid_constant__ CUtensorMap tmA4, int use3d,
                  const int32_t *__restrict__ lo, int d0, int D, int S,
                  int nl, int ld, const int32_t *__restrict__ gather, const float *__restrict__ bias,
                  __nv_bfloat16 *__restrict__ H, float *C, __nv_bfloat16 *__restrict__ Gact, int ld_g, ScatterA sc,
@@ -731,49 +723,47 @@ __global__ void __launch_bounds__(NW_THREADS, 1)
   dbg = dbg && blockIdx.x == 0;  // timeline of CTA 0 only
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
-  const int KBh = (int)cdiv(S, BK), Sp = KBh * BK;
-  uint8_t *Bsm = smem, *Usm = smem + NW_ST * NW_STAGE;  // B ring: [slot][half][R rows]; U: [slot][half][UROWS]
-  __shared__ __align__(8) uint64_t u_full, full[NW_ST], empty[NW_ST], acc_full[2], acc_empty[2];
-  __shared__ float zs[2][GATES * 8][NW_RMAX + 1];
+  const int KBh = (int)cdiv(S, BK), KB = 2 * KBh, Sp = KBh * BK;
+  uint8_t *Bsm = smem, *Usm = smem + KB * Cfg::BKB;  // B: [slot][half][8 rows]; U: [slot][half][UROWS]
+  __shared__ __align__(8) uint64_t u_full, b_full, b_empty, acc_full[2], acc_empty[2];
+  __shared__ float zs[2][GATES * 8][NW_ROWS + 1];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int j0 = blockIdx.x * 8;
   const int ncols = min(8, S - j0);
   if (tid == 0) {
     ptx::mbar_init(&u_full, 1);
-    for (int s2 = 0; s2 < NW_ST; s2++) { ptx::mbar_init(&full[s2], 1); ptx::mbar_init(&empty[s2], 1); }
+    ptx::mbar_init(&b_full, 1);
+    ptx::mbar_init(&b_empty, 1);
     for (int a = 0; a < 2; a++) { ptx::mbar_init(&acc_full[a], 1); ptx::mbar_init(&acc_empty[a], 3); }
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tmUs);
-    ptx::prefetch_tmap(&tmA8);
-    ptx::prefetch_tmap(&tmA16);
-    ptx::prefetch_tmap(&tmA32);
+    ptx::prefetch_tmap(&tmAL8);
+    ptx::prefetch_tmap(&tmAR8);
+    ptx::prefetch_tmap(&tmA4);
   }
-  if (warp == 2) { ptx::tmem_alloc(&tmem_base_sh, 128); ptx::tmem_relinquish(); }
+  if (warp == 2) { ptx::tmem_alloc(&tmem_base_sh, 32); ptx::tmem_relinquish(); }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = tmem_base_sh;
 
-  // chunk walk (every role keeps its own cursor): level d, rows [r, r + R)
+  // chunk walk (every role keeps its own cursor): level d, rows [r, r + rows)
   struct Cur {
-    int d, r, r1, R;
-    __device__ void load(const int32_t *lo) {
-      r = __ldg(lo + d); r1 = __ldg(lo + d + 1); R = nw_rows_per_chunk(r1 - r);
-    }
-    __device__ void init(const int32_t *lo, int d0) { d = d0; load(lo); }
+    int d, r, r1;
+    __device__ void init(const int32_t *lo, int d0) { d = d0; r = __ldg(lo + d); r1 = __ldg(lo + d + 1); }
     __device__ bool next(const int32_t *lo, int D) {  // advance to the next chunk
-      r += R;
+      r += NW_ROWS;
       while (r >= r1) {
         if (++d > D) return false;
-        load(lo);
+        r = __ldg(lo + d); r1 = __ldg(lo + d + 1);
       }
       return true;
     }
     __device__ bool valid(const int32_t *lo, int D) {  // skip empty leading levels
       while (r >= r1) {
         if (++d > D) return false;
-        load(lo);
+        r = __ldg(lo + d); r1 = __ldg(lo + d + 1);
       }
       return true;
     }
@@ -785,161 +775,112 @@ __global__ void __launch_bounds__(NW_THREADS, 1)
     const int tend = min(key + PM, cu.r1 - nl);
     return (tend - key) * 2 * S;
   };
-  // one K-block slot of a chunk = both halves of its R rows; a stage holds kps slots, and
-  // when all KBh slots fit in the ring one box fills every stage at once
-  auto all_in_ring = [&](int R) { return KBh * 2 * R * 128 <= NW_ST * NW_STAGE; };
 
   if (warp == 0) {
     if (lane == 0) {
       ptx::mbar_arrive_expect_tx(&u_full, (uint32_t)(KBh * Cfg::USLOT));
-      for (int kb = 0; kb < 2 * KBh; kb++) {
+      for (int kb = 0; kb < KB; kb++) {
         const int half = kb >= KBh, q = kb - half * KBh;
         ptx::tma_load_2d(&tmUs, &u_full, Usm + q * Cfg::USLOT + half * (Cfg::USLOT / 2), half * Sp + q * BK,
                          blockIdx.x * Cfg::UROWS);
       }
       Cur cu;
       cu.init(lo, d0);
-      int i = 0, it = 0;
+      int i = 0;
       for (bool ok = cu.valid(lo, D); ok; ok = cu.next(lo, D), i++) {
+        if (i > 0) ptx::mbar_wait(&b_empty, (i - 1) & 1);
         trace(dbg, 0, i);
         int key;
         const int target = tile_target(cu, key);
         ptx::wait_counter_relaxed(rt_cnt + key, target);
         ptx::fence_proxy_async_global();
         trace(dbg, 1, i);
-        const int R = cu.R, c0 = cu.r - nl;
-        const int slot_bytes = 2 * R * 128, kps = NW_STAGE / slot_bytes;
-        if (use4d && all_in_ring(R)) {
-          // the whole ring takes all K-blocks of the chunk in ONE box; every stage is used once
-          for (int k = 0; k < NW_ST; k++) ptx::mbar_wait(&empty[(it + k) % NW_ST], (((it + k) / NW_ST) & 1) ^ 1);
-          const int s0 = it % NW_ST;
-          ptx::mbar_arrive_expect_tx(&full[s0], (uint32_t)(KBh * slot_bytes));
-          ptx::tma_load_4d(R == 8 ? &tmA8 : R == 16 ? &tmA16 : &tmA32, &full[s0], Bsm, 0, c0, 0, 0);
-          for (int k = 1; k < NW_ST; k++) ptx::mbar_arrive(&full[(it + k) % NW_ST]);
-          it += NW_ST;
-          continue;
-        }
-        const CUtensorMap *mL = R == 8 ? &tmL8 : R == 16 ? &tmL16 : &tmL32;
-        const CUtensorMap *mR = R == 8 ? &tmR8 : R == 16 ? &tmR16 : &tmR32;
-        for (int q0 = 0; q0 < KBh; q0 += kps, it++) {
-          const int s2 = it % NW_ST;
-          ptx::mbar_wait(&empty[s2], ((it / NW_ST) & 1) ^ 1);
-          const int nk = min(kps, KBh - q0);
-          ptx::mbar_arrive_expect_tx(&full[s2], (uint32_t)(nk * slot_bytes));
-          for (int j = 0; j < nk; j++) {
-            uint8_t *dst = Bsm + s2 * NW_STAGE + j * slot_bytes;
-            ptx::tma_load_2d(mL, &full[s2], dst, (q0 + j) * BK, c0);
-            ptx::tma_load_2d(mR, &full[s2], dst + R * 128, (q0 + j) * BK, c0);
+        ptx::mbar_arrive_expect_tx(&b_full, (uint32_t)(KB * Cfg::BKB));
+        const int c0 = cu.r - nl;
+        if (use3d) {  // one 4D box: the chunk's 8 rows x both halves x all K-blocks
+          ptx::tma_load_4d(&tmA4, &b_full, Bsm, 0, c0, 0, 0);
+        } else {
+          for (int kb = 0; kb < KB; kb++) {
+            const int half = kb >= KBh, q = kb - half * KBh;
+            ptx::tma_load_2d(half ? &tmAR8 : &tmAL8, &b_full, Bsm + (2 * q + half) * Cfg::BKB, q * BK, c0);
           }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16(128, 2 * NW_ROWS, 0, 0);
       ptx::mbar_wait(&u_full, 0);
       Cur cu;
       cu.init(lo, d0);
-      int i = 0, it = 0;
-      const uint32_t u0 = ptx::smem_u32(Usm), b0 = ptx::smem_u32(Bsm);
+      int i = 0;
       for (bool ok = cu.valid(lo, D); ok; ok = cu.next(lo, D), i++) {
-        const int acc = i & 1, R = cu.R;
-        const int slot_bytes = 2 * R * 128, kps = NW_STAGE / slot_bytes;
-        const uint32_t idesc = ptx::idesc_bf16(128, 2 * R, 0, 0);
+        const int acc = i & 1;
         ptx::mbar_wait(&acc_empty[acc], ((i >> 1) & 1) ^ 1);
-        const uint32_t dst = tbase + acc * 2 * NW_RMAX;
-        // B rows 0..R-1: h_L K-block q of the chunk's rows, R..2R-1: h_R K-block q
-        if (use4d && all_in_ring(R)) {
-          for (int k = 0; k < NW_ST; k++) ptx::mbar_wait(&full[(it + k) % NW_ST], ((it + k) / NW_ST) & 1);
-          ptx::tc_fence_after();
-          trace(dbg, 7, i);
-          for (int q = 0; q < KBh; q++) {
+        ptx::mbar_wait(&b_full, i & 1);
+        ptx::tc_fence_after();
+        trace(dbg, 7, i);
+        const uint32_t dst = tbase + acc * 2 * NW_ROWS;
+        const uint32_t u0 = ptx::smem_u32(Usm), b0 = ptx::smem_u32(Bsm);
+        for (int q = 0; q < KBh; q++) {  // B rows 0..7: h_L K-block q, rows 8..15: h_R K-block q
 #pragma unroll
-            for (int k = 0; k < BK / 16; k++)
-              ptx::umma_bf16(dst, ptx::sdesc_sw128(u0 + q * Cfg::USLOT + 32 * k, 16, 1024),
-                             ptx::sdesc_sw128(b0 + q * slot_bytes + 32 * k, 16, 1024), idesc, (q | k) != 0);
-          }
-          for (int k = 0; k < NW_ST; k++) ptx::umma_commit(&empty[(it + k) % NW_ST]);
-          it += NW_ST;
-        } else {
-          for (int q0 = 0; q0 < KBh; q0 += kps, it++) {
-            const int s2 = it % NW_ST;
-            ptx::mbar_wait(&full[s2], (it / NW_ST) & 1);
-            ptx::tc_fence_after();
-            const int nk = min(kps, KBh - q0);
-            for (int j = 0; j < nk; j++) {
-              const int q = q0 + j;
-#pragma unroll
-              for (int k = 0; k < BK / 16; k++)
-                ptx::umma_bf16(dst, ptx::sdesc_sw128(u0 + q * Cfg::USLOT + 32 * k, 16, 1024),
-                               ptx::sdesc_sw128(b0 + s2 * NW_STAGE + j * slot_bytes + 32 * k, 16, 1024), idesc,
-                               (q | k) != 0);
-            }
-            ptx::umma_commit(&empty[s2]);
-          }
+          for (int k = 0; k < BK / 16; k++)
+            ptx::umma_bf16(dst, ptx::sdesc_sw128(u0 + q * Cfg::USLOT + 32 * k, 16, 1024),
+                           ptx::sdesc_sw128(b0 + 2 * q * Cfg::BKB + 32 * k, 16, 1024), idesc, (q | k) != 0);
         }
+        ptx::umma_commit(&b_empty);
         ptx::umma_commit(&acc_full[acc]);
         trace(dbg, 2, i);
       }
     }
   } else if (warp >= 4) {
-    const int t = tid - 128;          // 0..95
+    const int t = tid - 128;          // 0..95 (the math uses 0..63)
     const int q = warp & 3;           // TMEM lane quarter 0 / 1 / 2
-    constexpr int NIT = (NW_RMAX * 8 + 95) / 96;  // (row, column) items per thread at most
+    const int n = t >> 3, u = t & 7;  // this thread's (row in chunk, state column) in the math
+    const int j = j0 + u;
     Cur cu;
     cu.init(lo, d0);
     int i = 0;
     for (bool ok = cu.valid(lo, D); ok; ok = cu.next(lo, D), i++) {
-      const int acc = i & 1, R = cu.R;
-      const int rows = min(R, cu.r1 - cu.r);
+      const int acc = i & 1;
+      const int rows = min(NW_ROWS, cu.r1 - cu.r);
+      const int64_t r = cu.r + n;
+      const bool act = n < rows && u < ncols;
       // children's c (published with their h): fetched while the MMA runs
-      float cl[NIT], cr[NIT];
-      bool waited = false;
-#pragma unroll
-      for (int k = 0; k < NIT; k++) {
-        cl[k] = 0.f; cr[k] = 0.f;
-        const int item = t + 96 * k, n = item >> 3, u = item & 7;
-        if (GATES != 5 || item >= R * 8 || n >= rows || u >= ncols) continue;
-        const int64_t r = cu.r + n;
-        const int64_t gl = __ldg(gather + 2 * r), gr = __ldg(gather + 2 * r + 1);
-        if (gl < nl && gr < nl) continue;
-        if (!waited) {
+      int64_t gl = 0, gr = 0;
+      float cl = 0.f, cr = 0.f;
+      if (act) {
+        gl = __ldg(gather + 2 * r);
+        gr = __ldg(gather + 2 * r + 1);
+        if (GATES == 5 && (gl >= nl || gr >= nl)) {
           int key;
           const int target = tile_target(cu, key);
           ptx::wait_counter(rt_cnt + key, target);
-          waited = true;
+          if (gl >= nl) cl = __ldcg(C + gl * ld + j);
+          if (gr >= nl) cr = __ldcg(C + gr * ld + j);
         }
-        if (gl >= nl) cl[k] = __ldcg(C + gl * ld + j0 + u);
-        if (gr >= nl) cr[k] = __ldcg(C + gr * ld + j0 + u);
       }
       if (t == 0) trace(dbg, 5, i);
       ptx::mbar_wait(&acc_full[acc], (i >> 1) & 1);
       ptx::tc_fence_after();
       if (t == 0) trace(dbg, 3, i);
-      {
-        const int m = q * 32 + lane;  // D row = stacked U row
-        const int hf = m >= Cfg::UROWS;   // which K half this row accumulated
-        // its half's R columns: rows < UROWS pair with B rows 0..R-1, the next UROWS with
-        // R..2R-1 (tcgen05.ld addresses are warp-uniform: read both and select per lane)
-        const uint32_t ta = tbase + acc * 2 * NW_RMAX + ((uint32_t)(q * 32) << 16);
-        for (int c8 = 0; c8 < R; c8 += 8) {
-          float z0[8], z1[8];
-          ptx::tmem_ld8(ta + c8, z0);
-          ptx::tmem_ld8(ta + R + c8, z1);
-          ptx::tmem_ld_wait();
-          if (m < 2 * Cfg::UROWS)
+      float z0[8], z1[8];
+      const int m = q * 32 + lane;  // D row = stacked U row
+      const int hf = m >= Cfg::UROWS;   // which K half this row accumulated
+      // its half's 8 columns: rows < UROWS pair with B rows 0..7, the next UROWS with 8..15
+      // (tcgen05.ld addresses are warp-uniform: read both and select per lane)
+      const uint32_t ta = tbase + acc * 2 * NW_ROWS + ((uint32_t)(q * 32) << 16);
+      ptx::tmem_ld8(ta, z0);
+      ptx::tmem_ld8(ta + NW_ROWS, z1);
+      ptx::tmem_ld_wait();
+      if (m < 2 * Cfg::UROWS)
 #pragma unroll
-            for (int k = 0; k < 8; k++) zs[hf][m - hf * Cfg::UROWS][c8 + k] = hf ? z1[k] : z0[k];
-        }
-      }
+        for (int k = 0; k < NW_ROWS; k++) zs[hf][m - hf * Cfg::UROWS][k] = hf ? z1[k] : z0[k];
       ptx::tc_fence_before();
       ptx::named_bar_sync(1, 96);
       if (lane == 0) ptx::mbar_arrive(&acc_empty[acc]);
-#pragma unroll
-      for (int k = 0; k < NIT; k++) {
-        const int item = t + 96 * k, n = item >> 3, u = item & 7;
-        if (item >= R * 8 || n >= rows || u >= ncols) continue;
-        const int j = j0 + u;
-        const int64_t r = cu.r + n, c = r - nl;
+      if (act) {
+        const int64_t c = r - nl;
         float hh;
         if constexpr (GATES == 1) {
           hh = tanh_fast(zs[0][u][n] + zs[1][u][n] + __ldg(bias + j));
@@ -952,7 +893,7 @@ __global__ void __launch_bounds__(NW_THREADS, 1)
             const float x = zs[0][g * 8 + u][n] + zs[1][g * 8 + u][n] + __ldg(bias + g * S + j);
             gs[g] = g == 4 ? tanh_fast(x) : sigmoid_fast(x);
           }
-          const float cc = gs[0] * gs[4] + gs[1] * cl[k] + gs[2] * cr[k];
+          const float cc = gs[0] * gs[4] + gs[1] * cl + gs[2] * cr;
           hh = gs[3] * tanh_fast(cc);
           C[r * ld + j] = cc;
 #pragma unroll
@@ -981,7 +922,7 @@ __global__ void __launch_bounds__(NW_THREADS, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc(tbase, 128); }
+  if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc(tbase, 32); }
 }
 
 // =================================================================== dA = dZ * U (one level)
@@ -2140,31 +2081,29 @@ fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
   }
   if (d0 <= a.D) {
     using NC = NwCfg<GATES>;
-    CUtensorMap tmUs, tmL[3], tmR[3], tmA[3];
+    CUtensorMap tmUs, tmAL8, tmAR8;
     FOLD_TRY(make_map(&tmUs, a.Ub, (uint64_t)a.ld_u, il_rows, (uint64_t)a.ld_u * 2, BK, NC::UROWS));
-    // chunk rows R = 8 / 16 / 32: 2D boxes of R rows per plane and K-block, and (S % 64 == 0,
-    // A_R at a fixed offset from A_L) a 4D view of the two planes as [K-block][half][row][64]
-    // whose one box holds a chunk's R rows of both halves and all K-blocks, landing slot-major
-    // with the halves interleaved (the B operand's row groups)
+    FOLD_TRY(make_map(&tmAL8, a.sc.AL, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, NW_ROWS));
+    FOLD_TRY(make_map(&tmAR8, a.sc.AR, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, NW_ROWS));
+    // 4D view of the two planes as [K-block][half][row][64 columns] (S % 64 == 0 and A_R at a
+    // fixed offset from A_L): one box = the chunk's 8 rows of both halves and all K-blocks,
+    // landing slot-major with the halves interleaved (the B operand's 8-row groups)
+    CUtensorMap tmA4;
     const int64_t half_off = (const char *)a.sc.AR - (const char *)a.sc.AL;
-    int use4d = (S % BK == 0) && (S / BK) <= 256 && half_off > 0 && half_off % 16 == 0;
-    auto enc = encode_fn();
-    if (!enc) return FOLD_E_CUDA;
-    for (int v = 0; v < 3; v++) {
-      const int R = 8 << v;
-      FOLD_TRY(make_map(&tmL[v], a.sc.AL, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, R));
-      FOLD_TRY(make_map(&tmR[v], a.sc.AR, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, R));
-      tmA[v] = tmL[v];
-      if (!use4d || (S / BK) * 2 * R * 128 > NW_ST * NW_STAGE) continue;  // (box used only if it fits the ring)
+    int use3d = (S % BK == 0) && (S / BK) <= 256 && half_off > 0 && half_off % 16 == 0;
+    if (use3d) {
+      auto enc = encode_fn();
+      if (!enc) return FOLD_E_CUDA;
       cuuint64_t dims[4] = {(cuuint64_t)BK, (cuuint64_t)nc, 2, (cuuint64_t)(S / BK)};
       cuuint64_t strides[3] = {(cuuint64_t)a.sc.ld * 2, (cuuint64_t)half_off, (cuuint64_t)BK * 2};
-      cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)R, 2, (cuuint32_t)(S / BK)};
+      cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)NW_ROWS, 2, (cuuint32_t)(S / BK)};
       cuuint32_t es[4] = {1, 1, 1, 1};
-      if (enc(&tmA[v], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void *)a.sc.AL, dims, strides, box, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        use4d = 0;
+      CUresult r = enc(&tmA4, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, (void *)a.sc.AL, dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) use3d = 0;
     }
+    if (!use3d) tmA4 = tmAL8;
     const int nsm = NC::smem((int)cdiv(S, BK));
     auto nk = k_fwd_narrow<GATES>;
     FOLD_TRY(set_smem(nk, nsm));
@@ -2179,9 +2118,8 @@ fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
     int *rt = a.rt_cnt;
     const int32_t *ts = a.tstart;
     int d0v = d0, Sv = S, dbgv = dbg_fwd() == 2;
-    void *args[] = {(void *)&tmUs, (void *)&tmA[0], (void *)&tmA[1], (void *)&tmA[2], (void *)&tmL[0],
-                    (void *)&tmR[0], (void *)&tmL[1], (void *)&tmR[1], (void *)&tmL[2], (void *)&tmR[2],
-                    (void *)&use4d, (void *)&lo, (void *)&d0v, (void *)&D,
+    void *args[] = {(void *)&tmUs, (void *)&tmAL8, (void *)&tmAR8, (void *)&tmA4, (void *)&use3d,
+                    (void *)&lo, (void *)&d0v, (void *)&D,
                     (void *)&Sv, (void *)&nl, (void *)&ld, (void *)&gather, (void *)&bias, (void *)&H, (void *)&C,
                     (void *)&G, (void *)&ld_g, (void *)&sc, (void *)&rt, (void *)&ts, (void *)&dbgv};
     // cooperative: every CTA must be resident (they wait on each other's published columns)
