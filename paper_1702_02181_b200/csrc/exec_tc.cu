@@ -47,12 +47,6 @@ __device__ __forceinline__ void trace(int dbg, int pt, int T) {
 }
 
 constexpr int BM = 128;     // rows per CTA (the pair's MMA has M = 256)
-// A-operand box rows for a CTA holding m rows of a tile (narrow tiles load only their rows)
-#ifdef FOLD_AB_NOKPS
-#define FOLD_BOX(m) ((m) <= 0 ? 0 : BM)
-#else
-#define FOLD_BOX(m) ((m) <= 0 ? 0 : (m) <= 16 ? 16 : (m) <= 64 ? 64 : BM)
-#endif
 constexpr int PM = 2 * BM;  // rows per CTA pair
 constexpr int BK = 64;      // K elements per stage (128 B of bf16 = one swizzle row)
 constexpr int ST = 6;       // pipeline stages
@@ -135,9 +129,6 @@ struct FwdCfg {
 template <int GATES>
 __host__ __device__ inline int fwd_kps(int W, int bx0) {
   using Cfg = FwdCfg<GATES>;
-#ifdef FOLD_AB_NOKPS
-  return 1;
-#endif
   if (W == Cfg::WMAX) return 1;
   const int k = Cfg::STAGE / (bx0 * 128 + GATES * W * 64);
   return k < 1 ? 1 : k > 8 ? 8 : k;
@@ -221,7 +212,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         const int lt = T - cur.t0, W = cur.W;
         const int ct = (cur.r0 - nl) + (lt / cur.NT) * PM;  // first cell of the pair tile
         const int rows = min(PM, cur.r1 - nl - ct);
-        auto box_of = [](int m) { return FOLD_BOX(m); };
+        // A-operand box rows for a CTA holding m rows (narrow tiles load only their rows)
+        auto box_of = [](int m) { return m <= 0 ? 0 : m <= 16 ? 16 : m <= 64 ? 64 : BM; };
         const int bx0 = box_of(min(rows, BM)), bx1 = box_of(rows - BM), bx = rank ? bx1 : bx0;
         const CUtensorMap *mL = bx == 16 ? &tmAL16 : bx == 64 ? &tmAL64 : &tmAL;
         const CUtensorMap *mR = bx == 16 ? &tmAR16 : bx == 64 ? &tmAR64 : &tmAR;
@@ -236,12 +228,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         const int nst = (KB + kps - 1) / kps;
         // inputs already published (the common case on wide levels): A and U per stage in
         // order; otherwise the first stages' U boxes go out before the wait
-#ifdef FOLD_AB_NOPREFETCH
-        ptx::wait_counter_relaxed(rt_cnt + ct, rows * 2 * S);
-        const bool ready = true;
-#else
         const bool ready = ptx::ld_relaxed_gpu(rt_cnt + ct) >= rows * 2 * S;
-#endif
         if (ready) ptx::fence_proxy_async_global();
         const int pre = ready ? 0 : (nst < ST ? nst : ST);
         if (ready && rank == 0) trace(dbg, 1, T);
@@ -313,11 +300,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         const uint32_t dst = tbase + acc * Cfg::ACC_STRIDE;
         const int ct = (cur.r0 - nl) + ((T - cur.t0) / cur.NT) * PM;
         const int rows0 = min(BM, cur.r1 - nl - ct);
-        #ifdef FOLD_AB_NOKPS
-        const int bx0 = BM;
-#else
         const int bx0 = rows0 <= 16 ? 16 : rows0 <= 64 ? 64 : BM;
-#endif
         const int kps = fwd_kps<GATES>(cur.W, bx0), abox = bx0 * 128, ubox = GATES * cur.W * 64;
         const int nst = (KB + kps - 1) / kps;
         if (kps == 1) {  // one k-block per stage, U at the fixed offset A_BYTES
@@ -1082,9 +1065,6 @@ struct BwdCursor {  // walks levels D, D-1, ..., 2 in tile order
 
 // k-blocks per stage of a backward tile (see fwd_kps): dZ box of bx0 rows + N/2 U columns
 __host__ __device__ inline int bwd_kps(int N, int bx0) {
-#ifdef FOLD_AB_NOKPS
-  return 1;
-#endif
   const int k = DA_STAGE / (bx0 * 128 + (N / 128) * MN_CHUNK);
   return k < 1 ? 1 : k > 8 ? 8 : k;
 }
@@ -1139,7 +1119,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         const int ct = (cur.r0 - nl) + (lt / NTn) * PM;  // first cell of the pair tile
         const int rows = min(PM, cur.r1 - nl - ct);
         // narrow tiles load only the dZ rows they hold (see k_fwd_levels)
-        auto box_of = [](int m) { return FOLD_BOX(m); };
+        // A-operand box rows for a CTA holding m rows (narrow tiles load only their rows)
+        auto box_of = [](int m) { return m <= 0 ? 0 : m <= 16 ? 16 : m <= 64 ? 64 : BM; };
         const int bx0 = box_of(min(rows, BM)), bx1 = box_of(rows - BM), bx = rank ? bx1 : bx0;
         const CUtensorMap *mZ = bx == 16 ? &tmZ16 : bx == 64 ? &tmZ64 : &tmZ;
         const int mt = ct + (int)rank * BM;
@@ -1149,12 +1130,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         // kps k-blocks per stage
         const int kps = bwd_kps(N, bx0), abox = bx0 * 128, ubox = (N / 128) * MN_CHUNK;
         const int nst = (KB + kps - 1) / kps;
-#ifdef FOLD_AB_NOPREFETCH
-        ptx::wait_counter(rt_cnt + ct, rows * slabs);
-        const bool ready = true;
-#else
         const bool ready = ptx::ld_acquire_gpu(rt_cnt + ct) >= rows * slabs;
-#endif
         if (ready) ptx::fence_proxy_async_global();
         const int pre = ready ? 0 : (nst < ST ? nst : ST);
         if (ready && kps == 1) {  // inputs published: one (A, U) box set per stage
@@ -1215,11 +1191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         const uint32_t dst = tbase + acc * 256;
         const int ct = (cur.r0 - nl) + ((T - cur.t0) / cur.NTn) * PM;
         const int rows0 = min(BM, cur.r1 - nl - ct);
-        #ifdef FOLD_AB_NOKPS
-        const int bx0 = BM;
-#else
         const int bx0 = rows0 <= 16 ? 16 : rows0 <= 64 ? 64 : BM;
-#endif
         const int kps = bwd_kps(cur.N, bx0), abox = bx0 * 128, ubox = (cur.N / 128) * MN_CHUNK;
         const int nst = (KB + kps - 1) / kps;
         if (kps == 1) {  // one k-block per stage, U at the fixed offset DA_A_BYTES
