@@ -177,3 +177,25 @@ def test_batch_composition_bitwise_fp32():
         one = foldgen.sub_batch(gr, t, t + 1)
         o, _ = _run(one, "treelstm", "fp32", 40, params=p)
         assert np.array_equal(o["h"][0], full["h"][t])
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+@pytest.mark.parametrize("S", [1, 7, 33, 130])
+def test_odd_and_tiny_state_sizes(prec, S):
+    """S not a multiple of 8 / 64, odd S (the tree-like fused backward needs even S and the
+    library falls back to the per-level backward), S = 1."""
+    rng = np.random.default_rng(100 + S)
+    shapes = [foldgen.random_split_shape(rng, int(rng.integers(1, 25))) for _ in range(9)]
+    gr = foldgen.batch_from_shapes(shapes, foldgen.uniform_tokens(rng, 50), 50)
+    _check_fwd(gr, "treelstm", prec, S)
+    _check_bwd(gr, "treelstm", prec, S)
+
+
+def test_large_state_2048_bf16():
+    """S = 2048 (K = 4096 per cell GEMM; above the narrow kernels' stationary-U limit, so
+    every level runs in the wide kernels)."""
+    rng = np.random.default_rng(2048)
+    shapes = [foldgen.random_split_shape(rng, int(rng.integers(2, 9))) for _ in range(3)]
+    gr = foldgen.batch_from_shapes(shapes, foldgen.uniform_tokens(rng, 40), 40)
+    _check_fwd(gr, "treelstm", "bf16", 2048)
+    _check_bwd(gr, "treelstm", "bf16", 2048)
