@@ -29,6 +29,7 @@ enum {
   F_QCNT = 12,  // 3 rotating frontier counters 12..14
   F_MULTI = 24,     // 1: some row has >= 2 consumer edges, or a root row is consumed
   F_NDISTROOT = 25, // number of distinct root rows
+  F_SHARED = 26,    // 1: some node has >= 2 consumer edges (set in P1)
   F_BAR = 16,   // grid barrier count, generation (16, 17)
   F_NFLAGS = 64
 };
@@ -423,7 +424,11 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
     if (!ar_ok) atomicMin(&flags[F_ERR0 + E_ARITY], n);
     if (o == FOLD_OP_EMBED && (a.token[n] < 0 || a.token[n] >= V)) atomicMin(&flags[F_ERR0 + E_TOKEN], n);
     const bool good_cell = (o == FOLD_OP_CELL) && !crange && c0 >= 0 && c1 >= 0;
-    if (good_cell) { atomicAdd(&w.ncons[c0], 1); atomicAdd(&w.ncons[c1], 1); }
+    if (good_cell) {
+      // a node read by two edges (incl. cell(x, x)) needs the general consumer-CSR sort
+      const int o0 = atomicAdd(&w.ncons[c0], 1), o1 = atomicAdd(&w.ncons[c1], 1);
+      if (o0 > 0 || o1 > 0) flags[F_SHARED] = 1;
+    }
     if (a.level) {  // manual batching: level[EMBED] == 1, level[CELL] > level[children], <= N
       const int lv = a.level[n];
       bool bad = lv < 1 || lv > N;
@@ -574,6 +579,16 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
   // ---- P9: consumer CSR: cell edges e in [0, 2 n_cells), key = child row, stable
   const int nl = ld_volatile(&flags[F_NLEAVES]);
   const int ne = 2 * (N - nl);
+  if (ld_volatile(&flags[F_SHARED]) == 0) {
+    // every node is read by at most one edge (trees): cons_off is the exclusive scan of
+    // "row is consumed" and each edge lands at its child row's offset -- the same CSR the
+    // stable sort yields, without the sort passes
+    for (int64_t r = gtid; r <= N; r += gstride) w.seg_flag[r] = r < N ? w.ncons[s.perm[r]] : 0;
+    gsync(flags);
+    grid_excl_scan(w.seg_flag, s.cons_off, N + 1, nullptr, w, sw);
+    for (int64_t e = gtid; e < ne; e += gstride) s.cons_edge[s.cons_off[s.gather[2 * (int64_t)nl + e]]] = (int)e;
+    gsync(flags);
+  } else {
   for (int64_t e = gtid; e < ne; e += gstride) {
     w.ka[e] = (uint32_t)s.gather[2 * (int64_t)nl + e];
     w.va[e] = (int)e;
@@ -590,6 +605,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
     s.cons_off[r] = lo;
   }
   gsync(flags);
+  }
 
   // ---- P10: leaves by (token, row) and token segments
   for (int64_t r = gtid; r < nl; r += gstride) {
