@@ -234,8 +234,7 @@ def run_fold(args):
             sc = fold.schedule(op, child, token, root, V, workspace=sched_ws, stream=side, level=level)
             ev = torch.cuda.Event()
             ev.record(side)
-        for t in sc.arrays.values():
-            t.record_stream(main)
+        sc.arrays.buffer.record_stream(main)
         return sc, ev
 
     def run_step(sc, ev, g, train=True):

@@ -40,6 +40,7 @@
  *   FOLD_AUX_ORDER        0: embedding / db reductions on an auxiliary stream beside the
  *                         weight-gradient GEMM (default), 1: launched after it, 2: serial
  *   FOLD_DBG_FWD          1/2: per-tile forward timelines (fold_debug_fwd_trace)
+ *   FOLD_DBG_SCHED        1: scheduler phase timeline (fold_debug_sched_trace)
  *   FOLD_DEBUG_SYNC       1: synchronize and check after every launch
  */
 #ifndef FOLD_H
@@ -259,6 +260,10 @@ fold_status fold_profile_read(int32_t n_classes, double *ms, int64_t *launches);
  * the kernel's order: levels ascending, row tile, column tile); returns the count, or -1
  * on a CUDA error. */
 int32_t fold_debug_fwd_trace(unsigned long long *host, int32_t n_tiles);
+/* Instrumentation: with FOLD_DBG_SCHED=1, fold_schedule's block 0 stamps %globaltimer (ns)
+ * at the start of phases P0..P11 and at its end; copies the 13 stamps into host[13] and
+ * returns 13 (-1 on a CUDA error). */
+int32_t fold_debug_sched_trace(unsigned long long *host);
 
 #ifdef __cplusplus
 }

@@ -8,6 +8,7 @@
 namespace fold {
 
 fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws, size_t ws_bytes, cudaStream_t st);
+int debug_sched_trace(unsigned long long *host);
 size_t schedule_workspace(int64_t N, int64_t G);
 extern thread_local int32_t g_last_detail;
 
@@ -373,6 +374,9 @@ const char *fold_status_string(fold_status s) {
 
 int32_t fold_last_error_detail(void) { return g_last_detail; }
 int32_t fold_abi_version(void) { return FOLD_ABI_VERSION; }
+
+/* instrumentation: per-phase timeline of the last FOLD_DBG_SCHED=1 schedule (block 0) */
+int32_t fold_debug_sched_trace(unsigned long long *host) { return fold::debug_sched_trace(host); }
 
 /* instrumentation: per-tile forward timeline of the last FOLD_DBG_FWD=1 run */
 int32_t fold_debug_fwd_trace(unsigned long long *host, int32_t n_tiles) {

@@ -200,6 +200,7 @@ struct SchedArgs {
   const int32_t *level;  // caller-fixed levels (manual batching) or nullptr
   fold_schedule_t s;  // output arrays (device pointers)
   SchedWs w;
+  int dbg;            // FOLD_DBG_SCHED: phase timeline
 };
 
 __device__ __forceinline__ int ld_volatile(const int32_t *p) { return *(volatile const int32_t *)p; }
@@ -216,6 +217,17 @@ __device__ __forceinline__ int dev_bits_for(int maxval) {  // #bits for values i
 // Grid-wide barrier (all blocks co-resident: cooperative launch). Release: every thread's
 // prior writes are fenced before the block arrives; acquire: the waiting thread's
 // ld.acquire also invalidates this SM's L1, so later plain loads see other blocks' writes.
+// Debug phase timeline (FOLD_DBG_SCHED=1): block 0 stamps %globaltimer at each phase start
+// (read back with fold_debug_sched_trace; instrumentation only).
+__device__ unsigned long long g_sched_trace[16];
+__device__ __forceinline__ void sched_stamp(int dbg, int ph) {
+  if (dbg && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_sched_trace[ph] = t;
+  }
+}
+
 __device__ void gsync(int32_t *flags) {
   __syncthreads();
   // one block: __syncthreads orders the block's global writes; data updated by atomics is
@@ -406,12 +418,14 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
   const int tid = threadIdx.x, T = blockDim.x;
   const int64_t gtid = (int64_t)blockIdx.x * T + tid, gstride = (int64_t)gridDim.x * T;
 
+  sched_stamp(a.dbg, 0);
   // ---- P0: flags (barrier slots were zeroed by the host), counters
   if (blockIdx.x == 0 && tid < F_NFLAGS && (tid < F_BAR || tid > F_BAR + 1))
     flags[tid] = tid < E_NCLASS ? INT_MAX : 0;
   for (int64_t i = gtid; i <= N; i += gstride) { w.ncons[i] = 0; w.fillc[i] = 0; }
   gsync(flags);
 
+  sched_stamp(a.dbg, 1);
   // ---- P1: validate (classes in order CHILD_RANGE, OP_RANGE, ARITY, TOKEN_RANGE,
   // ROOT_RANGE; smallest offending id), consumer counts, pending child counts
   for (int64_t i = gtid; i < N; i += gstride) {
@@ -444,9 +458,11 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
   gsync(flags);
   if (any_input_error(flags)) return;  // uniform: every block reads the same flags
 
+  sched_stamp(a.dbg, 2);
   // ---- P2: parent-list offsets
   grid_excl_scan(w.ncons, w.pcons_off, N + 1, nullptr, w, sw);
 
+  sched_stamp(a.dbg, 3);
   // ---- P3: parent lists (unordered within a node), initial frontier = EMBED nodes (depth 1)
   {
     const int64_t nloop = cdiv(N, gstride) * gstride;
@@ -471,6 +487,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
   }
   gsync(flags);
 
+  sched_stamp(a.dbg, 4);
   // ---- P4: level-synchronous depth propagation: a parent whose last
   // pending child finishes at level L gets depth L + 1; one barrier per level.
   // One block (small batches; deep chains are the latency-bound case): the pending counts
@@ -534,6 +551,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
   const int D = a.level ? ld_volatile(&flags[F_MAXDEPTH]) : L - 1;
   if (gtid == 0 && !a.level) flags[F_MAXDEPTH] = D;
 
+  sched_stamp(a.dbg, 5);
   // ---- P5: sort keys (cycle: a node never reached keeps depth -1)
   for (int64_t i = gtid; i < N; i += gstride) {
     const int n = (int)i, d = s.depth[n];
@@ -544,12 +562,14 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
   gsync(flags);
   if (ld_volatile(&flags[F_ERR0 + E_CYCLE]) != INT_MAX) return;
 
+  sched_stamp(a.dbg, 6);
   // ---- P6: stable sort by key = 2 depth + op (L42-43); ties keep ascending node id
   const int nk = 2 * (D + 1);
   const uint32_t *sk;
   const int32_t *sv;
   sort_pairs(w, N, dev_bits_for(nk - 1), sk, sv, dsm);
 
+  sched_stamp(a.dbg, 7);
   // ---- P7: perm / rank, group and level offsets (binary search over the sorted keys)
   for (int64_t i = gtid; i < N; i += gstride) {
     const int n = sv[i];
@@ -567,6 +587,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
   }
   gsync(flags);
 
+  sched_stamp(a.dbg, 8);
   // ---- P8: gather vectors (L44: the indices encode the topology)
   for (int64_t r = gtid; r < N; r += gstride) {
     const int n = s.perm[r];
@@ -576,6 +597,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
   }
   gsync(flags);
 
+  sched_stamp(a.dbg, 9);
   // ---- P9: consumer CSR: cell edges e in [0, 2 n_cells), key = child row, stable
   const int nl = ld_volatile(&flags[F_NLEAVES]);
   const int ne = 2 * (N - nl);
@@ -607,6 +629,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
   gsync(flags);
   }
 
+  sched_stamp(a.dbg, 10);
   // ---- P10: leaves by (token, row) and token segments
   for (int64_t r = gtid; r < nl; r += gstride) {
     const int t = a.token[s.perm[r]];
@@ -626,6 +649,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
     if (w.seg_flag[i]) s.tok_seg[w.seg_scan[i]] = (int)i;
   if (gtid == 0) s.tok_seg[ld_volatile(&flags[F_NSEG])] = nl;
 
+  sched_stamp(a.dbg, 11);
   // ---- P11: roots, and graph ids ordered by (root row, g)
   if (G > 0) {
     for (int64_t g = gtid; g < G; g += gstride) {
@@ -645,6 +669,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
       }
     }
   }
+  sched_stamp(a.dbg, 12);
 }
 
 }  // namespace
@@ -658,6 +683,10 @@ fold_status scan_exclusive(const int32_t *in, int32_t *out, int64_t n, int32_t *
   return excl_scan(in, out, n, sums, total, st);
 }
 int64_t scan_sums_count(int64_t n) { return cdiv(n < 1 ? 1 : n, kScanTile) + 2; }
+
+int debug_sched_trace(unsigned long long *host) {
+  return cudaMemcpyFromSymbol(host, g_sched_trace, 13 * 8) == cudaSuccess ? 13 : -1;
+}
 
 size_t schedule_workspace(int64_t N, int64_t G) { return sched_ws_layout(nullptr, N, G).bytes; }
 
@@ -724,7 +753,8 @@ fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr
     FOLD_CUDA_TRY(cudaFuncSetAttribute(k_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)launch_smem));
     smem_set = launch_smem;
   }
-  SchedArgs args{N, G, V, gr->op, gr->child, gr->token, gr->root, gr->level, *s, w};
+  static const int dbg = [] { const char *e = getenv("FOLD_DBG_SCHED"); return e ? atoi(e) : 0; }();
+  SchedArgs args{N, G, V, gr->op, gr->child, gr->token, gr->root, gr->level, *s, w, dbg};
   if (blocks == 1) {  // no grid barrier: a plain launch (cheaper than a cooperative one)
     k_schedule<<<1, kSchedThreads, launch_smem, st>>>(args);
   } else {

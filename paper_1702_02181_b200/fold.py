@@ -112,6 +112,8 @@ def load() -> ctypes.CDLL:
     L.fold_profile_read.argtypes = [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
     L.fold_debug_fwd_trace.argtypes = [vp, i32]
     L.fold_debug_fwd_trace.restype = i32
+    L.fold_debug_sched_trace.argtypes = [vp]
+    L.fold_debug_sched_trace.restype = i32
     _lib = L
     return L
 
@@ -119,7 +121,8 @@ def load() -> ctypes.CDLL:
 EXPORTED = ("fold_schedule_workspace", "fold_schedule", "fold_acts_layout", "fold_forward_workspace",
             "fold_forward", "fold_backward_workspace", "fold_backward", "fold_sgd_update",
             "fold_status_string", "fold_last_error_detail", "fold_abi_version", "fold_device_check",
-            "fold_launch_count", "fold_profile_enable", "fold_profile_read", "fold_debug_fwd_trace")
+            "fold_launch_count", "fold_profile_enable", "fold_profile_read", "fold_debug_fwd_trace",
+            "fold_debug_sched_trace")
 
 PROF_CLASSES = ("schedule", "embed_fwd", "cell_fwd", "bwd_pointwise", "gemm_dA", "gemm_dU", "embed_bwd",
                 "db_colsum", "sgd", "weight_prep", "root_out")
@@ -169,6 +172,36 @@ def launch_count(reset: bool = False) -> int:
 
 # ----------------------------------------------------------------------------- schedule
 
+class _LazyArrays(dict):
+    """Views of the schedule arrays inside one device buffer, created on first access
+    (`.buffer` is the allocation, e.g. for record_stream)."""
+
+    def __init__(self, buf: torch.Tensor, offs: dict):
+        super().__init__()
+        self.buffer = buf
+        self._offs = offs
+
+    def __missing__(self, k):
+        o, n = self._offs[k]
+        v = self.buffer[o:o + n]
+        self[k] = v
+        return v
+
+    def _all(self):
+        for k in self._offs:
+            self[k]
+        return self
+
+    def items(self):
+        return dict.items(self._all())
+
+    def values(self):
+        return dict.values(self._all())
+
+    def keys(self):
+        return self._offs.keys()
+
+
 @dataclasses.dataclass
 class Schedule:
     """Device arrays of the executor-form schedule (fold.h) + host scalars."""
@@ -214,14 +247,22 @@ def schedule(op: torch.Tensor, child: torch.Tensor, token: torch.Tensor, root: t
     sizes = {"depth": N, "perm": N, "rank": N, "gather": 2 * N, "level_off": N + 2, "group_off": 2 * N + 3,
              "cons_off": N + 1, "cons_edge": 2 * N, "leaf_perm": N, "tok_seg": N + 1, "root_row": G,
              "root_perm": G, "leaf_token": N}
-    arrays = {k: torch.empty(max(n, 1), dtype=torch.int32, device=dev) for k, n in sizes.items()}
+    # one device allocation for all schedule arrays (each 256-byte aligned): a dozen small
+    # torch allocations cost more host time than a small batch's whole schedule kernel
+    offs, o = {}, 0
+    for k, n in sizes.items():
+        offs[k] = (o, max(n, 1))
+        o += (max(n, 1) + 63) // 64 * 64
+    buf = torch.empty(o, dtype=torch.int32, device=dev)
+    arrays = _LazyArrays(buf, offs)
     host = np.zeros(N + 2, np.int32)
     ws_bytes = int(L.fold_schedule_workspace(N, G))
     if workspace is None or workspace.numel() < ws_bytes:
         workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     g = _Graphs(N, G, int(vocab), op.data_ptr(), child.data_ptr(), token.data_ptr(), root.data_ptr(),
                 level.data_ptr() if level is not None else None)
-    s = _Sched(*[arrays[k].data_ptr() for k in _SCHED_ARRAYS], host.ctypes.data, 0, 0, 0, 0, 0, 0, 0)
+    base = buf.data_ptr()
+    s = _Sched(*[base + 4 * offs[k][0] for k in _SCHED_ARRAYS], host.ctypes.data, 0, 0, 0, 0, 0, 0, 0)
     _check(L.fold_schedule(ctypes.byref(g), ctypes.byref(s), ctypes.c_void_p(workspace.data_ptr()),
                            ws_bytes, _stream(stream)), "fold_schedule")
     return Schedule(arrays, host, s.n_nodes, s.n_graphs, s.n_levels, s.n_leaves, s.n_cells, s.n_tok_segs,
