@@ -55,9 +55,9 @@ def parse():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--ref-trees", type=int, default=1, help="trees per oracle step (--impl reference)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the nodes/s vs batch-size sweep")
-    ap.add_argument("--pipeline", default="auto", choices=["auto", "on", "off"],
+    ap.add_argument("--pipeline", default="on", choices=["on", "off"],
                     help="run the next batch's fold_schedule on a side stream while the current batch executes "
-                         "(auto: for batches of at most %d nodes and 64 levels, where it measured faster)" % 131072)
+                         "(batches of more than 131072 nodes or 64 levels: after its level sweep)")
     ap.add_argument("--no-table1", action="store_true",
                     help="skip the unbatched baseline and the PAPER.md Table 1 reproduction")
     return ap.parse_args()
@@ -210,43 +210,74 @@ def run_fold(args):
     # and its one host sync no longer idles the GPU; batch k+1's forward waits on its event.
     # Every step still schedules its own batch (K schedules in K timed steps).
     side_stream = torch.cuda.Stream(device=dev) if args.pipeline != "off" else None
-    pipe_max_nodes = {"auto": 131072, "on": 1 << 62, "off": -1}[args.pipeline]
+    pipe_max_nodes = 131072
     side = None  # set per timed workload by use_pipeline()
 
+    gate = [None]  # event the next schedule waits for (None: start right away)
+
     def use_pipeline(n_nodes, n_levels):
-        # measured crossover: with a few hundred thousand nodes, or hundreds of
-        # levels (one grid barrier each), the scheduler's cooperative kernel running beside
-        # the previous batch's GEMMs costs more than it hides
+        # measured: small batches gain most when the next schedule starts right
+        # away; with a few hundred thousand nodes or hundreds of levels its cooperative kernel
+        # must not take SMs from the persistent level kernels (which own every SM), so it is
+        # gated on the previous batch's level sweep and overlaps only its weight-gradient GEMM
         nonlocal side
-        ok = n_nodes <= pipe_max_nodes and (n_levels <= 64 or args.pipeline == "on")
-        side = side_stream if ok else None
+        side = side_stream if args.pipeline != "off" else None
+        small = n_nodes <= pipe_max_nodes and n_levels <= 64
+        gate[0] = None if small else sweep_done
         return side is not None
 
-    def schedule_async(op, child, token, root, copies=(), level=None):
+    sweep_done = torch.cuda.Event()  # re-recorded by every fold_backward after its level sweep
+    # no allocation inside the timed loops: three rotating schedule buffers (a buffer is
+    # rewritten only after the step that read it has finished on the compute stream) and one
+    # root-state output
+    sbuf = [torch.empty(fold.schedule_buffer_len(N_nodes, gr.n_graphs), dtype=torch.int32, device=dev)
+            for _ in range(3)]
+    sbuf_free = [torch.cuda.Event() for _ in range(3)]
+    sbuf_used = [False] * 3
+    slot = [0]
+    h_root_buf = torch.empty((gr.n_graphs, S), dtype=torch.float32, device=dev)
+
+    def schedule_async(op, child, token, root, copies=(), level=None, after=None):
+        nonlocal h_root_buf
+        need = fold.schedule_buffer_len(op.shape[0], root.shape[0])
+        if sbuf[0].numel() < need:  # a larger workload (Table 1 / sweeps, outside timed loops)
+            torch.cuda.synchronize()
+            for k in range(3):
+                sbuf[k] = torch.empty(need, dtype=torch.int32, device=dev)
+        if h_root_buf.shape[0] < root.shape[0]:
+            torch.cuda.synchronize()
+            h_root_buf = torch.empty((root.shape[0], S), dtype=torch.float32, device=dev)
+        i = slot[0]
+        slot[0] = (i + 1) % 3
         if side is None:
             for d, h in copies:
                 d.copy_(h, non_blocking=True)
-            return fold.schedule(op, child, token, root, V, workspace=sched_ws, level=level), None
-        main = torch.cuda.current_stream()
+            return fold.schedule(op, child, token, root, V, workspace=sched_ws, level=level, out=sbuf[i]), None, i
         with torch.cuda.stream(side):
+            if sbuf_used[i]:
+                side.wait_event(sbuf_free[i])
+            if after is not None:  # start once the previous batch's level sweep is done, so the
+                side.wait_event(after)  # scheduler overlaps its weight-gradient GEMM, not the
+                # persistent level kernels (which own every SM)
             for d, h in copies:
                 d.copy_(h, non_blocking=True)
-            sc = fold.schedule(op, child, token, root, V, workspace=sched_ws, stream=side, level=level)
+            sc = fold.schedule(op, child, token, root, V, workspace=sched_ws, stream=side, level=level, out=sbuf[i])
             ev = torch.cuda.Event()
             ev.record(side)
-        sc.arrays.buffer.record_stream(main)
-        return sc, ev
+        return sc, ev, i
 
-    def run_step(sc, ev, g, train=True):
+    def run_step(sc, ev, i, g, train=True):
+        main = torch.cuda.current_stream()
         if ev is not None:
-            torch.cuda.current_stream().wait_event(ev)
-        h, c, acts = fold.forward(sc, model, ws=ws, want_c=False)
-        if not train:
-            return h
-        fold.backward(sc, model, acts, g, grads=(dU, db, dE), ws=ws)
-        if world > 1:
-            dist.all_reduce(flat_g)
-        fold.sgd_update(flat_p, flat_g, args.lr)
+            main.wait_event(ev)
+        h, c, acts = fold.forward(sc, model, ws=ws, want_c=False, h_root=h_root_buf[:sc.n_graphs])
+        if train:
+            fold.backward(sc, model, acts, g, grads=(dU, db, dE), ws=ws, sweep_done=sweep_done)
+            if world > 1:
+                dist.all_reduce(flat_g)
+            fold.sgd_update(flat_p, flat_g, args.lr)
+        sbuf_free[i].record(main)
+        sbuf_used[i] = True
         return h
 
     def time_steps(o, g, nrep, level=None, train=True, warm=3):
@@ -255,16 +286,17 @@ def run_fold(args):
         nlev = fold.schedule(*o, V, workspace=sched_ws, level=level).n_levels
         use_pipeline(int(o[0].shape[0]), nlev)
         sp = schedule_async(*o, level=level)
+        aft = gate[0] if train else None
         for _ in range(warm):
             run_step(*sp, g, train)
-            sp = schedule_async(*o, level=level)
+            sp = schedule_async(*o, level=level, after=aft)
         torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record()
         for _ in range(nrep):
             run_step(*sp, g, train)
-            sp = schedule_async(*o, level=level)
+            sp = schedule_async(*o, level=level, after=aft)
         if sp[1] is not None:
             torch.cuda.current_stream().wait_event(sp[1])
         b.record()
@@ -289,7 +321,7 @@ def run_fold(args):
     sp = schedule_async(op, child, token, root)
     for _ in range(max(args.warmup, 3)):
         run_step(*sp, g_dev)
-        sp = schedule_async(op, child, token, root)
+        sp = schedule_async(op, child, token, root, after=gate[0])
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local) if not args.no_clocks else None
@@ -309,7 +341,7 @@ def run_fold(args):
     marks[0].record()
     for i in range(args.steps):
         run_step(*sp, g_dev)
-        sp = schedule_async(op, child, token, root)  # the next batch's schedule (side stream)
+        sp = schedule_async(op, child, token, root, after=gate[0])  # the next batch's schedule (side stream)
         marks[i + 1].record()
     if sp[1] is not None:
         torch.cuda.current_stream().wait_event(sp[1])  # the K-th schedule inside the region
@@ -350,7 +382,7 @@ def run_fold(args):
             # next batch's graph arrays H2D + schedule on the side stream (pipelined)
             d_g.copy_(h_g, non_blocking=True)
             hr = run_step(*sp, d_g)
-            nxt = schedule_async(d_op, d_child, d_tok, d_root, copies=graph_copies)
+            nxt = schedule_async(d_op, d_child, d_tok, d_root, copies=graph_copies, after=gate[0])
             h_out.copy_(hr, non_blocking=True)
             return nxt
 
@@ -460,8 +492,9 @@ def run_fold(args):
                    "l2": "working set > L2 (pool+saved gates+grads ~%.1f GB); no flush" % (
                        (N_nodes * S * 6 + n_cells * gates * S * 4 + n_cells * S * 16) / 1e9),
                    "parallelism": f"dp{world}",
-                   "pipeline": "next batch's fold_schedule on a side stream during this batch's step"
-                   if pipelined else "off (policy %s)" % args.pipeline},
+                   "pipeline": ("next batch's fold_schedule on a side stream during this batch's step" +
+                                ("" if gate[0] is None else ", started after this batch's level sweep"))
+                   if pipelined else "off"},
         "gpu_launches": int(launches),
         "step_ms": {"median": float(np.median(step_ms)), "p10": float(np.percentile(step_ms, 10)),
                     "p90": float(np.percentile(step_ms, 90)), "rank0": [round(x, 4) for x in step_ms]},

@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define FOLD_ABI_VERSION 2
+#define FOLD_ABI_VERSION 3
 
 typedef enum {
   FOLD_OK = 0,
@@ -216,6 +216,11 @@ fold_status fold_forward(const fold_schedule_t *sched, const fold_model *model,
 typedef struct {
   float *dU, *db, *dE;
   int32_t accumulate;
+  /* OPTIONAL (NULL = none): a cudaEvent_t recorded on the stream once the level sweep (the
+   * dA GEMMs and pointwise steps) is enqueued, before the weight-gradient GEMM and the
+   * embedding / bias reductions -- a caller may start independent work (e.g. the next
+   * batch's fold_schedule on another stream) that overlaps them. */
+  void *sweep_done_event;
 } fold_grads;
 
 size_t fold_backward_workspace(const fold_schedule_t *sched, const fold_model *model);

@@ -307,6 +307,7 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
   // The embedding gradient and db only need dA / dZ, the weight-gradient GEMM only dZ and
   // the A planes: run the two memory-bound reductions on an auxiliary stream beside the
   // tensor-bound dU GEMM, then join.
+  if (grads->sweep_done_event) FOLD_CUDA_TRY(cudaEventRecord((cudaEvent_t)grads->sweep_done_event, st));
   // FOLD_AUX_ORDER (experiments): 0 = reductions on the aux stream launched before the
   // GEMM (default), 1 = after it, 2 = everything serial on the caller's stream
   static const int aux_order = [] { const char *e = getenv("FOLD_AUX_ORDER"); return e ? atoi(e) : 0; }();

@@ -63,7 +63,7 @@ class _ActsLayout(ctypes.Structure):
 
 class _Grads(ctypes.Structure):
     _fields_ = [("dU", ctypes.c_void_p), ("db", ctypes.c_void_p), ("dE", ctypes.c_void_p),
-                ("accumulate", ctypes.c_int32)]
+                ("accumulate", ctypes.c_int32), ("sweep_done_event", ctypes.c_void_p)]
 
 
 _lib = None
@@ -235,25 +235,42 @@ class Schedule:
         return out
 
 
+def _schedule_layout(N: int, G: int):
+    sizes = {"depth": N, "perm": N, "rank": N, "gather": 2 * N, "level_off": N + 2, "group_off": 2 * N + 3,
+             "cons_off": N + 1, "cons_edge": 2 * N, "leaf_perm": N, "tok_seg": N + 1, "root_row": G,
+             "root_perm": G, "leaf_token": N}
+    offs, o = {}, 0
+    for k, n in sizes.items():  # each array 256-byte aligned
+        offs[k] = (o, max(n, 1))
+        o += (max(n, 1) + 63) // 64 * 64
+    return offs, o
+
+
+def schedule_buffer_len(n_nodes: int, n_graphs: int) -> int:
+    """int32 elements of the device buffer `schedule(..., out=)` needs."""
+    return _schedule_layout(int(n_nodes), int(n_graphs))[1]
+
+
 def schedule(op: torch.Tensor, child: torch.Tensor, token: torch.Tensor, root: torch.Tensor, vocab: int,
-             stream=None, workspace: torch.Tensor | None = None, level: torch.Tensor | None = None) -> Schedule:
+             stream=None, workspace: torch.Tensor | None = None, level: torch.Tensor | None = None,
+             out: torch.Tensor | None = None) -> Schedule:
     """fold_schedule over int32 device tensors op[N], child[N,2], token[N], root[G];
-    `level` = optional caller-fixed levels [N] (manual batching, fold.h fold_graphs.level)."""
+    `level` = optional caller-fixed levels [N] (manual batching, fold.h fold_graphs.level);
+    `out` = optional int32 device buffer of schedule_buffer_len(N, G) elements for the
+    schedule arrays (else one is allocated)."""
     L = load()
     dev = op.device
     N, G = int(op.shape[0]), int(root.shape[0])
     for t in (op, child, token, root) + ((level,) if level is not None else ()):
         assert t.dtype == torch.int32 and t.is_cuda and t.is_contiguous()
-    sizes = {"depth": N, "perm": N, "rank": N, "gather": 2 * N, "level_off": N + 2, "group_off": 2 * N + 3,
-             "cons_off": N + 1, "cons_edge": 2 * N, "leaf_perm": N, "tok_seg": N + 1, "root_row": G,
-             "root_perm": G, "leaf_token": N}
-    # one device allocation for all schedule arrays (each 256-byte aligned): a dozen small
-    # torch allocations cost more host time than a small batch's whole schedule kernel
-    offs, o = {}, 0
-    for k, n in sizes.items():
-        offs[k] = (o, max(n, 1))
-        o += (max(n, 1) + 63) // 64 * 64
-    buf = torch.empty(o, dtype=torch.int32, device=dev)
+    # one device buffer for all schedule arrays: a dozen small torch allocations cost more host
+    # time than a small batch's whole schedule kernel
+    offs, o = _schedule_layout(N, G)
+    if out is not None:
+        assert out.dtype == torch.int32 and out.is_cuda and out.numel() >= o
+        buf = out
+    else:
+        buf = torch.empty(o, dtype=torch.int32, device=dev)
     arrays = _LazyArrays(buf, offs)
     host = np.zeros(N + 2, np.int32)
     ws_bytes = int(L.fold_schedule_workspace(N, G))
@@ -321,7 +338,7 @@ class Workspace:
 
 
 def forward(sched: Schedule, model: Model, stream=None, ws: Workspace | None = None,
-            want_c: bool = True):
+            want_c: bool = True, h_root: torch.Tensor | None = None):
     L = load()
     dev = model.E.device
     ms = model.struct()
@@ -332,7 +349,9 @@ def forward(sched: Schedule, model: Model, stream=None, ws: Workspace | None = N
     fws = int(L.fold_forward_workspace(ctypes.byref(sched.struct()), ctypes.byref(ms)))
     fbuf = ws.get("fwd", fws)
     S, G = model.S, sched.n_graphs
-    h_root = torch.empty((G, S), dtype=torch.float32, device=dev)
+    if h_root is None:
+        h_root = torch.empty((G, S), dtype=torch.float32, device=dev)
+    assert h_root.dtype == torch.float32 and h_root.is_contiguous() and h_root.numel() >= G * S
     c_root = torch.empty((G, S), dtype=torch.float32, device=dev) if want_c else None
     _check(L.fold_forward(ctypes.byref(sched.struct()), ctypes.byref(ms), ctypes.c_void_p(acts_buf.data_ptr()),
                           _ptr(h_root), _ptr(c_root), ctypes.c_void_p(fbuf.data_ptr()), fws, _stream(stream)),
@@ -341,14 +360,21 @@ def forward(sched: Schedule, model: Model, stream=None, ws: Workspace | None = N
 
 
 def backward(sched: Schedule, model: Model, acts: Acts, dh_root: torch.Tensor, dc_root: torch.Tensor | None = None,
-             grads=None, accumulate: bool = False, stream=None, ws: Workspace | None = None):
+             grads=None, accumulate: bool = False, stream=None, ws: Workspace | None = None,
+             sweep_done: torch.cuda.Event | None = None):
+    """fold_backward; `sweep_done` (optional torch.cuda.Event) is recorded once the level sweep
+    is enqueued, before the weight-gradient GEMM (fold.h fold_grads.sweep_done_event)."""
     L = load()
     dev = model.E.device
     ms = model.struct()
     if grads is None:
         grads = (torch.empty_like(model.U), torch.empty_like(model.b), torch.empty_like(model.E))
     dU, db, dE = grads
-    gs = _Grads(dU.data_ptr(), db.data_ptr(), dE.data_ptr(), 1 if accumulate else 0)
+    ev = None
+    if sweep_done is not None:
+        sweep_done.record(torch.cuda.current_stream() if stream is None else stream)  # materialise the event
+        ev = sweep_done.cuda_event
+    gs = _Grads(dU.data_ptr(), db.data_ptr(), dE.data_ptr(), 1 if accumulate else 0, ev)
     ws = ws or Workspace(dev)
     bws = int(L.fold_backward_workspace(ctypes.byref(sched.struct()), ctypes.byref(ms)))
     bbuf = ws.get("bwd", bws)
