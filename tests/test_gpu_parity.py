@@ -199,3 +199,16 @@ def test_large_state_2048_bf16():
     gr = foldgen.batch_from_shapes(shapes, foldgen.uniform_tokens(rng, 40), 40)
     _check_fwd(gr, "treelstm", "bf16", 2048)
     _check_bwd(gr, "treelstm", "bf16", 2048)
+
+
+def test_very_deep_chain():
+    """A caterpillar 5000 levels deep (more levels than fold_schedule's level_off prefix copy
+    of 4096 entries, and than any tile counter window): schedule bit-exact, fwd/bwd parity."""
+    gr = foldgen.config_c4(2, vocab=64, leaves=5000)
+    ref = oracle.schedule(gr.op, gr.child, gr.token, gr.root, gr.vocab)
+    got, p = _run(gr, "treelstm", "bf16", 32)
+    assert got["sched"].n_levels == ref["n_levels"] == 5000
+    assert np.array_equal(got["sched"].to_numpy()["level_off"], ref["level_off"])
+    for prec in ("fp32", "bf16"):
+        _check_fwd(gr, "treelstm", prec, 32)
+        _check_bwd(gr, "treelstm", prec, 32)
