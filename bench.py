@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--pipeline", default="on", choices=["on", "off"],
                     help="run the next batch's fold_schedule on a side stream while the current batch executes "
                          "(batches of more than 131072 nodes or 64 levels: after its level sweep)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: testing the multi-rank path on one GPU)")
     ap.add_argument("--no-table1", action="store_true",
                     help="skip the unbatched baseline and the PAPER.md Table 1 reproduction")
     return ap.parse_args()
@@ -165,8 +167,12 @@ def run_fold(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(torch.cuda.device_count(), 1)  # (gloo test runs: several ranks per GPU)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     fold.device_check()
@@ -266,14 +272,14 @@ def run_fold(args):
             ev.record(side)
         return sc, ev, i
 
-    def run_step(sc, ev, i, g, train=True):
+    def run_step(sc, ev, i, g, train=True, collective=True):
         main = torch.cuda.current_stream()
         if ev is not None:
             main.wait_event(ev)
         h, c, acts = fold.forward(sc, model, ws=ws, want_c=False, h_root=h_root_buf[:sc.n_graphs])
         if train:
             fold.backward(sc, model, acts, g, grads=(dU, db, dE), ws=ws, sweep_done=sweep_done)
-            if world > 1:
+            if world > 1 and collective:
                 dist.all_reduce(flat_g)
             fold.sgd_update(flat_p, flat_g, args.lr)
         sbuf_free[i].record(main)
@@ -282,20 +288,21 @@ def run_fold(args):
 
     def time_steps(o, g, nrep, level=None, train=True, warm=3):
         """ms per step of nrep steps over the device graphs o (same step and pipelining
-        policy as the headline: schedule + forward [+ backward + SGD])."""
+        policy as the headline: schedule + forward [+ backward + SGD]). Rank 0 only (the
+        single-GPU context numbers): no collective, the other ranks wait at a barrier."""
         nlev = fold.schedule(*o, V, workspace=sched_ws, level=level).n_levels
         use_pipeline(int(o[0].shape[0]), nlev)
         sp = schedule_async(*o, level=level)
         aft = gate[0] if train else None
         for _ in range(warm):
-            run_step(*sp, g, train)
+            run_step(*sp, g, train, collective=False)
             sp = schedule_async(*o, level=level, after=aft)
         torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record()
         for _ in range(nrep):
-            run_step(*sp, g, train)
+            run_step(*sp, g, train, collective=False)
             sp = schedule_async(*o, level=level, after=aft)
         if sp[1] is not None:
             torch.cuda.current_stream().wait_event(sp[1])
