@@ -174,9 +174,9 @@ typedef struct {
 /* ----------------------------------------------------------------- activations
  * One caller-owned device buffer holding everything the forward saves for the
  * backward (the pool of PAPER.md L47's loop state for every depth):
- *   H [N][ld] bf16 (BF16) or fp32 (FP32)  hidden state h per pool row (BF16: written for
- *                                         leaf rows and for rows without consumers; a
- *                                         consumed cell's h lives in its consumers' A rows)
+ *   H [N][ld] bf16 (BF16) or fp32 (FP32)  hidden state h per pool row (BF16: written only
+ *                                         for rows without consumers; a consumed row's h
+ *                                         lives in its consumers' A rows)
  *   C [N][ld] fp32                        cell state c per pool row (0 for TreeRNN; leaf
  *                                         rows are c = 0 by definition and are not
  *                                         materialised in BF16 mode)

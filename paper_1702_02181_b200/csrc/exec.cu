@@ -42,7 +42,9 @@ __global__ void k_embed_fwd(int r0, int r1, const int32_t *__restrict__ leaf_tok
           uint2 pk;
           pk.x = *reinterpret_cast<uint32_t *>(&a);
           pk.y = *reinterpret_cast<uint32_t *>(&b2);
-          *reinterpret_cast<uint2 *>(h + j) = pk;
+          // BF16: the pool row only for leaves nobody consumes (roots); consumers read the
+          // pushed copy in their A rows
+          if (e1 == e0) *reinterpret_cast<uint2 *>(h + j) = pk;
           for (int q = e0; q < e1; q++) {
             int ed = sc.cons_edge[q];
             __nv_bfloat16 *dst = ((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld + j;
@@ -56,7 +58,7 @@ __global__ void k_embed_fwd(int r0, int r1, const int32_t *__restrict__ leaf_tok
     } else {
       for (int j = lane; j < S; j += 32) {
         T hv = from_f<T>(e[j]);
-        h[j] = hv;
+        if (sizeof(T) == 4 || e1 == e0) h[j] = hv;
         if (!has_sc) c[j] = 0.f;
         if constexpr (sizeof(T) == 2) {
           for (int q = e0; q < e1; q++) {
@@ -175,7 +177,7 @@ __global__ void k_root_out(int G, int S, int ld, int nl, const int32_t *__restri
     int64_t g = i / S, j = i - g * S;
     int64_t r = root_row[g];
     const T *src = H + r * ld;
-    if (has_sc && r >= nl && sc.cons_off[r + 1] > sc.cons_off[r]) {
+    if (has_sc && sc.cons_off[r + 1] > sc.cons_off[r]) {  // consumed (leaf or cell): its pushed copy
       int ed = sc.cons_edge[sc.cons_off[r]];
       src = reinterpret_cast<const T *>(((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld);
     }
