@@ -40,6 +40,7 @@
  *   FOLD_AUX_ORDER        0: embedding / db reductions on an auxiliary stream beside the
  *                         weight-gradient GEMM (default), 1: launched after it, 2: serial
  *   FOLD_DBG_FWD          1/2: per-tile forward timelines (fold_debug_fwd_trace)
+ *   FOLD_DBG_BWD          1: per-tile timelines of the wide backward (fold_debug_bwd_trace)
  *   FOLD_DBG_SCHED        1: scheduler phase timeline (fold_debug_sched_trace)
  *   FOLD_DEBUG_SYNC       1: synchronize and check after every launch
  */
@@ -265,6 +266,14 @@ fold_status fold_profile_read(int32_t n_classes, double *ms, int64_t *launches);
  * the kernel's order: levels ascending, row tile, column tile); returns the count, or -1
  * on a CUDA error. */
 int32_t fold_debug_fwd_trace(unsigned long long *host, int32_t n_tiles);
+/* Instrumentation: with FOLD_DBG_BWD=1 the wide backward kernel (k_bwd_levels) records
+ * %globaltimer (ns) per pair tile at six points: 0 producer starts the tile, 1 its inputs
+ * (dZ rows, dCe) are published, 2 its accumulator is free, 3 its last MMA is issued, 4 the
+ * accumulator is ready in the epilogue, 5 the epilogue has published. Tiles in the kernel's
+ * order (levels descending from the first wide level, row tile, column tile). Copies the
+ * first n_tiles stamps of each point into host[6][n_tiles]; returns the count, or -1 on a
+ * CUDA error. */
+int32_t fold_debug_bwd_trace(unsigned long long *host, int32_t n_tiles);
 /* Instrumentation: with FOLD_DBG_SCHED=1, fold_schedule's block 0 stamps %globaltimer (ns)
  * at the start of phases P0..P11 and at its end; copies the 13 stamps into host[13] and
  * returns 13 (-1 on a CUDA error). */

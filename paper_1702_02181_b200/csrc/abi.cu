@@ -384,6 +384,11 @@ int32_t fold_debug_fwd_trace(unsigned long long *host, int32_t n_tiles) {
   return fold::tc_debug_fwd_trace(host, n_tiles);
 }
 
+/* instrumentation: per-tile timeline of the wide backward kernel in the last FOLD_DBG_BWD=1 run */
+int32_t fold_debug_bwd_trace(unsigned long long *host, int32_t n_tiles) {
+  return fold::tc_debug_bwd_trace(host, n_tiles);
+}
+
 fold_status fold_device_check(void) {
   int dev = 0, major = 0, minor = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return FOLD_E_CUDA;

@@ -80,6 +80,7 @@ fold_status launch_zero(void *p, size_t bytes, cudaStream_t st);
 // gate-interleaved in 8-column blocks for the forward (K-major B operand, one TMA box).
 int tc_ld_u(int S);
 int tc_debug_fwd_trace(unsigned long long *host, int n);
+int tc_debug_bwd_trace(unsigned long long *host, int n);
 size_t tc_ut_bytes(int gates, int S);
 size_t tc_weights_bytes(int gates, int S);
 fold_status tc_prepare_U(int gates, int S, const float *U, __nv_bfloat16 *Ub, cudaStream_t st);

@@ -45,6 +45,15 @@ __device__ __forceinline__ void trace(int dbg, int pt, int T) {
     g_fwd_trace[pt][T] = t;
   }
 }
+// FOLD_DBG_BWD=1: the same for k_bwd_levels at six points (see fold_debug_bwd_trace)
+__device__ unsigned long long g_bwd_trace[6][kTraceTiles];
+__device__ __forceinline__ void btrace(int dbg, int pt, int T) {
+  if (dbg && T < kTraceTiles) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_bwd_trace[pt][T] = t;
+  }
+}
 
 constexpr int BM = 128;     // rows per CTA (the pair's MMA has M = 256)
 constexpr int PM = 2 * BM;  // rows per CTA pair
@@ -1082,7 +1091,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
                  int KB, int total_tiles, const int32_t *__restrict__ gather,
                  const __nv_bfloat16 *__restrict__ Gact, int ld_g, const float *__restrict__ C, int ld, float *dA,
                  float *dCe, __nv_bfloat16 *dZ, int ld_z, int *rt_cnt, const int32_t *__restrict__ tstart,
-                 int slabs) {
+                 int slabs, int dbg) {
   constexpr int ST = BW_ST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
@@ -1130,8 +1139,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         // kps k-blocks per stage
         const int kps = bwd_kps(N, bx0), abox = bx0 * 128, ubox = (N / 128) * MN_CHUNK;
         const int nst = (KB + kps - 1) / kps;
+        if (rank == 0) btrace(dbg, 0, T);
         const bool ready = ptx::ld_acquire_gpu(rt_cnt + ct) >= rows * slabs;
         if (ready) ptx::fence_proxy_async_global();
+        if (ready && rank == 0) btrace(dbg, 1, T);
         const int pre = ready ? 0 : (nst < ST ? nst : ST);
         if (ready && kps == 1) {  // inputs published: one (A, U) box set per stage
           for (int kb = 0; kb < KB; kb++, it++) {
@@ -1163,6 +1174,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
             // this pair tile's dZ rows (and their dCe) complete
             ptx::wait_counter(rt_cnt + ct, rows * slabs);
             ptx::fence_proxy_async_global();
+            if (rank == 0) btrace(dbg, 1, T);
             if (bx)
               for (int q2 = 0; q2 < pre; q2++) {
                 const int s2 = (it + q2) % ST;
@@ -1188,6 +1200,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         const int acc = tc & 1;
         ptx::mbar_wait(&tempty[acc], ((tc >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
+        btrace(dbg, 2, T);
         const uint32_t dst = tbase + acc * 256;
         const int ct = (cur.r0 - nl) + ((T - cur.t0) / cur.NTn) * PM;
         const int rows0 = min(BM, cur.r1 - nl - ct);
@@ -1208,6 +1221,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
             ptx::umma_commit_2cta(&empty[s]);
           }
           ptx::umma_commit_2cta(&tfull[acc]);
+          btrace(dbg, 3, T);
           continue;
         }
         for (int q = 0; q < nst; q++, it++) {
@@ -1226,6 +1240,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
           ptx::umma_commit_2cta(&empty[s]);
         }
         ptx::umma_commit_2cta(&tfull[acc]);
+        btrace(dbg, 3, T);
       }
     }
   } else if (warp >= 4) {
@@ -1262,9 +1277,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
           }
         }
       }
+      // warm L2 with this warp's pointwise operands (the child's gates and c, its children's
+      // c, dCe) while the tile's MMAs run: on latency-bound levels (chains) the epilogue's
+      // HBM round trips are otherwise on every level's critical path (only on levels that
+      // fit one wave of tiles: on wide levels the epilogue overlaps the next tile anyway)
+      if (my_valid && cur.nt <= npairs) {
+#pragma unroll 1
+        for (int slab = grp; slab < N / 64; slab += 2) {
+          const int np = n0 + slab * 64;
+          const int half = np >= Sp;
+          const int col = np - half * Sp;
+          const int x = my_x[half];
+          if (col >= S || x < nl) continue;
+          const int last = min(64, S - col) - 1;
+          const __nv_bfloat16 *gx = Gact + (int64_t)(x - nl) * ld_g + col;
+#pragma unroll
+          for (int g = 0; g < GATES; g++) { ptx::prefetch_l2(gx + g * ld); ptx::prefetch_l2(gx + g * ld + last); }
+          if constexpr (GATES == 5) {
+            const int rows[3] = {x, my_xl[half], my_xr[half]};
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+              if (rows[k] < nl) continue;
+              const float *cx = C + (int64_t)rows[k] * ld + col;
+              ptx::prefetch_l2(cx); ptx::prefetch_l2(cx + last / 2); ptx::prefetch_l2(cx + last);
+            }
+            const float *dx = dCe + (2 * (int64_t)my_c + half) * S + col;
+            ptx::prefetch_l2(dx); ptx::prefetch_l2(dx + last / 2); ptx::prefetch_l2(dx + last);
+          }
+        }
+      }
       int slab_cnt[2] = {0, 0};  // columns this warp completes (its 64-column slabs), per half
       ptx::mbar_wait(&tfull[acc], (tc >> 1) & 1);
       ptx::tc_fence_after();
+      if (warp == 4 && lane == 0 && rank == 0) btrace(dbg, 4, T);
       const uint32_t tl = tbase + acc * 256 + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
       for (int slab = grp; slab < N / 64; slab += 2) {
@@ -1377,6 +1422,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
 #pragma unroll
       for (int h = 0; h < 2; h++)
         if (my_valid && my_ts[h] >= 0 && slab_cnt[h] > 0) atomicAdd(rt_cnt + my_ts[h], slab_cnt[h]);
+      if (warp == 4 && lane == 0 && rank == 0) btrace(dbg, 5, T);
     }
   }
   ptx::tc_fence_before();
@@ -1976,6 +2022,10 @@ int max_pairs(K kernel, int threads, int smem) {
   return n < num_sms() / 2 ? n : num_sms() / 2;
 }
 
+int dbg_bwd() {
+  static int v = [] { const char *e = getenv("FOLD_DBG_BWD"); return e ? atoi(e) : 0; }();
+  return v;
+}
 int dbg_fwd() {
   static int v = [] { const char *e = getenv("FOLD_DBG_FWD"); return e ? atoi(e) : 0; }();
   return v;
@@ -2104,6 +2154,15 @@ fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
 }  // namespace
 
 int tc_ld_u(int S) { return 2 * (int)round_up(S, BK); }
+
+int tc_debug_bwd_trace(unsigned long long *host, int n) {
+  if (n > kTraceTiles) n = kTraceTiles;
+  for (int p = 0; p < 6; p++)
+    if (cudaMemcpyFromSymbol(host + (size_t)p * n, g_bwd_trace, (size_t)n * 8, (size_t)p * kTraceTiles * 8) !=
+        cudaSuccess)
+      return -1;
+  return n;
+}
 
 int tc_debug_fwd_trace(unsigned long long *host, int n) {
   if (n > kTraceTiles) n = kTraceTiles;
@@ -2312,7 +2371,7 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
   const int npairs = total < npairs_max ? (int)total : npairs_max;
   kern<<<2 * npairs, BW_THREADS, BW_SMEM, st>>>(tmZ, tmZ16, tmZ64, tmU, L, (int)cdiv(gates * S, BK), (int)total, a.gather,
                                                a.Gact, a.ld_g, a.C, a.ld, a.dA, a.dCe, a.dZ, a.ld_z, a.rt_cnt,
-                                               a.tstart, tc_bwd_slabs(S));
+                                               a.tstart, tc_bwd_slabs(S), dbg_bwd());
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }

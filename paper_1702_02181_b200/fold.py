@@ -112,6 +112,8 @@ def load() -> ctypes.CDLL:
     L.fold_profile_read.argtypes = [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
     L.fold_debug_fwd_trace.argtypes = [vp, i32]
     L.fold_debug_fwd_trace.restype = i32
+    L.fold_debug_bwd_trace.argtypes = [vp, i32]
+    L.fold_debug_bwd_trace.restype = i32
     L.fold_debug_sched_trace.argtypes = [vp]
     L.fold_debug_sched_trace.restype = i32
     _lib = L
@@ -121,7 +123,7 @@ def load() -> ctypes.CDLL:
 EXPORTED = ("fold_schedule_workspace", "fold_schedule", "fold_acts_layout", "fold_forward_workspace",
             "fold_forward", "fold_backward_workspace", "fold_backward", "fold_sgd_update",
             "fold_status_string", "fold_last_error_detail", "fold_abi_version", "fold_device_check",
-            "fold_launch_count", "fold_profile_enable", "fold_profile_read", "fold_debug_fwd_trace",
+            "fold_launch_count", "fold_profile_enable", "fold_profile_read", "fold_debug_fwd_trace", "fold_debug_bwd_trace",
             "fold_debug_sched_trace")
 
 PROF_CLASSES = ("schedule", "embed_fwd", "cell_fwd", "bwd_pointwise", "gemm_dA", "gemm_dU", "embed_bwd",

@@ -1,0 +1,65 @@
+"""Per-level timeline of the wide backward kernel from the FOLD_DBG_BWD=1 tile stamps
+(fold_debug_bwd_trace).   FOLD_DBG_BWD=1 python tools/trace_bwd.py --config c4 --batch 1024"""
+import argparse, math, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import foldgen
+from paper_1702_02181_b200 import fold
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c4"); ap.add_argument("--batch", type=int, default=1024)
+ap.add_argument("--levels", type=int, default=12)
+ap.add_argument("--narrow-max", type=int, default=int(os.environ.get("FOLD_BWD_NARROW_MAX", "128")))
+a = ap.parse_args()
+assert os.environ.get("FOLD_DBG_BWD") == "1"
+gr = foldgen.make_config(a.config, a.batch)
+S = foldgen.CONFIG_STATE[a.config]
+p = foldgen.make_params("treelstm", S, gr.vocab)
+dev = "cuda"
+model = fold.Model(torch.tensor(p.U, device=dev), torch.tensor(p.b, device=dev), torch.tensor(p.E, device=dev))
+op, child, token, root = fold.graphs_to_device(gr)
+s = fold.schedule(op, child, token, root, gr.vocab)
+ws = fold.Workspace(dev)
+g = torch.rand((gr.n_graphs, S), device=dev) * 2 - 1
+for _ in range(3):
+    _, _, acts = fold.forward(s, model, ws=ws)
+    fold.backward(s, model, acts, g, ws=ws)
+torch.cuda.synchronize()
+n = 65536
+buf = np.zeros((6, n), np.uint64)
+got = fold.load().fold_debug_bwd_trace(buf.ctypes.data, n)
+lo = [int(x) for x in s.level_off_host[: s.n_levels + 2]]
+D = s.n_levels
+npairs = 74
+ld_u = 2 * math.ceil(S / 64) * 64
+d = D
+while d >= 2 and lo[d + 1] - lo[d] <= a.narrow_max:
+    d -= 1
+tiles = []
+for dd in range(d, 1, -1):
+    M = lo[dd + 1] - lo[dd]
+    mt = math.ceil(M / 256)
+    N = 128 if mt * math.ceil(ld_u / 256) < npairs else 256
+    tiles.append((dd, M, N, mt * math.ceil(ld_u / N)))
+ntot = min(got, sum(x[3] for x in tiles))
+t = buf[:, :ntot].astype(np.int64)
+t0 = t[0][t[0] > 0].min()
+x = (t - t0) / 1e3
+names = ["start", "inputs", "acc_free", "mma_done", "acc_ready", "published"]
+print(f"{a.config} B={a.batch}: wide levels {len(tiles)} (from d={d}), tiles {ntot}, span {x[5].max():.1f} us")
+print("medians (us): " + " ".join(f"{names[i]}->{names[j]}={np.median(x[j] - x[i]):.2f}"
+                                   for i, j in ((0, 1), (1, 3), (2, 3), (3, 4), (4, 5), (0, 5))))
+print("level     M    N tiles |  first_start  max_inputs  max_mma_done  max_acc_ready  max_pub | period")
+T0, prev = 0, 0.0
+rows = []
+for (dd, M, N, nt) in tiles:
+    if T0 + nt > ntot:
+        break
+    sl = slice(T0, T0 + nt)
+    r = (dd, M, N, nt, x[0][sl].min(), x[1][sl].max(), x[3][sl].max(), x[4][sl].max(), x[5][sl].max())
+    rows.append(r)
+    T0 += nt
+for i, r in enumerate(rows):
+    if i < a.levels or i >= len(rows) - 3:
+        print(f"{r[0]:5d} {r[1]:6d} {r[2]:4d} {r[3]:5d} | {r[4]:11.1f} {r[5]:11.1f} {r[6]:13.1f} {r[7]:14.1f} {r[8]:8.1f} | "
+              f"{r[8] - (rows[i - 1][8] if i else 0):6.1f}")
