@@ -34,7 +34,39 @@ __global__ void k_embed_fwd(int r0, int r1, const int32_t *__restrict__ leaf_tok
     float *c = C + r * ld;
     int e0 = 0, e1 = 0;
     if (has_sc) { e0 = sc.cons_off[r]; e1 = sc.cons_off[r + 1]; }
-    if ((S & 3) == 0) {
+    if (sizeof(T) == 2 && has_sc && (S & 3) == 0) {
+      // BF16 push path: the (usually one) consumer rows resolved once, four float4 loads in
+      // flight per lane before the stores
+      __nv_bfloat16 *d0 = nullptr;
+      if (e1 > e0) {
+        const int ed = sc.cons_edge[e0];
+        d0 = ((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld;
+      }
+      for (int jb = lane * 4; jb < S; jb += 512) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          if (jb + 128 * u < S) v[u] = *reinterpret_cast<const float4 *>(e + jb + 128 * u);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int j = jb + 128 * u;
+          if (j >= S) break;
+          __nv_bfloat162 a = __floats2bfloat162_rn(v[u].x, v[u].y), b2 = __floats2bfloat162_rn(v[u].z, v[u].w);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t *>(&a);
+          pk.y = *reinterpret_cast<uint32_t *>(&b2);
+          // the pool row only for leaves nobody consumes (roots); consumers read the pushed
+          // copy in their A rows
+          if (e1 == e0) *reinterpret_cast<uint2 *>(h + j) = pk;
+          else *reinterpret_cast<uint2 *>(d0 + j) = pk;
+          for (int q = e0 + 1; q < e1; q++) {
+            const int ed = sc.cons_edge[q];
+            __nv_bfloat16 *dst = ((ed & 1) ? sc.AR : sc.AL) + (int64_t)(ed >> 1) * sc.ld + j;
+            *reinterpret_cast<uint2 *>(dst) = pk;
+          }
+        }
+      }
+    } else if ((S & 3) == 0) {
       for (int j = lane * 4; j < S; j += 128) {
         float4 v = *reinterpret_cast<const float4 *>(e + j);
         if constexpr (sizeof(T) == 2) {
@@ -607,9 +639,20 @@ __global__ void __launch_bounds__(128) k_embed_pieces_final(int S, int n_tok_seg
   }
 }
 
-__global__ void k_sgd(float *p, const float *g, int64_t n, float lr) {
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) p[i] -= lr * g[i];
+__global__ void k_sgd(float *p, const float *g, int64_t n, float lr, int v4) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t i0 = 0;
+  if (v4) {  // 16-byte aligned: float4 body, scalar tail
+    const int64_t n4 = n >> 2;
+    for (int64_t i = t; i < n4; i += stride) {
+      float4 a = reinterpret_cast<float4 *>(p)[i];
+      const float4 b = __ldcs(reinterpret_cast<const float4 *>(g) + i);
+      a.x -= lr * b.x; a.y -= lr * b.y; a.z -= lr * b.z; a.w -= lr * b.w;
+      reinterpret_cast<float4 *>(p)[i] = a;
+    }
+    i0 = n4 << 2;
+  }
+  for (int64_t i = i0 + t; i < n; i += stride) p[i] -= lr * g[i];
 }
 
 __global__ void k_zero(uint32_t *p, int64_t n) {
@@ -776,7 +819,8 @@ fold_status launch_embed_bwd_pieces(int S, int n_leaves, int n_tok_segs, const i
 
 fold_status launch_sgd(float *p, const float *g, int64_t n, float lr, cudaStream_t st) {
   if (n <= 0) return FOLD_OK;
-  k_sgd<<<grid_cap(cdiv(n, 256)), 256, 0, st>>>(p, g, n, lr);
+  const int v4 = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g)) & 15) == 0;
+  k_sgd<<<grid_cap(cdiv(v4 ? cdiv(n, 4) : n, 256)), 256, 0, st>>>(p, g, n, lr, v4);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
