@@ -58,7 +58,10 @@ __device__ __forceinline__ void btrace(int dbg, int pt, int T) {
 constexpr int BM = 128;     // rows per CTA (the pair's MMA has M = 256)
 constexpr int PM = 2 * BM;  // rows per CTA pair
 constexpr int BK = 64;      // K elements per stage (128 B of bf16 = one swizzle row)
-constexpr int ST = 6;       // pipeline stages
+#ifndef FOLD_DU_ST
+#define FOLD_DU_ST 6
+#endif
+constexpr int ST = FOLD_DU_ST;  // pipeline stages (dA / dU GEMMs)
 constexpr int kThreads = 256;
 
 __device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
@@ -1390,7 +1393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
                 const float ig = u ? gg[0].y : gg[0].x, fl = u ? gg[1].y : gg[1].x;
                 const float fr = u ? gg[2].y : gg[2].x, og = u ? gg[3].y : gg[3].x;
                 const float ug = u ? gg[4].y : gg[4].x;
-                const float tcv = tanhf(ccv[u]);
+                const float tcv = tanh_fast(ccv[u]);
                 const float dO = dhv[u] * tcv;
                 const float dcc = dcv[u] + dhv[u] * og * (1.f - tcv * tcv);
                 zz[0][u] = dcc * ug * ig * (1.f - ig);
@@ -1704,7 +1707,7 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
           dz[0] = __float2bfloat16_rn(dh * (1.f - gg[h][0] * gg[h][0]));
         } else {
           const float ig = gg[h][0], fl = gg[h][1], fr = gg[h][2], og = gg[h][3], ug = gg[h][4];
-          const float tcv = tanhf(cc[h]);
+          const float tcv = tanh_fast(cc[h]);
           const float dO = dh * tcv;
           const float dcc = dc[h] + dh * og * (1.f - tcv * tcv);
           dz[0] = __float2bfloat16_rn(dcc * ug * ig * (1.f - ig));
