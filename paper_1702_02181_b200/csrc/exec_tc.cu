@@ -1336,7 +1336,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         if (np - half * Sp < S) slab_cnt[half] += min(64, S - (np - half * Sp));
         // rows in groups of R: all loads of the group first (memory-level parallelism),
         // then the math and the stores
-        constexpr int R = 6;
+        constexpr int R = 4;
 #pragma unroll 1
         for (int i0 = 0; i0 < 32 && c_row0 + i0 < c_end; i0 += R) {
           int xs_[R], xls[R], xrs[R];
