@@ -2380,13 +2380,22 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
 }
 
 int tc_dU_splits(int n_cells, int gates, int S) {
-  int64_t tiles = 2 * 2 * cdiv(S, DU_N) * cdiv((int64_t)gates * S, PM);  // CTAs per split
-  int64_t kbs = cdiv(n_cells, BK);
-  int64_t want = cdiv(4 * 148, tiles);           // >= ~4 waves of CTAs in total
-  int64_t cap = kbs / 32;                         // keep >= 32 k-blocks (2048 cells) per split
-  int64_t sp = want < cap ? want : cap;
-  if (sp > 16) sp = 16;
-  return sp < 1 ? 1 : (int)sp;
+  // split-K count minimising (waves of CTA pairs) x (k-blocks per split) + the partial
+  // slabs' round trip: one CTA pair per SM pair, ~0.27 us per k-block of a pair tile at
+  // S = 1024 (scaled by the tile count below), ~14 us per extra 42 MB partial at S = 1024
+  // (C2 B=1024: 2 splits ran 4.3 waves, the last one third full; 6 splits run 13.0)
+  const int64_t pairs = 2 * cdiv(S, DU_N) * cdiv((int64_t)gates * S, PM);  // CTA pairs per split
+  const int64_t per_wave = num_sms() / 2;
+  const int64_t kbs = cdiv(n_cells, BK);
+  const int64_t cap = kbs / 32;  // keep >= 32 k-blocks (2048 cells) per split
+  const double part = 14.0 * ((double)gates * S * 2 * S) / (5.0 * 1024 * 2048) / 0.27;  // in k-block units
+  int64_t best = 1;
+  double best_t = 1e300;
+  for (int64_t sp = 1; sp <= 16 && (sp == 1 || sp <= cap); sp++) {
+    const double t = (double)cdiv(pairs * sp, per_wave) * (double)cdiv(kbs, sp) + (sp > 1 ? sp * part : 0.0);
+    if (t < best_t - 1e-9) { best_t = t; best = sp; }
+  }
+  return (int)best;
 }
 
 fold_status tc_gemm_dU(int n_cells, int S, int gates, const __nv_bfloat16 *dZ, int ld_z, const ScatterA &sc,
