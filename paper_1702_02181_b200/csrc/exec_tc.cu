@@ -1407,8 +1407,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
 #pragma unroll
               for (int g = 0; g < 5; g++)
                 *reinterpret_cast<__nv_bfloat162 *>(dz + g * S) = __floats2bfloat162_rn(zz[g][0], zz[g][1]);
-              *reinterpret_cast<float2 *>(dCe + (2 * xc) * S + col) = make_float2(el[0], el[1]);
-              *reinterpret_cast<float2 *>(dCe + (2 * xc + 1) * S + col) = make_float2(er[0], er[1]);
+              // dc into a leaf is dropped (its c is the constant 0): only cell grandchildren
+              if (xls[j] >= nl) *reinterpret_cast<float2 *>(dCe + (2 * xc) * S + col) = make_float2(el[0], el[1]);
+              if (xrs[j] >= nl) *reinterpret_cast<float2 *>(dCe + (2 * xc + 1) * S + col) = make_float2(er[0], er[1]);
             }
           }
         }
@@ -1636,6 +1637,7 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
       // was written by its row's own pointwise step, published with its dZ)
       int64_t x[2] = {-1, -1};
       float gg[2][GATES], cc[2] = {0.f, 0.f}, cl[2] = {0.f, 0.f}, cr[2] = {0.f, 0.f}, dc[2] = {0.f, 0.f};
+      bool gcl[2] = {false, false}, gcr[2] = {false, false};  // grandchildren that are cells
       bool waited = false;
 #pragma unroll
       for (int h = 0; h < 2; h++) {
@@ -1652,8 +1654,10 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
           if constexpr (GATES == 5) {
             const int64_t xl = __ldg(gather + 2 * xx), xr = __ldg(gather + 2 * xx + 1);
             cc[h] = __ldcg(C + xx * ld + j);
-            if (xl >= nl) cl[h] = __ldcg(C + xl * ld + j);
-            if (xr >= nl) cr[h] = __ldcg(C + xr * ld + j);
+            gcl[h] = xl >= nl;
+            gcr[h] = xr >= nl;
+            if (gcl[h]) cl[h] = __ldcg(C + xl * ld + j);
+            if (gcr[h]) cr[h] = __ldcg(C + xr * ld + j);
             if (!waited) {
               int key;
               const int target = tile_target(cu, key);
@@ -1715,8 +1719,8 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
           dz[2 * S] = __float2bfloat16_rn(dcc * cr[h] * fr * (1.f - fr));
           dz[3 * S] = __float2bfloat16_rn(dO * og * (1.f - og));
           dz[4 * S] = __float2bfloat16_rn(dcc * ig * (1.f - ug * ug));
-          dCe[(2 * xc) * S + j] = dcc * fl;
-          dCe[(2 * xc + 1) * S + j] = dcc * fr;
+          if (gcl[h]) dCe[(2 * xc) * S + j] = dcc * fl;  // (dc into a leaf is dropped)
+          if (gcr[h]) dCe[(2 * xc + 1) * S + j] = dcc * fr;
         }
       }
       ptx::fence_proxy_async_global();
