@@ -271,7 +271,8 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
     ProfScope ps(K_PREP, st);
     FOLD_TRY(tc_prepare_U(gates, S, m->U, b.Ub, st));
   }
-  if (bf16 && s->tree_like && (S & 1) == 0) {
+  const bool fused_tree = bf16 && s->tree_like && (S & 1) == 0;  // (leaf dA in bf16 on this path)
+  if (fused_tree) {
     // tree-like: roots' seeded pointwise step, then every level's dA GEMM with the
     // children's pointwise step fused into its epilogue (one persistent launch)
     TcBwdArgs ba{};
@@ -334,7 +335,8 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
   {
     ProfScope ps(K_EMBED_BWD, s2);
     FOLD_TRY(launch_embed_bwd_pieces(S, nl, s->n_tok_segs, s->tok_seg, s->leaf_perm, s->leaf_token, s->cons_off,
-                                     s->cons_edge, b.root_off, s->root_perm, dh_root, b.dA, grads->dE, b.emb, s2));
+                                     s->cons_edge, b.root_off, s->root_perm, dh_root, b.dA, fused_tree, grads->dE,
+                                     b.emb, s2));
   }
   {
     ProfScope ps(K_COLSUM, s2);

@@ -563,7 +563,7 @@ __global__ void k_embed_piece_cnt(int n_tok_segs, const int32_t *__restrict__ to
     cnt[s] = (int)cdiv(tok_seg[s + 1] - tok_seg[s], kEmbedPiece);
 }
 
-template <int VEC>
+template <int VEC, typename TA>
 __global__ void __launch_bounds__(128) k_embed_pieces(int S, int n_tok_segs, int n_pieces,
                                                       const int32_t *__restrict__ tok_seg,
                                                       const int32_t *__restrict__ piece_off,
@@ -573,9 +573,10 @@ __global__ void __launch_bounds__(128) k_embed_pieces(int S, int n_tok_segs, int
                                                       const int32_t *__restrict__ cons_edge,
                                                       const int32_t *__restrict__ root_off,
                                                       const int32_t *__restrict__ root_perm,
-                                                      const float *__restrict__ dh_root, const float *__restrict__ dA,
+                                                      const float *__restrict__ dh_root, const TA *__restrict__ dA,
                                                       float *__restrict__ dE, float *__restrict__ partial) {
   using IF = VecIO<float, VEC>;
+  using IA = VecIO<TA, VEC>;
   const int total = piece_off[n_tok_segs];  // n_pieces is only a host-side upper bound
   for (int64_t p = blockIdx.x; p < n_pieces && p < total; p += gridDim.x) {
     int lo = 0, hi = n_tok_segs;  // segment s with piece_off[s] <= p < piece_off[s+1]
@@ -603,7 +604,7 @@ __global__ void __launch_bounds__(128) k_embed_pieces(int S, int n_tok_segs, int
         }
         const int e1 = cons_off[r + 1];
         for (int e = cons_off[r]; e < e1; e++) {
-          IF::ld(dA + (int64_t)cons_edge[e] * S + j, t);
+          IA::ld(dA + (int64_t)cons_edge[e] * S + j, t);
 #pragma unroll
           for (int u = 0; u < VEC; u++) acc[u] += t[u];
         }
@@ -789,8 +790,8 @@ fold_status launch_embed_bwd(int S, int nl, int n_tok_segs, const int32_t *tok_s
 fold_status launch_embed_bwd_pieces(int S, int n_leaves, int n_tok_segs, const int32_t *tok_seg,
                                     const int32_t *leaf_perm, const int32_t *leaf_token, const int32_t *cons_off,
                                     const int32_t *cons_edge, const int32_t *root_off, const int32_t *root_perm,
-                                    const float *dh_root, const float *dA, float *dE, const EmbedBwdWs &w,
-                                    cudaStream_t st) {
+                                    const float *dh_root, const void *dA, bool dA_bf16, float *dE,
+                                    const EmbedBwdWs &w, cudaStream_t st) {
   (void)n_leaves;
   if (n_tok_segs <= 0) return FOLD_OK;
   k_embed_piece_cnt<<<grid_cap(cdiv(n_tok_segs, 256)), 256, 0, st>>>(n_tok_segs, tok_seg, w.piece_cnt);
@@ -802,10 +803,15 @@ fold_status launch_embed_bwd_pieces(int S, int n_leaves, int n_tok_segs, const i
   const int max_pieces = n_leaves / kEmbedPiece + n_tok_segs;
   const unsigned g = grid_cap(max_pieces);
   const bool v4 = (S & 3) == 0;
-#define EP_ARGS S, n_tok_segs, max_pieces, tok_seg, w.piece_off, leaf_perm, leaf_token, cons_off, cons_edge, \
-                root_off, root_perm, dh_root, dA, dE, w.partial
-  if (v4) k_embed_pieces<4><<<g, 128, 0, st>>>(EP_ARGS);
-  else k_embed_pieces<1><<<g, 128, 0, st>>>(EP_ARGS);
+#define EP_ARGS(T) S, n_tok_segs, max_pieces, tok_seg, w.piece_off, leaf_perm, leaf_token, cons_off, cons_edge, \
+                root_off, root_perm, dh_root, (const T *)dA, dE, w.partial
+  if (dA_bf16) {  // the fused tree backward stores leaf edges' dA in bf16
+    if (v4) k_embed_pieces<4, __nv_bfloat16><<<g, 128, 0, st>>>(EP_ARGS(__nv_bfloat16));
+    else k_embed_pieces<1, __nv_bfloat16><<<g, 128, 0, st>>>(EP_ARGS(__nv_bfloat16));
+  } else {
+    if (v4) k_embed_pieces<4, float><<<g, 128, 0, st>>>(EP_ARGS(float));
+    else k_embed_pieces<1, float><<<g, 128, 0, st>>>(EP_ARGS(float));
+  }
 #undef EP_ARGS
   FOLD_LAUNCH_CHECK();
   const unsigned g2 = grid_cap(n_tok_segs);

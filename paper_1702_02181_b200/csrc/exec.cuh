@@ -70,8 +70,8 @@ struct EmbedBwdWs {
 fold_status launch_embed_bwd_pieces(int S, int n_leaves, int n_tok_segs, const int32_t *tok_seg,
                                     const int32_t *leaf_perm, const int32_t *leaf_token, const int32_t *cons_off,
                                     const int32_t *cons_edge, const int32_t *root_off, const int32_t *root_perm,
-                                    const float *dh_root, const float *dA, float *dE, const EmbedBwdWs &w,
-                                    cudaStream_t st);
+                                    const float *dh_root, const void *dA, bool dA_bf16, float *dE,
+                                    const EmbedBwdWs &w, cudaStream_t st);
 fold_status launch_zero(void *p, size_t bytes, cudaStream_t st);
 
 // --- tcgen05 path (exec_tc.cu)

@@ -1371,8 +1371,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
           for (int j = 0; j < R; j++) {
             if (!ok[j]) continue;
             const int64_t e = 2 * (int64_t)(c_row0 + i0 + j) + half;
-            if (xs_[j] < nl) {  // leaf child: the embedding gradient reads dA
-              *reinterpret_cast<float2 *>(dA + e * S + col) = dh[j];
+            if (xs_[j] < nl) {  // leaf child: the embedding gradient reads dA (bf16 on this path)
+              *reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<__nv_bfloat16 *>(dA) + e * S + col) =
+                  __floats2bfloat162_rn(dh[j].x, dh[j].y);
               continue;
             }
             const int64_t xc = xs_[j] - nl;
@@ -1701,8 +1702,8 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
         for (int p = 0; p < NB_PARTS; p++) dh += red[p][c][n];
         const int64_t r = cu.r + n;
         const int64_t e = 2 * (r - nl) + half;
-        if (x[h] < nl) {
-          dA[e * S + j] = dh;  // leaf child: the embedding gradient reads dA
+        if (x[h] < nl) {  // leaf child: the embedding gradient reads dA (bf16 on this path)
+          reinterpret_cast<__nv_bfloat16 *>(dA)[e * S + j] = __float2bfloat16_rn(dh);
           continue;
         }
         const int64_t xc = x[h] - nl;
