@@ -325,7 +325,7 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
       FOLD_TRY(tc_gemm_dU(nc, S, gates, (const __nv_bfloat16 *)b.dZ, b.ld_z,
                           ScatterA{s->cons_off, s->cons_edge, (__nv_bfloat16 *)(a + L.al_off),
                                    (__nv_bfloat16 *)(a + L.ar_off), L.ld},
-                          grads->dU, acc, b.dU_split, st));
+                          grads->dU, acc, b.dU_split, grads->db, b.partial, st));  // (+ db, fused)
     else
       FOLD_TRY(launch_gemm_dU_simt(nc, nl, S, gates, (const float *)b.dZ, b.ld_z, s->gather, (const float *)H, L.ld,
                                    grads->dU, acc, st));
@@ -338,7 +338,7 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
                                      s->cons_edge, b.root_off, s->root_perm, dh_root, b.dA, fused_tree, grads->dE,
                                      b.emb, s2));
   }
-  {
+  if (!bf16) {  // (BF16: db is summed inside the dU GEMM from its dZ stage tiles)
     ProfScope ps(K_COLSUM, s2);
     FOLD_TRY(launch_colsum(bf16, nc, gates * S, b.dZ, b.ld_z, b.partial, b.nsplit, grads->db, acc, s2));
   }

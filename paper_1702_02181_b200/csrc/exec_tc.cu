@@ -1786,15 +1786,17 @@ constexpr int DU_N = 256;
 constexpr int DU_A_BYTES = BM * 128;         // 2 MN chunks x 64 K-rows x 128 B
 constexpr int DU_B_BYTES = (DU_N / 2) * 128; // 2 MN chunks x 64 K-rows x 128 B
 constexpr int DU_STAGE = DU_A_BYTES + DU_B_BYTES;
-constexpr int DU_SMEM = ST * DU_STAGE + 1024;
+constexpr int DU_DB_BYTES = 128 * 8 * 4;       // db: per-thread partial sums, reduced across k groups
+constexpr int DU_SMEM = ST * DU_STAGE + DU_DB_BYTES + 1024;
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_dU_tc(const __grid_constant__ CUtensorMap tmZ2, const __grid_constant__ CUtensorMap tmAL,
                  const __grid_constant__ CUtensorMap tmAR, int n_cells, int S, int Mg, int NT, int kb_per_split,
-                 float *__restrict__ out_base, int64_t split_stride, int accumulate) {
+                 float *__restrict__ out_base, int64_t split_stride, int accumulate, float *__restrict__ db_base,
+                 int db_accumulate) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
-  __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull;
+  __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull, dbfree[ST];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = ptx::cluster_ctarank();
@@ -1808,8 +1810,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int kb1 = min(KBall, kb0 + kb_per_split);
   const int KB = kb1 > kb0 ? kb1 - kb0 : 0;
   float *dU = out_base + (int64_t)blockIdx.z * split_stride;
+  // db = column sums of dZ: the first column tile's pair also sums the
+  // dZ^T stage tiles it streams anyway (each CTA's idle epilogue warps, for its own 128
+  // gate rows, after the MMA has consumed the stage and before it is refilled)
+  const bool is_db = db_base != nullptr && px == 0 && KB > 0;
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < ST; s++) { ptx::mbar_init(&full[s], 1); ptx::mbar_init(&empty[s], 1); }
+    for (int s = 0; s < ST; s++) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&dbfree[s], 4);  // the 4 epilogue warps
+    }
     ptx::mbar_init(&tfull, 1);
     ptx::fence_mbar_init();
     ptx::prefetch_tmap(&tmZ2);
@@ -1831,6 +1841,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int s = it % ST;
       uint32_t ph = (it / ST) & 1;
       ptx::mbar_wait(&empty[s], ph ^ 1);
+      if (is_db) ptx::mbar_wait(&dbfree[s], ph ^ 1);
       if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], 2 * DU_STAGE);
       uint8_t *A = smem + s * DU_STAGE;
       uint8_t *B = A + DU_A_BYTES;
@@ -1858,6 +1869,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const int q = warp & 3;
+    if (is_db) {
+      // thread t: 16-byte chunk bc of this CTA's 128 gate rows (box bc / 8, chunk bc % 8 =
+      // 8 rows) over cells 8 kg .. 8 kg + 7 of every k-block; a stage is read after the MMA
+      // has consumed it (empty) and released on dbfree before the producer refills it
+      const int t = tid - 128, bc = t & 15, kg = t >> 4;
+      float acc[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) acc[u] = 0.f;
+      for (int it = 0; it < KB; it++) {
+        const int s = it % ST;
+        ptx::mbar_wait(&empty[s], (it / ST) & 1);
+        const uint32_t base = (uint32_t)(s * DU_STAGE + (bc >> 3) * MN_CHUNK + kg * 8 * 128);
+#pragma unroll
+        for (int kk = 0; kk < 8; kk++) {
+          const uint32_t off = base + kk * 128 + ((((uint32_t)bc & 7) ^ (uint32_t)kk) << 4);
+          const uint4 a = *reinterpret_cast<const uint4 *>(smem + off);
+          const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&aw[u]));
+            acc[2 * u] += f.x;
+            acc[2 * u + 1] += f.y;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&dbfree[s]);
+      }
+      // reduce the 8 k groups (fixed order) and write this split's 128 gate rows
+      float *red = reinterpret_cast<float *>(smem + ST * DU_STAGE);
+#pragma unroll
+      for (int u = 0; u < 8; u++) red[t * 8 + u] = acc[u];
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      {
+        const int r = t, bcx = (r >> 6) * 8 + ((r >> 3) & 7), u = r & 7;
+        float v = 0.f;
+        for (int g = 0; g < 8; g++) v += red[(g * 16 + bcx) * 8 + u];
+        const int row = i0 + r;
+        if (row < Mg) {
+          float *dst = db_base + (int64_t)blockIdx.z * Mg + row;
+          *dst = db_accumulate ? *dst + v : v;
+        }
+      }
+    }
     if (KB > 0) ptx::mbar_wait(&tfull, 0);
     ptx::tc_fence_after();
     const int i = i0 + q * 32 + lane;
@@ -2404,7 +2458,7 @@ int tc_dU_splits(int n_cells, int gates, int S) {
 }
 
 fold_status tc_gemm_dU(int n_cells, int S, int gates, const __nv_bfloat16 *dZ, int ld_z, const ScatterA &sc,
-                       float *dU, int accumulate, float *split_ws, cudaStream_t st) {
+                       float *dU, int accumulate, float *split_ws, float *db, float *db_ws, cudaStream_t st) {
   CUtensorMap tmZ2, tmAL, tmAR;
   const uint64_t ncr = (uint64_t)(n_cells > 0 ? n_cells : 1);
   FOLD_TRY(make_map(&tmZ2, dZ, (uint64_t)gates * S, ncr, (uint64_t)ld_z * 2, 64, BK));
@@ -2417,19 +2471,29 @@ fold_status tc_gemm_dU(int n_cells, int S, int gates, const __nv_bfloat16 *dZ, i
   const int kbps = (int)cdiv(KBall, splits);
   dim3 grid((unsigned)(2 * 2 * NT), (unsigned)cdiv(gates * S, PM), (unsigned)splits);
   const int64_t n = (int64_t)gates * S * 2 * S;
+  // db (optional): straight into db with one split, else per-split partials in db_ws
+  if (db && splits > 1 && !db_ws) return FOLD_E_WORKSPACE;
+  float *dbo = db ? (splits == 1 ? db : db_ws) : nullptr;
+  const int dbacc = splits == 1 ? accumulate : 0;
   if (splits == 1) {
     k_gemm_dU_tc<<<grid, kThreads, DU_SMEM, st>>>(tmZ2, tmAL, tmAR, n_cells, S, gates * S, NT, kbps, dU, 0,
-                                                  accumulate);
+                                                  accumulate, dbo, dbacc);
     FOLD_LAUNCH_CHECK();
     return FOLD_OK;
   }
   if (!split_ws) return FOLD_E_WORKSPACE;
-  k_gemm_dU_tc<<<grid, kThreads, DU_SMEM, st>>>(tmZ2, tmAL, tmAR, n_cells, S, gates * S, NT, kbps, split_ws, n, 0);
+  k_gemm_dU_tc<<<grid, kThreads, DU_SMEM, st>>>(tmZ2, tmAL, tmAR, n_cells, S, gates * S, NT, kbps, split_ws, n, 0,
+                                                dbo, 0);
   FOLD_LAUNCH_CHECK();
   int64_t blocks = cdiv(cdiv(n, 4), 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
   k_reduce_splits<<<(unsigned)blocks, 256, 0, st>>>(n, splits, split_ws, dU, accumulate);
   FOLD_LAUNCH_CHECK();
+  if (db) {
+    const int64_t nb = (int64_t)gates * S;
+    k_reduce_splits<<<(unsigned)cdiv(cdiv(nb, 4), 256), 256, 0, st>>>(nb, splits, db_ws, db, accumulate);
+    FOLD_LAUNCH_CHECK();
+  }
   return FOLD_OK;
 }
 
