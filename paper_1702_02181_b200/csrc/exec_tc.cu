@@ -87,11 +87,22 @@ struct FwdLevels {
   const int32_t *lo;     // schedule level_off (device)
   int D, S, Ww, Wn;      // deepest level, state size, wide / narrow tile widths
   int narrow_below;      // a level whose wide tiling has fewer tiles than this uses Wn
+  int Wm, G, npairs;     // mid tile width, gates, CTA pairs of the launch
 };
 
 __host__ __device__ inline int fwd_level_W(const FwdLevels &L, int M) {
-  int mt = (int)cdiv(M, PM);
-  return (int64_t)mt * cdiv(L.S, L.Ww) < L.narrow_below ? L.Wn : L.Ww;
+  const int64_t mt = cdiv(M, PM);
+  if (mt * cdiv(L.S, L.Ww) < L.narrow_below) return L.Wn;
+  // wide levels: Ww unless the mid width fills the waves of CTA pairs better (a 1024-row
+  // level at S = 1024 is 88 W=48 tiles = two waves on 74 pairs, or 128 W=32 tiles in the
+  // same two waves of cheaper MMAs); per-MMA cost of an M=256 pair tile of N columns in
+  // 1/64 cycles: max(32 N, 4096 + 16 N) (tensor issue vs shared-memory operand bytes)
+  auto cost = [&](int W) {
+    const int64_t N = (int64_t)L.G * W, t = mt * cdiv(L.S, W);
+    const int64_t c = 32 * N > 4096 + 16 * N ? 32 * N : 4096 + 16 * N;
+    return cdiv(t, (int64_t)L.npairs) * c;
+  };
+  return cost(L.Wm) < cost(L.Ww) ? L.Wm : L.Ww;
 }
 
 // Walks the level table in tile order (each warp role keeps its own copy).
@@ -113,6 +124,7 @@ template <int GATES>
 struct FwdCfg {
   static constexpr int WMAX = GATES == 5 ? 48 : 128;   // wide tile: N = GATES * W <= 256
   static constexpr int WNAR = GATES == 5 ? 16 : 32;    // narrow tile (N/2 a multiple of 8 rows)
+  static constexpr int WMID = GATES == 5 ? 32 : 64;    // mid tile (wave filling on 1-2-wave levels)
   static constexpr int A_BYTES = BM * 128;
   static constexpr int B_BYTES = GATES * WMAX * 64;    // this CTA's half of the B rows
   static constexpr int STAGE = A_BYTES + B_BYTES;
@@ -132,6 +144,7 @@ struct FwdCfg {
   static constexpr int EPI_WARPS = 8;     // 2 per SM sub-partition: each owns half the columns
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static_assert(GATES * WMAX <= 256 && (GATES * WNAR) % 16 == 0 && (GATES * WNAR / 2) % 8 == 0, "UMMA N, M=256");
+  static_assert((GATES * WMID) % 16 == 0 && (GATES * WMID / 2) % 8 == 0, "UMMA N, M=256");
   static_assert(SMEM <= 227 * 1024, "smem");
 };
 
@@ -159,7 +172,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
                  const __grid_constant__ CUtensorMap tmAL64, const __grid_constant__ CUtensorMap tmAR64,
                  const __grid_constant__ CUtensorMap tmUw, const __grid_constant__ CUtensorMap tmUn,
                  const __grid_constant__ CUtensorMap tmGw, const __grid_constant__ CUtensorMap tmGn,
-                 const __grid_constant__ CUtensorMap tmCw, const __grid_constant__ CUtensorMap tmCn, FwdLevels L,
+                 const __grid_constant__ CUtensorMap tmUm, const __grid_constant__ CUtensorMap tmGm, FwdLevels L,
                  int total_tiles, int nl, int ld, const int32_t *__restrict__ gather, const float *__restrict__ bias,
                  __nv_bfloat16 *__restrict__ H, float *C, __nv_bfloat16 *__restrict__ Gact, int ld_g, ScatterA sc,
                  int *rt_cnt, const int32_t *__restrict__ tstart, int dbg) {
@@ -196,7 +209,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
     ptx::prefetch_tmap(&tmUw);
     ptx::prefetch_tmap(&tmUn);
     ptx::prefetch_tmap(&tmGw);
-    ptx::prefetch_tmap(&tmCw);
+    ptx::prefetch_tmap(&tmUm);
   }
   if (warp == 2) {
     ptx::tmem_alloc2(&tmem_base_sh, Cfg::TMEM_COLS);
@@ -230,7 +243,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         const CUtensorMap *mL = bx == 16 ? &tmAL16 : bx == 64 ? &tmAL64 : &tmAL;
         const CUtensorMap *mR = bx == 16 ? &tmAR16 : bx == 64 ? &tmAR64 : &tmAR;
         const int c0 = ct + (int)rank * BM, j0 = (lt % cur.NT) * W;
-        const CUtensorMap *tmU = W == Cfg::WMAX ? &tmUw : &tmUn;
+        const CUtensorMap *tmU = W == Cfg::WMAX ? &tmUw : W == Cfg::WMID ? &tmUm : &tmUn;
         if (rank == 0) trace(dbg, 0, T);
         // the leader's full barrier counts both CTAs' bytes: A rows of both + the B rows
         const uint32_t bytes = (uint32_t)(bx0 + bx1) * 128 + GATES * W * 128;
@@ -626,7 +639,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         const bool staged = j0 + W <= S && c_tile + BM <= cur.r1 - nl;
         ptx::mbar_wait(&epi_done, tc & 1);
         if (staged) {
-          const CUtensorMap *tG = W == Cfg::WMAX ? &tmGw : &tmGn;
+          const CUtensorMap *tG = W == Cfg::WMAX ? &tmGw : W == Cfg::WMID ? &tmGm : &tmGn;
 #pragma unroll
           for (int g = 0; g < GATES; g++) ptx::tma_store_2d(tG, gsm + g * BM * W * 2, g * ld + j0, (int)c_tile);
           ptx::bulk_commit();
@@ -2111,7 +2124,7 @@ template <int GATES>
 fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
   using Cfg = FwdCfg<GATES>;
   const int S = a.S, nc = a.n_cells;
-  CUtensorMap tmAL, tmAR, tmUw, tmUn, tmGw, tmGn, tmCw, tmCn;
+  CUtensorMap tmAL, tmAR, tmUw, tmUn, tmGw, tmGn, tmUm, tmGm;
   FOLD_TRY(make_map(&tmAL, a.sc.AL, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, BM));
   FOLD_TRY(make_map(&tmAR, a.sc.AR, (uint64_t)S, (uint64_t)nc, (uint64_t)a.sc.ld * 2, BK, BM));
   CUtensorMap tmAL16, tmAR16, tmAL64, tmAR64;  // narrow tiles: boxes of the rows they hold
@@ -2122,23 +2135,21 @@ fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
   const uint64_t il_rows = (uint64_t)cdiv(S, 8) * 8 * GATES;
   FOLD_TRY(make_map(&tmUw, a.Ub, (uint64_t)a.ld_u, il_rows, (uint64_t)a.ld_u * 2, BK, GATES * Cfg::WMAX / 2));
   FOLD_TRY(make_map(&tmUn, a.Ub, (uint64_t)a.ld_u, il_rows, (uint64_t)a.ld_u * 2, BK, GATES * Cfg::WNAR / 2));
+  FOLD_TRY(make_map(&tmUm, a.Ub, (uint64_t)a.ld_u, il_rows, (uint64_t)a.ld_u * 2, BK, GATES * Cfg::WMID / 2));
   // epilogue bulk stores: G [n_cells][GATES*S] bf16 and the pool's C [N][S] fp32, plain
   // (unswizzled) boxes of W columns x 128 rows
-  const uint64_t Nrows = (uint64_t)nc + a.nl;
   FOLD_TRY(make_map_ex(&tmGw, a.Gact, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (uint64_t)a.ld_g, (uint64_t)nc,
                        (uint64_t)a.ld_g * 2, Cfg::WMAX, BM, CU_TENSOR_MAP_SWIZZLE_NONE));
   FOLD_TRY(make_map_ex(&tmGn, a.Gact, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (uint64_t)a.ld_g, (uint64_t)nc,
                        (uint64_t)a.ld_g * 2, Cfg::WNAR, BM, CU_TENSOR_MAP_SWIZZLE_NONE));
-  FOLD_TRY(make_map_ex(&tmCw, a.C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (uint64_t)S, Nrows, (uint64_t)a.ld * 4,
-                       Cfg::WMAX, BM, CU_TENSOR_MAP_SWIZZLE_NONE));
-  FOLD_TRY(make_map_ex(&tmCn, a.C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (uint64_t)S, Nrows, (uint64_t)a.ld * 4,
-                       Cfg::WNAR, BM, CU_TENSOR_MAP_SWIZZLE_NONE));
+  FOLD_TRY(make_map_ex(&tmGm, a.Gact, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (uint64_t)a.ld_g, (uint64_t)nc,
+                       (uint64_t)a.ld_g * 2, Cfg::WMID, BM, CU_TENSOR_MAP_SWIZZLE_NONE));
   auto kern = k_fwd_levels<GATES>;
   const int smem_bytes = Cfg::SMEM;
   FOLD_TRY(set_smem(kern, smem_bytes));
   static thread_local int npairs_max = 0;
   if (!npairs_max) npairs_max = max_pairs(kern, Cfg::THREADS, smem_bytes);
-  FwdLevels L{a.level_off, a.D, S, Cfg::WMAX, Cfg::WNAR, npairs_max / 2};
+  FwdLevels L{a.level_off, a.D, S, Cfg::WMAX, Cfg::WNAR, npairs_max / 2, Cfg::WMID, GATES, npairs_max};
   // the narrow tail: levels d0..D all of at most narrow_max rows go to k_fwd_narrow
   const int d0 = fwd_narrow_start(a.level_off_host, a.D, S);
   int64_t total = 0;
@@ -2158,7 +2169,7 @@ fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
   if (total > 0) {
     const int npairs = total < npairs_max ? (int)total : npairs_max;
     kern<<<2 * npairs, Cfg::THREADS, smem_bytes, st>>>(tmAL, tmAR, tmAL16, tmAR16, tmAL64, tmAR64, tmUw, tmUn, tmGw,
-                                                        tmGn, tmCw, tmCn, L, (int)total, a.nl, a.ld, a.gather, a.b,
+                                                        tmGn, tmUm, tmGm, L, (int)total, a.nl, a.ld, a.gather, a.b,
                                                         a.H, a.C, a.Gact, a.ld_g, a.sc, a.rt_cnt, a.tstart,
                                                         dbg_fwd());
     FOLD_LAUNCH_CHECK();

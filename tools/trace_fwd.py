@@ -33,6 +33,9 @@ tiles = []
 for d in range(2, s.n_levels + 1):
     M = int(lo[d + 1] - lo[d]); mt = math.ceil(M / 256)
     W = 48 if mt * math.ceil(S / 48) >= npairs // 2 else 16
+    if W == 48:  # the kernel's wave model (fwd_level_W): mid width 32 when it fills the waves better
+        cost = lambda w: math.ceil(mt * math.ceil(S / w) / npairs) * max(32 * 5 * w, 4096 + 16 * 5 * w)
+        W = 32 if cost(32) < cost(48) else 48
     tiles.append((d, M, W, mt * math.ceil(S / W)))
 t = buf[:, :got].astype(np.int64)
 t0 = t[0][t[0] > 0].min()
