@@ -213,7 +213,8 @@ fold_status fold_forward(const fold_schedule_t *sched, const fold_model *model,
  * NULL = 0). Outputs dU/db/dE with the layouts of U/b/E (device fp32). With
  * accumulate = 0 they are overwritten (dE rows of untouched tokens become 0);
  * with accumulate = 1 the gradients are added. Deterministic: bitwise-identical
- * results for identical inputs (no floating-point atomics). */
+ * results for identical inputs (no floating-point atomics). dU, db and dE must be
+ * 16-byte aligned (FOLD_E_INVALID otherwise). */
 typedef struct {
   float *dU, *db, *dE;
   int32_t accumulate;

@@ -240,6 +240,8 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
   FOLD_TRY(check_sched(s));
   FOLD_TRY(check_model(m));
   if (!grads || !grads->dU || !grads->db || !grads->dE) return FOLD_E_INVALID;
+  // vectorised stores / read-modify-writes: gradient arrays must be 16-byte aligned
+  if (((uintptr_t)grads->dU | (uintptr_t)grads->db | (uintptr_t)grads->dE) & 15) return FOLD_E_INVALID;
   if (s->n_graphs > 0 && !dh_root) return FOLD_E_INVALID;
   BwdWs b = bwd_layout(ws, s, m);
   if (!ws || ws_bytes < b.bytes) return FOLD_E_WORKSPACE;

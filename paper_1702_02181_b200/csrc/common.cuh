@@ -49,6 +49,15 @@ fold_status launch_check(const char *file, int line);
     if (_s != FOLD_OK) return _s;                             \
   } while (0)
 
+// Current device id clamped to [0, kMaxDevices): index of the per-device host caches
+// (kernel attributes, occupancy and SM counts are per device).
+constexpr int kMaxDevices = 16;
+inline int cur_dev() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  return dev;
+}
+
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 

@@ -64,8 +64,10 @@ constexpr int BK = 64;      // K elements per stage (128 B of bf16 = one swizzle
 constexpr int ST = FOLD_DU_ST;  // pipeline stages (dA / dU GEMMs)
 constexpr int kThreads = 256;
 
+// (offset from the __shared__ base rather than integer casts of the pointer, so the compiler
+// keeps the shared address space and emits LDS/STS instead of generic LD/ST)
 __device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
-  return (uint8_t *)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
+  return p + ((1024u - (ptx::smem_u32(p) & 1023u)) & 1023u);
 }
 
 constexpr int tmem_cols_for(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
@@ -1887,17 +1889,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // 8 rows) over cells 8 kg .. 8 kg + 7 of every k-block; a stage is read after the MMA
       // has consumed it (empty) and released on dbfree before the producer refills it
       const int t = tid - 128, bc = t & 15, kg = t >> 4;
+      const uint32_t smem_base = ptx::smem_u32(smem);
       float acc[8];
 #pragma unroll
       for (int u = 0; u < 8; u++) acc[u] = 0.f;
       for (int it = 0; it < KB; it++) {
         const int s = it % ST;
         ptx::mbar_wait(&empty[s], (it / ST) & 1);
-        const uint32_t base = (uint32_t)(s * DU_STAGE + (bc >> 3) * MN_CHUNK + kg * 8 * 128);
+        const uint32_t base = smem_base + (uint32_t)(s * DU_STAGE + (bc >> 3) * MN_CHUNK + kg * 8 * 128);
 #pragma unroll
         for (int kk = 0; kk < 8; kk++) {
-          const uint32_t off = base + kk * 128 + ((((uint32_t)bc & 7) ^ (uint32_t)kk) << 4);
-          const uint4 a = *reinterpret_cast<const uint4 *>(smem + off);
+          const uint4 a = ptx::lds128(base + kk * 128 + ((((uint32_t)bc & 7) ^ (uint32_t)kk) << 4));
           const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
           for (int u = 0; u < 4; u++) {
@@ -1906,6 +1908,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             acc[2 * u + 1] += f.y;
           }
         }
+        // release the stage to the producer's next TMA (async proxy) only after this
+        // warp's generic-proxy reads: shared-window loads (LDS, ordered with the arrive in
+        // the shared-memory pipe) plus the cross-proxy fence. The first version read the
+        // tile through a generic pointer (LD.E), the arrive overtook those loads and under
+        // load the refill landed first (GPUTEST_r01: db differed between identical calls
+        // in whole 64-row boxes while dZ and dU matched)
+        ptx::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&dbfree[s]);
       }
@@ -1954,26 +1963,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc2(tbase, 256); }
 }
 
-// out[i] = (accumulate ? out[i] : 0) + sum_{s < nsplit} part[s][i]   (fixed order)
+// out[i] = (accumulate ? out[i] : 0) + sum_{s < nsplit} part[s][i]   (fixed order).
+// float4 lanes only when every slab start and out are 16-byte aligned (vec != 0: n % 4 == 0
+// and aligned bases, checked on the host); otherwise scalar (e.g. db with gates * S odd).
 __global__ void k_reduce_splits(int64_t n, int nsplit, const float *__restrict__ part, float *__restrict__ out,
-                                int accumulate) {
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i4 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i4 < n; i4 += stride * 4) {
-    if (i4 + 4 <= n) {
+                                int accumulate, int vec) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (vec) {
+    for (int64_t i4 = t0 * 4; i4 < n; i4 += stride * 4) {
       float4 acc = accumulate ? *reinterpret_cast<const float4 *>(out + i4) : make_float4(0.f, 0.f, 0.f, 0.f);
       for (int s = 0; s < nsplit; s++) {
-        float4 v = *reinterpret_cast<const float4 *>(part + (int64_t)s * n + i4);
+        const float4 v = *reinterpret_cast<const float4 *>(part + (int64_t)s * n + i4);
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
       *reinterpret_cast<float4 *>(out + i4) = acc;
-    } else {
-      for (int64_t i = i4; i < n; i++) {
-        float acc = accumulate ? out[i] : 0.f;
-        for (int s = 0; s < nsplit; s++) acc += part[(int64_t)s * n + i];
-        out[i] = acc;
-      }
+    }
+  } else {
+    for (int64_t i = t0; i < n; i += stride) {
+      float acc = accumulate ? out[i] : 0.f;
+      for (int s = 0; s < nsplit; s++) acc += part[(int64_t)s * n + i];
+      out[i] = acc;
     }
   }
+}
+
+fold_status launch_reduce_splits(int64_t n, int nsplit, const float *part, float *out, int accumulate,
+                                 cudaStream_t st) {
+  if (n <= 0) return FOLD_OK;
+  const int vec = (n % 4 == 0) && ((((uintptr_t)part) | ((uintptr_t)out)) & 15) == 0;
+  int64_t blocks = cdiv(vec ? cdiv(n, 4) : n, 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_reduce_splits<<<(unsigned)blocks, 256, 0, st>>>(n, nsplit, part, out, accumulate, vec);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
 }
 
 // =================================================================== weight prep
@@ -2065,15 +2088,15 @@ fold_status set_smem(K kernel, int bytes) {
   return FOLD_OK;
 }
 
-int g_num_sms = 0;
 int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
+  static int n[kMaxDevices] = {};
+  const int dev = cur_dev();
+  if (!n[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev] = v > 0 ? v : 148;
   }
-  return g_num_sms;
+  return n[dev];
 }
 
 // Max co-resident CTA pairs of a kernel (the persistent kernels' spin waits need every CTA
@@ -2147,7 +2170,8 @@ fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
   auto kern = k_fwd_levels<GATES>;
   const int smem_bytes = Cfg::SMEM;
   FOLD_TRY(set_smem(kern, smem_bytes));
-  static thread_local int npairs_max = 0;
+  static thread_local int npairs_dev[kMaxDevices] = {};
+  int &npairs_max = npairs_dev[cur_dev()];
   if (!npairs_max) npairs_max = max_pairs(kern, Cfg::THREADS, smem_bytes);
   FwdLevels L{a.level_off, a.D, S, Cfg::WMAX, Cfg::WNAR, npairs_max / 2, Cfg::WMID, GATES, npairs_max};
   // the narrow tail: levels d0..D all of at most narrow_max rows go to k_fwd_narrow
@@ -2366,7 +2390,8 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
   FOLD_TRY(make_map(&tmU, a.Ub, (uint64_t)ld_u, (uint64_t)gates * S, (uint64_t)ld_u * 2, 64, BK));
   auto kern = gates == 5 ? k_bwd_levels<5> : k_bwd_levels<1>;
   FOLD_TRY(set_smem(kern, BW_SMEM));
-  static thread_local int npairs_max = 0;
+  static thread_local int npairs_dev[kMaxDevices] = {};
+  int &npairs_max = npairs_dev[cur_dev()];
   if (!npairs_max) npairs_max = max_pairs(kern, BW_THREADS, BW_SMEM);
   // the narrow top: levels D..d1 (all of at most FOLD_BWD_NARROW_MAX rows) run first in
   // k_bwd_narrow, the wide kernel takes levels d1-1..2
@@ -2496,15 +2521,8 @@ fold_status tc_gemm_dU(int n_cells, int S, int gates, const __nv_bfloat16 *dZ, i
   k_gemm_dU_tc<<<grid, kThreads, DU_SMEM, st>>>(tmZ2, tmAL, tmAR, n_cells, S, gates * S, NT, kbps, split_ws, n, 0,
                                                 dbo, 0);
   FOLD_LAUNCH_CHECK();
-  int64_t blocks = cdiv(cdiv(n, 4), 256);
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  k_reduce_splits<<<(unsigned)blocks, 256, 0, st>>>(n, splits, split_ws, dU, accumulate);
-  FOLD_LAUNCH_CHECK();
-  if (db) {
-    const int64_t nb = (int64_t)gates * S;
-    k_reduce_splits<<<(unsigned)cdiv(cdiv(nb, 4), 256), 256, 0, st>>>(nb, splits, db_ws, db, accumulate);
-    FOLD_LAUNCH_CHECK();
-  }
+  FOLD_TRY(launch_reduce_splits(n, splits, split_ws, dU, accumulate, st));
+  if (db) FOLD_TRY(launch_reduce_splits((int64_t)gates * S, splits, db_ws, db, accumulate, st));
   return FOLD_OK;
 }
 

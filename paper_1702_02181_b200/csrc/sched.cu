@@ -719,10 +719,13 @@ fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr
   // grid: one block for small batches, else enough blocks for ~2K nodes each, all
   // co-resident (cooperative launch)
   const size_t dsmem = (size_t)(kSchedWarps * (kMaxBins + 1) + 2 * kMaxBins + 64) * sizeof(int);
-  static thread_local int max_blocks = 0;
+  static thread_local int max_blocks_dev[kMaxDevices] = {};
+  static thread_local size_t smem_set_dev[kMaxDevices] = {};
+  const int dev = cur_dev();
+  int &max_blocks = max_blocks_dev[dev];
+  size_t &smem_set = smem_set_dev[dev];
   if (!max_blocks) {
-    int dev, nsm, occ = 0;
-    FOLD_CUDA_TRY(cudaGetDevice(&dev));
+    int nsm, occ = 0;
     FOLD_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     FOLD_CUDA_TRY(cudaFuncSetAttribute(k_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
     FOLD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_schedule, kSchedThreads, dsmem));
@@ -748,7 +751,6 @@ fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr
   // memory (3N ints, at most 192 KB for kSmallN nodes)
   size_t launch_smem = dsmem;
   if (blocks == 1 && (size_t)3 * N * sizeof(int) > launch_smem) launch_smem = (size_t)3 * N * sizeof(int);
-  static thread_local size_t smem_set = 0;
   if (launch_smem > smem_set) {
     FOLD_CUDA_TRY(cudaFuncSetAttribute(k_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)launch_smem));
     smem_set = launch_smem;
