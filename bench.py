@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--cell", default=None, choices=["treelstm", "treernn"])
     ap.add_argument("--lr", type=float, default=1e-4)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c5-strong", action="store_true", help="N > 1: skip the C5 strong-scaling record")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-batch1", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
@@ -170,6 +171,9 @@ def run_fold(args):
     local = local % max(torch.cuda.device_count(), 1)  # (gloo test runs: several ranks per GPU)
     if world > 1:
         if args.backend == "nccl":
+            # communicator setup (ranks, NVLink / NVLS transport) in the log, on stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
@@ -416,6 +420,34 @@ def run_fold(args):
         e2e = {"value": global_nodes / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
+    # ---------------- N > 1: BASELINE configs[4] strong scaling beside the weak-scaled headline:
+    # ONE global batch of 8192 random 128-leaf trees sharded by node count (dp.shard), the
+    # same step (schedule + fwd + bwd + all_reduce + SGD), max over ranks
+    c5 = None
+    if world > 1 and args.config == "c2" and not args.no_c5_strong:
+        from paper_1702_02181_b200 import dp
+        full5 = foldgen.config_c5(8192)
+        gr5 = dp.shard(full5, rank, world)
+        o5 = fold.graphs_to_device(gr5, dev)
+        g5 = torch.from_numpy(foldgen.make_upstream(gr5.n_graphs, S)).to(dev)
+        for _ in range(max(args.warmup, 3)):
+            step(*o5, g5)
+        torch.cuda.synchronize()
+        dist.barrier()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(args.steps):
+            step(*o5, g5)
+        c1.record()
+        torch.cuda.synchronize()
+        t5 = torch.tensor([c0.elapsed_time(c1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t5, op=dist.ReduceOp.MAX)
+        ms5 = float(t5.item()) / args.steps
+        c5 = {"value": full5.n_nodes / (ms5 / 1e3), "unit": UNIT, "ms_per_step": ms5, "scaling": "strong",
+              "trees": full5.n_graphs, "nodes": full5.n_nodes, "nodes_rank0": gr5.n_nodes,
+              "shard": "contiguous tree ranges balanced by node count (dp.shard)",
+              "step": "schedule+fwd+bwd+all_reduce([dU|db|dE], %.0f MB)+sgd" % (flat_g.numel() * 4 / 1e6)}
+
     # ---------------- batch-1 (within-tree batching only) for the speedup-vs-batch-size context
     batch1 = None
     if not args.no_batch1 and rank == 0 and args.config in ("c2", "c3", "c4", "c5"):
@@ -452,36 +484,10 @@ def run_fold(args):
         return
 
     # ---------------- roofline of the dominant kernel class (tensor-bound GEMM kernels)
-    pk, pk_src = peaks()
-    flops_per_cell = 2.0 * gates * S * 2 * S  # one GEMM pass (fwd Z, bwd dA, or dU) per cell
     per_class = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
                  for k, v in prof.items() if v[1] > 0}
-    # kernel per class: the persistent all-levels forward; the persistent all-levels backward
-    # (dA GEMM with the children's pointwise step fused into its epilogue; tree-like
-    # schedules, as every bench workload is); the all-cells weight-gradient GEMM
-    tensor_classes = {"cell_fwd": "k_fwd_levels", "gemm_dA": "k_bwd_levels", "gemm_dU": "k_gemm_dU_tc"}
-    dom = max(tensor_classes, key=lambda k: prof[k][0])
-    dom_ms_total, dom_launches = prof[dom]
-    achieved = flops_per_cell * n_cells * args.steps / (dom_ms_total / 1e3) / 1e12
-    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
-    traffic = None
-    traffic_note = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            tr = json.load(open(tpath)).get(tensor_classes[dom], {})
-            traffic = tr.get("dram_bytes_per_launch")
-            traffic_note = tr.get("launch")
-        except Exception:
-            traffic = None
-    roofline = {"bound": "tensor", "kernel": tensor_classes[dom], "achieved": achieved, "peak": peak,
-                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                "peak_source": f"{pk_src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
-                "algorithmic": f"{flops_per_cell:.4g} FLOP/cell x {n_cells} cells per launch-set; "
-                               f"{dom_launches // max(args.steps, 1)} launches/step",
-                "share_of_step": (dom_ms_total / args.steps) / ms_per_step,
-                "traffic_source": ("ncu --set full, DRAM read+write bytes of one launch (%s); profiles/ncu_traffic.json"
-                                   % traffic_note) if traffic is not None else None}
+    roofline = roofline_record(prof, args.steps, ms_per_step, gates, S, n_cells, clk,
+                               cfg_key=f"{args.config}/{gr.n_graphs}/{S}/{args.prec}")
 
     # ---------------- CPU baseline: the fp64 oracle as it stands, bounded sample, 1 thread
     cpu = None
@@ -515,6 +521,8 @@ def run_fold(args):
         "e2e": e2e,
         "clocks": clk,
     }
+    if c5:
+        out["c5_strong"] = c5
     if sweep:
         out["sweep_nodes_per_s_vs_batch"] = sweep
     if batch1:
@@ -528,6 +536,65 @@ def run_fold(args):
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+# algorithmic DRAM bytes per cell of each tensor kernel (SURVEY §8(d.4), BF16 path; fp32 c and
+# gradients): forward reads 2S h (bf16) + 2S child c (fp32), writes S h + S c + 5S gates
+# (28 S); the dA sweep reads the edge gradients dh, dc (2 S fp32), gates (5S bf16), c, c_L,
+# c_R (3 S fp32), writes dZ (5S bf16) + dA / dCe (4 S fp32) (56 S); dU re-reads the 2S h
+# operand row and the 5S dZ row (14 S)
+ALGO_BYTES_PER_CELL_PER_S = {"k_fwd_levels": 28, "k_bwd_levels": 56, "k_gemm_dU_tc": 14}
+
+
+def roofline_record(prof, steps, ms_per_step, gates, S, n_cells, clk, cfg_key=None):
+    """Roofline of the three tcgen05 GEMM kernel classes (each = one persistent launch per
+    step), the dominant one as the headline object. achieved = 2 * gates*S * 2S FLOP per cell
+    x cells per launch / the class's CUDA-event time per step (on its launch stream, inside
+    the timed region). Peak: MEASURED_PEAKS.json's burst bf16 figure when the timed region's
+    median SM clock is within 5% of max (the GPU ran at full clock), else the sustained one
+    (power-capped clocks); both fractions are printed. traffic = ncu DRAM bytes of one launch
+    (profiles/ncu_traffic.json), beside the algorithmic bytes of SURVEY §8(d.4)."""
+    pk, pk_src = peaks()
+    burst = pk.get("bf16_tflops")
+    sustained = pk.get("bf16_tflops_sustained", burst)
+    full_clock = bool(clk and clk.get("sm_max_mhz") and clk["sm_mhz"] >= 0.95 * clk["sm_max_mhz"])
+    peak, which = (burst, "burst") if (full_clock or clk is None) else (sustained, "sustained")
+    flops_per_cell = 2.0 * gates * S * 2 * S  # one GEMM pass (fwd Z, bwd dA, or dU) per cell
+    tensor_classes = {"cell_fwd": "k_fwd_levels", "gemm_dA": "k_bwd_levels", "gemm_dU": "k_gemm_dU_tc"}
+    ncu = {}
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            ncu = json.load(open(tpath))
+        except Exception:
+            ncu = {}
+        if ncu.get("_config") != cfg_key:  # captured on another workload: no traffic figure
+            ncu = {}
+    per = {}
+    for cls, kern in tensor_classes.items():
+        ms_total, launches = prof.get(cls, (0.0, 0))
+        if launches <= 0 or ms_total <= 0:
+            continue
+        ms = ms_total / steps
+        ach = flops_per_cell * n_cells / (ms / 1e3) / 1e12
+        algo = ALGO_BYTES_PER_CELL_PER_S[kern] * S * n_cells
+        tr = ncu.get(kern, {}).get("dram_bytes_per_launch")
+        per[kern] = {"ms_per_step": ms, "achieved": ach, "frac": ach / peak, "frac_burst": ach / burst,
+                     "frac_sustained": ach / sustained, "share_of_step": ms / ms_per_step,
+                     "algorithmic_bytes": algo, "traffic": tr,
+                     "traffic_over_algorithmic": (tr / algo) if tr else None}
+    dom = max(per, key=lambda k: per[k]["ms_per_step"])
+    d = per[dom]
+    return {"bound": "tensor", "kernel": dom, "achieved": d["achieved"], "peak": peak, "unit": "TFLOP/s",
+            "frac": d["frac"], "traffic": d["traffic"],
+            "peak_kind": which, "frac_burst": d["frac_burst"], "frac_sustained": d["frac_sustained"],
+            "peak_source": f"{pk_src} bf16_tflops ({which}; burst {burst}, sustained {sustained} TF/s, "
+                           f"MEASURED_PEAKS.json); burst when the timed region's median SM clock >= 0.95 x max",
+            "algorithmic": f"{flops_per_cell:.4g} FLOP/cell x {n_cells} cells per launch (one launch per step)",
+            "share_of_step": d["share_of_step"],
+            "traffic_source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum of one launch "
+                              "(profiles/ncu_traffic.json)" if d["traffic"] else None,
+            "kernels": per}
 
 
 def _time(fn, nrep, warm=2):

@@ -54,7 +54,7 @@
 extern "C" {
 #endif
 
-#define FOLD_ABI_VERSION 3
+#define FOLD_ABI_VERSION 4
 
 typedef enum {
   FOLD_OK = 0,
@@ -241,6 +241,14 @@ const char *fold_status_string(fold_status s);
 /* Detail of the last data-dependent error on this thread: the offending node (or
  * graph) id, -1 if none. */
 int32_t fold_last_error_detail(void);
+/* (node, depth, op) context of the last data-dependent fold_schedule error on this thread
+ * (errors carry the depth and operation): node = the offending node (graph id
+ * for FOLD_E_ROOT_RANGE); op = that node's op[] value as given (-1 for ROOT_RANGE); depth =
+ * its caller-fixed level for FOLD_E_LEVEL, else -1 (every other class is detected before
+ * depths exist: validation precedes depth propagation, and a cycle has none). Host pointers,
+ * each may be NULL. Returns FOLD_OK if such an error is recorded, else FOLD_E_INVALID with
+ * all three set to -1. */
+fold_status fold_last_error_context(int32_t *node, int32_t *depth, int32_t *op);
 int32_t fold_abi_version(void);
 /* FOLD_OK if the current CUDA device is sm_100 (B200) and the kernels are loadable. */
 fold_status fold_device_check(void);

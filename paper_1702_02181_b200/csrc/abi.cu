@@ -11,6 +11,7 @@ fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws, si
 int debug_sched_trace(unsigned long long *host);
 size_t schedule_workspace(int64_t N, int64_t G);
 extern thread_local int32_t g_last_detail;
+extern thread_local int32_t g_last_ctx[3];
 
 namespace {
 
@@ -378,6 +379,12 @@ const char *fold_status_string(fold_status s) {
 }
 
 int32_t fold_last_error_detail(void) { return g_last_detail; }
+fold_status fold_last_error_context(int32_t *node, int32_t *depth, int32_t *op) {
+  if (node) *node = g_last_ctx[0];
+  if (depth) *depth = g_last_ctx[1];
+  if (op) *op = g_last_ctx[2];
+  return g_last_ctx[0] >= 0 ? FOLD_OK : FOLD_E_INVALID;
+}
 int32_t fold_abi_version(void) { return FOLD_ABI_VERSION; }
 
 /* instrumentation: per-phase timeline of the last FOLD_DBG_SCHED=1 schedule (block 0) */

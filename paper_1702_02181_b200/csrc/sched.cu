@@ -675,6 +675,9 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
 }  // namespace
 
 thread_local int32_t g_last_detail = -1;
+// (node, depth, op) context of the last data-dependent error (errors carry
+// (depth, operation)); see fold.h fold_last_error_context
+thread_local int32_t g_last_ctx[3] = {-1, -1, -1};
 
 // device-wide exclusive int32 scan for other translation units; `sums` needs
 // scan_sums_count(n) entries
@@ -693,6 +696,7 @@ size_t schedule_workspace(int64_t N, int64_t G) { return sched_ws_layout(nullptr
 fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr, size_t ws_bytes,
                          cudaStream_t st) {
   g_last_detail = -1;
+  g_last_ctx[0] = g_last_ctx[1] = g_last_ctx[2] = -1;
   if (!gr || !s) return FOLD_E_INVALID;
   const int N = gr->n_nodes, G = gr->n_graphs, V = gr->vocab;
   if (N < 0 || G < 0 || V < 0) return FOLD_E_INVALID;
@@ -700,7 +704,7 @@ fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr
   s->n_levels = s->n_leaves = s->n_cells = s->n_tok_segs = 0;
   s->tree_like = 0;
   if (N == 0) {
-    if (G > 0) { g_last_detail = 0; return FOLD_E_ROOT_RANGE; }
+    if (G > 0) { g_last_detail = 0; g_last_ctx[0] = 0; return FOLD_E_ROOT_RANGE; }
     if (s->level_off_host) { s->level_off_host[0] = 0; s->level_off_host[1] = 0; }
     if (s->level_off) FOLD_CUDA_TRY(cudaMemsetAsync(s->level_off, 0, 2 * sizeof(int32_t), st));
     if (s->group_off) FOLD_CUDA_TRY(cudaMemsetAsync(s->group_off, 0, 3 * sizeof(int32_t), st));
@@ -779,6 +783,19 @@ fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr
   for (int e = 0; e < E_NCLASS; e++) {
     if (hflags[F_ERR0 + e] != INT_MAX) {
       g_last_detail = hflags[F_ERR0 + e];
+      // error path only: the offending node's op id (and its caller-fixed level) from the
+      // caller's arrays; depth stays -1 for errors found before depths exist (validation,
+      // cycles) and is the caller's level for FOLD_E_LEVEL
+      const int32_t id = g_last_detail;
+      g_last_ctx[0] = id;
+      if (e != E_ROOT && id >= 0 && id < N) {
+        int32_t v[2] = {-1, -1};
+        FOLD_CUDA_TRY(cudaMemcpyAsync(&v[0], gr->op + id, 4, cudaMemcpyDeviceToHost, st));
+        if (e == E_LEVEL && gr->level) FOLD_CUDA_TRY(cudaMemcpyAsync(&v[1], gr->level + id, 4, cudaMemcpyDeviceToHost, st));
+        FOLD_CUDA_TRY(cudaStreamSynchronize(st));
+        g_last_ctx[2] = v[0];
+        g_last_ctx[1] = v[1];
+      }
       return kErrStatus[e];
     }
   }

@@ -102,6 +102,8 @@ def load() -> ctypes.CDLL:
     L.fold_status_string.restype = ctypes.c_char_p
     L.fold_status_string.argtypes = [i32]
     L.fold_last_error_detail.restype = i32
+    L.fold_last_error_context.restype = i32
+    L.fold_last_error_context.argtypes = [ctypes.POINTER(ctypes.c_int32)] * 3
     L.fold_abi_version.restype = i32
     L.fold_device_check.restype = i32
     L.fold_launch_count.restype = ctypes.c_int64
@@ -122,7 +124,7 @@ def load() -> ctypes.CDLL:
 
 EXPORTED = ("fold_schedule_workspace", "fold_schedule", "fold_acts_layout", "fold_forward_workspace",
             "fold_forward", "fold_backward_workspace", "fold_backward", "fold_sgd_update",
-            "fold_status_string", "fold_last_error_detail", "fold_abi_version", "fold_device_check",
+            "fold_status_string", "fold_last_error_detail", "fold_last_error_context", "fold_abi_version", "fold_device_check",
             "fold_launch_count", "fold_profile_enable", "fold_profile_read", "fold_debug_fwd_trace", "fold_debug_bwd_trace",
             "fold_debug_sched_trace")
 
@@ -144,15 +146,25 @@ def profile_read() -> dict:
 
 
 class FoldError(RuntimeError):
-    def __init__(self, status: int, what: str, detail: int = -1):
-        super().__init__(f"{what}: FOLD_E_{STATUS.get(status, status)} (detail {detail})")
+    def __init__(self, status: int, what: str, detail: int = -1, depth: int = -1, op: int = -1):
+        super().__init__(f"{what}: FOLD_E_{STATUS.get(status, status)} (node {detail}, depth {depth}, op {op})")
         self.status = STATUS.get(status, status)
         self.detail = detail
+        self.depth = depth
+        self.op = op
+
+
+def last_error_context() -> tuple[int, int, int]:
+    """(node, depth, op) of the last data-dependent fold_schedule error (fold.h)."""
+    v = [ctypes.c_int32(-1) for _ in range(3)]
+    load().fold_last_error_context(*(ctypes.byref(x) for x in v))
+    return tuple(int(x.value) for x in v)
 
 
 def _check(st: int, what: str):
     if st != OK:
-        raise FoldError(st, what, load().fold_last_error_detail())
+        node, depth, op = last_error_context()
+        raise FoldError(st, what, load().fold_last_error_detail(), depth, op)
 
 
 def _ptr(t: torch.Tensor | None):

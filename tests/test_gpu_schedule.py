@@ -114,6 +114,25 @@ def test_errors_match_oracle(case, status, node):
         _gpu_sched(gr)
     assert eg.value.status == eo.value.status == status
     assert eg.value.detail == eo.value.node == node
+    # (node, depth, op) context: op is the offending node's op id as given
+    ctx = fold.last_error_context()
+    assert ctx[0] == node
+    assert ctx[2] == (-1 if status == "ROOT_RANGE" else case["op"][node])
+    assert ctx[1] == -1
+
+
+def test_error_context_level():
+    """FOLD_E_LEVEL reports the offending node's caller-fixed level as its depth."""
+    import torch
+    from paper_1702_02181_b200 import fold
+    op = np.asarray([0, 0, 1, 1], np.int32)
+    child = np.asarray([[-1, -1], [-1, -1], [0, 1], [2, 0]], np.int32)
+    level = np.asarray([1, 1, 3, 3], np.int32)  # node 3 must be above its child 2
+    t = lambda a: torch.from_numpy(a).cuda()
+    with pytest.raises(fold.FoldError) as eg:
+        fold.schedule(t(op), t(child), t(np.zeros(4, np.int32)), t(np.asarray([3], np.int32)), 4, level=t(level))
+    assert eg.value.status == "LEVEL"
+    assert fold.last_error_context() == (3, 3, 1)
 
 
 def test_determinism():
