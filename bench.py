@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--impl", choices=["fold", "reference"], default="fold")
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--batch", type=int, default=None, help="trees per GPU (default: config's full size)")
-    ap.add_argument("--prec", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--prec", default="bf16", choices=["bf16", "tf32", "fp32"])
     ap.add_argument("--cell", default=None, choices=["treelstm", "treernn"])
     ap.add_argument("--lr", type=float, default=1e-4)
     ap.add_argument("--no-e2e", action="store_true")
@@ -487,7 +487,7 @@ def run_fold(args):
     per_class = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
                  for k, v in prof.items() if v[1] > 0}
     roofline = roofline_record(prof, args.steps, ms_per_step, gates, S, n_cells, clk,
-                               cfg_key=f"{args.config}/{gr.n_graphs}/{S}/{args.prec}")
+                               cfg_key=f"{args.config}/{gr.n_graphs}/{S}/{args.prec}", prec=args.prec)
 
     # ---------------- CPU baseline: the fp64 oracle as it stands, bounded sample, 1 thread
     cpu = None
@@ -546,7 +546,7 @@ def run_fold(args):
 ALGO_BYTES_PER_CELL_PER_S = {"k_fwd_levels": 28, "k_bwd_levels": 56, "k_gemm_dU_tc": 14}
 
 
-def roofline_record(prof, steps, ms_per_step, gates, S, n_cells, clk, cfg_key=None):
+def roofline_record(prof, steps, ms_per_step, gates, S, n_cells, clk, cfg_key=None, prec="bf16"):
     """Roofline of the three tcgen05 GEMM kernel classes (each = one persistent launch per
     step), the dominant one as the headline object. achieved = 2 * gates*S * 2S FLOP per cell
     x cells per launch / the class's CUDA-event time per step (on its launch stream, inside
@@ -557,10 +557,20 @@ def roofline_record(prof, steps, ms_per_step, gates, S, n_cells, clk, cfg_key=No
     pk, pk_src = peaks()
     burst = pk.get("bf16_tflops")
     sustained = pk.get("bf16_tflops_sustained", burst)
+    # TF32 / FP32 (3xTF32) modes: the TF32 peak = the measured bf16 peak x the nominal dense
+    # ratio 1.125 / 2.25 PF (B200_PROFILING.md); 3xTF32 issues three MMAs per algorithmic
+    # product, so its ceiling in algorithmic FLOP/s is a third of that
+    scale = {"bf16": 1.0, "tf32": 0.5, "fp32": 0.5 / 3}[prec]
+    burst, sustained = burst * scale, sustained * scale
+    dtype_note = {"bf16": "bf16", "tf32": "tf32 (= bf16 x 0.5 nominal ratio)",
+                  "fp32": "3xTF32 (= bf16 x 0.5 / 3 MMA passes)"}[prec]
     full_clock = bool(clk and clk.get("sm_max_mhz") and clk["sm_mhz"] >= 0.95 * clk["sm_max_mhz"])
     peak, which = (burst, "burst") if (full_clock or clk is None) else (sustained, "sustained")
     flops_per_cell = 2.0 * gates * S * 2 * S  # one GEMM pass (fwd Z, bwd dA, or dU) per cell
     tensor_classes = {"cell_fwd": "k_fwd_levels", "gemm_dA": "k_bwd_levels", "gemm_dU": "k_gemm_dU_tc"}
+    if prec != "bf16":  # per-level gather + k_gemm_tf32 + pointwise; dA and dU on k_gemm_tf32
+        tensor_classes = {"cell_fwd": "k_gemm_tf32 (fwd levels, + gather/pointwise)",
+                          "gemm_dA": "k_gemm_tf32 (dA levels)", "gemm_dU": "k_gemm_tf32 (dU)"}
     ncu = {}
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -577,7 +587,7 @@ def roofline_record(prof, steps, ms_per_step, gates, S, n_cells, clk, cfg_key=No
             continue
         ms = ms_total / steps
         ach = flops_per_cell * n_cells / (ms / 1e3) / 1e12
-        algo = ALGO_BYTES_PER_CELL_PER_S[kern] * S * n_cells
+        algo = ALGO_BYTES_PER_CELL_PER_S.get(kern, 0) * S * n_cells
         tr = ncu.get(kern, {}).get("dram_bytes_per_launch")
         per[kern] = {"ms_per_step": ms, "achieved": ach, "frac": ach / peak, "frac_burst": ach / burst,
                      "frac_sustained": ach / sustained, "share_of_step": ms / ms_per_step,
@@ -588,8 +598,9 @@ def roofline_record(prof, steps, ms_per_step, gates, S, n_cells, clk, cfg_key=No
     return {"bound": "tensor", "kernel": dom, "achieved": d["achieved"], "peak": peak, "unit": "TFLOP/s",
             "frac": d["frac"], "traffic": d["traffic"],
             "peak_kind": which, "frac_burst": d["frac_burst"], "frac_sustained": d["frac_sustained"],
-            "peak_source": f"{pk_src} bf16_tflops ({which}; burst {burst}, sustained {sustained} TF/s, "
-                           f"MEASURED_PEAKS.json); burst when the timed region's median SM clock >= 0.95 x max",
+            "peak_source": f"{pk_src} bf16_tflops ({which}) for {dtype_note}; burst {burst:.1f}, sustained "
+                           f"{sustained:.1f} TF/s (MEASURED_PEAKS.json); "
+                           f"burst when the timed region's median SM clock >= 0.95 x max",
             "algorithmic": f"{flops_per_cell:.4g} FLOP/cell x {n_cells} cells per launch (one launch per step)",
             "share_of_step": d["share_of_step"],
             "traffic_source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum of one launch "

@@ -43,6 +43,7 @@
  *   FOLD_DBG_BWD          1: per-tile timelines of the wide backward (fold_debug_bwd_trace)
  *   FOLD_DBG_SCHED        1: scheduler phase timeline (fold_debug_sched_trace)
  *   FOLD_DEBUG_SYNC       1: synchronize and check after every launch
+ *   FOLD_FP32_SIMT        1: FP32 mode on the SIMT FFMA kernels (A/B measurement only)
  */
 #ifndef FOLD_H
 #define FOLD_H
@@ -83,10 +84,14 @@ enum { FOLD_OP_EMBED = 0, FOLD_OP_CELL = 1, FOLD_N_OPS = 2 };
 /* Cell equations: DESIGN.md "Cell" (TreeRNN: Fig. 1 'RNN Cell', L67; TreeLSTM: Tai et
  * al. eqs 9-14 with x = 0, N = 2, cited at L301-304). */
 enum { FOLD_CELL_TREERNN = 0, FOLD_CELL_TREELSTM = 1 };
-/* FP32: every product and sum in fp32 (SIMT kernels).
+/* FP32: states, gates, gradients fp32; the three GEMM passes on the tensor cores as
+ *       3xTF32 (tcgen05 kind::tf32, x = hi + lo split, hi*hi + hi*lo + lo*hi, fp32
+ *       accumulation in TMEM): fp32-class results (north_star bar 1e-5).
+ * TF32: the FP32 mode's data and kernels with one kind::tf32 MMA per K step (operands
+ *       read as TF32, 10 mantissa bits; north_star bar 1e-2).
  * BF16: states h, saved gates and GEMM operands in bf16, fp32 accumulation in TMEM
- *       (tcgen05), c / gradients / reductions in fp32.                            */
-enum { FOLD_PREC_FP32 = 0, FOLD_PREC_BF16 = 2 };
+ *       (tcgen05), c / gradients / reductions in fp32 (the fused persistent kernels).  */
+enum { FOLD_PREC_FP32 = 0, FOLD_PREC_TF32 = 1, FOLD_PREC_BF16 = 2 };
 
 /* ----------------------------------------------------------------- input graphs
  * A batch of graphs = one disconnected DAG. Node n:
@@ -287,6 +292,15 @@ int32_t fold_debug_bwd_trace(unsigned long long *host, int32_t n_tiles);
  * at the start of phases P0..P11 and at its end; copies the 13 stamps into host[13] and
  * returns 13 (-1 on a CUDA error). */
 int32_t fold_debug_sched_trace(unsigned long long *host);
+/* Test hook: one tcgen05 TF32 GEMM of the FP32 / TF32 modes, C[M][N] (ldc) = A * B
+ * (accumulate: +=). A is [M][K] row-major (a_mn = 0, K-major) or [K][M] (a_mn = 1); B is
+ * [N][K] (b_mn = 0) or [K][N] (b_mn = 1); all device fp32, 16-byte aligned, ld % 4 == 0.
+ * npass 1 = TF32, 3 = 3xTF32. ws: split-K scratch of fold_debug_gemm_tf32_ws(M, N, K)
+ * floats (may be NULL: no split). */
+fold_status fold_debug_gemm_tf32(const float *A, int64_t lda, int32_t a_mn, const float *B, int64_t ldb,
+                                 int32_t b_mn, int32_t M, int32_t N, int32_t K, float *C, int64_t ldc,
+                                 int32_t accumulate, int32_t npass, float *ws, int64_t ws_floats, void *stream);
+int64_t fold_debug_gemm_tf32_ws(int32_t M, int32_t N, int32_t K);
 
 #ifdef __cplusplus
 }

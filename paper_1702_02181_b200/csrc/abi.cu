@@ -20,7 +20,7 @@ inline size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 fold_status check_model(const fold_model *m) {
   if (!m || !m->U || !m->b || !m->E) return FOLD_E_INVALID;
   if (m->cell != FOLD_CELL_TREERNN && m->cell != FOLD_CELL_TREELSTM) return FOLD_E_INVALID;
-  if (m->prec != FOLD_PREC_FP32 && m->prec != FOLD_PREC_BF16) return FOLD_E_INVALID;
+  if (m->prec != FOLD_PREC_FP32 && m->prec != FOLD_PREC_TF32 && m->prec != FOLD_PREC_BF16) return FOLD_E_INVALID;
   if (m->S <= 0 || m->S > 8192 || m->vocab <= 0) return FOLD_E_INVALID;
   // vectorised loads: parameter arrays must be 16-byte aligned
   if (((uintptr_t)m->U | (uintptr_t)m->b | (uintptr_t)m->E) & 15) return FOLD_E_INVALID;
@@ -33,6 +33,18 @@ fold_status check_sched(const fold_schedule_t *s) {
   return FOLD_OK;
 }
 
+// FOLD_FP32_SIMT=1 (A/B measurements only): the FP32 mode's contractions on the previous
+// SIMT FFMA kernels instead of the 3xTF32 tensor-core GEMMs
+bool simt_fp32() {
+  static const bool v = [] { const char *e = getenv("FOLD_FP32_SIMT"); return e && atoi(e) != 0; }();
+  return v;
+}
+size_t tf_u_bytes(int gates, int S) {
+  return a256((size_t)gates * ld_of(S) * tf_ld_u(S) * 4);
+}
+inline int npass_of(int prec) { return prec == FOLD_PREC_TF32 ? 1 : 3; }
+inline int64_t tf_ld_a(int S) { return round_up(2 * (int64_t)S, 8); }
+
 // backward workspace carve
 struct BwdWs {
   float *dA, *dCe, *partial, *dU_split;
@@ -42,6 +54,8 @@ struct BwdWs {
   EmbedBwdWs emb;
   void *dZ;
   __nv_bfloat16 *Ub, *Ut;
+  float *Utf;               // FP32 / TF32 modes: the natural-row U copy (MN-major B of dA)
+  int64_t tf_split_floats;  // their dU GEMM's split-K partials
   int ld_z, nsplit;
   size_t bytes;
 };
@@ -66,10 +80,13 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
   size_t o_pc = take((size_t)(nseg + 2) * 4), o_po = take((size_t)(nseg + 2) * 4);
   size_t o_ss = take((size_t)scan_sums_count(nseg + 1) * 4);
   size_t o_ep = take((size_t)max_pieces * S * 4);
-  size_t o_w = take(bf16 ? tc_weights_bytes(gates, (int)S) : 0);
+  const bool tf = !bf16 && !simt_fp32();
+  size_t o_w = take(bf16 ? tc_weights_bytes(gates, (int)S) : tf ? tf_u_bytes(gates, (int)S) : 0);
   size_t o_ut = take(bf16 ? tc_ut_bytes(gates, (int)S) : 0);
   const int splits = bf16 ? tc_dU_splits((int)nc, gates, (int)S) : 1;
-  size_t o_spl = take(splits > 1 ? (size_t)splits * gates * S * 2 * S * 4 : 0);
+  const int64_t tf_split = tf ? gemm_tf32_split_floats(gates * (int)S, 2 * (int)S, (int)nc) : 0;
+  b.tf_split_floats = tf_split;
+  size_t o_spl = take(splits > 1 ? (size_t)splits * gates * S * 2 * S * 4 : (size_t)tf_split * 4);
   b.bytes = off;
   if (base) {
     char *p = (char *)base;
@@ -84,8 +101,9 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
     b.emb.piece_off = (int32_t *)(p + o_po);
     b.emb.scan_sums = (int32_t *)(p + o_ss);
     b.emb.partial = (float *)(p + o_ep);
-    b.dU_split = splits > 1 ? (float *)(p + o_spl) : nullptr;
+    b.dU_split = (splits > 1 || tf_split > 0) ? (float *)(p + o_spl) : nullptr;
     b.Ub = bf16 ? (__nv_bfloat16 *)(p + o_w) : nullptr;
+    b.Utf = tf ? (float *)(p + o_w) : nullptr;
     b.Ut = bf16 ? (__nv_bfloat16 *)(p + o_ut) : nullptr;
   }
   return b;
@@ -119,7 +137,7 @@ AuxStream &aux_stream() {
 
 // forward workspace (BF16 path): bf16 U, then the row-tile counters and tile starts
 size_t fwd_ws_bytes(const fold_schedule_t *s, const fold_model *m) {
-  if (m->prec != FOLD_PREC_BF16) return 256;
+  if (m->prec != FOLD_PREC_BF16) return simt_fp32() ? 256 : tf_u_bytes(gates_of(m->cell), m->S);
   return tc_weights_bytes(gates_of(m->cell), m->S) + 2 * a256((size_t)(s->n_cells + 1) * sizeof(int));
 }
 
@@ -137,7 +155,11 @@ ActsLayout acts_layout(const fold_schedule_t *s, const fold_model *m) {
   L.c_off = off; off = a256(off + (size_t)(N + 1) * L.ld * 4);
   L.g_off = off; off = a256(off + (size_t)(nc + 1) * L.ld_g * L.helem);
   const bool planes = m->prec == FOLD_PREC_BF16;
-  L.al_off = off; off = a256(off + (planes ? (size_t)(nc + 1) * L.ld * 2 : 0));
+  // BF16: the two push-gathered operand planes A_L / A_R; FP32 / TF32: one gathered fp32
+  // plane Acat [n_cells][round_up(2S, 8)] (the level GEMMs' A, the dU GEMM's B)
+  const bool cat = !planes && !simt_fp32();
+  L.al_off = off;
+  off = a256(off + (planes ? (size_t)(nc + 1) * L.ld * 2 : cat ? (size_t)(nc + 1) * tf_ld_a((int)S) * 4 : 0));
   L.ar_off = off; off = a256(off + (planes ? (size_t)(nc + 1) * L.ld * 2 : 0));
   L.bytes = off;
   return L;
@@ -216,11 +238,33 @@ fold_status fold_forward(const fold_schedule_t *s, const fold_model *m, void *ac
       ProfScope ps(K_CELL_FWD, st);
       FOLD_TRY(tc_fwd_levels(m->cell, fa, st));
     }
-  } else {
+  } else if (simt_fp32()) {
     for (int d = 2; d <= D; d++) {
       ProfScope ps(K_CELL_FWD, st);
       FOLD_TRY(launch_cell_fwd_simt(m->cell, lo[d], lo[d + 1], s->gather, S, L.ld, m->U, m->b, (float *)H, C,
                                     (float *)Gact, L.ld_g, nl, st));
+    }
+  } else if (D >= 2) {
+    // FP32 (3xTF32) / TF32: per level gather -> tcgen05 GEMM -> pointwise
+    // append; Z lands in the level's saved-gate rows (gate blocks at g*ld: the forward U copy
+    // has gate-padded rows) and the pointwise step turns it into the gates in place
+    float *Uf = (float *)ws;
+    {
+      ProfScope ps(K_PREP, st);
+      FOLD_TRY(launch_prep_U_tf(gates, S, L.ld, m->U, Uf, nullptr, st));
+    }
+    float *Acat = (float *)(a + L.al_off);
+    const int64_t lda = tf_ld_a(S);
+    const int npass = npass_of(m->prec);
+    for (int d = 2; d <= D; d++) {
+      const int r0 = lo[d], r1 = lo[d + 1], M = r1 - r0, c0 = r0 - nl;
+      if (M <= 0) continue;
+      ProfScope ps(K_CELL_FWD, st);
+      FOLD_TRY(launch_gather_cat(r0, r1, nl, S, L.ld, s->gather, (const float *)H, Acat, lda, st));
+      FOLD_TRY(gemm_tf32(TfOperand{Acat + (int64_t)c0 * lda, lda, 0}, TfOperand{Uf, tf_ld_u(S), 0}, M, gates * L.ld,
+                         2 * S, (float *)Gact + (int64_t)c0 * L.ld_g, L.ld_g, 0, npass, nullptr, 0, st));
+      FOLD_TRY(launch_cell_fwd_pw(m->cell, r0, r1, nl, S, L.ld, L.ld_g, s->gather, m->b, (float *)H, C,
+                                  (float *)Gact, st));
     }
   }
   ProfScope ps(K_ROOT, st);
@@ -273,6 +317,9 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
   if (bf16) {
     ProfScope ps(K_PREP, st);
     FOLD_TRY(tc_prepare_U(gates, S, m->U, b.Ub, st));
+  } else if (b.Utf) {
+    ProfScope ps(K_PREP, st);
+    FOLD_TRY(launch_prep_U_tf(gates, S, L.ld, m->U, nullptr, b.Utf, st));
   }
   const bool fused_tree = bf16 && s->tree_like && (S & 1) == 0;  // (leaf dA in bf16 on this path)
   if (fused_tree) {
@@ -305,6 +352,10 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
     float *dA_lvl = b.dA + (size_t)2 * c0 * S;
     if (bf16)
       FOLD_TRY(tc_gemm_dA(c0, M, nc, S, gates, (const __nv_bfloat16 *)b.dZ, b.ld_z, b.Ub, b.dA, st));
+    else if (b.Utf)  // dA = dZ U: A = the level's dZ rows (K-major), B = U [gates*S][2S] (MN-major)
+      FOLD_TRY(gemm_tf32(TfOperand{(const float *)b.dZ + (int64_t)c0 * b.ld_z, b.ld_z, 0},
+                         TfOperand{b.Utf, tf_ld_u(S), 1}, M, 2 * S, gates * S, dA_lvl, 2 * S, 0,
+                         npass_of(m->prec), nullptr, 0, st));
     else
       FOLD_TRY(launch_gemm_dA_simt(M, S, gates, (const float *)b.dZ + (size_t)c0 * b.ld_z, b.ld_z, m->U, dA_lvl, st));
   }
@@ -329,6 +380,10 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
                           ScatterA{s->cons_off, s->cons_edge, (__nv_bfloat16 *)(a + L.al_off),
                                    (__nv_bfloat16 *)(a + L.ar_off), L.ld},
                           grads->dU, acc, b.dU_split, grads->db, b.partial, st));  // (+ db, fused)
+    else if (b.Utf)  // dU = dZ^T Acat: both operands MN-major (cells are the reduction)
+      FOLD_TRY(gemm_tf32(TfOperand{(const float *)b.dZ, b.ld_z, 1},
+                         TfOperand{(const float *)(a + L.al_off), tf_ld_a(S), 1}, gates * S, 2 * S, nc, grads->dU,
+                         2 * S, acc, npass_of(m->prec), b.dU_split, b.tf_split_floats, st));
     else
       FOLD_TRY(launch_gemm_dU_simt(nc, nl, S, gates, (const float *)b.dZ, b.ld_z, s->gather, (const float *)H, L.ld,
                                    grads->dU, acc, st));
@@ -399,6 +454,16 @@ int32_t fold_debug_fwd_trace(unsigned long long *host, int32_t n_tiles) {
 int32_t fold_debug_bwd_trace(unsigned long long *host, int32_t n_tiles) {
   return fold::tc_debug_bwd_trace(host, n_tiles);
 }
+
+/* instrumentation / tests: one k_gemm_tf32 GEMM (the FP32 / TF32 modes' contraction) */
+fold_status fold_debug_gemm_tf32(const float *A, int64_t lda, int32_t a_mn, const float *B, int64_t ldb,
+                                 int32_t b_mn, int32_t M, int32_t N, int32_t K, float *C, int64_t ldc,
+                                 int32_t accumulate, int32_t npass, float *ws, int64_t ws_floats, void *stream) {
+  if (M < 0 || N < 0 || K < 0 || !A || !B || !C) return FOLD_E_INVALID;
+  return fold::gemm_tf32(fold::TfOperand{A, lda, a_mn}, fold::TfOperand{B, ldb, b_mn}, M, N, K, C, ldc, accumulate,
+                         npass, ws, ws_floats, (cudaStream_t)stream);
+}
+int64_t fold_debug_gemm_tf32_ws(int32_t M, int32_t N, int32_t K) { return fold::gemm_tf32_split_floats(M, N, K); }
 
 fold_status fold_device_check(void) {
   int dev = 0, major = 0, minor = 0;

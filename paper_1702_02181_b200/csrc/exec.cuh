@@ -127,4 +127,37 @@ fold_status tc_gemm_dU(int n_cells, int S, int gates, const __nv_bfloat16 *dZ, i
                        float *dU, int accumulate, float *split_ws, float *db, float *db_ws,
                        cudaStream_t st);
 
+// out[i] = (accumulate ? out[i] : 0) + sum_{s < nsplit} part[s][i] in fixed order
+fold_status launch_reduce_splits(int64_t n, int nsplit, const float *part, float *out, int accumulate,
+                                 cudaStream_t st);
+
+// --- tcgen05 TF32 GEMM (gemm_tf32.cu): the FP32 (3xTF32) and TF32 modes' contractions.
+// An operand is a row-major fp32 matrix in global memory read either K-major (rows = M or
+// N, K contiguous) or MN-major (rows = K, M or N contiguous); ld in elements, ld * 4 and the
+// base 16-byte aligned (TMA).
+struct TfOperand {
+  const float *p;
+  int64_t ld;
+  int mn_major;
+};
+// C[M][N] (ldc) = A * B (accumulate: C +=) with fp32 accumulation in TMEM. npass = 1: one
+// kind::tf32 MMA per K step (TF32 mode); npass = 3: 3xTF32 (A_hi B_hi + A_hi B_lo +
+// A_lo B_hi, the lo parts split in shared memory): fp32-class accuracy (FP32 mode).
+// split_ws (nullable, split_ws_floats capacity): split-K partials for small tile counts,
+// reduced in fixed order (deterministic).
+fold_status gemm_tf32(const TfOperand &A, const TfOperand &B, int M, int N, int K, float *C, int64_t ldc,
+                      int accumulate, int npass, float *split_ws, int64_t split_ws_floats, cudaStream_t st);
+int64_t gemm_tf32_split_floats(int M, int N, int K);
+// FP32 / TF32 mode level helpers (gemm_tf32.cu)
+// Acat[c][0:S] = H[gather[2r]], Acat[c][S:2S] = H[gather[2r+1]] for rows r in [r0, r1), c = r - nl
+fold_status launch_gather_cat(int r0, int r1, int nl, int S, int ld, const int32_t *gather, const float *H,
+                              float *Acat, int64_t ld_a, cudaStream_t st);
+// Z rows of the level are in Gact (gate g of column j at g*ld + j): gates, c, h in place
+fold_status launch_cell_fwd_pw(int cell, int r0, int r1, int nl, int S, int ld, int ld_g, const int32_t *gather,
+                               const float *b, float *H, float *C, float *Gact, cudaStream_t st);
+// U copies for the TF32 GEMMs: fwd rows gate-padded (row g*ld + j <- U row g*S + j, zero for
+// j >= S), bwd rows natural; both [rows][ld_u] with ld_u = round_up(2S, 4)
+int64_t tf_ld_u(int S);
+fold_status launch_prep_U_tf(int gates, int S, int ld, const float *U, float *Ufwd, float *Ubwd, cudaStream_t st);
+
 }  // namespace fold

@@ -1988,6 +1988,8 @@ __global__ void k_reduce_splits(int64_t n, int nsplit, const float *__restrict__
   }
 }
 
+}  // namespace
+
 fold_status launch_reduce_splits(int64_t n, int nsplit, const float *part, float *out, int accumulate,
                                  cudaStream_t st) {
   if (n <= 0) return FOLD_OK;
@@ -1998,6 +2000,8 @@ fold_status launch_reduce_splits(int64_t n, int nsplit, const float *part, float
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
+
+namespace {
 
 // =================================================================== weight prep
 // Ub[r][half*Sp + k] = bf16(U[r][half*S + k]) for k < S, 0 for k in [S, Sp) (Sp =
@@ -2038,6 +2042,8 @@ __global__ void k_prep_U(int64_t rows, int S, int Sp, const float *__restrict__ 
   }
 }
 
+}  // namespace
+
 // =================================================================== host helpers
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -2066,6 +2072,8 @@ fold_status make_map_ex(CUtensorMap *m, const void *ptr, CUtensorMapDataType dt,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? FOLD_OK : FOLD_E_CUDA;
 }
+namespace {
+
 // bf16 operand map with 128B swizzle (UMMA operand tiles)
 fold_status make_map(CUtensorMap *m, const void *ptr, uint64_t cols, uint64_t rows, uint64_t row_bytes,
                      uint32_t box_cols, uint32_t box_rows) {

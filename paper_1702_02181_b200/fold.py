@@ -26,7 +26,7 @@ STATUS = {0: "OK", 1: "INVALID", 2: "CHILD_RANGE", 3: "ARITY", 4: "TOKEN_RANGE",
           6: "CYCLE", 7: "WORKSPACE", 8: "CUDA", 9: "MISMATCH", 10: "OP_RANGE", 11: "UNSUPPORTED",
           12: "LEVEL"}
 CELLS = {"treernn": 0, "treelstm": 1}
-PRECS = {"fp32": 0, "bf16": 2}
+PRECS = {"fp32": 0, "tf32": 1, "bf16": 2}
 
 _i32p = ctypes.POINTER(ctypes.c_int32)
 _f32p = ctypes.POINTER(ctypes.c_float)
@@ -118,6 +118,11 @@ def load() -> ctypes.CDLL:
     L.fold_debug_bwd_trace.restype = i32
     L.fold_debug_sched_trace.argtypes = [vp]
     L.fold_debug_sched_trace.restype = i32
+    L.fold_debug_gemm_tf32.restype = i32
+    L.fold_debug_gemm_tf32.argtypes = [vp, ctypes.c_int64, i32, vp, ctypes.c_int64, i32, i32, i32, i32, vp,
+                                       ctypes.c_int64, i32, i32, vp, ctypes.c_int64, vp]
+    L.fold_debug_gemm_tf32_ws.restype = ctypes.c_int64
+    L.fold_debug_gemm_tf32_ws.argtypes = [i32, i32, i32]
     _lib = L
     return L
 
@@ -126,7 +131,7 @@ EXPORTED = ("fold_schedule_workspace", "fold_schedule", "fold_acts_layout", "fol
             "fold_forward", "fold_backward_workspace", "fold_backward", "fold_sgd_update",
             "fold_status_string", "fold_last_error_detail", "fold_last_error_context", "fold_abi_version", "fold_device_check",
             "fold_launch_count", "fold_profile_enable", "fold_profile_read", "fold_debug_fwd_trace", "fold_debug_bwd_trace",
-            "fold_debug_sched_trace")
+            "fold_debug_sched_trace", "fold_debug_gemm_tf32", "fold_debug_gemm_tf32_ws")
 
 PROF_CLASSES = ("schedule", "embed_fwd", "cell_fwd", "bwd_pointwise", "gemm_dA", "gemm_dU", "embed_bwd",
                 "db_colsum", "sgd", "weight_prep", "root_out")
@@ -397,6 +402,21 @@ def backward(sched: Schedule, model: Model, acts: Acts, dh_root: torch.Tensor, d
                            _ptr(dh_root), _ptr(dc_root), ctypes.byref(gs), ctypes.c_void_p(bbuf.data_ptr()), bws,
                            _stream(stream)), "fold_backward")
     return dU, db, dE
+
+
+def debug_gemm_tf32(A: torch.Tensor, B: torch.Tensor, M: int, N: int, K: int, a_mn: bool, b_mn: bool,
+                    npass: int, C: torch.Tensor | None = None, accumulate: bool = False, stream=None):
+    """fold_debug_gemm_tf32 (test hook): C = A * B on the tcgen05 TF32 GEMM of the FP32 /
+    TF32 modes. A: [M][K] (or [K][M] if a_mn), B: [N][K] (or [K][N] if b_mn), fp32 2-D."""
+    L = load()
+    if C is None:
+        C = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    nws = int(L.fold_debug_gemm_tf32_ws(M, N, K))
+    ws = torch.empty(max(nws, 1), dtype=torch.float32, device=A.device)
+    _check(L.fold_debug_gemm_tf32(_ptr(A), A.stride(0), int(a_mn), _ptr(B), B.stride(0), int(b_mn), M, N, K,
+                                  _ptr(C), C.stride(0), int(accumulate), npass, _ptr(ws), nws, _stream(stream)),
+           "fold_debug_gemm_tf32")
+    return C
 
 
 def sgd_update(param: torch.Tensor, grad: torch.Tensor, lr: float, stream=None):
