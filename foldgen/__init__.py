@@ -35,6 +35,8 @@ CELL = 1
 GRAPH_SEED = 1702
 PARAM_SEED = 2181
 GRAD_SEED = 17022181
+LABEL_SEED = 297  # §3.5 synthetic per-node sentiment labels
+SST_CLASSES = 5
 
 
 @dataclasses.dataclass
@@ -305,3 +307,30 @@ def permute_nodes(gr: Graphs, perm: np.ndarray) -> Graphs:
     token = gr.token[perm].copy()
     root = inv[gr.root].astype(np.int32)
     return Graphs(op, child, token, root, gr.vocab, gr.tree_sizes.copy())
+
+
+# ----------------------------------------------------------------------------- §3.5 model (NEXT-2)
+
+@dataclasses.dataclass
+class SstParams:
+    W: np.ndarray   # [3S, S] leaf input weights, row blocks i, o, u (Tai W^(i), W^(o), W^(u))
+    Ws: np.ndarray  # [C, S] per-node classifier
+    bs: np.ndarray  # [C]
+
+
+def make_sst_params(S: int, C: int = SST_CLASSES, seed: int = PARAM_SEED + 1) -> SstParams:
+    """W ~ U(+-sqrt(6/(S + 3S))), Ws ~ U(+-sqrt(6/(S + C))), bs ~ U(+-0.1)."""
+    rng = np.random.default_rng(seed)
+    a = np.sqrt(6.0 / (4 * S))
+    W = rng.uniform(-a, a, size=(3 * S, S)).astype(np.float32)
+    a2 = np.sqrt(6.0 / (S + C))
+    Ws = rng.uniform(-a2, a2, size=(C, S)).astype(np.float32)
+    bs = rng.uniform(-0.1, 0.1, size=(C,)).astype(np.float32)
+    return SstParams(W, Ws, bs)
+
+
+def make_labels(N: int, C: int = SST_CLASSES, seed: int = LABEL_SEED) -> np.ndarray:
+    """Synthetic per-node labels in node-id order (SST labels every node, PAPER.md L297;
+    no dataset: uniform over the C classes)."""
+    rng = np.random.default_rng(seed)
+    return rng.integers(0, C, size=N).astype(np.int32)

@@ -8,6 +8,7 @@ the product; the two share only the seeded input generators in `foldgen`.
 Contents
   fold_oracle.c  plain C, fp64: schedule by definition, node-at-a-time forward,
                  level-ordered forward (self-check), hand-derived backward.
+                 §3.5 model (leaf TreeLSTM(E[w],0,0) + per-node softmax CE).
   paper_form.py  the paper-form schedule with pass-through operations and (d,t,i)
                  edge labels, pure Python, for Fig. 1 parity.
 
@@ -158,3 +159,39 @@ def backward(cell, op, child, token, root, U, b, E, dh_root, dc_root=None):
     if st != 0:
         raise OracleError(st)
     return dU, db, dE
+
+
+def sst_forward(op, child, token, label, U, b, E, W, Ws, bs, all_nodes=False):
+    """§3.5 model (fold_oracle.c oracle_sst_forward): total per-node
+    softmax cross-entropy over all nodes; with all_nodes=True also (H[N,S], C[N,S])."""
+    lib = _load()
+    op, child, token, label = _i32(op), _i32(child).reshape(-1), _i32(token), _i32(label)
+    U, b, E, W, Ws, bs = (_f64(x) for x in (U, b, E, W, Ws, bs))
+    N = len(op)
+    V, S = E.shape
+    C = bs.shape[0]
+    loss = np.zeros(1)
+    H = np.zeros((N, S)) if all_nodes else None
+    Cs = np.zeros((N, S)) if all_nodes else None
+    st = lib.oracle_sst_forward(S, N, V, C, _p(op), _p(child), _p(token), _p(label), _p(U), _p(b), _p(E), _p(W),
+                                _p(Ws), _p(bs), _p(loss), _p(H), _p(Cs))
+    if st != 0:
+        raise OracleError(st)
+    return (float(loss[0]), H, Cs) if all_nodes else float(loss[0])
+
+
+def sst_backward(op, child, token, label, U, b, E, W, Ws, bs):
+    """Reverse mode of the §3.5 loss: (loss, dU, db, dE, dW, dWs, dbs)."""
+    lib = _load()
+    op, child, token, label = _i32(op), _i32(child).reshape(-1), _i32(token), _i32(label)
+    U, b, E, W, Ws, bs = (_f64(x) for x in (U, b, E, W, Ws, bs))
+    N = len(op)
+    V, S = E.shape
+    C = bs.shape[0]
+    loss = np.zeros(1)
+    out = [np.zeros_like(x) for x in (U, b, E, W, Ws, bs)]
+    st = lib.oracle_sst_backward(S, N, V, C, _p(op), _p(child), _p(token), _p(label), _p(U), _p(b), _p(E), _p(W),
+                                 _p(Ws), _p(bs), _p(loss), *[_p(x) for x in out])
+    if st != 0:
+        raise OracleError(st)
+    return (float(loss[0]), *out)

@@ -22,6 +22,10 @@
  *   oracle_backward      — hand-derived reverse mode ("gradients ...
  *                          do not require any additional code" in TF; here written
  *                          out), pinned by finite differences in tests/.
+ *   oracle_sst_forward / oracle_sst_backward
+ *                        — the §3.5 sentiment model: leaves
+ *                          h = TreeLSTM(E[w], 0, 0), internal TreeLSTM(0, h_L, h_R),
+ *                          5-way softmax cross-entropy at every node (NEXT-2).
  * All floating point is fp64; parameters arrive as fp64 copies of the fp32 masters.
  *
  * Cell equations (Tai et al. eqs 9-14 with x = 0, N = 2, cited
@@ -473,5 +477,206 @@ int oracle_backward(int cell, int S, int N, int G, int V,
     }
 done:
     free(H); free(C); free(A); free(dH); free(dC); free(z); free(dz); free(topo);
+    return st;
+}
+
+/* ---------------------------------------------------------------- §3.5 model (NEXT-2)
+ * The sentiment model of PAPER.md L297-304 (§3.5 "Recursive definitions"):
+ *   h_word = TreeLSTM(Embedding(word), 0, 0)           (L300, leaves)
+ *   h_{left,right} = TreeLSTM(0, h_left, h_right)       (L301, internal nodes)
+ * with TreeLSTM = Tai et al. eqs 9-14, N = 2 (L304), and a per-node 5-way softmax
+ * classifier with cross-entropy, "every node has a sentiment label" (L297).
+ * Leaf (x = E[token], h_L = h_R = 0, c_L = c_R = 0; W = the input weights W^(i), W^(o),
+ * W^(u) stacked as row blocks of W[3S][S]; the bias b is the cell's, blocks i, o, u):
+ *   i = s(W_i x + b_i), o = s(W_o x + b_o), u = tanh(W_u x + b_u)
+ *   c = i*u   (the forget-gate terms f_k * c_k vanish: c_k = 0, so W^(f) never matters)
+ *   h = o*tanh(c)
+ * Internal nodes: the x = 0 cell above (cell_forward, TreeLSTM).
+ * Every node n: l = Ws h_n + bs (Ws[C][S], bs[C]), p = softmax(l),
+ *   loss_n = log(sum_k exp(l_k)) - l[label[n]];   L = sum over all nodes of loss_n.
+ */
+static void leaf_forward(int S, const double *W, const double *b, const double *x, double *h, double *c, double *act)
+{
+    for (int j = 0; j < S; j++) {
+        double zi = b[j], zo = b[3 * S + j], zu = b[4 * S + j];
+        const double *wi = W + (size_t)j * S, *wo = W + (size_t)(S + j) * S, *wu = W + (size_t)(2 * S + j) * S;
+        for (int k = 0; k < S; k++) { zi += wi[k] * x[k]; zo += wo[k] * x[k]; zu += wu[k] * x[k]; }
+        double i = sigm(zi), o = sigm(zo), u = tanh(zu);
+        c[j] = i * u;
+        h[j] = o * tanh(c[j]);
+        if (act) { act[j] = i; act[S + j] = o; act[2 * S + j] = u; }
+    }
+}
+
+/* log-softmax cross-entropy of one node: returns loss_n, writes dl = p - e_y */
+static double node_ce(int S, int C, const double *Ws, const double *bs, const double *h, int y, double *dl)
+{
+    double mx = -INFINITY;
+    for (int k = 0; k < C; k++) {
+        double l = bs[k];
+        for (int j = 0; j < S; j++) l += Ws[(size_t)k * S + j] * h[j];
+        dl[k] = l;
+        if (l > mx) mx = l;
+    }
+    double se = 0.0;
+    for (int k = 0; k < C; k++) se += exp(dl[k] - mx);
+    double lse = mx + log(se);
+    double loss = lse - dl[y];
+    for (int k = 0; k < C; k++) dl[k] = exp(dl[k] - lse) - (k == y ? 1.0 : 0.0);
+    return loss;
+}
+
+static int sst_eval(int S, int N, const int32_t *op, const int32_t *child, const int32_t *token,
+                    const double *U, const double *b, const double *E, const double *W,
+                    double *H, double *Cs, double *A, double *AL, int32_t *topo)
+{
+    int st = topo_order(N, op, child, topo);
+    if (st != OR_OK) return st;
+    double *z = malloc(sizeof(double) * 5 * (size_t)S);
+    for (int t = 0; t < N; t++) {
+        int n = topo[t];
+        double *h = H + (size_t)n * S, *c = Cs + (size_t)n * S;
+        if (op[n] == OR_EMBED) {
+            leaf_forward(S, W, b, E + (size_t)token[n] * S, h, c, AL ? AL + (size_t)n * 3 * S : NULL);
+        } else {
+            int L = child[2 * n], R = child[2 * n + 1];
+            cell_forward(OR_TREELSTM, S, U, b, H + (size_t)L * S, Cs + (size_t)L * S, H + (size_t)R * S,
+                         Cs + (size_t)R * S, h, c, z, A ? A + (size_t)n * 5 * S : NULL);
+        }
+    }
+    free(z);
+    return OR_OK;
+}
+
+/* Forward of the §3.5 model: total loss, optionally every node's h / c (node-id order). */
+int oracle_sst_forward(int S, int N, int V, int C, const int32_t *op, const int32_t *child, const int32_t *token,
+                       const int32_t *label, const double *U, const double *b, const double *E, const double *W,
+                       const double *Ws, const double *bs, double *loss, double *H_all, double *C_all)
+{
+    if (S <= 0 || C <= 0) return OR_E_INVALID;
+    int32_t err;
+    int32_t root0 = 0;
+    int st = validate(N, 0, V, op, child, token, &root0, &err);
+    if (st) return st;
+    for (int n = 0; n < N; n++)
+        if (label[n] < 0 || label[n] >= C) return OR_E_INVALID;
+    double *H = H_all ? H_all : malloc(sizeof(double) * (size_t)N * S + 8);
+    double *Cs = C_all ? C_all : malloc(sizeof(double) * (size_t)N * S + 8);
+    int32_t *topo = malloc(sizeof(int32_t) * ((size_t)N + 1));
+    double *dl = malloc(sizeof(double) * (size_t)C);
+    st = sst_eval(S, N, op, child, token, U, b, E, W, H, Cs, NULL, NULL, topo);
+    if (st == OR_OK) {
+        double L = 0.0;
+        for (int n = 0; n < N; n++) L += node_ce(S, C, Ws, bs, H + (size_t)n * S, label[n], dl);
+        *loss = L;
+    }
+    free(topo); free(dl);
+    if (!H_all) free(H);
+    if (!C_all) free(Cs);
+    return st;
+}
+
+/* Reverse mode of the §3.5 loss (hand-derived; pinned by finite differences in tests/):
+ * every node first gets its classifier's dh += Ws^T (p - e_y), dWs += (p - e_y) (x) h,
+ * dbs += p - e_y; then nodes in reverse topological order: cells as oracle_backward;
+ * leaves: tc = tanh(c); do = dh*tc; dc' = dc + dh*o*(1-tc^2);
+ *   dz_i = dc'*u*i(1-i), dz_o = do*o(1-o), dz_u = dc'*i*(1-u^2);
+ *   dW_g += dz_g (x) x, db[block g] += dz_g (g in i, o, u), dE[token] += sum_g W_g^T dz_g.
+ * All outputs overwritten. */
+int oracle_sst_backward(int S, int N, int V, int C, const int32_t *op, const int32_t *child, const int32_t *token,
+                        const int32_t *label, const double *U, const double *b, const double *E, const double *W,
+                        const double *Ws, const double *bs, double *loss, double *dU, double *db, double *dE,
+                        double *dW, double *dWs, double *dbs)
+{
+    if (S <= 0 || C <= 0) return OR_E_INVALID;
+    int32_t err, root0 = 0;
+    int st = validate(N, 0, V, op, child, token, &root0, &err);
+    if (st) return st;
+    for (int n = 0; n < N; n++)
+        if (label[n] < 0 || label[n] >= C) return OR_E_INVALID;
+    size_t NS = (size_t)N * S;
+    double *H = malloc(sizeof(double) * NS + 8), *Cs = malloc(sizeof(double) * NS + 8);
+    double *A = malloc(sizeof(double) * NS * 5 + 8), *AL = malloc(sizeof(double) * NS * 3 + 8);
+    double *dH = calloc(NS + 1, sizeof(double)), *dC = calloc(NS + 1, sizeof(double));
+    double *dz = malloc(sizeof(double) * 5 * (size_t)S), *dl = malloc(sizeof(double) * (size_t)C);
+    int32_t *topo = malloc(sizeof(int32_t) * ((size_t)N + 1));
+    st = sst_eval(S, N, op, child, token, U, b, E, W, H, Cs, A, AL, topo);
+    if (st != OR_OK) goto done;
+    memset(dU, 0, sizeof(double) * (size_t)5 * S * 2 * S);
+    memset(db, 0, sizeof(double) * (size_t)5 * S);
+    memset(dE, 0, sizeof(double) * (size_t)V * S);
+    memset(dW, 0, sizeof(double) * (size_t)3 * S * S);
+    memset(dWs, 0, sizeof(double) * (size_t)C * S);
+    memset(dbs, 0, sizeof(double) * (size_t)C);
+    double L = 0.0;
+    for (int n = 0; n < N; n++) {
+        const double *h = H + (size_t)n * S;
+        L += node_ce(S, C, Ws, bs, h, label[n], dl);
+        for (int k = 0; k < C; k++) {
+            dbs[k] += dl[k];
+            for (int j = 0; j < S; j++) {
+                dWs[(size_t)k * S + j] += dl[k] * h[j];
+                dH[(size_t)n * S + j] += Ws[(size_t)k * S + j] * dl[k];
+            }
+        }
+    }
+    *loss = L;
+    for (int t = N - 1; t >= 0; t--) {
+        int n = topo[t];
+        double *dh = dH + (size_t)n * S, *dc = dC + (size_t)n * S;
+        const double *c = Cs + (size_t)n * S;
+        if (op[n] == OR_EMBED) {
+            const double *a = AL + (size_t)n * 3 * S, *x = E + (size_t)token[n] * S;
+            for (int j = 0; j < S; j++) {
+                double i = a[j], o = a[S + j], u = a[2 * S + j];
+                double tc = tanh(c[j]);
+                double dO = dh[j] * tc;
+                double dcc = dc[j] + dh[j] * o * (1.0 - tc * tc);
+                dz[j] = dcc * u * i * (1.0 - i);
+                dz[S + j] = dO * o * (1.0 - o);
+                dz[2 * S + j] = dcc * i * (1.0 - u * u);
+            }
+            const int blk[3] = {0, 3, 4};  /* bias blocks of i, o, u */
+            double *de = dE + (size_t)token[n] * S;
+            for (int g = 0; g < 3; g++)
+                for (int j = 0; j < S; j++) {
+                    double d = dz[g * S + j];
+                    const double *w = W + (size_t)(g * S + j) * S;
+                    double *dw = dW + (size_t)(g * S + j) * S;
+                    db[blk[g] * S + j] += d;
+                    for (int k = 0; k < S; k++) { dw[k] += d * x[k]; de[k] += w[k] * d; }
+                }
+            continue;
+        }
+        int Lc = child[2 * n], R = child[2 * n + 1];
+        const double *a = A + (size_t)n * 5 * S;
+        const double *hL = H + (size_t)Lc * S, *hR = H + (size_t)R * S;
+        const double *cL = Cs + (size_t)Lc * S, *cR = Cs + (size_t)R * S;
+        for (int j = 0; j < S; j++) {
+            double i = a[j], fl = a[S + j], fr = a[2 * S + j], o = a[3 * S + j], u = a[4 * S + j];
+            double tc = tanh(c[j]);
+            double dO = dh[j] * tc;
+            double dcc = dc[j] + dh[j] * o * (1.0 - tc * tc);
+            dz[j] = dcc * u * i * (1.0 - i);
+            dz[S + j] = dcc * cL[j] * fl * (1.0 - fl);
+            dz[2 * S + j] = dcc * cR[j] * fr * (1.0 - fr);
+            dz[3 * S + j] = dO * o * (1.0 - o);
+            dz[4 * S + j] = dcc * i * (1.0 - u * u);
+            dC[(size_t)Lc * S + j] += dcc * fl;
+            dC[(size_t)R * S + j] += dcc * fr;
+        }
+        for (int r = 0; r < 5 * S; r++) {
+            double *du = dU + (size_t)r * 2 * S;
+            for (int k = 0; k < S; k++) { du[k] += dz[r] * hL[k]; du[S + k] += dz[r] * hR[k]; }
+            db[r] += dz[r];
+        }
+        double *dhL = dH + (size_t)Lc * S, *dhR = dH + (size_t)R * S;
+        for (int r = 0; r < 5 * S; r++) {
+            const double *u = U + (size_t)r * 2 * S;
+            for (int k = 0; k < S; k++) { dhL[k] += u[k] * dz[r]; dhR[k] += u[S + k] * dz[r]; }
+        }
+    }
+done:
+    free(H); free(Cs); free(A); free(AL); free(dH); free(dC); free(dz); free(dl); free(topo);
     return st;
 }
