@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["fold", "reference"], default="fold")
+    ap.add_argument("--model", choices=["r1", "sst"], default="r1",
+                    help="r1: the headline TreeLSTM (leaf = embedding lookup, root gradient); sst: the §3.5 "
+                         "sentiment model (NEXT-2)")
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--batch", type=int, default=None, help="trees per GPU (default: config's full size)")
     ap.add_argument("--prec", default="bf16", choices=["bf16", "tf32", "fp32"])
@@ -755,10 +758,151 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+# ============================================================================ §3.5 model (NEXT-2)
+
+def run_sst(args):
+    """--model sst: the §3.5 sentiment model (leaf TreeLSTM(E[w],0,0),
+    internal TreeLSTM(0,h_L,h_R), 5-way softmax cross-entropy at every node) training step
+    = fold_schedule + fold_sst_forward + fold_sst_backward + SGD over all parameters, on
+    parse-shaped trees (C3 shapes, S = 300, synthetic uniform labels); FP32 (3xTF32) or TF32
+    tensor-core GEMMs. One GPU (rank 0 prints)."""
+    import torch
+    from paper_1702_02181_b200 import fold
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    fold.device_check()
+    prec = args.prec if args.prec != "bf16" else "fp32"
+    cfg = args.config if args.config in ("c2", "c3", "c5") else "c3"
+    gr = foldgen.make_config(cfg, args.batch or DEFAULT_B[cfg])
+    S = foldgen.CONFIG_STATE[cfg]
+    V = gr.vocab
+    p = foldgen.make_params("treelstm", S, V)
+    q = foldgen.make_sst_params(S)
+    y = foldgen.make_labels(gr.n_nodes)
+    sizes = [p.U.size, p.b.size, p.E.size, q.W.size, q.Ws.size, q.bs.size]
+    flat_p = torch.empty(sum(sizes), dtype=torch.float32, device=dev)
+    flat_g = torch.zeros_like(flat_p)
+
+    def views(buf):
+        out, o = [], 0
+        for a, n in zip((p.U, p.b, p.E, q.W, q.Ws, q.bs), sizes):
+            out.append(buf[o:o + n].view(a.shape))
+            o += n
+        return out
+    P, Gr = views(flat_p), views(flat_g)
+    for d, a in zip(P, (p.U, p.b, p.E, q.W, q.Ws, q.bs)):
+        d.copy_(torch.from_numpy(a))
+    model = fold.Model(P[0], P[1], P[2], prec=prec)
+    head = fold.SstHead(P[3], P[4], P[5], torch.from_numpy(y).to(dev))
+    op, child, token, root = fold.graphs_to_device(gr, dev)
+    ws = fold.Workspace(dev)
+    n_cells = int((gr.op == 1).sum())
+
+    def step(o):
+        s = fold.schedule(*o, V, workspace=ws.get("sched", int(fold.load().fold_schedule_workspace(
+            o[0].shape[0], o[3].shape[0]))))
+        loss, acts = fold.sst_forward(s, model, head, ws=ws)
+        fold.sst_backward(s, model, head, acts, grads=tuple(Gr), ws=ws)
+        fold.sgd_update(flat_p, flat_g, args.lr)
+        return loss
+    for _ in range(max(args.warmup, 3)):
+        step((op, child, token, root))
+    torch.cuda.synchronize()
+    import gc
+    gc.collect()
+    gc.disable()
+    clocks = ClockSampler(0) if not args.no_clocks else None
+    if clocks:
+        clocks.start()
+    fold.launch_count(reset=True)
+    fold.profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step((op, child, token, root))
+    e1.record()
+    torch.cuda.synchronize()
+    launches = fold.launch_count()
+    prof = fold.profile_read()
+    fold.profile_enable(False)
+    clk = clocks.stop() if clocks else None
+    ms = e0.elapsed_time(e1) / args.steps
+    value = gr.n_nodes / (ms / 1e3)
+    # e2e: graph arrays + labels H2D from pinned memory, the loss D2H, every step
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    hs = [pin(a.astype(np.int32)) for a in (gr.op, gr.child, gr.token, gr.root, y)]
+    ds = [torch.empty_like(h, device=dev) for h in hs]
+    hloss = torch.empty(1, dtype=torch.float32).pin_memory()
+    h2d = sum(h.numel() * 4 for h in hs)
+
+    def e2e_step():
+        for d, h in zip(ds, hs):
+            d.copy_(h, non_blocking=True)
+        head.label = ds[4]
+        loss = step(tuple(ds[:4]))
+        hloss.copy_(loss, non_blocking=True)
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    a1.record()
+    torch.cuda.synchronize()
+    e_ms = a0.elapsed_time(a1) / args.steps
+    per_class = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
+                 for k, v in prof.items() if v[1] > 0}
+    # roofline: the three cell GEMM passes + the leaf level's (K = S, N = 5S padded: 10 S^2 per
+    # leaf forward, 2 x 10 S^2 backward) on the TF32 peak (3xTF32: a third of it)
+    pk, pk_src = peaks()
+    scale = 0.5 if prec == "tf32" else 0.5 / 3
+    full_clock = bool(clk and clk.get("sm_max_mhz") and clk["sm_mhz"] >= 0.95 * clk["sm_max_mhz"])
+    peak = pk["bf16_tflops"] * scale if (full_clock or clk is None) else pk["bf16_tflops_sustained"] * scale
+    n_leaves = gr.n_nodes - n_cells
+    flops = 3 * 20.0 * S * S * n_cells + 3 * 10.0 * S * S * n_leaves
+    gemm_ms = sum(per_class.get(k, {}).get("ms_per_step", 0.0) for k in ("cell_fwd", "gemm_dA", "gemm_dU",
+                                                                          "embed_fwd", "embed_bwd"))
+    achieved = flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle
+        sub = foldgen.sub_batch(gr, 0, min(16, gr.n_graphs))
+        t0 = time.perf_counter()
+        oracle.sst_backward(sub.op, sub.child, sub.token, y[:sub.n_nodes], p.U, p.b, p.E, q.W, q.Ws, q.bs)
+        dt = time.perf_counter() - t0
+        cpu = {"value": sub.n_nodes / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"first {sub.n_graphs} trees ({sub.n_nodes} nodes), fp64 §3.5 forward+backward "
+                         f"(oracle_sst_backward), single thread, {dt:.1f} s"}
+    out = {"metric": "§3.5 TreeLSTM sentiment model tree nodes/sec fwd+bwd (NEXT-2)", "value": value, "unit": UNIT,
+           "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+           "config": {"workload": f"{cfg.upper()} tree shapes, B={gr.n_graphs}, S={S}, V={V}, 5 classes, "
+                                  f"labels at every node (PAPER.md L297), leaf TreeLSTM(E[w],0,0)",
+                      "nodes": gr.n_nodes, "cells": n_cells, "leaves": n_leaves,
+                      "step": "schedule+sst_fwd+sst_bwd+sgd", "l2": "no flush (working set > L2 at B=1024)"},
+           "gpu_launches": int(launches), "kernels": per_class,
+           "roofline": {"bound": "tensor", "kernel": "k_gemm_tf32 (all GEMM passes)", "achieved": achieved,
+                        "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": None,
+                        "peak_source": f"{pk_src} bf16 x {scale:.4f} ({prec}: TF32 = bf16/2 nominal"
+                                       f"{', 3 MMA passes' if prec == 'fp32' else ''})",
+                        "algorithmic": "60 S^2 FLOP per cell + 30 S^2 per leaf (padded 5-gate leaf GEMMs)"},
+           "cpu_baseline": cpu,
+           "e2e": {"value": gr.n_nodes / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms, "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": 4},
+           "clocks": clk}
+    print(json.dumps(out), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.model == "sst":
+        run_sst(args)
     else:
         run_fold(args)
 

@@ -55,7 +55,7 @@
 extern "C" {
 #endif
 
-#define FOLD_ABI_VERSION 4
+#define FOLD_ABI_VERSION 5
 
 typedef enum {
   FOLD_OK = 0,
@@ -236,6 +236,45 @@ fold_status fold_backward(const fold_schedule_t *sched, const fold_model *model,
                           const void *d_acts, const float *d_dh_root, const float *d_dc_root,
                           fold_grads *grads, void *d_workspace, size_t workspace_bytes,
                           void *stream);
+
+/* ----------------------------------------------------------------- §3.5 model (NEXT-2)
+ * The sentiment model of PAPER.md L297-304: leaves h = TreeLSTM(Embedding(word), 0, 0)
+ * (L300), internal nodes TreeLSTM(0, h_L, h_R) (L301), Tai et al. eqs 9-14 with N = 2
+ * (L304), and a softmax classifier with cross-entropy at EVERY node ("every node has a
+ * sentiment label", L297). Loss L = sum over all nodes n of -log softmax(Ws h_n + bs)[label].
+ * The model's U, b, E are the fold_model's (cell must be FOLD_CELL_TREELSTM; prec FOLD_PREC_FP32
+ * or FOLD_PREC_TF32, else FOLD_E_UNSUPPORTED); b's i, o, u blocks are shared by leaves and
+ * cells. The leaf forget gates never contribute (c_L = c_R = 0, Tai eq 13), so there is no
+ * W^(f). Roots play no special role (fold_graphs.root is only validated). All device:
+ *   W[3S][S]         leaf input weights, row blocks (i, o, u); 16-byte aligned
+ *   Ws[C][S], bs[C]  classifier; Ws 16-byte aligned
+ *   label[n_nodes]   class of each node in NODE-ID order, in [0, C) (else the loss is NaN)
+ *   n_classes        C in [1, 8] (5 for SST) */
+typedef struct {
+  const float *W, *Ws, *bs;
+  const int32_t *label;
+  int32_t n_classes;
+} fold_sst;
+/* gradients of W, Ws, bs (layouts as above), 16-byte aligned; fold_grads.accumulate applies */
+typedef struct {
+  float *dW, *dWs, *dbs;
+} fold_sst_grads;
+
+/* Activation buffer of the §3.5 model (its own layout; H / C fp32 for every pool row, saved
+ * gates of leaves then cells at g_off) */
+fold_status fold_sst_acts_layout(const fold_schedule_t *sched, const fold_model *model, const fold_sst *sst,
+                                 fold_acts_layout_t *layout);
+size_t fold_sst_forward_workspace(const fold_schedule_t *sched, const fold_model *model, const fold_sst *sst);
+/* d_loss: device float[1] <- L. Per level a tcgen05 TF32 GEMM (the leaf level's A = the
+ * embedding gather), a pointwise step, then the per-node classifier. */
+fold_status fold_sst_forward(const fold_schedule_t *sched, const fold_model *model, const fold_sst *sst,
+                             void *d_acts, float *d_loss, void *d_workspace, size_t workspace_bytes,
+                             void *stream);
+size_t fold_sst_backward_workspace(const fold_schedule_t *sched, const fold_model *model, const fold_sst *sst);
+/* dL/d(U, b, E) into grads (sweep_done_event ignored) and dL/d(W, Ws, bs) into sst_grads. */
+fold_status fold_sst_backward(const fold_schedule_t *sched, const fold_model *model, const fold_sst *sst,
+                              const void *d_acts, fold_grads *grads, fold_sst_grads *sst_grads,
+                              void *d_workspace, size_t workspace_bytes, void *stream);
 
 /* param[i] -= lr * grad[i], i < n (device fp32). SPEC S:L511 sgd_step. */
 fold_status fold_sgd_update(float *d_param, const float *d_grad, int64_t n, float lr,

@@ -268,7 +268,8 @@ __global__ void k_cell_bwd_pw(int r0, int r1, int nl, int S, int ld, int ld_g, c
                               const int32_t *__restrict__ root_perm, int G, const float *__restrict__ dh_root,
                               const float *__restrict__ dc_root, const int32_t *__restrict__ gather,
                               const T *__restrict__ Gact, const float *__restrict__ C, const float *__restrict__ dA,
-                              float *__restrict__ dCe, T *__restrict__ dZ, int ld_z, const int32_t *__restrict__ root_row) {
+                              float *__restrict__ dCe, T *__restrict__ dZ, int ld_z, const int32_t *__restrict__ root_row,
+                              const float *__restrict__ dh_node, int c_rows0) {
   using IT = VecIO<T, VEC>;
   using IF = VecIO<float, VEC>;
   int lane = threadIdx.x & 31;
@@ -309,6 +310,11 @@ __global__ void k_cell_bwd_pw(int r0, int r1, int nl, int S, int ld, int ld_g, c
           for (int u = 0; u < VEC; u++) dc[u] += t[u];
         }
       }
+      if (dh_node) {  // a per-node loss term (§3.5 classifier), pool-row indexed [N][S]
+        IF::ld(dh_node + r * S + j, t);
+#pragma unroll
+        for (int u = 0; u < VEC; u++) dh[u] += t[u];
+      }
       for (int e = e0; e < e1; e++) {
         int64_t ed = cons_edge[e];
         IF::ld(dA + ed * S + j, t);
@@ -331,11 +337,12 @@ __global__ void k_cell_bwd_pw(int r0, int r1, int nl, int S, int ld, int ld_g, c
         IT::ld(ga + j, ig); IT::ld(ga + ld + j, fl); IT::ld(ga + 2 * ld + j, fr);
         IT::ld(ga + 3 * ld + j, og); IT::ld(ga + 4 * ld + j, ug);
         IF::ld(C + r * ld + j, cc);
-        // leaf children: c = 0 (not materialised in BF16 mode)
+        // children below row c_rows0 have c = 0: the R1 model's leaves (c_rows0 = nl; their C
+        // rows are not materialised in BF16 mode); the §3.5 leaf cells have c (c_rows0 = 0)
 #pragma unroll
         for (int u = 0; u < VEC; u++) { cl[u] = 0.f; cr[u] = 0.f; }
-        if (gL >= nl) IF::ld(C + gL * ld + j, cl);
-        if (gR >= nl) IF::ld(C + gR * ld + j, cr);
+        if (gL >= c_rows0) IF::ld(C + gL * ld + j, cl);
+        if (gR >= c_rows0) IF::ld(C + gR * ld + j, cr);
         float z0[VEC], z1[VEC], z2[VEC], z3[VEC], z4[VEC], eL[VEC], eR[VEC];
 #pragma unroll
         for (int u = 0; u < VEC; u++) {
@@ -352,8 +359,10 @@ __global__ void k_cell_bwd_pw(int r0, int r1, int nl, int S, int ld, int ld_g, c
         }
         IT::st(dz + j, z0); IT::st(dz + S + j, z1); IT::st(dz + 2 * S + j, z2);
         IT::st(dz + 3 * S + j, z3); IT::st(dz + 4 * S + j, z4);
-        IF::st(dCe + (2 * c) * S + j, eL);
-        IF::st(dCe + (2 * c + 1) * S + j, eR);
+        if (c >= 0) {  // (rows below nl: §3.5 leaf cells, no children)
+          IF::st(dCe + (2 * c) * S + j, eL);
+          IF::st(dCe + (2 * c + 1) * S + j, eR);
+        }
       }
     }
   }
@@ -574,7 +583,8 @@ __global__ void __launch_bounds__(128) k_embed_pieces(int S, int n_tok_segs, int
                                                       const int32_t *__restrict__ root_off,
                                                       const int32_t *__restrict__ root_perm,
                                                       const float *__restrict__ dh_root, const TA *__restrict__ dA,
-                                                      float *__restrict__ dE, float *__restrict__ partial) {
+                                                      float *__restrict__ dE, float *__restrict__ partial,
+                                                      const float *__restrict__ dX) {
   using IF = VecIO<float, VEC>;
   using IA = VecIO<TA, VEC>;
   const int total = piece_off[n_tok_segs];  // n_pieces is only a host-side upper bound
@@ -596,6 +606,12 @@ __global__ void __launch_bounds__(128) k_embed_pieces(int S, int n_tok_segs, int
       }
       for (int q = a; q < b; q++) {
         const int r = leaf_perm[q];
+        if (dX) {  // the leaf's input gradient is given densely (§3.5 leaf cell: dX = W^T dz)
+          IF::ld(dX + (int64_t)r * S + j, t);
+#pragma unroll
+          for (int u = 0; u < VEC; u++) acc[u] += t[u];
+          continue;
+        }
         const int k1 = root_off[r + 1];
         for (int kk = root_off[r]; kk < k1; kk++) {
           IF::ld(dh_root + (int64_t)root_perm[kk] * S + j, t);
@@ -705,13 +721,15 @@ fold_status launch_cell_bwd_pw(bool bf16, int cell, int r0, int r1, int nl, int 
                                const int32_t *cons_off, const int32_t *cons_edge, const int32_t *root_off,
                                const int32_t *root_perm, int G, const float *dh_root, const float *dc_root,
                                const int32_t *gather, const void *Gact, const float *C, const float *dA, float *dCe,
-                               void *dZ, int ld_z, cudaStream_t st, const int32_t *root_row) {
+                               void *dZ, int ld_z, cudaStream_t st, const int32_t *root_row, const float *dh_node,
+                               bool leaf_c) {
   if (r1 <= r0) return FOLD_OK;
   const int vec = (S & 3) == 0 ? 4 : 1;
   unsigned g = grid_cap(cdiv((int64_t)(r1 - r0) * cdiv(S, 32 * vec) * 32, 256));
 #define PW_ARGS r0, r1, nl, S, ld, ld_g, cons_off, cons_edge, root_off, root_perm, G, dh_root, dc_root, gather
 #define PW_LAUNCH(T, GT, VEC) \
-  k_cell_bwd_pw<T, GT, VEC><<<g, 256, 0, st>>>(PW_ARGS, (const T *)Gact, C, dA, dCe, (T *)dZ, ld_z, root_row)
+  k_cell_bwd_pw<T, GT, VEC><<<g, 256, 0, st>>>(PW_ARGS, (const T *)Gact, C, dA, dCe, (T *)dZ, ld_z, root_row, \
+                                               dh_node, leaf_c ? 0 : nl)
   const bool v4 = (S & 3) == 0;
   const bool lstm = cell == FOLD_CELL_TREELSTM;
   if (bf16) {
@@ -791,7 +809,7 @@ fold_status launch_embed_bwd_pieces(int S, int n_leaves, int n_tok_segs, const i
                                     const int32_t *leaf_perm, const int32_t *leaf_token, const int32_t *cons_off,
                                     const int32_t *cons_edge, const int32_t *root_off, const int32_t *root_perm,
                                     const float *dh_root, const void *dA, bool dA_bf16, float *dE,
-                                    const EmbedBwdWs &w, cudaStream_t st) {
+                                    const EmbedBwdWs &w, cudaStream_t st, const float *dX) {
   (void)n_leaves;
   if (n_tok_segs <= 0) return FOLD_OK;
   k_embed_piece_cnt<<<grid_cap(cdiv(n_tok_segs, 256)), 256, 0, st>>>(n_tok_segs, tok_seg, w.piece_cnt);
@@ -804,7 +822,7 @@ fold_status launch_embed_bwd_pieces(int S, int n_leaves, int n_tok_segs, const i
   const unsigned g = grid_cap(max_pieces);
   const bool v4 = (S & 3) == 0;
 #define EP_ARGS(T) S, n_tok_segs, max_pieces, tok_seg, w.piece_off, leaf_perm, leaf_token, cons_off, cons_edge, \
-                root_off, root_perm, dh_root, (const T *)dA, dE, w.partial
+                root_off, root_perm, dh_root, (const T *)dA, dE, w.partial, dX
   if (dA_bf16) {  // the fused tree backward stores leaf edges' dA in bf16
     if (v4) k_embed_pieces<4, __nv_bfloat16><<<g, 128, 0, st>>>(EP_ARGS(__nv_bfloat16));
     else k_embed_pieces<1, __nv_bfloat16><<<g, 128, 0, st>>>(EP_ARGS(__nv_bfloat16));

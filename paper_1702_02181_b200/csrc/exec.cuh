@@ -39,7 +39,9 @@ fold_status launch_cell_bwd_pw(bool bf16, int cell, int r0, int r1, int nl, int 
                                const int32_t *root_perm, int G, const float *dh_root, const float *dc_root,
                                const int32_t *gather, const void *Gact, const float *C, const float *dA,
                                float *dCe, void *dZ, int ld_z, cudaStream_t st,
-                               const int32_t *root_row = nullptr);  // root mode: rows = distinct root rows, [r0,r1)=[0,G)
+                               const int32_t *root_row = nullptr,  // root mode: rows = distinct root rows, [r0,r1)=[0,G)
+                               const float *dh_node = nullptr,     // + per-node dh [N][S] (pool rows; §3.5 classifier)
+                               bool leaf_c = false);               // leaves carry c (the §3.5 leaf cell)
 // dA[rows][2S] (edge-indexed, fp32) = dZ[rows][gates*S] * U[gates*S][2S]
 fold_status launch_gemm_dA_simt(int M, int S, int gates, const float *dZ, int ld_z, const float *U,
                                 float *dA, cudaStream_t st);
@@ -71,7 +73,8 @@ fold_status launch_embed_bwd_pieces(int S, int n_leaves, int n_tok_segs, const i
                                     const int32_t *leaf_perm, const int32_t *leaf_token, const int32_t *cons_off,
                                     const int32_t *cons_edge, const int32_t *root_off, const int32_t *root_perm,
                                     const float *dh_root, const void *dA, bool dA_bf16, float *dE,
-                                    const EmbedBwdWs &w, cudaStream_t st);
+                                    const EmbedBwdWs &w, cudaStream_t st,
+                                    const float *dX = nullptr);  // dense per-leaf gradient [nl][S] (§3.5)
 fold_status launch_zero(void *p, size_t bytes, cudaStream_t st);
 
 // --- tcgen05 path (exec_tc.cu)

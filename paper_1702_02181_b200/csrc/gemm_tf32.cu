@@ -354,7 +354,9 @@ __global__ void k_cell_fwd_pw(int r0, int r1, int nl, int S, int ld, int ld_g, c
       const float fr = 1.f / (1.f + expf(-(ga[2 * ld + j] + b[2 * S + j])));
       const float og = 1.f / (1.f + expf(-(ga[3 * ld + j] + b[3 * S + j])));
       const float ug = tanhf(ga[4 * ld + j] + b[4 * S + j]);
-      const float cl = C[(int64_t)gather[2 * r] * ld + j], cr = C[(int64_t)gather[2 * r + 1] * ld + j];
+      // (rows below nl: the §3.5 leaf cell, no children: c_L = c_R = 0)
+      const int64_t gl = gather[2 * r], gr = gather[2 * r + 1];
+      const float cl = gl >= 0 ? C[gl * ld + j] : 0.f, cr = gr >= 0 ? C[gr * ld + j] : 0.f;
       const float cc = ig * ug + fl * cl + fr * cr;
       C[r * ld + j] = cc;
       H[r * ld + j] = og * tanhf(cc);

@@ -66,6 +66,15 @@ class _Grads(ctypes.Structure):
                 ("accumulate", ctypes.c_int32), ("sweep_done_event", ctypes.c_void_p)]
 
 
+class _Sst(ctypes.Structure):
+    _fields_ = [("W", ctypes.c_void_p), ("Ws", ctypes.c_void_p), ("bs", ctypes.c_void_p), ("label", ctypes.c_void_p),
+                ("n_classes", ctypes.c_int32)]
+
+
+class _SstGrads(ctypes.Structure):
+    _fields_ = [("dW", ctypes.c_void_p), ("dWs", ctypes.c_void_p), ("dbs", ctypes.c_void_p)]
+
+
 _lib = None
 
 
@@ -118,6 +127,17 @@ def load() -> ctypes.CDLL:
     L.fold_debug_bwd_trace.restype = i32
     L.fold_debug_sched_trace.argtypes = [vp]
     L.fold_debug_sched_trace.restype = i32
+    SP, MP, SQ = ctypes.POINTER(_Sched), ctypes.POINTER(_Model), ctypes.POINTER(_Sst)
+    L.fold_sst_acts_layout.restype = i32
+    L.fold_sst_acts_layout.argtypes = [SP, MP, SQ, ctypes.POINTER(_ActsLayout)]
+    L.fold_sst_forward_workspace.restype = sz
+    L.fold_sst_forward_workspace.argtypes = [SP, MP, SQ]
+    L.fold_sst_backward_workspace.restype = sz
+    L.fold_sst_backward_workspace.argtypes = [SP, MP, SQ]
+    L.fold_sst_forward.restype = i32
+    L.fold_sst_forward.argtypes = [SP, MP, SQ, vp, vp, vp, sz, vp]
+    L.fold_sst_backward.restype = i32
+    L.fold_sst_backward.argtypes = [SP, MP, SQ, vp, ctypes.POINTER(_Grads), ctypes.POINTER(_SstGrads), vp, sz, vp]
     L.fold_debug_gemm_tf32.restype = i32
     L.fold_debug_gemm_tf32.argtypes = [vp, ctypes.c_int64, i32, vp, ctypes.c_int64, i32, i32, i32, i32, vp,
                                        ctypes.c_int64, i32, i32, vp, ctypes.c_int64, vp]
@@ -131,7 +151,9 @@ EXPORTED = ("fold_schedule_workspace", "fold_schedule", "fold_acts_layout", "fol
             "fold_forward", "fold_backward_workspace", "fold_backward", "fold_sgd_update",
             "fold_status_string", "fold_last_error_detail", "fold_last_error_context", "fold_abi_version", "fold_device_check",
             "fold_launch_count", "fold_profile_enable", "fold_profile_read", "fold_debug_fwd_trace", "fold_debug_bwd_trace",
-            "fold_debug_sched_trace", "fold_debug_gemm_tf32", "fold_debug_gemm_tf32_ws")
+            "fold_debug_sched_trace", "fold_debug_gemm_tf32", "fold_debug_gemm_tf32_ws",
+            "fold_sst_acts_layout", "fold_sst_forward_workspace", "fold_sst_forward", "fold_sst_backward_workspace",
+            "fold_sst_backward")
 
 PROF_CLASSES = ("schedule", "embed_fwd", "cell_fwd", "bwd_pointwise", "gemm_dA", "gemm_dU", "embed_bwd",
                 "db_colsum", "sgd", "weight_prep", "root_out")
@@ -402,6 +424,63 @@ def backward(sched: Schedule, model: Model, acts: Acts, dh_root: torch.Tensor, d
                            _ptr(dh_root), _ptr(dc_root), ctypes.byref(gs), ctypes.c_void_p(bbuf.data_ptr()), bws,
                            _stream(stream)), "fold_backward")
     return dU, db, dE
+
+
+# ----------------------------------------------------------------------------- §3.5 model (NEXT-2)
+
+@dataclasses.dataclass
+class SstHead:
+    """The §3.5 model's extra parameters (fold.h fold_sst): leaf input weights W [3S][S]
+    (row blocks i, o, u), per-node classifier Ws [C][S], bs [C]; labels [n_nodes] int32 in
+    node-id order."""
+    W: torch.Tensor
+    Ws: torch.Tensor
+    bs: torch.Tensor
+    label: torch.Tensor
+
+    def struct(self) -> _Sst:
+        for t in (self.W, self.Ws, self.bs):
+            assert t.dtype == torch.float32 and t.is_cuda and t.is_contiguous()
+        assert self.label.dtype == torch.int32 and self.label.is_cuda and self.label.is_contiguous()
+        return _Sst(self.W.data_ptr(), self.Ws.data_ptr(), self.bs.data_ptr(), self.label.data_ptr(),
+                    int(self.bs.shape[0]))
+
+
+def sst_forward(sched: Schedule, model: Model, head: SstHead, stream=None, ws: Workspace | None = None):
+    """fold_sst_forward: (loss [1] device tensor, Acts) of the §3.5 model."""
+    L = load()
+    ms, qs = model.struct(), head.struct()
+    lay = _ActsLayout()
+    _check(L.fold_sst_acts_layout(ctypes.byref(sched.struct()), ctypes.byref(ms), ctypes.byref(qs), ctypes.byref(lay)),
+           "fold_sst_acts_layout")
+    ws = ws or Workspace(model.E.device)
+    acts = ws.get("sst_acts", lay.bytes)
+    n = int(L.fold_sst_forward_workspace(ctypes.byref(sched.struct()), ctypes.byref(ms), ctypes.byref(qs)))
+    fbuf = ws.get("sst_fwd", n)
+    loss = torch.empty(1, dtype=torch.float32, device=model.E.device)
+    _check(L.fold_sst_forward(ctypes.byref(sched.struct()), ctypes.byref(ms), ctypes.byref(qs),
+                              ctypes.c_void_p(acts.data_ptr()), _ptr(loss), ctypes.c_void_p(fbuf.data_ptr()), n,
+                              _stream(stream)), "fold_sst_forward")
+    return loss, Acts(acts, lay)
+
+
+def sst_backward(sched: Schedule, model: Model, head: SstHead, acts: Acts, grads=None, accumulate: bool = False,
+                 stream=None, ws: Workspace | None = None):
+    """fold_sst_backward: (dU, db, dE, dW, dWs, dbs) of the summed per-node cross-entropy."""
+    L = load()
+    ms, qs = model.struct(), head.struct()
+    if grads is None:
+        grads = tuple(torch.empty_like(t) for t in (model.U, model.b, model.E, head.W, head.Ws, head.bs))
+    dU, db, dE, dW, dWs, dbs = grads
+    gs = _Grads(dU.data_ptr(), db.data_ptr(), dE.data_ptr(), 1 if accumulate else 0, None)
+    sg = _SstGrads(dW.data_ptr(), dWs.data_ptr(), dbs.data_ptr())
+    ws = ws or Workspace(model.E.device)
+    n = int(L.fold_sst_backward_workspace(ctypes.byref(sched.struct()), ctypes.byref(ms), ctypes.byref(qs)))
+    bbuf = ws.get("sst_bwd", n)
+    _check(L.fold_sst_backward(ctypes.byref(sched.struct()), ctypes.byref(ms), ctypes.byref(qs),
+                               ctypes.c_void_p(acts.buf.data_ptr()), ctypes.byref(gs), ctypes.byref(sg),
+                               ctypes.c_void_p(bbuf.data_ptr()), n, _stream(stream)), "fold_sst_backward")
+    return grads
 
 
 def debug_gemm_tf32(A: torch.Tensor, B: torch.Tensor, M: int, N: int, K: int, a_mn: bool, b_mn: bool,
