@@ -79,6 +79,7 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
   const int64_t max_pieces = s->n_leaves / kEmbedPiece + nseg + 1;
   size_t o_pc = take((size_t)(nseg + 2) * 4), o_po = take((size_t)(nseg + 2) * 4);
   size_t o_ss = take((size_t)scan_sums_count(nseg + 1) * 4);
+  size_t o_psg = take((size_t)max_pieces * 4);
   size_t o_ep = take((size_t)max_pieces * S * 4);
   const bool tf = !bf16 && !simt_fp32();
   size_t o_w = take(bf16 ? tc_weights_bytes(gates, (int)S) : tf ? tf_u_bytes(gates, (int)S) : 0);
@@ -100,6 +101,7 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
     b.emb.piece_cnt = (int32_t *)(p + o_pc);
     b.emb.piece_off = (int32_t *)(p + o_po);
     b.emb.scan_sums = (int32_t *)(p + o_ss);
+    b.emb.piece_seg = (int32_t *)(p + o_psg);
     b.emb.partial = (float *)(p + o_ep);
     b.dU_split = (splits > 1 || tf_split > 0) ? (float *)(p + o_spl) : nullptr;
     b.Ub = bf16 ? (__nv_bfloat16 *)(p + o_w) : nullptr;

@@ -572,10 +572,25 @@ __global__ void k_embed_piece_cnt(int n_tok_segs, const int32_t *__restrict__ to
     cnt[s] = (int)cdiv(tok_seg[s + 1] - tok_seg[s], kEmbedPiece);
 }
 
+// Per piece: first the piece's source rows are resolved into shared memory in parallel (one
+// thread per leaf: its seeded roots, then its consumer edges, ascending, i.e. the order the
+// sums take), so the column loop streams independent row loads (UNR in flight per thread)
+// instead of walking a leaf -> row -> cons_off -> cons_edge -> dA chain per leaf.
+// Source encoding: >= 0 an edge row of dA (or, with dX, the leaf's own dX row); < 0 the
+// seeded root -(g + 1) of dh_root.
+constexpr int kPieceSrc = 512;  // sources held per pass (a piece has <= kEmbedPiece leaves)
+// piece -> segment map (so a piece finds its segment with one load, not a binary search)
+__global__ void k_embed_piece_seg(int n_tok_segs, const int32_t *__restrict__ piece_off, int32_t *__restrict__ seg) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n_tok_segs; s += stride)
+    for (int k = piece_off[s]; k < piece_off[s + 1]; k++) seg[k] = (int)s;
+}
+
 template <int VEC, typename TA>
 __global__ void __launch_bounds__(128) k_embed_pieces(int S, int n_tok_segs, int n_pieces,
                                                       const int32_t *__restrict__ tok_seg,
                                                       const int32_t *__restrict__ piece_off,
+                                                      const int32_t *__restrict__ piece_seg,
                                                       const int32_t *__restrict__ leaf_perm,
                                                       const int32_t *__restrict__ leaf_token,
                                                       const int32_t *__restrict__ cons_off,
@@ -587,46 +602,106 @@ __global__ void __launch_bounds__(128) k_embed_pieces(int S, int n_tok_segs, int
                                                       const float *__restrict__ dX) {
   using IF = VecIO<float, VEC>;
   using IA = VecIO<TA, VEC>;
+  __shared__ int src[kPieceSrc];
+  __shared__ int cnt[kEmbedPiece + 1];
   const int total = piece_off[n_tok_segs];  // n_pieces is only a host-side upper bound
   for (int64_t p = blockIdx.x; p < n_pieces && p < total; p += gridDim.x) {
-    int lo = 0, hi = n_tok_segs;  // segment s with piece_off[s] <= p < piece_off[s+1]
-    while (lo < hi) { int mid = (lo + hi + 1) >> 1; if (piece_off[mid] <= p) lo = mid; else hi = mid - 1; }
-    const int s = lo;
+    const int s = piece_seg[p];  // segment s with piece_off[s] <= p < piece_off[s+1]
     const int k = (int)(p - piece_off[s]);
     const int np = piece_off[s + 1] - piece_off[s];
     const int a = tok_seg[s] + k * kEmbedPiece, b = min(tok_seg[s + 1], a + kEmbedPiece);
     const int tok = leaf_token[leaf_perm[tok_seg[s]]];
     float *dst = np == 1 ? dE + (int64_t)tok * S : partial + p * (int64_t)S;
+    // ---- resolve the sources (thread t <-> leaf a + t)
+    const int t = threadIdx.x, nleaf = b - a;
+    int r = -1, r0 = 0, r1 = 0, e0 = 0, e1 = 0;
+    if (t < nleaf) {
+      r = leaf_perm[a + t];
+      if (!dX) { r0 = root_off[r]; r1 = root_off[r + 1]; e0 = cons_off[r]; e1 = cons_off[r + 1]; }
+      cnt[t] = dX ? 1 : (r1 - r0) + (e1 - e0);
+    }
+    __syncthreads();
+    if (t == 0) {  // exclusive prefix over <= 64 counts
+      int acc = 0;
+      for (int i = 0; i < nleaf; i++) { const int c = cnt[i]; cnt[i] = acc; acc += c; }
+      cnt[nleaf] = acc;
+    }
+    __syncthreads();
+    const int nsrc = cnt[nleaf];
+    if (nsrc <= kPieceSrc && t < nleaf) {
+      int o = cnt[t];
+      if (dX) src[o] = r;
+      else {
+        for (int q = r0; q < r1; q++) src[o++] = -(root_perm[q] + 1);
+        for (int e = e0; e < e1; e++) src[o++] = cons_edge[e];
+      }
+    }
+    __syncthreads();
+    const float *xsrc = dX;
+    if (nsrc <= kPieceSrc) {
+      for (int j = threadIdx.x * VEC; j < S; j += blockDim.x * VEC) {
+        float acc[VEC];
+        if (np == 1) IF::ld(dst + j, acc);
+        else {
+#pragma unroll
+          for (int u = 0; u < VEC; u++) acc[u] = 0.f;
+        }
+        constexpr int UNR = 4;
+        int i = 0;
+        for (; i + UNR <= nsrc; i += UNR) {
+          float t4[UNR][VEC];
+#pragma unroll
+          for (int q = 0; q < UNR; q++) {
+            const int sv = src[i + q];
+            if (xsrc) IF::ld(xsrc + (int64_t)sv * S + j, t4[q]);
+            else if (sv >= 0) IA::ld(dA + (int64_t)sv * S + j, t4[q]);
+            else IF::ld(dh_root + (int64_t)(-sv - 1) * S + j, t4[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < UNR; q++)
+#pragma unroll
+            for (int u = 0; u < VEC; u++) acc[u] += t4[q][u];
+        }
+        for (; i < nsrc; i++) {
+          float tv[VEC];
+          const int sv = src[i];
+          if (xsrc) IF::ld(xsrc + (int64_t)sv * S + j, tv);
+          else if (sv >= 0) IA::ld(dA + (int64_t)sv * S + j, tv);
+          else IF::ld(dh_root + (int64_t)(-sv - 1) * S + j, tv);
+#pragma unroll
+          for (int u = 0; u < VEC; u++) acc[u] += tv[u];
+        }
+        IF::st(dst + j, acc);
+      }
+      __syncthreads();  // src / cnt reused by the next piece
+      continue;
+    }
+    // (more sources than the shared list holds: wide DAG fan-out) walk the leaves directly
     for (int j = threadIdx.x * VEC; j < S; j += blockDim.x * VEC) {
-      float acc[VEC], t[VEC];
+      float acc[VEC], tv[VEC];
       if (np == 1) IF::ld(dst + j, acc);
       else {
 #pragma unroll
         for (int u = 0; u < VEC; u++) acc[u] = 0.f;
       }
       for (int q = a; q < b; q++) {
-        const int r = leaf_perm[q];
-        if (dX) {  // the leaf's input gradient is given densely (§3.5 leaf cell: dX = W^T dz)
-          IF::ld(dX + (int64_t)r * S + j, t);
+        const int rr = leaf_perm[q];
+        const int k1 = root_off[rr + 1];
+        for (int kk = root_off[rr]; kk < k1; kk++) {
+          IF::ld(dh_root + (int64_t)root_perm[kk] * S + j, tv);
 #pragma unroll
-          for (int u = 0; u < VEC; u++) acc[u] += t[u];
-          continue;
+          for (int u = 0; u < VEC; u++) acc[u] += tv[u];
         }
-        const int k1 = root_off[r + 1];
-        for (int kk = root_off[r]; kk < k1; kk++) {
-          IF::ld(dh_root + (int64_t)root_perm[kk] * S + j, t);
+        const int ee = cons_off[rr + 1];
+        for (int e = cons_off[rr]; e < ee; e++) {
+          IA::ld(dA + (int64_t)cons_edge[e] * S + j, tv);
 #pragma unroll
-          for (int u = 0; u < VEC; u++) acc[u] += t[u];
-        }
-        const int e1 = cons_off[r + 1];
-        for (int e = cons_off[r]; e < e1; e++) {
-          IA::ld(dA + (int64_t)cons_edge[e] * S + j, t);
-#pragma unroll
-          for (int u = 0; u < VEC; u++) acc[u] += t[u];
+          for (int u = 0; u < VEC; u++) acc[u] += tv[u];
         }
       }
       IF::st(dst + j, acc);
     }
+    __syncthreads();
   }
 }
 
@@ -817,11 +892,13 @@ fold_status launch_embed_bwd_pieces(int S, int n_leaves, int n_tok_segs, const i
   // piece_off[0..n_tok_segs] (the total lands in piece_off[n_tok_segs] via a zero tail)
   FOLD_CUDA_TRY(cudaMemsetAsync(w.piece_cnt + n_tok_segs, 0, sizeof(int32_t), st));
   FOLD_TRY(scan_exclusive(w.piece_cnt, w.piece_off, (int64_t)n_tok_segs + 1, w.scan_sums, nullptr, st));
+  k_embed_piece_seg<<<grid_cap(cdiv(n_tok_segs, 256)), 256, 0, st>>>(n_tok_segs, w.piece_off, w.piece_seg);
+  FOLD_LAUNCH_CHECK();
   // upper bound on pieces (host-side, no sync): sum ceil(len/P) <= n_leaves/P + n_tok_segs
   const int max_pieces = n_leaves / kEmbedPiece + n_tok_segs;
   const unsigned g = grid_cap(max_pieces);
   const bool v4 = (S & 3) == 0;
-#define EP_ARGS(T) S, n_tok_segs, max_pieces, tok_seg, w.piece_off, leaf_perm, leaf_token, cons_off, cons_edge, \
+#define EP_ARGS(T) S, n_tok_segs, max_pieces, tok_seg, w.piece_off, w.piece_seg, leaf_perm, leaf_token, cons_off, cons_edge, \
                 root_off, root_perm, dh_root, (const T *)dA, dE, w.partial, dX
   if (dA_bf16) {  // the fused tree backward stores leaf edges' dA in bf16
     if (v4) k_embed_pieces<4, __nv_bfloat16><<<g, 128, 0, st>>>(EP_ARGS(__nv_bfloat16));

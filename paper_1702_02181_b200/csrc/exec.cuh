@@ -67,6 +67,7 @@ int64_t scan_sums_count(int64_t n);
 constexpr int kEmbedPiece = 64;
 struct EmbedBwdWs {
   int32_t *piece_cnt, *piece_off, *scan_sums;
+  int32_t *piece_seg;  // [n_leaves / kEmbedPiece + n_tok_segs + 1]: segment of each piece
   float *partial;
 };
 fold_status launch_embed_bwd_pieces(int S, int n_leaves, int n_tok_segs, const int32_t *tok_seg,

@@ -111,6 +111,7 @@ SstBwdWs bwd_ws(void *base, const fold_schedule_t *s, const fold_model *m, const
   const int64_t nseg = s->n_tok_segs, max_pieces = nl / kEmbedPiece + nseg + 1;
   const size_t opc = take((size_t)(nseg + 2) * 4), opo = take((size_t)(nseg + 2) * 4);
   const size_t oss = take((size_t)scan_sums_count(nseg + 1) * 4), oep = take((size_t)max_pieces * S * 4);
+  const size_t opsg = take((size_t)max_pieces * 4);
   w.bytes = o;
   if (base) {
     char *p = (char *)base;
@@ -120,6 +121,7 @@ SstBwdWs bwd_ws(void *base, const fold_schedule_t *s, const fold_model *m, const
     w.dW5 = (float *)(p + odw); w.split = sp > 0 ? (float *)(p + osp) : nullptr; w.root_off = (int32_t *)(p + oro);
     w.emb.piece_cnt = (int32_t *)(p + opc); w.emb.piece_off = (int32_t *)(p + opo);
     w.emb.scan_sums = (int32_t *)(p + oss); w.emb.partial = (float *)(p + oep);
+    w.emb.piece_seg = (int32_t *)(p + opsg);
   }
   return w;
 }
