@@ -334,3 +334,122 @@ def make_labels(N: int, C: int = SST_CLASSES, seed: int = LABEL_SEED) -> np.ndar
     no dataset: uniform over the C classes)."""
     rng = np.random.default_rng(seed)
     return rng.integers(0, C, size=N).astype(np.int32)
+
+
+# ----------------------------------------------------------------------------- multi-op (NEXT-3)
+# SURVEY §8(f) NEXT-3 / PAPER.md L31-44: several operations and tensor types per depth.
+# An op table (enumeration order = op id; PAPER.md L31 "it enumerates them") is input
+# data: kind, arity, input / output tensor type, vocabulary; tensor types have state sizes.
+# Graph encoding as above with op ids into the table; child[n, k] for k < arity, -1 else.
+MO_EMBED, MO_LSTM, MO_RNN = 0, 1, 2
+MO_MAXA = 2
+MO_SEED = 3133  # the C6 multi-op workload's graph seed
+
+
+@dataclasses.dataclass
+class MoTable:
+    kind: np.ndarray      # [n_ops] int32 MO_EMBED / MO_LSTM / MO_RNN
+    arity: np.ndarray     # [n_ops] int32 (0 for EMBED, 1..2 else)
+    in_type: np.ndarray   # [n_ops] int32 (EMBED: -1)
+    out_type: np.ndarray  # [n_ops] int32
+    vocab: np.ndarray     # [n_ops] int32 (EMBED: table rows, else 0)
+    S: np.ndarray         # [n_types] int32 state size of each tensor type
+
+    @property
+    def n_ops(self) -> int:
+        return int(self.kind.shape[0])
+
+    @property
+    def n_types(self) -> int:
+        return int(self.S.shape[0])
+
+
+def mo_table(ops, S) -> MoTable:
+    """ops: list of (kind, arity, in_type, out_type, vocab)."""
+    a = np.asarray(ops, np.int64).reshape(-1, 5)
+    return MoTable(*(a[:, i].astype(np.int32) for i in range(5)), np.asarray(S, np.int32))
+
+
+def mo_table_c6(S0: int = 300, S1: int = 128, vocab: int = 16384) -> MoTable:
+    """C6 (NEXT-3 workload): constituency-style trees with binary and unary (chain) nodes
+    and a typed sentence projection at the root:
+      op 0 EMBED  word      -> type 0 (S0)
+      op 1 LSTM   arity 2   type 0 -> 0   (binary TreeLSTM)
+      op 2 LSTM   arity 1   type 0 -> 0   (unary production: the N = 1 TreeLSTM)
+      op 3 RNN    arity 1   type 0 -> 1   (sentence projection into tensor type 1, S1)"""
+    return mo_table([(MO_EMBED, 0, -1, 0, vocab), (MO_LSTM, 2, 0, 0, 0), (MO_LSTM, 1, 0, 0, 0),
+                     (MO_RNN, 1, 0, 1, 0)], [S0, S1])
+
+
+@dataclasses.dataclass
+class MoGraphs:
+    op: np.ndarray      # [N] int32 op ids
+    child: np.ndarray   # [N, MO_MAXA] int32
+    token: np.ndarray   # [N] int32
+    root: np.ndarray    # [G] int32
+    table: MoTable
+
+    @property
+    def n_nodes(self) -> int:
+        return int(self.op.shape[0])
+
+    @property
+    def n_graphs(self) -> int:
+        return int(self.root.shape[0])
+
+
+def mo_batch_c6(B: int, seed: int = MO_SEED, table: MoTable | None = None, max_leaves: int = 60,
+                p_unary: float = 0.3, zipf: bool = True) -> MoGraphs:
+    """B trees: parse-skew binary shapes over 1..max_leaves leaves (C3's distribution); every
+    node gets a chain of unary LSTM parents (length ~ Geometric: each link with probability
+    p_unary); the root gets the RNN projection (op 3). Post-order numbering per tree."""
+    table = table or mo_table_c6()
+    rng = np.random.default_rng(seed)
+    V = int(table.vocab[0])
+    draw = zipf_tokens(rng, V) if zipf else uniform_tokens(rng, V)
+    ops, kids, toks, roots = [], [], [], []
+    for _ in range(B):
+        n_leaves = int(rng.integers(1, max_leaves + 1))
+        sop, sl, sr = parse_skew_shape(rng, n_leaves)
+        remap = np.empty(len(sop), np.int64)
+        for i in range(len(sop)):
+            if sop[i] == EMBED:
+                ops.append(0); kids.append((-1, -1)); toks.append(int(draw(1)[0]))
+            else:
+                ops.append(1); kids.append((int(remap[sl[i]]), int(remap[sr[i]]))); toks.append(0)
+            top = len(ops) - 1
+            while rng.random() < p_unary:
+                ops.append(2); kids.append((top, -1)); toks.append(0)
+                top = len(ops) - 1
+            remap[i] = top
+        ops.append(3); kids.append((int(remap[len(sop) - 1]), -1)); toks.append(0)
+        roots.append(len(ops) - 1)
+    return MoGraphs(np.asarray(ops, np.int32), np.asarray(kids, np.int32).reshape(-1, MO_MAXA),
+                    np.asarray(toks, np.int32), np.asarray(roots, np.int32), table)
+
+
+def make_mo_params(table: MoTable, seed: int = PARAM_SEED) -> list:
+    """Per op, in enumeration order: EMBED -> (E [V, S_out],); LSTM / RNN -> (U [rows, a*S_in],
+    b [rows]) with rows = (3 + a) S (LSTM) or S_out (RNN); U ~ U(+-sqrt(6/(fan_in + rows))),
+    b ~ U(+-0.1), E ~ U(+-0.5). float32 masters."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for o in range(table.n_ops):
+        k, a = int(table.kind[o]), int(table.arity[o])
+        So = int(table.S[table.out_type[o]])
+        if k == MO_EMBED:
+            out.append((rng.uniform(-0.5, 0.5, size=(int(table.vocab[o]), So)).astype(np.float32),))
+            continue
+        Si = int(table.S[table.in_type[o]])
+        rows = (3 + a) * So if k == MO_LSTM else So
+        lim = np.sqrt(6.0 / (a * Si + rows))
+        U = rng.uniform(-lim, lim, size=(rows, a * Si)).astype(np.float32)
+        b = rng.uniform(-0.1, 0.1, size=(rows,)).astype(np.float32)
+        out.append((U, b))
+    return out
+
+
+def make_mo_upstream(G: int, table: MoTable, seed: int = GRAD_SEED) -> np.ndarray:
+    """dL/dh_root as [G, S_max], g ~ U(+-1) (graph g reads the first S_{type(root)} entries)."""
+    rng = np.random.default_rng(seed)
+    return rng.uniform(-1.0, 1.0, size=(G, int(table.S.max()))).astype(np.float32)

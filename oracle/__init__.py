@@ -27,24 +27,25 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "fold_oracle.c")
+_SRC_MO = os.path.join(_HERE, "fold_oracle_mo.c")
 _LIB_PATH = os.path.join(_HERE, "_build", "liboracle.so")
 _lock = threading.Lock()
 _lib = None
 
 STATUS = {0: "OK", 1: "INVALID", 2: "CHILD_RANGE", 3: "ARITY", 4: "TOKEN_RANGE",
-          5: "ROOT_RANGE", 6: "CYCLE", 10: "OP_RANGE", 12: "LEVEL"}
+          5: "ROOT_RANGE", 6: "CYCLE", 10: "OP_RANGE", 11: "TYPE", 12: "LEVEL"}
 CELLS = {"treernn": 0, "treelstm": 1}
 
 
 def build(force: bool = False) -> str:
-    """Compile fold_oracle.c with gcc (plain C11, -O2, no fast-math)."""
+    """Compile fold_oracle.c + fold_oracle_mo.c with gcc (plain C11, -O2, no fast-math)."""
     os.makedirs(os.path.dirname(_LIB_PATH), exist_ok=True)
     if (not force and os.path.exists(_LIB_PATH)
-            and os.path.getmtime(_LIB_PATH) >= os.path.getmtime(_SRC)):
+            and all(os.path.getmtime(_LIB_PATH) >= os.path.getmtime(f) for f in (_SRC, _SRC_MO))):
         return _LIB_PATH
     tmp = _LIB_PATH + f".{os.getpid()}.tmp"
     subprocess.check_call(["gcc", "-O2", "-std=c11", "-fno-fast-math", "-fPIC", "-shared",
-                           "-o", tmp, _SRC, "-lm"])
+                           "-o", tmp, _SRC, _SRC_MO, "-lm"])
     os.replace(tmp, _LIB_PATH)
     return _LIB_PATH
 
@@ -195,3 +196,113 @@ def sst_backward(op, child, token, label, U, b, E, W, Ws, bs):
     if st != 0:
         raise OracleError(st)
     return (float(loss[0]), *out)
+
+
+# ----------------------------------------------------------------------------- multi-op (NEXT-3)
+# fold_oracle_mo.c: several operations and tensor types per depth.
+# Parameters travel as one flat fp64 array in the oracle's own layout (op o's block at
+# mo_param_offsets(table)[o]: EMBED E_o; LSTM / RNN U_o then b_o).
+
+def _table_args(table):
+    return (ctypes.c_int(table.n_ops), ctypes.c_int(table.n_types), *[_p(_i32(x)) for x in (
+        table.kind, table.arity, table.in_type, table.out_type, table.vocab, table.S)])
+
+
+def _keep(table):
+    return [_i32(x) for x in (table.kind, table.arity, table.in_type, table.out_type, table.vocab, table.S)]
+
+
+def mo_param_offsets(table):
+    lib = _load()
+    lib.mo_param_offsets.restype = ctypes.c_int64
+    poff = np.zeros(table.n_ops + 1, np.int64)
+    ks = _keep(table)
+    lib.mo_param_offsets(ctypes.c_int(table.n_ops), ctypes.c_int(table.n_types), *[_p(x) for x in ks], _p(poff))
+    return poff
+
+
+def mo_flatten(table, params):
+    """Per-op parameter tuples (foldgen.make_mo_params) -> the oracle's flat fp64 array."""
+    poff = mo_param_offsets(table)
+    P = np.zeros(int(poff[-1]), np.float64)
+    for o, blk in enumerate(params):
+        flat = np.concatenate([np.asarray(x, np.float64).reshape(-1) for x in blk])
+        assert flat.size == poff[o + 1] - poff[o]
+        P[poff[o]:poff[o + 1]] = flat
+    return P
+
+
+def mo_unflatten(table, params, P):
+    """Inverse of mo_flatten, shaped like `params` (gradients back per op)."""
+    poff = mo_param_offsets(table)
+    out = []
+    for o, blk in enumerate(params):
+        off, parts = int(poff[o]), []
+        for x in blk:
+            n = int(np.asarray(x).size)
+            parts.append(P[off:off + n].reshape(np.asarray(x).shape))
+            off += n
+        out.append(tuple(parts))
+    return out
+
+
+def mo_schedule(gr):
+    """fold_oracle_mo.c oracle_mo_schedule on a foldgen.MoGraphs: depth, group_off (per
+    (depth, op) key), type_off / pool / pool_row (the per-type concatenation of PAPER.md L43),
+    tlevel_off [n_types, D+2], label [N, 2, 3] = (d, t, i) per edge (L44)."""
+    lib = _load()
+    T = gr.table
+    ks = _keep(T)
+    op, child, token, root = _i32(gr.op), _i32(gr.child).reshape(-1), _i32(gr.token), _i32(gr.root)
+    N, G = len(op), len(root)
+    out = {k: np.zeros(n, np.int32) for k, n in [
+        ("depth", N), ("group_off", (N + 1) * T.n_ops + 1), ("type_off", T.n_types + 1), ("pool", N),
+        ("pool_row", N), ("tlevel_off", T.n_types * (N + 2)), ("label", N * 2 * 3)]}
+    info = np.zeros(2, np.int32)
+    st = lib.oracle_mo_schedule(ctypes.c_int(T.n_ops), ctypes.c_int(T.n_types), *[_p(x) for x in ks],
+                                ctypes.c_int(N), ctypes.c_int(G), _p(op), _p(child), _p(token), _p(root),
+                                *[_p(out[k]) for k in ("depth", "group_off", "type_off", "pool", "pool_row",
+                                                       "tlevel_off", "label")], _p(info))
+    if st != 0:
+        raise OracleError(st, int(info[1]))
+    D = int(info[0])
+    out["group_off"] = out["group_off"][:(D + 1) * T.n_ops + 1]
+    out["tlevel_off"] = out["tlevel_off"][:T.n_types * (D + 2)].reshape(T.n_types, D + 2)
+    out["label"] = out["label"].reshape(N, 2, 3)
+    out["n_levels"] = D
+    return out
+
+
+def mo_forward(gr, P):
+    """Node-at-a-time fp64 forward: (H [N, S_max], C [N, S_max]) in node-id order."""
+    lib = _load()
+    T = gr.table
+    ks = _keep(T)
+    op, child, token, root = _i32(gr.op), _i32(gr.child).reshape(-1), _i32(gr.token), _i32(gr.root)
+    N, G = len(op), len(root)
+    Sm = int(np.max(T.S))
+    H = np.zeros((N, Sm)); C = np.zeros((N, Sm))
+    P = _f64(P)
+    st = lib.oracle_mo_forward(ctypes.c_int(T.n_ops), ctypes.c_int(T.n_types), *[_p(x) for x in ks],
+                               ctypes.c_int(N), ctypes.c_int(G), _p(op), _p(child), _p(token), _p(root), _p(P),
+                               _p(H), _p(C))
+    if st != 0:
+        raise OracleError(st)
+    return H, C
+
+
+def mo_backward(gr, P, g):
+    """fp64 reverse mode of L = sum_g <g[g, :S_root], h_root(g)>; dP in P's layout."""
+    lib = _load()
+    T = gr.table
+    ks = _keep(T)
+    op, child, token, root = _i32(gr.op), _i32(gr.child).reshape(-1), _i32(gr.token), _i32(gr.root)
+    N, G = len(op), len(root)
+    P, g = _f64(P), _f64(g)
+    dP = np.zeros_like(P)
+    st = lib.oracle_mo_backward(ctypes.c_int(T.n_ops), ctypes.c_int(T.n_types), *[_p(x) for x in ks],
+                                ctypes.c_int(N), ctypes.c_int(G), _p(op), _p(child), _p(token), _p(root), _p(P),
+                                _p(g), _p(dP))
+    if st != 0:
+        raise OracleError(st)
+    return dP
