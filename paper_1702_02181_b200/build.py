@@ -16,8 +16,10 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-LIB_DIR = os.path.join(HERE, "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "libfold.so")
+# FOLD_LIB_PATH: build / load a variant library elsewhere (A/B experiments with
+# FOLD_NVCC_EXTRA macros); the default is the in-tree _lib/libfold.so
+LIB_PATH = os.environ.get("FOLD_LIB_PATH") or os.path.join(HERE, "_lib", "libfold.so")
+LIB_DIR = os.path.dirname(LIB_PATH)
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

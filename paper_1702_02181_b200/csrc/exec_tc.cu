@@ -90,6 +90,7 @@ struct FwdLevels {
   int D, S, Ww, Wn;      // deepest level, state size, wide / narrow tile widths
   int narrow_below;      // a level whose wide tiling has fewer tiles than this uses Wn
   int Wm, G, npairs;     // mid tile width, gates, CTA pairs of the launch
+  int pf;                // L2 prefetch distance of the A-plane boxes in k-blocks (0: off)
 };
 
 __host__ __device__ inline int fwd_level_W(const FwdLevels &L, int M) {
@@ -234,17 +235,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
       LevelCursor cur;
       cur.init(L);
       int it = 0;
+      // A-operand box rows for a CTA holding m rows (narrow tiles load only their rows)
+      auto box_of = [](int m) { return m <= 0 ? 0 : m <= 16 ? 16 : m <= 64 ? 64 : BM; };
+      const int pf = L.pf;
       for (int T = pair; T < total_tiles; T += npairs) {
         cur.seek(L, T);
         const int lt = T - cur.t0, W = cur.W;
         const int ct = (cur.r0 - nl) + (lt / cur.NT) * PM;  // first cell of the pair tile
         const int rows = min(PM, cur.r1 - nl - ct);
-        // A-operand box rows for a CTA holding m rows (narrow tiles load only their rows)
-        auto box_of = [](int m) { return m <= 0 ? 0 : m <= 16 ? 16 : m <= 64 ? 64 : BM; };
         const int bx0 = box_of(min(rows, BM)), bx1 = box_of(rows - BM), bx = rank ? bx1 : bx0;
         const CUtensorMap *mL = bx == 16 ? &tmAL16 : bx == 64 ? &tmAL64 : &tmAL;
         const CUtensorMap *mR = bx == 16 ? &tmAR16 : bx == 64 ? &tmAR64 : &tmAR;
         const int c0 = ct + (int)rank * BM, j0 = (lt % cur.NT) * W;
+        // L2 prefetch of the A-plane boxes pf k-blocks ahead (the planes were pushed one level
+        // earlier and mostly left L2; the column tiles of a row tile request each k-block at
+        // about the same time), and of the next tile's head during this tile's last k-blocks
+        const CUtensorMap *nL = nullptr, *nR = nullptr;
+        int c0n = 0, bxn = 0;
+        if (pf > 0 && T + npairs < total_tiles) {
+          LevelCursor nx = cur;
+          nx.seek(L, T + npairs);
+          const int ctn = (nx.r0 - nl) + ((T + npairs - nx.t0) / nx.NT) * PM;
+          const int rwn = min(PM, nx.r1 - nl - ctn);
+          bxn = rank ? box_of(rwn - BM) : box_of(min(rwn, BM));
+          nL = bxn == 16 ? &tmAL16 : bxn == 64 ? &tmAL64 : &tmAL;
+          nR = bxn == 16 ? &tmAR16 : bxn == 64 ? &tmAR64 : &tmAR;
+          c0n = ctn + (int)rank * BM;
+        }
         const CUtensorMap *tmU = W == Cfg::WMAX ? &tmUw : W == Cfg::WMID ? &tmUm : &tmUn;
         if (rank == 0) trace(dbg, 0, T);
         // the leader's full barrier counts both CTAs' bytes: A rows of both + the B rows
@@ -261,6 +278,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         if (ready && rank == 0) trace(dbg, 1, T);
         if (ready && kps == 1) {  // wide tiles, inputs published: one (A, U) box pair per stage
           for (int kb = 0; kb < KB; kb++, it++) {
+            if (pf > 0) {
+              const int kp = kb + pf;
+              if (kp < KB) {
+                const int hp = kp >= KBh;
+                if (bx) ptx::tma_prefetch_2d(hp ? mR : mL, (kp - hp * KBh) * BK, c0);
+              } else if (bxn && kp - KB < KB) {
+                const int kq = kp - KB, hq = kq >= KBh;
+                ptx::tma_prefetch_2d(hq ? nR : nL, (kq - hq * KBh) * BK, c0n);
+              }
+            }
             const int s = it % ST;
             const uint32_t ph = (it / ST) & 1;
             ptx::mbar_wait(&empty[s], ph ^ 1);
@@ -1072,6 +1099,7 @@ struct BwdLevels {
   const int32_t *lo;
   int D, S, nl, ld_u;
   int narrow_below;  // a level with fewer 256-column pair tiles than this uses 128 columns
+  int pf;            // L2 prefetch distance of the dZ (A operand) boxes in k-blocks (0: off)
 };
 __host__ __device__ inline int bwd_level_N(const BwdLevels &L, int M) {
   return cdiv(M, PM) * cdiv(L.ld_u, 256) < L.narrow_below ? 128 : 256;
@@ -1096,7 +1124,19 @@ __host__ __device__ inline int bwd_kps(int N, int bx0) {
   return k < 1 ? 1 : k > 8 ? 8 : k;
 }
 
-constexpr int BW_ST = 4;
+// epilogue load flavours (A/B switch at build time): read-once operands of the pointwise
+// step (the child's gates and c, its children's c, dCe)
+#ifdef FOLD_BWD_LDCS
+#define BWD_LDG(p) __ldcs(p)
+#define BWD_LDC(p) __ldcs(p)
+#else
+#define BWD_LDG(p) __ldg(p)
+#define BWD_LDC(p) __ldcg(p)
+#endif
+#ifndef FOLD_BW_ST
+#define FOLD_BW_ST 4
+#endif
+constexpr int BW_ST = FOLD_BW_ST;
 constexpr int BW_EPI = 8;                       // epilogue warps
 constexpr int BW_THREADS = 128 + 32 * BW_EPI;
 constexpr int BW_XS = 32 * 66;                  // floats per warp transpose buffer (32 x 64, padded)
@@ -1140,17 +1180,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
       BwdCursor cur;
       cur.init(L);
       int it = 0;
+      // A-operand box rows for a CTA holding m rows (narrow tiles load only their rows)
+      auto box_of = [](int m) { return m <= 0 ? 0 : m <= 16 ? 16 : m <= 64 ? 64 : BM; };
+      // this CTA's dZ box (map, first row) of tile T (bx = 0: the CTA holds no rows)
+      auto zbox = [&](const BwdCursor &c, int T, const CUtensorMap *&m, int &row) {
+        const int ctt = (c.r0 - nl) + ((T - c.t0) / c.NTn) * PM;
+        const int rw = min(PM, c.r1 - nl - ctt);
+        const int b = rank ? box_of(rw - BM) : box_of(min(rw, BM));
+        m = b == 16 ? &tmZ16 : b == 64 ? &tmZ64 : &tmZ;
+        row = ctt + (int)rank * BM;
+        return b;
+      };
+      const int pf = L.pf;
       for (int T = pair; T < total_tiles; T += npairs) {
         cur.seek(L, T);
         const int lt = T - cur.t0, NTn = cur.NTn, N = cur.N;
         const int ct = (cur.r0 - nl) + (lt / NTn) * PM;  // first cell of the pair tile
         const int rows = min(PM, cur.r1 - nl - ct);
         // narrow tiles load only the dZ rows they hold (see k_fwd_levels)
-        // A-operand box rows for a CTA holding m rows (narrow tiles load only their rows)
-        auto box_of = [](int m) { return m <= 0 ? 0 : m <= 16 ? 16 : m <= 64 ? 64 : BM; };
         const int bx0 = box_of(min(rows, BM)), bx1 = box_of(rows - BM), bx = rank ? bx1 : bx0;
         const CUtensorMap *mZ = bx == 16 ? &tmZ16 : bx == 64 ? &tmZ64 : &tmZ;
         const int mt = ct + (int)rank * BM;
+        // L2 prefetch: the dZ rows of a level were written one level earlier and mostly left
+        // L2 since; every column tile of the row tile requests the same k-block at about the
+        // same time, so without a prefetch each k-block costs a DRAM round trip that the
+        // 4-stage ring does not cover. Boxes pf k-blocks ahead are prefetched into L2, and
+        // the last pf k-blocks of a tile prefetch the head of this pair's next tile.
+        const CUtensorMap *mZn = nullptr;
+        int mtn = 0, bxn = 0;
+        if (pf > 0 && T + npairs < total_tiles) {
+          BwdCursor nx = cur;
+          nx.seek(L, T + npairs);
+          bxn = zbox(nx, T + npairs, mZn, mtn);
+        }
         const int nb = (lt % NTn) * N + (int)rank * (N / 2);
         const uint32_t bytes = (uint32_t)(bx0 + bx1) * 128 + N * 128;
         // the first stages' U boxes are issued before the dependency wait; narrow tiles pack
@@ -1164,6 +1226,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         const int pre = ready ? 0 : (nst < ST ? nst : ST);
         if (ready && kps == 1) {  // inputs published: one (A, U) box set per stage
           for (int kb = 0; kb < KB; kb++, it++) {
+            if (pf > 0) {
+              if (kb + pf < KB) {
+                if (bx) ptx::tma_prefetch_2d(mZ, (kb + pf) * BK, mt);
+              } else if (bxn && kb + pf - KB < KB) {
+                ptx::tma_prefetch_2d(mZn, (kb + pf - KB) * BK, mtn);
+              }
+            }
             const int s = it % ST;
             const uint32_t ph = (it / ST) & 1;
             ptx::mbar_wait(&empty[s], ph ^ 1);
@@ -1371,14 +1440,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
               const int64_t xc = xs_[j] - nl;
               const __nv_bfloat16 *gx = Gact + xc * ld_g + col;
 #pragma unroll
-              for (int g = 0; g < GATES; g++) graw[j][g] = __ldg(reinterpret_cast<const uint32_t *>(gx + g * ld));
+              for (int g = 0; g < GATES; g++) graw[j][g] = BWD_LDG(reinterpret_cast<const uint32_t *>(gx + g * ld));
               if constexpr (GATES == 5) {
-                cc[j] = __ldcg(reinterpret_cast<const float2 *>(C + (int64_t)xs_[j] * ld + col));
-                cl[j] = xls[j] >= nl ? __ldcg(reinterpret_cast<const float2 *>(C + (int64_t)xls[j] * ld + col))
+                cc[j] = BWD_LDC(reinterpret_cast<const float2 *>(C + (int64_t)xs_[j] * ld + col));
+                cl[j] = xls[j] >= nl ? BWD_LDC(reinterpret_cast<const float2 *>(C + (int64_t)xls[j] * ld + col))
                                      : make_float2(0.f, 0.f);
-                cr[j] = xrs[j] >= nl ? __ldcg(reinterpret_cast<const float2 *>(C + (int64_t)xrs[j] * ld + col))
+                cr[j] = xrs[j] >= nl ? BWD_LDC(reinterpret_cast<const float2 *>(C + (int64_t)xrs[j] * ld + col))
                                      : make_float2(0.f, 0.f);
-                dc[j] = __ldcg(reinterpret_cast<const float2 *>(dCe + e * S + col));
+                dc[j] = BWD_LDC(reinterpret_cast<const float2 *>(dCe + e * S + col));
               }
             }
           }
@@ -1808,7 +1877,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_dU_tc(const __grid_constant__ CUtensorMap tmZ2, const __grid_constant__ CUtensorMap tmAL,
                  const __grid_constant__ CUtensorMap tmAR, int n_cells, int S, int Mg, int NT, int kb_per_split,
                  float *__restrict__ out_base, int64_t split_stride, int accumulate, float *__restrict__ db_base,
-                 int db_accumulate) {
+                 int db_accumulate, int pf) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
   __shared__ __align__(8) uint64_t full[ST], empty[ST], tfull, dbfree[ST];
@@ -1853,6 +1922,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int jb = jn0 + (int)rank * (DU_N / 2);
     for (int it = 0; it < KB; it++) {
       const int kb = kb0 + it;
+      // L2 prefetch pf k-blocks ahead: dZ and the A planes stream from DRAM once, and the
+      // pairs sharing a row (column) tile request each k-block at about the same time
+      if (pf > 0 && it + pf < KB) {
+        const int kp = (kb + pf) * BK;
+        ptx::tma_prefetch_2d(&tmZ2, i0, kp);
+        ptx::tma_prefetch_2d(&tmZ2, i0 + 64, kp);
+        ptx::tma_prefetch_2d(tmB, jb, kp);
+        ptx::tma_prefetch_2d(tmB, jb + 64, kp);
+      }
       int s = it % ST;
       uint32_t ph = (it / ST) & 1;
       ptx::mbar_wait(&empty[s], ph ^ 1);
@@ -2128,6 +2206,14 @@ int max_pairs(K kernel, int threads, int smem) {
   return n < num_sms() / 2 ? n : num_sms() / 2;
 }
 
+// L2 prefetch distance (k-blocks) of the wide GEMMs' streamed operands, FOLD_PF_FWD /
+// FOLD_PF_BWD / FOLD_PF_DU (default 0 = off: measured at C2 B=1024, distances 4 / 8 / 16 made
+// dA +7%, dU +8-10% and C5 +15-25% slower; the ring's operands mostly hit L2 already)
+int l2_prefetch_dist(const char *env) {
+  const char *e = getenv(env);
+  return e ? atoi(e) : 0;
+}
+
 int dbg_bwd() {
   static int v = [] { const char *e = getenv("FOLD_DBG_BWD"); return e ? atoi(e) : 0; }();
   return v;
@@ -2181,7 +2267,8 @@ fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
   static thread_local int npairs_dev[kMaxDevices] = {};
   int &npairs_max = npairs_dev[cur_dev()];
   if (!npairs_max) npairs_max = max_pairs(kern, Cfg::THREADS, smem_bytes);
-  FwdLevels L{a.level_off, a.D, S, Cfg::WMAX, Cfg::WNAR, npairs_max / 2, Cfg::WMID, GATES, npairs_max};
+  FwdLevels L{a.level_off, a.D, S, Cfg::WMAX, Cfg::WNAR, npairs_max / 2, Cfg::WMID, GATES, npairs_max,
+              l2_prefetch_dist("FOLD_PF_FWD")};
   // the narrow tail: levels d0..D all of at most narrow_max rows go to k_fwd_narrow
   const int d0 = fwd_narrow_start(a.level_off_host, a.D, S);
   int64_t total = 0;
@@ -2466,7 +2553,7 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
     FOLD_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)nk, dim3(grid), dim3(NB_THREADS), args, (size_t)nsm, st));
     FOLD_LAUNCH_CHECK();
   }
-  BwdLevels L{a.level_off, d1 - 1, S, a.nl, ld_u, npairs_max};
+  BwdLevels L{a.level_off, d1 - 1, S, a.nl, ld_u, npairs_max, l2_prefetch_dist("FOLD_PF_BWD")};
   int64_t total = 0;
   for (int d = 2; d < d1; d++) {
     const int M = a.level_off_host[d + 1] - a.level_off_host[d];
@@ -2521,13 +2608,13 @@ fold_status tc_gemm_dU(int n_cells, int S, int gates, const __nv_bfloat16 *dZ, i
   const int dbacc = splits == 1 ? accumulate : 0;
   if (splits == 1) {
     k_gemm_dU_tc<<<grid, kThreads, DU_SMEM, st>>>(tmZ2, tmAL, tmAR, n_cells, S, gates * S, NT, kbps, dU, 0,
-                                                  accumulate, dbo, dbacc);
+                                                  accumulate, dbo, dbacc, l2_prefetch_dist("FOLD_PF_DU"));
     FOLD_LAUNCH_CHECK();
     return FOLD_OK;
   }
   if (!split_ws) return FOLD_E_WORKSPACE;
   k_gemm_dU_tc<<<grid, kThreads, DU_SMEM, st>>>(tmZ2, tmAL, tmAR, n_cells, S, gates * S, NT, kbps, split_ws, n, 0,
-                                                dbo, 0);
+                                                dbo, 0, l2_prefetch_dist("FOLD_PF_DU"));
   FOLD_LAUNCH_CHECK();
   FOLD_TRY(launch_reduce_splits(n, splits, split_ws, dU, accumulate, st));
   if (db) FOLD_TRY(launch_reduce_splits((int64_t)gates * S, splits, db_ws, db, accumulate, st));

@@ -79,6 +79,13 @@ __device__ __forceinline__ void tma_load_4d(const CUtensorMap *m, uint64_t *bar,
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "r"(w)
       : "memory");
 }
+// 2D tile prefetch into L2 (no shared memory, no completion): warms a box a few k-blocks
+// ahead of the ring so its TMA load hits L2 instead of waiting a DRAM round trip.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *m, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)),
+               "r"(x), "r"(y)
+               : "memory");
+}
 // Row gather: 4 arbitrary rows y0..y3, columns [x, x + box_cols) -> 4 consecutive smem rows.
 __device__ __forceinline__ void tma_gather4(const CUtensorMap *m, uint64_t *bar, void *dst, int x, int y0, int y1,
                                             int y2, int y3) {
