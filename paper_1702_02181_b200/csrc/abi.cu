@@ -3,6 +3,7 @@
 // iteration per depth) forward and in reverse for the backward (L49).
 #include <cstring>
 
+#include "../../include/fold_mo.h"
 #include "exec.cuh"
 
 namespace fold {
@@ -10,6 +11,17 @@ namespace fold {
 fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws, size_t ws_bytes, cudaStream_t st);
 int debug_sched_trace(unsigned long long *host);
 size_t schedule_workspace(int64_t N, int64_t G);
+size_t mo_schedule_workspace(const fold_mo_table *t, int64_t N, int64_t G);
+fold_status run_mo_schedule(const fold_mo_table *t, const fold_mo_graphs *gr, fold_mo_schedule_t *s, void *ws,
+                            size_t ws_bytes, cudaStream_t st);
+size_t mo_acts_bytes(const fold_mo_table *t, const fold_mo_schedule_t *s);
+size_t mo_forward_workspace(const fold_mo_table *t, const fold_mo_schedule_t *s);
+size_t mo_backward_workspace(const fold_mo_table *t, const fold_mo_schedule_t *s);
+fold_status mo_forward(const fold_mo_table *t, const fold_mo_schedule_t *s, const fold_mo_model *model, void *acts,
+                       float *h_root, void *ws, size_t ws_bytes, cudaStream_t st);
+fold_status mo_backward(const fold_mo_table *t, const fold_mo_schedule_t *s, const fold_mo_model *model,
+                        const void *acts, const float *dh_root, fold_mo_grads *gr, void *ws, size_t ws_bytes,
+                        cudaStream_t st);
 extern thread_local int32_t g_last_detail;
 extern thread_local int32_t g_last_ctx[3];
 
@@ -432,6 +444,7 @@ const char *fold_status_string(fold_status s) {
     case FOLD_E_UNSUPPORTED: return "FOLD_E_UNSUPPORTED";
     case FOLD_E_LEVEL: return "FOLD_E_LEVEL";
   }
+  if ((int)s == FOLD_E_TYPE) return "FOLD_E_TYPE";
   return "FOLD_E_UNKNOWN";
 }
 
@@ -443,6 +456,36 @@ fold_status fold_last_error_context(int32_t *node, int32_t *depth, int32_t *op) 
   return g_last_ctx[0] >= 0 ? FOLD_OK : FOLD_E_INVALID;
 }
 int32_t fold_abi_version(void) { return FOLD_ABI_VERSION; }
+
+// ----------------------------------------------------------------- multi-op (fold_mo.h)
+size_t fold_mo_schedule_workspace(const fold_mo_table *table, int32_t n_nodes, int32_t n_graphs) {
+  return fold::mo_schedule_workspace(table, n_nodes, n_graphs);
+}
+fold_status fold_mo_schedule(const fold_mo_table *table, const fold_mo_graphs *graphs, fold_mo_schedule_t *sched,
+                             void *ws, size_t ws_bytes, void *stream) {
+  fold::ProfScope ps(fold::K_SCHED, (cudaStream_t)stream);
+  return fold::run_mo_schedule(table, graphs, sched, ws, ws_bytes, (cudaStream_t)stream);
+}
+size_t fold_mo_acts_bytes(const fold_mo_table *table, const fold_mo_schedule_t *sched) {
+  return fold::mo_acts_bytes(table, sched);
+}
+size_t fold_mo_forward_workspace(const fold_mo_table *table, const fold_mo_schedule_t *sched) {
+  return fold::mo_forward_workspace(table, sched);
+}
+fold_status fold_mo_forward(const fold_mo_table *table, const fold_mo_schedule_t *sched, const fold_mo_model *model,
+                            void *acts, float *h_root, void *ws, size_t ws_bytes, void *stream) {
+  fold::ProfScope ps(fold::K_CELL_FWD, (cudaStream_t)stream);
+  return fold::mo_forward(table, sched, model, acts, h_root, ws, ws_bytes, (cudaStream_t)stream);
+}
+size_t fold_mo_backward_workspace(const fold_mo_table *table, const fold_mo_schedule_t *sched) {
+  return fold::mo_backward_workspace(table, sched);
+}
+fold_status fold_mo_backward(const fold_mo_table *table, const fold_mo_schedule_t *sched, const fold_mo_model *model,
+                             const void *acts, const float *dh_root, fold_mo_grads *grads, void *ws, size_t ws_bytes,
+                             void *stream) {
+  fold::ProfScope ps(fold::K_GEMM_DA, (cudaStream_t)stream);
+  return fold::mo_backward(table, sched, model, acts, dh_root, grads, ws, ws_bytes, (cudaStream_t)stream);
+}
 
 /* instrumentation: per-phase timeline of the last FOLD_DBG_SCHED=1 schedule (block 0) */
 int32_t fold_debug_sched_trace(unsigned long long *host) { return fold::debug_sched_trace(host); }

@@ -1,5 +1,7 @@
 // exec.cuh — declarations shared by the executor translation units.
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace fold {
@@ -152,6 +154,29 @@ struct TfOperand {
 fold_status gemm_tf32(const TfOperand &A, const TfOperand &B, int M, int N, int K, float *C, int64_t ldc,
                       int accumulate, int npass, float *split_ws, int64_t split_ws_floats, cudaStream_t st);
 int64_t gemm_tf32_split_floats(int M, int N, int K);
+// Grouped TF32 GEMM (multi-op levels, fold_mo.h): up to kTfGroupMax independent problems
+// C_i = A_i * B_i in ONE launch (problems with M or N <= 0 are skipped); split-K partials of
+// the problems that use them go to split_ws (gemm_tf32_grouped_ws_floats floats).
+constexpr int kTfGroupMax = 8;
+struct TfProblem {
+  TfOperand A, B;
+  int M, N, K;
+  float *C;
+  int64_t ldc;
+  int accumulate;
+};
+struct alignas(64) TfGroupArgs {
+  CUtensorMap ta[kTfGroupMax], tb[kTfGroupMax];
+  int a_mn[kTfGroupMax], b_mn[kTfGroupMax], M[kTfGroupMax], N[kTfGroupMax], K[kTfGroupMax];
+  int kbps[kTfGroupMax], nsplit[kTfGroupMax], ntn[kTfGroupMax], accumulate[kTfGroupMax];
+  float *C[kTfGroupMax];
+  int64_t ldc[kTfGroupMax], split_stride[kTfGroupMax];
+  int tile_start[kTfGroupMax + 1];
+  int n;
+};
+fold_status gemm_tf32_grouped(const TfProblem *q, int n, int npass, float *split_ws, int64_t split_ws_floats,
+                              cudaStream_t st);
+int64_t gemm_tf32_grouped_ws_floats(const TfProblem *q, int n, int npass);
 // FP32 / TF32 mode level helpers (gemm_tf32.cu)
 // Acat[c][0:S] = H[gather[2r]], Acat[c][S:2S] = H[gather[2r+1]] for rows r in [r0, r1), c = r - nl
 fold_status launch_gather_cat(int r0, int r1, int nl, int S, int ld, const int32_t *gather, const float *H,

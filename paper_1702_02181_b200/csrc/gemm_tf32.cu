@@ -109,11 +109,13 @@ __device__ __forceinline__ void load_block(const CUtensorMap *m, uint64_t *bar, 
   }
 }
 
+// One output tile (m0, n0) of one problem, K blocks [kb0, kb0 + kb_per_split) (the body of
+// the single-problem and the grouped kernels below).
 template <int BN, int NPASS>
-__global__ void __launch_bounds__(TF_THREADS, 1)
-    k_gemm_tf32(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int a_mn, int b_mn,
-                int M, int N, int K, int kb_per_split, float *__restrict__ C, int64_t ldc, int64_t split_stride,
-                int accumulate) {
+__device__ __forceinline__ void gemm_tf32_tile(const CUtensorMap *pA, const CUtensorMap *pB, int a_mn, int b_mn,
+                                               int M, int N, int K, int kb_per_split, float *__restrict__ C,
+                                               int64_t ldc, int64_t split_stride, int accumulate, int m0, int n0,
+                                               int split) {
   using Cfg = TfCfg<BN, NPASS>;
   constexpr int ST = Cfg::NST;
   extern __shared__ uint8_t smem_raw[];
@@ -121,12 +123,12 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
   __shared__ __align__(8) uint64_t full[ST], ready[ST], empty[ST], tfull;
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * TM;
   const int KBall = (K + TK - 1) / TK;
-  const int kb0 = blockIdx.z * kb_per_split;
+  const int kb0 = split * kb_per_split;
   const int kb1 = min(KBall, kb0 + kb_per_split);
   const int KB = kb1 > kb0 ? kb1 - kb0 : 0;
-  float *Cz = C + (int64_t)blockIdx.z * split_stride;
+  float *Cz = C + (int64_t)split * split_stride;
+  const CUtensorMap &tmA = *pA, &tmB = *pB;
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < ST; s++) {
       ptx::mbar_init(&full[s], 1);
@@ -228,6 +230,30 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
   if (warp == 2) { ptx::tc_fence_after(); ptx::tmem_dealloc(tbase, BN); }
 }
 
+template <int BN, int NPASS>
+__global__ void __launch_bounds__(TF_THREADS, 1)
+    k_gemm_tf32(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int a_mn, int b_mn,
+                int M, int N, int K, int kb_per_split, float *__restrict__ C, int64_t ldc, int64_t split_stride,
+                int accumulate) {
+  gemm_tf32_tile<BN, NPASS>(&tmA, &tmB, a_mn, b_mn, M, N, K, kb_per_split, C, ldc, split_stride, accumulate,
+                            blockIdx.y * TM, blockIdx.x * BN, blockIdx.z);
+}
+
+// Grouped: up to kTfGroupMax independent problems in ONE launch (the multi-op executor's
+// per-level operations, "each iteration of the loop will evaluate all of the
+// operations at a particular depth"); blockIdx.x enumerates the problems' output tiles
+// (problem p owns tiles [tile_start[p], tile_start[p + 1])), blockIdx.z the K split.
+template <int BN, int NPASS>
+__global__ void __launch_bounds__(TF_THREADS, 1) k_gemm_tf32_grouped(const __grid_constant__ TfGroupArgs P) {
+  int p = 0;
+  while (p + 1 < P.n && (int)blockIdx.x >= P.tile_start[p + 1]) p++;
+  if ((int)blockIdx.z >= P.nsplit[p]) return;  // another problem of the launch uses more splits
+  const int lt = (int)blockIdx.x - P.tile_start[p];
+  const int m0 = (lt / P.ntn[p]) * TM, n0 = (lt % P.ntn[p]) * BN;
+  gemm_tf32_tile<BN, NPASS>(&P.ta[p], &P.tb[p], P.a_mn[p], P.b_mn[p], P.M[p], P.N[p], P.K[p], P.kbps[p], P.C[p],
+                            P.ldc[p], P.split_stride[p], P.accumulate[p], m0, n0, blockIdx.z);
+}
+
 template <typename K>
 fold_status set_smem_tf(K kernel, int bytes) {
   static thread_local std::unordered_map<const void *, int> set;
@@ -294,6 +320,23 @@ fold_status launch_tf(const CUtensorMap &ma, const CUtensorMap &mb, const TfOper
                                             (int64_t)M * N, 0);
   FOLD_LAUNCH_CHECK();
   return launch_reduce_splits((int64_t)M * N, splits, split_ws, C, accumulate, st);
+}
+
+// Grouped launch: every problem's tiles in one grid (BN = 128), per-problem split-K into
+// partial slabs of split_ws (reduced per problem in fixed order, deterministic).
+int tf_group_splits(const TfProblem &q, int npass) {
+  if (q.M <= 0 || q.N <= 0) return 1;
+  return tf_splits(q.M, q.N, q.K, npass);
+}
+
+template <int NPASS>
+fold_status launch_tf_grouped(TfGroupArgs &P, int zmax, cudaStream_t st) {
+  using Cfg = TfCfg<128, NPASS>;
+  auto kern = k_gemm_tf32_grouped<128, NPASS>;
+  FOLD_TRY(set_smem_tf(kern, Cfg::SMEM));
+  kern<<<dim3((unsigned)P.tile_start[P.n], 1, (unsigned)zmax), TF_THREADS, Cfg::SMEM, st>>>(P);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
 }
 
 // ---------------------------------------------------------------- level helpers (FP32 / TF32 modes)
@@ -434,6 +477,61 @@ fold_status launch_prep_U_tf(int gates, int S, int ld, const float *U, float *Uf
   if (blocks > 148 * 16) blocks = 148 * 16;
   k_prep_U_tf<<<(unsigned)blocks, 256, 0, st>>>(gates, S, ld, tf_ld_u(S), U, Ufwd, Ubwd);
   FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+int64_t gemm_tf32_grouped_ws_floats(const TfProblem *q, int n, int npass) {
+  int64_t tot = 0;
+  for (int i = 0; i < n; i++) {
+    const int sp = tf_group_splits(q[i], npass);
+    if (sp > 1) tot += (int64_t)sp * q[i].M * q[i].N;
+  }
+  return tot;
+}
+
+fold_status gemm_tf32_grouped(const TfProblem *q, int n, int npass, float *split_ws, int64_t split_ws_floats,
+                              cudaStream_t st) {
+  if (npass != 1 && npass != 3) return FOLD_E_INVALID;
+  if (n > kTfGroupMax) return FOLD_E_INVALID;
+  TfGroupArgs P{};
+  int64_t ws_off = 0;
+  int zmax = 1, tiles = 0;
+  int red_n = 0, red_sp[kTfGroupMax] = {};
+  float *red_part[kTfGroupMax] = {}, *red_out[kTfGroupMax] = {};
+  int64_t red_cnt[kTfGroupMax] = {};
+  int red_acc[kTfGroupMax] = {};
+  for (int i = 0; i < n; i++) {
+    const TfProblem &x = q[i];
+    if (x.M <= 0 || x.N <= 0) continue;
+    const int k = P.n;
+    FOLD_TRY(tf_map(&P.ta[k], x.A, x.M, x.K > 0 ? x.K : 1, TM));
+    FOLD_TRY(tf_map(&P.tb[k], x.B, x.N, x.K > 0 ? x.K : 1, 128));
+    P.a_mn[k] = x.A.mn_major; P.b_mn[k] = x.B.mn_major;
+    P.M[k] = x.M; P.N[k] = x.N; P.K[k] = x.K;
+    int sp = tf_group_splits(x, npass);
+    if (sp > 1 && (!split_ws || ws_off + (int64_t)sp * x.M * x.N > split_ws_floats || x.ldc != x.N)) sp = 1;
+    const int KBall = (int)cdiv(x.K > 0 ? x.K : 1, TK);
+    P.kbps[k] = (int)cdiv(KBall, sp);
+    P.nsplit[k] = sp;
+    if (sp > 1) {
+      P.C[k] = split_ws + ws_off; P.ldc[k] = x.N; P.split_stride[k] = (int64_t)x.M * x.N; P.accumulate[k] = 0;
+      red_part[red_n] = split_ws + ws_off; red_out[red_n] = x.C; red_cnt[red_n] = (int64_t)x.M * x.N;
+      red_sp[red_n] = sp; red_acc[red_n] = x.accumulate; red_n++;
+      ws_off += (int64_t)sp * x.M * x.N;
+    } else {
+      P.C[k] = x.C; P.ldc[k] = x.ldc; P.split_stride[k] = 0; P.accumulate[k] = x.accumulate;
+    }
+    P.ntn[k] = (int)cdiv(x.N, 128);
+    P.tile_start[k] = tiles;
+    tiles += (int)(cdiv(x.M, TM) * P.ntn[k]);
+    if (sp > zmax) zmax = sp;
+    P.n++;
+  }
+  if (P.n == 0) return FOLD_OK;
+  P.tile_start[P.n] = tiles;
+  FOLD_TRY(npass == 3 ? launch_tf_grouped<3>(P, zmax, st) : launch_tf_grouped<1>(P, zmax, st));
+  for (int r = 0; r < red_n; r++)
+    FOLD_TRY(launch_reduce_splits(red_cnt[r], red_sp[r], red_part[r], red_out[r], red_acc[r], st));
   return FOLD_OK;
 }
 

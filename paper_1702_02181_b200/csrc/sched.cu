@@ -15,6 +15,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "../../include/fold_mo.h"
 
 namespace fold {
 
@@ -672,6 +673,224 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
   sched_stamp(a.dbg, 12);
 }
 
+
+// ================================================================ multi-op schedule (NEXT-3)
+// fold_mo.h: several operations and tensor types per depth. One
+// cooperative kernel, phases separated by grid barriers: validate (op table arities and
+// types, L33) -> depth by relaxation rounds (a node whose children all have depths takes
+// 1 + their max, L40; one barrier per round, D + 1 rounds; nodes never assigned depend on a
+// cycle) -> stable sort by key = depth*K + op (L42: the batched instances, ties by id) ->
+// stable partition of that order by output type (L43: per-type concatenation in depth and
+// enumeration order) -> per-(type, depth) offsets and (d, t, i) edge labels (L44) -> the
+// executor's consumer CSR, root lists and (op, token) leaf segments.
+enum { MOE_CHILD = 0, MOE_OP = 1, MOE_ARITY = 2, MOE_TYPE = 3, MOE_TOKEN = 4, MOE_ROOT = 5, MOE_CYCLE = 6,
+       MOE_NCLASS = 7 };
+const fold_status kMoErrStatus[MOE_NCLASS] = {FOLD_E_CHILD_RANGE, FOLD_E_OP_RANGE, FOLD_E_ARITY,
+                                             (fold_status)FOLD_E_TYPE, FOLD_E_TOKEN_RANGE, FOLD_E_ROOT_RANGE,
+                                             FOLD_E_CYCLE};
+
+struct MoSchedArgs {
+  int N, G, K, T;
+  int kind[FOLD_MO_MAX_OPS], arity[FOLD_MO_MAX_OPS], in_type[FOLD_MO_MAX_OPS], out_type[FOLD_MO_MAX_OPS],
+      vocab[FOLD_MO_MAX_OPS];
+  const int32_t *op, *child, *token, *root;
+  fold_mo_schedule_t s;
+  SchedWs w;
+  int32_t *opos, *gcnt, *tcnt, *tscan;
+};
+
+__global__ void __launch_bounds__(kSchedThreads) k_mo_schedule(MoSchedArgs a) {
+  extern __shared__ int dsm[];
+  __shared__ int sw[32];
+  SchedWs &w = a.w;
+  fold_mo_schedule_t &s = a.s;
+  int32_t *flags = w.flags;
+  const int N = a.N, G = a.G, K = a.K, T = a.T;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid, gstride = (int64_t)gridDim.x * blockDim.x;
+
+  // ---- P0: flags, depths unassigned (0)
+  if (blockIdx.x == 0 && tid < F_NFLAGS && (tid < F_BAR || tid > F_BAR + 1))
+    flags[tid] = tid < MOE_NCLASS ? INT_MAX : 0;
+  for (int64_t i = gtid; i < N; i += gstride) s.depth[i] = 0;
+  gsync(flags);
+
+  // ---- P1: validate (CHILD_RANGE, OP_RANGE, ARITY, TYPE, TOKEN_RANGE, ROOT_RANGE)
+  for (int64_t i = gtid; i < N; i += gstride) {
+    const int n = (int)i, o = a.op[n], c0 = a.child[2 * n], c1 = a.child[2 * n + 1];
+    const bool crange = c0 < -1 || c0 >= N || c1 < -1 || c1 >= N;
+    if (crange) atomicMin(&flags[F_ERR0 + MOE_CHILD], n);
+    if (o < 0 || o >= K) { atomicMin(&flags[F_ERR0 + MOE_OP], n); continue; }
+    const int ar = a.arity[o];
+    const bool ar_ok = (ar > 0 ? c0 >= 0 : c0 == -1) && (ar > 1 ? c1 >= 0 : c1 == -1);
+    if (!ar_ok) atomicMin(&flags[F_ERR0 + MOE_ARITY], n);
+    if (!crange && ar_ok)
+      for (int k = 0; k < ar; k++) {
+        const int oc = a.op[a.child[2 * n + k]];
+        if (oc >= 0 && oc < K && a.out_type[oc] != a.in_type[o]) atomicMin(&flags[F_ERR0 + MOE_TYPE], n);
+      }
+    if (a.kind[o] == FOLD_MO_EMBED && (a.token[n] < 0 || a.token[n] >= a.vocab[o]))
+      atomicMin(&flags[F_ERR0 + MOE_TOKEN], n);
+  }
+  for (int64_t g = gtid; g < G; g += gstride)
+    if (a.root[g] < 0 || a.root[g] >= N) atomicMin(&flags[F_ERR0 + MOE_ROOT], (int)g);
+  gsync(flags);
+  for (int e = 0; e < MOE_CYCLE; e++)
+    if (ld_volatile(&flags[F_ERR0 + e]) != INT_MAX) return;  // uniform across blocks
+
+  // ---- P2: depths by relaxation rounds (L40); round r's "changed" flag in F_QCNT + r % 3
+  for (int r = 0;; r++) {
+    const int slot = F_QCNT + r % 3;
+    if (gtid == 0) flags[F_QCNT + (r + 1) % 3] = 0;
+    bool changed = false;
+    const int64_t nloop = cdiv(N, gstride) * gstride;
+    for (int64_t i = gtid; i < nloop; i += gstride) {
+      bool ch = false;
+      if (i < N && ld_volatile(&s.depth[i]) == 0) {
+        const int n = (int)i, ar = a.arity[a.op[n]];
+        int dm = 0;
+        bool ready = true;
+        for (int k = 0; k < ar; k++) {
+          const int dc = ld_volatile(&s.depth[a.child[2 * n + k]]);
+          ready = ready && dc > 0;
+          dm = dc > dm ? dc : dm;
+        }
+        if (ready) {
+          s.depth[n] = 1 + dm;
+          atomicMax(&flags[F_MAXDEPTH], 1 + dm);
+          ch = true;
+        }
+      }
+      changed = changed || ch;
+    }
+    if (__any_sync(0xffffffffu, changed) && lane == 0) flags[slot] = 1;
+    gsync(flags);
+    if (ld_volatile(&flags[slot]) == 0) break;
+  }
+  for (int64_t i = gtid; i < N; i += gstride)
+    if (ld_volatile(&s.depth[i]) == 0) atomicMin(&flags[F_ERR0 + MOE_CYCLE], (int)i);
+  gsync(flags);
+  if (ld_volatile(&flags[F_ERR0 + MOE_CYCLE]) != INT_MAX) return;
+  const int D = ld_volatile(&flags[F_MAXDEPTH]);
+
+  // ---- P3: (depth, op) groups (L42) and the stable order by key = depth*K + op
+  const int nk = (D + 1) * K;
+  for (int64_t k = gtid; k <= nk; k += gstride) a.gcnt[k] = 0;
+  gsync(flags);
+  for (int64_t i = gtid; i < N; i += gstride) {
+    const int key = s.depth[i] * K + a.op[i];
+    w.ka[i] = (uint32_t)key;
+    w.va[i] = (int)i;
+    atomicAdd(&a.gcnt[key], 1);
+  }
+  gsync(flags);
+  grid_excl_scan(a.gcnt, s.group_off, nk + 1, nullptr, w, sw);
+  for (int64_t k = gtid; k <= nk && k < kLoMirror; k += gstride) flags[F_NFLAGS + k] = s.group_off[k];
+  const uint32_t *sk;
+  const int32_t *sv;
+  sort_pairs(w, N, dev_bits_for(nk - 1), sk, sv, dsm);
+  for (int64_t i = gtid; i < N; i += gstride) {
+    s.order[i] = sv[i];
+    a.opos[sv[i]] = (int)i;
+  }
+  gsync(flags);
+
+  // ---- P4: per-type pools (L43): the order, stably partitioned by output type
+  for (int64_t i = gtid; i < N; i += gstride) {
+    const int n = s.order[i];
+    w.ka[i] = (uint32_t)a.out_type[a.op[n]];
+    w.va[i] = n;
+  }
+  gsync(flags);
+  sort_pairs(w, N, dev_bits_for(T - 1), sk, sv, dsm);
+  for (int64_t t = gtid; t <= T; t += gstride) {
+    int lo = 0, hi = N;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if ((int)sk[mid] < (int)t) lo = mid + 1; else hi = mid; }
+    s.type_off[t] = lo;
+  }
+  const int tl = T * (D + 2);
+  for (int64_t k = gtid; k <= tl; k += gstride) a.tcnt[k] = 0;
+  gsync(flags);
+  for (int64_t i = gtid; i < N; i += gstride) {
+    const int n = sv[i], t = (int)sk[i];
+    s.pool[i] = n;
+    s.pool_row[n] = (int)i - s.type_off[t];
+    atomicAdd(&a.tcnt[t * (D + 2) + s.depth[n]], 1);
+  }
+  gsync(flags);
+  grid_excl_scan(a.tcnt, a.tscan, tl + 1, nullptr, w, sw);
+  for (int64_t k = gtid; k < tl; k += gstride) s.tlevel_off[k] = a.tscan[k] - a.tscan[(k / (D + 2)) * (D + 2)];
+  gsync(flags);
+
+  // ---- P5: edge labels (d, t, i) (L44)
+  for (int64_t e = gtid; e < 2 * (int64_t)N; e += gstride) {
+    const int c = a.child[e];
+    int32_t *lab = s.label + 3 * e;
+    if (c < 0) { lab[0] = lab[1] = lab[2] = -1; continue; }
+    const int d = s.depth[c], t = a.out_type[a.op[c]];
+    lab[0] = d; lab[1] = t; lab[2] = s.pool_row[c] - s.tlevel_off[t * (D + 2) + d];
+  }
+
+  // ---- P6: consumers by global pool index: edges e = 2 * order position + k, stable
+  for (int64_t e = gtid; e < 2 * (int64_t)N; e += gstride) {
+    const int m = s.order[e >> 1], c = a.child[2 * m + (int)(e & 1)];
+    w.ka[e] = (uint32_t)(c >= 0 ? s.type_off[a.out_type[a.op[c]]] + s.pool_row[c] : N);
+    w.va[e] = (int)e;
+  }
+  gsync(flags);
+  sort_pairs(w, 2 * N, dev_bits_for(N), sk, sv, dsm);
+  for (int64_t i = gtid; i < 2 * (int64_t)N; i += gstride) s.cons_edge[i] = sv[i];
+  for (int64_t r = gtid; r <= N; r += gstride) {
+    int lo = 0, hi = 2 * N;
+    while (lo < hi) { const int mid = (lo + hi) >> 1; if ((int)sk[mid] < (int)r) lo = mid + 1; else hi = mid; }
+    s.cons_off[r] = lo;
+  }
+  gsync(flags);
+
+  // ---- P7: graphs rooted at each node (by global pool index), ascending g
+  if (G > 0) {
+    for (int64_t g = gtid; g < G; g += gstride) {
+      const int n = a.root[g];
+      w.ka[g] = (uint32_t)(s.type_off[a.out_type[a.op[n]]] + s.pool_row[n]);
+      w.va[g] = (int)g;
+    }
+    gsync(flags);
+    sort_pairs(w, G, dev_bits_for(N - 1), sk, sv, dsm);
+    for (int64_t i = gtid; i < G; i += gstride) s.root_graph[i] = sv[i];
+    for (int64_t r = gtid; r <= N; r += gstride) {
+      int lo = 0, hi = G;
+      while (lo < hi) { const int mid = (lo + hi) >> 1; if ((int)sk[mid] < (int)r) lo = mid + 1; else hi = mid; }
+      s.root_off[r] = lo;
+    }
+  } else {
+    for (int64_t r = gtid; r <= N; r += gstride) s.root_off[r] = 0;
+  }
+  gsync(flags);
+
+  // ---- P8: leaves (the depth-1 groups, all EMBED) by (op, token, order position)
+  const int l0 = s.group_off[K], nl = s.group_off[2 * K] - l0;
+  int vmax = 1;
+  for (int o = 0; o < K; o++) vmax = a.vocab[o] > vmax ? a.vocab[o] : vmax;
+  const int vbits = dev_bits_for(vmax - 1);
+  for (int64_t i = gtid; i < nl; i += gstride) {
+    const int p = l0 + (int)i, n = s.order[p];
+    w.ka[i] = ((uint32_t)a.op[n] << vbits) | (uint32_t)a.token[n];
+    w.va[i] = p;
+  }
+  if (gtid == 0) flags[F_NLEAVES] = nl;
+  gsync(flags);
+  sort_pairs(w, nl, vbits + dev_bits_for(K - 1), sk, sv, dsm);
+  for (int64_t i = gtid; i < nl; i += gstride) {
+    s.leaf_order[i] = sv[i];
+    w.seg_flag[i] = (i == 0 || sk[i] != sk[i - 1]) ? 1 : 0;
+  }
+  gsync(flags);
+  grid_excl_scan(w.seg_flag, w.seg_scan, nl, &flags[F_NSEG], w, sw);
+  for (int64_t i = gtid; i < nl; i += gstride)
+    if (w.seg_flag[i]) s.leaf_seg[w.seg_scan[i]] = (int)i;
+  if (gtid == 0) s.leaf_seg[ld_volatile(&flags[F_NSEG])] = nl;
+}
+
 }  // namespace
 
 thread_local int32_t g_last_detail = -1;
@@ -812,6 +1031,136 @@ fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr
   // the (unconsumed) roots -- the backward can then form each child's gradient in the
   // epilogue of its single consumer's dA tile
   s->tree_like = (hflags[F_MULTI] == 0 && N - 2 * s->n_cells == hflags[F_NDISTROOT]) ? 1 : 0;
+  return FOLD_OK;
+}
+
+// ---------------------------------------------------------------- multi-op host side
+namespace {
+struct MoWsLayout {
+  SchedWs w;
+  int32_t *opos, *gcnt, *tcnt, *tscan;
+  size_t bytes;
+};
+MoWsLayout mo_ws_layout(void *base, int64_t N, int64_t G, int K, int T) {
+  MoWsLayout L{};
+  L.w = sched_ws_layout(base, N, G);
+  size_t off = L.w.bytes;
+  auto take = [&](size_t bytes) { size_t o = off; off = align256(off + bytes); return o; };
+  const size_t o_opos = take((N + 1) * 4), o_g = take(((N + 1) * K + 2) * 4);
+  const size_t o_t = take(((size_t)T * (N + 2) + 2) * 4), o_ts = take(((size_t)T * (N + 2) + 2) * 4);
+  L.bytes = off;
+  if (base) {
+    char *b = (char *)base;
+    L.opos = (int32_t *)(b + o_opos); L.gcnt = (int32_t *)(b + o_g);
+    L.tcnt = (int32_t *)(b + o_t); L.tscan = (int32_t *)(b + o_ts);
+  }
+  return L;
+}
+}  // namespace
+
+bool mo_table_ok(const fold_mo_table *t) {
+  if (!t || t->n_ops < 1 || t->n_ops > FOLD_MO_MAX_OPS || t->n_types < 1 || t->n_types > FOLD_MO_MAX_TYPES) return false;
+  for (int i = 0; i < t->n_types; i++) if (t->S[i] < 1 || t->S[i] > 4096) return false;
+  for (int o = 0; o < t->n_ops; o++) {
+    const int k = t->kind[o], a = t->arity[o];
+    if (t->out_type[o] < 0 || t->out_type[o] >= t->n_types) return false;
+    if (k == FOLD_MO_EMBED) { if (a != 0 || t->vocab[o] < 1 || t->vocab[o] > (1 << 24)) return false; continue; }
+    if (k != FOLD_MO_LSTM && k != FOLD_MO_RNN) return false;
+    if (a < 1 || a > 2 || t->in_type[o] < 0 || t->in_type[o] >= t->n_types) return false;
+    if (k == FOLD_MO_LSTM && t->in_type[o] != t->out_type[o]) return false;
+  }
+  return true;
+}
+
+size_t mo_schedule_workspace(const fold_mo_table *t, int64_t N, int64_t G) {
+  if (!mo_table_ok(t)) return 0;
+  return mo_ws_layout(nullptr, N < 0 ? 0 : N, G < 0 ? 0 : G, t->n_ops, t->n_types).bytes;
+}
+
+fold_status run_mo_schedule(const fold_mo_table *t, const fold_mo_graphs *gr, fold_mo_schedule_t *s, void *ws_ptr,
+                            size_t ws_bytes, cudaStream_t st) {
+  g_last_detail = -1;
+  g_last_ctx[0] = g_last_ctx[1] = g_last_ctx[2] = -1;
+  if (!mo_table_ok(t) || !gr || !s) return FOLD_E_INVALID;
+  const int N = gr->n_nodes, G = gr->n_graphs, K = t->n_ops, T = t->n_types;
+  if (N < 0 || G < 0) return FOLD_E_INVALID;
+  s->n_nodes = N; s->n_graphs = G; s->n_levels = 0; s->n_leaf_segs = 0;
+  s->op = gr->op; s->child = gr->child; s->token = gr->token; s->root = gr->root;
+  if (N == 0) {
+    if (G > 0) { g_last_detail = 0; g_last_ctx[0] = 0; return FOLD_E_ROOT_RANGE; }
+    if (s->group_off_host) s->group_off_host[0] = 0;
+    return FOLD_OK;
+  }
+  if (!gr->op || !gr->child || !gr->token || (G > 0 && !gr->root)) return FOLD_E_INVALID;
+  if (!s->depth || !s->group_off || !s->type_off || !s->pool || !s->pool_row || !s->tlevel_off || !s->label ||
+      !s->order || !s->cons_off || !s->cons_edge || !s->root_off || (G > 0 && !s->root_graph) || !s->leaf_seg ||
+      !s->leaf_order || !s->group_off_host)
+    return FOLD_E_INVALID;
+  MoWsLayout L = mo_ws_layout(ws_ptr, N, G, K, T);
+  if (!ws_ptr || ws_bytes < L.bytes) return FOLD_E_WORKSPACE;
+  const size_t dsmem = (size_t)(kSchedWarps * (kMaxBins + 1) + 2 * kMaxBins + 64) * sizeof(int);
+  static thread_local int max_blocks_dev[kMaxDevices] = {};
+  const int dev = cur_dev();
+  int &max_blocks = max_blocks_dev[dev];
+  if (!max_blocks) {
+    int nsm, occ = 0;
+    FOLD_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    FOLD_CUDA_TRY(cudaFuncSetAttribute(k_mo_schedule, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
+    FOLD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mo_schedule, kSchedThreads, dsmem));
+    if (occ < 1) occ = 1;
+    max_blocks = nsm * (occ < 2 ? occ : 2);
+    if (max_blocks > kMaxSchedBlocks) max_blocks = kMaxSchedBlocks;
+  }
+  int blocks = N <= kOneBlockN ? 1 : (int)cdiv(N, 2048);
+  if (blocks > max_blocks) blocks = max_blocks;
+  MoSchedArgs args{};
+  args.N = N; args.G = G; args.K = K; args.T = T;
+  for (int o = 0; o < K; o++) {
+    args.kind[o] = t->kind[o]; args.arity[o] = t->arity[o]; args.in_type[o] = t->in_type[o];
+    args.out_type[o] = t->out_type[o]; args.vocab[o] = t->vocab[o];
+  }
+  args.op = gr->op; args.child = gr->child; args.token = gr->token; args.root = gr->root;
+  args.s = *s; args.w = L.w;
+  args.opos = L.opos; args.gcnt = L.gcnt; args.tcnt = L.tcnt; args.tscan = L.tscan;
+  if (blocks == 1) {
+    k_mo_schedule<<<1, kSchedThreads, dsmem, st>>>(args);
+  } else {
+    FOLD_CUDA_TRY(cudaMemsetAsync(L.w.flags + F_BAR, 0, 2 * sizeof(int32_t), st));
+    void *kargs[] = {(void *)&args};
+    FOLD_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_mo_schedule, dim3(blocks), dim3(kSchedThreads), kargs,
+                                              dsmem, st));
+  }
+  FOLD_LAUNCH_CHECK();
+  // the one host sync: flags + the group_off prefix mirrored after them
+  static thread_local int32_t *hbuf = nullptr;
+  if (!hbuf) FOLD_CUDA_TRY(cudaMallocHost((void **)&hbuf, (F_NFLAGS + kLoMirror) * sizeof(int32_t)));
+  const int64_t cap = (int64_t)(N + 1) * K + 1;
+  const int npre = (int)(cap < kLoMirror ? cap : kLoMirror);
+  FOLD_CUDA_TRY(cudaMemcpyAsync(hbuf, L.w.flags, (size_t)(F_NFLAGS + npre) * 4, cudaMemcpyDeviceToHost, st));
+  FOLD_CUDA_TRY(cudaStreamSynchronize(st));
+  for (int e = 0; e < MOE_NCLASS; e++) {
+    if (hbuf[F_ERR0 + e] != INT_MAX) {
+      g_last_detail = hbuf[F_ERR0 + e];
+      g_last_ctx[0] = g_last_detail;
+      if (e != MOE_ROOT && g_last_detail >= 0 && g_last_detail < N) {
+        int32_t v = -1;
+        FOLD_CUDA_TRY(cudaMemcpyAsync(&v, gr->op + g_last_detail, 4, cudaMemcpyDeviceToHost, st));
+        FOLD_CUDA_TRY(cudaStreamSynchronize(st));
+        g_last_ctx[2] = v;
+      }
+      return kMoErrStatus[e];
+    }
+  }
+  const int D = hbuf[F_MAXDEPTH];
+  const int ng = (D + 1) * K + 1;
+  if (ng <= npre) {
+    memcpy(s->group_off_host, hbuf + F_NFLAGS, (size_t)ng * 4);
+  } else {
+    FOLD_CUDA_TRY(cudaMemcpyAsync(s->group_off_host, s->group_off, (size_t)ng * 4, cudaMemcpyDeviceToHost, st));
+    FOLD_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  s->n_levels = D;
+  s->n_leaf_segs = hbuf[F_NSEG];
   return FOLD_OK;
 }
 

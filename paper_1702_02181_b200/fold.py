@@ -24,7 +24,7 @@ from . import build as _build
 OK = 0
 STATUS = {0: "OK", 1: "INVALID", 2: "CHILD_RANGE", 3: "ARITY", 4: "TOKEN_RANGE", 5: "ROOT_RANGE",
           6: "CYCLE", 7: "WORKSPACE", 8: "CUDA", 9: "MISMATCH", 10: "OP_RANGE", 11: "UNSUPPORTED",
-          12: "LEVEL"}
+          12: "LEVEL", 13: "TYPE"}
 CELLS = {"treernn": 0, "treelstm": 1}
 PRECS = {"fp32": 0, "tf32": 1, "bf16": 2}
 
