@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["fold", "reference"], default="fold")
-    ap.add_argument("--model", choices=["r1", "sst"], default="r1",
+    ap.add_argument("--model", choices=["r1", "sst", "mo"], default="r1",
                     help="r1: the headline TreeLSTM (leaf = embedding lookup, root gradient); sst: the §3.5 "
                          "sentiment model (NEXT-2)")
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
@@ -897,12 +897,165 @@ def run_sst(args):
     print(json.dumps(out), flush=True)
 
 
+# ============================================================================ multi-op levels (NEXT-3)
+
+def run_mo(args):
+    """--model mo: multi-op dynamic batching (fold_mo.h) on the C6 workload
+    (foldgen.mo_batch_c6: parse-shaped trees with binary TreeLSTM, unary TreeLSTM chains and a
+    typed projection RNN at the root; S0 = 300, S1 = 128, V = 16384 Zipf). Training step =
+    fold_mo_schedule + fold_mo_forward + fold_mo_backward + SGD over all parameters; FP32
+    (3xTF32) or TF32 tensor-core GEMMs. One GPU (rank 0 prints)."""
+    import torch
+    from paper_1702_02181_b200 import fold, fold_mo
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    fold.device_check()
+    prec = args.prec if args.prec != "bf16" else "fp32"
+    B = args.batch or 1024
+    gr = foldgen.mo_batch_c6(B)
+    T = gr.table
+    params = foldgen.make_mo_params(T)
+    arrs = [x for blk in params for x in blk]
+    sizes = [a.size for a in arrs]
+    # 16-byte aligned parameter blocks: pad each block's offset to 4 floats
+    offs, o = [], 0
+    for n in sizes:
+        offs.append(o)
+        o += (n + 3) // 4 * 4
+    flat_p = torch.zeros(o, dtype=torch.float32, device=dev)
+    flat_g = torch.zeros_like(flat_p)
+
+    def views(buf):
+        out, k = [], 0
+        for blk in params:
+            v = []
+            for x in blk:
+                v.append(buf[offs[k]:offs[k] + x.size].view(x.shape))
+                k += 1
+            out.append(tuple(v))
+        return out
+    P, Gr = views(flat_p), views(flat_g)
+    for blk, src in zip(P, params):
+        for d, a in zip(blk, src):
+            d.copy_(torch.from_numpy(a))
+    model = fold_mo.MoModel(P, prec)
+    t = lambda x: torch.tensor(np.ascontiguousarray(x, np.int32).reshape(-1), device=dev)
+    dvs = (t(gr.op), t(gr.child), t(gr.token), t(gr.root))
+    g = torch.tensor(foldgen.make_mo_upstream(gr.n_graphs, T), device=dev)
+
+    def step(o):
+        s = fold_mo.schedule(T, *o)
+        h, acts = fold_mo.forward(s, model)
+        fold_mo.backward(s, model, acts, g, grads=Gr)
+        fold.sgd_update(flat_p, flat_g, args.lr)
+        return h
+    for _ in range(max(args.warmup, 3)):
+        step(dvs)
+    torch.cuda.synchronize()
+    import gc
+    gc.collect()
+    gc.disable()
+    clocks = ClockSampler(0) if not args.no_clocks else None
+    if clocks:
+        clocks.start()
+    fold.launch_count(reset=True)
+    fold.profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step(dvs)
+    e1.record()
+    torch.cuda.synchronize()
+    launches = fold.launch_count()
+    prof = fold.profile_read()
+    fold.profile_enable(False)
+    clk = clocks.stop() if clocks else None
+    ms = e0.elapsed_time(e1) / args.steps
+    value = gr.n_nodes / (ms / 1e3)
+    # e2e: graph arrays H2D from pinned memory, the root states D2H, every step
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.int32).reshape(-1)).pin_memory()
+    hs = [pin(a) for a in (gr.op, gr.child, gr.token, gr.root)]
+    ds = [torch.empty_like(h, device=dev) for h in hs]
+    hout = torch.empty((gr.n_graphs, int(T.S.max())), dtype=torch.float32).pin_memory()
+    h2d = sum(h.numel() * 4 for h in hs)
+
+    def e2e_step():
+        for d, h in zip(ds, hs):
+            d.copy_(h, non_blocking=True)
+        hout.copy_(step(tuple(ds)), non_blocking=True)
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    a1.record()
+    torch.cuda.synchronize()
+    e_ms = a0.elapsed_time(a1) / args.steps
+    per_class = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
+                 for k, v in prof.items() if v[1] > 0}
+    # roofline: three GEMM passes (forward Z, backward dA, weight dU) of 2 * nout * kin FLOP per
+    # cell node, on the TF32 peak (3xTF32: a third of it); the schedule is excluded
+    pk, pk_src = peaks()
+    scale = 0.5 if prec == "tf32" else 0.5 / 3
+    full_clock = bool(clk and clk.get("sm_max_mhz") and clk["sm_mhz"] >= 0.95 * clk["sm_max_mhz"])
+    peak = pk["bf16_tflops"] * scale if (full_clock or clk is None) else pk["bf16_tflops_sustained"] * scale
+    cnt = np.bincount(gr.op, minlength=T.n_ops)
+    flops = 0.0
+    for o in range(T.n_ops):
+        if T.kind[o] == foldgen.MO_EMBED:
+            continue
+        So, Si, a = int(T.S[T.out_type[o]]), int(T.S[T.in_type[o]]), int(T.arity[o])
+        nout = (3 + a) * So if T.kind[o] == foldgen.MO_LSTM else So
+        flops += 6.0 * nout * a * Si * cnt[o]
+    exec_ms = sum(per_class.get(k, {}).get("ms_per_step", 0.0) for k in ("cell_fwd", "gemm_dA"))
+    achieved = flops / (exec_ms / 1e3) / 1e12 if exec_ms > 0 else 0.0
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle
+        n1 = int(gr.root[min(16, gr.n_graphs) - 1]) + 1
+        sub = foldgen.MoGraphs(gr.op[:n1], gr.child[:n1], gr.token[:n1], gr.root[:min(16, gr.n_graphs)], T)
+        Pf = oracle.mo_flatten(T, params)
+        t0 = time.perf_counter()
+        oracle.mo_backward(sub, Pf, foldgen.make_mo_upstream(sub.n_graphs, T))
+        dt = time.perf_counter() - t0
+        cpu = {"value": sub.n_nodes / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"first {sub.n_graphs} trees ({sub.n_nodes} nodes), fp64 multi-op forward+backward "
+                         f"(oracle_mo_backward), single thread, {dt:.1f} s"}
+    out = {"metric": "multi-op TreeLSTM tree nodes/sec fwd+bwd (NEXT-3: binary + unary cells, typed projection)",
+           "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+           "config": {"workload": f"C6 multi-op: B={gr.n_graphs} parse-shaped trees + unary LSTM chains "
+                                  f"(p=0.3) + root projection; ops EMBED/LSTM2/LSTM1/RNN1, S0={int(T.S[0])}, "
+                                  f"S1={int(T.S[1])}, V={int(T.vocab[0])} Zipf",
+                      "nodes": gr.n_nodes, "nodes_per_op": cnt.tolist(),
+                      "step": "mo_schedule+mo_fwd+mo_bwd+sgd", "l2": "no flush (working set > L2 at B=1024)"},
+           "gpu_launches": int(launches), "kernels": per_class,
+           "roofline": {"bound": "tensor", "kernel": "k_gemm_tf32_grouped (+ gather / pointwise per level)",
+                        "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                        "frac": achieved / peak if peak else None, "traffic": None,
+                        "peak_source": f"{pk_src} bf16 x {scale:.4f} ({prec}: TF32 = bf16/2 nominal"
+                                       f"{', 3 MMA passes' if prec == 'fp32' else ''})",
+                        "algorithmic": "6 * nout * kin FLOP per cell node (forward Z, dA, dU)"},
+           "cpu_baseline": cpu,
+           "e2e": {"value": gr.n_nodes / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms, "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": int(hout.numel() * 4)},
+           "clocks": clk}
+    print(json.dumps(out), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
     elif args.model == "sst":
         run_sst(args)
+    elif args.model == "mo":
+        run_mo(args)
     else:
         run_fold(args)
 
