@@ -64,6 +64,8 @@ def parse():
                          "(batches of more than 131072 nodes or 64 levels: after its level sweep)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo: testing the multi-rank path on one GPU)")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "sparse", "dense"],
+                    help="N > 1: dE exchange (auto: sparse all-gather of the touched rows when cheaper)")
     ap.add_argument("--no-table1", action="store_true",
                     help="skip the unbatched baseline and the PAPER.md Table 1 reproduction")
     return ap.parse_args()
@@ -166,7 +168,7 @@ def run_fold(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1702_02181_b200 import fold
+    from paper_1702_02181_b200 import dp, fold
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -205,6 +207,17 @@ def run_fold(args):
     ws = fold.Workspace(dev)
     sched_ws = torch.empty(1, dtype=torch.uint8, device=dev)
 
+    # the data-parallel exchange (N > 1): all_reduce of [dU | db]; dE as the all-gathered
+    # touched rows when that moves fewer bytes than its dense all_reduce (dp.exchange_plan,
+    # SURVEY §8(f) NEXT-4), else dense. The mode of the last step is reported.
+    xrows = torch.empty(max(N_nodes, 1), dtype=torch.int32, device=dev)
+    xscratch = {}
+    xmode = ["none"]
+
+    def exchange(sc):
+        rows = fold.touched_rows(sc, out=xrows)
+        xmode[0] = dp.exchange_grads(flat_g, nU + nb, dE, rows, mode=args.exchange, scratch=xscratch)
+
     def step(op, child, token, root, g, level=None, train=True):
         nonlocal sched_ws
         s = fold.schedule(op, child, token, root, V, workspace=sched_ws, level=level)
@@ -213,7 +226,7 @@ def run_fold(args):
             return h
         fold.backward(s, model, acts, g, grads=(dU, db, dE), ws=ws)
         if world > 1:
-            dist.all_reduce(flat_g)
+            exchange(s)
         fold.sgd_update(flat_p, flat_g, args.lr)
         return h
 
@@ -287,7 +300,7 @@ def run_fold(args):
         if train:
             fold.backward(sc, model, acts, g, grads=(dU, db, dE), ws=ws, sweep_done=sweep_done)
             if world > 1 and collective:
-                dist.all_reduce(flat_g)
+                exchange(sc)
             fold.sgd_update(flat_p, flat_g, args.lr)
         sbuf_free[i].record(main)
         sbuf_used[i] = True
@@ -449,7 +462,8 @@ def run_fold(args):
         c5 = {"value": full5.n_nodes / (ms5 / 1e3), "unit": UNIT, "ms_per_step": ms5, "scaling": "strong",
               "trees": full5.n_graphs, "nodes": full5.n_nodes, "nodes_rank0": gr5.n_nodes,
               "shard": "contiguous tree ranges balanced by node count (dp.shard)",
-              "step": "schedule+fwd+bwd+all_reduce([dU|db|dE], %.0f MB)+sgd" % (flat_g.numel() * 4 / 1e6)}
+              "step": "schedule+fwd+bwd+exchange(all_reduce [dU|db] %.0f MB + dE %s)+sgd"
+                      % ((nU + nb) * 4 / 1e6, xmode[0])}
 
     # ---------------- batch-1 (within-tree batching only) for the speedup-vs-batch-size context
     batch1 = None
@@ -508,6 +522,7 @@ def run_fold(args):
                    "l2": "working set > L2 (pool+saved gates+grads ~%.1f GB); no flush" % (
                        (N_nodes * S * 6 + n_cells * gates * S * 4 + n_cells * S * 16) / 1e9),
                    "parallelism": f"dp{world}",
+                   "exchange": (xmode[0] if world > 1 else None),
                    "pipeline": ("next batch's fold_schedule on a side stream during this batch's step" +
                                 ("" if gate[0] is None else ", started after this batch's level sweep"))
                    if pipelined else "off"},

@@ -276,6 +276,23 @@ fold_status fold_sst_backward(const fold_schedule_t *sched, const fold_model *mo
                               const void *d_acts, fold_grads *grads, fold_sst_grads *sst_grads,
                               void *d_workspace, size_t workspace_bytes, void *stream);
 
+/* ----------------------------------------------------------------- sparse dE exchange
+ * (a data-parallel step needs only the embedding rows its
+ * batch touched, so the ranks can all-gather those rows instead of all-reducing the whole
+ * [V][S] table). All device pointers, stream-ordered, no host sync.
+ *   fold_touched_rows    d_rows[0 .. n_tok_segs) = the batch's distinct tokens, ascending (one
+ *                        per token segment of the schedule; n_tok_segs is the host count)
+ *   fold_gather_rows     d_dst[i][0..S) = d_src[d_rows[i]][0..S)   (row stride ld of d_src;
+ *                        d_rows[i] < 0: a zero row, i.e. padding)
+ *   fold_scatter_add_rows d_dst[d_rows[i]][0..S) += d_src[i][0..S) (rows of one call must be
+ *                        distinct; d_rows[i] < 0 skipped). Summing the ranks' packed rows
+ *                        with one call per rank in rank order is deterministic. */
+fold_status fold_touched_rows(const fold_schedule_t *sched, int32_t *d_rows, void *stream);
+fold_status fold_gather_rows(const float *d_src, int64_t ld, const int32_t *d_rows, int32_t n, int32_t S,
+                             float *d_dst, void *stream);
+fold_status fold_scatter_add_rows(const float *d_src, const int32_t *d_rows, int32_t n, int32_t S,
+                                  float *d_dst, int64_t ld, void *stream);
+
 /* param[i] -= lr * grad[i], i < n (device fp32). SPEC S:L511 sgd_step. */
 fold_status fold_sgd_update(float *d_param, const float *d_grad, int64_t n, float lr,
                             void *stream);

@@ -428,6 +428,21 @@ fold_status fold_sgd_update(float *p, const float *g, int64_t n, float lr, void 
   return launch_sgd(p, g, n, lr, (cudaStream_t)stream);
 }
 
+fold_status fold_touched_rows(const fold_schedule_t *s, int32_t *d_rows, void *stream) {
+  if (!s || (s->n_tok_segs > 0 && (!d_rows || !s->tok_seg || !s->leaf_perm || !s->leaf_token))) return FOLD_E_INVALID;
+  return launch_touched_rows(s->n_tok_segs, s->tok_seg, s->leaf_perm, s->leaf_token, d_rows, (cudaStream_t)stream);
+}
+fold_status fold_gather_rows(const float *d_src, int64_t ld, const int32_t *d_rows, int32_t n, int32_t S,
+                             float *d_dst, void *stream) {
+  if (n < 0 || S < 0 || ld < S || (n > 0 && (!d_src || !d_rows || !d_dst))) return FOLD_E_INVALID;
+  return launch_gather_rows(d_src, ld, d_rows, n, S, d_dst, (cudaStream_t)stream);
+}
+fold_status fold_scatter_add_rows(const float *d_src, const int32_t *d_rows, int32_t n, int32_t S, float *d_dst,
+                                  int64_t ld, void *stream) {
+  if (n < 0 || S < 0 || ld < S || (n > 0 && (!d_src || !d_rows || !d_dst))) return FOLD_E_INVALID;
+  return launch_scatter_add_rows(d_src, d_rows, n, S, d_dst, ld, (cudaStream_t)stream);
+}
+
 const char *fold_status_string(fold_status s) {
   switch (s) {
     case FOLD_OK: return "FOLD_OK";

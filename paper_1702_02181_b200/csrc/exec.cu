@@ -731,6 +731,34 @@ __global__ void __launch_bounds__(128) k_embed_pieces_final(int S, int n_tok_seg
   }
 }
 
+// ---- sparse embedding-gradient exchange: the batch's distinct tokens
+// (the rows of dE a step can touch), row packing and rank-ordered scatter-add
+// rows[i] = token of the i-th token segment (ascending tokens: leaf_perm is sorted by token)
+__global__ void k_touched_rows(int n_seg, const int32_t *__restrict__ tok_seg, const int32_t *__restrict__ leaf_perm,
+                               const int32_t *__restrict__ leaf_token, int32_t *__restrict__ rows) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_seg; i += gridDim.x * blockDim.x)
+    rows[i] = leaf_token[leaf_perm[tok_seg[i]]];
+}
+// dst[i][0..S) = src[rows[i]][0..S) (0 for rows[i] < 0: padding)
+__global__ void k_gather_rows(const float *__restrict__ src, int64_t ld, const int32_t *__restrict__ rows, int n,
+                              int S, float *__restrict__ dst) {
+  const int64_t total = (int64_t)n * S, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int r = rows[i / S];
+    dst[i] = r >= 0 ? src[(int64_t)r * ld + i % S] : 0.f;
+  }
+}
+// dst[rows[i]][0..S) += src[i][0..S) (rows of one call distinct: no conflicts, no atomics;
+// skipped for rows[i] < 0)
+__global__ void k_scatter_add_rows(const float *__restrict__ src, const int32_t *__restrict__ rows, int n, int S,
+                                   float *__restrict__ dst, int64_t ld) {
+  const int64_t total = (int64_t)n * S, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int r = rows[i / S];
+    if (r >= 0) dst[(int64_t)r * ld + i % S] += src[i];
+  }
+}
+
 __global__ void k_sgd(float *p, const float *g, int64_t n, float lr, int v4) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x, t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t i0 = 0;
@@ -914,6 +942,28 @@ fold_status launch_embed_bwd_pieces(int S, int n_leaves, int n_tok_segs, const i
                                                      w.partial, dE);
   else k_embed_pieces_final<1><<<g2, 128, 0, st>>>(S, n_tok_segs, tok_seg, w.piece_off, leaf_perm, leaf_token,
                                                   w.partial, dE);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+
+fold_status launch_touched_rows(int n_seg, const int32_t *tok_seg, const int32_t *leaf_perm,
+                                const int32_t *leaf_token, int32_t *rows, cudaStream_t st) {
+  if (n_seg <= 0) return FOLD_OK;
+  k_touched_rows<<<grid_cap(cdiv(n_seg, 256)), 256, 0, st>>>(n_seg, tok_seg, leaf_perm, leaf_token, rows);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+fold_status launch_gather_rows(const float *src, int64_t ld, const int32_t *rows, int n, int S, float *dst,
+                               cudaStream_t st) {
+  if (n <= 0 || S <= 0) return FOLD_OK;
+  k_gather_rows<<<grid_cap(cdiv((int64_t)n * S, 256)), 256, 0, st>>>(src, ld, rows, n, S, dst);
+  FOLD_LAUNCH_CHECK();
+  return FOLD_OK;
+}
+fold_status launch_scatter_add_rows(const float *src, const int32_t *rows, int n, int S, float *dst, int64_t ld,
+                                    cudaStream_t st) {
+  if (n <= 0 || S <= 0) return FOLD_OK;
+  k_scatter_add_rows<<<grid_cap(cdiv((int64_t)n * S, 256)), 256, 0, st>>>(src, rows, n, S, dst, ld);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }

@@ -61,6 +61,12 @@ fold_status launch_embed_bwd(int S, int nl, int n_tok_segs, const int32_t *tok_s
 fold_status launch_root_off(int N, int G, const int32_t *root_row, const int32_t *root_perm, int32_t *root_off,
                             cudaStream_t st);
 fold_status launch_sgd(float *p, const float *g, int64_t n, float lr, cudaStream_t st);
+fold_status launch_touched_rows(int n_seg, const int32_t *tok_seg, const int32_t *leaf_perm,
+                                const int32_t *leaf_token, int32_t *rows, cudaStream_t st);
+fold_status launch_gather_rows(const float *src, int64_t ld, const int32_t *rows, int n, int S, float *dst,
+                               cudaStream_t st);
+fold_status launch_scatter_add_rows(const float *src, const int32_t *rows, int n, int S, float *dst, int64_t ld,
+                                    cudaStream_t st);
 // exclusive int32 scan (sched.cu)
 fold_status scan_exclusive(const int32_t *in, int32_t *out, int64_t n, int32_t *sums, int32_t *total,
                            cudaStream_t st);

@@ -106,6 +106,12 @@ def load() -> ctypes.CDLL:
     L.fold_backward.restype = i32
     L.fold_backward.argtypes = [ctypes.POINTER(_Sched), ctypes.POINTER(_Model), vp, vp, vp,
                                 ctypes.POINTER(_Grads), vp, sz, vp]
+    L.fold_touched_rows.restype = i32
+    L.fold_touched_rows.argtypes = [ctypes.POINTER(_Sched), vp, vp]
+    L.fold_gather_rows.restype = i32
+    L.fold_gather_rows.argtypes = [vp, ctypes.c_int64, vp, i32, i32, vp, vp]
+    L.fold_scatter_add_rows.restype = i32
+    L.fold_scatter_add_rows.argtypes = [vp, vp, i32, i32, vp, ctypes.c_int64, vp]
     L.fold_sgd_update.restype = i32
     L.fold_sgd_update.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_float, vp]
     L.fold_status_string.restype = ctypes.c_char_p
@@ -153,7 +159,7 @@ EXPORTED = ("fold_schedule_workspace", "fold_schedule", "fold_acts_layout", "fol
             "fold_launch_count", "fold_profile_enable", "fold_profile_read", "fold_debug_fwd_trace", "fold_debug_bwd_trace",
             "fold_debug_sched_trace", "fold_debug_gemm_tf32", "fold_debug_gemm_tf32_ws",
             "fold_sst_acts_layout", "fold_sst_forward_workspace", "fold_sst_forward", "fold_sst_backward_workspace",
-            "fold_sst_backward")
+            "fold_sst_backward", "fold_touched_rows", "fold_gather_rows", "fold_scatter_add_rows")
 
 PROF_CLASSES = ("schedule", "embed_fwd", "cell_fwd", "bwd_pointwise", "gemm_dA", "gemm_dU", "embed_bwd",
                 "db_colsum", "sgd", "weight_prep", "root_out")
@@ -502,6 +508,32 @@ def sgd_update(param: torch.Tensor, grad: torch.Tensor, lr: float, stream=None):
     assert param.dtype == torch.float32 and grad.dtype == torch.float32
     _check(load().fold_sgd_update(_ptr(param), _ptr(grad), param.numel(), ctypes.c_float(lr), _stream(stream)),
            "fold_sgd_update")
+
+
+def touched_rows(sched: Schedule, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """fold_touched_rows: int32 device tensor of the batch's distinct tokens (ascending)."""
+    n = sched.n_tok_segs
+    dev = sched.arrays.buffer.device if hasattr(sched.arrays, "buffer") else None
+    if out is None:
+        out = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    _check(load().fold_touched_rows(ctypes.byref(sched.struct()), _ptr(out), _stream(stream)), "fold_touched_rows")
+    return out[:n]
+
+
+def gather_rows(src: torch.Tensor, rows: torch.Tensor, out: torch.Tensor, stream=None):
+    """fold_gather_rows: out[i] = src[rows[i]] (zero rows where rows[i] < 0)."""
+    n, S = int(rows.numel()), int(src.shape[1])
+    _check(load().fold_gather_rows(_ptr(src), src.stride(0), _ptr(rows), n, S, _ptr(out), _stream(stream)),
+           "fold_gather_rows")
+    return out
+
+
+def scatter_add_rows(src: torch.Tensor, rows: torch.Tensor, dst: torch.Tensor, stream=None):
+    """fold_scatter_add_rows: dst[rows[i]] += src[i] (distinct rows; rows[i] < 0 skipped)."""
+    n, S = int(rows.numel()), int(dst.shape[1])
+    _check(load().fold_scatter_add_rows(_ptr(src), _ptr(rows), n, S, _ptr(dst), dst.stride(0), _stream(stream)),
+           "fold_scatter_add_rows")
+    return dst
 
 
 def graphs_to_device(gr, device="cuda", non_blocking=False):

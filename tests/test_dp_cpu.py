@@ -71,3 +71,18 @@ def test_two_rank_gradient_allreduce_equals_full_batch():
     dU, db, dE = oracle.backward("treelstm", gr.op, gr.child, gr.token, gr.root, p.U, p.b, p.E, g)
     ref = np.concatenate([dU.ravel(), db.ravel(), dE.ravel()]).astype(np.float32)
     np.testing.assert_allclose(got, ref, rtol=1e-5, atol=1e-6)
+
+
+def test_exchange_plan():
+    """Sparse dE exchange only when its all-gather moves fewer bytes than the dense ring
+    all-reduce; maxn = the largest per-rank row count (the padding)."""
+    from paper_1702_02181_b200 import dp
+    assert dp.exchange_plan([3000, 5000], 300, 16384, 2) == ("sparse", 5000)
+    # C2-like: every token touched -> dense
+    assert dp.exchange_plan([16384] * 8, 1024, 16384, 8)[0] == "dense"
+    assert dp.exchange_plan([0, 0], 8, 100, 2) == ("sparse", 0)
+    # the crossover: world * maxn * (S + 1) vs 2 (world - 1) / world * V * S
+    S, V, w = 64, 1000, 4
+    lim = 2 * (w - 1) / w * V * S / (w * (S + 1))
+    assert dp.exchange_plan([int(lim) - 1], S, V, w)[0] == "sparse"
+    assert dp.exchange_plan([int(lim) + 1], S, V, w)[0] == "dense"
