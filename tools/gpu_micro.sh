@@ -1,6 +1,6 @@
-mkdir -p gpurun_out
-./tools/micro/hop_latency > gpurun_out/hop_latency.json 2>&1
-F="--no-cpu-baseline --no-e2e --no-table1 --no-batch1 --no-sweep"
-timeout 300 python bench.py --config c4 --batch 1 $F > gpurun_out/bench_c4b1.json 2>&1
-timeout 300 python bench.py --config c3 --batch 1024 --pipeline off $F > gpurun_out/bench_c3_nopipe.json 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "exit $?" >> gpurun_out/pytest_gpu.log
+O=gpurun_out/micro; mkdir -p $O
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1702_02181_b200/csrc tools/micro/l2_ingress.cu -o /tmp/l2_ingress -lcuda 2>/dev/null
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1702_02181_b200/csrc tools/micro/mma_contention.cu -o /tmp/mma_contention -lcuda 2>/dev/null
+timeout 120 /tmp/l2_ingress > $O/l2_ingress.json 2>&1
+timeout 300 /tmp/mma_contention > $O/mma_contention.json 2>&1
+cat $O/*.json
