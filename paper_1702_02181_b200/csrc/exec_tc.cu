@@ -190,6 +190,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
   __shared__ __align__(8) uint64_t epi_done, stg_free;
   __shared__ int2 credit_list[2][8][32];  // per tile parity, per epilogue warp: (tile, credit)
   __shared__ int credit_n[2][8];          // entries, or -1: overflow (the store warp walks the rows)
+  // per epilogue warp: the bias of its column chunks of the current tile (GATES x 8 floats per
+  // chunk, fetched before the accumulator wait so the loads hide behind the tile's MMAs)
+  __shared__ __align__(16) float bias_sm[Cfg::EPI_WARPS][GATES * Cfg::WMAX / 2];
   __shared__ uint32_t tmem_base_sh;
   const int S = L.S;
   const uint32_t rank = ptx::cluster_ctarank();
@@ -519,6 +522,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
       // (the bulk stores never write past the level's last row: a later level's tile may
       // already own those rows)
       const bool staged = j0 + W <= S && c_tile + BM <= cur.r1 - nl;
+      float *bw = bias_sm[warp - 4];
+      {
+        const int nchw = (chunks - grp + 1) / 2;  // this warp's chunks jc = grp, grp + 2, ...
+        for (int i = lane; i < nchw * GATES * 8; i += 32) {
+          const int cl = i / (GATES * 8), rem = i - cl * (GATES * 8), g = rem >> 3, u = rem & 7;
+          const int jj = j0 + (grp + 2 * cl) * 8 + u;
+          bw[i] = jj < S ? __ldg(bsrc + g * S + jj) : 0.f;
+        }
+        __syncwarp();
+      }
       ptx::mbar_wait(&tfull[acc], aph);
       ptx::tc_fence_after();
       if (warp == 4 && lane == 0 && rank == 0) trace(dbg, 3, T);
@@ -541,11 +554,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         // full 8-column chunk: H / C / A rows (stride ld) and G gate blocks (stride ld) are
         // 16-byte aligned for any S; the bias gate blocks (stride S) only when S % 4 == 0
         const bool fullc = jb + 8 <= S;
-        const bool bias_vec = fullc && (S & 3) == 0;
         float hh[8];
         if constexpr (GATES == 1) {
 #pragma unroll
-          for (int u = 0; u < 8; u++) hh[u] = tanh_fast(z[0][u] + (jb + u < S ? bsrc[jb + u] : 0.f));
+          for (int u = 0; u < 8; u++) hh[u] = tanh_fast(z[0][u] + bw[((jc - grp) >> 1) * 8 + u]);
           if (staged) {
             uint4 pk = make_uint4(pack_bf16x2(hh[0], hh[1]), pack_bf16x2(hh[2], hh[3]), pack_bf16x2(hh[4], hh[5]),
                                   pack_bf16x2(hh[6], hh[7]));
@@ -566,17 +578,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
           }
         } else {
           float gs[5][8], cc[8];
+          const float *bc = bw + ((jc - grp) >> 1) * (GATES * 8);
 #pragma unroll
           for (int g = 0; g < 5; g++) {
             float bz[8];
-            if (bias_vec) {
-              float4 x = __ldg(reinterpret_cast<const float4 *>(bsrc + g * S + jb));
-              float4 y = __ldg(reinterpret_cast<const float4 *>(bsrc + g * S + jb + 4));
-              bz[0] = x.x; bz[1] = x.y; bz[2] = x.z; bz[3] = x.w; bz[4] = y.x; bz[5] = y.y; bz[6] = y.z; bz[7] = y.w;
-            } else {
-#pragma unroll
-              for (int u = 0; u < 8; u++) bz[u] = jb + u < S ? bsrc[g * S + jb + u] : 0.f;
-            }
+            const float4 x = *reinterpret_cast<const float4 *>(bc + g * 8);
+            const float4 y = *reinterpret_cast<const float4 *>(bc + g * 8 + 4);
+            bz[0] = x.x; bz[1] = x.y; bz[2] = x.z; bz[3] = x.w; bz[4] = y.x; bz[5] = y.y; bz[6] = y.z; bz[7] = y.w;
 #pragma unroll
             for (int u = 0; u < 8; u++) gs[g][u] = g == 4 ? tanh_fast(z[g][u] + bz[u]) : sigmoid_fast(z[g][u] + bz[u]);
           }
