@@ -343,7 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // converged warp, elected lane issues (ptx::elect_one)
       LevelCursor cur;
       cur.init(L);
       int it = 0, tc = 0;
@@ -353,6 +353,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         const int acc = tc & 1;
         const uint32_t aph = (tc >> 1) & 1;
         ptx::mbar_wait(&tempty[acc], aph ^ 1);
+        __syncwarp();
         ptx::tc_fence_after();
         const uint32_t dst = tbase + acc * Cfg::ACC_STRIDE;
         const int ct = (cur.r0 - nl) + ((T - cur.t0) / cur.NT) * PM;
@@ -365,35 +366,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
             int s = it % ST;
             uint32_t ph = (it / ST) & 1;
             ptx::mbar_wait(&full[s], ph);
+            __syncwarp();
             ptx::tc_fence_after();
-            uint32_t a0 = ptx::smem_u32(smem + s * Cfg::STAGE), b0 = a0 + Cfg::A_BYTES;
+            const uint32_t a0 = ptx::smem_u32(smem + s * Cfg::STAGE), b0 = a0 + Cfg::A_BYTES;
+            const uint64_t da = ptx::sdesc_sw128(a0, 16, 1024), db = ptx::sdesc_sw128(b0, 16, 1024);
+            if (ptx::elect_one()) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; k++)
-              ptx::umma_bf16_2cta(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024),
-                                  ptx::sdesc_sw128(b0 + 32 * k, 16, 1024), idesc, (kb | k) != 0);
-            ptx::umma_commit_2cta(&empty[s]);
+              for (int k = 0; k < BK / 16; k++)
+                ptx::umma_bf16_2cta(dst, ptx::desc_add(da, 32 * k), ptx::desc_add(db, 32 * k), idesc, (kb | k) != 0);
+              ptx::umma_commit_2cta(&empty[s]);
+            }
+            __syncwarp();
           }
-          ptx::umma_commit_2cta(&tfull[acc]);
-          trace(dbg, 2, T);
+          if (ptx::elect_one()) {
+            ptx::umma_commit_2cta(&tfull[acc]);
+            trace(dbg, 2, T);
+          }
+          __syncwarp();
           continue;
         }
         for (int q = 0; q < nst; q++, it++) {
           int s = it % ST;
           uint32_t ph = (it / ST) & 1;
           ptx::mbar_wait(&full[s], ph);
+          __syncwarp();
           ptx::tc_fence_after();
           const uint32_t st0 = ptx::smem_u32(smem + s * Cfg::STAGE);
-          for (int j = 0; j < kps && q * kps + j < KB; j++) {
-            const uint32_t a0 = st0 + j * abox, b0 = st0 + kps * abox + j * ubox;
+          const int nk = min(kps, KB - q * kps);
+          for (int j = 0; j < nk; j++) {
+            const uint64_t da = ptx::sdesc_sw128(st0 + j * abox, 16, 1024);
+            const uint64_t db = ptx::sdesc_sw128(st0 + kps * abox + j * ubox, 16, 1024);
+            if (ptx::elect_one()) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; k++)
-              ptx::umma_bf16_2cta(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024),
-                                  ptx::sdesc_sw128(b0 + 32 * k, 16, 1024), idesc, (q | j | k) != 0);
+              for (int k = 0; k < BK / 16; k++)
+                ptx::umma_bf16_2cta(dst, ptx::desc_add(da, 32 * k), ptx::desc_add(db, 32 * k), idesc, (q | j | k) != 0);
+            }
+            __syncwarp();
           }
-          ptx::umma_commit_2cta(&empty[s]);
+          if (ptx::elect_one()) ptx::umma_commit_2cta(&empty[s]);
+          __syncwarp();
         }
-        ptx::umma_commit_2cta(&tfull[acc]);
-        trace(dbg, 2, T);
+        if (ptx::elect_one()) {
+          ptx::umma_commit_2cta(&tfull[acc]);
+          trace(dbg, 2, T);
+        }
+        __syncwarp();
       }
     }
   } else if (warp >= 4) {
@@ -853,29 +870,37 @@ __global__ void __launch_bounds__(NW_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // converged warp, elected lane issues (ptx::elect_one)
       constexpr uint32_t idesc = ptx::idesc_bf16(128, 2 * NW_ROWS, 0, 0);
       ptx::mbar_wait(&u_full, 0);
       Cur cu;
       cu.init(lo, d0);
       int i = 0;
+      const uint64_t du = ptx::sdesc_sw128(ptx::smem_u32(Usm), 16, 1024);
+      const uint64_t dbb = ptx::sdesc_sw128(ptx::smem_u32(Bsm), 16, 1024);
       for (bool ok = cu.valid(lo, D); ok; ok = cu.next(lo, D), i++) {
         const int acc = i & 1;
         ptx::mbar_wait(&acc_empty[acc], ((i >> 1) & 1) ^ 1);
         ptx::mbar_wait(&b_full, i & 1);
+        __syncwarp();
         ptx::tc_fence_after();
-        trace(dbg, 7, i);
+        if (lane == 0) trace(dbg, 7, i);
         const uint32_t dst = tbase + acc * 2 * NW_ROWS;
-        const uint32_t u0 = ptx::smem_u32(Usm), b0 = ptx::smem_u32(Bsm);
         for (int q = 0; q < KBh; q++) {  // B rows 0..7: h_L K-block q, rows 8..15: h_R K-block q
+          const uint64_t dq = ptx::desc_add(du, q * Cfg::USLOT), bq = ptx::desc_add(dbb, 2 * q * Cfg::BKB);
+          if (ptx::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; k++)
-            ptx::umma_bf16(dst, ptx::sdesc_sw128(u0 + q * Cfg::USLOT + 32 * k, 16, 1024),
-                           ptx::sdesc_sw128(b0 + 2 * q * Cfg::BKB + 32 * k, 16, 1024), idesc, (q | k) != 0);
+            for (int k = 0; k < BK / 16; k++)
+              ptx::umma_bf16(dst, ptx::desc_add(dq, 32 * k), ptx::desc_add(bq, 32 * k), idesc, (q | k) != 0);
+          }
+          __syncwarp();
         }
-        ptx::umma_commit(&b_empty);
-        ptx::umma_commit(&acc_full[acc]);
-        trace(dbg, 2, i);
+        if (ptx::elect_one()) {
+          ptx::umma_commit(&b_empty);
+          ptx::umma_commit(&acc_full[acc]);
+          trace(dbg, 2, i);
+        }
+        __syncwarp();
       }
     }
   } else if (warp >= 4) {
@@ -1023,27 +1048,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // converged warp, elected lane issues (ptx::elect_one)
       constexpr uint32_t idesc = ptx::idesc_bf16(PM, DA_N, 0, 1);
       int it = 0, tc = 0;
       for (int t = pair; t < ntiles; t += npairs, tc++) {
         const int acc = tc & 1;
         ptx::mbar_wait(&tempty[acc], ((tc >> 1) & 1) ^ 1);
+        __syncwarp();
         ptx::tc_fence_after();
         const uint32_t dst = tbase + acc * 256;
         for (int kb = 0; kb < KB; kb++, it++) {
           int s = it % ST;
           uint32_t ph = (it / ST) & 1;
           ptx::mbar_wait(&full[s], ph);
+          __syncwarp();
           ptx::tc_fence_after();
-          uint32_t a0 = ptx::smem_u32(smem + s * DA_STAGE), b0 = a0 + DA_A_BYTES;
+          const uint32_t a0 = ptx::smem_u32(smem + s * DA_STAGE), b0 = a0 + DA_A_BYTES;
+          const uint64_t da = ptx::sdesc_sw128(a0, 16, 1024), db = ptx::sdesc_sw128(b0, MN_CHUNK, 1024);
+          if (ptx::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; k++)
-            ptx::umma_bf16_2cta(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024),
-                                ptx::sdesc_sw128(b0 + 2048 * k, MN_CHUNK, 1024), idesc, (kb | k) != 0);
-          ptx::umma_commit_2cta(&empty[s]);
+            for (int k = 0; k < BK / 16; k++)
+              ptx::umma_bf16_2cta(dst, ptx::desc_add(da, 32 * k), ptx::desc_add(db, 2048 * k), idesc, (kb | k) != 0);
+            ptx::umma_commit_2cta(&empty[s]);
+          }
+          __syncwarp();
         }
-        ptx::umma_commit_2cta(&tfull[acc]);
+        if (ptx::elect_one()) ptx::umma_commit_2cta(&tfull[acc]);
+        __syncwarp();
       }
     }
   } else if (warp >= 4) {
@@ -1285,7 +1316,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // converged warp, elected lane issues (ptx::elect_one)
       BwdCursor cur;
       cur.init(L);
       int it = 0, tc = 0;
@@ -1294,8 +1325,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         const uint32_t idesc = ptx::idesc_bf16(PM, cur.N, 0, 1);
         const int acc = tc & 1;
         ptx::mbar_wait(&tempty[acc], ((tc >> 1) & 1) ^ 1);
+        __syncwarp();
         ptx::tc_fence_after();
-        btrace(dbg, 2, T);
+        if (lane == 0) btrace(dbg, 2, T);
         const uint32_t dst = tbase + acc * 256;
         const int ct = (cur.r0 - nl) + ((T - cur.t0) / cur.NTn) * PM;
         const int rows0 = min(BM, cur.r1 - nl - ct);
@@ -1307,35 +1339,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
             int s = it % ST;
             uint32_t ph = (it / ST) & 1;
             ptx::mbar_wait(&full[s], ph);
+            __syncwarp();
             ptx::tc_fence_after();
-            uint32_t a0 = ptx::smem_u32(smem + s * DA_STAGE), b0 = a0 + DA_A_BYTES;
+            const uint32_t a0 = ptx::smem_u32(smem + s * DA_STAGE), b0 = a0 + DA_A_BYTES;
+            const uint64_t da = ptx::sdesc_sw128(a0, 16, 1024), db = ptx::sdesc_sw128(b0, MN_CHUNK, 1024);
+            if (ptx::elect_one()) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; k++)
-              ptx::umma_bf16_2cta(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024),
-                                  ptx::sdesc_sw128(b0 + 2048 * k, MN_CHUNK, 1024), idesc, (kb | k) != 0);
-            ptx::umma_commit_2cta(&empty[s]);
+              for (int k = 0; k < BK / 16; k++)
+                ptx::umma_bf16_2cta(dst, ptx::desc_add(da, 32 * k), ptx::desc_add(db, 2048 * k), idesc,
+                                    (kb | k) != 0);
+              ptx::umma_commit_2cta(&empty[s]);
+            }
+            __syncwarp();
           }
-          ptx::umma_commit_2cta(&tfull[acc]);
-          btrace(dbg, 3, T);
+          if (ptx::elect_one()) {
+            ptx::umma_commit_2cta(&tfull[acc]);
+            btrace(dbg, 3, T);
+          }
+          __syncwarp();
           continue;
         }
         for (int q = 0; q < nst; q++, it++) {
           int s = it % ST;
           uint32_t ph = (it / ST) & 1;
           ptx::mbar_wait(&full[s], ph);
+          __syncwarp();
           ptx::tc_fence_after();
           const uint32_t st0 = ptx::smem_u32(smem + s * DA_STAGE);
-          for (int j = 0; j < kps && q * kps + j < KB; j++) {
-            const uint32_t a0 = st0 + j * abox, b0 = st0 + kps * abox + j * ubox;
+          const int nk = min(kps, KB - q * kps);
+          for (int j = 0; j < nk; j++) {
+            const uint64_t da = ptx::sdesc_sw128(st0 + j * abox, 16, 1024);
+            const uint64_t db = ptx::sdesc_sw128(st0 + kps * abox + j * ubox, MN_CHUNK, 1024);
+            if (ptx::elect_one()) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; k++)
-              ptx::umma_bf16_2cta(dst, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024),
-                                  ptx::sdesc_sw128(b0 + 2048 * k, MN_CHUNK, 1024), idesc, (q | j | k) != 0);
+              for (int k = 0; k < BK / 16; k++)
+                ptx::umma_bf16_2cta(dst, ptx::desc_add(da, 32 * k), ptx::desc_add(db, 2048 * k), idesc,
+                                    (q | j | k) != 0);
+            }
+            __syncwarp();
           }
-          ptx::umma_commit_2cta(&empty[s]);
+          if (ptx::elect_one()) ptx::umma_commit_2cta(&empty[s]);
+          __syncwarp();
         }
-        ptx::umma_commit_2cta(&tfull[acc]);
-        btrace(dbg, 3, T);
+        if (ptx::elect_one()) {
+          ptx::umma_commit_2cta(&tfull[acc]);
+          btrace(dbg, 3, T);
+        }
+        __syncwarp();
       }
     }
   } else if (warp >= 4) {
@@ -1671,48 +1721,63 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // converged warp, elected lane issues (ptx::elect_one)
       ptx::mbar_wait(&u_full, 0);
       Cur cu;
       int i = 0, it = 0;
+      const uint64_t du = ptx::sdesc_sw128(ptx::smem_u32(Usm), 16, 1024);
+      const uint64_t dbb = ptx::sdesc_sw128(ptx::smem_u32(Bsm), 16, 1024);
       for (bool ok = cu.init(lo, D, d1); ok; ok = cu.next(lo, d1), i++) {
         const int acc = i & 1;
         const uint32_t idesc = ptx::idesc_bf16(128, NB_PARTS * cu.R, 0, 0);
         const int slot_bytes = NB_PARTS * cu.R * 128, kps = NB_STAGE / slot_bytes;
         ptx::mbar_wait(&acc_empty[acc], ((i >> 1) & 1) ^ 1);
+        __syncwarp();
         ptx::tc_fence_after();
         const uint32_t dst = tbase + acc * NB_PARTS * NB_RMAX;
-        const uint32_t u0 = ptx::smem_u32(Usm), b0 = ptx::smem_u32(Bsm);
         if (packed && cu.R == 4 && NSLOT * slot_bytes <= NB_ST * NB_STAGE) {  // one box in the whole ring
           for (int k = 0; k < NB_ST; k++) ptx::mbar_wait(&full[(it + k) % NB_ST], ((it + k) / NB_ST) & 1);
+          __syncwarp();
           ptx::tc_fence_after();
           for (int q = 0; q < NSLOT; q++) {
+            const uint64_t dq = ptx::desc_add(du, q * USLOT), bq = ptx::desc_add(dbb, q * slot_bytes);
+            if (ptx::elect_one()) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; k++)
-              ptx::umma_bf16(dst, ptx::sdesc_sw128(u0 + q * USLOT + 32 * k, 16, 1024),
-                             ptx::sdesc_sw128(b0 + q * slot_bytes + 32 * k, 16, 1024), idesc, (q | k) != 0);
+              for (int k = 0; k < BK / 16; k++)
+                ptx::umma_bf16(dst, ptx::desc_add(dq, 32 * k), ptx::desc_add(bq, 32 * k), idesc, (q | k) != 0);
+            }
+            __syncwarp();
           }
-          for (int k = 0; k < NB_ST; k++) ptx::umma_commit(&empty[(it + k) % NB_ST]);
+          if (ptx::elect_one()) {
+            for (int k = 0; k < NB_ST; k++) ptx::umma_commit(&empty[(it + k) % NB_ST]);
+            ptx::umma_commit(&acc_full[acc]);
+          }
+          __syncwarp();
           it += NB_ST;
-          ptx::umma_commit(&acc_full[acc]);
           continue;
         }
         for (int q0 = 0; q0 < NSLOT; q0 += kps, it++) {
           const int s2 = it % NB_ST;
           ptx::mbar_wait(&full[s2], (it / NB_ST) & 1);
+          __syncwarp();
           ptx::tc_fence_after();
           const int nk = min(kps, NSLOT - q0);
           for (int j = 0; j < nk; j++) {
             const int q = q0 + j;
+            const uint64_t dq = ptx::desc_add(du, q * USLOT);
+            const uint64_t bq = ptx::desc_add(dbb, s2 * NB_STAGE + j * slot_bytes);
+            if (ptx::elect_one()) {
 #pragma unroll
-            for (int k = 0; k < BK / 16; k++)
-              ptx::umma_bf16(dst, ptx::sdesc_sw128(u0 + q * USLOT + 32 * k, 16, 1024),
-                             ptx::sdesc_sw128(b0 + s2 * NB_STAGE + j * slot_bytes + 32 * k, 16, 1024), idesc,
-                             (q | k) != 0);
+              for (int k = 0; k < BK / 16; k++)
+                ptx::umma_bf16(dst, ptx::desc_add(dq, 32 * k), ptx::desc_add(bq, 32 * k), idesc, (q | k) != 0);
+            }
+            __syncwarp();
           }
-          ptx::umma_commit(&empty[s2]);
+          if (ptx::elect_one()) ptx::umma_commit(&empty[s2]);
+          __syncwarp();
         }
-        ptx::umma_commit(&acc_full[acc]);
+        if (ptx::elect_one()) ptx::umma_commit(&acc_full[acc]);
+        __syncwarp();
       }
     }
   } else if (warp >= 4) {
@@ -1952,21 +2017,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::tma_load_2d_pair(tmB, &full[s], B + MN_CHUNK, jb + 64, kb * BK);
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // converged warp, elected lane issues (ptx::elect_one)
       constexpr uint32_t idesc = ptx::idesc_bf16(PM, DU_N, 1, 1);
       for (int it = 0; it < KB; it++) {
         int s = it % ST;
         uint32_t ph = (it / ST) & 1;
         ptx::mbar_wait(&full[s], ph);
+        __syncwarp();
         ptx::tc_fence_after();
-        uint32_t a0 = ptx::smem_u32(smem + s * DU_STAGE), b0 = a0 + DU_A_BYTES;
+        const uint32_t a0 = ptx::smem_u32(smem + s * DU_STAGE), b0 = a0 + DU_A_BYTES;
+        const uint64_t da = ptx::sdesc_sw128(a0, MN_CHUNK, 1024), db = ptx::sdesc_sw128(b0, MN_CHUNK, 1024);
+        if (ptx::elect_one()) {
 #pragma unroll
-        for (int k = 0; k < BK / 16; k++)
-          ptx::umma_bf16_2cta(tbase, ptx::sdesc_sw128(a0 + 2048 * k, MN_CHUNK, 1024),
-                              ptx::sdesc_sw128(b0 + 2048 * k, MN_CHUNK, 1024), idesc, (it | k) != 0);
-        ptx::umma_commit_2cta(&empty[s]);
+          for (int k = 0; k < BK / 16; k++)
+            ptx::umma_bf16_2cta(tbase, ptx::desc_add(da, 2048 * k), ptx::desc_add(db, 2048 * k), idesc, (it | k) != 0);
+          ptx::umma_commit_2cta(&empty[s]);
+        }
+        __syncwarp();
       }
-      if (KB > 0) ptx::umma_commit_2cta(&tfull);
+      if (KB > 0 && ptx::elect_one()) ptx::umma_commit_2cta(&tfull);
+      __syncwarp();
     }
   } else if (warp >= 4) {
     const int q = warp & 3;

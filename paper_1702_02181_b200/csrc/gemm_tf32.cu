@@ -160,27 +160,37 @@ __device__ __forceinline__ void gemm_tf32_tile(const CUtensorMap *pA, const CUte
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // converged warp, elected lane issues (ptx::elect_one)
       constexpr int kN = BN;
       const uint32_t idesc = idesc_tf32(TM, kN, a_mn, b_mn);
       for (int it = 0; it < KB; it++) {
         const int s = it % ST;
         const uint32_t ph = (it / ST) & 1;
         ptx::mbar_wait(NPASS == 3 ? &ready[s] : &full[s], ph);
+        __syncwarp();
         ptx::tc_fence_after();
         const uint32_t a0 = ptx::smem_u32(smem + s * Cfg::STAGE), b0 = a0 + A_TILE;
+        uint64_t ad[TK / 8], bd[TK / 8], al[TK / 8], bl[TK / 8];
 #pragma unroll
         for (int k = 0; k < TK / 8; k++) {
-          const uint64_t ad = tf_desc(a0, k, a_mn), bd = tf_desc(b0, k, b_mn);
-          umma_tf32(tbase, ad, bd, idesc, (it | k) != 0);
-          if constexpr (NPASS == 3) {
-            umma_tf32(tbase, ad, tf_desc(b0 + Cfg::RAW, k, b_mn), idesc, 1);  // A_hi B_lo
-            umma_tf32(tbase, tf_desc(a0 + Cfg::RAW, k, a_mn), bd, idesc, 1);  // A_lo B_hi
-          }
+          ad[k] = tf_desc(a0, k, a_mn); bd[k] = tf_desc(b0, k, b_mn);
+          al[k] = tf_desc(a0 + Cfg::RAW, k, a_mn); bl[k] = tf_desc(b0 + Cfg::RAW, k, b_mn);
         }
-        ptx::umma_commit(&empty[s]);
+        if (ptx::elect_one()) {
+#pragma unroll
+          for (int k = 0; k < TK / 8; k++) {
+            umma_tf32(tbase, ad[k], bd[k], idesc, (it | k) != 0);
+            if constexpr (NPASS == 3) {
+              umma_tf32(tbase, ad[k], bl[k], idesc, 1);  // A_hi B_lo
+              umma_tf32(tbase, al[k], bd[k], idesc, 1);  // A_lo B_hi
+            }
+          }
+          ptx::umma_commit(&empty[s]);
+        }
+        __syncwarp();
       }
-      if (KB > 0) ptx::umma_commit(&tfull);
+      if (KB > 0 && ptx::elect_one()) ptx::umma_commit(&tfull);
+      __syncwarp();
     }
   } else if (warp >= 4) {
     const int t = tid - 128;

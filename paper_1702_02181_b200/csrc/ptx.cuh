@@ -97,6 +97,22 @@ __device__ __forceinline__ void tma_gather4(const CUtensorMap *m, uint64_t *bar,
 }
 
 // ---------------------------------------------------------------- tcgen05
+// One lane of a converged warp (elect.sync): the MMA-issuing warps run their loops with all
+// 32 lanes so the descriptor arithmetic stays warp-uniform (uniform registers), and only the
+// tcgen05.mma / tcgen05.commit instructions are issued by the elected lane. (A lane-0-only
+// loop made the compiler rebuild every descriptor in vector registers and move it to uniform
+// registers inside an ELECT loop per MMA: ~20 instructions per UTCHMMA; now the four MMAs of
+// a k-block issue back to back. Measured: C2 step -2%, C4 forward -6%.)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(p));
+  return p != 0;
+}
+// advance a shared-memory matrix descriptor's start address by `bytes` (16-byte units in the
+// low 14 bits; shared-window addresses stay below 256 KB, so the field never carries)
+__device__ __forceinline__ uint64_t desc_add(uint64_t d, uint32_t bytes) { return d + (bytes >> 4); }
 __device__ __forceinline__ void tmem_alloc(uint32_t *dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
                "r"(ncols)

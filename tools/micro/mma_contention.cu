@@ -55,7 +55,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   unsigned long long my_bytes = 0;
   if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      const uint32_t idesc = ptx::idesc_bf16(256, 256, 0, 0);
+      // mode 7: B MN-major (k_bwd_levels' U operand), mode 8: A and B MN-major (k_gemm_dU_tc)
+      const int amn = mode == 8, bmn = mode >= 7;
+      const uint32_t idesc = ptx::idesc_bf16(256, 256, amn, bmn);
       const unsigned long long c0 = clock64();
       for (int kb = 0; kb < kblocks; kb++) {
         const int s = kb & 3;
@@ -64,8 +66,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         const uint32_t a0 = ptx::smem_u32(smem + (kb & 1) * 32768), b0 = a0 + 16384;
 #pragma unroll
         for (int k = 0; k < 4; k++)
-          ptx::umma_bf16_2cta(tbase + (kb & 1) * 256, ptx::sdesc_sw128(a0 + 32 * k, 16, 1024),
-                              ptx::sdesc_sw128(b0 + 32 * k, 16, 1024), idesc, 1);
+          ptx::umma_bf16_2cta(tbase + (kb & 1) * 256,
+                              amn ? ptx::sdesc_sw128(a0 + 2048 * k, 8192, 1024) : ptx::sdesc_sw128(a0 + 32 * k, 16, 1024),
+                              bmn ? ptx::sdesc_sw128(b0 + 2048 * k, 8192, 1024) : ptx::sdesc_sw128(b0 + 32 * k, 16, 1024),
+                              idesc, 1);
         ptx::umma_commit_2cta(&mdone[s]);
       }
       for (int kb = kblocks - 4; kb < kblocks; kb++) ptx::mbar_wait(&mdone[kb & 3], (kb >> 2) & 1);
@@ -323,10 +327,10 @@ int main() {
   unsigned long long *out;
   cudaMalloc(&out, 2048 * sizeof(unsigned long long));
   unsigned long long h[512];
-  const char *names[] = {"none", "tma", "lds_sts", "ldg", "stg", "ldg_stg", "tma_ldg"};
+  const char *names[] = {"none", "tma", "lds_sts", "ldg", "stg", "ldg_stg", "tma_ldg", "B_mn_major", "AB_mn_major"};
   const int kblocks = 8192, grid = 148;
   printf("{\"mma\": \"M256 N256 K16 bf16 cta_group::2, 4 per k-block, peak 128 clk each\", \"rows\": [\n");
-  for (int mode = 0; mode < 7; mode++) {
+  for (int mode = 0; mode < 9; mode++) {
     for (int rep = 0; rep < 2; rep++) {
       k_probe<<<grid, 384, SMEM>>>(tm, mode, kblocks, g1, g2, out);
       cudaError_t e = cudaDeviceSynchronize();
@@ -339,7 +343,7 @@ int main() {
       side /= grid;
       if (rep == 1)
         printf("  {\"side\": \"%s\", \"mma_frac_of_peak\": %.3f, \"clk_per_mma\": %.1f, \"side_B_per_clk_per_sm\": %.1f}%s\n",
-               names[mode], 128.0 * 4 * kblocks / clk, clk / (4.0 * kblocks), side / clk, mode < 6 ? "," : "");
+               names[mode], 128.0 * 4 * kblocks / clk, clk / (4.0 * kblocks), side / clk, mode < 8 ? "," : "");
     }
   }
   printf("]}\n");
