@@ -1178,7 +1178,11 @@ __host__ __device__ inline int bwd_kps(int N, int bx0) {
 constexpr int BW_ST = FOLD_BW_ST;
 constexpr int BW_EPI = 8;                       // epilogue warps
 constexpr int BW_THREADS = 128 + 32 * BW_EPI;
-constexpr int BW_XS = 32 * 66;                  // floats per warp transpose buffer (32 x 64, padded)
+// floats per warp transpose buffer: 32 rows x 64 columns, unpadded; float2 granules XOR-
+// swizzled by the row (column c of row r at r * 64 + (c ^ 2r)): the row-wise float2 writes and
+// the column-wise float2 reads are both conflict-free per half-warp, and the 2 KB the padding
+// took leaves room for a fifth pipeline stage
+constexpr int BW_XS = 32 * 64;
 constexpr int BW_SMEM = BW_ST * DA_STAGE + BW_EPI * BW_XS * 4 + 1024;
 
 template <int GATES>
@@ -1469,7 +1473,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         }
         ptx::tmem_ld_wait();
 #pragma unroll
-        for (int k = 0; k < 64; k += 2) *reinterpret_cast<float2 *>(xs + lane * 66 + k) = make_float2(v[k], v[k + 1]);
+        for (int k = 0; k < 64; k += 2)
+          *reinterpret_cast<float2 *>(xs + lane * 64 + (k ^ (2 * lane))) = make_float2(v[k], v[k + 1]);
         __syncwarp();
         const int np = n0 + slab * 64;  // padded column of the slab (the slab lies in one half)
         const int half = np >= Sp;
@@ -1492,7 +1497,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
             xls[j] = __shfl_sync(0xffffffffu, half ? my_xl[1] : my_xl[0], i);
             xrs[j] = __shfl_sync(0xffffffffu, half ? my_xr[1] : my_xr[0], i);
             ok[j] = colok && i < 32 && c_row0 + i < c_end;
-            dh[j] = *reinterpret_cast<const float2 *>(xs + (i & 31) * 66 + 2 * lane);
+            dh[j] = *reinterpret_cast<const float2 *>(xs + (i & 31) * 64 + ((2 * lane) ^ (2 * (i & 31))));
             const int64_t e = 2 * (int64_t)(c_row0 + i) + half;
             if (ok[j] && xs_[j] >= nl) {
               const int64_t xc = xs_[j] - nl;
