@@ -185,3 +185,32 @@ def test_c6_bench_size_sampled_roots_and_linearity():
     for b1, b2, b12 in zip(*out):
         for x, y, z in zip(b1, b2, b12):
             assert rel_err((x + y).cpu().numpy(), z.cpu().numpy()) <= 1e-5
+
+
+def test_accumulate_and_degenerate_batches():
+    """fold_mo_grads.accumulate adds a second backward's gradients; a batch of one leaf (depth 1,
+    no cell op present) and a batch whose root is a leaf of the second tensor type run."""
+    import torch
+    from paper_1702_02181_b200 import fold_mo
+    gr = foldgen.mo_batch_c6(12, seed=3, table=foldgen.mo_table_c6(S0=36, S1=20, vocab=50))
+    params = foldgen.make_mo_params(gr.table)
+    g = torch.tensor(foldgen.make_mo_upstream(gr.n_graphs, gr.table), device="cuda")
+    s = fold_mo.schedule(gr.table, *_dev(gr))
+    model = fold_mo.MoModel([tuple(torch.tensor(x, device="cuda") for x in blk) for blk in params], "fp32")
+    h, acts = fold_mo.forward(s, model)
+    one = fold_mo.backward(s, model, acts, g)
+    one = [tuple(x.clone() for x in blk) for blk in one]
+    two = fold_mo.backward(s, model, acts, g, grads=[tuple(x.clone() for x in blk) for blk in one], accumulate=True)
+    for b1, b2 in zip(one, two):
+        for x, y in zip(b1, b2):
+            assert rel_err(y.cpu().numpy(), 2 * x.cpu().numpy()) <= 1e-6
+    # one EMBED leaf of type 1 as the whole batch (only depth 1)
+    T = table7(6, 4)
+    leaf = _graph(T, [1], [[-1, -1]], [3], [0])
+    _check(leaf, "fp32")
+    # a leaf root beside a tree
+    rng = np.random.default_rng(5)
+    gr2 = random_mo_graph(T, rng, 40, 3)
+    gr2 = _graph(T, np.concatenate([gr2.op, [0]]), np.concatenate([gr2.child, [[-1, -1]]]),
+                 np.concatenate([gr2.token, [2]]), np.concatenate([gr2.root, [40]]))
+    _check(gr2, "fp32")
