@@ -549,10 +549,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         }
         __syncwarp();
       }
+      // the children's cell states of the first chunk are loaded while the tile's MMAs run:
+      // once this warp itself has observed the tile's inputs published (acquire), not only
+      // after the accumulator is ready (on latency-bound levels the L2 round trip was on every
+      // level's critical path)
+      {
+        const int ct = (cur.r0 - nl) + (lt / cur.NT) * PM;
+        if (lane == 0) ptx::wait_counter(rt_cnt + ct, min(PM, cur.r1 - nl - ct) * 2 * S);
+        __syncwarp();
+      }
+      load_c(j0 + grp * 8);
       ptx::mbar_wait(&tfull[acc], aph);
       ptx::tc_fence_after();
       if (warp == 4 && lane == 0 && rank == 0) trace(dbg, 3, T);
-      load_c(j0 + grp * 8);
       if (tc > 0) ptx::mbar_wait(&stg_free, (tc - 1) & 1);  // previous tile's staging consumed
       if (warp == 4 && lane == 0 && rank == 0) trace(dbg, 5, T);
       const uint32_t tl = tbase + acc * Cfg::ACC_STRIDE + ((uint32_t)(q * 32) << 16);
