@@ -111,7 +111,20 @@ struct MoView {
   float *A[FOLD_MO_MAX_OPS], *Z[FOLD_MO_MAX_OPS];
   const float *b[FOLD_MO_MAX_OPS], *E[FOLD_MO_MAX_OPS];
   const int32_t *op, *child, *token, *order, *pool_row, *type_off;
+  // push-gather (forward): a node's h goes straight into the A slab rows of its consumers
+  const int32_t *cons_off, *cons_edge, *slab_of_pos;
 };
+
+// h of node n (type t, global pool index gp) at state column j -> the A rows of every
+// consumer edge e = 2 p + k (consumer at order position p, input slot k): the gather of
+// PAPER.md L30 / L47 performed by the producer (as in the BF16 path), so no gather launch
+__device__ __forceinline__ void push_h(const MoView &v, int gp, int S, int j, float h) {
+  for (int e = v.cons_off[gp]; e < v.cons_off[gp + 1]; e++) {
+    const int ed = v.cons_edge[e], pm = ed >> 1, k = ed & 1;
+    const int om = v.op[v.order[pm]];
+    v.A[om][(int64_t)v.slab_of_pos[pm] * v.ldK[om] + k * S + j] = h;
+  }
+}
 
 // find the group of a level-row index (rows of the level's groups concatenated)
 __device__ __forceinline__ int grp_of(const MoLevel &L, int64_t r) {
@@ -133,26 +146,10 @@ __global__ void k_mo_embed(MoView v, MoLevel L) {
     if (col >= S) continue;
     const int n = v.order[L.gstart[g] + (r - L.row0[g])];
     const int64_t row = v.pool_row[n];
-    v.H[t][row * v.ldS[t] + col] = v.E[o][(int64_t)v.token[n] * S + col];
+    const float h = v.E[o][(int64_t)v.token[n] * S + col];
+    v.H[t][row * v.ldS[t] + col] = h;
     v.C[t][row * v.ldS[t] + col] = 0.f;
-  }
-}
-
-// gather (PAPER.md L30 / L47): A_o[slab row] = [H_in[child_1] | .. | H_in[child_a]]
-__global__ void k_mo_gather(MoView v, MoLevel L, int kmax) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t total = L.rows_total * kmax;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-    const int64_t r = i / kmax;
-    const int col = (int)(i % kmax);
-    const int g = grp_of(L, r), o = L.op[g];
-    if (col >= v.kin[o]) continue;
-    const int64_t j = r - L.row0[g];
-    const int n = v.order[L.gstart[g] + j];
-    const int ti = v.in_t[o], Si = v.S[ti];
-    const int k = col / Si, cc = col - k * Si;
-    const int c = v.child[2 * n + k];
-    v.A[o][(L.sstart[g] + j) * v.ldK[o] + col] = v.H[ti][(int64_t)v.pool_row[c] * v.ldS[ti] + cc];
+    push_h(v, v.type_off[t] + (int)row, S, col, h);
   }
 }
 
@@ -178,6 +175,7 @@ __global__ void k_mo_cell_fwd(MoView v, MoLevel L) {
       z[j] = h;
       v.H[t][row * v.ldS[t] + j] = h;
       v.C[t][row * v.ldS[t] + j] = 0.f;
+      push_h(v, v.type_off[t] + (int)row, S, j, h);
       continue;
     }
     const int a = v.arity[o];
@@ -193,7 +191,9 @@ __global__ void k_mo_cell_fwd(MoView v, MoLevel L) {
     }
     z[j] = ig; z[(1 + a) * S + j] = og; z[(2 + a) * S + j] = ug;
     v.C[t][row * v.ldS[t] + j] = cc;
-    v.H[t][row * v.ldS[t] + j] = og * tanhf(cc);
+    const float h = og * tanhf(cc);
+    v.H[t][row * v.ldS[t] + j] = h;
+    push_h(v, v.type_off[t] + (int)row, S, j, h);
   }
 }
 
@@ -353,6 +353,8 @@ struct MoFwdWs {
   float *Up[FOLD_MO_MAX_OPS];
   float *split;
   int64_t split_floats;
+  int32_t *slab_of_pos;
+  int64_t *gsstart;
   size_t bytes;
 };
 inline size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -383,6 +385,10 @@ MoFwdWs fwd_ws(const fold_mo_table *t, const MoDims &m, int npass, void *base) {
   w.split_floats = fwd_split_floats(t, m, npass);
   if (b) w.split = (float *)(b + off);
   off = a256(off + (size_t)w.split_floats * 4);
+  if (b) w.slab_of_pos = (int32_t *)(b + off);
+  off = a256(off + (size_t)(m.N + 1) * 4);
+  if (b) w.gsstart = (int64_t *)(b + off);
+  off = a256(off + (size_t)((m.D + 1) * m.K + 1) * 8);
   w.bytes = off;
   return w;
 }
@@ -493,6 +499,14 @@ fold_status mo_forward(const fold_mo_table *t, const fold_mo_schedule_t *s, cons
                                                                        w.Up[o]);
     FOLD_LAUNCH_CHECK();
   }
+  {  // order position -> slab row, for the push-gather
+    const std::vector<int64_t> ss = slab_starts(s, m.K, m.D);
+    const int ngroups = (m.D + 1) * m.K;
+    FOLD_CUDA_TRY(cudaMemcpyAsync(w.gsstart, ss.data(), (size_t)ngroups * 8, cudaMemcpyHostToDevice, st));
+    k_mo_slab_index<<<blocks_for(m.N), 256, 0, st>>>(m.N, m.K, ngroups, s->group_off, w.gsstart, w.slab_of_pos);
+    FOLD_LAUNCH_CHECK();
+  }
+  v.cons_off = s->cons_off; v.cons_edge = s->cons_edge; v.slab_of_pos = w.slab_of_pos;
   std::vector<int64_t> sacc(m.K, 0);
   for (int d = 1; d <= m.D; d++) {
     MoLevel L = level_groups(t, s, nullptr, d, sacc);
@@ -502,10 +516,7 @@ fold_status mo_forward(const fold_mo_table *t, const fold_mo_schedule_t *s, cons
       FOLD_LAUNCH_CHECK();
       continue;
     }
-    int kmax = 1;
-    for (int g = 0; g < L.n; g++) kmax = std::max(kmax, m.kin[L.op[g]]);
-    k_mo_gather<<<blocks_for(L.rows_total * kmax), 256, 0, st>>>(v, L, kmax);
-    FOLD_LAUNCH_CHECK();
+    // (the level's A slab rows were filled by their producers' push-gather)
     TfProblem q[kMoGroups];
     for (int g = 0; g < L.n; g++) {
       const int o = L.op[g];
