@@ -482,6 +482,8 @@ __global__ void k_colsum_partial(int n_rows, int ncols, const T *__restrict__ X,
     float acc[VEC];
 #pragma unroll
     for (int u = 0; u < VEC; u++) acc[u] = 0.f;
+    // (unrolled: several rows' loads in flight per thread; the sum stays in row order)
+#pragma unroll 8
     for (int64_t r = a; r < b; r++) {
       const T *x = X + r * ldx + j;
       if constexpr (VEC == 8) {

@@ -294,20 +294,30 @@ __global__ void k_mo_slab_index(int N, int K, int ngroups, const int32_t *group_
   }
 }
 
-// dE_o[token] = sum over the (op, token) segment of the leaves' dh, in segment order
-// (fixed order: deterministic); every row of dE_o first zeroed (accumulate = 0)
-__global__ void k_mo_embed_bwd(MoView v, int nseg, const int32_t *leaf_seg, const int32_t *leaf_order, int l0,
-                               const float *dh_leaf, float *const *dE) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)nseg * v.Smax; i += stride) {
-    const int sg = (int)(i / v.Smax), j = (int)(i % v.Smax);
-    const int q0 = leaf_seg[sg], q1 = leaf_seg[sg + 1];
-    const int n0 = v.order[leaf_order[q0]], o = v.op[n0];
-    const int S = v.S[v.out_t[o]];
-    if (j >= S || !dE[o]) continue;
-    float acc = 0.f;
-    for (int q = q0; q < q1; q++) acc += dh_leaf[(int64_t)(leaf_order[q] - l0) * v.Smax + j];
-    dE[o][(int64_t)v.token[n0] * S + j] += acc;
+// dE_o[token] = sum over the (op, token) segment of the leaves' dh (every row of dE_o first
+// zeroed unless accumulating). One block per (segment, 32-column chunk): warp w sums the
+// segment's leaves w, w + 8, w + 16, ... in order (lane = column), then warp 0 adds the eight
+// partials in warp order — a fixed order (deterministic), and a Zipf-heavy token's thousands of
+// leaves no longer run on one thread.
+__global__ void __launch_bounds__(256) k_mo_embed_bwd(MoView v, const int32_t *leaf_seg, const int32_t *leaf_order,
+                                                      int l0, const float *dh_leaf, float *const *dE) {
+  __shared__ float part[8][33];
+  const int sg = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.y * 32 + lane;
+  const int q0 = leaf_seg[sg], q1 = leaf_seg[sg + 1];
+  const int n0 = v.order[leaf_order[q0]], o = v.op[n0];
+  const int S = v.S[v.out_t[o]];
+  if ((int)blockIdx.y * 32 >= S || !dE[o]) return;  // (uniform over the block)
+  float acc = 0.f;
+  if (j < S)
+    for (int q = q0 + warp; q < q1; q += 8) acc += dh_leaf[(int64_t)(leaf_order[q] - l0) * v.Smax + j];
+  part[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && j < S) {
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; w++) tot += part[w][lane];
+    dE[o][(int64_t)v.token[n0] * S + j] += tot;
   }
 }
 
@@ -630,8 +640,8 @@ fold_status mo_backward(const fold_mo_table *t, const fold_mo_schedule_t *s, con
     float *dEh[FOLD_MO_MAX_OPS] = {};
     for (int o = 0; o < m.K; o++) dEh[o] = is_cell(t, o) ? nullptr : gr->dE[o];
     FOLD_CUDA_TRY(cudaMemcpyAsync(w.dE_dev, dEh, sizeof(dEh), cudaMemcpyHostToDevice, st));
-    k_mo_embed_bwd<<<blocks_for((int64_t)s->n_leaf_segs * m.Smax), 256, 0, st>>>(
-        v, s->n_leaf_segs, s->leaf_seg, s->leaf_order, bv.l0, w.dh_leaf, w.dE_dev);
+    k_mo_embed_bwd<<<dim3((unsigned)s->n_leaf_segs, (unsigned)cdiv(m.Smax, 32)), 256, 0, st>>>(
+        v, s->leaf_seg, s->leaf_order, bv.l0, w.dh_leaf, w.dE_dev);
     FOLD_LAUNCH_CHECK();
   }
   return FOLD_OK;
