@@ -1111,7 +1111,14 @@ fold_status run_mo_schedule(const fold_mo_table *t, const fold_mo_graphs *gr, fo
     max_blocks = nsm * (occ < 2 ? occ : 2);
     if (max_blocks > kMaxSchedBlocks) max_blocks = kMaxSchedBlocks;
   }
-  int blocks = N <= kOneBlockN ? 1 : (int)cdiv(N, 2048);
+  // nodes per block (FOLD_MO_SCHED_PER_BLOCK; measured on C6 B=1024, 87k nodes: 2048 -> 0.75 ms,
+  // 512 -> 1.00, 8192 -> 1.21: the depth rounds' grid barriers cost more with more blocks)
+  static const int mo_per_block = [] {
+    const char *e = getenv("FOLD_MO_SCHED_PER_BLOCK");
+    const int v = e ? atoi(e) : 2048;
+    return v < 128 ? 128 : v;
+  }();
+  int blocks = N <= kOneBlockN ? 1 : (int)cdiv(N, mo_per_block);
   if (blocks > max_blocks) blocks = max_blocks;
   MoSchedArgs args{};
   args.N = N; args.G = G; args.K = K; args.T = T;
