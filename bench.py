@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--cell", default=None, choices=["treelstm", "treernn"])
     ap.add_argument("--lr", type=float, default=1e-4)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--prof", default="roofline", choices=["roofline", "all"],
+                    help="kernel classes bracketed by CUDA events inside the timed region: only the "
+                         "roofline's tensor classes (default; the per-class breakdown then comes from "
+                         "a separate profiled pass after it) or all classes")
     ap.add_argument("--no-c5-strong", action="store_true", help="N > 1: skip the C5 strong-scaling record")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-batch1", action="store_true")
@@ -359,7 +363,7 @@ def run_fold(args):
     if clocks:
         clocks.start()
     fold.launch_count(reset=True)
-    fold.profile_enable(True)
+    fold.profile_enable(True, classes=timed_prof_classes(args))
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     # per-step boundaries (median and p10/p90 of the steps)
@@ -381,6 +385,16 @@ def run_fold(args):
     if world > 1:
         dist.barrier()
     clk = clocks.stop() if clocks else None
+    sp_box = [sp]
+
+    def _bd_step():
+        run_step(*sp_box[0], g_dev)
+        sp_box[0] = schedule_async(op, child, token, root, after=gate[0])
+    per_class = breakdown_pass(args, fold, _bd_step, prof)
+    sp = sp_box[0]
+    if sp[1] is not None:
+        torch.cuda.current_stream().wait_event(sp[1])
+    torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -501,8 +515,6 @@ def run_fold(args):
         return
 
     # ---------------- roofline of the dominant kernel class (tensor-bound GEMM kernels)
-    per_class = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
-                 for k, v in prof.items() if v[1] > 0}
     roofline = roofline_record(prof, args.steps, ms_per_step, gates, S, n_cells, clk,
                                cfg_key=f"{args.config}/{gr.n_graphs}/{S}/{args.prec}", prec=args.prec)
 
@@ -529,7 +541,7 @@ def run_fold(args):
         "gpu_launches": int(launches),
         "step_ms": {"median": float(np.median(step_ms)), "p10": float(np.percentile(step_ms, 10)),
                     "p90": float(np.percentile(step_ms, 90)), "rank0": [round(x, 4) for x in step_ms]},
-        "kernels": per_class,
+        "kernels": per_class, "kernels_source": kernels_source(args),
         "us_per_level": {  # the latency-bound view (n_levels - 1 cell levels)
             "fwd": 1e3 * sum(per_class.get(k, {}).get("ms_per_step", 0.0) for k in ("cell_fwd",)) / max(n_levels - 1, 1),
             "bwd": 1e3 * sum(per_class.get(k, {}).get("ms_per_step", 0.0) for k in ("gemm_dA", "bwd_pointwise"))
@@ -562,6 +574,37 @@ def run_fold(args):
 # c_R (3 S fp32), writes dZ (5S bf16) + dA / dCe (4 S fp32) (56 S); dU re-reads the 2S h
 # operand row and the 5S dZ row (14 S)
 ALGO_BYTES_PER_CELL_PER_S = {"k_fwd_levels": 28, "k_bwd_levels": 56, "k_gemm_dU_tc": 14}
+
+
+ROOF_CLASSES = ("cell_fwd", "gemm_dA", "gemm_dU")
+
+
+def timed_prof_classes(args, extra=()):
+    """Classes recorded inside the timed region: each bracket is a pair of event records on
+    the stream, which costs host enqueue time in the many-level configs (SST, C6)."""
+    return None if args.prof == "all" else ROOF_CLASSES + tuple(extra)
+
+
+def kernels_source(args):
+    return ("CUDA events inside the timed region" if args.prof == "all" else
+            f"CUDA events over a profiled pass of {min(args.steps, 5)} steps after the timed region "
+            f"(the timed region brackets only the roofline classes)")
+
+
+def breakdown_pass(args, fold, run, prof):
+    """Per-class kernel times (ms/step, launches/step): from the timed region when every
+    class was recorded there, else from a profiled pass of min(steps, 5) more steps."""
+    import torch
+    n = args.steps
+    if args.prof != "all":
+        n = min(args.steps, 5)
+        fold.profile_enable(True)
+        for _ in range(n):
+            run()
+        torch.cuda.synchronize()
+        prof = fold.profile_read()
+        fold.profile_enable(False)
+    return {k: {"ms_per_step": v[0] / n, "launches_per_step": v[1] / n} for k, v in prof.items() if v[1] > 0}
 
 
 def roofline_record(prof, steps, ms_per_step, gates, S, n_cells, clk, cfg_key=None, prec="bf16"):
@@ -816,12 +859,41 @@ def run_sst(args):
     ws = fold.Workspace(dev)
     n_cells = int((gr.op == 1).sum())
 
-    def step(o):
-        s = fold.schedule(*o, V, workspace=ws.get("sched", int(fold.load().fold_schedule_workspace(
+    # pipelined steps as in the headline bench: the next batch's fold_schedule on a side stream
+    # during this batch's step (K schedules in K timed steps)
+    side = torch.cuda.Stream(device=dev) if args.pipeline != "off" else None
+    pend = [None]
+
+    def sched(o, stream=None):
+        return fold.schedule(*o, V, stream=stream, workspace=ws.get("sched", int(fold.load().fold_schedule_workspace(
             o[0].shape[0], o[3].shape[0]))))
+
+    def step(o, copies=(), o_next=None, copies_next=(), done_prev=None, label=None, label_next=None):
+        main = torch.cuda.current_stream()
+        if pend[0] is None:
+            for d, hsrc in copies:
+                d.copy_(hsrc, non_blocking=True)
+            s = sched(o)
+        else:
+            s, ev = pend[0]
+            main.wait_event(ev)
+            s.arrays.buffer.record_stream(main)
+            pend[0] = None
+        if label is not None:
+            head.label = label
         loss, acts = fold.sst_forward(s, model, head, ws=ws)
         fold.sst_backward(s, model, head, acts, grads=tuple(Gr), ws=ws)
         fold.sgd_update(flat_p, flat_g, args.lr)
+        if side is not None:
+            with torch.cuda.stream(side):
+                if done_prev is not None:
+                    side.wait_event(done_prev)
+                for d, hsrc in copies_next:
+                    d.copy_(hsrc, non_blocking=True)
+                sn = sched(o_next or o, stream=side)
+                ev = torch.cuda.Event()
+                ev.record(side)
+            pend[0] = (sn, ev)
         return loss
     for _ in range(max(args.warmup, 3)):
         step((op, child, token, root))
@@ -833,32 +905,46 @@ def run_sst(args):
     if clocks:
         clocks.start()
     fold.launch_count(reset=True)
-    fold.profile_enable(True)
+    fold.profile_enable(True, classes=timed_prof_classes(args, ("embed_fwd", "embed_bwd")))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0.record()
-    for _ in range(args.steps):
+    marks[0].record()
+    for i_step in range(args.steps):
         step((op, child, token, root))
+        marks[i_step + 1].record()
     e1.record()
     torch.cuda.synchronize()
     launches = fold.launch_count()
     prof = fold.profile_read()
     fold.profile_enable(False)
     clk = clocks.stop() if clocks else None
+    step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
+    per_class = breakdown_pass(args, fold, lambda: step((op, child, token, root)), prof)
+    timed = {k: v[0] / args.steps for k, v in prof.items() if v[1] > 0}
     ms = e0.elapsed_time(e1) / args.steps
     value = gr.n_nodes / (ms / 1e3)
     # e2e: graph arrays + labels H2D from pinned memory, the loss D2H, every step
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
     hs = [pin(a.astype(np.int32)) for a in (gr.op, gr.child, gr.token, gr.root, y)]
-    ds = [torch.empty_like(h, device=dev) for h in hs]
+    # two device buffer sets (the next batch's copies never overwrite arrays a running step reads)
+    dsets = [[torch.empty_like(h, device=dev) for h in hs] for _ in range(2)]
+    dev_done = [None, None]
     hloss = torch.empty(1, dtype=torch.float32).pin_memory()
     h2d = sum(h.numel() * 4 for h in hs)
+    pend[0] = None
+    k_e2e = [0]
 
     def e2e_step():
-        for d, h in zip(ds, hs):
-            d.copy_(h, non_blocking=True)
-        head.label = ds[4]
-        loss = step(tuple(ds[:4]))
+        i = k_e2e[0] % 2
+        cur, nxt = dsets[i], dsets[1 - i]
+        loss = step(tuple(cur[:4]), copies=list(zip(cur, hs)), o_next=tuple(nxt[:4]),
+                    copies_next=list(zip(nxt, hs)), done_prev=dev_done[1 - i], label=cur[4])
         hloss.copy_(loss, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        dev_done[i] = ev
+        k_e2e[0] += 1
     for _ in range(3):
         e2e_step()
     torch.cuda.synchronize()
@@ -869,8 +955,6 @@ def run_sst(args):
     a1.record()
     torch.cuda.synchronize()
     e_ms = a0.elapsed_time(a1) / args.steps
-    per_class = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
-                 for k, v in prof.items() if v[1] > 0}
     # roofline: the three cell GEMM passes + the leaf level's (K = S, N = 5S padded: 10 S^2 per
     # leaf forward, 2 x 10 S^2 backward) on the TF32 peak (3xTF32: a third of it)
     pk, pk_src = peaks()
@@ -879,7 +963,7 @@ def run_sst(args):
     peak = pk["bf16_tflops"] * scale if (full_clock or clk is None) else pk["bf16_tflops_sustained"] * scale
     n_leaves = gr.n_nodes - n_cells
     flops = 3 * 20.0 * S * S * n_cells + 3 * 10.0 * S * S * n_leaves
-    gemm_ms = sum(per_class.get(k, {}).get("ms_per_step", 0.0) for k in ("cell_fwd", "gemm_dA", "gemm_dU",
+    gemm_ms = sum(timed.get(k, 0.0) for k in ("cell_fwd", "gemm_dA", "gemm_dU",
                                                                           "embed_fwd", "embed_bwd"))
     achieved = flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
     cpu = None
@@ -898,8 +982,12 @@ def run_sst(args):
            "config": {"workload": f"{cfg.upper()} tree shapes, B={gr.n_graphs}, S={S}, V={V}, 5 classes, "
                                   f"labels at every node (PAPER.md L297), leaf TreeLSTM(E[w],0,0)",
                       "nodes": gr.n_nodes, "cells": n_cells, "leaves": n_leaves,
-                      "step": "schedule+sst_fwd+sst_bwd+sgd", "l2": "no flush (working set > L2 at B=1024)"},
-           "gpu_launches": int(launches), "kernels": per_class,
+                      "step": "schedule+sst_fwd+sst_bwd+sgd", "l2": "no flush (working set > L2 at B=1024)",
+                      "pipeline": "next batch's fold_schedule on a side stream during this batch's step"
+                      if side is not None else "off"},
+           "gpu_launches": int(launches), "step_ms": {"median": float(np.median(step_ms)), "p10": float(np.percentile(step_ms, 10)),
+                       "p90": float(np.percentile(step_ms, 90)), "all": [round(x, 4) for x in step_ms]},
+           "kernels": per_class, "kernels_source": kernels_source(args),
            "roofline": {"bound": "tensor", "kernel": "k_gemm_tf32 (all GEMM passes)", "achieved": achieved,
                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": None,
                         "peak_source": f"{pk_src} bf16 x {scale:.4f} ({prec}: TF32 = bf16/2 nominal"
@@ -1007,17 +1095,23 @@ def run_mo(args):
     if clocks:
         clocks.start()
     fold.launch_count(reset=True)
-    fold.profile_enable(True)
+    fold.profile_enable(True, classes=timed_prof_classes(args))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0.record()
-    for _ in range(args.steps):
+    marks[0].record()
+    for i_step in range(args.steps):
         step(dvs)
+        marks[i_step + 1].record()
     e1.record()
     torch.cuda.synchronize()
     launches = fold.launch_count()
     prof = fold.profile_read()
     fold.profile_enable(False)
     clk = clocks.stop() if clocks else None
+    step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
+    per_class = breakdown_pass(args, fold, lambda: step(dvs), prof)
+    timed = {k: v[0] / args.steps for k, v in prof.items() if v[1] > 0}
     ms = e0.elapsed_time(e1) / args.steps
     value = gr.n_nodes / (ms / 1e3)
     # e2e: graph arrays H2D from pinned memory, the root states D2H, every step
@@ -1051,8 +1145,6 @@ def run_mo(args):
     a1.record()
     torch.cuda.synchronize()
     e_ms = a0.elapsed_time(a1) / args.steps
-    per_class = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
-                 for k, v in prof.items() if v[1] > 0}
     # roofline: three GEMM passes (forward Z, backward dA, weight dU) of 2 * nout * kin FLOP per
     # cell node, on the TF32 peak (3xTF32: a third of it); the schedule is excluded
     pk, pk_src = peaks()
@@ -1067,7 +1159,7 @@ def run_mo(args):
         So, Si, a = int(T.S[T.out_type[o]]), int(T.S[T.in_type[o]]), int(T.arity[o])
         nout = (3 + a) * So if T.kind[o] == foldgen.MO_LSTM else So
         flops += 6.0 * nout * a * Si * cnt[o]
-    exec_ms = sum(per_class.get(k, {}).get("ms_per_step", 0.0) for k in ("cell_fwd", "gemm_dA"))
+    exec_ms = sum(timed.get(k, 0.0) for k in ("cell_fwd", "gemm_dA"))
     achieved = flops / (exec_ms / 1e3) / 1e12 if exec_ms > 0 else 0.0
     cpu = None
     if not args.no_cpu_baseline:
@@ -1091,7 +1183,9 @@ def run_mo(args):
                       "step": "mo_schedule+mo_fwd+mo_bwd+sgd", "l2": "no flush (working set > L2 at B=1024)",
                       "pipeline": "next batch's fold_mo_schedule on a side stream during this batch's step"
                       if side is not None else "off"},
-           "gpu_launches": int(launches), "kernels": per_class,
+           "gpu_launches": int(launches), "step_ms": {"median": float(np.median(step_ms)), "p10": float(np.percentile(step_ms, 10)),
+                       "p90": float(np.percentile(step_ms, 90)), "all": [round(x, 4) for x in step_ms]},
+           "kernels": per_class, "kernels_source": kernels_source(args),
            "roofline": {"bound": "tensor", "kernel": "k_gemm_tf32_grouped (+ gather / pointwise per level)",
                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                         "frac": achieved / peak if peak else None, "traffic": None,

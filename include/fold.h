@@ -321,11 +321,16 @@ int64_t fold_launch_count(int32_t reset);
  * CUDA events recorded on the launch stream (calling thread only). fold_profile_enable
  * resets the records. fold_profile_read synchronizes on the recorded events and returns,
  * per class, the summed elapsed milliseconds and the number of bracketed launches.
- * Classes: 0 schedule (whole call), 1 embedding forward, 2 cell forward (one per level),
- * 3 backward pointwise, 4 dA GEMM, 5 dU GEMM, 6 embedding backward, 7 db column sum,
+ * Classes: 0 schedule (whole call), 1 embedding forward, 2 cell forward (the level sweep:
+ * one bracket per call), 3 backward pointwise (BF16 tree path: the roots' seeded step),
+ * 4 dA GEMM (the backward level sweep: one bracket per call; on the per-level paths it
+ * includes each level's pointwise step), 5 dU GEMM, 6 embedding backward, 7 db column sum,
  * 8 SGD, 9 weight conversion, 10 root read-out. */
 #define FOLD_PROF_NCLASS 11
 void fold_profile_enable(int32_t on);
+/* As fold_profile_enable(mask != 0), recording only the classes whose bit is set in mask
+ * (bit c = class c): fewer events on the stream when one class is timed inside a long step. */
+void fold_profile_enable_classes(uint32_t mask);
 fold_status fold_profile_read(int32_t n_classes, double *ms, int64_t *launches);
 /* Instrumentation: with FOLD_DBG_FWD=1 in the environment the BF16 forward kernel stamps
  * %globaltimer (ns) per pair tile at nine points: 0 producer starts the tile, 1 its

@@ -253,8 +253,8 @@ fold_status fold_forward(const fold_schedule_t *s, const fold_model *m, void *ac
       FOLD_TRY(tc_fwd_levels(m->cell, fa, st));
     }
   } else if (simt_fp32()) {
+    ProfScope ps(K_CELL_FWD, st);  // one bracket around the level sweep
     for (int d = 2; d <= D; d++) {
-      ProfScope ps(K_CELL_FWD, st);
       FOLD_TRY(launch_cell_fwd_simt(m->cell, lo[d], lo[d + 1], s->gather, S, L.ld, m->U, m->b, (float *)H, C,
                                     (float *)Gact, L.ld_g, nl, st));
     }
@@ -270,10 +270,10 @@ fold_status fold_forward(const fold_schedule_t *s, const fold_model *m, void *ac
     float *Acat = (float *)(a + L.al_off);
     const int64_t lda = tf_ld_a(S);
     const int npass = npass_of(m->prec);
+    ProfScope ps(K_CELL_FWD, st);  // one bracket around the level sweep (fewer events in the step)
     for (int d = 2; d <= D; d++) {
       const int r0 = lo[d], r1 = lo[d + 1], M = r1 - r0, c0 = r0 - nl;
       if (M <= 0) continue;
-      ProfScope ps(K_CELL_FWD, st);
       FOLD_TRY(launch_gather_cat(r0, r1, nl, S, L.ld, s->gather, (const float *)H, Acat, lda, st));
       FOLD_TRY(gemm_tf32(TfOperand{Acat + (int64_t)c0 * lda, lda, 0}, TfOperand{Uf, tf_ld_u(S), 0}, M, gates * L.ld,
                          2 * S, (float *)Gact + (int64_t)c0 * L.ld_g, L.ld_g, 0, npass, nullptr, 0, st));
@@ -353,16 +353,13 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
     }
     ProfScope ps(K_GEMM_DA, st);
     FOLD_TRY(tc_bwd_levels(m->cell, ba, st));
-  } else
+  } else {
+  ProfScope ps(K_GEMM_DA, st);  // the backward level sweep (pointwise + dA GEMM per level), one bracket
   for (int d = D; d >= 2; d--) {
     const int r0 = lo[d], r1 = lo[d + 1], M = r1 - r0, c0 = r0 - nl;
     if (M <= 0) continue;
-    {
-    ProfScope ps(K_BWD_PW, st);
     FOLD_TRY(launch_cell_bwd_pw(bf16, m->cell, r0, r1, nl, S, L.ld, L.ld_g, s->cons_off, s->cons_edge, b.root_off,
                                 s->root_perm, G, dh_root, dc_root, s->gather, Gact, C, b.dA, b.dCe, b.dZ, b.ld_z, st));
-    }
-    ProfScope ps(K_GEMM_DA, st);
     float *dA_lvl = b.dA + (size_t)2 * c0 * S;
     if (bf16)
       FOLD_TRY(tc_gemm_dA(c0, M, nc, S, gates, (const __nv_bfloat16 *)b.dZ, b.ld_z, b.Ub, b.dA, st));
@@ -372,6 +369,7 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
                          npass_of(m->prec), nullptr, 0, st));
     else
       FOLD_TRY(launch_gemm_dA_simt(M, S, gates, (const float *)b.dZ + (size_t)c0 * b.ld_z, b.ld_z, m->U, dA_lvl, st));
+  }
   }
   // The embedding gradient and db only need dA / dZ, the weight-gradient GEMM only dZ and
   // the A planes: run the two memory-bound reductions on an auxiliary stream beside the

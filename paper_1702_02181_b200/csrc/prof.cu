@@ -14,6 +14,7 @@ struct Rec {
   cudaEvent_t a, b;
 };
 thread_local bool g_on = false;
+thread_local uint32_t g_mask = ~0u;  // classes recorded while on
 thread_local std::vector<Rec> g_recs;
 thread_local std::vector<cudaEvent_t> g_pool;
 thread_local std::vector<std::pair<int, cudaEvent_t>> g_open;  // per-class open begin events
@@ -46,7 +47,7 @@ fold_status launch_check(const char *file, int line) {
 }
 
 void prof_mark(int cls, cudaStream_t st, bool begin) {
-  if (!g_on) return;
+  if (!g_on || cls >= 32 || !((g_mask >> cls) & 1u)) return;
   cudaEvent_t e = get_event();
   cudaEventRecord(e, st);
   if (begin) {
@@ -75,6 +76,12 @@ void fold_profile_enable(int32_t on) {
   for (auto &o : g_open) g_pool.push_back(o.second);
   g_open.clear();
   g_on = on != 0;
+  g_mask = ~0u;
+}
+
+void fold_profile_enable_classes(uint32_t mask) {
+  fold_profile_enable(mask != 0);
+  g_mask = mask;
 }
 
 fold_status fold_profile_read(int32_t n_classes, double *ms, int64_t *launches) {

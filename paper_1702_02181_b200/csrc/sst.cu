@@ -319,14 +319,16 @@ fold_status fold_sst_forward(const fold_schedule_t *s, const fold_model *m, cons
     FOLD_TRY(launch_cell_fwd_pw(FOLD_CELL_TREELSTM, 0, nl, nl, S, L.ld, L.ld_g, s->gather, m->b, H, Cm, Gc, st));
   }
   const int64_t lda = ld_a_of(S);
+  {
+  ProfScope ps(K_CELL_FWD, st);  // one bracket around the level sweep (fewer events in the step)
   for (int d = 2; d <= D; d++) {
     const int r0 = lo[d], r1 = lo[d + 1], M = r1 - r0, c0 = r0 - nl;
     if (M <= 0) continue;
-    ProfScope ps(K_CELL_FWD, st);
     FOLD_TRY(launch_gather_cat(r0, r1, nl, S, L.ld, s->gather, H, Acat, lda, st));
     FOLD_TRY(gemm_tf32(TfOperand{Acat + (int64_t)c0 * lda, lda, 0}, TfOperand{w.Uf, tf_ld_u(S), 0}, M, 5 * L.ld,
                        2 * S, Gc + (int64_t)c0 * L.ld_g, L.ld_g, 0, npass, nullptr, 0, st));
     FOLD_TRY(launch_cell_fwd_pw(FOLD_CELL_TREELSTM, r0, r1, nl, S, L.ld, L.ld_g, s->gather, m->b, H, Cm, Gc, st));
+  }
   }
   ProfScope ps(K_ROOT, st);
   float *dlog = (float *)(a + L.dlog), *rowloss = (float *)(a + L.rowloss);
@@ -388,16 +390,15 @@ fold_status fold_sst_backward(const fold_schedule_t *s, const fold_model *m, con
                               w.root_off, s->root_perm, 0, nullptr, nullptr, s->gather, Gc, Cm, w.dA, w.dCe, dZc,
                               w.ld_z, st, nullptr, w.dH, true);
   };
+  {
+  ProfScope ps(K_GEMM_DA, st);  // the backward level sweep (pointwise + dA GEMM per level)
   for (int d = D; d >= 2; d--) {
     const int r0 = lo[d], r1 = lo[d + 1], M = r1 - r0, c0 = r0 - nl;
     if (M <= 0) continue;
-    {
-      ProfScope ps(K_BWD_PW, st);
-      FOLD_TRY(pw(r0, r1));
-    }
-    ProfScope ps(K_GEMM_DA, st);
+    FOLD_TRY(pw(r0, r1));
     FOLD_TRY(gemm_tf32(TfOperand{dZc + (int64_t)c0 * w.ld_z, w.ld_z, 0}, TfOperand{w.Ub, tf_ld_u(S), 1}, M, 2 * S,
                        5 * S, w.dA + (int64_t)2 * c0 * S, 2 * S, 0, npass, nullptr, 0, st));
+  }
   }
   {
     // depth 1: the leaf cells (no children), then their input gradient dX = dz W -> dE

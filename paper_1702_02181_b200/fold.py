@@ -125,6 +125,8 @@ def load() -> ctypes.CDLL:
     L.fold_launch_count.argtypes = [i32]
     L.fold_profile_enable.restype = None
     L.fold_profile_enable.argtypes = [i32]
+    L.fold_profile_enable_classes.restype = None
+    L.fold_profile_enable_classes.argtypes = [ctypes.c_uint32]
     L.fold_profile_read.restype = i32
     L.fold_profile_read.argtypes = [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]
     L.fold_debug_fwd_trace.argtypes = [vp, i32]
@@ -156,7 +158,7 @@ def load() -> ctypes.CDLL:
 EXPORTED = ("fold_schedule_workspace", "fold_schedule", "fold_acts_layout", "fold_forward_workspace",
             "fold_forward", "fold_backward_workspace", "fold_backward", "fold_sgd_update",
             "fold_status_string", "fold_last_error_detail", "fold_last_error_context", "fold_abi_version", "fold_device_check",
-            "fold_launch_count", "fold_profile_enable", "fold_profile_read", "fold_debug_fwd_trace", "fold_debug_bwd_trace",
+            "fold_launch_count", "fold_profile_enable", "fold_profile_enable_classes", "fold_profile_read", "fold_debug_fwd_trace", "fold_debug_bwd_trace",
             "fold_debug_sched_trace", "fold_debug_gemm_tf32", "fold_debug_gemm_tf32_ws",
             "fold_sst_acts_layout", "fold_sst_forward_workspace", "fold_sst_forward", "fold_sst_backward_workspace",
             "fold_sst_backward", "fold_touched_rows", "fold_gather_rows", "fold_scatter_add_rows")
@@ -165,8 +167,12 @@ PROF_CLASSES = ("schedule", "embed_fwd", "cell_fwd", "bwd_pointwise", "gemm_dA",
                 "db_colsum", "sgd", "weight_prep", "root_out")
 
 
-def profile_enable(on: bool = True):
-    load().fold_profile_enable(1 if on else 0)
+def profile_enable(on: bool = True, classes=None):
+    """classes: names from PROF_CLASSES to record (None: all)."""
+    if on and classes is not None:
+        load().fold_profile_enable_classes(sum(1 << PROF_CLASSES.index(c) for c in set(classes)))
+    else:
+        load().fold_profile_enable(1 if on else 0)
 
 
 def profile_read() -> dict:

@@ -212,3 +212,26 @@ def test_very_deep_chain():
     for prec in ("fp32", "bf16"):
         _check_fwd(gr, "treelstm", prec, 32)
         _check_bwd(gr, "treelstm", prec, 32)
+
+
+# ------------------------------------------------------------------ instrumentation
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_profile_classes_bracket_each_sweep_once(prec):
+    """fold_profile_enable brackets each level sweep once per call (cell_fwd, gemm_dA), and
+    fold_profile_enable_classes records only the requested classes."""
+    from paper_1702_02181_b200 import fold
+    gr = foldgen.config_c3(32)
+    S = 64
+    g = foldgen.make_upstream(gr.n_graphs, S)
+    fold.profile_enable(True)
+    _run(gr, "treelstm", prec, S, g=g)
+    allp = fold.profile_read()
+    fold.profile_enable(True, classes=("cell_fwd",))
+    _run(gr, "treelstm", prec, S, g=g)
+    onep = fold.profile_read()
+    fold.profile_enable(False)
+    assert allp["cell_fwd"][1] == 1 and allp["gemm_dA"][1] == 1 and allp["schedule"][1] == 1
+    assert allp["cell_fwd"][0] > 0 and allp["gemm_dA"][0] > 0
+    assert onep["cell_fwd"][1] == 1
+    assert all(n == 0 for k, (_, n) in onep.items() if k != "cell_fwd")
