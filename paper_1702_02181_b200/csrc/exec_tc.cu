@@ -45,13 +45,15 @@ __device__ __forceinline__ void trace(int dbg, int pt, int T) {
     g_fwd_trace[pt][T] = t;
   }
 }
-// FOLD_DBG_BWD=1: the same for k_bwd_levels at six points (see fold_debug_bwd_trace)
-__device__ unsigned long long g_bwd_trace[6][kTraceTiles];
+// FOLD_DBG_BWD=1: the same for k_bwd_levels at nine points (see fold_debug_bwd_trace)
+__device__ unsigned long long g_bwd_trace[9][kTraceTiles];
+__device__ unsigned long long g_bwd_clk[2][kTraceTiles];  // SM clock64 at points 8 and 3
 __device__ __forceinline__ void btrace(int dbg, int pt, int T) {
   if (dbg && T < kTraceTiles) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_bwd_trace[pt][T] = t;
+    if (pt == 8 || pt == 3) g_bwd_clk[pt == 3][T] = clock64();
   }
 }
 
@@ -275,6 +277,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(FwdCfg<GATES>::THREA
         const int nst = (KB + kps - 1) / kps;
         // inputs already published (the common case on wide levels): A and U per stage in
         // order; otherwise the first stages' U boxes go out before the wait
+#ifndef FOLD_FWD_EARLY_U
+        // wait for the inputs before any box of the tile (as in k_bwd_levels; FOLD_FWD_EARLY_U
+        // restores the early U boxes: C4 forward 4.80 -> 5.05 ms)
+        ptx::wait_counter_relaxed(rt_cnt + ct, rows * 2 * S);
+#endif
         const bool ready = ptx::ld_relaxed_gpu(rt_cnt + ct) >= rows * 2 * S;
         if (ready) ptx::fence_proxy_async_global();
         const int pre = ready ? 0 : (nst < ST ? nst : ST);
@@ -1172,9 +1179,10 @@ __host__ __device__ inline int bwd_kps(int N, int bx0) {
   return k < 1 ? 1 : k > 8 ? 8 : k;
 }
 
-// epilogue load flavours (A/B switch at build time): read-once operands of the pointwise
-// step (the child's gates and c, its children's c, dCe)
-#ifdef FOLD_BWD_LDCS
+// epilogue load flavours: the read-once operands of the pointwise step (the child's gates
+// and c, its children's c, dCe) stream with evict-first loads (ld.global.cs) so they do not
+// displace the dZ rows and U the MMAs read from L2 (FOLD_BWD_LDG build switch: plain loads)
+#ifndef FOLD_BWD_LDG
 #define BWD_LDG(p) __ldcs(p)
 #define BWD_LDC(p) __ldcs(p)
 #else
@@ -1183,6 +1191,14 @@ __host__ __device__ inline int bwd_kps(int N, int bx0) {
 #endif
 #ifndef FOLD_BW_ST
 #define FOLD_BW_ST 4
+#endif
+// U (the B operand every tile of every level re-reads): TMA loads with an L2 evict_last
+// policy (FOLD_BWD_U_NOHINT build switch: none). With the evict-first epilogue loads:
+// C4 dA 11.7 -> 11.55 ms, C3 0.577 -> 0.563 ms
+#ifndef FOLD_BWD_U_NOHINT
+#define BWD_TMA_U(m, bar, dst, x, y) ptx::tma_load_2d_pair_hint(m, bar, dst, x, y, pol_u)
+#else
+#define BWD_TMA_U(m, bar, dst, x, y) ptx::tma_load_2d_pair(m, bar, dst, x, y)
 #endif
 constexpr int BW_ST = FOLD_BW_ST;
 constexpr int BW_EPI = 8;                       // epilogue warps
@@ -1232,6 +1248,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
       BwdCursor cur;
       cur.init(L);
       int it = 0;
+#ifndef FOLD_BWD_U_NOHINT
+      const uint64_t pol_u = ptx::createpolicy_evict_last();
+#endif
       // A-operand box rows for a CTA holding m rows (narrow tiles load only their rows)
       auto box_of = [](int m) { return m <= 0 ? 0 : m <= 16 ? 16 : m <= 64 ? 64 : BM; };
       // this CTA's dZ box (map, first row) of tile T (bx = 0: the CTA holds no rows)
@@ -1272,6 +1291,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         const int kps = bwd_kps(N, bx0), abox = bx0 * 128, ubox = (N / 128) * MN_CHUNK;
         const int nst = (KB + kps - 1) / kps;
         if (rank == 0) btrace(dbg, 0, T);
+#ifndef FOLD_BWD_EARLY_U
+        // wait for the tile's inputs before issuing any of its boxes: issuing the first stages'
+        // U boxes before the wait (FOLD_BWD_EARLY_U, the round-1 design) left the tile's whole
+        // mainloop ~25% slower on latency-bound levels (C4 B=1024: 27.1 -> 21.6 us per tile,
+        // per-tile stamps; dA 13.0 -> 11.7 ms)
+        ptx::wait_counter(rt_cnt + ct, rows * slabs);
+#endif
         const bool ready = ptx::ld_acquire_gpu(rt_cnt + ct) >= rows * slabs;
         if (ready) ptx::fence_proxy_async_global();
         if (ready && rank == 0) btrace(dbg, 1, T);
@@ -1292,7 +1318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
             uint8_t *A = smem + s * DA_STAGE;
             if (bx) ptx::tma_load_2d_pair(mZ, &full[s], A, kb * BK, mt);
             for (int ch = 0; ch < N / 128; ch++)
-              ptx::tma_load_2d_pair(&tmU, &full[s], A + DA_A_BYTES + ch * MN_CHUNK, nb + ch * 64, kb * BK);
+              BWD_TMA_U(&tmU, &full[s], A + DA_A_BYTES + ch * MN_CHUNK, nb + ch * 64, kb * BK);
           }
           continue;
         }
@@ -1306,8 +1332,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
           if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)nk * bytes);
           for (int j = 0; j < nk; j++)
             for (int ch = 0; ch < N / 128; ch++)
-              ptx::tma_load_2d_pair(&tmU, &full[s], stg + uoff + j * ubox + ch * MN_CHUNK, nb + ch * 64,
-                                    (kb0 + j) * BK);
+              BWD_TMA_U(&tmU, &full[s], stg + uoff + j * ubox + ch * MN_CHUNK, nb + ch * 64, (kb0 + j) * BK);
           if (q < pre - 1) continue;
           if (q == pre - 1) {
             // this pair tile's dZ rows (and their dCe) complete
@@ -1354,6 +1379,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
             ptx::mbar_wait(&full[s], ph);
             __syncwarp();
             ptx::tc_fence_after();
+            if (kb == 0 && lane == 0) btrace(dbg, 8, T);
             const uint32_t a0 = ptx::smem_u32(smem + s * DA_STAGE), b0 = a0 + DA_A_BYTES;
             const uint64_t da = ptx::sdesc_sw128(a0, 16, 1024), db = ptx::sdesc_sw128(b0, MN_CHUNK, 1024);
             if (ptx::elect_one()) {
@@ -1378,6 +1404,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
           ptx::mbar_wait(&full[s], ph);
           __syncwarp();
           ptx::tc_fence_after();
+          if (q == 0 && lane == 0) btrace(dbg, 8, T);
           const uint32_t st0 = ptx::smem_u32(smem + s * DA_STAGE);
           const int nk = min(kps, KB - q * kps);
           for (int j = 0; j < nk; j++) {
@@ -1439,7 +1466,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
       // c, dCe) while the tile's MMAs run: on latency-bound levels (chains) the epilogue's
       // HBM round trips are otherwise on every level's critical path (only on levels that
       // fit one wave of tiles: on wide levels the epilogue overlaps the next tile anyway)
+#ifdef FOLD_DIAG_BWD_NOPF  // diagnostics: no L2 warm-up of the pointwise operands
+      if (false) {
+#else
       if (my_valid && cur.nt <= npairs) {
+#endif
 #pragma unroll 1
         for (int slab = grp; slab < N / 64; slab += 2) {
           const int np = n0 + slab * 64;
@@ -1465,10 +1496,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         }
       }
       int slab_cnt[2] = {0, 0};  // columns this warp completes (its 64-column slabs), per half
+#ifdef FOLD_DIAG_EPI_SLEEP
+      ptx::mbar_wait_sleep(&tfull[acc], (tc >> 1) & 1);
+#else
       ptx::mbar_wait(&tfull[acc], (tc >> 1) & 1);
+#endif
       ptx::tc_fence_after();
       if (warp == 4 && lane == 0 && rank == 0) btrace(dbg, 4, T);
       const uint32_t tl = tbase + acc * 256 + ((uint32_t)(q * 32) << 16);
+#ifdef FOLD_DIAG_BWD_EPIMIN  // diagnostics only (wrong results): the epilogue only counts columns
+      for (int slab = grp; slab < N / 64; slab += 2) {
+        const int np = n0 + slab * 64, half = np >= Sp;
+        if (np - half * Sp < S) slab_cnt[half] += min(64, S - (np - half * Sp));
+      }
+      if (c_end < 0)
+#endif
 #pragma unroll 1
       for (int slab = grp; slab < N / 64; slab += 2) {
         // TMEM (thread = row) -> smem transpose buffer
@@ -1485,6 +1527,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         for (int k = 0; k < 64; k += 2)
           *reinterpret_cast<float2 *>(xs + lane * 64 + (k ^ (2 * lane))) = make_float2(v[k], v[k + 1]);
         __syncwarp();
+        if (warp == 4 && lane == 0 && rank == 0 && slab == grp) btrace(dbg, 6, T);
         const int np = n0 + slab * 64;  // padded column of the slab (the slab lies in one half)
         const int half = np >= Sp;
         const int col = np - half * Sp + 2 * lane;  // this lane's 2 state columns
@@ -1508,7 +1551,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
             ok[j] = colok && i < 32 && c_row0 + i < c_end;
             dh[j] = *reinterpret_cast<const float2 *>(xs + (i & 31) * 64 + ((2 * lane) ^ (2 * (i & 31))));
             const int64_t e = 2 * (int64_t)(c_row0 + i) + half;
+#ifdef FOLD_DIAG_BWD_NOLOAD  // diagnostics only (wrong results): the row loop without its loads
+            if (false) {
+#else
             if (ok[j] && xs_[j] >= nl) {
+#endif
               const int64_t xc = xs_[j] - nl;
               const __nv_bfloat16 *gx = Gact + xc * ld_g + col;
 #pragma unroll
@@ -1523,6 +1570,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
               }
             }
           }
+#ifdef FOLD_DIAG_BWD_NOLOAD
+#pragma unroll
+          for (int j = 0; j < R; j++) {
+#pragma unroll
+            for (int g = 0; g < GATES; g++) graw[j][g] = 0x3f003f00u;
+            cc[j] = cl[j] = cr[j] = dc[j] = make_float2(0.5f, 0.5f);
+          }
+#endif
+#ifdef FOLD_DIAG_BWD_NOSTORE  // diagnostics only: the row loop without its stores
+          if (c_end < 0)
+#endif
 #pragma unroll
           for (int j = 0; j < R; j++) {
             if (!ok[j]) continue;
@@ -1571,6 +1629,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
           }
         }
         __syncwarp();
+        if (warp == 4 && lane == 0 && rank == 0 && slab == grp) btrace(dbg, 7, T);
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -2441,8 +2500,12 @@ int tc_ld_u(int S) { return 2 * (int)round_up(S, BK); }
 
 int tc_debug_bwd_trace(unsigned long long *host, int n) {
   if (n > kTraceTiles) n = kTraceTiles;
-  for (int p = 0; p < 6; p++)
+  for (int p = 0; p < 9; p++)
     if (cudaMemcpyFromSymbol(host + (size_t)p * n, g_bwd_trace, (size_t)n * 8, (size_t)p * kTraceTiles * 8) !=
+        cudaSuccess)
+      return -1;
+  for (int p = 0; p < 2; p++)
+    if (cudaMemcpyFromSymbol(host + (size_t)(9 + p) * n, g_bwd_clk, (size_t)n * 8, (size_t)p * kTraceTiles * 8) !=
         cudaSuccess)
       return -1;
   return n;

@@ -39,6 +39,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
+// non-blocking probe of a barrier phase (mbarrier.test_wait: no suspend)
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// wait with back-off: for warps that wait long on a barrier (epilogue warps during a tile's
+// mainloop) without taking issue slots from the producer / MMA warps
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+  while (!mbar_test(bar, parity)) __nanosleep(128);
+}
+
 // ---------------------------------------------------------------- TMA
 // 16-byte shared-memory load at a shared-window address (volatile: stays after the
 // barrier wait that precedes it)
@@ -266,6 +284,25 @@ __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap *m, uint64_t 
       "%4}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & kLeaderMask), "r"(x), "r"(y)
       : "memory");
+}
+// the same with an L2 cache-policy hint (createpolicy_*)
+__device__ __forceinline__ void tma_load_2d_pair_hint(const CUtensorMap *m, uint64_t *bar, void *dst, int x, int y,
+                                                      uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & kLeaderMask), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t createpolicy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t createpolicy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 // arrive on the leader's copy of a barrier (either CTA)
 __device__ __forceinline__ void mbar_arrive_leader(uint64_t *bar) {

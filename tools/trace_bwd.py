@@ -26,7 +26,7 @@ for _ in range(3):
     fold.backward(s, model, acts, g, ws=ws)
 torch.cuda.synchronize()
 n = 65536
-buf = np.zeros((6, n), np.uint64)
+buf = np.zeros((11, n), np.uint64)
 got = fold.load().fold_debug_bwd_trace(buf.ctypes.data, n)
 lo = [int(x) for x in s.level_off_host[: s.n_levels + 2]]
 D = s.n_levels
@@ -45,10 +45,15 @@ ntot = min(got, sum(x[3] for x in tiles))
 t = buf[:, :ntot].astype(np.int64)
 t0 = t[0][t[0] > 0].min()
 x = (t - t0) / 1e3
-names = ["start", "inputs", "acc_free", "mma_done", "acc_ready", "published"]
+names = ["start", "inputs", "acc_free", "mma_done", "acc_ready", "published", "slab0_in_smem", "slab0_rows_done", "first_stage"]
 print(f"{a.config} B={a.batch}: wide levels {len(tiles)} (from d={d}), tiles {ntot}, span {x[5].max():.1f} us")
 print("medians (us): " + " ".join(f"{names[i]}->{names[j]}={np.median(x[j] - x[i]):.2f}"
-                                   for i, j in ((0, 1), (1, 3), (2, 3), (3, 4), (4, 5), (0, 5))))
+                                   for i, j in ((0, 1), (1, 8), (8, 3), (1, 3), (3, 4), (4, 5), (4, 6), (6, 7), (7, 5), (0, 5))))
+cyc = (buf[10, :ntot].astype(np.int64) - buf[9, :ntot].astype(np.int64))
+ns = (buf[3, :ntot].astype(np.int64) - buf[8, :ntot].astype(np.int64))
+okc = (ns > 0) & (cyc > 0)
+print(f"first_stage->mma_done: median {np.median(cyc[okc]):.0f} SM cycles, {np.median(ns[okc]) / 1e3:.2f} us, "
+      f"implied SM clock {np.median(cyc[okc] / ns[okc]) * 1e3:.0f} MHz")
 print("level     M    N tiles |  first_start  max_inputs  max_mma_done  max_acc_ready  max_pub | period")
 T0, prev = 0, 0.0
 rows = []
