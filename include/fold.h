@@ -333,7 +333,7 @@ void fold_profile_enable(int32_t on);
 void fold_profile_enable_classes(uint32_t mask);
 fold_status fold_profile_read(int32_t n_classes, double *ms, int64_t *launches);
 /* Instrumentation: with FOLD_DBG_FWD=1 in the environment the BF16 forward kernel stamps
- * %globaltimer (ns) per pair tile at nine points: 0 producer starts the tile, 1 its
+ * %globaltimer (ns) per pair tile at ten points: 0 producer starts the tile, 1 its
  * inputs are published, 2 its last MMA is issued, 3 its accumulator is ready in the
  * epilogue, 4 its outputs are published, 5 the epilogue may write its staging, 6 the
  * epilogue math is done, 7 the bulk stores have read the staging, 8 the bulk stores are
@@ -342,14 +342,15 @@ fold_status fold_profile_read(int32_t n_classes, double *ms, int64_t *launches);
  * on a CUDA error. */
 int32_t fold_debug_fwd_trace(unsigned long long *host, int32_t n_tiles);
 /* Instrumentation: with FOLD_DBG_BWD=1 the wide backward kernel (k_bwd_levels) records
- * %globaltimer (ns) per pair tile at nine points: 0 producer starts the tile, 1 its inputs
+ * %globaltimer (ns) per pair tile at ten points: 0 producer starts the tile, 1 its inputs
  * (dZ rows, dCe) are published, 2 its accumulator is free, 3 its last MMA is issued, 4 the
  * accumulator is ready in the epilogue, 5 the epilogue has published, 6 the first epilogue
  * warp's first slab is in its transpose buffer, 7 that slab's pointwise rows are done,
- * 8 the tile's first pipeline stage has landed (MMA warp). Tiles in the kernel's order
- * (levels descending from the first wide level, row tile, column tile). Copies the first
- * n_tiles stamps of each point into host[9][n_tiles], then the SM clock64 values at points 8
- * and 3 into host[9..10][n_tiles] (host holds 11 x n_tiles);
+ * 8 the tile's first pipeline stage has landed (MMA warp), 9 that warp's first row group
+ * is done. Tiles in the kernel's order (levels descending from the first wide level, row
+ * tile, column tile, k-half). Copies the first n_tiles stamps of each point into
+ * host[10][n_tiles], then the SM clock64 values at points 8 and 3 into host[10..11][n_tiles]
+ * (host holds 12 x n_tiles);
  * returns the count, or -1 on a CUDA error. */
 int32_t fold_debug_bwd_trace(unsigned long long *host, int32_t n_tiles);
 /* Instrumentation: with FOLD_DBG_SCHED=1, fold_schedule's block 0 stamps %globaltimer (ns)

@@ -63,6 +63,8 @@ struct BwdWs {
   int32_t *root_off;
   int *rt_cnt;      // [n_cells] row-tile counters of the fused backward
   int32_t *tstart;  // [n_cells]
+  float *ks_ring;   // its split-K hand-over slots (BF16 path)
+  int *ks_cnt;
   EmbedBwdWs emb;
   void *dZ;
   __nv_bfloat16 *Ub, *Ut;
@@ -100,6 +102,7 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
   const int64_t tf_split = tf ? gemm_tf32_split_floats(gates * (int)S, 2 * (int)S, (int)nc) : 0;
   b.tf_split_floats = tf_split;
   size_t o_spl = take(splits > 1 ? (size_t)splits * gates * S * 2 * S * 4 : (size_t)tf_split * 4);
+  size_t o_ksr = take(bf16 ? tc_ks_ring_bytes() : 0), o_ksc = take(bf16 ? (size_t)2 * kKsRing * 4 : 0);
   b.bytes = off;
   if (base) {
     char *p = (char *)base;
@@ -119,6 +122,8 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
     b.Ub = bf16 ? (__nv_bfloat16 *)(p + o_w) : nullptr;
     b.Utf = tf ? (float *)(p + o_w) : nullptr;
     b.Ut = bf16 ? (__nv_bfloat16 *)(p + o_ut) : nullptr;
+    b.ks_ring = bf16 ? (float *)(p + o_ksr) : nullptr;
+    b.ks_cnt = bf16 ? (int *)(p + o_ksc) : nullptr;
   }
   return b;
 }
@@ -344,6 +349,7 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
     ba.D = D; ba.S = S; ba.nl = nl; ba.n_cells = nc; ba.ld = L.ld; ba.ld_g = L.ld_g; ba.ld_z = b.ld_z;
     ba.gather = s->gather; ba.Ub = b.Ub; ba.U = m->U; ba.Ut = b.Ut; ba.Gact = (const __nv_bfloat16 *)Gact; ba.C = C;
     ba.dA = b.dA; ba.dCe = b.dCe; ba.dZ = (__nv_bfloat16 *)b.dZ; ba.rt_cnt = b.rt_cnt; ba.tstart = b.tstart;
+    ba.ks_ring = b.ks_ring; ba.ks_cnt = b.ks_cnt;
     {
       ProfScope ps(K_BWD_PW, st);
       FOLD_TRY(launch_cell_bwd_pw(bf16, m->cell, 0, G, nl, S, L.ld, L.ld_g, s->cons_off, s->cons_edge, b.root_off,

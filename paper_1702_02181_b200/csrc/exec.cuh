@@ -127,7 +127,13 @@ struct TcBwdArgs {
   __nv_bfloat16 *dZ;
   int *rt_cnt;       // [n_cells] per-row-tile completion counters (keyed by a tile's first cell)
   int32_t *tstart;   // [n_cells] first cell of each cell's row tile
+  float *ks_ring;    // [kKsRing][kKsSlotFloats] split-K hand-over slots (k_bwd_levels)
+  int *ks_cnt;       // [2 * kKsRing] their written / read counts (zeroed by tc_bwd_prelude)
 };
+// split-K hand-over ring of the wide backward (see k_bwd_levels)
+constexpr int kKsRing = 256;
+constexpr int kKsSlotFloats = 2 * 128 * 128;
+inline size_t tc_ks_ring_bytes() { return (size_t)kKsRing * kKsSlotFloats * 4; }
 // tile bookkeeping (zero counters, tstart, roots' pre-credit); before the seeded pass
 fold_status tc_bwd_prelude(const TcBwdArgs &a, const int32_t *cons_off, cudaStream_t st);
 fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st);

@@ -45,8 +45,8 @@ __device__ __forceinline__ void trace(int dbg, int pt, int T) {
     g_fwd_trace[pt][T] = t;
   }
 }
-// FOLD_DBG_BWD=1: the same for k_bwd_levels at nine points (see fold_debug_bwd_trace)
-__device__ unsigned long long g_bwd_trace[9][kTraceTiles];
+// FOLD_DBG_BWD=1: the same for k_bwd_levels at ten points (see fold_debug_bwd_trace)
+__device__ unsigned long long g_bwd_trace[10][kTraceTiles];
 __device__ unsigned long long g_bwd_clk[2][kTraceTiles];  // SM clock64 at points 8 and 3
 __device__ __forceinline__ void btrace(int dbg, int pt, int T) {
   if (dbg && T < kTraceTiles) {
@@ -1155,21 +1155,51 @@ struct BwdLevels {
   int D, S, nl, ld_u;
   int narrow_below;  // a level with fewer 256-column pair tiles than this uses 128 columns
   int pf;            // L2 prefetch distance of the dZ (A operand) boxes in k-blocks (0: off)
+  int ksplit_max;    // split-K units allowed per level (0: no split; else the number of CTA pairs)
+  int KB;            // k-blocks of the full K = GATES*S reduction
+  int ks256;         // split-K also for 256-column tiles
 };
-__host__ __device__ inline int bwd_level_N(const BwdLevels &L, int M) {
-  return cdiv(M, PM) * cdiv(L.ld_u, 256) < L.narrow_below ? 128 : 256;
+// Per-level tiling: N (128 or 256 columns) and KS (1, or 2 = split-K in two k-halves). A
+// latency-bound level that fits one wave of CTA pairs twice over runs each tile as two
+// k-half units on two pairs: each pair accumulates half of the K = GATES*S reduction, hands
+// the partial of the OTHER half's columns to its partner through L2 (ring slots) and
+// finishes its own half of the columns, so a level's mainloop and epilogue both halve.
+struct BwdCfg {
+  int N, KS;
+};
+__host__ __device__ inline BwdCfg bwd_level_cfg(const BwdLevels &L, int M) {
+  const int rt = (int)cdiv(M, PM), t256 = rt * (int)cdiv(L.ld_u, 256), t128 = rt * (int)cdiv(L.ld_u, 128);
+  if (L.ksplit_max > 0 && L.KB >= 8) {
+    if (2 * t128 <= L.ksplit_max) return {128, 2};
+    if (L.ks256 && 2 * t256 <= L.ksplit_max) return {256, 2};
+  }
+  return {t256 < L.narrow_below ? 128 : 256, 1};
 }
 struct BwdCursor {  // walks levels D, D-1, ..., 2 in tile order
-  int d, t0, nt, r0, r1, N, NTn;
+  int d, t0, nt, r0, r1, N, NTn, KS;
   __device__ void load(const BwdLevels &L) {
     r0 = __ldg(L.lo + d); r1 = __ldg(L.lo + d + 1);
-    N = bwd_level_N(L, r1 - r0);
+    const BwdCfg c = bwd_level_cfg(L, r1 - r0);
+    N = c.N;
+    KS = c.KS;
     NTn = (int)cdiv(L.ld_u, N);
-    nt = (int)cdiv(r1 - r0, PM) * NTn;
+    nt = (int)cdiv(r1 - r0, PM) * NTn * KS;
   }
   __device__ void init(const BwdLevels &L) { d = L.D; t0 = 0; load(L); }
   __device__ void seek(const BwdLevels &L, int T) {
     while (T >= t0 + nt) { t0 += nt; d--; load(L); }
+  }
+  // level-local tile lt = ((row tile) * NTn + column tile) * KS + k-half
+  __device__ int row_tile(int lt) const { return lt / (NTn * KS); }
+  __device__ int col_tile(int lt) const { return (lt / KS) % NTn; }
+  __device__ int khalf(int lt) const { return lt % KS; }
+  __device__ int first_cell(const BwdLevels &L, int lt) const { return (r0 - L.nl) + row_tile(lt) * PM; }
+  // k-block range of tile lt: the whole K, or one half of it
+  __device__ void krange(const BwdLevels &L, int lt, int &k0, int &k1) const {
+    const int h = L.KB / 2;
+    if (KS == 1) { k0 = 0; k1 = L.KB; }
+    else if (khalf(lt) == 0) { k0 = 0; k1 = h; }
+    else { k0 = h; k1 = L.KB; }
   }
 };
 
@@ -1208,6 +1238,9 @@ constexpr int BW_THREADS = 128 + 32 * BW_EPI;
 // the column-wise float2 reads are both conflict-free per half-warp, and the 2 KB the padding
 // took leaves room for a fifth pipeline stage
 constexpr int BW_XS = 32 * 64;
+// split-K hand-over ring: kKsRing slots of [2 CTAs][128 rows][128 columns] fp32 partial sums;
+// slot T % kKsRing holds unit T's partial (use T / kKsRing), with a written count and a read
+// count per slot (k_bwd_levels waits for the previous use's read before reusing a slot)
 constexpr int BW_SMEM = BW_ST * DA_STAGE + BW_EPI * BW_XS * 4 + 1024;
 
 template <int GATES>
@@ -1217,7 +1250,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
                  int KB, int total_tiles, const int32_t *__restrict__ gather,
                  const __nv_bfloat16 *__restrict__ Gact, int ld_g, const float *__restrict__ C, int ld, float *dA,
                  float *dCe, __nv_bfloat16 *dZ, int ld_z, int *rt_cnt, const int32_t *__restrict__ tstart,
-                 int slabs, int dbg) {
+                 int slabs, int dbg, float *ks_ring, int *ks_wr, int *ks_cons) {
   constexpr int ST = BW_ST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
@@ -1255,7 +1288,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
       auto box_of = [](int m) { return m <= 0 ? 0 : m <= 16 ? 16 : m <= 64 ? 64 : BM; };
       // this CTA's dZ box (map, first row) of tile T (bx = 0: the CTA holds no rows)
       auto zbox = [&](const BwdCursor &c, int T, const CUtensorMap *&m, int &row) {
-        const int ctt = (c.r0 - nl) + ((T - c.t0) / c.NTn) * PM;
+        const int ctt = c.first_cell(L, T - c.t0);
         const int rw = min(PM, c.r1 - nl - ctt);
         const int b = rank ? box_of(rw - BM) : box_of(min(rw, BM));
         m = b == 16 ? &tmZ16 : b == 64 ? &tmZ64 : &tmZ;
@@ -1265,9 +1298,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
       const int pf = L.pf;
       for (int T = pair; T < total_tiles; T += npairs) {
         cur.seek(L, T);
-        const int lt = T - cur.t0, NTn = cur.NTn, N = cur.N;
-        const int ct = (cur.r0 - nl) + (lt / NTn) * PM;  // first cell of the pair tile
+        const int lt = T - cur.t0, N = cur.N;
+        const int ct = cur.first_cell(L, lt);  // first cell of the pair tile
         const int rows = min(PM, cur.r1 - nl - ct);
+        int k0, k1;  // this unit's k-blocks (all, or one k-half)
+        cur.krange(L, lt, k0, k1);
+        const int nkb = k1 - k0;
         // narrow tiles load only the dZ rows they hold (see k_fwd_levels)
         const int bx0 = box_of(min(rows, BM)), bx1 = box_of(rows - BM), bx = rank ? bx1 : bx0;
         const CUtensorMap *mZ = bx == 16 ? &tmZ16 : bx == 64 ? &tmZ64 : &tmZ;
@@ -1279,17 +1315,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         // the last pf k-blocks of a tile prefetch the head of this pair's next tile.
         const CUtensorMap *mZn = nullptr;
         int mtn = 0, bxn = 0;
+        int kn0 = 0;
         if (pf > 0 && T + npairs < total_tiles) {
           BwdCursor nx = cur;
           nx.seek(L, T + npairs);
           bxn = zbox(nx, T + npairs, mZn, mtn);
+          int kn1;
+          nx.krange(L, T + npairs - nx.t0, kn0, kn1);
         }
-        const int nb = (lt % NTn) * N + (int)rank * (N / 2);
+        const int nb = cur.col_tile(lt) * N + (int)rank * (N / 2);
         const uint32_t bytes = (uint32_t)(bx0 + bx1) * 128 + N * 128;
         // the first stages' U boxes are issued before the dependency wait; narrow tiles pack
         // kps k-blocks per stage
         const int kps = bwd_kps(N, bx0), abox = bx0 * 128, ubox = (N / 128) * MN_CHUNK;
-        const int nst = (KB + kps - 1) / kps;
+        const int nst = (nkb + kps - 1) / kps;
         if (rank == 0) btrace(dbg, 0, T);
 #ifndef FOLD_BWD_EARLY_U
         // wait for the tile's inputs before issuing any of its boxes: issuing the first stages'
@@ -1303,12 +1342,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         if (ready && rank == 0) btrace(dbg, 1, T);
         const int pre = ready ? 0 : (nst < ST ? nst : ST);
         if (ready && kps == 1) {  // inputs published: one (A, U) box set per stage
-          for (int kb = 0; kb < KB; kb++, it++) {
+          for (int kb = k0; kb < k1; kb++, it++) {
             if (pf > 0) {
-              if (kb + pf < KB) {
+              if (kb + pf < k1) {
                 if (bx) ptx::tma_prefetch_2d(mZ, (kb + pf) * BK, mt);
-              } else if (bxn && kb + pf - KB < KB) {
-                ptx::tma_prefetch_2d(mZn, (kb + pf - KB) * BK, mtn);
+              } else if (bxn && kb + pf - k1 < KB) {
+                ptx::tma_prefetch_2d(mZn, (kn0 + kb + pf - k1) * BK, mtn);
               }
             }
             const int s = it % ST;
@@ -1326,7 +1365,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         for (int q = 0; q < nst; q++) {
           const int s = (it + q) % ST;
           const uint32_t ph = ((it + q) / ST) & 1;
-          const int kb0 = q * kps, nk = min(kps, KB - kb0);
+          const int kb0 = k0 + q * kps, nk = min(kps, k1 - kb0);
           uint8_t *stg = smem + s * DA_STAGE;
           ptx::mbar_wait(&empty[s], ph ^ 1);
           if (rank == 0) ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)nk * bytes);
@@ -1342,8 +1381,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
             if (bx)
               for (int q2 = 0; q2 < pre; q2++) {
                 const int s2 = (it + q2) % ST;
-                for (int j = 0; j < kps && q2 * kps + j < KB; j++)
-                  ptx::tma_load_2d_pair(mZ, &full[s2], smem + s2 * DA_STAGE + j * abox, (q2 * kps + j) * BK, mt);
+                for (int j = 0; j < kps && q2 * kps + j < nkb; j++)
+                  ptx::tma_load_2d_pair(mZ, &full[s2], smem + s2 * DA_STAGE + j * abox, (k0 + q2 * kps + j) * BK,
+                                        mt);
               }
             continue;
           }
@@ -1367,26 +1407,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         ptx::tc_fence_after();
         if (lane == 0) btrace(dbg, 2, T);
         const uint32_t dst = tbase + acc * 256;
-        const int ct = (cur.r0 - nl) + ((T - cur.t0) / cur.NTn) * PM;
+        const int ct = cur.first_cell(L, T - cur.t0);
         const int rows0 = min(BM, cur.r1 - nl - ct);
         const int bx0 = rows0 <= 16 ? 16 : rows0 <= 64 ? 64 : BM;
         const int kps = bwd_kps(cur.N, bx0), abox = bx0 * 128, ubox = (cur.N / 128) * MN_CHUNK;
-        const int nst = (KB + kps - 1) / kps;
+        int k0, k1;
+        cur.krange(L, T - cur.t0, k0, k1);
+        const int nst = (k1 - k0 + kps - 1) / kps;
         if (kps == 1) {  // one k-block per stage, U at the fixed offset DA_A_BYTES
-          for (int kb = 0; kb < KB; kb++, it++) {
+          for (int kb = k0; kb < k1; kb++, it++) {
             int s = it % ST;
             uint32_t ph = (it / ST) & 1;
             ptx::mbar_wait(&full[s], ph);
             __syncwarp();
             ptx::tc_fence_after();
-            if (kb == 0 && lane == 0) btrace(dbg, 8, T);
+            if (kb == k0 && lane == 0) btrace(dbg, 8, T);
             const uint32_t a0 = ptx::smem_u32(smem + s * DA_STAGE), b0 = a0 + DA_A_BYTES;
             const uint64_t da = ptx::sdesc_sw128(a0, 16, 1024), db = ptx::sdesc_sw128(b0, MN_CHUNK, 1024);
             if (ptx::elect_one()) {
 #pragma unroll
               for (int k = 0; k < BK / 16; k++)
                 ptx::umma_bf16_2cta(dst, ptx::desc_add(da, 32 * k), ptx::desc_add(db, 2048 * k), idesc,
-                                    (kb | k) != 0);
+                                    (kb != k0 || k != 0));
               ptx::umma_commit_2cta(&empty[s]);
             }
             __syncwarp();
@@ -1406,7 +1448,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
           ptx::tc_fence_after();
           if (q == 0 && lane == 0) btrace(dbg, 8, T);
           const uint32_t st0 = ptx::smem_u32(smem + s * DA_STAGE);
-          const int nk = min(kps, KB - q * kps);
+          const int nk = min(kps, k1 - k0 - q * kps);
           for (int j = 0; j < nk; j++) {
             const uint64_t da = ptx::sdesc_sw128(st0 + j * abox, 16, 1024);
             const uint64_t db = ptx::sdesc_sw128(st0 + kps * abox + j * ubox, MN_CHUNK, 1024);
@@ -1434,22 +1476,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
     BwdCursor cur;
     cur.init(L);
     int tc = 0;
+    // TMEM (thread = row) -> this warp's smem transpose buffer: 32 rows x the 64 columns of
+    // accumulator slab `slab` (row r's column c at r * 64 + (c ^ 2r), float2 granules)
+    auto slab_to_xs = [&](uint32_t tl, int slab) {
+      float v[64];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        float t8[8];
+        ptx::tmem_ld8(tl + slab * 64 + k * 8, t8);
+#pragma unroll
+        for (int u = 0; u < 8; u++) v[k * 8 + u] = t8[u];
+      }
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int k = 0; k < 64; k += 2)
+        *reinterpret_cast<float2 *>(xs + lane * 64 + (k ^ (2 * lane))) = make_float2(v[k], v[k + 1]);
+      __syncwarp();
+    };
     for (int T = pair; T < total_tiles; T += npairs, tc++) {
       cur.seek(L, T);
-      const int NTn = cur.NTn, N = cur.N;
+      const int N = cur.N, KS = cur.KS;
       const int acc = tc & 1;
       const int lt = T - cur.t0;
+      const int ct = cur.first_cell(L, lt);
       {  // order this warp's dCe reads after the tile's publication (already complete)
-        const int ct = (cur.r0 - nl) + (lt / NTn) * PM;
         if (lane == 0) ptx::wait_counter(rt_cnt + ct, min(PM, cur.r1 - nl - ct) * slabs);
         __syncwarp();
       }
-      const int c_row0 = (cur.r0 - nl) + (lt / NTn) * PM + (int)rank * BM + q * 32;  // cell of row 0
+      const int c_row0 = ct + (int)rank * BM + q * 32;  // cell of row 0
       const int c_end = cur.r1 - nl;
-      const int n0 = (lt % NTn) * N;
+      const int n0 = cur.col_tile(lt) * N;
+      // this unit's own 64-column slabs (all N / 64, or its k-half's half of them) and, on a
+      // split-K level, the partner's slabs whose partial sums it hands over
+      const int nsl = N / 64, kh = cur.khalf(lt);
+      const int own_n = KS == 1 ? nsl : nsl / 2, own_lo = KS == 1 ? 0 : kh * own_n;
+      const int oth_n = KS == 1 ? 0 : nsl / 2, oth_lo = (1 - kh) * oth_n;
+      // a unit owning one slab: the two warps of a lane quarter split its 32 rows
+      const bool rsplit = own_n == 1;
+      const int i_lo = rsplit ? 16 * grp : 0, i_hi = rsplit ? i_lo + 16 : 32;
+      const int w0 = rsplit ? 0 : grp, wstep = rsplit ? 1 : 2;
       // per-row metadata for this warp's 32 rows: lane i <-> row i
       const int my_c = c_row0 + lane;
       const bool my_valid = my_c < c_end;
+      const bool my_rows = lane >= i_lo && lane < i_hi;  // rows this warp finishes
       int my_x[2] = {-1, -1}, my_xl[2] = {-1, -1}, my_xr[2] = {-1, -1}, my_ts[2] = {-1, -1};
       if (my_valid) {
 #pragma unroll
@@ -1466,14 +1535,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
       // c, dCe) while the tile's MMAs run: on latency-bound levels (chains) the epilogue's
       // HBM round trips are otherwise on every level's critical path (only on levels that
       // fit one wave of tiles: on wide levels the epilogue overlaps the next tile anyway)
-#ifdef FOLD_DIAG_BWD_NOPF  // diagnostics: no L2 warm-up of the pointwise operands
-      if (false) {
-#else
-      if (my_valid && cur.nt <= npairs) {
-#endif
+      if (my_valid && my_rows && cur.nt <= npairs) {
 #pragma unroll 1
-        for (int slab = grp; slab < N / 64; slab += 2) {
-          const int np = n0 + slab * 64;
+        for (int w = w0; w < own_n; w += wstep) {
+          const int np = n0 + (own_lo + w) * 64;
           const int half = np >= Sp;
           const int col = np - half * Sp;
           const int x = my_x[half];
@@ -1496,38 +1561,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         }
       }
       int slab_cnt[2] = {0, 0};  // columns this warp completes (its 64-column slabs), per half
-#ifdef FOLD_DIAG_EPI_SLEEP
-      ptx::mbar_wait_sleep(&tfull[acc], (tc >> 1) & 1);
-#else
       ptx::mbar_wait(&tfull[acc], (tc >> 1) & 1);
-#endif
       ptx::tc_fence_after();
       if (warp == 4 && lane == 0 && rank == 0) btrace(dbg, 4, T);
       const uint32_t tl = tbase + acc * 256 + ((uint32_t)(q * 32) << 16);
-#ifdef FOLD_DIAG_BWD_EPIMIN  // diagnostics only (wrong results): the epilogue only counts columns
-      for (int slab = grp; slab < N / 64; slab += 2) {
-        const int np = n0 + slab * 64, half = np >= Sp;
-        if (np - half * Sp < S) slab_cnt[half] += min(64, S - (np - half * Sp));
-      }
-      if (c_end < 0)
-#endif
-#pragma unroll 1
-      for (int slab = grp; slab < N / 64; slab += 2) {
-        // TMEM (thread = row) -> smem transpose buffer
-        float v[64];
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-          float t8[8];
-          ptx::tmem_ld8(tl + slab * 64 + k * 8, t8);
-#pragma unroll
-          for (int u = 0; u < 8; u++) v[k * 8 + u] = t8[u];
+      // split-K, phase A: the partner's slabs' partial sums -> this unit's ring slot (fp32,
+      // [CTA rank][128 rows][128 columns], rows through the transpose buffer so each store
+      // is a coalesced row segment); every epilogue warp of the pair then raises the slot's
+      // written count (release), 2 * BW_EPI per use
+      const float *pp = nullptr;
+      int pslot = 0;
+      if (KS == 2) {
+        const int slot = T % kKsRing, use = T / kKsRing;
+        float *dst = ks_ring + (size_t)slot * kKsSlotFloats + (size_t)rank * BM * 128 + (size_t)q * 32 * 128;
+        if (use > 0) {  // the slot's previous unit (tile T - kKsRing) has been read by its partner
+          if (lane == 0) ptx::wait_counter(ks_cons + slot, use * 2 * BW_EPI);
+          __syncwarp();
         }
-        ptx::tmem_ld_wait();
-#pragma unroll
-        for (int k = 0; k < 64; k += 2)
-          *reinterpret_cast<float2 *>(xs + lane * 64 + (k ^ (2 * lane))) = make_float2(v[k], v[k + 1]);
+#pragma unroll 1
+        for (int o = (grp + 1) & 1; o < oth_n; o += 2) {
+          slab_to_xs(tl, oth_lo + o);
+#pragma unroll 4
+          for (int i = 0; i < 32; i++)
+            *reinterpret_cast<float2 *>(dst + i * 128 + o * 64 + 2 * lane) =
+                *reinterpret_cast<const float2 *>(xs + i * 64 + ((2 * lane) ^ (2 * i)));
+          __syncwarp();
+        }
+        __threadfence();
         __syncwarp();
-        if (warp == 4 && lane == 0 && rank == 0 && slab == grp) btrace(dbg, 6, T);
+        if (lane == 0) atomicAdd(ks_wr + slot, 1);
+        // the partner unit's partial sums of this unit's slabs
+        const int Tp = kh == 0 ? T + 1 : T - 1;
+        pslot = Tp % kKsRing;
+        if (lane == 0) ptx::wait_counter(ks_wr + pslot, (Tp / kKsRing + 1) * 2 * BW_EPI);
+        __syncwarp();
+        pp = ks_ring + (size_t)pslot * kKsSlotFloats + (size_t)rank * BM * 128 + (size_t)q * 32 * 128;
+      }
+#pragma unroll 1
+      for (int w = w0; w < own_n; w += wstep) {
+        const int slab = own_lo + w;
+        slab_to_xs(tl, slab);
+        if (warp == 4 && lane == 0 && rank == 0 && w == w0) btrace(dbg, 6, T);
         const int np = n0 + slab * 64;  // padded column of the slab (the slab lies in one half)
         const int half = np >= Sp;
         const int col = np - half * Sp + 2 * lane;  // this lane's 2 state columns
@@ -1537,10 +1611,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         // then the math and the stores
         constexpr int R = 4;
 #pragma unroll 1
-        for (int i0 = 0; i0 < 32 && c_row0 + i0 < c_end; i0 += R) {
+        for (int i0 = i_lo; i0 < i_hi && c_row0 + i0 < c_end; i0 += R) {
           int xs_[R], xls[R], xrs[R];
           bool ok[R];
-          float2 dh[R], cc[R], cl[R], cr[R], dc[R];
+          float2 dh[R], cc[R], cl[R], cr[R], dc[R], pv[R];
           uint32_t graw[R][GATES];
 #pragma unroll
           for (int j = 0; j < R; j++) {
@@ -1548,14 +1622,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
             xs_[j] = __shfl_sync(0xffffffffu, half ? my_x[1] : my_x[0], i);
             xls[j] = __shfl_sync(0xffffffffu, half ? my_xl[1] : my_xl[0], i);
             xrs[j] = __shfl_sync(0xffffffffu, half ? my_xr[1] : my_xr[0], i);
-            ok[j] = colok && i < 32 && c_row0 + i < c_end;
+            ok[j] = colok && i < i_hi && c_row0 + i < c_end;
             dh[j] = *reinterpret_cast<const float2 *>(xs + (i & 31) * 64 + ((2 * lane) ^ (2 * (i & 31))));
+            // split-K: the partner's partial sum, added below (fixed order: own + partner); the
+            // add waits for the load, so it stays out of this loop of loads
+            pv[j] = pp && ok[j] ? __ldcg(reinterpret_cast<const float2 *>(pp + i * 128 + w * 64 + 2 * lane))
+                                : make_float2(0.f, 0.f);
             const int64_t e = 2 * (int64_t)(c_row0 + i) + half;
-#ifdef FOLD_DIAG_BWD_NOLOAD  // diagnostics only (wrong results): the row loop without its loads
-            if (false) {
-#else
             if (ok[j] && xs_[j] >= nl) {
-#endif
               const int64_t xc = xs_[j] - nl;
               const __nv_bfloat16 *gx = Gact + xc * ld_g + col;
 #pragma unroll
@@ -1570,21 +1644,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
               }
             }
           }
-#ifdef FOLD_DIAG_BWD_NOLOAD
-#pragma unroll
-          for (int j = 0; j < R; j++) {
-#pragma unroll
-            for (int g = 0; g < GATES; g++) graw[j][g] = 0x3f003f00u;
-            cc[j] = cl[j] = cr[j] = dc[j] = make_float2(0.5f, 0.5f);
-          }
-#endif
-#ifdef FOLD_DIAG_BWD_NOSTORE  // diagnostics only: the row loop without its stores
-          if (c_end < 0)
-#endif
 #pragma unroll
           for (int j = 0; j < R; j++) {
             if (!ok[j]) continue;
             const int64_t e = 2 * (int64_t)(c_row0 + i0 + j) + half;
+            if (pp) {
+              dh[j].x += pv[j].x;
+              dh[j].y += pv[j].y;
+            }
             if (xs_[j] < nl) {  // leaf child: the embedding gradient reads dA (bf16 on this path)
               *reinterpret_cast<__nv_bfloat162 *>(reinterpret_cast<__nv_bfloat16 *>(dA) + e * S + col) =
                   __floats2bfloat162_rn(dh[j].x, dh[j].y);
@@ -1627,9 +1694,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
               if (xrs[j] >= nl) *reinterpret_cast<float2 *>(dCe + (2 * xc + 1) * S + col) = make_float2(er[0], er[1]);
             }
           }
+          if (warp == 4 && lane == 0 && rank == 0 && w == w0 && i0 == i_lo) btrace(dbg, 9, T);
         }
         __syncwarp();
-        if (warp == 4 && lane == 0 && rank == 0 && slab == grp) btrace(dbg, 7, T);
+        if (warp == 4 && lane == 0 && rank == 0 && w == w0) btrace(dbg, 7, T);
       }
       ptx::tc_fence_before();
       __syncwarp();
@@ -1639,9 +1707,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
       ptx::fence_proxy_async_global();
       __threadfence();
       __syncwarp();
+      if (KS == 2 && lane == 0) atomicAdd(ks_cons + pslot, 1);  // the partner's slot is read
 #pragma unroll
       for (int h = 0; h < 2; h++)
-        if (my_valid && my_ts[h] >= 0 && slab_cnt[h] > 0) atomicAdd(rt_cnt + my_ts[h], slab_cnt[h]);
+        if (my_valid && my_rows && my_ts[h] >= 0 && slab_cnt[h] > 0) atomicAdd(rt_cnt + my_ts[h], slab_cnt[h]);
       if (warp == 4 && lane == 0 && rank == 0) btrace(dbg, 5, T);
     }
   }
@@ -2500,12 +2569,12 @@ int tc_ld_u(int S) { return 2 * (int)round_up(S, BK); }
 
 int tc_debug_bwd_trace(unsigned long long *host, int n) {
   if (n > kTraceTiles) n = kTraceTiles;
-  for (int p = 0; p < 9; p++)
+  for (int p = 0; p < 10; p++)
     if (cudaMemcpyFromSymbol(host + (size_t)p * n, g_bwd_trace, (size_t)n * 8, (size_t)p * kTraceTiles * 8) !=
         cudaSuccess)
       return -1;
   for (int p = 0; p < 2; p++)
-    if (cudaMemcpyFromSymbol(host + (size_t)(9 + p) * n, g_bwd_clk, (size_t)n * 8, (size_t)p * kTraceTiles * 8) !=
+    if (cudaMemcpyFromSymbol(host + (size_t)(10 + p) * n, g_bwd_clk, (size_t)n * 8, (size_t)p * kTraceTiles * 8) !=
         cudaSuccess)
       return -1;
   return n;
@@ -2606,6 +2675,7 @@ int tc_bwd_slabs(int S) { return S; }
 fold_status tc_bwd_prelude(const TcBwdArgs &a, const int32_t *cons_off, cudaStream_t st) {
   if (a.n_cells <= 0) return FOLD_OK;
   FOLD_CUDA_TRY(cudaMemsetAsync(a.rt_cnt, 0, (size_t)a.n_cells * sizeof(int), st));
+  if (a.ks_cnt) FOLD_CUDA_TRY(cudaMemsetAsync(a.ks_cnt, 0, (size_t)2 * kKsRing * sizeof(int), st));
   int64_t blocks = cdiv(a.n_cells, 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
   k_bwd_prelude<<<(unsigned)blocks, 256, 0, st>>>(a.level_off, a.D, a.nl, a.n_cells, cons_off, a.tstart, a.rt_cnt,
@@ -2708,18 +2778,25 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
     FOLD_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)nk, dim3(grid), dim3(NB_THREADS), args, (size_t)nsm, st));
     FOLD_LAUNCH_CHECK();
   }
-  BwdLevels L{a.level_off, d1 - 1, S, a.nl, ld_u, npairs_max, l2_prefetch_dist("FOLD_PF_BWD")};
+  // FOLD_BWD_KSPLIT=0 disables the split-K units of latency-bound levels, 2 keeps them to
+  // 128-column tiles (A/B switches; C3 B=1024 dA 0.60 -> 0.50 ms, C4 12.1 -> 11.2-11.5 ms)
+  static const int ksplit_on = [] { const char *e = getenv("FOLD_BWD_KSPLIT"); return e ? atoi(e) : 1; }();
+  const int KB = (int)cdiv(gates * S, BK);
+  BwdLevels L{a.level_off, d1 - 1, S, a.nl, ld_u, npairs_max, l2_prefetch_dist("FOLD_PF_BWD"),
+              (ksplit_on && a.ks_ring && a.ks_cnt && npairs_max >= 2) ? npairs_max : 0, KB, ksplit_on != 2};
   int64_t total = 0;
   for (int d = 2; d < d1; d++) {
     const int M = a.level_off_host[d + 1] - a.level_off_host[d];
-    total += cdiv(M, PM) * cdiv(ld_u, bwd_level_N(L, M));
+    const BwdCfg c = bwd_level_cfg(L, M);
+    total += cdiv(M, PM) * cdiv(ld_u, c.N) * c.KS;
   }
   if (total <= 0) return FOLD_OK;
   if (total > INT32_MAX) return FOLD_E_INVALID;
   const int npairs = total < npairs_max ? (int)total : npairs_max;
-  kern<<<2 * npairs, BW_THREADS, BW_SMEM, st>>>(tmZ, tmZ16, tmZ64, tmU, L, (int)cdiv(gates * S, BK), (int)total, a.gather,
+  kern<<<2 * npairs, BW_THREADS, BW_SMEM, st>>>(tmZ, tmZ16, tmZ64, tmU, L, KB, (int)total, a.gather,
                                                a.Gact, a.ld_g, a.C, a.ld, a.dA, a.dCe, a.dZ, a.ld_z, a.rt_cnt,
-                                               a.tstart, tc_bwd_slabs(S), dbg_bwd());
+                                               a.tstart, tc_bwd_slabs(S), dbg_bwd(), a.ks_ring, a.ks_cnt,
+                                               a.ks_cnt ? a.ks_cnt + kKsRing : nullptr);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }

@@ -26,7 +26,7 @@ for _ in range(3):
     fold.backward(s, model, acts, g, ws=ws)
 torch.cuda.synchronize()
 n = 65536
-buf = np.zeros((11, n), np.uint64)
+buf = np.zeros((12, n), np.uint64)
 got = fold.load().fold_debug_bwd_trace(buf.ctypes.data, n)
 lo = [int(x) for x in s.level_off_host[: s.n_levels + 2]]
 D = s.n_levels
@@ -36,25 +36,34 @@ d = D
 while d >= 2 and lo[d + 1] - lo[d] <= a.narrow_max:
     d -= 1
 tiles = []
+KB = math.ceil(5 * S / 64)
+ks_on = os.environ.get("FOLD_BWD_KSPLIT", "1") != "0"
+ks256 = os.environ.get("FOLD_BWD_KSPLIT", "1") != "2"
 for dd in range(d, 1, -1):
     M = lo[dd + 1] - lo[dd]
     mt = math.ceil(M / 256)
-    N = 128 if mt * math.ceil(ld_u / 256) < npairs else 256
-    tiles.append((dd, M, N, mt * math.ceil(ld_u / N)))
+    t256, t128 = mt * math.ceil(ld_u / 256), mt * math.ceil(ld_u / 128)
+    if ks_on and KB >= 8 and 2 * t128 <= npairs:
+        N, KS = 128, 2
+    elif ks_on and ks256 and KB >= 8 and 2 * t256 <= npairs:
+        N, KS = 256, 2
+    else:
+        N, KS = (128 if t256 < npairs else 256), 1
+    tiles.append((dd, M, N * 10 + KS, mt * math.ceil(ld_u / N) * KS))
 ntot = min(got, sum(x[3] for x in tiles))
 t = buf[:, :ntot].astype(np.int64)
 t0 = t[0][t[0] > 0].min()
 x = (t - t0) / 1e3
-names = ["start", "inputs", "acc_free", "mma_done", "acc_ready", "published", "slab0_in_smem", "slab0_rows_done", "first_stage"]
+names = ["start", "inputs", "acc_free", "mma_done", "acc_ready", "published", "slab0_in_smem", "slab0_rows_done", "first_stage", "group0_done"]
 print(f"{a.config} B={a.batch}: wide levels {len(tiles)} (from d={d}), tiles {ntot}, span {x[5].max():.1f} us")
 print("medians (us): " + " ".join(f"{names[i]}->{names[j]}={np.median(x[j] - x[i]):.2f}"
-                                   for i, j in ((0, 1), (1, 8), (8, 3), (1, 3), (3, 4), (4, 5), (4, 6), (6, 7), (7, 5), (0, 5))))
-cyc = (buf[10, :ntot].astype(np.int64) - buf[9, :ntot].astype(np.int64))
+                                   for i, j in ((0, 1), (1, 8), (8, 3), (1, 3), (3, 4), (4, 5), (4, 6), (6, 9), (9, 7), (6, 7), (7, 5), (0, 5))))
+cyc = (buf[11, :ntot].astype(np.int64) - buf[10, :ntot].astype(np.int64))
 ns = (buf[3, :ntot].astype(np.int64) - buf[8, :ntot].astype(np.int64))
 okc = (ns > 0) & (cyc > 0)
 print(f"first_stage->mma_done: median {np.median(cyc[okc]):.0f} SM cycles, {np.median(ns[okc]) / 1e3:.2f} us, "
       f"implied SM clock {np.median(cyc[okc] / ns[okc]) * 1e3:.0f} MHz")
-print("level     M    N tiles |  first_start  max_inputs  max_mma_done  max_acc_ready  max_pub | period")
+print("level     M N*10+KS tiles |  first_start  max_inputs  max_mma_done  max_acc_ready  max_pub | period")
 T0, prev = 0, 0.0
 rows = []
 for (dd, M, N, nt) in tiles:
