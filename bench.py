@@ -57,6 +57,8 @@ def parse():
                     help="kernel classes bracketed by CUDA events inside the timed region: only the "
                          "roofline's tensor classes (default; the per-class breakdown then comes from "
                          "a separate profiled pass after it) or all classes")
+    ap.add_argument("--sched-bg-blocks", type=int, default=32,
+                    help="scheduler CTAs of a pipelined schedule that overlaps the weight-gradient GEMM")
     ap.add_argument("--no-c5-strong", action="store_true", help="N > 1: skip the C5 strong-scaling record")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-batch1", action="store_true")
@@ -291,7 +293,10 @@ def run_fold(args):
                 # persistent level kernels (which own every SM)
             for d, h in copies:
                 d.copy_(h, non_blocking=True)
-            sc = fold.schedule(op, child, token, root, V, workspace=sched_ws, stream=side, level=level, out=sbuf[i])
+            # gated (it overlaps the weight-gradient GEMM): a few scheduler CTAs leave the GEMM
+            # its SMs (fold_schedule_ex)
+            sc = fold.schedule(op, child, token, root, V, workspace=sched_ws, stream=side, level=level, out=sbuf[i],
+                               max_blocks=args.sched_bg_blocks if after is not None else 0)
             ev = torch.cuda.Event()
             ev.record(side)
         return sc, ev, i

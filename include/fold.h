@@ -55,7 +55,7 @@
 extern "C" {
 #endif
 
-#define FOLD_ABI_VERSION 5
+#define FOLD_ABI_VERSION 6
 
 typedef enum {
   FOLD_OK = 0,
@@ -162,6 +162,16 @@ size_t fold_schedule_workspace(int32_t n_nodes, int32_t n_graphs);
  * unspecified. Exactly one blocking D2H copy (two if n_levels + 2 > 4096). */
 fold_status fold_schedule(const fold_graphs *graphs, fold_schedule_t *sched,
                           void *d_workspace, size_t workspace_bytes, void *stream);
+
+/* fold_schedule with a cap on the scheduler's grid (CTAs of its cooperative kernel; 0 = the
+ * default sizing, values below 2 act as 2 on batches that need the cooperative kernel).
+ * Same outputs, bit for bit, for any cap. For a schedule that runs BESIDE other work (the
+ * next batch's schedule on a side stream overlapping this batch's weight-gradient GEMM,
+ * SURVEY §8(f) NEXT-4): a few CTAs leave the GEMM its SMs (C4 B=1024 step
+ * 21.5 -> 20.0-20.9 ms with 32 CTAs; C2 and C5 within noise). FOLD_E_INVALID if
+ * max_blocks < 0. */
+fold_status fold_schedule_ex(const fold_graphs *graphs, fold_schedule_t *sched,
+                             void *d_workspace, size_t workspace_bytes, void *stream, int32_t max_blocks);
 
 /* ----------------------------------------------------------------- model
  * Parameters are the caller's fp32 masters (device):

@@ -8,7 +8,8 @@
 
 namespace fold {
 
-fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws, size_t ws_bytes, cudaStream_t st);
+fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws, size_t ws_bytes, int max_blocks,
+                         cudaStream_t st);
 int debug_sched_trace(unsigned long long *host);
 size_t schedule_workspace(int64_t N, int64_t G);
 size_t mo_schedule_workspace(const fold_mo_table *t, int64_t N, int64_t G);
@@ -197,7 +198,14 @@ size_t fold_schedule_workspace(int32_t n_nodes, int32_t n_graphs) {
 fold_status fold_schedule(const fold_graphs *graphs, fold_schedule_t *sched, void *ws, size_t ws_bytes,
                           void *stream) {
   ProfScope ps(K_SCHED, (cudaStream_t)stream);
-  return run_schedule(graphs, sched, ws, ws_bytes, (cudaStream_t)stream);
+  return run_schedule(graphs, sched, ws, ws_bytes, 0, (cudaStream_t)stream);
+}
+
+fold_status fold_schedule_ex(const fold_graphs *graphs, fold_schedule_t *sched, void *ws, size_t ws_bytes,
+                             void *stream, int32_t max_blocks) {
+  ProfScope ps(K_SCHED, (cudaStream_t)stream);
+  if (max_blocks < 0) return FOLD_E_INVALID;
+  return run_schedule(graphs, sched, ws, ws_bytes, max_blocks, (cudaStream_t)stream);
 }
 
 fold_status fold_acts_layout(const fold_schedule_t *s, const fold_model *m, fold_acts_layout_t *out) {

@@ -1222,6 +1222,14 @@ __host__ __device__ inline int bwd_kps(int N, int bx0) {
 #ifndef FOLD_BW_ST
 #define FOLD_BW_ST 4
 #endif
+// rows per epilogue load group (FOLD_BWD_R build switch) and the one-wave-level L2 prefetch
+// of the pointwise operands (FOLD_BWD_PF1=0 disables it)
+#ifndef FOLD_BWD_R
+#define FOLD_BWD_R 4
+#endif
+#ifndef FOLD_BWD_PF1
+#define FOLD_BWD_PF1 0
+#endif
 // U (the B operand every tile of every level re-reads): TMA loads with an L2 evict_last
 // policy (FOLD_BWD_U_NOHINT build switch: none). With the evict-first epilogue loads:
 // C4 dA 11.7 -> 11.55 ms, C3 0.577 -> 0.563 ms
@@ -1535,7 +1543,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
       // c, dCe) while the tile's MMAs run: on latency-bound levels (chains) the epilogue's
       // HBM round trips are otherwise on every level's critical path (only on levels that
       // fit one wave of tiles: on wide levels the epilogue overlaps the next tile anyway)
-      if (my_valid && my_rows && cur.nt <= npairs) {
+      if (FOLD_BWD_PF1 && my_valid && my_rows && cur.nt <= npairs) {
 #pragma unroll 1
         for (int w = w0; w < own_n; w += wstep) {
           const int np = n0 + (own_lo + w) * 64;
@@ -1609,7 +1617,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         if (np - half * Sp < S) slab_cnt[half] += min(64, S - (np - half * Sp));
         // rows in groups of R: all loads of the group first (memory-level parallelism),
         // then the math and the stores
-        constexpr int R = 4;
+        constexpr int R = FOLD_BWD_R;
 #pragma unroll 1
         for (int i0 = i_lo; i0 < i_hi && c_row0 + i0 < c_end; i0 += R) {
           int xs_[R], xls[R], xrs[R];
@@ -1635,6 +1643,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
 #pragma unroll
               for (int g = 0; g < GATES; g++) graw[j][g] = BWD_LDG(reinterpret_cast<const uint32_t *>(gx + g * ld));
               if constexpr (GATES == 5) {
+#ifdef FOLD_DIAG_NOC  // diagnostic only (results invalid): the c operands are not loaded
+                cc[j] = make_float2(0.5f, 0.5f); cl[j] = cc[j]; cr[j] = cc[j];
+                dc[j] = BWD_LDC(reinterpret_cast<const float2 *>(dCe + e * S + col));
+              }
+              if constexpr (false) {
+#endif
                 cc[j] = BWD_LDC(reinterpret_cast<const float2 *>(C + (int64_t)xs_[j] * ld + col));
                 cl[j] = xls[j] >= nl ? BWD_LDC(reinterpret_cast<const float2 *>(C + (int64_t)xls[j] * ld + col))
                                      : make_float2(0.f, 0.f);

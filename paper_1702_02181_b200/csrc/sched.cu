@@ -912,7 +912,7 @@ int debug_sched_trace(unsigned long long *host) {
 
 size_t schedule_workspace(int64_t N, int64_t G) { return sched_ws_layout(nullptr, N, G).bytes; }
 
-fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr, size_t ws_bytes,
+fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr, size_t ws_bytes, int max_blocks_hint,
                          cudaStream_t st) {
   g_last_detail = -1;
   g_last_ctx[0] = g_last_ctx[1] = g_last_ctx[2] = -1;
@@ -970,6 +970,10 @@ fold_status run_schedule(const fold_graphs *gr, fold_schedule_t *s, void *ws_ptr
   }();
   int blocks = N <= small_n ? 1 : (int)cdiv(N, per_block);
   if (blocks > max_blocks) blocks = max_blocks;
+  // caller cap (fold_schedule_ex): a schedule that runs BESIDE other kernels (the next batch's,
+  // overlapping this batch's weight-gradient GEMM) takes few SMs; the cap never selects the
+  // one-block path, whose shared-memory frontier holds only small batches
+  if (max_blocks_hint > 0 && blocks > max_blocks_hint) blocks = max_blocks_hint < 2 ? 2 : max_blocks_hint;
   // one block: its depth propagation keeps pending counts and both frontiers in shared
   // memory (3N ints, at most 192 KB for kSmallN nodes)
   size_t launch_smem = dsmem;

@@ -95,6 +95,8 @@ def load() -> ctypes.CDLL:
     L.fold_schedule_workspace.argtypes = [i32, i32]
     L.fold_schedule.restype = i32
     L.fold_schedule.argtypes = [ctypes.POINTER(_Graphs), ctypes.POINTER(_Sched), vp, sz, vp]
+    L.fold_schedule_ex.restype = i32
+    L.fold_schedule_ex.argtypes = [ctypes.POINTER(_Graphs), ctypes.POINTER(_Sched), vp, sz, vp, i32]
     L.fold_acts_layout.restype = i32
     L.fold_acts_layout.argtypes = [ctypes.POINTER(_Sched), ctypes.POINTER(_Model), ctypes.POINTER(_ActsLayout)]
     L.fold_forward_workspace.restype = sz
@@ -155,7 +157,7 @@ def load() -> ctypes.CDLL:
     return L
 
 
-EXPORTED = ("fold_schedule_workspace", "fold_schedule", "fold_acts_layout", "fold_forward_workspace",
+EXPORTED = ("fold_schedule_workspace", "fold_schedule", "fold_schedule_ex", "fold_acts_layout", "fold_forward_workspace",
             "fold_forward", "fold_backward_workspace", "fold_backward", "fold_sgd_update",
             "fold_status_string", "fold_last_error_detail", "fold_last_error_context", "fold_abi_version", "fold_device_check",
             "fold_launch_count", "fold_profile_enable", "fold_profile_enable_classes", "fold_profile_read", "fold_debug_fwd_trace", "fold_debug_bwd_trace",
@@ -306,11 +308,12 @@ def schedule_buffer_len(n_nodes: int, n_graphs: int) -> int:
 
 def schedule(op: torch.Tensor, child: torch.Tensor, token: torch.Tensor, root: torch.Tensor, vocab: int,
              stream=None, workspace: torch.Tensor | None = None, level: torch.Tensor | None = None,
-             out: torch.Tensor | None = None) -> Schedule:
+             out: torch.Tensor | None = None, max_blocks: int = 0) -> Schedule:
     """fold_schedule over int32 device tensors op[N], child[N,2], token[N], root[G];
     `level` = optional caller-fixed levels [N] (manual batching, fold.h fold_graphs.level);
     `out` = optional int32 device buffer of schedule_buffer_len(N, G) elements for the
-    schedule arrays (else one is allocated)."""
+    schedule arrays (else one is allocated); `max_blocks` > 0 caps the scheduler's grid
+    (fold_schedule_ex: a schedule running beside other kernels)."""
     L = load()
     dev = op.device
     N, G = int(op.shape[0]), int(root.shape[0])
@@ -333,8 +336,12 @@ def schedule(op: torch.Tensor, child: torch.Tensor, token: torch.Tensor, root: t
                 level.data_ptr() if level is not None else None)
     base = buf.data_ptr()
     s = _Sched(*[base + 4 * offs[k][0] for k in _SCHED_ARRAYS], host.ctypes.data, 0, 0, 0, 0, 0, 0, 0)
-    _check(L.fold_schedule(ctypes.byref(g), ctypes.byref(s), ctypes.c_void_p(workspace.data_ptr()),
-                           ws_bytes, _stream(stream)), "fold_schedule")
+    if max_blocks:
+        _check(L.fold_schedule_ex(ctypes.byref(g), ctypes.byref(s), ctypes.c_void_p(workspace.data_ptr()),
+                                  ws_bytes, _stream(stream), int(max_blocks)), "fold_schedule_ex")
+    else:
+        _check(L.fold_schedule(ctypes.byref(g), ctypes.byref(s), ctypes.c_void_p(workspace.data_ptr()),
+                               ws_bytes, _stream(stream)), "fold_schedule")
     return Schedule(arrays, host, s.n_nodes, s.n_graphs, s.n_levels, s.n_leaves, s.n_cells, s.n_tok_segs,
                     bool(s.tree_like), _struct=s, _host_buf=host)
 

@@ -42,7 +42,7 @@ def test_library_host_only_calls():
     fbuild.build()
     from paper_1702_02181_b200 import fold
     L = fold.load()
-    assert L.fold_abi_version() == 5
+    assert L.fold_abi_version() == 6
     assert L.fold_status_string(6) == b"FOLD_E_CYCLE"
     assert L.fold_schedule_workspace(1000, 10) > 0
     assert L.fold_schedule_workspace(2_000_000, 8192) > L.fold_schedule_workspace(1000, 10)

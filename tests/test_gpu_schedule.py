@@ -141,3 +141,19 @@ def test_determinism():
     b = _gpu_sched(gr)
     for k in KEYS:
         assert np.array_equal(a[k], b[k])
+
+
+@pytest.mark.parametrize("name,B", [("c2", 64), ("c4", 32), ("c3", 1024)])
+def test_grid_cap_bit_exact(name, B):
+    """fold_schedule_ex: a capped scheduler grid (the pipelined schedule beside the dU GEMM)
+    gives the oracle's schedule bit for bit, for caps from 1 (acts as 2) to above the default."""
+    import torch
+    from paper_1702_02181_b200 import fold
+    gr = foldgen.make_config(name, B)
+    ref = oracle.schedule(gr.op, gr.child, gr.token, gr.root, gr.vocab)
+    op, child, token, root = fold.graphs_to_device(gr)
+    for cap in (1, 2, 3, 8, 16, 1000):
+        got = fold.schedule(op, child, token, root, gr.vocab, max_blocks=cap).to_numpy()
+        torch.cuda.synchronize()
+        for k in KEYS:
+            assert np.array_equal(np.asarray(got[k]), np.asarray(ref[k])), (cap, k)

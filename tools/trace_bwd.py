@@ -77,3 +77,16 @@ for i, r in enumerate(rows):
     if i < a.levels or i >= len(rows) - 3:
         print(f"{r[0]:5d} {r[1]:6d} {r[2]:4d} {r[3]:5d} | {r[4]:11.1f} {r[5]:11.1f} {r[6]:13.1f} {r[7]:14.1f} {r[8]:8.1f} | "
               f"{r[8] - (rows[i - 1][8] if i else 0):6.1f}")
+# per-level phase medians (us): MMA (first stage -> accumulator committed), the MMA warp's wait
+# for a free accumulator (start -> acc_free), the epilogue (accumulator ready -> published) and
+# the epilogue's wait on the accumulator of the tile (previous tile published -> acc ready)
+print("level tiles | mma(first_stage->mma_done) acc_wait(start->acc_free) epi(acc_ready->published) "
+      "slab_rows(slab0_in_smem->rows_done) inputs_wait(start->inputs)")
+T0 = 0
+for (dd, M, N, nt) in tiles:
+    if T0 + nt > ntot:
+        break
+    sl = slice(T0, T0 + nt)
+    med = lambda i, j: float(np.median(x[j][sl] - x[i][sl]))
+    print(f"{dd:5d} {nt:5d} | {med(8, 3):8.2f} {med(0, 2):8.2f} {med(4, 5):8.2f} {med(6, 7):8.2f} {med(0, 1):8.2f}")
+    T0 += nt
