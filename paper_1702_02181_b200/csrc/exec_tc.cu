@@ -1569,10 +1569,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         }
       }
       int slab_cnt[2] = {0, 0};  // columns this warp completes (its 64-column slabs), per half
+#if defined(FOLD_BWD_TFULL_SPIN)
+      while (!ptx::mbar_test(&tfull[acc], (tc >> 1) & 1)) {}
+#elif defined(FOLD_BWD_TFULL_SLEEP)
+      ptx::mbar_wait_sleep(&tfull[acc], (tc >> 1) & 1);
+#else
       ptx::mbar_wait(&tfull[acc], (tc >> 1) & 1);
+#endif
       ptx::tc_fence_after();
       if (warp == 4 && lane == 0 && rank == 0) btrace(dbg, 4, T);
       const uint32_t tl = tbase + acc * 256 + ((uint32_t)(q * 32) << 16);
+#ifdef FOLD_DBG_TMEM  // diagnostic: stamp 9 = one probe TMEM load (8 columns) complete
+      {
+        float t8[8];
+        ptx::tmem_ld8(tl, t8);
+        ptx::tmem_ld_wait();
+        if (warp == 4 && lane == 0 && rank == 0) btrace(dbg, 9, T + (t8[0] == 12345.f));
+      }
+#endif
       // split-K, phase A: the partner's slabs' partial sums -> this unit's ring slot (fp32,
       // [CTA rank][128 rows][128 columns], rows through the transpose buffer so each store
       // is a coalesced row segment); every epilogue warp of the pair then raises the slot's
@@ -1708,7 +1722,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
               if (xrs[j] >= nl) *reinterpret_cast<float2 *>(dCe + (2 * xc + 1) * S + col) = make_float2(er[0], er[1]);
             }
           }
+#ifndef FOLD_DBG_TMEM
           if (warp == 4 && lane == 0 && rank == 0 && w == w0 && i0 == i_lo) btrace(dbg, 9, T);
+#endif
         }
         __syncwarp();
         if (warp == 4 && lane == 0 && rank == 0 && w == w0) btrace(dbg, 7, T);

@@ -453,6 +453,9 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
       if (o == FOLD_OP_EMBED || good_cell) atomicMax(&flags[F_MAXDEPTH], lv < 1 ? 1 : lv);
     }
     w.pending[n] = (o == FOLD_OP_CELL) ? (good_cell ? 2 : kPendingInvalid) : 0;
+    // tree-like depth walk (P4): no parent yet, empty arrival slot (sort scratch, free until P5)
+    reinterpret_cast<int32_t *>(w.kb)[n] = -1;
+    w.va[n] = -1;
   }
   for (int64_t g = gtid; g < G; g += gstride)
     if (a.root[g] < 0 || a.root[g] >= N) atomicMin(&flags[F_ERR0 + E_ROOT], (int)g);
@@ -476,6 +479,9 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
         if (o == FOLD_OP_CELL) {
           w.pcons[w.pcons_off[c0] + atomicAdd(&w.fillc[c0], 1)] = n;
           w.pcons[w.pcons_off[c1] + atomicAdd(&w.fillc[c1], 1)] = n;
+          // the parent of each child (meaningful when every node has <= 1 consumer edge)
+          reinterpret_cast<int32_t *>(w.kb)[c0] = n;
+          reinterpret_cast<int32_t *>(w.kb)[c1] = n;
         }
         leaf = (o == FOLD_OP_EMBED);
         s.depth[n] = a.level ? a.level[n] : (leaf ? 1 : -1);
@@ -524,6 +530,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
       __syncthreads();
     }
   }
+#ifdef FOLD_SCHED_LEVELSYNC  // the level-synchronous frontier (one grid barrier per level)
   for (; !a.level && gridDim.x > 1; L++) {
     const int ncur = ld_volatile(&flags[F_QCNT + (L % 3)]);
     if (ncur == 0) break;
@@ -549,7 +556,91 @@ __global__ void __launch_bounds__(kSchedThreads) k_schedule(SchedArgs a) {
     }
     gsync(flags);
   }
+#else
+  // Many blocks: asynchronous propagation by last arrival, no barrier per level. A thread
+  // takes a node whose depth is final and decrements each parent's pending count (release:
+  // fence, then the atomic); the thread that brings a parent to 0 (acquire: the atomic, then a
+  // fence) reads its children's depths and sets depth = 1 + max (L40: the same value the
+  // level-synchronous frontier gives, whose last finishing child has the largest depth), then
+  // walks on from that parent. Trees: every walk ends at a parent another walk completes, so
+  // the whole depth pass is ONE barrier; the chain of a depth-256 caterpillar is walked by one
+  // thread (C4 B=1024 P4 1203 us with a barrier per level). DAGs: a node completing several
+  // parents walks one and queues the rest for the next round (a barrier per round).
+  if (!a.level && gridDim.x > 1 && ld_volatile(&flags[F_SHARED]) == 0) {
+    // tree-like batches (every node read by <= 1 edge): a node's parent is unique (kb), and its
+    // two children meet in an exchange slot (va, -1 = empty): the first arriver leaves its depth
+    // there, the second gets it back from the same atomic and continues with
+    // 1 + max(both). The depth travels inside the atomic, so no fence or depth load is on the
+    // walk; the parent's parent is loaded while the exchange is in flight (one L2 round trip
+    // per tree level).
+    const int32_t *par = reinterpret_cast<const int32_t *>(w.kb);
+    const int n0 = ld_volatile(&flags[F_QCNT + 1]);
+    int dmax = n0 > 0 ? 1 : 0;
+    for (int64_t i = gtid; i < n0; i += gstride) {
+      int dx = 1;
+      int p = __ldcg(&par[w.q0[i]]);
+      while (p >= 0) {
+        const int pp = __ldcg(&par[p]);
+        const int other = atomicExch(&w.va[p], dx);
+        if (other < 0) break;  // the sibling is not done: it continues from p
+        dx = 1 + (other > dx ? other : dx);
+        s.depth[p] = dx;
+        if (dx > dmax) dmax = dx;
+        p = pp;
+      }
+    }
+    if (dmax > 0) atomicMax(&flags[F_MAXDEPTH], dmax);
+    gsync(flags);
+  } else if (!a.level && gridDim.x > 1) {
+    int dmax = 0;
+    for (int r = 1;; r++) {
+      const int ncur = ld_volatile(&flags[F_QCNT + (r % 3)]);
+      if (ncur == 0) break;
+      const int32_t *src = (r & 1) ? w.q0 : w.q1;
+      int32_t *ovf = (r & 1) ? w.q1 : w.q0;
+      if (gtid == 0) flags[F_QCNT + ((r + 2) % 3)] = 0;
+      for (int64_t i = gtid; i < ncur; i += gstride) {
+        int x = src[i];
+        int dx = r == 1 ? 1 : __ldcg(&s.depth[x]);  // round 1: the leaves (depth 1)
+        if (dx > dmax) dmax = dx;
+        for (;;) {
+          int next = -1, dnext = 0;
+          const int e0 = __ldcg(&w.pcons_off[x]), e1 = __ldcg(&w.pcons_off[x + 1]);
+          for (int e = e0; e < e1; e++) {
+            const int p = __ldcg(&w.pcons[e]);
+            const int c0 = __ldg(&a.child[2 * p]), c1 = __ldg(&a.child[2 * p + 1]);
+            __threadfence();
+            if (atomicSub(&w.pending[p], 1) != 1) continue;
+            __threadfence();
+            const int d0 = c0 == x ? dx : __ldcg(&s.depth[c0]);
+            const int d1 = c1 == x ? dx : __ldcg(&s.depth[c1]);
+            const int dp = 1 + (d0 > d1 ? d0 : d1);
+            s.depth[p] = dp;
+            if (next < 0) {
+              next = p;
+              dnext = dp;
+            } else {  // a second completed parent (shared node): the next round walks it
+              __threadfence();
+              ovf[atomicAdd(&flags[F_QCNT + ((r + 1) % 3)], 1)] = p;
+            }
+          }
+          if (next < 0) break;
+          x = next;
+          dx = dnext;
+          if (dx > dmax) dmax = dx;
+        }
+      }
+      gsync(flags);
+    }
+    if (dmax > 0) atomicMax(&flags[F_MAXDEPTH], dmax);
+    gsync(flags);
+  }
+#endif
+#ifdef FOLD_SCHED_LEVELSYNC
   const int D = a.level ? ld_volatile(&flags[F_MAXDEPTH]) : L - 1;
+#else
+  const int D = (a.level || gridDim.x > 1) ? ld_volatile(&flags[F_MAXDEPTH]) : L - 1;
+#endif
   if (gtid == 0 && !a.level) flags[F_MAXDEPTH] = D;
 
   sched_stamp(a.dbg, 5);

@@ -81,12 +81,12 @@ for i, r in enumerate(rows):
 # for a free accumulator (start -> acc_free), the epilogue (accumulator ready -> published) and
 # the epilogue's wait on the accumulator of the tile (previous tile published -> acc ready)
 print("level tiles | mma(first_stage->mma_done) acc_wait(start->acc_free) epi(acc_ready->published) "
-      "slab_rows(slab0_in_smem->rows_done) inputs_wait(start->inputs)")
+      "slab_rows(slab0_in_smem->rows_done) inputs_wait(start->inputs) acc_ready->slab0_in_smem acc_ready->pt9")
 T0 = 0
 for (dd, M, N, nt) in tiles:
     if T0 + nt > ntot:
         break
     sl = slice(T0, T0 + nt)
     med = lambda i, j: float(np.median(x[j][sl] - x[i][sl]))
-    print(f"{dd:5d} {nt:5d} | {med(8, 3):8.2f} {med(0, 2):8.2f} {med(4, 5):8.2f} {med(6, 7):8.2f} {med(0, 1):8.2f}")
+    print(f"{dd:5d} {nt:5d} | {med(8, 3):8.2f} {med(0, 2):8.2f} {med(4, 5):8.2f} {med(6, 7):8.2f} {med(0, 1):8.2f} {med(4, 6):8.2f} {med(4, 9):8.2f}")
     T0 += nt
