@@ -312,6 +312,13 @@ const char *fold_status_string(fold_status s);
 /* Detail of the last data-dependent error on this thread: the offending node (or
  * graph) id, -1 if none. */
 int32_t fold_last_error_detail(void);
+/* The persistent level kernels of fold_forward / fold_backward (BF16) leave n SMs free (rounded
+ * up to CTA pairs; default 0) for work on other streams: the next batch's fold_schedule,
+ * launched beside a small batch's latency-bound levels, then runs on those SMs instead of
+ * waiting for the level kernels to finish. Process-wide, read at each launch;
+ * returns the previous value; n < 0 acts as 0. Results do not depend on it. */
+int32_t fold_set_reserved_sms(int32_t n);
+
 /* (node, depth, op) context of the last data-dependent fold_schedule error on this thread
  * (errors carry the depth and operation): node = the offending node (graph id
  * for FOLD_E_ROOT_RANGE); op = that node's op[] value as given (-1 for ROOT_RANGE); depth =

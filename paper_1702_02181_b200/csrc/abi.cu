@@ -484,6 +484,8 @@ fold_status fold_last_error_context(int32_t *node, int32_t *depth, int32_t *op) 
 }
 int32_t fold_abi_version(void) { return FOLD_ABI_VERSION; }
 
+int32_t fold_set_reserved_sms(int32_t n) { return set_reserved_sms(n); }
+
 // ----------------------------------------------------------------- multi-op (fold_mo.h)
 size_t fold_mo_schedule_workspace(const fold_mo_table *table, int32_t n_nodes, int32_t n_graphs) {
   return fold::mo_schedule_workspace(table, n_nodes, n_graphs);

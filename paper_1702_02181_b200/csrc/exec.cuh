@@ -141,6 +141,7 @@ fold_status tc_gemm_dA(int c0, int M, int n_cells, int S, int gates, const __nv_
                        const __nv_bfloat16 *Ub, float *dA, cudaStream_t st);
 // split-K over cells into split_ws [splits][gates*S][2S] (fp32), then a fixed-order sum
 int tc_dU_splits(int n_cells, int gates, int S);
+int set_reserved_sms(int n);  // fold_set_reserved_sms
 fold_status tc_gemm_dU(int n_cells, int S, int gates, const __nv_bfloat16 *dZ, int ld_z, const ScatterA &sc,
                        float *dU, int accumulate, float *split_ws, float *db, float *db_ws,
                        cudaStream_t st);

@@ -22,6 +22,7 @@
 // Warp roles: warp 0 TMA producer (both CTAs), warp 1 MMA issuer (leader CTA, one lane),
 // warp 2 TMEM allocator, warp 3 idle, warps 4.. epilogue (warp w reads TMEM lanes
 // 32 (w % 4) .. +31 of its own CTA).
+#include <atomic>
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
@@ -2435,6 +2436,13 @@ int num_sms() {
   return n[dev];
 }
 
+// SMs the persistent level kernels leave free for concurrent work (fold_set_reserved_sms)
+std::atomic<int> g_reserved_sms{0};
+int reserve_pairs(int npairs) {
+  const int r = npairs - (g_reserved_sms.load(std::memory_order_relaxed) + 1) / 2;
+  return r < 1 ? 1 : r;
+}
+
 // Max co-resident CTA pairs of a kernel (the persistent kernels' spin waits need every CTA
 // of the grid resident: the grid never exceeds this).
 template <typename K>
@@ -2515,8 +2523,9 @@ fold_status launch_fwd_levels(const TcFwdArgs &a, cudaStream_t st) {
   const int smem_bytes = Cfg::SMEM;
   FOLD_TRY(set_smem(kern, smem_bytes));
   static thread_local int npairs_dev[kMaxDevices] = {};
-  int &npairs_max = npairs_dev[cur_dev()];
-  if (!npairs_max) npairs_max = max_pairs(kern, Cfg::THREADS, smem_bytes);
+  int &npairs_dev_max = npairs_dev[cur_dev()];
+  if (!npairs_dev_max) npairs_dev_max = max_pairs(kern, Cfg::THREADS, smem_bytes);
+  const int npairs_max = reserve_pairs(npairs_dev_max);
   FwdLevels L{a.level_off, a.D, S, Cfg::WMAX, Cfg::WNAR, npairs_max / 2, Cfg::WMID, GATES, npairs_max,
               l2_prefetch_dist("FOLD_PF_FWD")};
   // the narrow tail: levels d0..D all of at most narrow_max rows go to k_fwd_narrow
@@ -2741,8 +2750,9 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
   auto kern = gates == 5 ? k_bwd_levels<5> : k_bwd_levels<1>;
   FOLD_TRY(set_smem(kern, BW_SMEM));
   static thread_local int npairs_dev[kMaxDevices] = {};
-  int &npairs_max = npairs_dev[cur_dev()];
-  if (!npairs_max) npairs_max = max_pairs(kern, BW_THREADS, BW_SMEM);
+  int &npairs_dev_max = npairs_dev[cur_dev()];
+  if (!npairs_dev_max) npairs_dev_max = max_pairs(kern, BW_THREADS, BW_SMEM);
+  const int npairs_max = reserve_pairs(npairs_dev_max);
   // the narrow top: levels D..d1 (all of at most FOLD_BWD_NARROW_MAX rows) run first in
   // k_bwd_narrow, the wide kernel takes levels d1-1..2
   const int d1 = bwd_narrow_start(a.level_off_host, a.D, S, gates);
@@ -2882,5 +2892,7 @@ fold_status tc_gemm_dU(int n_cells, int S, int gates, const __nv_bfloat16 *dZ, i
   if (db) FOLD_TRY(launch_reduce_splits((int64_t)gates * S, splits, db_ws, db, accumulate, st));
   return FOLD_OK;
 }
+
+int set_reserved_sms(int n) { return g_reserved_sms.exchange(n < 0 ? 0 : n); }
 
 }  // namespace fold

@@ -95,6 +95,8 @@ def load() -> ctypes.CDLL:
     L.fold_schedule_workspace.argtypes = [i32, i32]
     L.fold_schedule.restype = i32
     L.fold_schedule.argtypes = [ctypes.POINTER(_Graphs), ctypes.POINTER(_Sched), vp, sz, vp]
+    L.fold_set_reserved_sms.restype = i32
+    L.fold_set_reserved_sms.argtypes = [i32]
     L.fold_schedule_ex.restype = i32
     L.fold_schedule_ex.argtypes = [ctypes.POINTER(_Graphs), ctypes.POINTER(_Sched), vp, sz, vp, i32]
     L.fold_acts_layout.restype = i32
@@ -157,7 +159,7 @@ def load() -> ctypes.CDLL:
     return L
 
 
-EXPORTED = ("fold_schedule_workspace", "fold_schedule", "fold_schedule_ex", "fold_acts_layout", "fold_forward_workspace",
+EXPORTED = ("fold_schedule_workspace", "fold_schedule", "fold_schedule_ex", "fold_set_reserved_sms", "fold_acts_layout", "fold_forward_workspace",
             "fold_forward", "fold_backward_workspace", "fold_backward", "fold_sgd_update",
             "fold_status_string", "fold_last_error_detail", "fold_last_error_context", "fold_abi_version", "fold_device_check",
             "fold_launch_count", "fold_profile_enable", "fold_profile_enable_classes", "fold_profile_read", "fold_debug_fwd_trace", "fold_debug_bwd_trace",
@@ -215,6 +217,11 @@ def _ptr(t: torch.Tensor | None):
 def _stream(stream=None):
     s = stream if stream is not None else torch.cuda.current_stream()
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def set_reserved_sms(n: int) -> int:
+    """fold_set_reserved_sms: SMs the persistent level kernels leave free (returns the old value)."""
+    return int(load().fold_set_reserved_sms(int(n)))
 
 
 def device_check():
