@@ -157,3 +157,24 @@ def test_grid_cap_bit_exact(name, B):
         torch.cuda.synchronize()
         for k in KEYS:
             assert np.array_equal(np.asarray(got[k]), np.asarray(ref[k])), (cap, k)
+
+
+@pytest.mark.parametrize("N,seed", [(6000, 1), (20000, 2), (9000, 3)])
+def test_multiblock_dag_walk(N, seed):
+    """DAGs large enough for the cooperative scheduler (> 4096 nodes): the depth walk with
+    pending counts and overflow rounds (shared nodes, cell(x, x)) on shuffled ids, bit-exact
+    with the oracle, five times over (a race in the walk would show as a flipped depth)."""
+    rng = np.random.default_rng(seed)
+    gr = random_dag(rng, N, 50)
+    gr = foldgen.permute_nodes(gr, rng.permutation(gr.n_nodes))
+    for _ in range(5):
+        _compare(gr)
+
+
+@pytest.mark.parametrize("name,B", [("c4", 64), ("c2", 128), ("c5", 64)])
+def test_multiblock_tree_walk_repeat(name, B):
+    """Tree-like batches through the exchange-slot walk, repeated with shuffled ids."""
+    rng = np.random.default_rng(7)
+    gr = foldgen.make_config(name, B)
+    _compare(gr)
+    _compare(foldgen.permute_nodes(gr, rng.permutation(gr.n_nodes)))
