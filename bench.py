@@ -57,8 +57,10 @@ def parse():
                     help="kernel classes bracketed by CUDA events inside the timed region: only the "
                          "roofline's tensor classes (default; the per-class breakdown then comes from "
                          "a separate profiled pass after it) or all classes")
-    ap.add_argument("--reserve-sms", type=int, default=16,
+    ap.add_argument("--reserve-sms", type=int, default=24,
                     help="SMs the level kernels leave to a small batch's pipelined schedule")
+    ap.add_argument("--reserve-max-work", type=float, default=2e10,
+                    help="largest nodes x S^2 whose pipelined schedule gets --reserve-sms SMs")
     ap.add_argument("--sched-bg-blocks", type=int, default=32,
                     help="scheduler CTAs of a pipelined schedule that overlaps the weight-gradient GEMM")
     ap.add_argument("--no-c5-strong", action="store_true", help="N > 1: skip the C5 strong-scaling record")
@@ -258,11 +260,13 @@ def run_fold(args):
         side = side_stream if args.pipeline != "off" else None
         small = n_nodes <= pipe_max_nodes and n_levels <= 64
         gate[0] = None if small else sweep_done
-        # a small batch's next schedule starts right away: below 32768 nodes the level kernels
-        # (latency-bound there) leave it SMs so it runs beside them (fold_set_reserved_sms;
-        # measured with 16 SMs: C2 B=64 0.924 -> 0.83 ms; C3 B=1024 (60k nodes) within noise,
-        # C2 B=256 (65k) +2%, so larger batches reserve none)
-        fold.set_reserved_sms(args.reserve_sms if (small and side is not None and n_nodes <= 32768) else 0)
+        # a small batch's next schedule starts right away: when the level kernels have little
+        # GEMM work (~ nodes x S^2 <= args.reserve_max_work; they are latency-bound there) they
+        # leave it SMs so it runs beside them (fold_set_reserved_sms; measured with 24 SMs:
+        # C3 B=1024 1.135 -> 1.077 ms, C2 B=64 0.924 -> 0.91 ms; C2 B=256 (6.8e10) +7%, so
+        # larger work reserves none; 16 SMs: C2 B=64 0.83 ms but C3 1.15 ms)
+        fold.set_reserved_sms(args.reserve_sms if (small and side is not None
+                                                   and n_nodes * S * S <= args.reserve_max_work) else 0)
         return side is not None
 
     sweep_done = torch.cuda.Event()  # re-recorded by every fold_backward after its level sweep
