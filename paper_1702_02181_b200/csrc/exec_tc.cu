@@ -1570,17 +1570,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         }
       }
       int slab_cnt[2] = {0, 0};  // columns this warp completes (its 64-column slabs), per half
-#if defined(FOLD_BWD_TFULL_SPIN)
-      while (!ptx::mbar_test(&tfull[acc], (tc >> 1) & 1)) {}
-#elif defined(FOLD_BWD_TFULL_SLEEP)
-      ptx::mbar_wait_sleep(&tfull[acc], (tc >> 1) & 1);
-#else
       ptx::mbar_wait(&tfull[acc], (tc >> 1) & 1);
-#endif
       ptx::tc_fence_after();
       if (warp == 4 && lane == 0 && rank == 0) btrace(dbg, 4, T);
       const uint32_t tl = tbase + acc * 256 + ((uint32_t)(q * 32) << 16);
-#ifdef FOLD_DBG_TMEM  // diagnostic: stamp 9 = one probe TMEM load (8 columns) complete
+#ifdef FOLD_DBG_TMEM  // diagnostic (DESIGN §15): stamp 9 = one probe TMEM load (8 columns) complete
       {
         float t8[8];
         ptx::tmem_ld8(tl, t8);
@@ -1658,7 +1652,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
 #pragma unroll
               for (int g = 0; g < GATES; g++) graw[j][g] = BWD_LDG(reinterpret_cast<const uint32_t *>(gx + g * ld));
               if constexpr (GATES == 5) {
-#ifdef FOLD_DIAG_NOC  // diagnostic only (results invalid): the c operands are not loaded
+#ifdef FOLD_DIAG_NOC  // diagnostic only (results invalid, DESIGN §15): the c operands are not loaded
                 cc[j] = make_float2(0.5f, 0.5f); cl[j] = cc[j]; cr[j] = cc[j];
                 dc[j] = BWD_LDC(reinterpret_cast<const float2 *>(dCe + e * S + col));
               }
