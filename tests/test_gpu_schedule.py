@@ -178,3 +178,13 @@ def test_multiblock_tree_walk_repeat(name, B):
     gr = foldgen.make_config(name, B)
     _compare(gr)
     _compare(foldgen.permute_nodes(gr, rng.permutation(gr.n_nodes)))
+
+
+@pytest.mark.parametrize("leaves,B", [(3000, 1), (1200, 3)])
+def test_multiblock_deep_chains(leaves, B):
+    """Caterpillars deeper than any bench config (depth 3000, one chain walked by one thread in
+    the cooperative scheduler), mixed with shuffled ids: bit-exact with the oracle."""
+    rng = np.random.default_rng(leaves)
+    gr = foldgen.config_c4(B, leaves=leaves)
+    _compare(gr)
+    _compare(foldgen.permute_nodes(gr, rng.permutation(gr.n_nodes)))
