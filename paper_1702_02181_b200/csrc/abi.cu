@@ -66,6 +66,7 @@ struct BwdWs {
   int32_t *tstart;  // [n_cells]
   float *ks_ring;   // its split-K hand-over slots (BF16 path)
   int *ks_cnt;
+  int *lvl_tab;     // the wide backward's per-level tile tables (tc_bwd_lvl_tab_ints)
   EmbedBwdWs emb;
   void *dZ;
   __nv_bfloat16 *Ub, *Ut;
@@ -104,6 +105,7 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
   b.tf_split_floats = tf_split;
   size_t o_spl = take(splits > 1 ? (size_t)splits * gates * S * 2 * S * 4 : (size_t)tf_split * 4);
   size_t o_ksr = take(bf16 ? tc_ks_ring_bytes() : 0), o_ksc = take(bf16 ? (size_t)2 * kKsRing * 4 : 0);
+  size_t o_lvt = take(bf16 ? (size_t)tc_bwd_lvl_tab_ints(s->n_levels) * 4 : 0);
   b.bytes = off;
   if (base) {
     char *p = (char *)base;
@@ -125,6 +127,7 @@ BwdWs bwd_layout(void *base, const fold_schedule_t *s, const fold_model *m) {
     b.Ut = bf16 ? (__nv_bfloat16 *)(p + o_ut) : nullptr;
     b.ks_ring = bf16 ? (float *)(p + o_ksr) : nullptr;
     b.ks_cnt = bf16 ? (int *)(p + o_ksc) : nullptr;
+    b.lvl_tab = bf16 ? (int *)(p + o_lvt) : nullptr;
   }
   return b;
 }
@@ -357,7 +360,7 @@ fold_status fold_backward(const fold_schedule_t *s, const fold_model *m, const v
     ba.D = D; ba.S = S; ba.nl = nl; ba.n_cells = nc; ba.ld = L.ld; ba.ld_g = L.ld_g; ba.ld_z = b.ld_z;
     ba.gather = s->gather; ba.Ub = b.Ub; ba.U = m->U; ba.Ut = b.Ut; ba.Gact = (const __nv_bfloat16 *)Gact; ba.C = C;
     ba.dA = b.dA; ba.dCe = b.dCe; ba.dZ = (__nv_bfloat16 *)b.dZ; ba.rt_cnt = b.rt_cnt; ba.tstart = b.tstart;
-    ba.ks_ring = b.ks_ring; ba.ks_cnt = b.ks_cnt;
+    ba.ks_ring = b.ks_ring; ba.ks_cnt = b.ks_cnt; ba.lvl_tab = b.lvl_tab;
     {
       ProfScope ps(K_BWD_PW, st);
       FOLD_TRY(launch_cell_bwd_pw(bf16, m->cell, 0, G, nl, S, L.ld, L.ld_g, s->cons_off, s->cons_edge, b.root_off,

@@ -129,7 +129,11 @@ struct TcBwdArgs {
   int32_t *tstart;   // [n_cells] first cell of each cell's row tile
   float *ks_ring;    // [kKsRing][kKsSlotFloats] split-K hand-over slots (k_bwd_levels)
   int *ks_cnt;       // [2 * kKsRing] their written / read counts (zeroed by tc_bwd_prelude)
+  int *lvl_tab;      // [tc_bwd_lvl_tab_ints(D)] per-level tile tables of k_bwd_levels
 };
+// per level d <= D: three int4 (critical units, deferred tiles run inline, deferred tiles run
+// at the end) and one flag word, + the total
+inline int64_t tc_bwd_lvl_tab_ints(int64_t D) { return (D + 2) * 13 + 8; }
 // split-K hand-over ring of the wide backward (see k_bwd_levels)
 constexpr int kKsRing = 256;
 constexpr int kKsSlotFloats = 2 * 128 * 128;

@@ -1159,41 +1159,45 @@ struct BwdLevels {
   int ksplit_max;    // split-K units allowed per level (0: no split; else the number of CTA pairs)
   int KB;            // k-blocks of the full K = GATES*S reduction
   int ks256;         // split-K also for 256-column tiles
+  // per-level tile tables (k_bwd_tiles): per level D..2 its critical units, then some of its
+  // deferred (leaf-children-only) column tiles inline; after all levels the rest of the
+  // deferred tiles of levels D..2. x = first unit, y = units, z = N / 128 | KS << 2 | v << 4
+  // (critical entries: v = the level's first split-unit ordinal; deferred entries: their first
+  // level-local tile), w = first column tile | column tiles << 16
+  const int4 *tcrit, *tinl, *tend;
+  const int *total;  // units in all sections
 };
-// Per-level tiling: N (128 or 256 columns) and KS (1, or 2 = split-K in two k-halves). A
-// latency-bound level that fits one wave of CTA pairs twice over runs each tile as two
-// k-half units on two pairs: each pair accumulates half of the K = GATES*S reduction, hands
-// the partial of the OTHER half's columns to its partner through L2 (ring slots) and
-// finishes its own half of the columns, so a level's mainloop and epilogue both halve.
-struct BwdCfg {
-  int N, KS;
-};
-__host__ __device__ inline BwdCfg bwd_level_cfg(const BwdLevels &L, int M) {
-  const int rt = (int)cdiv(M, PM), t256 = rt * (int)cdiv(L.ld_u, 256), t128 = rt * (int)cdiv(L.ld_u, 128);
-  if (L.ksplit_max > 0 && L.KB >= 8) {
-    if (2 * t128 <= L.ksplit_max) return {128, 2};
-    if (L.ks256 && 2 * t256 <= L.ksplit_max) return {256, 2};
-  }
-  return {t256 < L.narrow_below ? 128 : 256, 1};
-}
-struct BwdCursor {  // walks levels D, D-1, ..., 2 in tile order
-  int d, t0, nt, r0, r1, N, NTn, KS;
+// Per-level tiling (k_bwd_tiles): N (128 or 256 columns) and KS (1, or 2 = split-K in two
+// k-halves). A latency-bound level whose critical tiles fit one wave of CTA pairs twice over
+// runs each tile as two k-half units on two pairs: each pair accumulates half of the
+// K = GATES*S reduction, hands the partial of the OTHER half's columns to its partner through
+// L2 (ring slots) and finishes its own half of the columns, so a level's mainloop and
+// epilogue both halve.
+struct BwdCursor {  // per level D..2: critical units, inline deferred tiles; then the end section
+  int d, t0, nt, r0, r1, N, NTn, KS, ctlo, lt_off, sbase, sec;
   __device__ void load(const BwdLevels &L) {
     r0 = __ldg(L.lo + d); r1 = __ldg(L.lo + d + 1);
-    const BwdCfg c = bwd_level_cfg(L, r1 - r0);
-    N = c.N;
-    KS = c.KS;
-    NTn = (int)cdiv(L.ld_u, N);
-    nt = (int)cdiv(r1 - r0, PM) * NTn * KS;
+    const int4 c = sec == 0 ? L.tcrit[d] : sec == 1 ? L.tinl[d] : L.tend[d];
+    t0 = c.x; nt = c.y; N = (c.z & 3) * 128; KS = (c.z >> 2) & 3;
+    lt_off = sec == 0 ? 0 : c.z >> 4;  // critical entries carry the split ordinal base instead
+    sbase = sec == 0 ? c.z >> 4 : 0;
+    ctlo = c.w & 0xffff; NTn = c.w >> 16;
   }
-  __device__ void init(const BwdLevels &L) { d = L.D; t0 = 0; load(L); }
+  __device__ void init(const BwdLevels &L) { d = L.D; sec = 0; load(L); }
   __device__ void seek(const BwdLevels &L, int T) {
-    while (T >= t0 + nt) { t0 += nt; d--; load(L); }
+    while (T >= t0 + nt) {
+      if (sec == 0) sec = 1;
+      else if (sec == 1) {
+        if (--d < 2) { sec = 2; d = L.D; }
+        else sec = 0;
+      } else if (--d < 2) return;  // past the last unit (callers stay below *L.total)
+      load(L);
+    }
   }
-  // level-local tile lt = ((row tile) * NTn + column tile) * KS + k-half
-  __device__ int row_tile(int lt) const { return lt / (NTn * KS); }
-  __device__ int col_tile(int lt) const { return (lt / KS) % NTn; }
-  __device__ int khalf(int lt) const { return lt % KS; }
+  // level-local unit lt = ((row tile) * NTn + column tile - ctlo) * KS + k-half
+  __device__ int row_tile(int lt) const { return (lt + lt_off) / (NTn * KS); }
+  __device__ int col_tile(int lt) const { return ctlo + ((lt + lt_off) / KS) % NTn; }
+  __device__ int khalf(int lt) const { return (lt + lt_off) % KS; }
   __device__ int first_cell(const BwdLevels &L, int lt) const { return (r0 - L.nl) + row_tile(lt) * PM; }
   // k-block range of tile lt: the whole K, or one half of it
   __device__ void krange(const BwdLevels &L, int lt, int &k0, int &k1) const {
@@ -1248,7 +1252,8 @@ constexpr int BW_THREADS = 128 + 32 * BW_EPI;
 // took leaves room for a fifth pipeline stage
 constexpr int BW_XS = 32 * 64;
 // split-K hand-over ring: kKsRing slots of [2 CTAs][128 rows][128 columns] fp32 partial sums;
-// slot T % kKsRing holds unit T's partial (use T / kKsRing), with a written count and a read
+// split unit o (its ordinal among the split units, k_bwd_tiles) uses slot o % kKsRing (use
+// o / kKsRing), with a written count and a read
 // count per slot (k_bwd_levels waits for the previous use's read before reusing a slot)
 constexpr int BW_SMEM = BW_ST * DA_STAGE + BW_EPI * BW_XS * 4 + 1024;
 
@@ -1261,6 +1266,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
                  float *dCe, __nv_bfloat16 *dZ, int ld_z, int *rt_cnt, const int32_t *__restrict__ tstart,
                  int slabs, int dbg, float *ks_ring, int *ks_wr, int *ks_cons) {
   constexpr int ST = BW_ST;
+  total_tiles = min(total_tiles, __ldg(L.total));  // the host passes an upper bound
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = align1024(smem_raw);
   float *xs_all = reinterpret_cast<float *>(smem + ST * DA_STAGE);
@@ -1589,7 +1595,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
       const float *pp = nullptr;
       int pslot = 0;
       if (KS == 2) {
-        const int slot = T % kKsRing, use = T / kKsRing;
+        const int ord = cur.sbase + lt;  // this unit's ordinal among all split units
+        const int slot = ord % kKsRing, use = ord / kKsRing;
         float *dst = ks_ring + (size_t)slot * kKsSlotFloats + (size_t)rank * BM * 128 + (size_t)q * 32 * 128;
         if (use > 0) {  // the slot's previous unit (tile T - kKsRing) has been read by its partner
           if (lane == 0) ptx::wait_counter(ks_cons + slot, use * 2 * BW_EPI);
@@ -1608,7 +1615,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BW_THREADS, 1)
         __syncwarp();
         if (lane == 0) atomicAdd(ks_wr + slot, 1);
         // the partner unit's partial sums of this unit's slabs
-        const int Tp = kh == 0 ? T + 1 : T - 1;
+        const int Tp = kh == 0 ? ord + 1 : ord - 1;  // the partner's ordinal
         pslot = Tp % kKsRing;
         if (lane == 0) ptx::wait_counter(ks_wr + pslot, (Tp / kKsRing + 1) * 2 * BW_EPI);
         __syncwarp();
@@ -2072,7 +2079,7 @@ __global__ void __launch_bounds__(NB_THREADS, 1)
 // zeroed before.
 __global__ void k_bwd_prelude(const int32_t *__restrict__ lo, int D, int nl, int n_cells,
                               const int32_t *__restrict__ cons_off, int32_t *__restrict__ tstart, int *rt_cnt,
-                              int slabs) {
+                              int slabs, const int32_t *__restrict__ gather, int *lvl_flags) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n_cells; c += stride) {
     const int r = (int)c + nl;
@@ -2082,7 +2089,103 @@ __global__ void k_bwd_prelude(const int32_t *__restrict__ lo, int D, int nl, int
     const int ts = (r0 - nl) + ((r - r0) / PM) * PM;
     tstart[c] = ts;
     if (__ldg(cons_off + r + 1) == __ldg(cons_off + r)) atomicAdd(rt_cnt + ts, slabs);
+    if (lvl_flags) {  // bit k: some cell of level a has a cell (not a leaf) in child slot k
+      const int bits = (__ldg(gather + 2 * (int64_t)r) >= nl ? 1 : 0) | (__ldg(gather + 2 * (int64_t)r + 1) >= nl ? 2 : 0);
+      if (bits && (__ldcg(lvl_flags + a) & bits) != bits) atomicOr(lvl_flags + a, bits);
+    }
   }
+}
+
+// Tile tables of k_bwd_levels (one block; levels in parallel, offsets by a block scan):
+// per level d = Dw..2 the CRITICAL units -- the
+// column tiles that touch a child slot holding a cell somewhere in the level (their epilogue
+// produces the next level's dZ) -- then, after all levels, the DEFERRED tiles: column tiles
+// that lie entirely in a slot whose children are all leaves in that level (chains: the
+// right child of every cell). A deferred tile only writes the leaves' dA for the embedding
+// gradient, so it leaves the dependent sweep; the critical tiles of a level that then fits
+// one wave of CTA pairs twice over run split-K (KS = 2). defer = 0: every tile critical.
+__global__ void __launch_bounds__(1024) k_bwd_tiles(const int32_t *__restrict__ lo, int D, int Dw, int Sp, int ld_u,
+                                                    int KB, int npairs, int ksplit_max, int ks256, int defer, int *tab) {
+  int4 *crit = reinterpret_cast<int4 *>(tab), *inl = crit + (D + 2), *endt = inl + (D + 2);
+  const int *flags = reinterpret_cast<const int *>(endt + (D + 2));
+  int *total = const_cast<int *>(flags) + (D + 2);
+  __shared__ int sc[1024], sc2[1024];
+  __shared__ int carry, carry2;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // column tiles [lo_t, lo_t + n) of width N touching (crit = true) / lying outside (false)
+  // the child slots set in mask (bit 0: columns [0, Sp), bit 1: [Sp, 2 Sp))
+  auto range = [&](int N, int mask, bool want_crit, int &lo_t, int &n) {
+    const int NT = (ld_u + N - 1) / N;
+    const int lc = (Sp + N - 1) / N, rc0 = Sp / N;  // tiles touching slot 0: [0, lc); slot 1: [rc0, NT)
+    int a = 0, b = 0;                               // critical range [a, b)
+    if ((mask & 3) == 3) { a = 0; b = NT; }
+    else if (mask & 1) { a = 0; b = lc; }
+    else if (mask & 2) { a = rc0; b = NT; }
+    if (want_crit) { lo_t = a; n = b - a; return; }
+    if (b == a) { lo_t = 0; n = NT; }               // nothing critical: all deferred
+    else if (a == 0) { lo_t = b; n = NT - b; }      // the tiles after the critical range
+    else { lo_t = 0; n = a; }                       // the tiles before it
+  };
+  const int nlev = Dw - 1;  // levels Dw, Dw - 1, ..., 2 (index i = Dw - d)
+  if (tid == 0) { carry = 0; carry2 = 0; }
+  __syncthreads();
+  for (int sec = 0; sec < 2; sec++) {  // 0: critical + inline deferred per level, 1: the end section
+    for (int base = 0; base < nlev; base += nt) {
+      const int i = base + tid, d = Dw - i;
+      int4 vc = make_int4(0, 0, 0, 0), vi = vc, ve = vc;
+      int cnt = 0, c = 0, cs = 0;  // cs: split units (the ring's ordinals)
+      if (i < nlev) {
+        const int M = __ldg(lo + d + 1) - __ldg(lo + d), rt = (M + PM - 1) / PM;
+        const int mask = defer ? flags[d] : 3;
+        int l128, n128, l256, n256;
+        range(128, mask, true, l128, n128);
+        range(256, mask, true, l256, n256);
+        int N = 256, KS = 1, lt0 = l256, n = n256;
+        if (ksplit_max > 0 && KB >= 8 && n128 > 0 && 2 * rt * n128 <= ksplit_max) { N = 128; KS = 2; lt0 = l128; n = n128; }
+        else if (ksplit_max > 0 && KB >= 8 && ks256 && n256 > 0 && 2 * rt * n256 <= ksplit_max) { KS = 2; }
+        else if (rt * n256 < npairs) { N = 128; lt0 = l128; n = n128; }
+        c = rt * n * KS;
+        cs = KS == 2 ? c : 0;
+        vc = make_int4(0, c, (N >> 7) | (KS << 2), lt0 | (n << 16));
+        // deferred tiles (256 columns): as many as fill the level's last round of CTA pairs
+        // run right after its critical units (pairs the level leaves idle), the rest at the end
+        int ld0, nd;
+        range(256, mask, false, ld0, nd);
+        if (mask == 3) nd = 0;
+        const int e = rt * nd, fill = (npairs - c % npairs) % npairs, ni = c > 0 ? min(e, fill) : 0;
+        vi = make_int4(0, ni, 2 | (1 << 2), ld0 | (nd << 16));
+        ve = make_int4(0, e - ni, 2 | (1 << 2) | (ni << 4), ld0 | (nd << 16));
+        cnt = sec == 0 ? c + ni : e - ni;
+      }
+      sc[tid] = cnt;  // inclusive scans over the chunk (Hillis-Steele)
+      sc2[tid] = cs;
+      __syncthreads();
+      for (int o = 1; o < nt; o <<= 1) {
+        const int add = tid >= o ? sc[tid - o] : 0, add2 = tid >= o ? sc2[tid - o] : 0;
+        __syncthreads();
+        sc[tid] += add;
+        sc2[tid] += add2;
+        __syncthreads();
+      }
+      if (i < nlev) {
+        const int off = carry + sc[tid] - cnt;
+        if (sec == 0) {
+          vc.x = off;
+          vc.z |= (carry2 + sc2[tid] - cs) << 4;
+          vi.x = off + c;
+          crit[d] = vc;
+          inl[d] = vi;
+        } else {
+          ve.x = off;
+          endt[d] = ve;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) { carry += sc[nt - 1]; carry2 += sc2[nt - 1]; }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) *total = carry;
 }
 
 // Forward row-tile bookkeeping: tstart[c] as for the backward; a tile's counter counts the
@@ -2709,10 +2812,12 @@ fold_status tc_bwd_prelude(const TcBwdArgs &a, const int32_t *cons_off, cudaStre
   if (a.n_cells <= 0) return FOLD_OK;
   FOLD_CUDA_TRY(cudaMemsetAsync(a.rt_cnt, 0, (size_t)a.n_cells * sizeof(int), st));
   if (a.ks_cnt) FOLD_CUDA_TRY(cudaMemsetAsync(a.ks_cnt, 0, (size_t)2 * kKsRing * sizeof(int), st));
+  int *lvl_flags = a.lvl_tab ? a.lvl_tab + 12 * (a.D + 2) : nullptr;
+  if (lvl_flags) FOLD_CUDA_TRY(cudaMemsetAsync(lvl_flags, 0, (size_t)(a.D + 2) * sizeof(int), st));
   int64_t blocks = cdiv(a.n_cells, 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
   k_bwd_prelude<<<(unsigned)blocks, 256, 0, st>>>(a.level_off, a.D, a.nl, a.n_cells, cons_off, a.tstart, a.rt_cnt,
-                                                  tc_bwd_slabs(a.S));
+                                                  tc_bwd_slabs(a.S), a.gather, lvl_flags);
   FOLD_LAUNCH_CHECK();
   return FOLD_OK;
 }
@@ -2816,16 +2921,22 @@ fold_status tc_bwd_levels(int cell, const TcBwdArgs &a, cudaStream_t st) {
   // 128-column tiles (A/B switches; C3 B=1024 dA 0.60 -> 0.50 ms, C4 12.1 -> 11.2-11.5 ms)
   static const int ksplit_on = [] { const char *e = getenv("FOLD_BWD_KSPLIT"); return e ? atoi(e) : 1; }();
   const int KB = (int)cdiv(gates * S, BK);
+  if (!a.lvl_tab) return FOLD_E_INVALID;
+  const int4 *tcrit = reinterpret_cast<const int4 *>(a.lvl_tab), *tinl = tcrit + (a.D + 2), *tend = tinl + (a.D + 2);
+  const int *ttotal = a.lvl_tab + 13 * (a.D + 2);
   BwdLevels L{a.level_off, d1 - 1, S, a.nl, ld_u, npairs_max, l2_prefetch_dist("FOLD_PF_BWD"),
-              (ksplit_on && a.ks_ring && a.ks_cnt && npairs_max >= 2) ? npairs_max : 0, KB, ksplit_on != 2};
+              (ksplit_on && a.ks_ring && a.ks_cnt && npairs_max >= 2) ? npairs_max : 0, KB, ksplit_on != 2,
+              tcrit, tinl, tend, ttotal};
+  // an upper bound of the units (128-column tiles, all split): the tables are built on the
+  // device from the levels' child slots; the kernel reads the exact count
   int64_t total = 0;
-  for (int d = 2; d < d1; d++) {
-    const int M = a.level_off_host[d + 1] - a.level_off_host[d];
-    const BwdCfg c = bwd_level_cfg(L, M);
-    total += cdiv(M, PM) * cdiv(ld_u, c.N) * c.KS;
-  }
+  for (int d = 2; d < d1; d++) total += cdiv(a.level_off_host[d + 1] - a.level_off_host[d], PM) * cdiv(ld_u, 128) * 2;
   if (total <= 0) return FOLD_OK;
   if (total > INT32_MAX) return FOLD_E_INVALID;
+  static const int defer = [] { const char *e = getenv("FOLD_BWD_DEFER"); return e ? atoi(e) : 1; }();
+  k_bwd_tiles<<<1, 1024, 0, st>>>(a.level_off, a.D, d1 - 1, (int)round_up(S, BK), ld_u, KB, npairs_max, L.ksplit_max,
+                                L.ks256, defer, a.lvl_tab);
+  FOLD_LAUNCH_CHECK();
   const int npairs = total < npairs_max ? (int)total : npairs_max;
   kern<<<2 * npairs, BW_THREADS, BW_SMEM, st>>>(tmZ, tmZ16, tmZ64, tmU, L, KB, (int)total, a.gather,
                                                a.Gact, a.ld_g, a.C, a.ld, a.dA, a.dCe, a.dZ, a.ld_z, a.rt_cnt,

@@ -35,21 +35,53 @@ ld_u = 2 * math.ceil(S / 64) * 64
 d = D
 while d >= 2 and lo[d + 1] - lo[d] <= a.narrow_max:
     d -= 1
-tiles = []
 KB = math.ceil(5 * S / 64)
 ks_on = os.environ.get("FOLD_BWD_KSPLIT", "1") != "0"
 ks256 = os.environ.get("FOLD_BWD_KSPLIT", "1") != "2"
+defer = os.environ.get("FOLD_BWD_DEFER", "1") != "0"
+Sp = math.ceil(S / 64) * 64
+sn = s.to_numpy()
+gat = np.asarray(sn["gather"]).reshape(-1, 2)
+nl = s.n_leaves
+
+
+def mask_of(dd):  # bit k: some cell of level dd has a cell child in slot k (k_bwd_prelude)
+    g = gat[lo[dd]:lo[dd + 1]]
+    return int((g[:, 0] >= nl).any()) | (int((g[:, 1] >= nl).any()) << 1) if defer else 3
+
+
+def rng(N, mask, crit):  # k_bwd_tiles' column-tile ranges
+    NT = math.ceil(ld_u / N)
+    lc, rc0 = math.ceil(Sp / N), Sp // N
+    a_, b_ = (0, NT) if mask & 3 == 3 else (0, lc) if mask & 1 else (rc0, NT) if mask & 2 else (0, 0)
+    if crit:
+        return b_ - a_
+    return NT if b_ == a_ else (NT - b_ if a_ == 0 else a_)
+
+
+tiles = []   # (level, M, N*10+KS, units) in unit order: per level its critical units (level),
+end = []     # its inline deferred tiles (1000 + level); then the end section (-level)
 for dd in range(d, 1, -1):
     M = lo[dd + 1] - lo[dd]
     mt = math.ceil(M / 256)
-    t256, t128 = mt * math.ceil(ld_u / 256), mt * math.ceil(ld_u / 128)
-    if ks_on and KB >= 8 and 2 * t128 <= npairs:
-        N, KS = 128, 2
-    elif ks_on and ks256 and KB >= 8 and 2 * t256 <= npairs:
-        N, KS = 256, 2
+    mk = mask_of(dd)
+    n128, n256 = rng(128, mk, True), rng(256, mk, True)
+    if ks_on and KB >= 8 and n128 > 0 and 2 * mt * n128 <= npairs:
+        N, KS, n = 128, 2, n128
+    elif ks_on and ks256 and KB >= 8 and n256 > 0 and 2 * mt * n256 <= npairs:
+        N, KS, n = 256, 2, n256
+    elif mt * n256 < npairs:
+        N, KS, n = 128, 1, n128
     else:
-        N, KS = (128 if t256 < npairs else 256), 1
-    tiles.append((dd, M, N * 10 + KS, mt * math.ceil(ld_u / N) * KS))
+        N, KS, n = 256, 1, n256
+    c = mt * n * KS
+    e = 0 if mk == 3 else mt * rng(256, mk, False)
+    ni = min(e, (npairs - c % npairs) % npairs) if c > 0 else 0
+    tiles.append((dd, M, N * 10 + KS, c))
+    tiles.append((1000 + dd, M, 2561, ni))
+    end.append((-dd, M, 2561, e - ni))
+tiles += end
+tiles = [t_ for t_ in tiles if t_[3] > 0]
 ntot = min(got, sum(x[3] for x in tiles))
 t = buf[:, :ntot].astype(np.int64)
 t0 = t[0][t[0] > 0].min()
