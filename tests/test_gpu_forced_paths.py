@@ -42,14 +42,29 @@ gr = foldgen.table1_batch(6, True, leaves=30, vocab=64)
 check(gr, 512, "treelstm", foldgen.manual_levels(gr))
 gr = foldgen.config_c4(5, leaves=40)
 check(gr, 1024, "treelstm")
+# chains at S where the child slots' column halves do not align with the column tiles
+# (deferred leaf-child tiles of the wide backward, k_bwd_tiles), and mirrored chains (the
+# LEFT child is the leaf: the left half's tiles are deferred)
+check(foldgen.config_c4(5, leaves=40), 300, "treelstm")
+check(foldgen.config_c4(3, leaves=24), 130, "treelstm")
+gm = foldgen.config_c4(4, leaves=30)
+ch = gm.child.copy()
+cells = gm.op == 1
+ch[cells] = ch[cells][:, ::-1]
+import dataclasses
+gm = dataclasses.replace(gm, child=ch)
+check(gm, 1024, "treelstm")
+check(gm, 300, "treelstm")
 print("ok")
 """ % ROOT
 
 
-@pytest.mark.parametrize("mode", ["all_narrow", "no_narrow"])
+@pytest.mark.parametrize("mode", ["all_narrow", "no_narrow", "no_narrow_nodefer"])
 def test_forced_narrow_modes(mode):
     env = dict(os.environ)
     big = "100000000" if mode == "all_narrow" else "0"
     env.update(FOLD_FWD_NARROW_MAX=big, FOLD_BWD_NARROW_MAX=big)
+    if mode == "no_narrow_nodefer":  # every backward tile in the dependent sweep
+        env.update(FOLD_BWD_DEFER="0")
     r = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-4000:]
