@@ -434,16 +434,21 @@ def run_fold(args):
         d2h = h_out.numel() * 4
 
         graph_copies = ((d_op, h_op), (d_child, h_child), (d_tok, h_tok), (d_root, h_root))
-        # pipelined: the root states go D2H on a copy stream from the other of two root buffers,
-        # so the copy does not sit between two steps' kernels on the compute stream (it still
-        # runs every step inside the timed region, which ends after the last one). Measured
-        # against the D2H on the compute stream: e2e - device gap 0.35-0.44 -> 0.09-0.16 ms at
-        # C2; also moving the gradient H2D to the side stream measured no better (it queues
-        # behind the next schedule there)
+        # pipelined: the root states go D2H on a copy stream from the other of two root buffers
+        # and the next step's upstream gradient H2D on another, so neither copy sits between two
+        # steps' kernels on the compute stream (both still run every step inside the timed
+        # region, which ends after the last of them). On the pipeline's side stream the gradient
+        # copy measured no better (it queues behind the next schedule there)
         hbufs = [torch.empty((gr.n_graphs, S), dtype=torch.float32, device=dev) for _ in range(2)]
         out_done = [torch.cuda.Event(), torch.cuda.Event()]
         out_used = [False, False]
         copy_stream = torch.cuda.Stream(device=dev)
+        # the upstream gradient: the next step's H2D on its own stream into the other of two
+        # device buffers, once the step before has finished reading it
+        h2d_stream = torch.cuda.Stream(device=dev)
+        d_gs = [d_g, torch.empty_like(d_g)]
+        g_ready = [torch.cuda.Event(), torch.cuda.Event()]
+        g_free = [torch.cuda.Event(), torch.cuda.Event()]
         ke = [0]
 
         def e2e_step(sp):
@@ -451,17 +456,23 @@ def run_fold(args):
             # arrays H2D + schedule on the side stream (pipelined); the result D2H on the copy
             # stream (pipelined) or the compute stream (--pipeline off)
             main = torch.cuda.current_stream()
-            d_g.copy_(h_g, non_blocking=True)
             if side is None:
+                d_g.copy_(h_g, non_blocking=True)
                 hr = run_step(*sp, d_g)
                 nxt = schedule_async(d_op, d_child, d_tok, d_root, copies=graph_copies, after=gate[0])
                 h_out.copy_(hr, non_blocking=True)
                 return nxt
             j = ke[0] % 2
             ke[0] += 1
+            main.wait_event(g_ready[j])
             if out_used[j]:
                 main.wait_event(out_done[j])
-            hr = run_step(*sp, d_g, hbuf=hbufs[j])
+            hr = run_step(*sp, d_gs[j], hbuf=hbufs[j])
+            g_free[j].record(main)
+            with torch.cuda.stream(h2d_stream):  # the next step's gradient
+                h2d_stream.wait_event(g_free[1 - j])
+                d_gs[1 - j].copy_(h_g, non_blocking=True)
+                g_ready[1 - j].record(h2d_stream)
             done = torch.cuda.Event()
             done.record(main)
             nxt = schedule_async(d_op, d_child, d_tok, d_root, copies=graph_copies, after=gate[0])
@@ -474,6 +485,10 @@ def run_fold(args):
 
         use_pipeline(N_nodes, n_levels)
         sp = schedule_async(d_op, d_child, d_tok, d_root, copies=graph_copies)
+        for j in range(2):  # both gradient buffers filled once; each step refills the other
+            d_gs[j].copy_(h_g, non_blocking=True)
+            g_ready[j].record(torch.cuda.current_stream())
+            g_free[j].record(torch.cuda.current_stream())
         for _ in range(max(args.warmup, 3)):
             sp = e2e_step(sp)
         torch.cuda.synchronize()
@@ -487,6 +502,7 @@ def run_fold(args):
         if sp[1] is not None:
             torch.cuda.current_stream().wait_event(sp[1])
         torch.cuda.current_stream().wait_stream(copy_stream)  # the last root-state D2H
+        torch.cuda.current_stream().wait_stream(h2d_stream)   # and the last gradient H2D
         a1.record()
         torch.cuda.synchronize()
         t2 = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)
