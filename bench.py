@@ -607,7 +607,10 @@ def run_fold(args):
         "us_per_level": {  # the latency-bound view (n_levels - 1 cell levels)
             "fwd": 1e3 * sum(per_class.get(k, {}).get("ms_per_step", 0.0) for k in ("cell_fwd",)) / max(n_levels - 1, 1),
             "bwd": 1e3 * sum(per_class.get(k, {}).get("ms_per_step", 0.0) for k in ("gemm_dA", "bwd_pointwise"))
-                   / max(n_levels - 1, 1)},
+                   / max(n_levels - 1, 1),
+            # one cross-SM dependency hop with the executor's publication pattern, measured
+            # (tools/micro/hop_latency.cu, profiles/r01/hop_latency.json)
+            "hop_floor_us": 0.40},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
