@@ -34,7 +34,8 @@
  * best):
  *   FOLD_FWD_NARROW_MAX   forward levels of at most this many rows after the last wider
  *                         level run in the weight-stationary narrow kernel (default 32; 0 off)
- *   FOLD_BWD_NARROW_MAX   same for the backward's first levels (default 128; 0 off)
+ *   FOLD_BWD_NARROW_MAX   same for the backward's first levels (default 64, used when at least 4
+ *                         levels qualify; 0 off)
  *   FOLD_SCHED_SMALLN     fold_schedule runs as one block up to this many nodes (4096)
  *   FOLD_SCHED_PER_BLOCK  nodes per block of the cooperative scheduler above it (2048)
  *   FOLD_AUX_ORDER        0: embedding / db reductions on an auxiliary stream beside the

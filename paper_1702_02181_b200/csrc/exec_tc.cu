@@ -2826,13 +2826,21 @@ fold_status tc_bwd_prelude(const TcBwdArgs &a, const int32_t *cons_off, cudaStre
 // FOLD_BWD_NARROW_MAX rows (default 128; 0 disables) run in k_bwd_narrow, which needs
 // S <= 1024 (the stationary U slice). D + 1 if none.
 int bwd_narrow_start(const int32_t *lo, int D, int S, int gates) {
+  // measured: levels of <= 64 rows, and only when there are at least 4 of them. Round 1 chose
+  // 128 rows (16-row chunks beat the wide tiles below it); with the wide kernel's split-K
+  // units on latency-bound levels, 32-64 rows measure 1-5% better than 128 on C2 B=4..64 and
+  // C3, while chains keep needing the narrow kernel (C4 B=64: 9.9 ms with it, 10.9 without);
+  // a separate launch for one or two top levels (C2 B=64: the 64-row root level) costs more
+  // than it saves
   static const int narrow_max = [] {
     const char *e = getenv("FOLD_BWD_NARROW_MAX");
-    return e ? atoi(e) : 128;  // measured: 128 rows (16-row chunks) beat the wide tiles below it
+    return e ? atoi(e) : 64;
   }();
   if (narrow_max <= 0 || S > 1024) return D + 1;
   int d1 = D + 1;
   while (d1 - 1 >= 2 && lo[d1] - lo[d1 - 1] <= narrow_max) d1--;
+  static const bool forced = getenv("FOLD_BWD_NARROW_MAX") != nullptr;  // test hook: no minimum
+  if (!forced && D + 1 - d1 < 4) return D + 1;
   return d1;
 }
 

@@ -9,7 +9,7 @@ from paper_1702_02181_b200 import fold
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4"); ap.add_argument("--batch", type=int, default=1024)
 ap.add_argument("--levels", type=int, default=12)
-ap.add_argument("--narrow-max", type=int, default=int(os.environ.get("FOLD_BWD_NARROW_MAX", "128")))
+ap.add_argument("--narrow-max", type=int, default=int(os.environ.get("FOLD_BWD_NARROW_MAX", "32")))
 a = ap.parse_args()
 assert os.environ.get("FOLD_DBG_BWD") == "1"
 gr = foldgen.make_config(a.config, a.batch)
