@@ -317,7 +317,9 @@ int32_t fold_last_error_detail(void);
  * up to CTA pairs; default 0) for work on other streams: the next batch's fold_schedule,
  * launched beside a small batch's latency-bound levels, then runs on those SMs instead of
  * waiting for the level kernels to finish. Process-wide, read at each launch;
- * returns the previous value; n < 0 acts as 0. Results do not depend on it. */
+ * returns the previous value; n < 0 acts as 0. Results stay deterministic for a given value;
+ * across values they can differ in the last bits, because the backward's split-K choice for
+ * latency-bound levels depends on the number of CTA pairs. */
 int32_t fold_set_reserved_sms(int32_t n);
 
 /* (node, depth, op) context of the last data-dependent fold_schedule error on this thread

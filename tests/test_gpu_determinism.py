@@ -36,3 +36,39 @@ def test_repeated_steps_bitwise(config, B, reps):
             assert torch.equal(x, y), f"{config} B={B}: {name} differs in repetition {r}"
     del acts, ws, s
     torch.cuda.empty_cache()
+
+
+def test_reserved_sms_results():
+    """fold_set_reserved_sms changes only how many CTA pairs the level kernels use: results are
+    bitwise repeatable for a given reservation, and across reservations agree within the BF16
+    path's tolerance (the split-K choice of latency-bound levels depends on the pair count, and
+    a different fp32 sum order can flip bf16 roundings of dZ downstream)."""
+    import numpy as np
+    import torch
+    import foldgen
+    from paper_1702_02181_b200 import fold
+    gr = foldgen.make_config("c3", 64)
+    S = 300
+    p = foldgen.make_params("treelstm", S, gr.vocab)
+    m = fold.Model(torch.tensor(p.U, device="cuda"), torch.tensor(p.b, device="cuda"),
+                   torch.tensor(p.E, device="cuda"))
+    op, child, token, root = fold.graphs_to_device(gr)
+    s = fold.schedule(op, child, token, root, gr.vocab)
+    g = torch.tensor(foldgen.make_upstream(gr.n_graphs, S), device="cuda")
+
+    def run():
+        h, c, acts = fold.forward(s, m)
+        return [h] + list(fold.backward(s, m, acts, g))
+
+    old = fold.set_reserved_sms(0)
+    try:
+        a = run()
+        fold.set_reserved_sms(24)
+        b, b2 = run(), run()
+    finally:
+        fold.set_reserved_sms(old)
+    torch.cuda.synchronize()
+    for x, y, y2 in zip(a, b, b2):
+        assert torch.equal(y, y2)
+        err = float((x - y).abs().max()) / max(float(x.abs().max()), 1e-30)
+        assert err <= 1e-2, err
